@@ -1,0 +1,544 @@
+"""Pins of the CPU oracle against things other than itself.
+
+Each test names the pin id (P1..P35) and what fixes it: a closed form, an
+extended-precision (mpmath, 40 digits) recomputation, a textbook quadrature
+fact, an invariant of the mathematics, or brute force on tiny inputs.
+"""
+import itertools
+import json
+import math
+import os
+from fractions import Fraction
+
+import mpmath as mp
+import numpy as np
+import pytest
+
+import synth
+from oracle import entries, geometry, greens, maxvol, ttcross, ttmv, ttsvd, validate
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+K0 = 2 * np.pi * synth.configs.FREQ_7T / synth.configs.C0
+
+
+# ---------------------------------------------------------------- Green's function
+
+def test_P5_g_closed_forms():
+    # k0 = 0 static limit, phase wrap at k0 R = 2 pi, k0 = 1, R = 2
+    assert abs(greens.g_scalar(0.7, 0.0) - 1 / (4 * np.pi * 0.7)) < 1e-15
+    R = 2 * np.pi / K0
+    assert abs(greens.g_scalar(R, K0) - 1 / (4 * np.pi * R)) < 1e-15 / R
+    ref = (np.cos(2.0) - 1j * np.sin(2.0)) / (8 * np.pi)
+    assert abs(greens.g_scalar(2.0, 1.0) - ref) < 1e-16
+
+
+def _mp_dyad(Rv, k0, dps=40):
+    """(I + grad grad / k0^2) g by mpmath numerical differentiation at 40 digits."""
+    with mp.workdps(dps):
+        k = mp.mpf(k0)
+        def g(x, y, z):
+            R = mp.sqrt(x * x + y * y + z * z)
+            return mp.exp(-1j * k * R) / (4 * mp.pi * R)
+        X = [mp.mpf(float(c)) for c in Rv]
+        D = np.empty((3, 3), dtype=complex)
+        g0 = g(*X)
+        for i in range(3):
+            for j in range(3):
+                order = [0, 0, 0]
+                order[i] += 1
+                order[j] += 1
+                d2 = mp.diff(g, X, tuple(order))
+                D[i, j] = complex((1 if i == j else 0) * g0 + d2 / (k * k))
+        return D
+
+
+def test_P2_dyad_closed_form_vs_mpmath_derivatives():
+    rng = np.random.default_rng(2)
+    for _ in range(4):
+        Rv = rng.normal(size=3)
+        Rv *= rng.uniform(0.1, 3.0) / np.linalg.norm(Rv)
+        ref = _mp_dyad(Rv, K0)
+        got = greens.dyad(Rv, K0)
+        assert np.max(np.abs(got - ref)) <= 1e-14 * np.max(np.abs(ref))
+        # dyad_apply is the same operator applied to a real vector
+        J = rng.normal(size=3)
+        assert np.max(np.abs(greens.dyad_apply(Rv, J, K0) - ref @ J)) <= 1e-14 * np.max(np.abs(ref @ J))
+
+
+def test_P1_trace_identity():
+    # Helmholtz: lap g = -k0^2 g  =>  tr G = 3 g + lap g / k0^2 = 2 g
+    rng = np.random.default_rng(1)
+    Rv = rng.normal(size=(200, 3)) * rng.uniform(0.05, 5.0, size=(200, 1))
+    D = greens.dyad(Rv, K0)
+    tr = np.trace(D, axis1=-2, axis2=-1)
+    g = greens.g_scalar(np.linalg.norm(Rv, axis=1), K0)
+    assert np.max(np.abs(tr / g - 2.0)) < 1e-14
+
+
+def test_P3_symmetry_and_parity():
+    rng = np.random.default_rng(3)
+    Rv = rng.normal(size=(50, 3))
+    D = greens.dyad(Rv, K0)
+    assert np.max(np.abs(D - np.swapaxes(D, -1, -2))) <= 1e-15 * np.max(np.abs(D))
+    assert np.max(np.abs(D - greens.dyad(-Rv, K0))) <= 1e-15 * np.max(np.abs(D))
+
+
+def test_P4_far_field_transversality():
+    rh = np.array([0.3, -0.5, 0.8]); rh /= np.linalg.norm(rh)
+    devs = []
+    for R in (2.0, 5.0, 20.0, 50.0):
+        D = greens.dyad(R * rh, K0)
+        g = greens.g_scalar(R, K0)
+        far = g * (np.eye(3) - np.outer(rh, rh))
+        devs.append(np.max(np.abs(D - far)) / abs(g))
+    assert all(a > b for a, b in zip(devs, devs[1:]))
+    assert devs[-1] < 1e-2
+
+
+# ---------------------------------------------------------------- quadrature
+
+def test_P6_gauss2_exact_to_cubics():
+    h = (0.3, 0.5, 0.7)
+    offs, w = geometry.gauss_legendre_offsets(h, 2)
+    for p in itertools.product(range(5), repeat=3):
+        if max(p) > 4:
+            continue
+        num = np.sum(w * np.prod(offs ** np.array(p), axis=1))
+        exact = 1.0
+        for a in range(3):
+            k = p[a]
+            exact *= 0.0 if k % 2 else 2 * (h[a] / 2) ** (k + 1) / (k + 1)
+        if max(p) <= 3:
+            assert abs(num - exact) < 1e-15 * max(1.0, abs(exact)) + 1e-18
+        elif p.count(4) == 1 and sum(p) == 4:
+            assert abs(num - exact) > 1e-6 * abs(exact)   # quartics are NOT exact
+
+
+def test_P7_triangle_rule_exact_to_quadratics():
+    v = np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 1.0]])   # reference triangle, area 1/2
+    pts = geometry.TRI_BARY @ v
+    for a in range(4):
+        for b in range(4 - a):
+            num = 0.5 / 3 * np.sum(pts[:, 0] ** a * pts[:, 1] ** b)
+            exact = math.factorial(a) * math.factorial(b) / math.factorial(a + b + 2)
+            if a + b <= 2:
+                assert abs(num - exact) < 1e-15
+            elif a + b == 3 and (a == 3 or b == 3):
+                assert abs(num - exact) > 1e-4
+
+
+def test_P8_weights():
+    h = (5e-3, 4e-3, 3e-3)
+    _, w = geometry.gauss_legendre_offsets(h, 2)
+    assert abs(w.sum() - np.prod(h)) < 1e-15 * np.prod(h)
+    assert np.allclose(w, np.prod(h) / 8, rtol=0, atol=1e-22)
+    assert abs(geometry.TRI_BARY.sum(axis=1) - 1).max() < 1e-15
+
+
+# ---------------------------------------------------------------- mesh / RWG
+
+def test_P11_mesh_counts():
+    for N_az, N_ax in ((24, 16), (72, 47), (88, 57), (80, 63), (100, 67), (90, 74)):
+        xyz, tri = synth.cylinder_mesh(0.34, 1.2, N_az, N_ax)
+        assert len(tri) == 2 * N_az * N_ax
+        edges = {tuple(sorted((t[i], t[(i + 1) % 3]))) for t in tri for i in range(3)}
+        assert len(edges) == N_az * (3 * N_ax + 1)
+        if N_az == 24:
+            r = geometry.rwg_edges(xyz, tri)
+            assert len(r["a"]) == N_az * (3 * N_ax - 1) == 1128
+    assert synth.get_config(3).m == 30000 and synth.get_config(4).m == 39890
+
+
+def test_P9_P10_rwg_moments(prob1, cfg1):
+    xyz, tri = cfg1.meshes()[0]
+    rwg = geometry.rwg_edges(xyz, tri)
+    rs, js = prob1.rs, prob1.js
+    for n in range(0, len(rwg["a"]), 37):
+        a, b = xyz[rwg["a"][n]], xyz[rwg["b"][n]]
+        l = np.linalg.norm(a - b)
+        pp, pm = xyz[rwg["pp"][n]], xyz[rwg["pm"][n]]
+        cp = xyz[tri[rwg["tp"][n]]].mean(0)
+        cm = xyz[tri[rwg["tm"][n]]].mean(0)
+        # P10: sum_s J_s = (l/2)[(c+ - p+) + (p- - c-)]
+        ref = 0.5 * l * ((cp - pp) + (pm - cm))
+        assert np.max(np.abs(js[n].sum(0) - ref)) < 1e-14 * np.linalg.norm(ref)
+        # P9: recover f_n = J_q / (A/3) at the nodes; f is linear, so extrapolate to
+        # the edge midpoint and check the normal component is 1 from both sides.
+        for side, (T, p, sgn) in enumerate(((rwg["tp"][n], pp, 1), (rwg["tm"][n], pm, -1))):
+            V = xyz[tri[T]]
+            A = 0.5 * np.linalg.norm(np.cross(V[1] - V[0], V[2] - V[0]))
+            J = js[n, 3 * side:3 * side + 3]
+            r = rs[n, 3 * side:3 * side + 3]
+            coef = (J / (A / 3.0)) / (sgn * (r - p))               # = l/(2A) per component
+            c = coef[np.abs(sgn * (r - p)) > 1e-9 * l]
+            assert np.max(np.abs(c - l / (2 * A))) < 1e-12 * l / (2 * A)
+            mid = 0.5 * (a + b)
+            normal = np.cross(np.cross(V[1] - V[0], V[2] - V[0]), b - a)
+            normal /= np.linalg.norm(normal)
+            if np.dot(normal, mid - p) < 0:
+                normal = -normal          # points away from p, i.e. T+ -> T- on T+
+            f = sgn * l / (2 * A) * (mid - p)
+            assert abs(abs(np.dot(f, normal)) - 1.0) < 1e-12
+
+
+# ---------------------------------------------------------------- entries
+
+def _mp_entry(cfg, rwg_idx, chi, vox):
+    """P12: one entry at 40 digits, from the definitions (f_n = l/(2A)(r - p) with the
+    area-weighted 3-point rule; dyad by mpmath differentiation of g)."""
+    xyz, tri = cfg.meshes()[0]
+    rwg = geometry.rwg_edges(xyz, tri)
+    a, b = rwg["a"][rwg_idx], rwg["b"][rwg_idx]
+    adj = [t for t in range(len(tri)) if a in tri[t] and b in tri[t]]
+    assert len(adj) == 2
+    tp, tm = sorted(adj)
+    mp.mp.dps = 40
+    P = lambda v: [mp.mpf(float(c)) for c in v]
+    va, vb = P(xyz[a]), P(xyz[b])
+    l = mp.sqrt(sum((va[i] - vb[i]) ** 2 for i in range(3)))
+    i1, i2, i3 = vox
+    c = [mp.mpf(float(cfg.origin[0])) + i1 * mp.mpf(float(cfg.h[0])),
+         mp.mpf(float(cfg.origin[1])) + i2 * mp.mpf(float(cfg.h[1])),
+         mp.mpf(float(cfg.origin[2])) + i3 * mp.mpf(float(cfg.h[2]))]
+    hh = [mp.mpf(float(x)) for x in cfg.h]
+    k0 = 2 * mp.pi * mp.mpf(synth.configs.FREQ_7T) / mp.mpf(synth.configs.C0)
+    total = mp.mpc(0)
+    for sgn, T in ((1, tp), (-1, tm)):
+        V = [P(xyz[v]) for v in tri[T]]
+        p = [P(xyz[v]) for v in tri[T] if v not in (a, b)][0]
+        e1 = [V[1][i] - V[0][i] for i in range(3)]
+        e2 = [V[2][i] - V[0][i] for i in range(3)]
+        cr = [e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]]
+        A = mp.sqrt(sum(x * x for x in cr)) / 2
+        for q in range(3):
+            bary = [mp.mpf(1) / 6] * 3
+            bary[q] = mp.mpf(2) / 3
+            rq = [sum(bary[j] * V[j][i] for j in range(3)) for i in range(3)]
+            f = [sgn * l / (2 * A) * (rq[i] - p[i]) for i in range(3)]
+            for sig in itertools.product((-1, 1), repeat=3):
+                rp = [c[i] + sig[i] * hh[i] / (2 * mp.sqrt(3)) for i in range(3)]
+                w = hh[0] * hh[1] * hh[2] / 8
+                R = [rp[i] - rq[i] for i in range(3)]
+                def g(x, y, z):
+                    rr = mp.sqrt(x * x + y * y + z * z)
+                    return mp.exp(-1j * k0 * rr) / (4 * mp.pi * rr)
+                row = []
+                for j in range(3):
+                    order = [0, 0, 0]
+                    order[chi] += 1
+                    order[j] += 1
+                    row.append((g(*R) if j == chi else 0) + mp.diff(g, R, tuple(order)) / k0 ** 2)
+                total += w * (A / 3) * sum(row[j] * f[j] for j in range(3))
+    return complex(total)
+
+
+@pytest.mark.slow
+def test_P12_entry_extended_precision(prob1, cfg1):
+    for (n, chi, vox) in ((5, 0, (0, 3, 11)), (700, 2, (6, 6, 6))):
+        ref = _mp_entry(cfg1, n, chi, vox)
+        v = vox[0] + cfg1.n[0] * (vox[1] + cfg1.n[1] * vox[2])
+        got = entries.entries(prob1, [chi * cfg1.n_v + v], [n])[0]
+        assert abs(got - ref) <= 1e-14 * abs(ref), (got, ref)
+
+
+def test_P13_reciprocity(prob1, cfg1):
+    """Swapped roles: sum_s sum_p J_s . G(r_s - r_p) e_chi w_p equals the entry."""
+    rng = np.random.default_rng(13)
+    rows = rng.integers(0, 3 * cfg1.n_v, 30)
+    cols = rng.integers(0, prob1.m, 30)
+    got = entries.entries(prob1, rows, cols)
+    for t in range(30):
+        chi, v = divmod(int(rows[t]), cfg1.n_v)
+        i1, i2, i3 = geometry.voxel_index(v, cfg1.n)
+        c = np.array(cfg1.origin) + np.array([i1, i2, i3]) * np.array(cfg1.h)
+        acc = 0j
+        for p in range(8):
+            rp = c + prob1.offs[p]
+            for s in range(6):
+                D = greens.dyad(prob1.rs[cols[t], s] - rp, prob1.k0)   # G(r_s - r_p)
+                acc += prob1.wts[p] * (prob1.js[cols[t], s] @ D)[chi]
+        assert abs(acc - got[t]) <= 1e-13 * abs(got[t])
+
+
+def _subdivided_rule(L):
+    """3-point interior rule on the 4^L midpoint sub-triangles, as barycentrics."""
+    tris = [np.eye(3)]
+    for _ in range(L):
+        nxt = []
+        for T in tris:
+            m01, m12, m20 = (T[0] + T[1]) / 2, (T[1] + T[2]) / 2, (T[2] + T[0]) / 2
+            nxt += [np.array([T[0], m01, m20]), np.array([m01, T[1], m12]),
+                    np.array([m20, m12, T[2]]), np.array([m01, m12, m20])]
+        tris = nxt
+    return np.concatenate([geometry.TRI_BARY @ T for T in tris])
+
+
+def test_P14_quadrature_convergence(cfg1):
+    """Refining either rule converges monotonically; the 2x2x2 / 3-point error is reported."""
+    meshes = cfg1.meshes()
+    row, col = [0 * cfg1.n_v + 5 + 12 * 7], [400]
+    seq_v = []
+    for ng in (2, 3, 4, 5):
+        p = entries.make_problem(cfg1.n, cfg1.h, cfg1.origin, meshes, cfg1.freq, ng=ng, bary=_subdivided_rule(2))
+        seq_v.append(entries.entries(p, row, col)[0])
+    seq_t = []
+    for L in (0, 1, 2, 3):
+        p = entries.make_problem(cfg1.n, cfg1.h, cfg1.origin, meshes, cfg1.freq, ng=4, bary=_subdivided_rule(L))
+        seq_t.append(entries.entries(p, row, col)[0])
+    dv = [abs(a - b) for a, b in zip(seq_v, seq_v[1:])]
+    dt = [abs(a - b) for a, b in zip(seq_t, seq_t[1:])]
+    assert all(x > y for x, y in zip(dt, dt[1:])), dt
+    assert dv[0] > dv[-1], dv
+    assert dt[-1] < 1e-3 * abs(seq_t[-1])
+
+
+def test_P15_point_dipole_limit():
+    """Far away (quasi-static k0 D << 1, where the multipole remainder is O(size/D)),
+    an RWG acts like a point dipole of moment sum_s J_s."""
+    xyz = np.array([[0, -0.01, 0], [0, 0.01, 0], [0.015, 0, 0.002], [-0.012, 0.001, 0]], dtype=float)
+    tri = np.array([[0, 1, 2], [1, 0, 3]], dtype=np.int32)
+    errs = []
+    for D in (0.5, 1.0, 2.0, 4.0):
+        shifted = xyz + np.array([D, 0.3 * D, 0.1])
+        p = entries.make_problem((1, 1, 1), (4e-3,) * 3, (0.0, 0.0, 0.0), [(shifted, tri)], 1.0e6)
+        E = entries.field_vectors(p, [0], [0])[0]
+        cen = p.rs[0].mean(0)
+        dip = (4e-3) ** 3 * greens.dyad_apply(-cen, p.js[0].sum(0), p.k0)
+        errs.append(np.max(np.abs(E - dip)) / np.max(np.abs(dip)))
+    assert all(a > b for a, b in zip(errs, errs[1:])), errs
+    assert errs[-1] < 5e-3
+
+
+def test_P16_c2_rotation_symmetry(dense1, cfg1):
+    xyz, tri = cfg1.meshes()[0]
+    N_az = cfg1.surfaces[0].n_az
+    rwg = geometry.rwg_edges(xyz, tri)
+    def vmap(v):
+        k, j = divmod(int(v), N_az)
+        return k * N_az + (j + N_az // 2) % N_az
+    def tmap(t):
+        q, s = divmod(int(t), 2)
+        k, j = divmod(q, N_az)
+        return 2 * (k * N_az + (j + N_az // 2) % N_az) + s
+    lookup = {(int(a), int(b)): n for n, (a, b) in enumerate(zip(rwg["a"], rwg["b"]))}
+    nmap, sig = [], []
+    for n in range(len(rwg["a"])):
+        a, b = vmap(rwg["a"][n]), vmap(rwg["b"][n])
+        n2 = lookup[(min(a, b), max(a, b))]
+        nmap.append(n2)
+        sig.append(1.0 if tmap(rwg["tp"][n]) == rwg["tp"][n2] else -1.0)
+    nmap, sig = np.array(nmap), np.array(sig)
+    assert (sig < 0).sum() > 0
+    n1, n2, n3 = cfg1.n
+    nv = cfg1.n_v
+    v = np.arange(nv)
+    i1, i2, i3 = geometry.voxel_index(v, cfg1.n)
+    Rv = (n1 - 1 - i1) + n1 * ((n2 - 1 - i2) + n2 * i3)
+    scale = np.abs(dense1).max()
+    for chi, c in ((0, -1.0), (1, -1.0), (2, 1.0)):
+        Zc = dense1[chi * nv:(chi + 1) * nv]
+        lhs = Zc[Rv][:, nmap]
+        rhs = c * sig[None, :] * Zc
+        assert np.max(np.abs(lhs - rhs)) <= 1e-13 * scale
+
+
+def test_P17_golden_dense_summary(dense1, cfg1):
+    with open(os.path.join(GOLDEN, "cfg1_dense_summary.json")) as f:
+        g = json.load(f)
+    nv = cfg1.n_v
+    for chi in range(3):
+        nrm = np.linalg.norm(dense1[chi * nv:(chi + 1) * nv])
+        assert abs(nrm - g["fro"][chi]) <= 1e-13 * g["fro"][chi]
+    W = synth.complex_gaussian(dense1.size, g["checksum_seed"]).reshape(dense1.shape)
+    cs = np.sum(W * dense1)
+    ref = complex(g["checksum"][0], g["checksum"][1])
+    assert abs(cs - ref) <= 1e-12 * abs(ref)
+
+
+# ---------------------------------------------------------------- TT-SVD
+
+def _rand_tt(dims, ranks, seed):
+    rng = np.random.default_rng(seed)
+    rr = (1,) + tuple(ranks) + (1,)
+    return [(rng.normal(size=(rr[k], dims[k], rr[k + 1])) + 1j * rng.normal(size=(rr[k], dims[k], rr[k + 1])))
+            for k in range(len(dims))]
+
+
+def test_P18_P19_ttsvd_bound_and_ranks(dense1, cfg1):
+    for chi in range(3):
+        A = ttmv.tensor_of(dense1, cfg1.n, chi)
+        cores = ttsvd.tt_svd(A, 1e-8)
+        err = np.linalg.norm(ttmv.full(cores) - A) / np.linalg.norm(A)
+        assert err <= 1e-8
+        r = ttmv.ranks_of(cores)
+        # informational (P19): probe at 1-pt voxel rule gave (7,31,73) / z (7,30,73)
+        assert 5 <= r[0] <= 9 and 25 <= r[1] <= 37 and 65 <= r[2] <= 81, r
+
+
+def test_P20_ttsvd_special_cases():
+    dims = (5, 6, 7, 8)
+    vs = [np.random.default_rng(k).normal(size=d) + 1j for k, d in enumerate(dims)]
+    A = np.einsum("i,j,k,l->ijkl", *vs)
+    assert ttmv.ranks_of(ttsvd.tt_svd(A, 1e-12)) == (1, 1, 1)
+    Z = np.zeros(dims, dtype=complex)
+    c = ttsvd.tt_svd(Z, 1e-6)
+    assert ttmv.ranks_of(c) == (1, 1, 1) and np.all(ttmv.full(c) == 0)
+    i = np.arange(10)
+    H = 1.0 / (i[:, None, None, None] + i[None, :, None, None] + i[None, None, :, None] + i[None, None, None, :] + 1)
+    c = ttsvd.tt_svd(H, 1e-6)
+    assert np.linalg.norm(ttmv.full(c) - H) <= 1e-6 * np.linalg.norm(H)
+    assert max(ttmv.ranks_of(c)) <= 8
+
+
+# ---------------------------------------------------------------- maxvol
+
+def test_P21_maxvol_invariants():
+    rng = np.random.default_rng(21)
+    for (n, r) in ((50, 5), (200, 17), (31, 30)):
+        A = rng.normal(size=(n, r)) + 1j * rng.normal(size=(n, r))
+        I0 = maxvol.lu_pivots(A)
+        I, B, swaps = maxvol.maxvol(A, tau=0.05)
+        assert len(set(I.tolist())) == r
+        assert np.max(np.abs(B[I] - np.eye(r))) < 1e-12
+        assert np.max(np.abs(B)) <= 1.05 + 1e-12
+        assert np.max(np.abs(B - A @ np.linalg.inv(A[I]))) < 1e-10 * max(1, np.abs(B).max())
+        d0 = abs(np.linalg.det(A[I0]))
+        d1 = abs(np.linalg.det(A[I]))
+        assert d1 >= d0 * (1.05 ** swaps) * (1 - 1e-10)
+
+
+def test_P22_maxvol_brute_force_hadamard_bound():
+    rng = np.random.default_rng(22)
+    for (n, r) in ((8, 2), (10, 3), (12, 4)):
+        A = rng.normal(size=(n, r)) + 1j * rng.normal(size=(n, r))
+        I, _, _ = maxvol.maxvol(A, tau=0.05)
+        dI = abs(np.linalg.det(A[I]))
+        bound = (np.sqrt(r) * 1.05) ** r
+        best = max(abs(np.linalg.det(A[list(J)])) for J in itertools.combinations(range(n), r))
+        assert best <= bound * dI * (1 + 1e-12)
+
+
+def test_P23_maxvol_identity_top():
+    rng = np.random.default_rng(23)
+    r = 6
+    C = rng.uniform(-0.6, 0.6, size=(30, r)) + 1j * rng.uniform(-0.6, 0.6, size=(30, r))
+    A = np.vstack([np.eye(r), C])
+    I, B, swaps = maxvol.maxvol(A)
+    assert list(I) == list(range(r)) and swaps == 0
+
+
+# ---------------------------------------------------------------- TT-cross
+
+def _cross_on(T, tol, seed=0):
+    dims = T.shape
+    fn = lambda idx: T[idx[:, 0], idx[:, 1], idx[:, 2], idx[:, 3]]
+    hi = synth.uniform_indices(dims, 300, 1000 + seed)
+    st = synth.uniform_indices(dims, 1, 2000 + seed)[0]
+    return ttcross.tt_cross(fn, dims, tol, st, hi)
+
+
+def test_P24_cross_recovers_random_tt():
+    for ranks, seed in (((2, 3, 2), 1), ((3, 5, 4), 2)):
+        cores = _rand_tt((12, 12, 12, 64), ranks, seed)
+        T = ttmv.full(cores)
+        res = _cross_on(T, 1e-12, seed)
+        assert res.ranks == ranks
+        assert np.linalg.norm(ttmv.full(res.cores) - T) <= 1e-12 * np.linalg.norm(T)
+
+
+def test_P25_cross_rank_one_cases():
+    dims = (6, 7, 8, 9)
+    C = np.full(dims, 2.5 - 1j)
+    assert _cross_on(C, 1e-10).ranks == (1, 1, 1)
+    vs = [np.random.default_rng(k).normal(size=d) + 0.5j for k, d in enumerate(dims)]
+    S = np.einsum("i,j,k,l->ijkl", *vs)
+    res = _cross_on(S, 1e-10)
+    assert res.ranks == (1, 1, 1)
+    assert np.linalg.norm(ttmv.full(res.cores) - S) <= 1e-12 * np.linalg.norm(S)
+
+
+def test_P26_cross_cfg1_vs_dense(dense1, cfg1):
+    dims = cfg1.n + (dense1.shape[1],)
+    hi = synth.uniform_indices(dims, 1000, synth.SEEDS["heldout"])
+    for chi in range(3):
+        A = ttmv.tensor_of(dense1, cfg1.n, chi)
+        fn = lambda idx: A[idx[:, 0], idx[:, 1], idx[:, 2], idx[:, 3]]
+        st = synth.uniform_indices(dims, 1, synth.SEEDS["cross"] + chi)[0]
+        res = ttcross.tt_cross(fn, dims, cfg1.tol, st, hi)
+        err = np.linalg.norm(ttmv.full(res.cores) - A) / np.linalg.norm(A)
+        assert err <= 10 * cfg1.tol, (chi, err, res.ranks)
+        assert res.converged
+
+
+# ---------------------------------------------------------------- TT matvecs
+
+DIMS = (5, 6, 7, 9)
+
+
+def _tts(seed=0, ranks=(3, 4, 5)):
+    return [_rand_tt(DIMS, ranks, seed + 10 * chi) for chi in range(3)]
+
+
+def test_P28_matvec_vs_dense_expansion():
+    tts = _tts()
+    Zt = ttmv.full_matrix(tts)
+    x = synth.complex_gaussian(DIMS[3], 1)
+    u = synth.complex_gaussian(3 * 5 * 6 * 7, 2)
+    assert validate.rel_l2(ttmv.apply(tts, x, "N"), Zt @ x) < 1e-13
+    assert validate.rel_l2(ttmv.apply(tts, u, "T"), Zt.T @ u) < 1e-13
+    assert validate.rel_l2(ttmv.apply(tts, u, "C"), Zt.conj().T @ u) < 1e-13
+    # element-wise: the dense expansion agrees with the chain evaluation (Eq. 9)
+    idx = synth.uniform_indices(DIMS, 50, 3)
+    T0 = ttmv.full(tts[0])
+    assert np.allclose(ttmv.eval_at(tts[0], idx), T0[tuple(idx.T)], rtol=1e-13, atol=0)
+
+
+def test_P29_adjoint_identities():
+    tts = _tts(5)
+    x = synth.complex_gaussian(DIMS[3], 4)
+    u = synth.complex_gaussian(3 * 5 * 6 * 7, 5)
+    lhs = np.sum(ttmv.apply(tts, x, "N") * u)            # bilinear, no conjugation
+    rhs = np.sum(x * ttmv.apply(tts, u, "T"))
+    assert abs(lhs - rhs) <= 1e-13 * abs(lhs)
+    lhs = np.vdot(ttmv.apply(tts, x, "N"), u)
+    rhs = np.vdot(x, ttmv.apply(tts, u, "C"))
+    assert abs(lhs - rhs) <= 1e-13 * abs(lhs)
+
+
+def test_P30_special_cases():
+    tts = _tts(7)
+    assert np.all(ttmv.apply(tts, np.zeros(DIMS[3], complex), "N") == 0)
+    Zt = ttmv.full_matrix(tts)
+    e = np.zeros(DIMS[3], complex); e[4] = 1
+    assert np.allclose(ttmv.apply(tts, e, "N"), Zt[:, 4], rtol=1e-14, atol=1e-14 * np.abs(Zt).max())
+    ones = [[np.ones((1, d, 1), complex) if k < 3 else np.ones((1, d, 1), complex) for k, d in enumerate(DIMS)]] * 3
+    y = ttmv.apply(ones, np.ones(DIMS[3], complex), "N")
+    assert np.all(y == DIMS[3])
+
+
+def test_P31_P32_block_and_linearity():
+    tts = _tts(9)
+    X = synth.complex_gaussian(DIMS[3], 6, ncols=8)
+    Y = ttmv.apply(tts, X, "N")
+    for j in range(8):
+        assert np.array_equal(Y[:, j], ttmv.apply(tts, X[:, j], "N"))
+    a, b = 0.3 - 2j, 1.7 + 0.2j
+    lhs = ttmv.apply(tts, a * X[:, 0] + b * X[:, 1], "N")
+    rhs = a * Y[:, 0] + b * Y[:, 1]
+    assert validate.rel_l2(lhs, rhs) < 1e-13
+
+
+def test_P35_compression_factor_exact():
+    f = validate.compression_factor((12, 12, 12), 1128, [(7, 31, 73)] * 3)
+    dense = 3 * 1728 * 1128
+    tt = 3 * (12 * 7 + 7 * 12 * 31 + 31 * 12 * 73 + 73 * 1128)
+    assert f == Fraction(dense, tt) and isinstance(f, Fraction)
+
+
+def test_T1_entry_parity_metric():
+    ref = np.array([1.0, 1e-9, -2.0 + 1j, 0.0])
+    ok, _ = validate.entry_parity(ref * (1 + 1e-14), ref)
+    assert ok
+    bad = ref.copy(); bad[2] += 1e-10
+    ok, w = validate.entry_parity(bad, ref)
+    assert not ok and w["elementwise_rel"] > 1e-12
