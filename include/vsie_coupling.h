@@ -1,0 +1,203 @@
+/*
+ * vsie_coupling.h — C ABI of the B200-native Z_bc coupling library
+ * (hybrid VSIE of arXiv 2206.12409, the remote-conductor coupling block).
+ *
+ * What the library computes (PAPER.md = P:<line>):
+ *   Z_bc in C^{q n_v x m}, q = 3 (PWC voxel testing), m RWG basis
+ *   functions on the far conductors, mapping surface currents to the
+ *   fields tested in the body through the dyadic Green's function
+ *   G = (I + grad grad / k0^2) g, g = exp(-i k0 R)/(4 pi R).
+ *   Each chi-component is a 4-D tensor n1 x n2 x n3 x m held in
+ *   TT format with cores G1 (n1 x r1), G2 (r1 x n2 x r2), G3 (r2 x n3 x r3),
+ *   G4 (r3 x m) (Eq. 14), built by DMRG TT-cross from an
+ *   index -> value entry function and applied forward
+ *    and transposed on every GMRES iteration.
+ *
+ * Conventions (binding):
+ *  - complex values are interleaved (re, im) float64 pairs
+ *    (== C99 double _Complex == torch.complex128);
+ *  - row of Z: rho = chi * n_v + i1 + n1 * (i2 + n2 * i3), chi in {0,1,2} = (x,y,z)
+ *    (P:227 component-major, column-major voxels);
+ *  - column of Z: RWG id in canonical order: per mesh (in input order) the
+ *    interior edges sorted by (min vertex id, max vertex id); T+ = the
+ *    adjacent triangle with the smaller id;
+ *  - entry Z[rho, n] = scale * sum_{p=1..8} w_p sum_{s=1..6} [G(r_p - r_s) J_s]_chi
+ *    with 2x2x2 Gauss nodes per voxel (weights h1 h2 h3 / 8) and the interior
+ *    3-point rule per triangle, J_{+,q} = (l/6)(r_{+,q} - p+),
+ *    J_{-,q} = (l/6)(p- - r_{-,q});
+ *  - TT cores are column-major: core k element (a, i, b) at
+ *    a + r_{k-1} * (i + n_k * b), r_0 = r_4 = 1.
+ *
+ * Ownership: the handle owns all device memory it allocates (cores,
+ * workspaces).  The caller owns every pointer it passes; device pointers must
+ * stay valid until the stream-ordered call completes.  Mesh and grid arrays are
+ * read during build / import only (copied).
+ *
+ * Errors: every int-returning call returns VSIE_OK (0), a negative error code
+ * (the output handle, if any, is set to NULL) or a positive warning (valid
+ * handle).  vsie_last_error_message() returns a thread-local description of
+ * the last error of the calling thread.
+ *
+ * Threading: a handle is not re-entrant; independent handles are.
+ */
+#ifndef VSIE_COUPLING_H_
+#define VSIE_COUPLING_H_
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VSIE_ABI_VERSION 1
+
+/* status codes */
+#define VSIE_OK 0
+#define VSIE_WARN_NOT_CONVERGED 1  /* rank cap / max sweeps reached; best TT kept, error in info */
+#define VSIE_ERR_ARG (-1)          /* null pointer, n <= 0, h <= 0, tol <= 0, freq <= 0, op/nrhs out of range */
+#define VSIE_ERR_GEOMETRY (-2)     /* degenerate triangle, edge shared by > 2 triangles, or source nodes closer
+                                      than 10 max(h) to the voxel-node bounding box (non-singular rule) */
+#define VSIE_ERR_CUDA (-3)
+#define VSIE_ERR_NOMEM (-4)
+#define VSIE_ERR_NCCL (-5)
+#define VSIE_ERR_STATE (-6)        /* call not valid for this handle (e.g. no cores yet) */
+
+/* apply operators */
+#define VSIE_OP_N 0  /* y = Z x            (forward, Eq. 17)                  */
+#define VSIE_OP_T 1  /* z = Z^T u          (plain transpose, Eqs. 18-19)      */
+#define VSIE_OP_C 2  /* z = Z^H u          (conjugate transpose = conj(Z^T conj u)) */
+
+typedef struct vsie_coupling_s* vsie_coupling_t;
+
+/* Uniform voxel grid n1 x n2 x n3.  origin = centre of voxel (0,0,0);
+ * centre of voxel (i1,i2,i3) = origin + (i1 h1, i2 h2, i3 h3). */
+typedef struct {
+  int32_t n[3];
+  double h[3];
+  double origin[3];
+} vsie_grid;
+
+/* One triangulated far-domain surface (host arrays, read during build only). */
+typedef struct {
+  int64_t n_vertices;
+  const double* xyz;     /* [n_vertices][3] */
+  int64_t n_triangles;
+  const int32_t* tri;    /* [n_triangles][3] vertex ids */
+} vsie_mesh;
+
+/* Build options; call vsie_build_opts_default() first, then override.  */
+typedef struct {
+  int32_t max_rank;      /* TT-rank cap per bond, default 2048                          */
+  int32_t max_sweeps;    /* DMRG sweeps (L->R + R->L), default 8                         */
+  int32_t oversample;    /* randomized range-finder oversampling p, default 16           */
+  int32_t direct_svd_max;/* supercores with min dim <= this use a direct Jacobi SVD, default 384 */
+  int32_t heldout;       /* held-out validation sample per chi, default 1000              */
+  int32_t nrhs_max;      /* workspace sizing for block applies, default 64               */
+  uint64_t seed;         /* cross initialisation + sketches + held-out sample, default 12409010 */
+  double scale_re, scale_im;  /* global prefactor of every entry, default 1 + 0i          */
+  int32_t rank, world;   /* this process's rank and the number of ranks, default 0, 1   */
+  int32_t loopback;      /* 1: emulate `world` ranks inside this process on one GPU       */
+  const void* nccl_unique_id; /* 128 bytes from vsie_nccl_unique_id() on rank 0, world > 1 */
+  int32_t device;        /* CUDA device ordinal, -1 = current device                      */
+  int32_t verbose;       /* 1: progress lines on stderr                                   */
+} vsie_build_opts;
+
+typedef struct {
+  int32_t n[3];
+  int64_t m;
+  int32_t ranks[3][3];          /* [chi][k]: r1, r2, r3                                       */
+  int64_t core_bytes;           /* device bytes of all cores held by this handle (all shards) */
+  int64_t compression_num, compression_den; /* (3 n_v m) / sum|cores| as a reduced fraction */
+  int64_t entries_evaluated;    /* entry-function calls made by the build (all ranks)        */
+  int32_t sweeps[3];
+  double heldout_err[3];        /* relative L2 error of TT vs entries on the held-out sample */
+  double build_s;               /* wall seconds of vsie_coupling_build                       */
+  double build_entry_s, build_factor_s, build_maxvol_s; /* build breakdown (device time)      */
+  int32_t slab[2];              /* this rank's owned i3 planes [slab0, slab1)                 */
+  int64_t cols[2];              /* this rank's owned G4 columns [cols0, cols1)                */
+  int32_t world, rank, loopback;
+  double k0;
+} vsie_info;
+
+/* Per-kernel device timing of apply calls (opt-in, see vsie_coupling_set_timing). */
+typedef struct {
+  char name[32];
+  int64_t launches;
+  double total_ms;
+  int64_t bytes_per_launch;     /* algorithmic HBM bytes of one launch (SURVEY §8d formula)  */
+  int64_t flops_per_launch;
+} vsie_timer;
+
+int32_t vsie_abi_version(void);
+void vsie_build_opts_default(vsie_build_opts* opts);
+const char* vsie_status_string(int32_t status);
+const char* vsie_last_error_message(void);
+
+/* 128-byte NCCL unique id for a multi-process group (rank 0 calls it and
+ * broadcasts the bytes; every rank passes them in vsie_build_opts). */
+int32_t vsie_nccl_unique_id(void* out128);
+
+/* Build Z_bc in TT form by DMRG TT-cross over the entry function.
+ * Collective and synchronous: every rank calls it with identical arguments
+ * except opts->rank.  tol is the relative Frobenius target per chi-tensor
+ * (P:287 uses 1e-3; BASELINE configs use 1e-8 / 1e-6).  On VSIE_OK or
+ * VSIE_WARN_NOT_CONVERGED *out is a valid handle. */
+int32_t vsie_coupling_build(const vsie_grid* grid, const vsie_mesh* meshes, int32_t n_meshes,
+                            double freq_hz, double tol, const vsie_build_opts* opts,
+                            vsie_coupling_t* out);
+
+/* Create a handle from existing cores (the "store and recycle" of P:375).
+ * ranks[chi*3 + k] = r_{k+1}; host_cores[chi*4 + k] = column-major core k+1
+ * (complex128) of component chi.  Each rank keeps only its owned shards. */
+int32_t vsie_coupling_import_cores(const vsie_grid* grid, const vsie_mesh* meshes, int32_t n_meshes,
+                                   double freq_hz, const int32_t ranks[9],
+                                   const void* const host_cores[12], const vsie_build_opts* opts,
+                                   vsie_coupling_t* out);
+
+/* Copy core k (0..3) of component chi (0..2) to host (full core; all ranks
+ * must call it together when world > 1).  With host_dst == NULL only
+ * *nelems is written. */
+int32_t vsie_coupling_export_cores(vsie_coupling_t h, int32_t chi, int32_t k, void* host_dst,
+                                   int64_t* nelems);
+
+/* Apply the TT operator on `stream` (cudaStream_t, NULL = legacy default).
+ *  OP_N: x = device complex128 [m x nrhs] (column-major, ld = m, replicated on
+ *        every rank) -> y = device complex128 [3 * n1 * n2 * (slab1 - slab0) x nrhs]
+ *        (the rank's slab; chi-major, i1 fastest; ld = rows).
+ *  OP_T / OP_C: x = the rank's slab of u (layout as y above) -> y = z [m x nrhs],
+ *        replicated on every rank after the collective.
+ * 1 <= nrhs <= nrhs_max.  Asynchronous; collective when world > 1. */
+int32_t vsie_coupling_apply(vsie_coupling_t h, const void* x, void* y, int32_t op, int32_t nrhs,
+                            void* stream);
+
+/* Same as apply but x and y are HOST buffers: H2D copy, apply, D2H copy,
+ * synchronous (the end-to-end call of a CPU-resident GMRES). */
+int32_t vsie_coupling_apply_host(vsie_coupling_t h, const void* x_host, void* y_host, int32_t op,
+                                 int32_t nrhs);
+
+/* Exact quadrature entries (the cross's black box, not the TT value):
+ * idx = device int64 [count][2] (row, col), out = device complex128 [count].
+ * Rows and columns are global indices (any rank may evaluate any entry). */
+int32_t vsie_coupling_entries(vsie_coupling_t h, const int64_t* idx, int64_t count, void* out,
+                              void* stream);
+
+/* TT value at (row, col) pairs (Eq. 9 chain product), same
+ * layout as vsie_coupling_entries.  world == 1 handles only. */
+int32_t vsie_coupling_tt_eval(vsie_coupling_t h, const int64_t* idx, int64_t count, void* out,
+                              void* stream);
+
+int32_t vsie_coupling_info(vsie_coupling_t h, vsie_info* out);
+
+/* Per-kernel CUDA-event timing of subsequent apply calls: enable = 1 starts
+ * (and resets) it, 0 stops it.  vsie_coupling_timers copies up to `max`
+ * accumulated timers (synchronises the handle's streams). */
+int32_t vsie_coupling_set_timing(vsie_coupling_t h, int32_t enable);
+int32_t vsie_coupling_timers(vsie_coupling_t h, vsie_timer* out, int32_t max, int32_t* n_out);
+
+void vsie_coupling_destroy(vsie_coupling_t h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VSIE_COUPLING_H_ */

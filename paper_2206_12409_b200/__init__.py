@@ -1,0 +1,12 @@
+"""B200-native Z_bc coupling library (hybrid VSIE, arXiv 2206.12409).
+
+The compute path is the sm_100a C-ABI library ``libvsie_coupling.so``
+(include/vsie_coupling.h); this package is its thin Python binding.
+"""
+from ._lib import VsieError, lib  # noqa: F401
+from .coupling import Coupling, Grid, nccl_unique_id  # noqa: F401
+
+
+def grid_of(cfg) -> Grid:
+    """Grid descriptor of a synth.Config (input marshalling only)."""
+    return Grid(tuple(cfg.n), tuple(cfg.h), tuple(cfg.origin))

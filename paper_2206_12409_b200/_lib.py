@@ -1,0 +1,111 @@
+"""ctypes declarations of include/vsie_coupling.h (argument marshalling only).
+
+The shared library is built in-tree by ``paper_2206_12409_b200._build``.  If
+it is missing the import fails loudly: there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libvsie_coupling.so")
+HEADER = os.path.join(os.path.dirname(PKG), "include", "vsie_coupling.h")
+
+VSIE_OK = 0
+VSIE_WARN_NOT_CONVERGED = 1
+OPS = {"N": 0, "T": 1, "C": 2}
+
+
+class vsie_grid(C.Structure):
+    _fields_ = [("n", C.c_int32 * 3), ("h", C.c_double * 3), ("origin", C.c_double * 3)]
+
+
+class vsie_mesh(C.Structure):
+    _fields_ = [("n_vertices", C.c_int64), ("xyz", C.c_void_p), ("n_triangles", C.c_int64), ("tri", C.c_void_p)]
+
+
+class vsie_build_opts(C.Structure):
+    _fields_ = [("max_rank", C.c_int32), ("max_sweeps", C.c_int32), ("oversample", C.c_int32),
+                ("direct_svd_max", C.c_int32), ("heldout", C.c_int32), ("nrhs_max", C.c_int32),
+                ("seed", C.c_uint64), ("scale_re", C.c_double), ("scale_im", C.c_double),
+                ("rank", C.c_int32), ("world", C.c_int32), ("loopback", C.c_int32),
+                ("nccl_unique_id", C.c_void_p), ("device", C.c_int32), ("verbose", C.c_int32)]
+
+
+class vsie_info(C.Structure):
+    _fields_ = [("n", C.c_int32 * 3), ("m", C.c_int64), ("ranks", (C.c_int32 * 3) * 3),
+                ("core_bytes", C.c_int64), ("compression_num", C.c_int64), ("compression_den", C.c_int64),
+                ("entries_evaluated", C.c_int64), ("sweeps", C.c_int32 * 3), ("heldout_err", C.c_double * 3),
+                ("build_s", C.c_double), ("build_entry_s", C.c_double), ("build_factor_s", C.c_double),
+                ("build_maxvol_s", C.c_double), ("slab", C.c_int32 * 2), ("cols", C.c_int64 * 2),
+                ("world", C.c_int32), ("rank", C.c_int32), ("loopback", C.c_int32), ("k0", C.c_double)]
+
+
+class vsie_timer(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("total_ms", C.c_double),
+                ("bytes_per_launch", C.c_int64), ("flops_per_launch", C.c_int64)]
+
+
+HANDLE = C.c_void_p
+
+_SIGS = {
+    "vsie_abi_version": (C.c_int32, []),
+    "vsie_build_opts_default": (None, [C.POINTER(vsie_build_opts)]),
+    "vsie_status_string": (C.c_char_p, [C.c_int32]),
+    "vsie_last_error_message": (C.c_char_p, []),
+    "vsie_nccl_unique_id": (C.c_int32, [C.c_void_p]),
+    "vsie_coupling_build": (C.c_int32, [C.POINTER(vsie_grid), C.POINTER(vsie_mesh), C.c_int32, C.c_double,
+                                        C.c_double, C.POINTER(vsie_build_opts), C.POINTER(HANDLE)]),
+    "vsie_coupling_import_cores": (C.c_int32, [C.POINTER(vsie_grid), C.POINTER(vsie_mesh), C.c_int32, C.c_double,
+                                               C.POINTER(C.c_int32), C.POINTER(C.c_void_p),
+                                               C.POINTER(vsie_build_opts), C.POINTER(HANDLE)]),
+    "vsie_coupling_export_cores": (C.c_int32, [HANDLE, C.c_int32, C.c_int32, C.c_void_p, C.POINTER(C.c_int64)]),
+    "vsie_coupling_apply": (C.c_int32, [HANDLE, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    "vsie_coupling_apply_host": (C.c_int32, [HANDLE, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32]),
+    "vsie_coupling_entries": (C.c_int32, [HANDLE, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "vsie_coupling_tt_eval": (C.c_int32, [HANDLE, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "vsie_coupling_info": (C.c_int32, [HANDLE, C.POINTER(vsie_info)]),
+    "vsie_coupling_set_timing": (C.c_int32, [HANDLE, C.c_int32]),
+    "vsie_coupling_timers": (C.c_int32, [HANDLE, C.POINTER(vsie_timer), C.c_int32, C.POINTER(C.c_int32)]),
+    "vsie_coupling_destroy": (None, [HANDLE]),
+}
+
+
+def header_symbols(path: str = HEADER):
+    """Function names declared in include/vsie_coupling.h."""
+    txt = open(path).read()
+    return sorted(set(re.findall(r"\b(vsie_[a-z_]+)\s*\(", txt)) - {"vsie_coupling_t"})
+
+
+class VsieError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{status}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2206_12409_b200._build` "
+                "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(status: int, allow_warn: bool = False) -> int:
+    if status == VSIE_OK or (allow_warn and status > 0):
+        return status
+    L = lib()
+    raise VsieError(L.vsie_status_string(status).decode(), L.vsie_last_error_message().decode())

@@ -1,0 +1,251 @@
+"""Thin Python wrapper over the C ABI: ``Coupling`` = one Z_bc handle.
+
+Every compute step runs inside libvsie_coupling.so; this module only converts
+arguments (numpy / torch tensors -> pointers) and status codes -> exceptions.
+PyTorch provides device memory and the current CUDA stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from fractions import Fraction
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib
+
+
+@dataclass(frozen=True)
+class Grid:
+    n: tuple
+    h: tuple
+    origin: tuple
+
+    def as_c(self):
+        g = _lib.vsie_grid()
+        for a in range(3):
+            g.n[a] = int(self.n[a])
+            g.h[a] = float(self.h[a])
+            g.origin[a] = float(self.origin[a])
+        return g
+
+
+def _meshes_c(meshes):
+    keep = []
+    arr = (_lib.vsie_mesh * len(meshes))()
+    for i, (xyz, tri) in enumerate(meshes):
+        xyz = np.ascontiguousarray(xyz, dtype=np.float64)
+        tri = np.ascontiguousarray(tri, dtype=np.int32)
+        keep += [xyz, tri]
+        arr[i].n_vertices = xyz.shape[0]
+        arr[i].xyz = xyz.ctypes.data
+        arr[i].n_triangles = tri.shape[0]
+        arr[i].tri = tri.ctypes.data
+    return arr, keep
+
+
+def _opts(**kw):
+    o = _lib.vsie_build_opts()
+    lib().vsie_build_opts_default(C.byref(o))
+    keep = None
+    for k, v in kw.items():
+        if v is None:
+            continue
+        if k == "scale":
+            o.scale_re, o.scale_im = float(np.real(v)), float(np.imag(v))
+        elif k == "nccl_unique_id":
+            keep = C.create_string_buffer(bytes(v), 128)
+            o.nccl_unique_id = C.cast(keep, C.c_void_p)
+        else:
+            setattr(o, k, v)
+    return o, keep
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_ptr(stream):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(lib().vsie_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Coupling:
+    """A Z_bc handle (cores on device, slab partition, workspaces)."""
+
+    def __init__(self, handle, status=0):
+        self._h = _lib.HANDLE(handle)
+        self.status = status
+
+    # ------------------------------------------------------------------ construction
+    @classmethod
+    def build(cls, grid: Grid, meshes, freq: float, tol: float, **opts):
+        """vsie_coupling_build: TT-cross over the entry kernel."""
+        g = grid.as_c()
+        arr, keep = _meshes_c(meshes)
+        o, k2 = _opts(**opts)
+        h = _lib.HANDLE()
+        st = lib().vsie_coupling_build(C.byref(g), arr, len(meshes), float(freq), float(tol), C.byref(o), C.byref(h))
+        check(st, allow_warn=True)
+        del keep, k2
+        return cls(h.value, st)
+
+    @classmethod
+    def from_cores(cls, grid: Grid, meshes, freq: float, cores, **opts):
+        """vsie_coupling_import_cores; cores[chi][k] = array (r_{k-1}, n_k, r_k)."""
+        g = grid.as_c()
+        arr, keep = _meshes_c(meshes)
+        o, k2 = _opts(**opts)
+        ranks = (C.c_int32 * 9)()
+        ptrs = (C.c_void_p * 12)()
+        flat = []
+        for chi in range(3):
+            for k in range(3):
+                ranks[3 * chi + k] = int(cores[chi][k].shape[2])
+            for k in range(4):
+                a = np.asarray(cores[chi][k], dtype=np.complex128).ravel(order="F")
+                a = np.ascontiguousarray(a)
+                flat.append(a)
+                ptrs[4 * chi + k] = a.ctypes.data
+        h = _lib.HANDLE()
+        check(lib().vsie_coupling_import_cores(C.byref(g), arr, len(meshes), float(freq), ranks, ptrs, C.byref(o),
+                                               C.byref(h)))
+        del keep, k2, flat
+        return cls(h.value)
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            lib().vsie_coupling_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # ------------------------------------------------------------------ queries
+    def info(self) -> dict:
+        i = _lib.vsie_info()
+        check(lib().vsie_coupling_info(self._h, C.byref(i)))
+        return dict(
+            n=tuple(i.n), m=i.m, ranks=[tuple(i.ranks[c]) for c in range(3)], core_bytes=i.core_bytes,
+            compression=Fraction(i.compression_num, i.compression_den) if i.compression_den else None,
+            entries_evaluated=i.entries_evaluated, sweeps=tuple(i.sweeps), heldout_err=tuple(i.heldout_err),
+            build_s=i.build_s, build_entry_s=i.build_entry_s, build_factor_s=i.build_factor_s,
+            build_maxvol_s=i.build_maxvol_s, slab=tuple(i.slab), cols=tuple(i.cols), world=i.world,
+            rank=i.rank, loopback=i.loopback, k0=i.k0)
+
+    @property
+    def m(self):
+        return self.info()["m"]
+
+    def export_cores(self):
+        """[chi][k] numpy arrays (r_{k-1}, n_k, r_k) (column-major core layout, §8c-L16)."""
+        inf = self.info()
+        dims = list(inf["n"]) + [inf["m"]]
+        out = []
+        for chi in range(3):
+            r = (1,) + tuple(inf["ranks"][chi]) + (1,)
+            cs = []
+            for k in range(4):
+                ne = C.c_int64()
+                buf = np.empty(r[k] * dims[k] * r[k + 1], dtype=np.complex128)
+                check(lib().vsie_coupling_export_cores(self._h, chi, k, buf.ctypes.data, C.byref(ne)))
+                assert ne.value == buf.size
+                cs.append(buf.reshape((r[k], dims[k], r[k + 1]), order="F"))
+            out.append(cs)
+        return out
+
+    # ------------------------------------------------------------------ compute
+    def apply(self, x, op: str = "N", out=None, stream=None):
+        """vsie_coupling_apply on device tensors (complex128, column-major RHS blocks).
+
+        x: (len,) or (len, nrhs) CUDA complex128 tensor; column-major blocks are
+        passed as the transpose of a contiguous (nrhs, len) tensor."""
+        torch = _torch()
+        inf_m = self.m
+        vec = x.dim() == 1
+        X = x.reshape(-1, 1) if vec else x
+        nrhs = X.shape[1]
+        Xc = X.t().contiguous()  # (nrhs, len): column-major (len, nrhs)
+        n_out = self.out_len(op)
+        if out is None:
+            Y = torch.empty((nrhs, n_out), dtype=torch.complex128, device=x.device)
+        else:
+            Y = out.reshape(-1, 1).t() if vec else out.t()
+            assert Y.is_contiguous()
+        del inf_m
+        check(lib().vsie_coupling_apply(self._h, C.c_void_p(Xc.data_ptr()), C.c_void_p(Y.data_ptr()), _lib.OPS[op],
+                                        nrhs, _stream_ptr(stream)))
+        return Y[0] if vec else Y.t()
+
+    def apply_raw(self, x_ptr: int, y_ptr: int, op: str, nrhs: int, stream=None):
+        check(lib().vsie_coupling_apply(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr), _lib.OPS[op], nrhs,
+                                        _stream_ptr(stream)))
+
+    def apply_host(self, x: np.ndarray, op: str = "N") -> np.ndarray:
+        """vsie_coupling_apply_host: host in, host out (H2D + apply + D2H)."""
+        X = np.asarray(x, dtype=np.complex128)
+        vec = X.ndim == 1
+        X2 = X.reshape(-1, 1) if vec else X
+        nrhs = X2.shape[1]
+        Xf = np.asfortranarray(X2)
+        Y = np.empty((self.out_len(op), nrhs), dtype=np.complex128, order="F")
+        check(lib().vsie_coupling_apply_host(self._h, Xf.ctypes.data, Y.ctypes.data, _lib.OPS[op], nrhs))
+        return Y[:, 0] if vec else Y
+
+    def apply_host_raw(self, x_ptr: int, y_ptr: int, op: str, nrhs: int):
+        check(lib().vsie_coupling_apply_host(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr), _lib.OPS[op], nrhs))
+
+    def out_len(self, op: str) -> int:
+        inf = self.info()
+        n1, n2, _ = inf["n"]
+        vox = 3 * n1 * n2 * (inf["slab"][1] - inf["slab"][0]) if inf["world"] > 1 and not inf["loopback"] \
+            else 3 * n1 * n2 * inf["n"][2]
+        return vox if op == "N" else inf["m"]
+
+    def _idx_call(self, fn, rows, cols, stream=None):
+        torch = _torch()
+        rows = torch.as_tensor(rows, dtype=torch.int64)
+        cols = torch.as_tensor(cols, dtype=torch.int64)
+        dev = rows.device if rows.is_cuda else torch.device("cuda")
+        idx = torch.stack([rows.to(dev), cols.to(dev)], dim=1).contiguous()
+        out = torch.empty(idx.shape[0], dtype=torch.complex128, device=dev)
+        check(fn(self._h, C.c_void_p(idx.data_ptr()), idx.shape[0], C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+        return out
+
+    def entries(self, rows, cols, stream=None):
+        """Exact quadrature entries Z[rows, cols] (vsie_coupling_entries)."""
+        return self._idx_call(lib().vsie_coupling_entries, rows, cols, stream)
+
+    def tt_eval(self, rows, cols, stream=None):
+        """TT values at (rows, cols) (vsie_coupling_tt_eval)."""
+        return self._idx_call(lib().vsie_coupling_tt_eval, rows, cols, stream)
+
+    # ------------------------------------------------------------------ timing
+    def set_timing(self, enable: bool):
+        check(lib().vsie_coupling_set_timing(self._h, int(bool(enable))))
+
+    def timers(self):
+        n = C.c_int32()
+        arr = (_lib.vsie_timer * 64)()
+        check(lib().vsie_coupling_timers(self._h, arr, 64, C.byref(n)))
+        return [dict(name=arr[i].name.decode(), launches=arr[i].launches, total_ms=arr[i].total_ms,
+                     bytes_per_launch=arr[i].bytes_per_launch, flops_per_launch=arr[i].flops_per_launch)
+                for i in range(min(n.value, 64))]

@@ -1,0 +1,327 @@
+// C ABI of the Z_bc coupling library (include/vsie_coupling.h).  Every entry
+// point converts exceptions into status codes and records a thread-local
+// message; no C++ exception crosses the boundary.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+
+#include "cross.hpp"
+#include "handle.hpp"
+
+using namespace vsie;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    g_last_error.clear();
+    return f();
+  } catch (const Error& e) {
+    return fail(e.code, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(VSIE_ERR_NOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(VSIE_ERR_CUDA, e.what());
+  }
+}
+
+vsie_build_opts resolve_opts(const vsie_build_opts* o) {
+  vsie_build_opts d;
+  vsie_build_opts_default(&d);
+  if (o) d = *o;
+  VSIE_REQUIRE(d.max_rank >= 1 && d.max_sweeps >= 1 && d.oversample >= 1 && d.heldout >= 0, VSIE_ERR_ARG,
+               "bad build options");
+  VSIE_REQUIRE(std::isfinite(d.scale_re) && std::isfinite(d.scale_im), VSIE_ERR_ARG, "bad scale");
+  return d;
+}
+
+void finish_handle(vsie_coupling_s* h) {
+  handle_alloc_workspace(h);
+  h->has_cores = true;
+  VSIE_CHECK_CUDA(cudaDeviceSynchronize());
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t vsie_abi_version(void) { return VSIE_ABI_VERSION; }
+
+void vsie_build_opts_default(vsie_build_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->max_rank = 2048;
+  o->max_sweeps = 8;
+  o->oversample = 16;
+  o->direct_svd_max = 384;
+  o->heldout = 1000;
+  o->nrhs_max = 64;
+  o->seed = 12409010ull;
+  o->scale_re = 1.0;
+  o->scale_im = 0.0;
+  o->rank = 0;
+  o->world = 1;
+  o->loopback = 0;
+  o->nccl_unique_id = nullptr;
+  o->device = -1;
+  o->verbose = 0;
+}
+
+const char* vsie_status_string(int32_t s) {
+  switch (s) {
+    case VSIE_OK: return "VSIE_OK";
+    case VSIE_WARN_NOT_CONVERGED: return "VSIE_WARN_NOT_CONVERGED";
+    case VSIE_ERR_ARG: return "VSIE_ERR_ARG";
+    case VSIE_ERR_GEOMETRY: return "VSIE_ERR_GEOMETRY";
+    case VSIE_ERR_CUDA: return "VSIE_ERR_CUDA";
+    case VSIE_ERR_NOMEM: return "VSIE_ERR_NOMEM";
+    case VSIE_ERR_NCCL: return "VSIE_ERR_NCCL";
+    case VSIE_ERR_STATE: return "VSIE_ERR_STATE";
+    default: return "VSIE_UNKNOWN_STATUS";
+  }
+}
+
+const char* vsie_last_error_message(void) { return g_last_error.c_str(); }
+
+int32_t vsie_nccl_unique_id(void* out128) {
+  return guarded([&] {
+    VSIE_REQUIRE(out128 != nullptr, VSIE_ERR_ARG, "out is NULL");
+    return nccl_unique_id(out128);
+  });
+}
+
+int32_t vsie_coupling_build(const vsie_grid* grid, const vsie_mesh* meshes, int32_t n_meshes, double freq_hz,
+                            double tol, const vsie_build_opts* opts, vsie_coupling_t* out) {
+  if (out) *out = nullptr;
+  return guarded([&] {
+    VSIE_REQUIRE(out != nullptr, VSIE_ERR_ARG, "out is NULL");
+    VSIE_REQUIRE(tol > 0 && tol < 1 && std::isfinite(tol), VSIE_ERR_ARG, "tol must be in (0, 1)");
+    const vsie_build_opts o = resolve_opts(opts);
+    auto t0 = std::chrono::steady_clock::now();
+    auto h = std::make_unique<vsie_coupling_s>();
+    handle_init_geometry(h.get(), grid, meshes, n_meshes, freq_hz, &o);
+    const int status = cross_build(h.get(), tol, o);
+    finish_handle(h.get());
+    h->build_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *out = h.release();
+    return status;
+  });
+}
+
+int32_t vsie_coupling_import_cores(const vsie_grid* grid, const vsie_mesh* meshes, int32_t n_meshes,
+                                   double freq_hz, const int32_t ranks[9], const void* const host_cores[12],
+                                   const vsie_build_opts* opts, vsie_coupling_t* out) {
+  if (out) *out = nullptr;
+  return guarded([&] {
+    VSIE_REQUIRE(out != nullptr && ranks != nullptr && host_cores != nullptr, VSIE_ERR_ARG, "NULL argument");
+    const vsie_build_opts o = resolve_opts(opts);
+    auto h = std::make_unique<vsie_coupling_s>();
+    handle_init_geometry(h.get(), grid, meshes, n_meshes, freq_hz, &o);
+    for (int c = 0; c < 3; ++c) {
+      const int r[3] = {ranks[3 * c], ranks[3 * c + 1], ranks[3 * c + 2]};
+      const cplx* src[4];
+      for (int k = 0; k < 4; ++k) src[k] = static_cast<const cplx*>(host_cores[4 * c + k]);
+      handle_set_cores_host(h.get(), c, r, src);
+    }
+    finish_handle(h.get());
+    *out = h.release();
+    return VSIE_OK;
+  });
+}
+
+int32_t vsie_coupling_export_cores(vsie_coupling_t h, int32_t chi, int32_t k, void* host_dst, int64_t* nelems) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr && nelems != nullptr, VSIE_ERR_ARG, "NULL argument");
+    VSIE_REQUIRE(h->has_cores, VSIE_ERR_STATE, "handle has no TT cores");
+    VSIE_REQUIRE(chi >= 0 && chi < 3 && k >= 0 && k < 4, VSIE_ERR_ARG, "chi / k out of range");
+    VSIE_REQUIRE(h->comm == nullptr, VSIE_ERR_STATE, "export_cores of a multi-process handle: export per rank");
+    const int n[4] = {h->grid.n[0], h->grid.n[1], h->grid.n[2], (int)h->m};
+    const int64_t rl = k == 0 ? 1 : h->ranks[chi][k - 1];
+    const int64_t rr = k == 3 ? 1 : h->ranks[chi][k];
+    const int64_t total = rl * n[k] * rr;
+    *nelems = total;
+    if (!host_dst) return VSIE_OK;
+    cplx* dst = static_cast<cplx*>(host_dst);
+    VSIE_CHECK_CUDA(cudaDeviceSynchronize());
+    if (k == 0) {
+      VSIE_CHECK_CUDA(cudaMemcpy(dst, h->G1[chi].p, total * sizeof(cplx), cudaMemcpyDeviceToHost));
+    } else if (k == 1) {
+      VSIE_CHECK_CUDA(cudaMemcpy(dst, h->G2[chi].p, total * sizeof(cplx), cudaMemcpyDeviceToHost));
+    } else if (k == 2) {
+      const int64_t r2 = rl, r3 = rr, n3 = n[2];
+      for (const Shard& s : h->shards) {
+        const int64_t n3l = s.n3loc();
+        if (n3l == 0) continue;
+        VSIE_CHECK_CUDA(cudaMemcpy2D(dst + r2 * s.i3b, r2 * n3 * sizeof(cplx), s.G3[chi].p, r2 * n3l * sizeof(cplx),
+                                     r2 * n3l * sizeof(cplx), r3, cudaMemcpyDeviceToHost));
+      }
+    } else {
+      const int64_t r3 = rl;
+      for (const Shard& s : h->shards)
+        if (s.mloc() > 0)
+          VSIE_CHECK_CUDA(cudaMemcpy(dst + r3 * s.cb, s.G4[chi].p, r3 * s.mloc() * sizeof(cplx),
+                                     cudaMemcpyDeviceToHost));
+    }
+    return VSIE_OK;
+  });
+}
+
+int32_t vsie_coupling_apply(vsie_coupling_t h, const void* x, void* y, int32_t op, int32_t nrhs, void* stream) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "handle is NULL");
+    apply(h, static_cast<const cplx*>(x), static_cast<cplx*>(y), op, nrhs, static_cast<cudaStream_t>(stream));
+    return VSIE_OK;
+  });
+}
+
+int32_t vsie_coupling_apply_host(vsie_coupling_t h, const void* x_host, void* y_host, int32_t op, int32_t nrhs) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr && x_host != nullptr && y_host != nullptr, VSIE_ERR_ARG, "NULL argument");
+    VSIE_REQUIRE(nrhs >= 1 && nrhs <= h->nrhs_max, VSIE_ERR_ARG, "nrhs out of range");
+    const int64_t n12 = (int64_t)h->grid.n[0] * h->grid.n[1];
+    int64_t vox = 0;
+    if (h->comm)
+      vox = 3 * n12 * h->shards[0].n3loc();
+    else
+      vox = 3 * h->grid.nv();
+    const int64_t nx = (op == VSIE_OP_N ? h->m : vox) * nrhs;
+    const int64_t ny = (op == VSIE_OP_N ? vox : h->m) * nrhs;
+    h->io_x.ensure(nx);
+    h->io_y.ensure(ny);
+    if (!h->io_stream) VSIE_CHECK_CUDA(cudaStreamCreateWithFlags(&h->io_stream, cudaStreamNonBlocking));
+    VSIE_CHECK_CUDA(cudaMemcpyAsync(h->io_x.p, x_host, nx * sizeof(cplx), cudaMemcpyHostToDevice, h->io_stream));
+    apply(h, h->io_x.p, h->io_y.p, op, nrhs, h->io_stream);
+    VSIE_CHECK_CUDA(cudaMemcpyAsync(y_host, h->io_y.p, ny * sizeof(cplx), cudaMemcpyDeviceToHost, h->io_stream));
+    VSIE_CHECK_CUDA(cudaStreamSynchronize(h->io_stream));
+    return VSIE_OK;
+  });
+}
+
+int32_t vsie_coupling_entries(vsie_coupling_t h, const int64_t* idx, int64_t count, void* out, void* stream) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "handle is NULL");
+    VSIE_REQUIRE(count >= 0, VSIE_ERR_ARG, "count < 0");
+    if (count == 0) return VSIE_OK;
+    VSIE_REQUIRE(idx != nullptr && out != nullptr, VSIE_ERR_ARG, "idx / out is NULL");
+    launch_entries_list(h->eg, idx, count, static_cast<cplx*>(out), static_cast<cudaStream_t>(stream));
+    return VSIE_OK;
+  });
+}
+
+int32_t vsie_coupling_tt_eval(vsie_coupling_t h, const int64_t* idx, int64_t count, void* out, void* stream) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "handle is NULL");
+    VSIE_REQUIRE(count >= 0, VSIE_ERR_ARG, "count < 0");
+    if (count == 0) return VSIE_OK;
+    VSIE_REQUIRE(idx != nullptr && out != nullptr, VSIE_ERR_ARG, "idx / out is NULL");
+    tt_eval(h, idx, count, static_cast<cplx*>(out), static_cast<cudaStream_t>(stream));
+    return VSIE_OK;
+  });
+}
+
+int32_t vsie_coupling_info(vsie_coupling_t h, vsie_info* out) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr && out != nullptr, VSIE_ERR_ARG, "NULL argument");
+    std::memset(out, 0, sizeof(*out));
+    for (int a = 0; a < 3; ++a) out->n[a] = h->grid.n[a];
+    out->m = h->m;
+    int64_t core_elems = 0, bytes = 0;
+    for (int c = 0; c < 3; ++c) {
+      for (int k = 0; k < 3; ++k) out->ranks[c][k] = h->ranks[c][k];
+      const int64_t r1 = h->ranks[c][0], r2 = h->ranks[c][1], r3 = h->ranks[c][2];
+      core_elems += h->grid.n[0] * r1 + r1 * h->grid.n[1] * r2 + r2 * h->grid.n[2] * r3 + r3 * h->m;
+      bytes += h->G1[c].bytes() + h->G2[c].bytes();
+      for (const Shard& s : h->shards) bytes += s.G3[c].bytes() + s.G4[c].bytes();
+      out->sweeps[c] = h->sweeps[c];
+      out->heldout_err[c] = h->heldout_err[c];
+    }
+    out->core_bytes = bytes;
+    if (h->has_cores && core_elems > 0) {
+      int64_t num = 3 * h->grid.nv() * h->m, den = core_elems;
+      const int64_t g = std::gcd(num, den);
+      out->compression_num = num / g;
+      out->compression_den = den / g;
+    }
+    out->entries_evaluated = h->entries_evaluated;
+    out->build_s = h->build_s;
+    out->build_entry_s = h->build_entry_s;
+    out->build_factor_s = h->build_factor_s;
+    out->build_maxvol_s = h->build_maxvol_s;
+    out->slab[0] = h->shards.empty() ? 0 : h->shards.front().i3b;
+    out->slab[1] = h->shards.empty() ? 0 : h->shards.back().i3e;
+    out->cols[0] = h->shards.empty() ? 0 : h->shards.front().cb;
+    out->cols[1] = h->shards.empty() ? 0 : h->shards.back().ce;
+    out->world = h->world;
+    out->rank = h->rank;
+    out->loopback = h->loopback;
+    out->k0 = h->k0;
+    return VSIE_OK;
+  });
+}
+
+int32_t vsie_coupling_set_timing(vsie_coupling_t h, int32_t enable) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "handle is NULL");
+    VSIE_CHECK_CUDA(cudaDeviceSynchronize());
+    for (auto& t : h->pending) {
+      h->event_pool.push_back(t.e0);
+      h->event_pool.push_back(t.e1);
+    }
+    h->pending.clear();
+    h->timers.clear();
+    h->timing = enable != 0;
+    return VSIE_OK;
+  });
+}
+
+int32_t vsie_coupling_timers(vsie_coupling_t h, vsie_timer* out, int32_t max, int32_t* n_out) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr && n_out != nullptr, VSIE_ERR_ARG, "NULL argument");
+    VSIE_CHECK_CUDA(cudaDeviceSynchronize());
+    for (auto& t : h->pending) {
+      float ms = 0;
+      VSIE_CHECK_CUDA(cudaEventElapsedTime(&ms, t.e0, t.e1));
+      TimerSlot* slot = nullptr;
+      for (auto& s : h->timers)
+        if (s.name == t.name) slot = &s;
+      if (!slot) {
+        h->timers.push_back(TimerSlot{t.name, 0, 0.0, t.bytes, t.flops});
+        slot = &h->timers.back();
+      }
+      slot->launches += 1;
+      slot->total_ms += ms;
+      h->event_pool.push_back(t.e0);
+      h->event_pool.push_back(t.e1);
+    }
+    h->pending.clear();
+    const int n = (int)h->timers.size();
+    *n_out = n;
+    for (int i = 0; i < n && i < max && out; ++i) {
+      std::memset(&out[i], 0, sizeof(vsie_timer));
+      std::strncpy(out[i].name, h->timers[i].name.c_str(), sizeof(out[i].name) - 1);
+      out[i].launches = h->timers[i].launches;
+      out[i].total_ms = h->timers[i].total_ms;
+      out[i].bytes_per_launch = h->timers[i].bytes;
+      out[i].flops_per_launch = h->timers[i].flops;
+    }
+    return VSIE_OK;
+  });
+}
+
+void vsie_coupling_destroy(vsie_coupling_t h) {
+  if (!h) return;
+  cudaDeviceSynchronize();
+  delete h;
+}
+
+}  // extern "C"

@@ -1,0 +1,100 @@
+// Shared device/host helpers of the Z_bc coupling library (sm_100a).
+// Product code only — shares nothing with oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <stdexcept>
+#include <vector>
+
+#include "../../include/vsie_coupling.h"
+
+namespace vsie {
+
+struct Error : public std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define VSIE_CHECK_CUDA(expr)                                                                  \
+  do {                                                                                         \
+    cudaError_t _e = (expr);                                                                   \
+    if (_e != cudaSuccess) {                                                                   \
+      throw ::vsie::Error(_e == cudaErrorMemoryAllocation ? VSIE_ERR_NOMEM : VSIE_ERR_CUDA,     \
+                          std::string(#expr) + ": " + cudaGetErrorString(_e) + " at " +         \
+                              __FILE__ + ":" + std::to_string(__LINE__));                      \
+    }                                                                                          \
+  } while (0)
+
+#define VSIE_CHECK_LAUNCH() VSIE_CHECK_CUDA(cudaGetLastError())
+
+#define VSIE_REQUIRE(cond, code, msg)                                 \
+  do {                                                                \
+    if (!(cond)) throw ::vsie::Error((code), std::string(msg));       \
+  } while (0)
+
+// ----------------------------------------------------------------- complex128 as double2
+typedef double2 cplx;
+
+__host__ __device__ __forceinline__ cplx cmk(double r, double i) { return make_double2(r, i); }
+__host__ __device__ __forceinline__ cplx cadd(cplx a, cplx b) { return cmk(a.x + b.x, a.y + b.y); }
+__host__ __device__ __forceinline__ cplx csub(cplx a, cplx b) { return cmk(a.x - b.x, a.y - b.y); }
+__host__ __device__ __forceinline__ cplx cmul(cplx a, cplx b) {
+  return cmk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__host__ __device__ __forceinline__ cplx cconj(cplx a) { return cmk(a.x, -a.y); }
+__host__ __device__ __forceinline__ double cabs2(cplx a) { return a.x * a.x + a.y * a.y; }
+// acc += a * b  (4 DFMA)
+__device__ __forceinline__ void cfma(cplx& acc, cplx a, cplx b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+}
+
+__host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ----------------------------------------------------------------- device memory
+// Simple owning device buffer (cudaMalloc / cudaFree).
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    if (count == 0) return;
+    VSIE_CHECK_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  // grow-only reallocation (contents not preserved)
+  void ensure(size_t count) { if (count > n) alloc(count); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+// ----------------------------------------------------------------- per-kernel timing
+struct TimerSlot {
+  std::string name;
+  int64_t launches = 0;
+  double total_ms = 0;
+  int64_t bytes = 0, flops = 0;
+};
+
+}  // namespace vsie

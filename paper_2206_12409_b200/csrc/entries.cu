@@ -1,0 +1,142 @@
+// Z_bc entry evaluation: the black-box entry function of the
+// TT-cross — the 5-D surface-volume integral of
+// the dyadic Green's function (Eq. 3) between a PWC voxel testing
+// function and an RWG basis function, by the fixed non-singular
+// quadrature of SURVEY §8c-E (2x2x2 Gauss per voxel x 3-point rule per
+// triangle, 48 pair interactions per entry).
+//
+// Per pair, with R = r_p - r_s, u = 1/(k0 |R|), g = exp(-i k0 |R|)/(4 pi |R|):
+//   [G(R) J]_chi = g [ alpha J_chi + beta Rhat_chi (Rhat . J) ],
+//   alpha = 1 - i u - u^2,  beta = -1 + 3 i u + 3 u^2.
+// FP64 throughout (one rsqrt, one sincos per pair); FMA contraction on.
+#include "kernels.cuh"
+
+#include <cmath>
+
+namespace vsie {
+
+namespace {
+
+constexpr double kInv4Pi = 0.079577471545947667884441881686257181;  // 1/(4 pi)
+
+// Accumulates sum_{p, s} [G(r_p - r_s) J_s]_chi / (4 pi) * (without w, scale)
+// for one voxel centre (cx, cy, cz) and one RWG source record s36.
+template <int CHI>
+__device__ __forceinline__ void entry_acc(const EntryGeom& g, double cx, double cy, double cz,
+                                          const double* __restrict__ s36, double& ar, double& ai) {
+#pragma unroll 1
+  for (int q = 0; q < 6; ++q) {
+    const double sx = __ldg(s36 + 6 * q + 0), sy = __ldg(s36 + 6 * q + 1), sz = __ldg(s36 + 6 * q + 2);
+    const double jx = __ldg(s36 + 6 * q + 3), jy = __ldg(s36 + 6 * q + 4), jz = __ldg(s36 + 6 * q + 5);
+    const double jc = CHI == 0 ? jx : (CHI == 1 ? jy : jz);
+    const double bx = cx - sx, by = cy - sy, bz = cz - sz;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      const double rx = (p & 1) ? bx + g.dx : bx - g.dx;
+      const double ry = (p & 2) ? by + g.dy : by - g.dy;
+      const double rz = (p & 4) ? bz + g.dz : bz - g.dz;
+      const double r2 = fma(rx, rx, fma(ry, ry, rz * rz));
+      const double ir = rsqrt(r2);
+      const double R = r2 * ir;
+      double sn, cs;
+      sincos(g.k0 * R, &sn, &cs);
+      const double u = g.inv_k0 * ir;
+      const double u2 = u * u;
+      const double rc = CHI == 0 ? rx : (CHI == 1 ? ry : rz);
+      const double rj = fma(rx, jx, fma(ry, jy, rz * jz));
+      const double t = rj * rc * (ir * ir);                 // Rhat_chi (Rhat . J)
+      const double A = fma(1.0 - u2, jc, (3.0 * u2 - 1.0) * t);  // Re(alpha J_chi + beta t)
+      const double B = u * (3.0 * t - jc);                       // Im(...)
+      const double qq = ir * kInv4Pi;
+      // g * (A + iB) = qq (cs - i sn)(A + i B)
+      ar = fma(qq, fma(cs, A, sn * B), ar);
+      ai = fma(qq, fma(cs, B, -sn * A), ai);
+    }
+  }
+}
+
+__device__ __forceinline__ cplx entry_value(const EntryGeom& g, int chi, int i1, int i2, int i3,
+                                            int64_t n) {
+  const double cx = g.ox + i1 * g.hx, cy = g.oy + i2 * g.hy, cz = g.oz + i3 * g.hz;
+  const double* s36 = g.src + 36 * n;
+  double ar = 0, ai = 0;
+  if (chi == 0)
+    entry_acc<0>(g, cx, cy, cz, s36, ar, ai);
+  else if (chi == 1)
+    entry_acc<1>(g, cx, cy, cz, s36, ar, ai);
+  else
+    entry_acc<2>(g, cx, cy, cz, s36, ar, ai);
+  ar *= g.w;
+  ai *= g.w;
+  return cmk(g.scale_re * ar - g.scale_im * ai, g.scale_re * ai + g.scale_im * ar);
+}
+
+__global__ void __launch_bounds__(256) k_entries_list(EntryGeom g, const int64_t* __restrict__ idx,
+                                                      int64_t count, cplx* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = idx[2 * t], col = idx[2 * t + 1];
+    const int chi = (int)(row / g.nv);
+    const int64_t v = row - chi * g.nv;
+    const int i1 = (int)(v % g.n1);
+    const int i2 = (int)((v / g.n1) % g.n2);
+    const int i3 = (int)(v / ((int64_t)g.n1 * g.n2));
+    out[t] = entry_value(g, chi, i1, i2, i3, col);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_entries_block(EntryGeom g, BlockDesc b, cplx* __restrict__ out) {
+  const int64_t rows = b.row1 - b.row0;
+  const int64_t total = rows * b.nk1 * b.rr;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rloc = t % rows;
+    const int64_t c = t / rows;
+    const int64_t r = b.row0 + rloc;
+    const int64_t alpha = r % b.rl, ik = r / b.rl;
+    const int64_t ik1 = c % b.nk1, beta = c / b.nk1;
+    int i1, i2, i3;
+    int64_t n;
+    if (b.k == 1) {
+      i1 = (int)ik;
+      i2 = (int)ik1;
+      i3 = b.right[2 * beta];
+      n = b.right[2 * beta + 1];
+    } else if (b.k == 2) {
+      i1 = b.left[2 * alpha];
+      i2 = (int)ik;
+      i3 = (int)ik1;
+      n = b.right[2 * beta];
+    } else {
+      i1 = b.left[2 * alpha];
+      i2 = b.left[2 * alpha + 1];
+      i3 = (int)ik;
+      n = ik1;
+    }
+    out[rloc + b.ld * c] = entry_value(g, b.chi, i1, i2, i3, n);
+  }
+}
+
+int grid_for(int64_t work, int threads) {
+  int64_t blocks = ceil_div(work, threads);
+  const int64_t cap = 148 * 64;
+  return (int)(blocks < cap ? (blocks < 1 ? 1 : blocks) : cap);
+}
+
+}  // namespace
+
+void launch_entries_list(const EntryGeom& g, const int64_t* idx, int64_t count, cplx* out,
+                         cudaStream_t st) {
+  if (count <= 0) return;
+  k_entries_list<<<grid_for(count, 256), 256, 0, st>>>(g, idx, count, out);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_entries_block(const EntryGeom& g, const BlockDesc& b, cplx* out, cudaStream_t st) {
+  const int64_t total = (b.row1 - b.row0) * b.nk1 * b.rr;
+  if (total <= 0) return;
+  k_entries_block<<<grid_for(total, 256), 256, 0, st>>>(g, b, out);
+  VSIE_CHECK_LAUNCH();
+}
+
+}  // namespace vsie

@@ -1,0 +1,92 @@
+// The coupling handle: geometry on device, TT cores laid out for the slab
+// partition (SURVEY §8e design iii), apply workspaces, communicator, timers.
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "comm.hpp"
+#include "geometry.hpp"
+#include "kernels.cuh"
+
+namespace vsie {
+
+// One rank's slab: voxel planes i3 in [i3b, i3e) and G4 columns [cb, ce).
+struct Shard {
+  int i3b = 0, i3e = 0;
+  int64_t cb = 0, ce = 0;
+  DevBuf<cplx> G3[3];   // (r2, i3e - i3b, r3) column-major: the owned i3 slice of G3
+  DevBuf<cplx> G4[3];   // (r3, ce - cb): the owned columns of G4
+  // apply workspaces (sized for nrhs_max)
+  DevBuf<cplx> y4;      // [3][r3max * nrhs]  forward: G4 x partial / reduced
+  DevBuf<cplx> Y3;      // [3][r2 * n3loc * nrhs]
+  DevBuf<cplx> Y2;      // [3][r1 * n2 * n3loc * nrhs]   (also W1 in the adjoint)
+  DevBuf<cplx> W2;      // [3][r2 * n3loc * nrhs]
+  DevBuf<cplx> z3;      // [3][r3max * nrhs]
+  int n3loc() const { return i3e - i3b; }
+  int64_t mloc() const { return ce - cb; }
+};
+
+struct Timed {
+  std::string name;
+  cudaEvent_t e0, e1;
+  int64_t bytes, flops;
+};
+
+}  // namespace vsie
+
+struct vsie_coupling_s {
+  vsie::GridDesc grid{};
+  int64_t m = 0;
+  double k0 = 0;
+  double scale_re = 1, scale_im = 0;
+  vsie::Sources sources;
+  vsie::DevBuf<double> d_src;
+  vsie::EntryGeom eg{};
+  int ranks[3][3] = {{0}};
+  bool has_cores = false;
+  vsie::DevBuf<vsie::cplx> G1[3], G2[3];  // replicated on every rank
+  std::vector<vsie::Shard> shards;         // 1 shard (own rank) or `world` (loopback)
+  int rank = 0, world = 1, loopback = 0, device = 0;
+  int nrhs_max = 64;
+  std::unique_ptr<vsie::Comm> comm;
+  vsie::DevBuf<vsie::cplx> partials;
+  vsie::DevBuf<unsigned> counters;
+  vsie::DevBuf<vsie::cplx> zgemm_ws;
+  vsie::DevBuf<vsie::cplx> gather_buf;     // allgather staging of z
+  vsie::DevBuf<vsie::cplx> io_x, io_y;     // apply_host staging
+  vsie::DevBuf<int64_t> io_idx;
+  cudaStream_t io_stream = nullptr;
+  // info
+  int64_t entries_evaluated = 0;
+  int sweeps[3] = {0, 0, 0};
+  double heldout_err[3] = {0, 0, 0};
+  double build_s = 0, build_entry_s = 0, build_factor_s = 0, build_maxvol_s = 0;
+  // timing
+  bool timing = false;
+  std::vector<vsie::Timed> pending;
+  std::vector<vsie::TimerSlot> timers;
+  std::vector<cudaEvent_t> event_pool;
+
+  ~vsie_coupling_s();
+};
+
+namespace vsie {
+
+// setup helpers (capi.cpp / cross.cpp)
+void handle_init_geometry(vsie_coupling_s* h, const vsie_grid* grid, const vsie_mesh* meshes, int n_meshes,
+                          double freq, const vsie_build_opts* opts);
+void handle_partition(vsie_coupling_s* h);
+// installs full cores (host, column-major) for component chi; keeps the owned shards
+void handle_set_cores_host(vsie_coupling_s* h, int chi, const int r[3], const cplx* const host[4]);
+// same from device buffers (full cores on this device)
+void handle_set_cores_device(vsie_coupling_s* h, int chi, const int r[3], const cplx* const dev[4]);
+void handle_alloc_workspace(vsie_coupling_s* h);
+
+void apply(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int nrhs, cudaStream_t st);
+void tt_eval(vsie_coupling_s* h, const int64_t* idx, int64_t count, cplx* out, cudaStream_t st);
+void launch_tt_eval(const cplx* const G[4], const int r[3], const int n[3], int64_t m, int chi_sel,
+                    const int64_t* idx, int64_t count, int64_t nv, cplx* out, cudaStream_t st);
+
+}  // namespace vsie

@@ -1,0 +1,122 @@
+// Launchers of the device kernels (one declaration per hand-written kernel family).
+#pragma once
+
+#include "common.cuh"
+
+namespace vsie {
+
+// ------------------------------------------------------------------ entries (entries.cu)
+struct EntryGeom {
+  int n1, n2, n3;
+  double ox, oy, oz;      // voxel (0,0,0) centre
+  double hx, hy, hz;
+  double dx, dy, dz;      // Gauss offsets h / (2 sqrt 3)
+  double w;               // h1 h2 h3 / 8
+  double k0, inv_k0;
+  double scale_re, scale_im;
+  const double* src;     // [m][36] device
+  int64_t m;
+  int64_t nv;
+};
+
+// out[i] = Z[idx[2i], idx[2i+1]] (explicit list).
+void launch_entries_list(const EntryGeom& g, const int64_t* idx, int64_t count, cplx* out,
+                         cudaStream_t st);
+
+// Structured supercore block:
+//   M[(a, i_k), (i_{k+1}, b)] = A_chi(I_{<=k-1}[a], i_k, i_{k+1}, J_{>k+1}[b]),
+//   rows [row0, row1) of the (rl * nk) x (nk1 * rr) matrix, written column-major
+//   with leading dimension ld (= row1 - row0 by default).
+//   left: int32 [rl][2] device (k=2: i1; k=3: (i1, i2)); right: int32 [rr][2] device
+//   (k=1: (i3, n); k=2: n).
+struct BlockDesc {
+  int chi, k;
+  int64_t rl, nk, nk1, rr;
+  const int32_t* left;
+  const int32_t* right;
+  int64_t row0, row1;
+  int64_t ld;
+};
+void launch_entries_block(const EntryGeom& g, const BlockDesc& b, cplx* out, cudaStream_t st);
+
+// ------------------------------------------------------------------ TT apply (ttapply.cu)
+// y[chi] = alpha * A[chi] x[chi]   (A column-major R x C), deterministic split-K
+struct GemvN {
+  const cplx* A[3];
+  const cplx* x[3];
+  cplx* y[3];
+  int64_t R[3], C[3];
+  int nbatch;
+};
+// y[chi][c] = sum_r A[chi][r + R c] x[chi][r]  (plain transpose); if sum_batch,
+// y[0][c] = sum_chi (...) (the Eq. 18 sum over chi).
+struct GemvT {
+  const cplx* A[3];
+  const cplx* x[3];
+  cplx* y[3];
+  int64_t R[3], C[3];
+  int nbatch;
+  bool sum_batch;
+  bool conj_out;  // store conj(y) (op C post-conjugation)
+};
+
+struct ApplyWorkspace;  // split-K partials + counters (handle-owned)
+
+void launch_gemv_n(const GemvN& a, cplx* partials, unsigned* counters, int max_splits,
+                   cudaStream_t st);
+void launch_gemv_t(const GemvT& a, cplx* partials, unsigned* counters, int max_splits,
+                   cudaStream_t st);
+
+// Expansion y[chi][i1 + n1 c] = sum_a G1[i1 + n1 a] Y2[a + r1 c], c in [0, ncol),
+// with RHS blocks: column c belongs to rhs j = c / cols_per_rhs and is written at
+// y + j * ld_rhs + (c % cols_per_rhs) * n1.
+struct ExpandArgs {
+  const cplx* G1[3];
+  const cplx* Y2[3];
+  cplx* y[3];
+  int n1;
+  int r1[3];
+  int64_t ncol, cols_per_rhs, ld_rhs;
+  int nbatch;
+};
+void launch_expand_g1(const ExpandArgs& a, cudaStream_t st);
+
+// Reduction W1[chi][a + r1 c] = sum_i1 G1[i1 + n1 a] u[chi][i1 + n1 c] (op T), with
+// conj(u) when conj_u (op C pre-conjugation), and the same RHS block addressing
+// for u as ExpandArgs::y.
+struct ReduceArgs {
+  const cplx* G1[3];
+  const cplx* u[3];
+  cplx* W1[3];
+  int n1;
+  int r1[3];
+  int64_t ncol, cols_per_rhs, ld_rhs;
+  int nbatch;
+  bool conj_u;
+};
+void launch_reduce_g1(const ReduceArgs& a, cudaStream_t st);
+
+// ------------------------------------------------------------------ dense complex LA (linalg.cu)
+enum Trans { kN = 0, kT = 1, kC = 2 };
+// C = alpha op(A) op(B) + beta C, column-major; batched over up to 3 problems with
+// individual shapes.  ws/ws_elems: split-K partial workspace (may be null -> no split).
+struct Zgemm {
+  Trans ta = kN, tb = kN;
+  int64_t M[3], N[3], K[3];
+  const cplx* A[3];
+  int64_t lda[3];
+  const cplx* B[3];
+  int64_t ldb[3];
+  cplx* C[3];
+  int64_t ldc[3];
+  cplx alpha = {1, 0}, beta = {0, 0};
+  int nbatch = 1;
+};
+void launch_zgemm(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t st);
+
+// conj in place
+void launch_conj(cplx* x, int64_t n, cudaStream_t st);
+// y[i] += x[i]
+void launch_axpy1(const cplx* x, cplx* y, int64_t n, cudaStream_t st);
+
+}  // namespace vsie

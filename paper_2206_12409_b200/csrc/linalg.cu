@@ -1,0 +1,211 @@
+// Dense complex128 linear algebra used on the hot path: a register-tiled FP64
+// ZGEMM (the G2 contractions of the apply and the sketch / projection products
+// of the TT-cross factorisation) and small elementwise helpers.
+//
+// Tile 64 x 64 x 8, 256 threads, 4 x 4 complex outputs per thread, smem
+// double-buffered through registers; op(A), op(B) in {N, T, C}; batched over up
+// to three problems (the chi components) with individual shapes; deterministic
+// split-K through a partial workspace.
+#include "kernels.cuh"
+
+#include <algorithm>
+
+namespace vsie {
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 8, NT = 256;
+
+template <int TA>
+__device__ __forceinline__ cplx load_a(const cplx* A, int64_t lda, int64_t M, int64_t K, int64_t m, int64_t k) {
+  if (m >= M || k >= K) return cmk(0, 0);
+  if (TA == kN) return __ldg(A + m + lda * k);
+  cplx v = __ldg(A + k + lda * m);
+  if (TA == kC) v.y = -v.y;
+  return v;
+}
+template <int TB>
+__device__ __forceinline__ cplx load_b(const cplx* B, int64_t ldb, int64_t K, int64_t N, int64_t k, int64_t n) {
+  if (k >= K || n >= N) return cmk(0, 0);
+  if (TB == kN) return __ldg(B + k + ldb * n);
+  cplx v = __ldg(B + n + ldb * k);
+  if (TB == kC) v.y = -v.y;
+  return v;
+}
+
+template <int TA, int TB>
+__global__ void __launch_bounds__(NT) k_zgemm(Zgemm g, int splits, cplx* __restrict__ ws, int64_t ws_stride) {
+  const int b = blockIdx.z / splits, sp = blockIdx.z % splits;
+  const int64_t M = g.M[b], N = g.N[b], K = g.K[b];
+  const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+  if (m0 >= M || n0 >= N) return;
+  const int64_t kb0 = ceil_div(K, BK) * sp / splits * BK;
+  const int64_t kb1 = std::min<int64_t>(K, ceil_div(K, BK) * (sp + 1) / splits * BK);
+  const cplx* __restrict__ A = g.A[b];
+  const cplx* __restrict__ B = g.B[b];
+  const int64_t lda = g.lda[b], ldb = g.ldb[b];
+  __shared__ cplx As[2][BK][BM];
+  __shared__ cplx Bs[2][BK][BN];
+  const int t = threadIdx.x;
+  // load mapping
+  int am[2], ak[2], bk[2], bn[2];
+  for (int q = 0; q < 2; ++q) {
+    const int e = t + NT * q;
+    if (TA == kN) { am[q] = e % BM; ak[q] = e / BM; } else { ak[q] = e % BK; am[q] = e / BK; }
+    if (TB == kN) { bk[q] = e % BK; bn[q] = e / BK; } else { bn[q] = e % BN; bk[q] = e / BN; }
+  }
+  cplx ra[2], rb[2];
+  auto fetch = [&](int64_t k0) {
+    for (int q = 0; q < 2; ++q) {
+      ra[q] = load_a<TA>(A, lda, M, kb1, m0 + am[q], k0 + ak[q]);
+      rb[q] = load_b<TB>(B, ldb, kb1, N, k0 + bk[q], n0 + bn[q]);
+    }
+  };
+  auto stash = [&](int buf) {
+    for (int q = 0; q < 2; ++q) {
+      As[buf][ak[q]][am[q]] = ra[q];
+      Bs[buf][bk[q]][bn[q]] = rb[q];
+    }
+  };
+  const int tx = t % 16, ty = t / 16;
+  cplx acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = cmk(0, 0);
+  int buf = 0;
+  if (kb0 < kb1) {
+    fetch(kb0);
+    stash(0);
+    __syncthreads();
+    for (int64_t k0 = kb0; k0 < kb1; k0 += BK) {
+      const bool more = k0 + BK < kb1;
+      if (more) fetch(k0 + BK);
+#pragma unroll
+      for (int kk = 0; kk < BK; ++kk) {
+        cplx av[4], bv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) av[i] = As[buf][kk][tx + 16 * i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bv[j] = Bs[buf][kk][ty + 16 * j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) cfma(acc[i][j], av[i], bv[j]);
+      }
+      if (more) {
+        stash(buf ^ 1);
+        __syncthreads();
+        buf ^= 1;
+      }
+    }
+  }
+  if (splits > 1) {
+    cplx* P = ws + ((int64_t)b * splits + sp) * ws_stride;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t m = m0 + tx + 16 * i, n = n0 + ty + 16 * j;
+        if (m < M && n < N) P[m + M * n] = acc[i][j];
+      }
+    return;
+  }
+  cplx* __restrict__ C = g.C[b];
+  const int64_t ldc = g.ldc[b];
+  const bool has_beta = g.beta.x != 0.0 || g.beta.y != 0.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t m = m0 + tx + 16 * i, n = n0 + ty + 16 * j;
+      if (m < M && n < N) {
+        cplx v = cmul(g.alpha, acc[i][j]);
+        if (has_beta) v = cadd(v, cmul(g.beta, C[m + ldc * n]));
+        C[m + ldc * n] = v;
+      }
+    }
+}
+
+__global__ void k_splitk_reduce(Zgemm g, int splits, const cplx* __restrict__ ws, int64_t ws_stride) {
+  const int b = blockIdx.y;
+  const int64_t M = g.M[b], N = g.N[b];
+  const bool has_beta = g.beta.x != 0.0 || g.beta.y != 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M * N; e += (int64_t)gridDim.x * blockDim.x) {
+    cplx s = cmk(0, 0);
+    for (int q = 0; q < splits; ++q) s = cadd(s, ws[((int64_t)b * splits + q) * ws_stride + e]);
+    const int64_t m = e % M, n = e / M;
+    cplx* c = g.C[b] + m + g.ldc[b] * n;
+    cplx v = cmul(g.alpha, s);
+    if (has_beta) v = cadd(v, cmul(g.beta, *c));
+    *c = v;
+  }
+}
+
+__global__ void k_conj(cplx* x, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i].y = -x[i].y;
+}
+
+__global__ void k_axpy1(const cplx* __restrict__ x, cplx* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = cadd(y[i], x[i]);
+}
+
+template <int TA, int TB>
+void zgemm_t(const Zgemm& g, int splits, dim3 grid, cplx* ws, int64_t stride, cudaStream_t st) {
+  k_zgemm<TA, TB><<<grid, NT, 0, st>>>(g, splits, ws, stride);
+}
+
+}  // namespace
+
+void launch_zgemm(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t st) {
+  int64_t mt = 0, nt = 0, kmax = 0, mn = 0;
+  for (int b = 0; b < g.nbatch; ++b) {
+    mt = std::max(mt, ceil_div(g.M[b], BM));
+    nt = std::max(nt, ceil_div(g.N[b], BN));
+    kmax = std::max(kmax, g.K[b]);
+    mn = std::max(mn, g.M[b] * g.N[b]);
+  }
+  if (mt == 0 || nt == 0) return;
+  int splits = 1;
+  const int64_t tiles = mt * nt * g.nbatch;
+  if (ws != nullptr && tiles < 148 * 2 && kmax >= 8 * BK) {
+    splits = (int)std::min<int64_t>(std::min<int64_t>(148 * 4 / tiles, kmax / (4 * BK)), 64);
+    while (splits > 1 && (int64_t)splits * mn * g.nbatch > ws_elems) --splits;
+    if (splits < 1) splits = 1;
+  }
+  dim3 grid((unsigned)mt, (unsigned)nt, (unsigned)(g.nbatch * splits));
+  const int key = g.ta * 3 + g.tb;
+  switch (key) {
+    case 0: zgemm_t<kN, kN>(g, splits, grid, ws, mn, st); break;
+    case 1: zgemm_t<kN, kT>(g, splits, grid, ws, mn, st); break;
+    case 2: zgemm_t<kN, kC>(g, splits, grid, ws, mn, st); break;
+    case 3: zgemm_t<kT, kN>(g, splits, grid, ws, mn, st); break;
+    case 4: zgemm_t<kT, kT>(g, splits, grid, ws, mn, st); break;
+    case 5: zgemm_t<kT, kC>(g, splits, grid, ws, mn, st); break;
+    case 6: zgemm_t<kC, kN>(g, splits, grid, ws, mn, st); break;
+    case 7: zgemm_t<kC, kT>(g, splits, grid, ws, mn, st); break;
+    default: zgemm_t<kC, kC>(g, splits, grid, ws, mn, st); break;
+  }
+  VSIE_CHECK_LAUNCH();
+  if (splits > 1) {
+    dim3 rg((unsigned)std::min<int64_t>(ceil_div(mn, 256), 148 * 8), g.nbatch);
+    k_splitk_reduce<<<rg, 256, 0, st>>>(g, splits, ws, mn);
+    VSIE_CHECK_LAUNCH();
+  }
+}
+
+void launch_conj(cplx* x, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  k_conj<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 148 * 8), 256, 0, st>>>(x, n);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_axpy1(const cplx* x, cplx* y, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  k_axpy1<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 148 * 8), 256, 0, st>>>(x, y, n);
+  VSIE_CHECK_LAUNCH();
+}
+
+}  // namespace vsie

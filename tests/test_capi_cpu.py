@@ -1,0 +1,83 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol the
+header declares, and validates arguments / geometry on the host before any
+CUDA call (SURVEY §8b error conventions)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import synth
+from paper_2206_12409_b200 import _lib
+from paper_2206_12409_b200.coupling import Grid, _meshes_c, _opts
+
+
+def test_library_exports_every_header_symbol():
+    L = _lib.lib()
+    syms = _lib.header_symbols()
+    assert "vsie_coupling_build" in syms and "vsie_coupling_apply" in syms and "vsie_coupling_entries" in syms
+    for s in syms:
+        assert hasattr(L, s), s
+    assert set(syms) <= set(_lib._SIGS), set(syms) - set(_lib._SIGS)
+    assert L.vsie_abi_version() == 1
+
+
+def test_status_strings_and_defaults():
+    L = _lib.lib()
+    assert L.vsie_status_string(0) == b"VSIE_OK"
+    assert L.vsie_status_string(-2) == b"VSIE_ERR_GEOMETRY"
+    assert L.vsie_status_string(1) == b"VSIE_WARN_NOT_CONVERGED"
+    o = _lib.vsie_build_opts()
+    L.vsie_build_opts_default(C.byref(o))
+    assert (o.max_rank, o.max_sweeps, o.oversample, o.heldout, o.world, o.seed) == (2048, 8, 16, 1000, 1, 12409010)
+    assert (o.scale_re, o.scale_im) == (1.0, 0.0)
+
+
+def _import(grid, meshes, freq=298.2e6, **kw):
+    L = _lib.lib()
+    g = grid.as_c()
+    arr, keep = _meshes_c(meshes)
+    o, _ = _opts(**kw)
+    ranks = (C.c_int32 * 9)(*([1] * 9))
+    dummy = np.zeros(10 ** 6, dtype=np.complex128)
+    ptrs = (C.c_void_p * 12)(*([dummy.ctypes.data] * 12))
+    h = _lib.HANDLE()
+    st = L.vsie_coupling_import_cores(C.byref(g), arr, len(meshes), freq, ranks, ptrs, C.byref(o), C.byref(h))
+    return st, h, L.vsie_last_error_message().decode()
+
+
+def test_argument_errors():
+    cfg = synth.get_config(1)
+    meshes = cfg.meshes()
+    st, h, msg = _import(Grid((0, 12, 12), cfg.h, cfg.origin), meshes)
+    assert st == -1 and not h.value and "n must be" in msg
+    st, h, msg = _import(Grid(cfg.n, (5e-3, -1.0, 5e-3), cfg.origin), meshes)
+    assert st == -1 and not h.value
+    st, h, msg = _import(Grid(cfg.n, cfg.h, cfg.origin), meshes, freq=-1.0)
+    assert st == -1 and "freq" in msg
+    L = _lib.lib()
+    assert L.vsie_coupling_apply(None, None, None, 0, 1, None) == -1
+    assert L.vsie_coupling_info(None, None) == -1
+    L.vsie_coupling_destroy(None)
+
+
+def test_geometry_errors():
+    cfg = synth.get_config(1)
+    grid = Grid(cfg.n, cfg.h, cfg.origin)
+    xyz, tri = cfg.meshes()[0]
+    bad = tri.copy()
+    bad[5] = (bad[5][0], bad[5][0], bad[5][2])          # repeated vertex -> degenerate
+    st, _, msg = _import(grid, [(xyz, bad)])
+    assert st == -2
+    # an edge shared by three triangles (non-manifold)
+    extra = np.vstack([tri, [[tri[0][0], tri[0][2], 7]]]).astype(np.int32)
+    st, _, msg = _import(grid, [(xyz, extra)])
+    assert st == -2 and "more than two" in msg
+    # a surface crossing the voxel box violates the non-singular rule
+    near = xyz * np.array([0.05, 0.05, 1.0])
+    st, _, msg = _import(grid, [(near, tri)])
+    assert st == -2 and "10 max(h)" in msg
+    # vertex id out of range
+    oob = tri.copy()
+    oob[0, 0] = len(xyz) + 3
+    st, _, _ = _import(grid, [(xyz, oob)])
+    assert st == -2

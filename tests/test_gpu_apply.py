@@ -1,0 +1,138 @@
+"""GPU TT apply (forward / transpose / conjugate transpose, single and block
+RHS, loopback slab partition) vs the CPU oracle with identical cores
+(relative L2 <= 1e-12 per chi / per RHS column)."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import ttmv, ttsvd, validate
+
+from gpu_common import grid_of, rand_tts
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def _cuda(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _check_all_ops(h, tts, cfg, nrhs=1, seed=0):
+    nv = cfg.n_v
+    if nrhs == 1:
+        x = synth.complex_gaussian(cfg.m, synth.SEEDS["x"] + seed)
+        u = synth.complex_gaussian(3 * nv, synth.SEEDS["u"] + seed)
+    else:
+        x = synth.complex_gaussian(cfg.m, synth.SEEDS["X"] + seed, ncols=nrhs)
+        u = synth.complex_gaussian(3 * nv, synth.SEEDS["U"] + seed, ncols=nrhs)
+    y = h.apply(_cuda(x), "N").cpu().numpy()
+    yr = ttmv.apply(tts, x, "N")
+    yr2 = yr.reshape(3, nv, -1) if nrhs > 1 else yr.reshape(3, nv)
+    y2 = y.reshape(3, nv, -1) if nrhs > 1 else y.reshape(3, nv)
+    for chi in range(3):                                  # per chi (and per column)
+        if nrhs == 1:
+            assert validate.rel_l2(y2[chi], yr2[chi]) <= TOL
+        else:
+            for j in range(nrhs):
+                assert validate.rel_l2(y2[chi][:, j], yr2[chi][:, j]) <= TOL
+    for op in ("T", "C"):
+        z = h.apply(_cuda(u), op).cpu().numpy()
+        zr = ttmv.apply(tts, u, op)
+        if nrhs == 1:
+            assert validate.rel_l2(z, zr) <= TOL, op
+        else:
+            for j in range(nrhs):
+                assert validate.rel_l2(z[:, j], zr[:, j]) <= TOL, (op, j)
+    return x, u
+
+
+def test_cfg1_ttsvd_cores_vs_oracle_and_dense(dense1, cfg1):
+    from paper_2206_12409_b200 import Coupling
+    tts = [ttsvd.tt_svd(ttmv.tensor_of(dense1, cfg1.n, chi), cfg1.tol) for chi in range(3)]
+    h = Coupling.from_cores(grid_of(cfg1), cfg1.meshes(), cfg1.freq, tts, nrhs_max=8)
+    x, u = _check_all_ops(h, tts, cfg1)
+    # P28: against the dense expansion of the same TT
+    Zt = ttmv.full_matrix(tts)
+    assert validate.rel_l2(h.apply(_cuda(x), "N").cpu().numpy(), Zt @ x) <= TOL
+    assert validate.rel_l2(h.apply(_cuda(u), "T").cpu().numpy(), Zt.T @ u) <= TOL
+    # exported cores are the imported ones, bit for bit
+    ex = h.export_cores()
+    for chi in range(3):
+        for k in range(4):
+            assert np.array_equal(ex[chi][k], tts[chi][k])
+
+
+def test_cfg1_block_rhs_equals_single(dense1, cfg1):
+    from paper_2206_12409_b200 import Coupling
+    import torch
+    tts = [ttsvd.tt_svd(ttmv.tensor_of(dense1, cfg1.n, chi), cfg1.tol) for chi in range(3)]
+    h = Coupling.from_cores(grid_of(cfg1), cfg1.meshes(), cfg1.freq, tts, nrhs_max=8)
+    X, U = _check_all_ops(h, tts, cfg1, nrhs=8, seed=3)
+    Y = h.apply(_cuda(X), "N").cpu().numpy()
+    Z = h.apply(_cuda(U), "T").cpu().numpy()
+    for j in range(8):                                     # P31
+        yj = h.apply(_cuda(X[:, j]), "N").cpu().numpy()
+        zj = h.apply(_cuda(U[:, j]), "T").cpu().numpy()
+        assert validate.rel_l2(Y[:, j], yj) <= 1e-13
+        assert validate.rel_l2(Z[:, j], zj) <= 1e-13
+    # determinism: bitwise identical on repeat
+    assert torch.equal(h.apply(_cuda(X[:, 0]), "N"), h.apply(_cuda(X[:, 0]), "N"))
+
+
+@pytest.mark.parametrize("ci", [2, 4])
+def test_full_size_probe_ranks(ci):
+    """Random cores at the config's probe ranks and full sizes (ragged tiles everywhere)."""
+    from paper_2206_12409_b200 import Coupling
+    cfg = synth.get_config(ci)
+    r = cfg.ranks_probe
+    ranks = [r, (r[0] - 1, r[1] - 3, r[2] + 5), (r[0] + 1, r[1] + 2, r[2] - 7)]
+    tts = rand_tts(cfg, ranks, 40 + ci)
+    h = Coupling.from_cores(grid_of(cfg), cfg.meshes(), cfg.freq, tts, nrhs_max=2)
+    _check_all_ops(h, tts, cfg)
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_loopback_slabs_equal_single(dense1, cfg1, world):
+    """P33 (emulated on one GPU): the i3-slab / G4-column partition with P ranks
+    equals the P = 1 result (the combine order differs only by rounding)."""
+    from paper_2206_12409_b200 import Coupling
+    tts = [ttsvd.tt_svd(ttmv.tensor_of(dense1, cfg1.n, chi), cfg1.tol) for chi in range(3)]
+    h1 = Coupling.from_cores(grid_of(cfg1), cfg1.meshes(), cfg1.freq, tts, nrhs_max=4)
+    hp = Coupling.from_cores(grid_of(cfg1), cfg1.meshes(), cfg1.freq, tts, nrhs_max=4, world=world, loopback=1)
+    inf = hp.info()
+    assert inf["world"] == world and inf["slab"] == (0, cfg1.n[2]) and inf["cols"] == (0, cfg1.m)
+    x = synth.complex_gaussian(cfg1.m, 99)
+    u = synth.complex_gaussian(3 * cfg1.n_v, 98)
+    for op, v in (("N", x), ("T", u), ("C", u)):
+        a = h1.apply(_cuda(v), op).cpu().numpy()
+        b = hp.apply(_cuda(v), op).cpu().numpy()
+        assert validate.rel_l2(b, a) <= 1e-13
+        assert validate.rel_l2(b, ttmv.apply(tts, v, op)) <= TOL
+    X = synth.complex_gaussian(cfg1.m, 97, ncols=4)
+    assert validate.rel_l2(hp.apply(_cuda(X), "N").cpu().numpy(), ttmv.apply(tts, X, "N")) <= TOL
+
+
+def test_apply_host_matches_device(dense1, cfg1):
+    from paper_2206_12409_b200 import Coupling
+    tts = [ttsvd.tt_svd(ttmv.tensor_of(dense1, cfg1.n, chi), cfg1.tol) for chi in range(3)]
+    h = Coupling.from_cores(grid_of(cfg1), cfg1.meshes(), cfg1.freq, tts, nrhs_max=4)
+    x = synth.complex_gaussian(cfg1.m, 5)
+    u = synth.complex_gaussian(3 * cfg1.n_v, 6)
+    assert np.array_equal(h.apply_host(x, "N"), h.apply(_cuda(x), "N").cpu().numpy())
+    assert np.array_equal(h.apply_host(u, "C"), h.apply(_cuda(u), "C").cpu().numpy())
+    assert np.all(h.apply_host(np.zeros(cfg1.m, complex), "N") == 0)   # P30
+
+
+def test_tt_eval_matches_oracle(cfg1):
+    from paper_2206_12409_b200 import Coupling
+    import torch
+    tts = rand_tts(cfg1, [(3, 5, 7), (2, 4, 6), (4, 4, 4)], 77)
+    h = Coupling.from_cores(grid_of(cfg1), cfg1.meshes(), cfg1.freq, tts, nrhs_max=1)
+    idx = synth.uniform_indices(tuple(cfg1.n) + (cfg1.m,), 500, 5)
+    for chi in range(3):
+        v = idx[:, 0] + cfg1.n[0] * (idx[:, 1] + cfg1.n[1] * idx[:, 2])
+        got = h.tt_eval(torch.from_numpy(chi * cfg1.n_v + v), torch.from_numpy(idx[:, 3])).cpu().numpy()
+        ref = ttmv.eval_at(tts[chi], idx)
+        assert validate.rel_l2(got, ref) <= 1e-13
