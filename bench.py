@@ -1,0 +1,376 @@
+"""Benchmark of the Z_bc hot path (BASELINE.json metric):
+  "Z_bc TT matvec+adjoint ms & HBM GB/s per GMRES step; Z_bc entries/sec (FP64)".
+
+One step = one GMRES iteration's use of the block: a forward apply y = Z x
+(Eq. 17) plus a transpose apply z = Z^T u (Eqs. 18-19) through the C
+ABI, on TT cores built by vsie_coupling_build (TT-cross) for
+BASELINE config 2 (head 2 mm: 100x120x110 voxels, shield 10080 RWG, tol 1e-6).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
+
+N > 1 runs under torchrun, one process per GPU: the voxel grid is slab-sharded
+along i3 and G4 along its columns (SURVEY §8e design iii); partials are
+combined with NCCL inside the library (strong scaling: fixed total work).
+Rank 0 prints ONE JSON line.  --impl reference times the CPU oracle (NumPy) on
+the host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "Z_bc TT matvec+adjoint ms & HBM GB/s per GMRES step; Z_bc entries/sec (FP64)"
+
+
+def step_bytes_flops(n, m, ranks):
+    """B_fwd = 16 [sum_chi (n1 r1 + r1 n2 r2 + r2 n3 r3 + r3 m) + m + 3 n_v], B_adj = B_fwd;
+    F = 8 sum_chi (r3 m + r2 n3 r3 + r1 n2 r2 n3 + n_v r1) per direction."""
+    n1, n2, n3 = n
+    nv = n1 * n2 * n3
+    cores = sum(n1 * r1 + r1 * n2 * r2 + r2 * n3 * r3 + r3 * m for (r1, r2, r3) in ranks)
+    b_fwd = 16 * (cores + m + 3 * nv)
+    f_fwd = 8 * sum(r3 * m + r2 * n3 * r3 + r1 * n2 * r2 * n3 + nv * r1 for (r1, r2, r3) in ranks)
+    return 2 * b_fwd, 2 * f_fwd
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.p is not None:
+            time.sleep(0.25)
+            self.p.terminate()
+            try:
+                out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], None, set()
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for k, nm in enumerate(names):
+                if f[3 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_step_rate(cfg, ranks, steps=2, seed=5):
+    """The CPU oracle (oracle/ttmv.py, as it stands) timed on the host cores on the
+    same workload: random cores with the GPU build's ranks (matvec cost does not
+    depend on the core values)."""
+    from oracle import ttmv
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from gpu_common import rand_tts
+    tts = rand_tts(cfg, ranks, seed)
+    x = synth.complex_gaussian(cfg.m, synth.SEEDS["x"])
+    u = synth.complex_gaussian(3 * cfg.n_v, synth.SEEDS["u"])
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        ttmv.apply(tts, x, "N")
+        ttmv.apply(tts, u, "T")
+        ts.append(time.perf_counter() - t0)
+    return statistics.median(ts), ts
+
+
+def oracle_entry_rate(cfg, count=20000):
+    from oracle import entries as oent
+    prob = oent.problem_from_config(cfg)
+    idx = synth.uniform_indices((3 * cfg.n_v, cfg.m), count, 777)
+    t0 = time.perf_counter()
+    oent.entries(prob, idx[:, 0], idx[:, 1])
+    return count / (time.perf_counter() - t0)
+
+
+def ranks_hint(cfg):
+    """Ranks of the last GPU build of this config (committed under profiles/), else the probe ranks."""
+    p = os.path.join(ROOT, "profiles", f"ranks_cfg{cfg.idx}.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return [tuple(r) for r in json.load(f)["ranks"]]
+    return [tuple(cfg.ranks_probe)] * 3
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = synth.get_config(args.config)
+    ranks = ranks_hint(cfg)
+    B, F = step_bytes_flops(cfg.n, cfg.m, ranks)
+    from threadpoolctl import threadpool_info
+    for _ in range(max(0, min(args.warmup, 1))):
+        oracle_step_rate(cfg, ranks, steps=1)
+    t, ts = oracle_step_rate(cfg, ranks, steps=args.steps)
+    cores = cpu_cores()
+    blas = [d.get("num_threads") for d in threadpool_info()]
+    val = B / t / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "GB/s", "n_gpus": 0, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": f"cfg{cfg.idx} {cfg.name}", "grid": list(cfg.n), "m": cfg.m, "tol": cfg.tol,
+                   "ranks": ranks, "step": "TT forward + transpose apply (oracle/ttmv.py, NumPy einsum)"},
+        "cpu_baseline": {"value": val, "unit": "GB/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{args.steps} full GMRES steps of cfg{cfg.idx} with random cores at the GPU ranks",
+                         "blas_threads": blas},
+        "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2206_12409_b200 import Coupling, grid_of, nccl_unique_id
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus or world == 1, "launch N > 1 with torchrun --nproc-per-node N"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    uid = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    cfg = synth.get_config(args.config)
+    t0 = time.perf_counter()
+    h = Coupling.build(grid_of(cfg), cfg.meshes(), cfg.freq, cfg.tol, nrhs_max=1, rank=rank, world=world,
+                       nccl_unique_id=uid, device=local)
+    build_s = time.perf_counter() - t0
+    inf = h.info()
+    ranks = inf["ranks"]
+    if rank == 0:
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    B, F = step_bytes_flops(cfg.n, cfg.m, ranks)
+    n1, n2, n3 = cfg.n
+    n3loc = inf["slab"][1] - inf["slab"][0]
+    vox_loc = 3 * n1 * n2 * n3loc
+    x = torch.from_numpy(synth.complex_gaussian(cfg.m, synth.SEEDS["x"])).to(dev)
+    u_full = synth.complex_gaussian(3 * cfg.n_v, synth.SEEDS["u"]).reshape(3, -1)
+    u_np = np.ascontiguousarray(u_full[:, n1 * n2 * inf["slab"][0]:n1 * n2 * inf["slab"][1]].reshape(-1))
+    u = torch.from_numpy(u_np).to(dev)
+    y = torch.empty(vox_loc, dtype=torch.complex128, device=dev)
+    z = torch.empty(cfg.m, dtype=torch.complex128, device=dev)
+    flush = torch.empty(512 * 2 ** 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def step():
+        h.apply_raw(x.data_ptr(), y.data_ptr(), "N", 1, stream)
+        h.apply_raw(u.data_ptr(), z.data_ptr(), "T", 1, stream)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = h.info()["apply_launches"]
+    h.set_timing(True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)                     # evict L2 between timed steps
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = h.info()["apply_launches"] - launches0
+    timers = h.timers()
+    h.set_timing(False)
+    per = [a.elapsed_time(b) for a, b in ev]
+    ms = float(np.mean(per))
+    if world > 1:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    value = B / (ms * 1e-3) / 1e9
+
+    # ---- end to end: host buffers through the C ABI (H2D + apply + D2H inside)
+    xh = torch.from_numpy(synth.complex_gaussian(cfg.m, synth.SEEDS["x"])).pin_memory()
+    uh = torch.from_numpy(u_np).pin_memory()
+    yh = torch.empty(vox_loc, dtype=torch.complex128).pin_memory()
+    zh = torch.empty(cfg.m, dtype=torch.complex128).pin_memory()
+    for _ in range(2):
+        h.apply_host_raw(xh.data_ptr(), yh.data_ptr(), "N", 1)
+        h.apply_host_raw(uh.data_ptr(), zh.data_ptr(), "T", 1)
+    e2e = []
+    for _ in range(max(3, min(args.steps, 20))):
+        if world > 1:
+            dist.barrier()
+        t1 = time.perf_counter()
+        h.apply_host_raw(xh.data_ptr(), yh.data_ptr(), "N", 1)
+        h.apply_host_raw(uh.data_ptr(), zh.data_ptr(), "T", 1)
+        e2e.append(time.perf_counter() - t1)
+    e2e_s = float(np.mean(e2e))
+    if world > 1:
+        tt = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+
+    # ---- entries/s (FP64): 1e6 uniform random (row, col) through vsie_coupling_entries
+    ne = 1_000_000
+    idx = synth.uniform_indices((3 * cfg.n_v, cfg.m), ne, 424242)
+    rows_t = torch.from_numpy(idx[:, 0]).to(dev)
+    cols_t = torch.from_numpy(idx[:, 1]).to(dev)
+    h.entries(rows_t, cols_t)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        h.entries(rows_t, cols_t)
+    e1.record()
+    torch.cuda.synchronize()
+    ent_s = ne * 5 / (e0.elapsed_time(e1) * 1e-3)
+
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel (largest share of the step)
+    peak, peak_kind = load_peaks()
+    kern = [t for t in timers if t["bytes_per_launch"] > 0 and t["launches"] > 0]
+    dom = max(kern, key=lambda t: t["total_ms"]) if kern else None
+    roof = None
+    if dom:
+        avg_ms = dom["total_ms"] / dom["launches"]
+        ach = dom["bytes_per_launch"] / (avg_ms * 1e-3) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f).get(dom["name"])
+        roof = {"bound": "hbm", "kernel": dom["name"], "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "traffic": traffic, "peak_source": peak_kind,
+                "share_of_step": dom["total_ms"] / max(1e-9, sum(t["total_ms"] for t in timers)),
+                "bytes_per_launch": dom["bytes_per_launch"], "avg_us": avg_ms * 1e3}
+    kern_table = {t["name"]: {"avg_us": 1e3 * t["total_ms"] / max(1, t["launches"]),
+                              "gbs": (t["bytes_per_launch"] / (t["total_ms"] / t["launches"] * 1e-3) / 1e9)
+                              if t["bytes_per_launch"] else None} for t in timers}
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        t_cpu, ts = oracle_step_rate(cfg, ranks, steps=2)
+        cpu = {"value": B / t_cpu / 1e9, "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
+               "sample": "2 full GMRES steps (oracle TT fwd + transpose, NumPy) of the same cfg and ranks, "
+                         "random cores", "ms_per_step": t_cpu * 1e3,
+               "entries_per_s": oracle_entry_rate(cfg)}
+    h2d = 16 * (cfg.m + vox_loc)
+    d2h = 16 * (vox_loc + cfg.m)
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": f"cfg{cfg.idx} {cfg.name}: grid {cfg.n}, h {cfg.h[0]*1e3:.0f} mm, m={cfg.m} RWG "
+                               f"(shield {cfg.surfaces[0].n_az}x{cfg.surfaces[0].n_ax}), f=298.2 MHz, tol {cfg.tol}",
+                   "step": "1 forward (y = Z x) + 1 transpose (z = Z^T u) TT apply", "ranks": ranks,
+                   "parallelism": f"slab{world} (i3 planes + G4 columns, NCCL)" if world > 1 else "1 GPU",
+                   "l2": "flushed between timed steps (512 MiB write)",
+                   "bytes_per_step": B, "flops_per_step": F, "build_s": build_s,
+                   "build_breakdown_s": {"entries": inf["build_entry_s"], "factor": inf["build_factor_s"],
+                                         "maxvol": inf["build_maxvol_s"]},
+                   "heldout_err": inf["heldout_err"], "sweeps": inf["sweeps"],
+                   "compression": float(inf["compression"]) if inf["compression"] else None},
+        "entries": {"value": ent_s, "unit": "entries/s", "pair_interactions_per_s": 48 * ent_s,
+                    "sample": "1e6 uniform random (row, col), 5 reps"},
+        "roofline": roof,
+        "kernels": kern_table,
+        "cpu_baseline": cpu,
+        "e2e": {"value": B / e2e_s / 1e9, "unit": "GB/s", "ms_per_step": e2e_s * 1e3,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line))
+    with open(os.path.join(ROOT, "gpurun_out", f"bench_cfg{cfg.idx}_n{world}.json"), "w") as f:
+        json.dump(line, f, indent=1)
+    with open(os.path.join(ROOT, "gpurun_out", f"ranks_cfg{cfg.idx}.json"), "w") as f:
+        json.dump({"ranks": ranks, "source": "vsie_coupling_build on B200"}, f)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

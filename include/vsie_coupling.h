@@ -118,6 +118,8 @@ typedef struct {
   int64_t cols[2];              /* this rank's owned G4 columns [cols0, cols1)                */
   int32_t world, rank, loopback;
   double k0;
+  int64_t apply_launches;       /* kernel launches made by vsie_coupling_apply* so far (this handle) */
+  int64_t apply_calls;
 } vsie_info;
 
 /* Per-kernel device timing of apply calls (opt-in, see vsie_coupling_set_timing). */

@@ -40,7 +40,8 @@ class vsie_info(C.Structure):
                 ("entries_evaluated", C.c_int64), ("sweeps", C.c_int32 * 3), ("heldout_err", C.c_double * 3),
                 ("build_s", C.c_double), ("build_entry_s", C.c_double), ("build_factor_s", C.c_double),
                 ("build_maxvol_s", C.c_double), ("slab", C.c_int32 * 2), ("cols", C.c_int64 * 2),
-                ("world", C.c_int32), ("rank", C.c_int32), ("loopback", C.c_int32), ("k0", C.c_double)]
+                ("world", C.c_int32), ("rank", C.c_int32), ("loopback", C.c_int32), ("k0", C.c_double),
+                ("apply_launches", C.c_int64), ("apply_calls", C.c_int64)]
 
 
 class vsie_timer(C.Structure):

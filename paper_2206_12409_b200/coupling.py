@@ -149,7 +149,8 @@ class Coupling:
             entries_evaluated=i.entries_evaluated, sweeps=tuple(i.sweeps), heldout_err=tuple(i.heldout_err),
             build_s=i.build_s, build_entry_s=i.build_entry_s, build_factor_s=i.build_factor_s,
             build_maxvol_s=i.build_maxvol_s, slab=tuple(i.slab), cols=tuple(i.cols), world=i.world,
-            rank=i.rank, loopback=i.loopback, k0=i.k0)
+            rank=i.rank, loopback=i.loopback, k0=i.k0, apply_launches=i.apply_launches,
+            apply_calls=i.apply_calls)
 
     @property
     def m(self):

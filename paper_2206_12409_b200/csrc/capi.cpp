@@ -265,6 +265,8 @@ int32_t vsie_coupling_info(vsie_coupling_t h, vsie_info* out) {
     out->rank = h->rank;
     out->loopback = h->loopback;
     out->k0 = h->k0;
+    out->apply_launches = h->apply_launches;
+    out->apply_calls = h->apply_calls;
     return VSIE_OK;
   });
 }

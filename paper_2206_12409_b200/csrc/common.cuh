@@ -29,7 +29,7 @@ struct Error : public std::runtime_error {
     }                                                                                          \
   } while (0)
 
-#define VSIE_CHECK_LAUNCH() VSIE_CHECK_CUDA(cudaGetLastError())
+#define VSIE_CHECK_LAUNCH() do { VSIE_COUNT_LAUNCH(); VSIE_CHECK_CUDA(cudaGetLastError()); } while (0)
 
 #define VSIE_REQUIRE(cond, code, msg)                                 \
   do {                                                                \
@@ -88,6 +88,12 @@ struct DevBuf {
   }
   size_t bytes() const { return n * sizeof(T); }
 };
+
+// ----------------------------------------------------------------- launch accounting
+// Every launcher of this library increments this counter (one per kernel launch);
+// the handle reports the delta over its apply calls (vsie_info.apply_launches).
+int64_t& launch_counter();
+#define VSIE_COUNT_LAUNCH() (++::vsie::launch_counter())
 
 // ----------------------------------------------------------------- per-kernel timing
 struct TimerSlot {

@@ -1,0 +1,487 @@
+// Device kernels of the TT-cross driver (see crosskern.cuh).
+//
+// * one-sided Jacobi SVD (Hestenes): each launch performs one round of the
+//   round-robin ordering, one CTA per column pair, complex rotation
+//     a_i' = cs a_i - sn e^{-i phi} a_j,   a_j' = sn a_i + cs e^{-i phi} a_j,
+//   with c = a_i^H a_j = |c| e^{i phi}, zeta = (|a_j|^2 - |a_i|^2) / (2|c|),
+//   t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), cs = 1/sqrt(1 + t^2), sn = cs t;
+// * maxvol: LU with partial pivoting for the initial rows,
+//   B = A A[I]^{-1} = P^T [I; L2 L1^{-1}], then rank-1 updates
+//   B <- B - B[:, j*] (B[i*, :] - e_j*^T) / B[i*, j*] while max |B| > 1 + tau,
+//   ties broken towards the smallest (original row, column) as in the oracle.
+#include "crosskern.cuh"
+
+#include <algorithm>
+
+namespace vsie {
+
+namespace {
+
+constexpr int NT = 256;
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_gaussian(cplx* out, int64_t n, uint64_t seed) {
+  const uint64_t s = splitmix64(seed);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t a = splitmix64(s ^ (2 * (uint64_t)e)), b = splitmix64(s ^ (2 * (uint64_t)e + 1));
+    const double u1 = ((a >> 11) + 1) * 0x1.0p-53;  // (0, 1]
+    const double u2 = (b >> 11) * 0x1.0p-53;        // [0, 1)
+    const double rr = sqrt(-2.0 * log(u1)) * 0.70710678118654752440;
+    double sn, cs;
+    sincospi(2.0 * u2, &sn, &cs);
+    out[e] = cmk(rr * cs, rr * sn);
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void block_sum(double (&v)[N], double* sh /* >= 8 * N */) {
+#pragma unroll
+  for (int k = 0; k < N; ++k)
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0)
+#pragma unroll
+    for (int k = 0; k < N; ++k) sh[w * N + k] = v[k];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    double s = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) s += sh[q * N + k];
+    v[k] = s;
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_jacobi_round(cplx* A, int64_t p, int64_t lda, cplx* V, int64_t q,
+                                                     const int2* pairs, double thr, unsigned* cnt) {
+  const int2 pr = pairs[blockIdx.x];
+  const int i = pr.x, j = pr.y;
+  if (i >= q || j >= q) return;
+  cplx* Ai = A + lda * i;
+  cplx* Aj = A + lda * j;
+  double v[4] = {0, 0, 0, 0};
+  for (int64_t r = threadIdx.x; r < p; r += NT) {
+    const cplx x = Ai[r], y = Aj[r];
+    v[0] += x.x * x.x + x.y * x.y;
+    v[1] += y.x * y.x + y.y * y.y;
+    v[2] += x.x * y.x + x.y * y.y;  // Re(conj(x) y)
+    v[3] += x.x * y.y - x.y * y.x;  // Im(conj(x) y)
+  }
+  __shared__ double sh[8 * 4];
+  block_sum<4>(v, sh);
+  const double a = v[0], b = v[1];
+  const double cabs = sqrt(v[2] * v[2] + v[3] * v[3]);
+  if (!(a > 0 && b > 0) || !(cabs > thr * sqrt(a) * sqrt(b))) return;
+  const double zeta = (b - a) / (2.0 * cabs);
+  const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+  const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+  const cplx ph = cmk(v[2] / cabs, -v[3] / cabs);  // e^{-i phi}
+  const cplx snph = cmk(sn * ph.x, sn * ph.y), csph = cmk(cs * ph.x, cs * ph.y);
+  for (int64_t r = threadIdx.x; r < p; r += NT) {
+    const cplx x = Ai[r], y = Aj[r];
+    const cplx py = cmul(snph, y), qy = cmul(csph, y);
+    Ai[r] = cmk(cs * x.x - py.x, cs * x.y - py.y);
+    Aj[r] = cmk(sn * x.x + qy.x, sn * x.y + qy.y);
+  }
+  if (V) {
+    cplx* Vi = V + q * i;
+    cplx* Vj = V + q * j;
+    for (int64_t r = threadIdx.x; r < q; r += NT) {
+      const cplx x = Vi[r], y = Vj[r];
+      const cplx py = cmul(snph, y), qy = cmul(csph, y);
+      Vi[r] = cmk(cs * x.x - py.x, cs * x.y - py.y);
+      Vj[r] = cmk(sn * x.x + qy.x, sn * x.y + qy.y);
+    }
+  }
+  if (threadIdx.x == 0) atomicAdd(cnt, 1u);
+}
+
+__global__ void __launch_bounds__(NT) k_col_norms(const cplx* A, int64_t p, int64_t lda, double* out) {
+  const cplx* a = A + lda * blockIdx.x;
+  double v[1] = {0};
+  for (int64_t r = threadIdx.x; r < p; r += NT) v[0] += cabs2(a[r]);
+  __shared__ double sh[8];
+  block_sum<1>(v, sh);
+  if (threadIdx.x == 0) out[blockIdx.x] = sqrt(v[0]);
+}
+
+__global__ void __launch_bounds__(NT) k_frob_partial(const cplx* A, int64_t n, double* partial) {
+  double v[1] = {0};
+  for (int64_t e = blockIdx.x * (int64_t)NT + threadIdx.x; e < n; e += (int64_t)gridDim.x * NT) v[0] += cabs2(A[e]);
+  __shared__ double sh[8];
+  block_sum<1>(v, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = v[0];
+}
+__global__ void k_frob_final(const double* partial, int np, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0;
+    for (int i = 0; i < np; ++i) s += partial[i];
+    *out = s;
+  }
+}
+
+__global__ void k_gather_cols(const cplx* src, int64_t rows, int64_t lds, const int* idx, const double* scale,
+                              int ncols, cplx* dst, int64_t ldd, int conj) {
+  const int j = blockIdx.y;
+  const cplx* s = src + lds * idx[j];
+  const double f = scale ? scale[j] : 1.0;
+  for (int64_t r = blockIdx.x * (int64_t)NT + threadIdx.x; r < rows; r += (int64_t)gridDim.x * NT) {
+    cplx v = s[r];
+    dst[r + ldd * j] = cmk(f * v.x, conj ? -f * v.y : f * v.y);
+  }
+}
+
+__global__ void k_gather_rows(const cplx* src, int64_t lds, const int* idx, int nr, int64_t cols, cplx* dst) {
+  const int64_t total = (int64_t)nr * cols;
+  for (int64_t e = blockIdx.x * (int64_t)NT + threadIdx.x; e < total; e += (int64_t)gridDim.x * NT) {
+    const int64_t i = e % nr, c = e / nr;
+    dst[e] = src[idx[i] + lds * c];
+  }
+}
+
+__global__ void k_transpose(const cplx* src, int64_t R, int64_t C, cplx* dst, int conj) {
+  __shared__ cplx tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 256 threads: 8 rows per pass
+  for (int k = ty; k < 32; k += 8) {
+    const int64_t r = r0 + tx, c = c0 + k;
+    if (r < R && c < C) tile[k][tx] = src[r + R * c];
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    const int64_t c = c0 + tx, r = r0 + k;
+    if (r < R && c < C) {
+      cplx v = tile[tx][k];
+      if (conj) v.y = -v.y;
+      dst[c + C * r] = v;
+    }
+  }
+}
+
+// ----------------------------------------------------------------------- argmax helpers
+__device__ __forceinline__ bool better(double v, int64_t key, double bv, int64_t bkey) {
+  return v > bv || (v == bv && key < bkey);
+}
+
+__device__ void block_argmax(ArgMax& m, ArgMax* sh /* >= 8 */) {
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v = __shfl_xor_sync(0xffffffffu, m.v, o);
+    const long long key = __shfl_xor_sync(0xffffffffu, (long long)m.key, o);
+    const long long i = __shfl_xor_sync(0xffffffffu, (long long)m.i, o);
+    const int c = __shfl_xor_sync(0xffffffffu, m.c, o);
+    if (better(v, key, m.v, m.key)) { m.v = v; m.key = key; m.i = i; m.c = c; }
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < (int)(blockDim.x >> 5); ++q)
+      if (better(sh[q].v, sh[q].key, sh[0].v, sh[0].key)) sh[0] = sh[q];
+  }
+  __syncthreads();
+  m = sh[0];
+}
+
+__global__ void __launch_bounds__(NT) k_lu_update(cplx* W, int64_t n, int r, int j, ArgMax* partials) {
+  extern __shared__ cplx urow[];
+  __shared__ cplx inv;
+  __shared__ ArgMax sh[8];
+  if (j >= 0) {
+    for (int c = j + 1 + threadIdx.x; c < r; c += NT) urow[c] = W[j + n * c];
+    if (threadIdx.x == 0) {
+      const cplx pv = W[j + n * j];
+      const double d = cabs2(pv);
+      inv = cmk(pv.x / d, -pv.y / d);
+    }
+    __syncthreads();
+  }
+  ArgMax best{-1.0, INT64_MAX, -1, j + 1};
+  for (int64_t i = j + 1 + blockIdx.x * (int64_t)NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NT) {
+    if (j >= 0) {
+      const cplx l = cmul(W[i + n * j], inv);
+      W[i + n * j] = l;
+      for (int c = j + 1; c < r; ++c) {
+        const cplx u = urow[c];
+        cplx w = W[i + n * c];
+        w.x -= l.x * u.x - l.y * u.y;
+        w.y -= l.x * u.y + l.y * u.x;
+        W[i + n * c] = w;
+      }
+    }
+    if (j + 1 < r) {
+      const double v = cabs2(W[i + n * (j + 1)]);
+      if (better(v, i, best.v, best.key)) { best.v = v; best.key = i; best.i = i; }
+    }
+  }
+  block_argmax(best, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = best;
+}
+
+__global__ void __launch_bounds__(NT) k_lu_pivot(cplx* W, int64_t n, int r, int j, int* perm, const ArgMax* partials,
+                                                 int nparts, int* bad) {
+  __shared__ ArgMax sh[8];
+  ArgMax best{-1.0, INT64_MAX, -1, j};
+  for (int q = threadIdx.x; q < nparts; q += NT)
+    if (better(partials[q].v, partials[q].key, best.v, best.key)) best = partials[q];
+  block_argmax(best, sh);
+  const int64_t p = best.i;
+  if (best.v <= 0.0 || p < 0) {
+    if (threadIdx.x == 0) *bad = 1;
+    return;
+  }
+  if (p != j) {
+    for (int c = threadIdx.x; c < r; c += NT) {
+      const cplx t = W[j + n * c];
+      W[j + n * c] = W[p + n * c];
+      W[p + n * c] = t;
+    }
+    if (threadIdx.x == 0) {
+      const int t = perm[j];
+      perm[j] = perm[p];
+      perm[p] = t;
+    }
+  }
+}
+
+__global__ void k_copy_lower(const cplx* W, int64_t n, int r, cplx* Lr) {
+  const int64_t total = (int64_t)r * r;
+  for (int64_t e = blockIdx.x * (int64_t)NT + threadIdx.x; e < total; e += (int64_t)gridDim.x * NT) {
+    const int64_t i = e / r, k = e % r;
+    Lr[e] = k < i ? W[i + n * k] : cmk(0, 0);
+  }
+}
+
+__global__ void __launch_bounds__(128) k_unit_lower_inverse(const cplx* Lr, int r, cplx* T) {
+  extern __shared__ cplx tcol[];
+  __shared__ double sh[8 * 2];
+  const int c = blockIdx.x;
+  for (int k = threadIdx.x; k < r; k += blockDim.x) tcol[k] = cmk(k == c ? 1.0 : 0.0, 0.0);
+  __syncthreads();
+  for (int i = c + 1; i < r; ++i) {
+    double v[2] = {0, 0};
+    const cplx* row = Lr + (int64_t)i * r;
+    for (int k = c + threadIdx.x; k < i; k += blockDim.x) {
+      const cplx l = row[k], t = tcol[k];
+      v[0] += l.x * t.x - l.y * t.y;
+      v[1] += l.x * t.y + l.y * t.x;
+    }
+    block_sum<2>(v, sh);
+    if (threadIdx.x == 0) tcol[i] = cmk(-v[0], -v[1]);
+    __syncthreads();
+  }
+  for (int k = threadIdx.x; k < r; k += blockDim.x) T[k + (int64_t)r * c] = tcol[k];
+}
+
+__global__ void k_set_identity_top(cplx* B, int64_t n, int r) {
+  const int64_t total = (int64_t)r * r;
+  for (int64_t e = blockIdx.x * (int64_t)NT + threadIdx.x; e < total; e += (int64_t)gridDim.x * NT) {
+    const int64_t i = e % r, c = e / r;
+    B[i + n * c] = cmk(i == c ? 1.0 : 0.0, 0.0);
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_maxvol_update(cplx* B, int64_t n, int r, const int* perm, const cplx* rowbuf,
+                                                      const MaxvolState* st, int update, ArgMax* partials) {
+  extern __shared__ cplx rb[];
+  __shared__ ArgMax sh[8];
+  __shared__ int s_done, s_istar, s_cstar;
+  __shared__ cplx s_inv;
+  if (threadIdx.x == 0) {
+    s_done = update ? st->done : 0;
+    s_istar = st->i_star;
+    s_cstar = st->c_star;
+    const cplx pv = st->piv;
+    const double d = cabs2(pv);
+    s_inv = d > 0 ? cmk(pv.x / d, -pv.y / d) : cmk(0, 0);
+  }
+  __syncthreads();
+  if (s_done) return;
+  if (update)
+    for (int c = threadIdx.x; c < r; c += NT) rb[c] = rowbuf[c];
+  __syncthreads();
+  const int cs = s_cstar;
+  ArgMax best{-1.0, INT64_MAX, -1, 0};
+  for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NT) {
+    const int64_t key0 = (int64_t)perm[i] * r;
+    if (update) {
+      if (i == s_istar) {
+        for (int c = 0; c < r; ++c) B[i + n * c] = cmk(c == cs ? 1.0 : 0.0, 0.0);
+        if (better(1.0, key0 + cs, best.v, best.key)) { best.v = 1.0; best.key = key0 + cs; best.i = i; best.c = cs; }
+        continue;
+      }
+      const cplx f = cmul(B[i + n * cs], s_inv);
+      for (int c = 0; c < r; ++c) {
+        const cplx u = rb[c];
+        cplx w = B[i + n * c];
+        w.x -= f.x * u.x - f.y * u.y;
+        w.y -= f.x * u.y + f.y * u.x;
+        B[i + n * c] = w;
+        const double v = cabs2(w);
+        if (better(v, key0 + c, best.v, best.key)) { best.v = v; best.key = key0 + c; best.i = i; best.c = c; }
+      }
+    } else {
+      for (int c = 0; c < r; ++c) {
+        const double v = cabs2(B[i + n * c]);
+        if (better(v, key0 + c, best.v, best.key)) { best.v = v; best.key = key0 + c; best.i = i; best.c = c; }
+      }
+    }
+  }
+  block_argmax(best, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = best;
+}
+
+__global__ void __launch_bounds__(NT) k_maxvol_select(cplx* B, int64_t n, int r, const ArgMax* partials, int nparts,
+                                                      double tau, int* piv_pos, cplx* rowbuf, MaxvolState* st) {
+  __shared__ ArgMax sh[8];
+  __shared__ int s_done;
+  if (threadIdx.x == 0) s_done = st->done;
+  __syncthreads();
+  if (s_done) return;
+  ArgMax best{-1.0, INT64_MAX, -1, 0};
+  for (int q = threadIdx.x; q < nparts; q += NT)
+    if (better(partials[q].v, partials[q].key, best.v, best.key)) best = partials[q];
+  block_argmax(best, sh);
+  const double m = sqrt(best.v);
+  if (m <= 1.0 + tau || best.i < 0) {
+    if (threadIdx.x == 0) {
+      st->done = 1;
+      st->maxabs = m;
+    }
+    return;
+  }
+  const int64_t i = best.i;
+  const int c = best.c;
+  for (int cc = threadIdx.x; cc < r; cc += NT) {
+    cplx v = B[i + n * cc];
+    if (cc == c) v.x -= 1.0;
+    rowbuf[cc] = v;
+  }
+  if (threadIdx.x == 0) {
+    st->i_star = (int)i;
+    st->c_star = c;
+    st->piv = B[i + n * c];
+    st->maxabs = m;
+    st->swaps += 1;
+    piv_pos[c] = (int)i;
+  }
+}
+
+__global__ void k_scatter_rows(const cplx* B, int64_t n, int r, const int* perm, cplx* Bout) {
+  const int64_t total = n * r;
+  for (int64_t e = blockIdx.x * (int64_t)NT + threadIdx.x; e < total; e += (int64_t)gridDim.x * NT) {
+    const int64_t i = e % n, c = e / n;
+    Bout[perm[i] + n * c] = B[e];
+  }
+}
+
+unsigned grid1(int64_t work) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, NT), 148 * 16)); }
+
+}  // namespace
+
+void launch_gaussian(cplx* out, int64_t n, uint64_t seed, cudaStream_t st) {
+  if (n <= 0) return;
+  k_gaussian<<<grid1(n), NT, 0, st>>>(out, n, seed);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_jacobi_round(cplx* A, int64_t p, int64_t lda, cplx* V, int64_t q, const int2* pairs, int npairs,
+                         double thr, unsigned* cnt, cudaStream_t st) {
+  k_jacobi_round<<<npairs, NT, 0, st>>>(A, p, lda, V, q, pairs, thr, cnt);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_col_norms(const cplx* A, int64_t p, int64_t q, int64_t lda, double* out, cudaStream_t st) {
+  if (q <= 0) return;
+  k_col_norms<<<(unsigned)q, NT, 0, st>>>(A, p, lda, out);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_frob2(const cplx* A, int64_t n, double* partial, double* out, cudaStream_t st) {
+  const int np = (int)std::min<int64_t>(1024, std::max<int64_t>(1, ceil_div(n, NT)));
+  k_frob_partial<<<np, NT, 0, st>>>(A, n, partial);
+  k_frob_final<<<1, 32, 0, st>>>(partial, np, out);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_gather_cols(const cplx* src, int64_t rows, int64_t lds, const int* idx, const double* scale, int ncols,
+                        cplx* dst, int64_t ldd, bool conj, cudaStream_t st) {
+  if (ncols <= 0 || rows <= 0) return;
+  dim3 g((unsigned)std::min<int64_t>(ceil_div(rows, NT), 64), ncols);
+  k_gather_cols<<<g, NT, 0, st>>>(src, rows, lds, idx, scale, ncols, dst, ldd, conj ? 1 : 0);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_gather_rows(const cplx* src, int64_t lds, const int* idx, int nr, int64_t cols, cplx* dst,
+                        cudaStream_t st) {
+  if (nr <= 0 || cols <= 0) return;
+  k_gather_rows<<<grid1((int64_t)nr * cols), NT, 0, st>>>(src, lds, idx, nr, cols, dst);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_transpose(const cplx* src, int64_t R, int64_t C, cplx* dst, bool conj, cudaStream_t st) {
+  if (R <= 0 || C <= 0) return;
+  dim3 g((unsigned)ceil_div(R, 32), (unsigned)ceil_div(C, 32));
+  k_transpose<<<g, NT, 0, st>>>(src, R, C, dst, conj ? 1 : 0);
+  VSIE_CHECK_LAUNCH();
+}
+
+int lu_nparts(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, NT), 592)); }
+
+void launch_lu_update(cplx* W, int64_t n, int r, int j, ArgMax* partials, int nparts, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_lu_update, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_maxvol_update, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_unit_lower_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    configured = true;
+  }
+  k_lu_update<<<nparts, NT, (size_t)r * sizeof(cplx), st>>>(W, n, r, j, partials);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_lu_pivot(cplx* W, int64_t n, int r, int j, int* perm, const ArgMax* partials, int nparts, int* bad,
+                     cudaStream_t st) {
+  k_lu_pivot<<<1, NT, 0, st>>>(W, n, r, j, perm, partials, nparts, bad);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_copy_lower(const cplx* W, int64_t n, int r, cplx* Lr, cudaStream_t st) {
+  k_copy_lower<<<grid1((int64_t)r * r), NT, 0, st>>>(W, n, r, Lr);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_unit_lower_inverse(const cplx* Lr, int r, cplx* T, cudaStream_t st) {
+  k_unit_lower_inverse<<<r, 128, (size_t)r * sizeof(cplx), st>>>(Lr, r, T);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_set_identity_top(cplx* B, int64_t n, int r, cudaStream_t st) {
+  k_set_identity_top<<<grid1((int64_t)r * r), NT, 0, st>>>(B, n, r);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_maxvol_update(cplx* B, int64_t n, int r, const int* perm, const cplx* rowbuf, const MaxvolState* s,
+                          bool update, ArgMax* partials, int nparts, cudaStream_t st) {
+  k_maxvol_update<<<nparts, NT, (size_t)r * sizeof(cplx), st>>>(B, n, r, perm, rowbuf, s, update ? 1 : 0, partials);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_maxvol_select(cplx* B, int64_t n, int r, const ArgMax* partials, int nparts, double tau, int* piv_pos,
+                          cplx* rowbuf, MaxvolState* s, cudaStream_t st) {
+  k_maxvol_select<<<1, NT, 0, st>>>(B, n, r, partials, nparts, tau, piv_pos, rowbuf, s);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_scatter_rows(const cplx* B, int64_t n, int r, const int* perm, cplx* Bout, cudaStream_t st) {
+  k_scatter_rows<<<grid1(n * r), NT, 0, st>>>(B, n, r, perm, Bout);
+  VSIE_CHECK_LAUNCH();
+}
+
+}  // namespace vsie

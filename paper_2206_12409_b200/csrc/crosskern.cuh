@@ -1,0 +1,68 @@
+// Device kernels of the TT-cross driver: rank-revealing
+// factorisation of supercores (one-sided Jacobi SVD, randomized range finder
+// sketches), maxvol (LU-initialised, rank-1 updates) and index gathers.
+#pragma once
+
+#include "common.cuh"
+
+namespace vsie {
+
+// complex normal (a + ib)/sqrt 2 from a counter-based generator (splitmix64 + Box-Muller)
+void launch_gaussian(cplx* out, int64_t n, uint64_t seed, cudaStream_t st);
+
+// one round of the parallel one-sided (Hestenes) Jacobi method on the columns of
+// A (p x q, ld lda), accumulating the same rotations into V (q x q, ld q) if V != null.
+// pairs: int2[npairs] column pairs; rotations applied counted into *rot_count.
+void launch_jacobi_round(cplx* A, int64_t p, int64_t lda, cplx* V, int64_t q, const int2* pairs, int npairs,
+                         double thr, unsigned* rot_count, cudaStream_t st);
+// out[j] = ||A[:, j]||_2
+void launch_col_norms(const cplx* A, int64_t p, int64_t q, int64_t lda, double* out, cudaStream_t st);
+// sum |a_i|^2 (deterministic two-pass) -> *out (device)
+void launch_frob2(const cplx* A, int64_t n, double* partial /*>= 1024*/, double* out, cudaStream_t st);
+
+// dst[:, j] = scale_j * src[:, idx[j]]  (idx, scale on device; scale may be null; conj optional)
+void launch_gather_cols(const cplx* src, int64_t rows, int64_t lds, const int* idx, const double* scale, int ncols,
+                        cplx* dst, int64_t ldd, bool conj, cudaStream_t st);
+// dst[i, :] = src[idx[i], :]   (dst nr x cols, ld nr)
+void launch_gather_rows(const cplx* src, int64_t lds, const int* idx, int nr, int64_t cols, cplx* dst,
+                        cudaStream_t st);
+// dst (C x R) = op(src (R x C)), op = transpose or conj-transpose
+void launch_transpose(const cplx* src, int64_t R, int64_t C, cplx* dst, bool conj, cudaStream_t st);
+
+// ---- maxvol -------------------------------------------------------------
+struct ArgMax {
+  double v;     // |value|^2
+  int64_t key;  // tie-break key (smaller wins)
+  int64_t i;    // row (permuted frame)
+  int c;        // column
+};
+
+// LU with partial pivoting of W (n x r, ld n), in place, rows physically swapped;
+// perm[i] = original row of permuted row i.  j = -1: argmax of column 0 only.
+void launch_lu_update(cplx* W, int64_t n, int r, int j, ArgMax* partials, int nparts, cudaStream_t st);
+void launch_lu_pivot(cplx* W, int64_t n, int r, int j, int* perm, const ArgMax* partials, int nparts,
+                     int* bad, cudaStream_t st);
+int lu_nparts(int64_t n);
+// Lr[i * r + k] = W[i + n k] for k < i (strict lower of the leading r x r), row-major
+void launch_copy_lower(const cplx* W, int64_t n, int r, cplx* Lr, cudaStream_t st);
+// T = inverse of the unit lower triangular matrix whose strict lower part is Lr (row-major); T column-major r x r
+void launch_unit_lower_inverse(const cplx* Lr, int r, cplx* T, cudaStream_t st);
+// B[0:r, 0:r] = identity (B ld n)
+void launch_set_identity_top(cplx* B, int64_t n, int r, cudaStream_t st);
+
+struct MaxvolState {
+  int i_star, c_star;  // chosen element (permuted frame)
+  cplx piv;            // B[i*, c*]
+  int done;            // 1: converged (max |B| <= 1 + tau) or it cap
+  int swaps;
+  double maxabs;       // |B[i*, c*]| of the last selection
+};
+// argmax pass (update = false) or rank-1 update + argmax pass over B (n x r, ld n)
+void launch_maxvol_update(cplx* B, int64_t n, int r, const int* perm, const cplx* rowbuf, const MaxvolState* s,
+                          bool update, ArgMax* partials, int nparts, cudaStream_t st);
+void launch_maxvol_select(cplx* B, int64_t n, int r, const ArgMax* partials, int nparts, double tau,
+                          int* piv_pos, cplx* rowbuf, MaxvolState* s, cudaStream_t st);
+// Bout[perm[i], :] = B[i, :]
+void launch_scatter_rows(const cplx* B, int64_t n, int r, const int* perm, cplx* Bout, cudaStream_t st);
+
+}  // namespace vsie

@@ -86,13 +86,13 @@ __global__ void __launch_bounds__(256) k_entries_list(EntryGeom g, const int64_t
 }
 
 __global__ void __launch_bounds__(256) k_entries_block(EntryGeom g, BlockDesc b, cplx* __restrict__ out) {
-  const int64_t rows = b.row1 - b.row0;
-  const int64_t total = rows * b.nk1 * b.rr;
+  const int64_t rows = b.rl * b.nk;
+  const int64_t total = rows * (b.col1 - b.col0);
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t rloc = t % rows;
-    const int64_t c = t / rows;
-    const int64_t r = b.row0 + rloc;
+    const int64_t r = t % rows;
+    const int64_t cl = t / rows;
+    const int64_t c = b.col0 + cl;
     const int64_t alpha = r % b.rl, ik = r / b.rl;
     const int64_t ik1 = c % b.nk1, beta = c / b.nk1;
     int i1, i2, i3;
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(256) k_entries_block(EntryGeom g, BlockDesc b,
       i3 = (int)ik;
       n = ik1;
     }
-    out[rloc + b.ld * c] = entry_value(g, b.chi, i1, i2, i3, n);
+    out[r + b.ld * cl] = entry_value(g, b.chi, i1, i2, i3, n);
   }
 }
 
@@ -133,7 +133,7 @@ void launch_entries_list(const EntryGeom& g, const int64_t* idx, int64_t count, 
 }
 
 void launch_entries_block(const EntryGeom& g, const BlockDesc& b, cplx* out, cudaStream_t st) {
-  const int64_t total = (b.row1 - b.row0) * b.nk1 * b.rr;
+  const int64_t total = b.rl * b.nk * (b.col1 - b.col0);
   if (total <= 0) return;
   k_entries_block<<<grid_for(total, 256), 256, 0, st>>>(g, b, out);
   VSIE_CHECK_LAUNCH();

@@ -9,6 +9,11 @@
 
 namespace vsie {
 
+int64_t& launch_counter() {
+  static thread_local int64_t n = 0;
+  return n;
+}
+
 namespace {
 
 // ------------------------------------------------------------------ small kernels
@@ -292,7 +297,16 @@ void combine_r3(vsie_coupling_s* h, DevBuf<cplx> Shard::*buf, int64_t n, cudaStr
 
 }  // namespace
 
+static void apply_impl(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int nrhs, cudaStream_t st);
+
 void apply(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int nrhs, cudaStream_t st) {
+  const int64_t before = launch_counter();
+  apply_impl(h, x, y, op, nrhs, st);
+  h->apply_launches += launch_counter() - before;
+  h->apply_calls += 1;
+}
+
+static void apply_impl(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int nrhs, cudaStream_t st) {
   VSIE_REQUIRE(h->has_cores, VSIE_ERR_STATE, "handle has no TT cores");
   VSIE_REQUIRE(op == VSIE_OP_N || op == VSIE_OP_T || op == VSIE_OP_C, VSIE_ERR_ARG, "bad op");
   VSIE_REQUIRE(nrhs >= 1 && nrhs <= h->nrhs_max, VSIE_ERR_ARG, "nrhs out of range");
@@ -582,10 +596,31 @@ void tt_eval(vsie_coupling_s* h, const int64_t* idx, int64_t count, cplx* out, c
   }
   const size_t smem = (size_t)rmax * sizeof(cplx);
   VSIE_REQUIRE(smem <= 200 * 1024, VSIE_ERR_ARG, "ranks too large for tt_eval");
-  if (smem > 48 * 1024)
-    VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_tt_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_tt_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   const int blocks = (int)std::min<int64_t>(count, 148 * 16);
   k_tt_eval<<<blocks, 128, smem, st>>>(c, h->grid.n[0], h->grid.n[1], h->grid.n[2], h->grid.nv(), idx, count, out);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_tt_eval(const cplx* const G[4], const int r[3], const int n[3], int64_t m, int chi_sel,
+                    const int64_t* idx, int64_t count, int64_t nv, cplx* out, cudaStream_t st) {
+  (void)m;
+  (void)chi_sel;
+  if (count <= 0) return;
+  EvalCores c{};
+  for (int q = 0; q < 3; ++q) {
+    for (int k = 0; k < 4; ++k) c.G[q][k] = G[k];
+    for (int j = 0; j < 3; ++j) c.r[q][j] = r[j];
+  }
+  const size_t smem = (size_t)(r[0] + r[1] + r[2]) * sizeof(cplx);
+  VSIE_REQUIRE(smem <= 200 * 1024, VSIE_ERR_ARG, "ranks too large for tt_eval");
+  static bool configured = false;
+  if (!configured) {
+    VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_tt_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    configured = true;
+  }
+  const int blocks = (int)std::min<int64_t>(count, 148 * 16);
+  k_tt_eval<<<blocks, 128, smem, st>>>(c, n[0], n[1], n[2], nv, idx, count, out);
   VSIE_CHECK_LAUNCH();
 }
 

@@ -63,6 +63,7 @@ struct vsie_coupling_s {
   int sweeps[3] = {0, 0, 0};
   double heldout_err[3] = {0, 0, 0};
   double build_s = 0, build_entry_s = 0, build_factor_s = 0, build_maxvol_s = 0;
+  int64_t apply_launches = 0, apply_calls = 0;
   // timing
   bool timing = false;
   std::vector<vsie::Timed> pending;

@@ -25,8 +25,8 @@ void launch_entries_list(const EntryGeom& g, const int64_t* idx, int64_t count, 
 
 // Structured supercore block:
 //   M[(a, i_k), (i_{k+1}, b)] = A_chi(I_{<=k-1}[a], i_k, i_{k+1}, J_{>k+1}[b]),
-//   rows [row0, row1) of the (rl * nk) x (nk1 * rr) matrix, written column-major
-//   with leading dimension ld (= row1 - row0 by default).
+//   columns [col0, col1) of the (rl * nk) x (nk1 * rr) matrix, written column-major
+//   (all rows) with leading dimension ld >= rl * nk at out + ld * (c - col0).
 //   left: int32 [rl][2] device (k=2: i1; k=3: (i1, i2)); right: int32 [rr][2] device
 //   (k=1: (i3, n); k=2: n).
 struct BlockDesc {
@@ -34,7 +34,7 @@ struct BlockDesc {
   int64_t rl, nk, nk1, rr;
   const int32_t* left;
   const int32_t* right;
-  int64_t row0, row1;
+  int64_t col0, col1;
   int64_t ld;
 };
 void launch_entries_block(const EntryGeom& g, const BlockDesc& b, cplx* out, cudaStream_t st);
