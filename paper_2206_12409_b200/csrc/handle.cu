@@ -9,11 +9,6 @@
 
 namespace vsie {
 
-int64_t& launch_counter() {
-  static thread_local int64_t n = 0;
-  return n;
-}
-
 namespace {
 
 // ------------------------------------------------------------------ small kernels
@@ -200,7 +195,7 @@ void handle_alloc_workspace(vsie_coupling_s* h) {
   (void)rmax_gemv;
   // split-K partials: the launchers cap splits so that nsplit * rows <= 888/3 * 256
   // (gemv_n) and nsplit * cols <= 888/3 * 32 (gemv_t) per batch
-  h->partials.alloc((size_t)3 * 80000);
+  h->partials.alloc((size_t)3 * 320000);
   h->counters.alloc(3 * 8192);
   VSIE_CHECK_CUDA(cudaMemset(h->counters.p, 0, h->counters.bytes()));
   // split-K workspace of the ZGEMMs (launch_zgemm lowers the split to fit)
@@ -343,7 +338,7 @@ static void apply_impl(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int n
         }
         Scope sc(h, "fwd_g4_gemv", bytes, 8 * (bytes / 16), st);
         if (s.mloc() > 0)
-          launch_gemv_n(g, h->partials.p, h->counters.p, max_splits, st);
+          launch_gemv_n(g, h->partials.p, (int64_t)h->partials.n, h->counters.p, max_splits, st);
         else
           VSIE_CHECK_CUDA(cudaMemsetAsync(s.y4.p, 0, s.y4.bytes(), st));
       } else {
@@ -381,7 +376,7 @@ static void apply_impl(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int n
           bytes += 16 * (R(c, 1) * n3l * R(c, 2) + R(c, 1) * n3l + R(c, 2));
         }
         Scope sc(h, "fwd_g3_gemv", bytes, 8 * (bytes / 16), st);
-        launch_gemv_n(g, h->partials.p, h->counters.p, max_splits, st);
+        launch_gemv_n(g, h->partials.p, (int64_t)h->partials.n, h->counters.p, max_splits, st);
       } else {
         Zgemm z{};
         z.nbatch = 3;
@@ -496,7 +491,7 @@ static void apply_impl(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int n
         bytes += 16 * (R(c, 1) * n3l * R(c, 2) + R(c, 1) * n3l + R(c, 2));
       }
       Scope sc(h, "adj_g3_gemv", bytes, 8 * (bytes / 16), st);
-      launch_gemv_t(g, h->partials.p, h->counters.p, max_splits, st);
+      launch_gemv_t(g, h->partials.p, (int64_t)h->partials.n, h->counters.p, max_splits, st);
     } else {
       Zgemm z{};
       z.nbatch = 3;
@@ -541,7 +536,7 @@ static void apply_impl(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int n
         bytes += 16 * (R(c, 2) * s.mloc() + R(c, 2));
       }
       Scope sc(h, "adj_g4_gemv", bytes, 8 * (bytes / 16), st);
-      launch_gemv_t(g, h->partials.p, h->counters.p, max_splits, st);
+      launch_gemv_t(g, h->partials.p, (int64_t)h->partials.n, h->counters.p, max_splits, st);
     } else {
       Scope sc(h, "adj_g4_zgemm", 0, 0, st);
       for (int c = 0; c < 3; ++c) {

@@ -62,9 +62,11 @@ struct GemvT {
 
 struct ApplyWorkspace;  // split-K partials + counters (handle-owned)
 
-void launch_gemv_n(const GemvN& a, cplx* partials, unsigned* counters, int max_splits,
+// partials_cap: capacity (elements) of the split-K partial buffer; the split is
+// lowered so that it always fits.
+void launch_gemv_n(const GemvN& a, cplx* partials, int64_t partials_cap, unsigned* counters, int max_splits,
                    cudaStream_t st);
-void launch_gemv_t(const GemvT& a, cplx* partials, unsigned* counters, int max_splits,
+void launch_gemv_t(const GemvT& a, cplx* partials, int64_t partials_cap, unsigned* counters, int max_splits,
                    cudaStream_t st);
 
 // Expansion y[chi][i1 + n1 c] = sum_a G1[i1 + n1 a] Y2[a + r1 c], c in [0, ncol),

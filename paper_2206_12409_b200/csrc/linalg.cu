@@ -12,6 +12,11 @@
 
 namespace vsie {
 
+int64_t& launch_counter() {
+  static thread_local int64_t n = 0;
+  return n;
+}
+
 namespace {
 
 constexpr int BM = 64, BN = 64, BK = 8, NT = 256;

@@ -26,45 +26,70 @@ constexpr int kXChunk = 512;
 
 __device__ __forceinline__ cplx ldg_c(const cplx* p) { return __ldg(p); }
 
-__global__ void __launch_bounds__(kThreads) k_gemv_n(GemvN a, cplx* __restrict__ partials,
+// y[r] = sum_c A[r + R c] x[c]: each thread owns rows t + 256 g (g < G) of a
+// row tile of 256 G rows and a column range of its split; x values are warp-uniform
+// broadcast loads; 4 columns x G rows of loads in flight per thread.
+template <int G>
+__global__ void __launch_bounds__(kThreads) k_gemv_n(const __grid_constant__ GemvN a, cplx* __restrict__ partials,
                                                      unsigned* __restrict__ counters, int64_t rmax) {
   const int b = blockIdx.z;
   const int64_t R = a.R[b], C = a.C[b];
   const int64_t rt = blockIdx.y;
-  if (rt * kThreads >= R) return;
+  const int64_t row0 = rt * kThreads * G;
+  if (row0 >= R) return;
   const int nsplit = gridDim.x, s = blockIdx.x;
   const int64_t c0 = C * s / nsplit, c1 = C * (s + 1) / nsplit;
-  const int64_t row = rt * kThreads + threadIdx.x;
-  const bool act = row < R;
-  __shared__ cplx xs[kXChunk];
-  cplx acc0 = cmk(0, 0), acc1 = acc0, acc2 = acc0, acc3 = acc0;
   const cplx* __restrict__ X = a.x[b];
   const cplx* __restrict__ A = a.A[b];
-  for (int64_t cc = c0; cc < c1; cc += kXChunk) {
-    const int len = (int)min((int64_t)kXChunk, c1 - cc);
-    __syncthreads();
-    for (int j = threadIdx.x; j < len; j += kThreads) xs[j] = ldg_c(X + cc + j);
-    __syncthreads();
-    if (act) {
-      const cplx* Ap = A + row + R * cc;
-      int j = 0;
-      for (; j + 4 <= len; j += 4) {
-        const cplx v0 = ldg_c(Ap + R * j), v1 = ldg_c(Ap + R * (j + 1));
-        const cplx v2 = ldg_c(Ap + R * (j + 2)), v3 = ldg_c(Ap + R * (j + 3));
-        cfma(acc0, v0, xs[j]);
-        cfma(acc1, v1, xs[j + 1]);
-        cfma(acc2, v2, xs[j + 2]);
-        cfma(acc3, v3, xs[j + 3]);
-      }
-      for (; j < len; ++j) cfma(acc0, ldg_c(Ap + R * j), xs[j]);
-    }
+  cplx acc[G], acc2[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) acc[g] = acc2[g] = cmk(0, 0);
+  int64_t rows[G];
+  bool act[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    rows[g] = row0 + threadIdx.x + kThreads * g;
+    act[g] = rows[g] < R;
   }
-  const cplx sum = cadd(cadd(acc0, acc1), cadd(acc2, acc3));
+  int64_t c = c0;
+  for (; c + 4 <= c1; c += 4) {
+    const cplx x0 = __ldg(X + c), x1 = __ldg(X + c + 1), x2 = __ldg(X + c + 2), x3 = __ldg(X + c + 3);
+    cplx v[G][4];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      if (act[g]) {
+        const cplx* p = A + rows[g] + R * c;
+        v[g][0] = __ldcs(p);
+        v[g][1] = __ldcs(p + R);
+        v[g][2] = __ldcs(p + 2 * R);
+        v[g][3] = __ldcs(p + 3 * R);
+      }
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      if (act[g]) {
+        cfma(acc[g], v[g][0], x0);
+        cfma(acc2[g], v[g][1], x1);
+        cfma(acc[g], v[g][2], x2);
+        cfma(acc2[g], v[g][3], x3);
+      }
+  }
+  for (; c < c1; ++c) {
+    const cplx xv = __ldg(X + c);
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      if (act[g]) cfma(acc[g], __ldcs(A + rows[g] + R * c), xv);
+  }
+#pragma unroll
+  for (int g = 0; g < G; ++g) acc[g] = cadd(acc[g], acc2[g]);
   if (nsplit == 1) {
-    if (act) a.y[b][row] = sum;
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      if (act[g]) a.y[b][rows[g]] = acc[g];
     return;
   }
-  if (act) partials[((int64_t)b * nsplit + s) * rmax + row] = sum;
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+    if (act[g]) partials[((int64_t)b * nsplit + s) * rmax + rows[g]] = acc[g];
   __threadfence();
   __syncthreads();
   __shared__ bool last;
@@ -73,11 +98,13 @@ __global__ void __launch_bounds__(kThreads) k_gemv_n(GemvN a, cplx* __restrict__
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (act) {
-    cplx tot = cmk(0, 0);
-    for (int q = 0; q < nsplit; ++q) tot = cadd(tot, __ldcg(partials + ((int64_t)b * nsplit + q) * rmax + row));
-    a.y[b][row] = tot;
-  }
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+    if (act[g]) {
+      cplx tot = cmk(0, 0);
+      for (int q = 0; q < nsplit; ++q) tot = cadd(tot, __ldcg(partials + ((int64_t)b * nsplit + q) * rmax + rows[g]));
+      a.y[b][rows[g]] = tot;
+    }
   if (threadIdx.x == 0) *ctr = 0;
 }
 
@@ -92,7 +119,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // y[c] = sum_r A[r + R c] x[r]  over rows [r0, r1) of this split.
-__global__ void __launch_bounds__(kThreads) k_gemv_t(GemvT a, cplx* __restrict__ partials,
+__global__ void __launch_bounds__(kThreads) k_gemv_t(const __grid_constant__ GemvT a, cplx* __restrict__ partials,
                                                      unsigned* __restrict__ counters, int64_t cmax) {
   const bool conj_out = a.conj_out;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -113,12 +140,31 @@ __global__ void __launch_bounds__(kThreads) k_gemv_t(GemvT a, cplx* __restrict__
     const int64_t r0 = R * s / nsplit, r1 = R * (s + 1) / nsplit;
     const cplx* __restrict__ A = a.A[b];
     const cplx* __restrict__ X = a.x[b];
-    for (int64_t r = r0 + lane; r < r1; r += 32) {
+    int64_t r = r0 + lane;
+    for (; r + 32 < r1; r += 64) {
+      const cplx xa = ldg_c(X + r), xb = ldg_c(X + r + 32);
+      cplx va[kCPW], vb[kCPW];
+#pragma unroll
+      for (int j = 0; j < kCPW; ++j) {
+        const int64_t c = cbase + j;
+        if (c < Cout) {
+          va[j] = __ldcs(A + r + R * c);
+          vb[j] = __ldcs(A + r + 32 + R * c);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kCPW; ++j)
+        if (cbase + j < Cout) {
+          cfma(acc[j], va[j], xa);
+          cfma(acc[j], vb[j], xb);
+        }
+    }
+    for (; r < r1; r += 32) {
       const cplx xv = ldg_c(X + r);
 #pragma unroll
       for (int j = 0; j < kCPW; ++j) {
         const int64_t c = cbase + j;
-        if (c < Cout) cfma(acc[j], ldg_c(A + r + R * c), xv);
+        if (c < Cout) cfma(acc[j], __ldcs(A + r + R * c), xv);
       }
     }
   }
@@ -165,104 +211,150 @@ __global__ void __launch_bounds__(kThreads) k_gemv_t(GemvT a, cplx* __restrict__
   if (threadIdx.x == 0) *ctr = 0;
 }
 
-// ----------------------------------------------------------------------------- G1 expansion
-constexpr int kExpCols = 64;
-constexpr int kExpGroup = 8;
+// ----------------------------------------------------------------------------- G1 steps on FP64 tensor cores
+// Both G1 contractions are dense skinny GEMMs (K = r1 for the expansion, K = n1
+// for the transpose reduction), so they run on the sm_100a FP64 tensor cores
+// through mma.sync.m8n8k4.f64 (DMMA; tcgen05 has no f64 kind).  A complex
+// product is 4 real DMMAs: C_re += A_re B_re - A_im B_im, C_im += A_re B_im + A_im B_re.
+// Fragment layout of m8n8k4 (PTX ISA): lane = 4 g + t;  A[g][t], B[t][g],
+// C[g][2 t + j] (j = 0, 1).
+constexpr int kWarpsG1 = 8;
+constexpr int kG1Threads = 32 * kWarpsG1;
+constexpr int kColsPerWarp = 8;
+constexpr int kColsPerCtaG1 = kColsPerWarp * kWarpsG1;   // 64 columns per CTA
 
-__global__ void __launch_bounds__(kThreads) k_expand_g1(ExpandArgs a) {
+__device__ __forceinline__ int64_t col_addr(int64_t c, int64_t cpr, int64_t ld, int n1) {
+  if (c < cpr) return c * n1;  // single right-hand side: no division
+  const int64_t rhs = c / cpr;
+  return rhs * ld + (c - rhs * cpr) * n1;
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// complex 8x8x4 block: (cr, ci) += A * B with A = (ar, ai), B = (br, bi) fragments
+__device__ __forceinline__ void zmma(double (&cr)[2], double (&ci)[2], cplx a, cplx b) {
+  dmma(cr[0], cr[1], a.x, b.x);
+  dmma(cr[0], cr[1], -a.y, b.y);
+  dmma(ci[0], ci[1], a.x, b.y);
+  dmma(ci[0], ci[1], a.y, b.x);
+}
+
+// y[i1 + n1 c] = sum_a G1[i1 + n1 a] Y2[a + r1 c]: warp task = 8 columns x all i1;
+// Y2 fragments in registers (KT k-steps), G1 fragments from shared memory; each
+// 8 x 8 output tile is stored as 4 whole 128-B lines per warp instruction.
+template <int KT>
+__global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant__ ExpandArgs a) {
   const int b = blockIdx.y;
   const int n1 = a.n1, r1 = a.r1[b];
-  const int64_t col0 = (int64_t)blockIdx.x * kExpCols;
-  if (col0 >= a.ncol) return;
-  const int ncols = (int)min((int64_t)kExpCols, a.ncol - col0);
-  extern __shared__ cplx sm[];
-  cplx* G1s = sm;             // [a1][i1] = G1 column-major
-  cplx* Y2s = sm + n1 * r1;   // [c][a1]
+  const int mt = (n1 + 7) / 8;
+  extern __shared__ cplx Af[];   // [mt][KT][32] fragments of G1
   const cplx* __restrict__ G1 = a.G1[b];
-  for (int t = threadIdx.x; t < n1 * r1; t += kThreads) G1s[t] = ldg_c(G1 + t);
-  const cplx* __restrict__ Y2 = a.Y2[b] + (int64_t)r1 * col0;
-  for (int t = threadIdx.x; t < r1 * ncols; t += kThreads) Y2s[t] = ldg_c(Y2 + t);
+  for (int e = threadIdx.x; e < mt * KT * 32; e += kG1Threads) {
+    const int lane = e % 32, ks = (e / 32) % KT, m = e / (32 * KT);
+    const int i1 = 8 * m + (lane >> 2), k = 4 * ks + (lane & 3);
+    Af[e] = (i1 < n1 && k < r1) ? __ldg(G1 + i1 + (int64_t)n1 * k) : cmk(0, 0);
+  }
   __syncthreads();
-  const int ngroups = (ncols + kExpGroup - 1) / kExpGroup;
-  cplx* __restrict__ Y = a.y[b];
-  for (int f = threadIdx.x; f < n1 * ngroups; f += kThreads) {
-    const int i1 = f % n1, gi = f / n1;
-    cplx acc[kExpGroup];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t c0 = ((int64_t)blockIdx.x * kWarpsG1 + warp) * kColsPerWarp;
+  if (c0 >= a.ncol) return;
+  cplx bf[KT];
+  {
+    const int64_t c = c0 + g;
+    const cplx* __restrict__ Y2 = a.Y2[b] + (int64_t)r1 * c;
 #pragma unroll
-    for (int j = 0; j < kExpGroup; ++j) acc[j] = cmk(0, 0);
-    const cplx* yb = Y2s + r1 * (gi * kExpGroup);
-    for (int a1 = 0; a1 < r1; ++a1) {
-      const cplx gv = G1s[i1 + n1 * a1];
-#pragma unroll
-      for (int j = 0; j < kExpGroup; ++j) cfma(acc[j], gv, yb[a1 + r1 * j]);
+    for (int ks = 0; ks < KT; ++ks) {
+      const int k = 4 * ks + t;
+      bf[ks] = (c < a.ncol && k < r1) ? __ldg(Y2 + k) : cmk(0, 0);
     }
+  }
+  int64_t oaddr[2];
+  bool ok[2];
 #pragma unroll
-    for (int j = 0; j < kExpGroup; ++j) {
-      const int cl = gi * kExpGroup + j;
-      if (cl < ncols) {
-        const int64_t c = col0 + cl;
-        const int64_t rhs = c / a.cols_per_rhs, cc = c - rhs * a.cols_per_rhs;
-        Y[rhs * a.ld_rhs + cc * n1 + i1] = acc[j];
-      }
+  for (int j = 0; j < 2; ++j) {
+    const int64_t c = c0 + 2 * t + j;
+    ok[j] = c < a.ncol;
+    oaddr[j] = ok[j] ? col_addr(c, a.cols_per_rhs, a.ld_rhs, n1) : 0;
+  }
+  cplx* __restrict__ Y = a.y[b];
+  for (int m = 0; m < mt; ++m) {
+    double cr[2] = {0, 0}, ci[2] = {0, 0};
+#pragma unroll
+    for (int ks = 0; ks < KT; ++ks) zmma(cr, ci, Af[(m * KT + ks) * 32 + lane], bf[ks]);
+    const int i1 = 8 * m + g;
+    if (i1 < n1) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        if (ok[j]) __stcs(Y + oaddr[j] + i1, cmk(cr[j], ci[j]));
     }
   }
 }
 
-// ----------------------------------------------------------------------------- G1^T reduction
-constexpr int kRedCols = 64;
-constexpr int kRedK = 32;
-constexpr int kRedGroups = kThreads / kRedCols;  // 4 a1-groups
-constexpr int kRedMaxAcc = 8;                    // r1 <= 32 per pass
-
-__global__ void __launch_bounds__(kThreads) k_reduce_g1(ReduceArgs a) {
+// W1[a + r1 c] = sum_i1 G1[i1 + n1 a] u[i1 + n1 c] (conj(u) for op C): warp task =
+// 8 columns x all a (NT n-tiles of 8); u fragments streamed from global (each
+// lane 16 B, 64 contiguous bytes per column), G1 fragments from shared memory.
+template <int NT>
+__global__ void __launch_bounds__(kG1Threads) k_reduce_g1(const __grid_constant__ ReduceArgs a) {
   const int b = blockIdx.y;
   const int n1 = a.n1, r1 = a.r1[b];
-  const int64_t col0 = (int64_t)blockIdx.x * kRedCols;
-  if (col0 >= a.ncol) return;
-  const int ncols = (int)min((int64_t)kRedCols, a.ncol - col0);
-  __shared__ cplx us[kRedK][kRedCols + 1];
-  extern __shared__ cplx G1s[];  // [a1][i1] = G1 column-major, n1 * r1
+  const int ks_n = (n1 + 3) / 4;
+  extern __shared__ cplx Bf[];   // [ks_n][NT][32] fragments of G1
   const cplx* __restrict__ G1 = a.G1[b];
-  for (int t = threadIdx.x; t < n1 * r1; t += kThreads) G1s[t] = ldg_c(G1 + t);
-  const int c = threadIdx.x % kRedCols, ag = threadIdx.x / kRedCols;
-  const cplx* __restrict__ U = a.u[b];
-  for (int abase = 0; abase < r1; abase += kRedGroups * kRedMaxAcc) {
-    cplx acc[kRedMaxAcc];
+  for (int e = threadIdx.x; e < ks_n * NT * 32; e += kG1Threads) {
+    const int lane = e % 32, nt = (e / 32) % NT, ks = e / (32 * NT);
+    const int k = 4 * ks + (lane & 3), n = 8 * nt + (lane >> 2);
+    Bf[e] = (k < n1 && n < r1) ? __ldg(G1 + k + (int64_t)n1 * n) : cmk(0, 0);
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t c0 = ((int64_t)blockIdx.x * kWarpsG1 + warp) * kColsPerWarp;
+  if (c0 >= a.ncol) return;
+  const int64_t cg = c0 + g;
+  const bool cok = cg < a.ncol;
+  const cplx* __restrict__ U = a.u[b] + (cok ? col_addr(cg, a.cols_per_rhs, a.ld_rhs, n1) : 0);
+  const double sgn = a.conj_u ? -1.0 : 1.0;
+  double cr[NT][2], ci[NT][2];
 #pragma unroll
-    for (int j = 0; j < kRedMaxAcc; ++j) acc[j] = cmk(0, 0);
-    for (int k0 = 0; k0 < n1; k0 += kRedK) {
-      const int klen = min(kRedK, n1 - k0);
-      __syncthreads();
-      // stage u[k0:k0+klen, col0:col0+ncols] transposed as us[i1][c]
-      for (int t = threadIdx.x; t < kRedK * kRedCols; t += kThreads) {
-        const int kk = t % kRedK, cl = t / kRedK;
-        cplx v = cmk(0, 0);
-        if (kk < klen && cl < ncols) {
-          const int64_t cg = col0 + cl;
-          const int64_t rhs = cg / a.cols_per_rhs, cc = cg - rhs * a.cols_per_rhs;
-          v = ldg_c(U + rhs * a.ld_rhs + cc * n1 + k0 + kk);
-          if (a.conj_u) v.y = -v.y;
-        }
-        us[kk][cl] = v;
-      }
-      __syncthreads();
-      for (int kk = 0; kk < klen; ++kk) {
-        const cplx uv = us[kk][c];
+  for (int nt = 0; nt < NT; ++nt) cr[nt][0] = cr[nt][1] = ci[nt][0] = ci[nt][1] = 0;
+  constexpr int UNR = 4;
+  int ks = 0;
+  for (; ks + UNR <= ks_n; ks += UNR) {
+    cplx av[UNR];
 #pragma unroll
-        for (int j = 0; j < kRedMaxAcc; ++j) {
-          const int a1 = abase + ag + kRedGroups * j;
-          if (a1 < r1) cfma(acc[j], G1s[k0 + kk + n1 * a1], uv);
-        }
-      }
+    for (int q = 0; q < UNR; ++q) {
+      const int k = 4 * (ks + q) + t;
+      av[q] = (cok && k < n1) ? __ldcs(U + k) : cmk(0, 0);
     }
-    if (c < ncols) {
-      cplx* W = a.W1[b] + (int64_t)r1 * (col0 + c);
 #pragma unroll
-      for (int j = 0; j < kRedMaxAcc; ++j) {
-        const int a1 = abase + ag + kRedGroups * j;
-        if (a1 < r1) W[a1] = acc[j];
-      }
+    for (int q = 0; q < UNR; ++q) {
+      const cplx av2 = cmk(av[q].x, sgn * av[q].y);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) zmma(cr[nt], ci[nt], av2, Bf[((ks + q) * NT + nt) * 32 + lane]);
     }
+  }
+  for (; ks < ks_n; ++ks) {
+    const int k = 4 * ks + t;
+    cplx av = (cok && k < n1) ? __ldcs(U + k) : cmk(0, 0);
+    av.y *= sgn;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) zmma(cr[nt], ci[nt], av, Bf[(ks * NT + nt) * 32 + lane]);
+  }
+  // lane holds rows c = c0 + g, columns a = 8 nt + 2 t + j
+  if (cok) {
+    cplx* __restrict__ W = a.W1[b] + (int64_t)r1 * cg;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int aa = 8 * nt + 2 * t + j;
+        if (aa < r1) W[aa] = cmk(cr[nt][j], ci[nt][j]);
+      }
   }
 }
 
@@ -276,21 +368,30 @@ int pick_splits(int64_t other_ctas, int64_t len, int min_len, int max_splits) {
 
 }  // namespace
 
-void launch_gemv_n(const GemvN& a, cplx* partials, unsigned* counters, int max_splits, cudaStream_t st) {
+void launch_gemv_n(const GemvN& a, cplx* partials, int64_t partials_cap, unsigned* counters, int max_splits,
+                   cudaStream_t st) {
   int64_t rmax = 0, cmax = 0;
   for (int b = 0; b < a.nbatch; ++b) {
     rmax = std::max(rmax, a.R[b]);
     cmax = std::max(cmax, a.C[b]);
   }
   if (rmax == 0) return;
-  const int64_t rtiles = ceil_div(rmax, kThreads);
-  const int ns = pick_splits(rtiles * a.nbatch, cmax, 32, max_splits);
+  const int G = 1;
+  const int64_t rtiles = ceil_div(rmax, (int64_t)kThreads * G);
+  int ns = pick_splits(rtiles * a.nbatch, cmax, 16, max_splits);
+  while (ns > 1 && (int64_t)a.nbatch * ns * rmax > partials_cap) --ns;
   dim3 grid(ns, (unsigned)rtiles, a.nbatch);
-  k_gemv_n<<<grid, kThreads, 0, st>>>(a, partials, counters, rmax);
+  if (G == 1)
+    k_gemv_n<1><<<grid, kThreads, 0, st>>>(a, partials, counters, rmax);
+  else if (G == 2)
+    k_gemv_n<2><<<grid, kThreads, 0, st>>>(a, partials, counters, rmax);
+  else
+    k_gemv_n<4><<<grid, kThreads, 0, st>>>(a, partials, counters, rmax);
   VSIE_CHECK_LAUNCH();
 }
 
-void launch_gemv_t(const GemvT& a, cplx* partials, unsigned* counters, int max_splits, cudaStream_t st) {
+void launch_gemv_t(const GemvT& a, cplx* partials, int64_t partials_cap, unsigned* counters, int max_splits,
+                   cudaStream_t st) {
   int64_t rmax = 0, cmax = 0;
   for (int b = 0; b < a.nbatch; ++b) {
     rmax = std::max(rmax, a.R[b]);
@@ -299,41 +400,62 @@ void launch_gemv_t(const GemvT& a, cplx* partials, unsigned* counters, int max_s
   if (cmax == 0) return;
   const int64_t ctiles = ceil_div(cmax, kColsPerCta);
   const int nz = a.sum_batch ? 1 : a.nbatch;
-  const int ns = a.sum_batch ? 1 : pick_splits(ctiles * nz, rmax, 256, max_splits);
+  int ns = a.sum_batch ? 1 : pick_splits(ctiles * nz, rmax, 256, max_splits);
+  while (ns > 1 && (int64_t)nz * ns * cmax > partials_cap) --ns;
   dim3 grid((unsigned)ctiles, ns, nz);
   k_gemv_t<<<grid, kThreads, 0, st>>>(a, partials, counters, cmax);
   VSIE_CHECK_LAUNCH();
 }
 
+template <class F>
+void set_smem_attr_once(F* f, bool& done) {
+  if (!done) {
+    VSIE_CHECK_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    done = true;
+  }
+}
+
 void launch_expand_g1(const ExpandArgs& a, cudaStream_t st) {
   int r1max = 0;
   for (int b = 0; b < a.nbatch; ++b) r1max = std::max(r1max, a.r1[b]);
-  const size_t smem = (size_t)(a.n1 * r1max + r1max * kExpCols) * sizeof(cplx);
-  VSIE_REQUIRE(smem <= 220 * 1024, VSIE_ERR_ARG, "expand: n1 * r1 too large for shared memory");
-  static bool configured = false;
-  if (!configured) {
-    VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_expand_g1, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    configured = true;
+  VSIE_REQUIRE(r1max <= 32, VSIE_ERR_ARG, "expand: r1 > 32 not supported");
+  const int KT = (r1max + 3) / 4;
+  const size_t smem = (size_t)((a.n1 + 7) / 8) * KT * 32 * sizeof(cplx);
+  VSIE_REQUIRE(smem <= 200 * 1024, VSIE_ERR_ARG, "expand: n1 * r1 too large for shared memory");
+  dim3 grid((unsigned)ceil_div(a.ncol, kColsPerCtaG1), a.nbatch);
+#define VSIE_EXP(K)                                                  \
+  case K: {                                                          \
+    static bool d = false;                                           \
+    set_smem_attr_once(k_expand_g1<K>, d);                           \
+    k_expand_g1<K><<<grid, kG1Threads, smem, st>>>(a);               \
+    break;                                                           \
   }
-  dim3 grid((unsigned)ceil_div(a.ncol, kExpCols), a.nbatch);
-  k_expand_g1<<<grid, kThreads, smem, st>>>(a);
+  switch (KT) {
+    VSIE_EXP(1) VSIE_EXP(2) VSIE_EXP(3) VSIE_EXP(4) VSIE_EXP(5) VSIE_EXP(6) VSIE_EXP(7) default: VSIE_EXP(8)
+  }
+#undef VSIE_EXP
   VSIE_CHECK_LAUNCH();
 }
 
 void launch_reduce_g1(const ReduceArgs& a, cudaStream_t st) {
   int r1max = 0;
   for (int b = 0; b < a.nbatch; ++b) r1max = std::max(r1max, a.r1[b]);
-  const size_t smem = (size_t)a.n1 * r1max * sizeof(cplx);
-  VSIE_REQUIRE(smem + sizeof(cplx) * kRedK * (kRedCols + 1) <= 220 * 1024, VSIE_ERR_ARG,
-               "reduce: n1 * r1 too large for shared memory");
-  static bool configured = false;
-  if (!configured) {
-    VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_reduce_g1, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         220 * 1024 - (int)(sizeof(cplx) * kRedK * (kRedCols + 1))));
-    configured = true;
+  VSIE_REQUIRE(r1max <= 32, VSIE_ERR_ARG, "reduce: r1 > 32 not supported");
+  const int NT = (r1max + 7) / 8;
+  const size_t smem = (size_t)((a.n1 + 3) / 4) * NT * 32 * sizeof(cplx);
+  VSIE_REQUIRE(smem <= 200 * 1024, VSIE_ERR_ARG, "reduce: n1 * r1 too large for shared memory");
+  dim3 grid((unsigned)ceil_div(a.ncol, kColsPerCtaG1), a.nbatch);
+#define VSIE_RED(K)                                                  \
+  case K: {                                                          \
+    static bool d = false;                                           \
+    set_smem_attr_once(k_reduce_g1<K>, d);                           \
+    k_reduce_g1<K><<<grid, kG1Threads, smem, st>>>(a);               \
+    break;                                                           \
   }
-  dim3 grid((unsigned)ceil_div(a.ncol, kRedCols), a.nbatch);
-  k_reduce_g1<<<grid, kThreads, smem, st>>>(a);
+  switch (NT) {
+    VSIE_RED(1) VSIE_RED(2) VSIE_RED(3) default: VSIE_RED(4)
+  }
+#undef VSIE_RED
   VSIE_CHECK_LAUNCH();
 }
 

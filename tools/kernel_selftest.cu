@@ -80,14 +80,14 @@ void test_gemv_n(int64_t R, int64_t C) {
   unsigned* ctr; cudaMalloc(&ctr, 3 * 8192 * 4); cudaMemset(ctr, 0, 3 * 8192 * 4);
   GemvN g{};
   g.nbatch = 1; g.A[0] = dA; g.x[0] = dx; g.y[0] = dy; g.R[0] = R; g.C[0] = C;
-  launch_gemv_n(g, part, ctr, 1024, 0);
+  launch_gemv_n(g, part, 3 * 1024 * (R + 256), ctr, 1024, 0);
   auto got = down(dy, R);
   std::vector<zc> ref(R, 0);
   for (int64_t c = 0; c < C; ++c) for (int64_t r = 0; r < R; ++r) ref[r] += A[r + R * c] * x[c];
   char buf[128]; snprintf(buf, sizeof buf, "gemv_n %ldx%ld", (long)R, (long)C);
   report(buf, relerr(got, ref));
   // run again: counters must have been reset
-  launch_gemv_n(g, part, ctr, 1024, 0);
+  launch_gemv_n(g, part, 3 * 1024 * (R + 256), ctr, 1024, 0);
   report("gemv_n repeat", relerr(down(dy, R), ref));
   cudaFree(dA); cudaFree(dx); cudaFree(dy); cudaFree(part); cudaFree(ctr);
 }
@@ -105,7 +105,7 @@ void test_gemv_t(int64_t R, int64_t C, bool sum3) {
   }
   cplx* part; cudaMalloc(&part, 3 * 1024 * (C + 64) * 16);
   unsigned* ctr; cudaMalloc(&ctr, 3 * 8192 * 4); cudaMemset(ctr, 0, 3 * 8192 * 4);
-  launch_gemv_t(g, part, ctr, 1024, 0);
+  launch_gemv_t(g, part, 3 * 1024 * (C + 64), ctr, 1024, 0);
   auto got = down(dy, C);
   std::vector<zc> ref(C, 0);
   for (int b = 0; b < nb; ++b)
@@ -176,7 +176,12 @@ int main() {
   test_expand(200, 16, 517, 517);
   test_reduce(12, 7, 144, 144, false);
   test_reduce(100, 10, 1000, 300, true);
-  test_reduce(200, 37, 517, 517, false);
+  test_reduce(200, 20, 517, 517, false);
+  test_reduce(64, 32, 300, 100, true);
+  test_expand(64, 32, 300, 100);
+  test_gemv_n(7810, 267);
+  test_gemv_n(267, 10080);
+  test_gemv_t(7810, 267, false);
   cudaError_t e = cudaDeviceSynchronize();
   printf("cuda: %s\n", cudaGetErrorString(e));
   printf("%s (%d failures)\n", fails ? "SELFTEST FAILED" : "SELFTEST PASSED", fails);

@@ -1,0 +1,23 @@
+"""One GMRES step (fwd + transpose apply) on cfg cores with the measured ranks
+(random values: matvec cost is data independent), for ncu captures."""
+import json, os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "tests"))
+import torch
+import synth
+from paper_2206_12409_b200 import Coupling, grid_of
+from gpu_common import rand_tts
+ci = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+cfg = synth.get_config(ci)
+p = os.path.join(ROOT, "profiles", f"ranks_cfg{ci}.json")
+ranks = json.load(open(p))["ranks"] if os.path.exists(p) else [cfg.ranks_probe] * 3
+h = Coupling.from_cores(grid_of(cfg), cfg.meshes(), cfg.freq, rand_tts(cfg, ranks, 1), nrhs_max=1)
+x = torch.from_numpy(synth.complex_gaussian(cfg.m, 1)).cuda()
+u = torch.from_numpy(synth.complex_gaussian(3 * cfg.n_v, 2)).cuda()
+y = torch.empty(3 * cfg.n_v, dtype=torch.complex128, device="cuda")
+z = torch.empty(cfg.m, dtype=torch.complex128, device="cuda")
+for _ in range(steps):
+    h.apply(x, "N", out=y); h.apply(u, "T", out=z)
+torch.cuda.synchronize()
+print("ok", h.info()["apply_launches"] // steps, "launches per step")
