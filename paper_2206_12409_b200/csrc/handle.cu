@@ -338,7 +338,7 @@ static void apply_impl(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int n
         }
         Scope sc(h, "fwd_g4_gemv", bytes, 8 * (bytes / 16), st);
         if (s.mloc() > 0)
-          launch_gemv_n(g, h->partials.p, (int64_t)h->partials.n, h->counters.p, max_splits, st);
+          launch_gemv_n(g, h->partials.p, (int64_t)h->partials.n, max_splits, st);
         else
           VSIE_CHECK_CUDA(cudaMemsetAsync(s.y4.p, 0, s.y4.bytes(), st));
       } else {
@@ -376,7 +376,7 @@ static void apply_impl(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int n
           bytes += 16 * (R(c, 1) * n3l * R(c, 2) + R(c, 1) * n3l + R(c, 2));
         }
         Scope sc(h, "fwd_g3_gemv", bytes, 8 * (bytes / 16), st);
-        launch_gemv_n(g, h->partials.p, (int64_t)h->partials.n, h->counters.p, max_splits, st);
+        launch_gemv_n(g, h->partials.p, (int64_t)h->partials.n, max_splits, st);
       } else {
         Zgemm z{};
         z.nbatch = 3;
@@ -403,7 +403,7 @@ static void apply_impl(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int n
           flops += 8 * R(c, 0) * n2 * R(c, 1) * n3l * k;
         }
         Scope sc(h, "fwd_g2_zgemm", bytes, flops, st);
-        launch_zgemm(z, h->zgemm_ws.p, h->zgemm_ws.n, st);
+        launch_zgemm_dmma(z, h->zgemm_ws.p, h->zgemm_ws.n, st);
       }
       // ---- step 4: y = G1 Y2 into the voxel slab
       {
@@ -475,7 +475,7 @@ static void apply_impl(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int n
         flops += 8 * R(c, 0) * n2 * R(c, 1) * n3l * k;
       }
       Scope sc(h, "adj_g2_zgemm", bytes, flops, st);
-      launch_zgemm(z, h->zgemm_ws.p, h->zgemm_ws.n, st);
+      launch_zgemm_dmma(z, h->zgemm_ws.p, h->zgemm_ws.n, st);
     }
     // ---- z3 = G3^T W2, partial over the owned planes
     if (k == 1) {
@@ -491,7 +491,7 @@ static void apply_impl(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int n
         bytes += 16 * (R(c, 1) * n3l * R(c, 2) + R(c, 1) * n3l + R(c, 2));
       }
       Scope sc(h, "adj_g3_gemv", bytes, 8 * (bytes / 16), st);
-      launch_gemv_t(g, h->partials.p, (int64_t)h->partials.n, h->counters.p, max_splits, st);
+      launch_gemv_t(g, h->partials.p, (int64_t)h->partials.n, max_splits, st);
     } else {
       Zgemm z{};
       z.nbatch = 3;
@@ -536,7 +536,7 @@ static void apply_impl(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int n
         bytes += 16 * (R(c, 2) * s.mloc() + R(c, 2));
       }
       Scope sc(h, "adj_g4_gemv", bytes, 8 * (bytes / 16), st);
-      launch_gemv_t(g, h->partials.p, (int64_t)h->partials.n, h->counters.p, max_splits, st);
+      launch_gemv_t(g, h->partials.p, (int64_t)h->partials.n, max_splits, st);
     } else {
       Scope sc(h, "adj_g4_zgemm", 0, 0, st);
       for (int c = 0; c < 3; ++c) {

@@ -64,10 +64,8 @@ struct ApplyWorkspace;  // split-K partials + counters (handle-owned)
 
 // partials_cap: capacity (elements) of the split-K partial buffer; the split is
 // lowered so that it always fits.
-void launch_gemv_n(const GemvN& a, cplx* partials, int64_t partials_cap, unsigned* counters, int max_splits,
-                   cudaStream_t st);
-void launch_gemv_t(const GemvT& a, cplx* partials, int64_t partials_cap, unsigned* counters, int max_splits,
-                   cudaStream_t st);
+void launch_gemv_n(const GemvN& a, cplx* partials, int64_t partials_cap, int max_splits, cudaStream_t st);
+void launch_gemv_t(const GemvT& a, cplx* partials, int64_t partials_cap, int max_splits, cudaStream_t st);
 
 // Expansion y[chi][i1 + n1 c] = sum_a G1[i1 + n1 a] Y2[a + r1 c], c in [0, ncol),
 // with RHS blocks: column c belongs to rhs j = c / cols_per_rhs and is written at
@@ -115,6 +113,9 @@ struct Zgemm {
   int nbatch = 1;
 };
 void launch_zgemm(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t st);
+// same contract on FP64 tensor cores (DMMA), warp-tiled, for small / skinny
+// problems; op(B) must be N.
+void launch_zgemm_dmma(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t st);
 
 // conj in place
 void launch_conj(cplx* x, int64_t n, cudaStream_t st);

@@ -31,7 +31,7 @@ __device__ __forceinline__ cplx ldg_c(const cplx* p) { return __ldg(p); }
 // broadcast loads; 4 columns x G rows of loads in flight per thread.
 template <int G>
 __global__ void __launch_bounds__(kThreads) k_gemv_n(const __grid_constant__ GemvN a, cplx* __restrict__ partials,
-                                                     unsigned* __restrict__ counters, int64_t rmax) {
+                                                     int64_t rmax) {
   const int b = blockIdx.z;
   const int64_t R = a.R[b], C = a.C[b];
   const int64_t rt = blockIdx.y;
@@ -90,27 +90,65 @@ __global__ void __launch_bounds__(kThreads) k_gemv_n(const __grid_constant__ Gem
 #pragma unroll
   for (int g = 0; g < G; ++g)
     if (act[g]) partials[((int64_t)b * nsplit + s) * rmax + rows[g]] = acc[g];
-  __threadfence();
-  __syncthreads();
-  __shared__ bool last;
-  unsigned* ctr = counters + (int64_t)b * gridDim.y + rt;
-  if (threadIdx.x == 0) last = (atomicAdd(ctr, 1u) == (unsigned)(nsplit - 1));
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
+}
+
+struct SumArgs {
+  cplx* y[3];
+  int64_t n[3];
+  int nbatch;
+  bool conj_out;
+};
+
+// One warp per output: lanes stride over the splits, butterfly sum (fixed order).
+__global__ void __launch_bounds__(kThreads) k_sum_partials_warp(const __grid_constant__ SumArgs a,
+                                                                const cplx* __restrict__ partials, int nsplit,
+                                                                int64_t stride) {
+  const int b = blockIdx.y;
+  const int64_t r = blockIdx.x * (int64_t)(kThreads / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= a.n[b]) return;
+  const cplx* p = partials + (int64_t)b * nsplit * stride + r;
+  double sx = 0, sy = 0;
+  for (int q = lane; q < nsplit; q += 32) {
+    const cplx v = p[(int64_t)q * stride];
+    sx += v.x;
+    sy += v.y;
+  }
 #pragma unroll
-  for (int g = 0; g < G; ++g)
-    if (act[g]) {
-      cplx tot = cmk(0, 0);
-      for (int q = 0; q < nsplit; ++q) tot = cadd(tot, __ldcg(partials + ((int64_t)b * nsplit + q) * rmax + rows[g]));
-      a.y[b][rows[g]] = tot;
-    }
-  if (threadIdx.x == 0) *ctr = 0;
+  for (int o = 16; o > 0; o >>= 1) {
+    sx += __shfl_xor_sync(0xffffffffu, sx, o);
+    sy += __shfl_xor_sync(0xffffffffu, sy, o);
+  }
+  if (lane == 0) a.y[b][r] = cmk(sx, a.conj_out ? -sy : sy);
+}
+
+// y[b][r] = sum_q partials[(b * nsplit + q) * stride + r], fixed summation order
+// (4 interleaved partial sums combined at the end): deterministic.
+
+__global__ void __launch_bounds__(kThreads) k_sum_partials(const __grid_constant__ SumArgs a,
+                                                           const cplx* __restrict__ partials, int nsplit,
+                                                           int64_t stride) {
+  const int b = blockIdx.y;
+  const int64_t r = blockIdx.x * (int64_t)kThreads + threadIdx.x;
+  if (r >= a.n[b]) return;
+  const cplx* p = partials + (int64_t)b * nsplit * stride + r;
+  cplx s0 = cmk(0, 0), s1 = s0, s2 = s0, s3 = s0;
+  int q = 0;
+  for (; q + 4 <= nsplit; q += 4) {
+    s0 = cadd(s0, p[(int64_t)q * stride]);
+    s1 = cadd(s1, p[(int64_t)(q + 1) * stride]);
+    s2 = cadd(s2, p[(int64_t)(q + 2) * stride]);
+    s3 = cadd(s3, p[(int64_t)(q + 3) * stride]);
+  }
+  for (; q < nsplit; ++q) s0 = cadd(s0, p[(int64_t)q * stride]);
+  cplx v = cadd(cadd(s0, s1), cadd(s2, s3));
+  if (a.conj_out) v.y = -v.y;
+  a.y[b][r] = v;
 }
 
 constexpr int kWarps = kThreads / 32;
-constexpr int kCPW = 4;                     // columns per warp
-constexpr int kColsPerCta = kWarps * kCPW;  // 32
+constexpr int kCPW = 2;                     // columns per warp
+constexpr int kColsPerCta = kWarps * kCPW;  // 16
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -120,7 +158,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // y[c] = sum_r A[r + R c] x[r]  over rows [r0, r1) of this split.
 __global__ void __launch_bounds__(kThreads) k_gemv_t(const __grid_constant__ GemvT a, cplx* __restrict__ partials,
-                                                     unsigned* __restrict__ counters, int64_t cmax) {
+                                                     int64_t cmax) {
   const bool conj_out = a.conj_out;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ct = blockIdx.x;
@@ -192,23 +230,6 @@ __global__ void __launch_bounds__(kThreads) k_gemv_t(const __grid_constant__ Gem
     const int64_t c = cbase + lane;
     if (c < Cout) partials[((int64_t)bz * nsplit + s) * cmax + c] = v;
   }
-  __threadfence();
-  __syncthreads();
-  __shared__ bool last;
-  unsigned* ctr = counters + (int64_t)bz * gridDim.x + ct;
-  if (threadIdx.x == 0) last = (atomicAdd(ctr, 1u) == (unsigned)(nsplit - 1));
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  for (int t = threadIdx.x; t < kColsPerCta; t += kThreads) {
-    const int64_t c = (int64_t)ct * kColsPerCta + t;
-    if (c < Cout) {
-      cplx tot = cmk(0, 0);
-      for (int q = 0; q < nsplit; ++q) tot = cadd(tot, __ldcg(partials + ((int64_t)bz * nsplit + q) * cmax + c));
-      a.y[bz][c] = conj_out ? cconj(tot) : tot;
-    }
-  }
-  if (threadIdx.x == 0) *ctr = 0;
 }
 
 // ----------------------------------------------------------------------------- G1 steps on FP64 tensor cores
@@ -368,8 +389,7 @@ int pick_splits(int64_t other_ctas, int64_t len, int min_len, int max_splits) {
 
 }  // namespace
 
-void launch_gemv_n(const GemvN& a, cplx* partials, int64_t partials_cap, unsigned* counters, int max_splits,
-                   cudaStream_t st) {
+void launch_gemv_n(const GemvN& a, cplx* partials, int64_t partials_cap, int max_splits, cudaStream_t st) {
   int64_t rmax = 0, cmax = 0;
   for (int b = 0; b < a.nbatch; ++b) {
     rmax = std::max(rmax, a.R[b]);
@@ -381,17 +401,28 @@ void launch_gemv_n(const GemvN& a, cplx* partials, int64_t partials_cap, unsigne
   int ns = pick_splits(rtiles * a.nbatch, cmax, 16, max_splits);
   while (ns > 1 && (int64_t)a.nbatch * ns * rmax > partials_cap) --ns;
   dim3 grid(ns, (unsigned)rtiles, a.nbatch);
-  if (G == 1)
-    k_gemv_n<1><<<grid, kThreads, 0, st>>>(a, partials, counters, rmax);
-  else if (G == 2)
-    k_gemv_n<2><<<grid, kThreads, 0, st>>>(a, partials, counters, rmax);
-  else
-    k_gemv_n<4><<<grid, kThreads, 0, st>>>(a, partials, counters, rmax);
+  k_gemv_n<1><<<grid, kThreads, 0, st>>>(a, partials, rmax);
   VSIE_CHECK_LAUNCH();
+  (void)G;
+  if (ns > 1) {
+    SumArgs sa{};
+    sa.nbatch = a.nbatch;
+    for (int b = 0; b < a.nbatch; ++b) {
+      sa.y[b] = a.y[b];
+      sa.n[b] = a.R[b];
+    }
+    if (ns >= 16) {
+      dim3 g2((unsigned)ceil_div(rmax, kThreads / 32), a.nbatch);
+      k_sum_partials_warp<<<g2, kThreads, 0, st>>>(sa, partials, ns, rmax);
+    } else {
+      dim3 g2((unsigned)ceil_div(rmax, kThreads), a.nbatch);
+      k_sum_partials<<<g2, kThreads, 0, st>>>(sa, partials, ns, rmax);
+    }
+    VSIE_CHECK_LAUNCH();
+  }
 }
 
-void launch_gemv_t(const GemvT& a, cplx* partials, int64_t partials_cap, unsigned* counters, int max_splits,
-                   cudaStream_t st) {
+void launch_gemv_t(const GemvT& a, cplx* partials, int64_t partials_cap, int max_splits, cudaStream_t st) {
   int64_t rmax = 0, cmax = 0;
   for (int b = 0; b < a.nbatch; ++b) {
     rmax = std::max(rmax, a.R[b]);
@@ -403,8 +434,25 @@ void launch_gemv_t(const GemvT& a, cplx* partials, int64_t partials_cap, unsigne
   int ns = a.sum_batch ? 1 : pick_splits(ctiles * nz, rmax, 256, max_splits);
   while (ns > 1 && (int64_t)nz * ns * cmax > partials_cap) --ns;
   dim3 grid((unsigned)ctiles, ns, nz);
-  k_gemv_t<<<grid, kThreads, 0, st>>>(a, partials, counters, cmax);
+  k_gemv_t<<<grid, kThreads, 0, st>>>(a, partials, cmax);
   VSIE_CHECK_LAUNCH();
+  if (ns > 1) {
+    SumArgs sa{};
+    sa.nbatch = nz;
+    sa.conj_out = a.conj_out;
+    for (int b = 0; b < nz; ++b) {
+      sa.y[b] = a.y[b];
+      sa.n[b] = a.C[b];
+    }
+    if (ns >= 16) {
+      dim3 g2((unsigned)ceil_div(cmax, kThreads / 32), nz);
+      k_sum_partials_warp<<<g2, kThreads, 0, st>>>(sa, partials, ns, cmax);
+    } else {
+      dim3 g2((unsigned)ceil_div(cmax, kThreads), nz);
+      k_sum_partials<<<g2, kThreads, 0, st>>>(sa, partials, ns, cmax);
+    }
+    VSIE_CHECK_LAUNCH();
+  }
 }
 
 template <class F>

@@ -47,7 +47,7 @@ static zc opel(const std::vector<zc>& A, int64_t ld, int t, int64_t r, int64_t c
   return t == kC ? std::conj(v) : v;
 }
 
-void test_zgemm(int ta, int tb, int64_t M, int64_t N, int64_t K, bool ws) {
+void test_zgemm(int ta, int tb, int64_t M, int64_t N, int64_t K, bool ws, bool use_dmma = false) {
   int64_t lda = ta == kN ? M : K, ldb = tb == kN ? K : N;
   auto A = randv(lda * (ta == kN ? K : M)), B = randv(ldb * (tb == kN ? N : K)), Cc = randv(M * N);
   cplx *dA = up(A), *dB = up(B), *dC = up(Cc);
@@ -57,7 +57,7 @@ void test_zgemm(int ta, int tb, int64_t M, int64_t N, int64_t K, bool ws) {
   g.ta = (Trans)ta; g.tb = (Trans)tb; g.nbatch = 1;
   g.M[0] = M; g.N[0] = N; g.K[0] = K; g.A[0] = dA; g.lda[0] = lda; g.B[0] = dB; g.ldb[0] = ldb;
   g.C[0] = dC; g.ldc[0] = M; g.alpha = cmk(0.5, -1); g.beta = cmk(2, 0.25);
-  launch_zgemm(g, dws, ws ? 64 * M * N : 0, 0);
+  if (use_dmma) launch_zgemm_dmma(g, dws, ws ? 64 * M * N : 0, 0); else launch_zgemm(g, dws, ws ? 64 * M * N : 0, 0);
   auto got = down(dC, M * N);
   std::vector<zc> ref(M * N);
   for (int64_t j = 0; j < N; ++j)
@@ -67,7 +67,7 @@ void test_zgemm(int ta, int tb, int64_t M, int64_t N, int64_t K, bool ws) {
       ref[i + M * j] = zc(0.5, -1) * s + zc(2, 0.25) * Cc[i + M * j];
     }
   char buf[128];
-  snprintf(buf, sizeof buf, "zgemm ta%d tb%d %ldx%ldx%ld ws%d", ta, tb, (long)M, (long)N, (long)K, (int)ws);
+  snprintf(buf, sizeof buf, "zgemm%s ta%d tb%d %ldx%ldx%ld ws%d", use_dmma ? "_dmma" : "", ta, tb, (long)M, (long)N, (long)K, (int)ws);
   report(buf, relerr(got, ref));
   cudaFree(dA); cudaFree(dB); cudaFree(dC); if (dws) cudaFree(dws);
 }
@@ -80,14 +80,14 @@ void test_gemv_n(int64_t R, int64_t C) {
   unsigned* ctr; cudaMalloc(&ctr, 3 * 8192 * 4); cudaMemset(ctr, 0, 3 * 8192 * 4);
   GemvN g{};
   g.nbatch = 1; g.A[0] = dA; g.x[0] = dx; g.y[0] = dy; g.R[0] = R; g.C[0] = C;
-  launch_gemv_n(g, part, 3 * 1024 * (R + 256), ctr, 1024, 0);
+  launch_gemv_n(g, part, 3 * 1024 * (R + 256), 1024, 0);
   auto got = down(dy, R);
   std::vector<zc> ref(R, 0);
   for (int64_t c = 0; c < C; ++c) for (int64_t r = 0; r < R; ++r) ref[r] += A[r + R * c] * x[c];
   char buf[128]; snprintf(buf, sizeof buf, "gemv_n %ldx%ld", (long)R, (long)C);
   report(buf, relerr(got, ref));
   // run again: counters must have been reset
-  launch_gemv_n(g, part, 3 * 1024 * (R + 256), ctr, 1024, 0);
+  launch_gemv_n(g, part, 3 * 1024 * (R + 256), 1024, 0);
   report("gemv_n repeat", relerr(down(dy, R), ref));
   cudaFree(dA); cudaFree(dx); cudaFree(dy); cudaFree(part); cudaFree(ctr);
 }
@@ -105,7 +105,7 @@ void test_gemv_t(int64_t R, int64_t C, bool sum3) {
   }
   cplx* part; cudaMalloc(&part, 3 * 1024 * (C + 64) * 16);
   unsigned* ctr; cudaMalloc(&ctr, 3 * 8192 * 4); cudaMemset(ctr, 0, 3 * 8192 * 4);
-  launch_gemv_t(g, part, 3 * 1024 * (C + 64), ctr, 1024, 0);
+  launch_gemv_t(g, part, 3 * 1024 * (C + 64), 1024, 0);
   auto got = down(dy, C);
   std::vector<zc> ref(C, 0);
   for (int b = 0; b < nb; ++b)
@@ -165,6 +165,10 @@ int main() {
   test_zgemm(0, 0, 130, 70, 300, true);
   test_zgemm(1, 0, 63, 220, 2400, true);
   test_zgemm(2, 0, 200, 33, 1000, true);
+  for (int ta = 0; ta < 3; ++ta) test_zgemm(ta, 0, 84, 12, 31, false, true);
+  test_zgemm(0, 0, 1200, 110, 71, true, true);
+  test_zgemm(1, 0, 71, 110, 1200, true, true);
+  test_zgemm(2, 0, 37, 5, 1001, true, true);
   test_gemv_n(73, 1128);
   test_gemv_n(372, 73);
   test_gemv_n(1000, 3000);
