@@ -136,6 +136,12 @@ void vsie_build_opts_default(vsie_build_opts* opts);
 const char* vsie_status_string(int32_t status);
 const char* vsie_last_error_message(void);
 
+/* Slab partition of design (iii), host-only: rank `rank` of `world`
+ * owns voxel planes i3 in [slab[0], slab[1]) and G4 columns [cols[0], cols[1]);
+ * planes are split as n3 p / P, columns in equal padded chunks ceil(m / P) (the
+ * allgather of z needs equal counts).  Pure function, no CUDA call. */
+int32_t vsie_slab_partition(int32_t n3, int64_t m, int32_t world, int32_t rank, int32_t slab[2], int64_t cols[2]);
+
 /* 128-byte NCCL unique id for a multi-process group (rank 0 calls it and
  * broadcasts the bytes; every rank passes them in vsie_build_opts). */
 int32_t vsie_nccl_unique_id(void* out128);

@@ -57,6 +57,8 @@ _SIGS = {
     "vsie_status_string": (C.c_char_p, [C.c_int32]),
     "vsie_last_error_message": (C.c_char_p, []),
     "vsie_nccl_unique_id": (C.c_int32, [C.c_void_p]),
+    "vsie_slab_partition": (C.c_int32, [C.c_int32, C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int32),
+                                        C.POINTER(C.c_int64)]),
     "vsie_coupling_build": (C.c_int32, [C.POINTER(vsie_grid), C.POINTER(vsie_mesh), C.c_int32, C.c_double,
                                         C.c_double, C.POINTER(vsie_build_opts), C.POINTER(HANDLE)]),
     "vsie_coupling_import_cores": (C.c_int32, [C.POINTER(vsie_grid), C.POINTER(vsie_mesh), C.c_int32, C.c_double,

@@ -73,6 +73,14 @@ def _stream_ptr(stream):
     return C.c_void_p(s.cuda_stream)
 
 
+def slab_partition(n3: int, m: int, world: int, rank: int):
+    """(i3 range, G4 column range) owned by `rank` (vsie_slab_partition, host only)."""
+    sl = (C.c_int32 * 2)()
+    cl = (C.c_int64 * 2)()
+    check(lib().vsie_slab_partition(int(n3), int(m), int(world), int(rank), sl, cl))
+    return (sl[0], sl[1]), (cl[0], cl[1])
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     check(lib().vsie_nccl_unique_id(buf))

@@ -93,6 +93,16 @@ const char* vsie_status_string(int32_t s) {
 
 const char* vsie_last_error_message(void) { return g_last_error.c_str(); }
 
+int32_t vsie_slab_partition(int32_t n3, int64_t m, int32_t world, int32_t rank, int32_t slab[2], int64_t cols[2]) {
+  return guarded([&] {
+    VSIE_REQUIRE(slab != nullptr && cols != nullptr, VSIE_ERR_ARG, "NULL argument");
+    VSIE_REQUIRE(world >= 1 && rank >= 0 && rank < world && n3 >= world && m >= 1, VSIE_ERR_ARG,
+                 "bad partition arguments");
+    slab_partition(n3, m, world, rank, slab, cols);
+    return VSIE_OK;
+  });
+}
+
 int32_t vsie_nccl_unique_id(void* out128) {
   return guarded([&] {
     VSIE_REQUIRE(out128 != nullptr, VSIE_ERR_ARG, "out is NULL");

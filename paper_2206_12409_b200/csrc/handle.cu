@@ -155,20 +155,29 @@ void handle_init_geometry(vsie_coupling_s* h, const vsie_grid* grid, const vsie_
   handle_partition(h);
 }
 
+void slab_partition(int n3, int64_t m, int world, int rank, int slab[2], int64_t cols[2]) {
+  const int64_t mp = ceil_div(m, world);
+  slab[0] = (int)((int64_t)n3 * rank / world);
+  slab[1] = (int)((int64_t)n3 * (rank + 1) / world);
+  cols[0] = std::min(m, mp * rank);
+  cols[1] = std::min(m, mp * (rank + 1));
+}
+
 void handle_partition(vsie_coupling_s* h) {
   const int P = h->world;
-  const int n3 = h->grid.n[2];
-  const int64_t mp = ceil_div(h->m, P);
   h->shards.clear();
   const int first = h->loopback ? 0 : h->rank;
   const int last = h->loopback ? P : h->rank + 1;
   h->shards.resize(last - first);
   for (int p = first; p < last; ++p) {
     Shard& s = h->shards[p - first];
-    s.i3b = (int)((int64_t)n3 * p / P);
-    s.i3e = (int)((int64_t)n3 * (p + 1) / P);
-    s.cb = std::min(h->m, mp * p);
-    s.ce = std::min(h->m, mp * (p + 1));
+    int sl[2];
+    int64_t cl[2];
+    slab_partition(h->grid.n[2], h->m, P, p, sl, cl);
+    s.i3b = sl[0];
+    s.i3e = sl[1];
+    s.cb = cl[0];
+    s.ce = cl[1];
   }
 }
 

@@ -79,6 +79,7 @@ namespace vsie {
 void handle_init_geometry(vsie_coupling_s* h, const vsie_grid* grid, const vsie_mesh* meshes, int n_meshes,
                           double freq, const vsie_build_opts* opts);
 void handle_partition(vsie_coupling_s* h);
+void slab_partition(int n3, int64_t m, int world, int rank, int slab[2], int64_t cols[2]);
 // installs full cores (host, column-major) for component chi; keeps the owned shards
 void handle_set_cores_host(vsie_coupling_s* h, int chi, const int r[3], const cplx* const host[4]);
 // same from device buffers (full cores on this device)
