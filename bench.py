@@ -241,12 +241,18 @@ def main():
     if world > 1:
         dist.barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    launches0 = h.info()["apply_launches"]
-    h.set_timing(True)
     with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
+        # keep the GPU under the same load for >= 0.6 s so that the 200 ms clock
+        # samples see it (untimed), then the timed region
+        t_end = time.perf_counter() + 0.6
+        while time.perf_counter() < t_end:
+            for _ in range(20):
+                flush.fill_(1)
+                step()
+            torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        launches0 = h.info()["apply_launches"]
         for i in range(args.steps):
             flush.fill_(i & 0xFF)                     # evict L2 between timed steps
             ev[i][0].record(stream)
@@ -256,10 +262,18 @@ def main():
         if world > 1:
             dist.barrier()
     launches = h.info()["apply_launches"] - launches0
-    timers = h.timers()
-    h.set_timing(False)
     per = [a.elapsed_time(b) for a, b in ev]
     ms = float(np.mean(per))
+    # per-kernel CUDA-event timing: a second pass of the same K steps (same stream,
+    # same inputs, L2 flushed) directly after the timed region, so the headline is
+    # not perturbed by the event records between kernels
+    h.set_timing(True)
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        step()
+    torch.cuda.synchronize()
+    timers = h.timers()
+    h.set_timing(False)
     if world > 1:
         tt = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -360,6 +374,7 @@ def main():
         "e2e": {"value": B / e2e_s / 1e9, "unit": "GB/s", "ms_per_step": e2e_s * 1e3,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
+        "gpu_launches_note": "kernel launches of this library inside the K timed steps (count from the library's launch counter; includes split-K sum kernels)",
         "clocks": clk.summary(),
     }
     print(json.dumps(line))

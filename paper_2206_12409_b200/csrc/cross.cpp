@@ -42,6 +42,7 @@ uint64_t host_splitmix(uint64_t& s) {
 
 struct Ws {
   DevBuf<cplx> M, J, V, Y, Q, Bh, basis, Bp, Bout, T, Lr, omega, Vr, rowbuf;
+  DevBuf<cplx> G, Rinv, Rt, Rtmp, Ra, Rb, Atmp, zws, other;
   DevBuf<double> norms, frob_partial, frob;
   DevBuf<int> perm, piv_pos, idx, bad;
   DevBuf<ArgMax> partials;
@@ -62,6 +63,7 @@ struct Ctx {
   double t_entry = 0, t_factor = 0, t_maxvol = 0;
   int64_t n_eval = 0;
   int64_t jacobi_sweeps = 0;
+  double t_jsmall = 0, t_jtall = 0, t_gram = 0, t_chol = 0, t_gemm = 0;
 };
 
 void sync(Ctx& c) { VSIE_CHECK_CUDA(cudaStreamSynchronize(c.st)); }
@@ -98,14 +100,33 @@ void jacobi(Ctx& c, cplx* A, int64_t p, int q, cplx* V) {
   // (tol / sqrt 3 >= 5.8e-9) — while avoiding the long tail of sweeps that
   // a sqrt(p) eps threshold spends on rounding noise.
   const double thr = std::max(1e-12, std::sqrt((double)p) * 2.3e-16);
+  c.ws.frob_partial.ensure(1024);
+  c.ws.frob.ensure(1);
+  launch_frob2(A, p * q, c.ws.frob_partial.p, c.ws.frob.p, c.st);
+  double fro2 = 0;
+  VSIE_CHECK_CUDA(cudaMemcpyAsync(&fro2, c.ws.frob.p, sizeof(double), cudaMemcpyDeviceToHost, c.st));
+  sync(c);
+  // columns below 1e-14 ||A||_F are numerical zeros (never rotated)
+  const double small2 = 1e-28 * fro2;
+  c.ws.rotcnt.ensure(3);
+  VSIE_CHECK_CUDA(cudaMemsetAsync(c.ws.rotcnt.p, 0, 3 * sizeof(unsigned), c.st));
+  if (launch_jacobi_coop(A, p, p, V, q, sch, Q / 2, Q - 1, thr, small2, 40, c.ws.rotcnt.p, c.st)) {
+    unsigned hs[3];
+    VSIE_CHECK_CUDA(cudaMemcpyAsync(hs, c.ws.rotcnt.p, sizeof(hs), cudaMemcpyDeviceToHost, c.st));
+    sync(c);
+    c.jacobi_sweeps += hs[2];
+    if (c.o.verbose >= 2) fprintf(stderr, "    jacobi(coop) p=%ld q=%d sweeps %u\n", (long)p, q, hs[2]);
+    return;
+  }
   for (int sweep = 0; sweep < 40; ++sweep) {
     c.jacobi_sweeps++;
     VSIE_CHECK_CUDA(cudaMemsetAsync(c.ws.rotcnt.p, 0, sizeof(unsigned), c.st));
     for (int t = 0; t < Q - 1; ++t)
-      launch_jacobi_round(A, p, p, V, q, sch + (int64_t)t * (Q / 2), Q / 2, thr, c.ws.rotcnt.p, c.st);
+      launch_jacobi_round(A, p, p, V, q, sch + (int64_t)t * (Q / 2), Q / 2, thr, small2, c.ws.rotcnt.p, c.st);
     unsigned cnt = 0;
     VSIE_CHECK_CUDA(cudaMemcpyAsync(&cnt, c.ws.rotcnt.p, sizeof(unsigned), cudaMemcpyDeviceToHost, c.st));
     sync(c);
+    if (c.o.verbose >= 2) fprintf(stderr, "    jacobi p=%ld q=%d sweep %d rotations %u\n", (long)p, q, sweep, cnt);
     if (cnt == 0) return;
   }
 }
@@ -154,13 +175,89 @@ void zgemm1(Ctx& c, Trans ta, Trans tb, int64_t M, int64_t N, int64_t K, const c
   z.A[0] = A; z.lda[0] = lda;
   z.B[0] = B; z.ldb[0] = ldb;
   z.C[0] = C; z.ldc[0] = ldc;
-  launch_zgemm(z, nullptr, 0, c.st);
+  if (!c.ws.zws.p) c.ws.zws.alloc((size_t)16 << 20);  // split-K partials (256 MiB)
+  launch_zgemm(z, c.ws.zws.p, (int64_t)c.ws.zws.n, c.st);
+}
+
+void set_identity(Ctx& c, DevBuf<cplx>& V, int q) {
+  V.ensure((int64_t)q * q);
+  std::vector<cplx> I((size_t)q * q, cmk(0, 0));
+  for (int j = 0; j < q; ++j) I[(size_t)j * q + j] = cmk(1, 0);
+  VSIE_CHECK_CUDA(cudaMemcpyAsync(V.p, I.data(), I.size() * sizeof(cplx), cudaMemcpyHostToDevice, c.st));
+  sync(c);
+}
+
+// Gram-preconditioned one-sided Jacobi SVD of a tall A (p x q): the eigenvectors
+// V1 of G = A^H A (one-sided Jacobi on the q x q Cholesky factor of G + s I; the
+// shift only guards the factorisation, eigenvectors are unchanged) make the
+// columns of A V1 orthogonal except among singular values below sqrt(u) ||A||,
+// so the final one-sided Jacobi on the tall A V1 converges in a few sweeps while
+// keeping the one-sided method's relative accuracy.  On exit A holds U S and
+// V (if given) the accumulated right singular vectors V1 V2.
+void precond_jacobi(Ctx& c, cplx* A, int64_t p, int q, cplx* V) {
+  Ws& w = c.ws;
+  if (q <= 1) {
+    if (V) {
+      set_identity(c, w.Rtmp, 1);
+      VSIE_CHECK_CUDA(cudaMemcpyAsync(V, w.Rtmp.p, sizeof(cplx), cudaMemcpyDeviceToDevice, c.st));
+    }
+    return;
+  }
+  const int64_t qq = (int64_t)q * q;
+  w.G.ensure(qq);
+  w.Rtmp.ensure(qq);
+  w.Atmp.ensure(p * q);
+  w.frob.ensure(1);
+  w.bad.ensure(1);
+  VSIE_CHECK_CUDA(cudaMemsetAsync(w.bad.p, 0, sizeof(int), c.st));
+  auto t0 = Clock::now();
+  zgemm1(c, kC, kN, q, q, p, A, p, A, p, w.G.p, q);
+  launch_trace_real(w.G.p, q, w.frob.p, c.st);
+  double tr = 0;
+  VSIE_CHECK_CUDA(cudaMemcpyAsync(&tr, w.frob.p, sizeof(double), cudaMemcpyDeviceToHost, c.st));
+  sync(c);
+  if (!(tr > 0)) {
+    if (V) {
+      set_identity(c, w.Rtmp, q);
+      VSIE_CHECK_CUDA(cudaMemcpyAsync(V, w.Rtmp.p, qq * sizeof(cplx), cudaMemcpyDeviceToDevice, c.st));
+    }
+    return;
+  }
+  c.t_gram += secs(t0);
+  t0 = Clock::now();
+  launch_add_diag(w.G.p, q, 1e-13 * tr, c.st);
+  launch_cholesky_upper(w.G.p, q, w.bad.p, c.st);
+  int bad = 0;
+  VSIE_CHECK_CUDA(cudaMemcpyAsync(&bad, w.bad.p, sizeof(int), cudaMemcpyDeviceToHost, c.st));
+  sync(c);
+  c.t_chol += secs(t0);
+  set_identity(c, w.Ra, q);
+  cplx* V1 = w.Ra.p;
+  if (!bad) {
+    t0 = Clock::now();
+    jacobi(c, w.G.p, q, q, V1);  // G now holds R V1 (not needed)
+    c.t_jsmall += secs(t0);
+    t0 = Clock::now();
+    zgemm1(c, kN, kN, p, q, q, A, p, V1, q, w.Atmp.p, p);
+    VSIE_CHECK_CUDA(cudaMemcpyAsync(A, w.Atmp.p, p * q * sizeof(cplx), cudaMemcpyDeviceToDevice, c.st));
+    sync(c);
+    c.t_gemm += secs(t0);
+  }
+  w.Rb.ensure(qq);
+  set_identity(c, w.Rb, q);
+  t0 = Clock::now();
+  jacobi(c, A, p, q, w.Rb.p);
+  c.t_jtall += secs(t0);
+  if (V) zgemm1(c, kN, kN, q, q, q, V1, q, w.Rb.p, q, V, q);
 }
 
 // Rank-revealing factorisation of M (rows x cols, ld rows).
 //  left = true : ws.basis <- rows x r basis of the dominant column space (L of L->R)
 //  left = false: ws.basis <- cols x r basis R with M ~ X R^T (R->L)
-int factorize(Ctx& c, const cplx* M, int64_t rows, int64_t cols, bool left, int r_prev) {
+// other != null also receives the basis of the opposite side (right basis R for
+// left = true, left basis L for left = false) of the same truncated SVD, so that
+// the half-sweep turnaround on the same supercore needs no second factorisation.
+int factorize(Ctx& c, const cplx* M, int64_t rows, int64_t cols, bool left, int r_prev, DevBuf<cplx>* other) {
   Ws& w = c.ws;
   const int64_t mn = std::min(rows, cols);
   const int cap = (int)std::min<int64_t>(c.o.max_rank, mn);
@@ -174,13 +271,7 @@ int factorize(Ctx& c, const cplx* M, int64_t rows, int64_t cols, bool left, int 
     else
       launch_transpose(M, rows, cols, w.J.p, true, c.st);  // M^H
     w.V.ensure((int64_t)q * q);
-    {
-      std::vector<cplx> I((size_t)q * q, cmk(0, 0));
-      for (int j = 0; j < q; ++j) I[(size_t)j * q + j] = cmk(1, 0);
-      VSIE_CHECK_CUDA(cudaMemcpyAsync(w.V.p, I.data(), I.size() * sizeof(cplx), cudaMemcpyHostToDevice, c.st));
-      sync(c);
-    }
-    jacobi(c, w.J.p, p, q, w.V.p);
+    precond_jacobi(c, w.J.p, p, q, w.V.p);
     auto s = sorted_norms(c, w.J.p, p, q);
     double total2 = 0;
     for (auto& e : s) total2 += e.first * e.first;
@@ -200,6 +291,21 @@ int factorize(Ctx& c, const cplx* M, int64_t rows, int64_t cols, bool left, int 
         launch_gather_cols(w.V.p, cols, q, c.ws.idx.p, nullptr, r, w.basis.p, cols, true, c.st);
       else
         launch_gather_cols(w.J.p, cols, cols, c.ws.idx.p, nullptr, r, w.basis.p, cols, true, c.st);
+    }
+    if (other) {
+      if (left) {  // right basis conj(V_sel) (tall) or conj(M^H V_sel) (wide)
+        other->ensure(cols * r);
+        if (tall)
+          launch_gather_cols(w.V.p, cols, q, c.ws.idx.p, nullptr, r, other->p, cols, true, c.st);
+        else
+          launch_gather_cols(w.J.p, cols, cols, c.ws.idx.p, nullptr, r, other->p, cols, true, c.st);
+      } else {     // left basis M V_sel (tall) or V_sel (wide)
+        other->ensure(rows * r);
+        if (tall)
+          launch_gather_cols(w.J.p, rows, rows, c.ws.idx.p, nullptr, r, other->p, rows, false, c.st);
+        else
+          launch_gather_cols(w.V.p, rows, q, c.ws.idx.p, nullptr, r, other->p, rows, false, c.st);
+      }
     }
     return r;
   }
@@ -232,7 +338,7 @@ int factorize(Ctx& c, const cplx* M, int64_t rows, int64_t cols, bool left, int 
       zgemm1(c, kN, kN, rows, kk, cols, M, rows, w.omega.p, cols, w.Y.p, rows);
     else
       zgemm1(c, kC, kN, cols, kk, rows, M, rows, w.omega.p, rows, w.Y.p, cols);
-    jacobi(c, w.Y.p, p1, kk, nullptr);
+    precond_jacobi(c, w.Y.p, p1, kk, nullptr);
     auto sy = sorted_norms(c, w.Y.p, p1, kk);
     std::vector<int> keep;
     std::vector<double> inv;
@@ -254,13 +360,7 @@ int factorize(Ctx& c, const cplx* M, int64_t rows, int64_t cols, bool left, int 
     else
       zgemm1(c, kN, kN, rows, kq, cols, M, rows, w.Q.p, cols, w.Bh.p, rows);
     w.V.ensure((int64_t)kq * kq);
-    {
-      std::vector<cplx> I((size_t)kq * kq, cmk(0, 0));
-      for (int j = 0; j < kq; ++j) I[(size_t)j * kq + j] = cmk(1, 0);
-      VSIE_CHECK_CUDA(cudaMemcpyAsync(w.V.p, I.data(), I.size() * sizeof(cplx), cudaMemcpyHostToDevice, c.st));
-      sync(c);
-    }
-    jacobi(c, w.Bh.p, p2, kq, w.V.p);
+    precond_jacobi(c, w.Bh.p, p2, kq, w.V.p);
     auto s = sorted_norms(c, w.Bh.p, p2, kq);
     const int r = choose_rank(s, total2, true, c.delta, std::min(cap, kq));
     if (r > kq - os && kk < mn) {
@@ -275,6 +375,10 @@ int factorize(Ctx& c, const cplx* M, int64_t rows, int64_t cols, bool left, int 
     w.basis.ensure(p1 * r);
     zgemm1(c, kN, kN, p1, r, kq, w.Q.p, p1, w.Vr.p, kq, w.basis.p, p1);
     if (!left) launch_conj(w.basis.p, p1 * r, c.st);
+    if (other) {  // Bh V = U S: conj for the right basis (L->R), as is for the left basis (R->L)
+      other->ensure(p2 * r);
+      launch_gather_cols(w.Bh.p, p2, p2, c.ws.idx.p, nullptr, r, other->p, p2, left, c.st);
+    }
     return r;
   }
 }
@@ -484,15 +588,25 @@ int cross_chi(Ctx& c, int chi, Heldout& ho) {
   int prev[3] = {-1, -1, -1};
   int sweeps = 0;
   bool reuse = false;  // ws.M already holds the next supercore
+  int reuse_r = 0;     // ... and ws.other holds its opposite-side basis of rank reuse_r
   int64_t rows = 0, cols = 0;
   for (int sweep = 1; sweep <= c.o.max_sweeps; ++sweep) {
     sweeps = sweep;
     // ---------------- left-to-right
     for (int k = 1; k <= 3; ++k) {
-      if (!reuse) eval_supercore(c, s, k, rows, cols);
-      reuse = false;
       auto t0 = Clock::now();
-      const int r = factorize(c, c.ws.M.p, rows, cols, true, s.r[k]);
+      int r;
+      if (reuse) {  // same M_1 as the last R->L step: its left basis is ready
+        r = reuse_r;
+        c.ws.basis.ensure(rows * r);
+        VSIE_CHECK_CUDA(cudaMemcpyAsync(c.ws.basis.p, c.ws.other.p, rows * r * sizeof(cplx),
+                                        cudaMemcpyDeviceToDevice, c.st));
+      } else {
+        eval_supercore(c, s, k, rows, cols);
+        t0 = Clock::now();
+        r = factorize(c, c.ws.M.p, rows, cols, true, s.r[k], k == 3 ? &c.ws.other : nullptr);
+      }
+      reuse = false;
       sync(c);
       c.t_factor += secs(t0);
       t0 = Clock::now();
@@ -512,16 +626,26 @@ int cross_chi(Ctx& c, int chi, Heldout& ho) {
         upload_idx(c, P);
         s.core[3].ensure((int64_t)r * cols);
         launch_gather_rows(c.ws.M.p, rows, c.ws.idx.p, r, cols, s.core[3].p, c.st);
-        reuse = true;  // R->L starts with the same M_3
+        reuse = true;  // R->L starts with the same M_3 (right basis in ws.other)
+        reuse_r = r;
       }
       s.r[k] = r;
     }
     // ---------------- right-to-left
     for (int k = 3; k >= 1; --k) {
-      if (!reuse) eval_supercore(c, s, k, rows, cols);
-      reuse = false;
       auto t0 = Clock::now();
-      const int r = factorize(c, c.ws.M.p, rows, cols, false, s.r[k]);
+      int r;
+      if (reuse) {  // same M_3 as the last L->R step: its right basis is ready
+        r = reuse_r;
+        c.ws.basis.ensure(cols * r);
+        VSIE_CHECK_CUDA(cudaMemcpyAsync(c.ws.basis.p, c.ws.other.p, cols * r * sizeof(cplx),
+                                        cudaMemcpyDeviceToDevice, c.st));
+      } else {
+        eval_supercore(c, s, k, rows, cols);
+        t0 = Clock::now();
+        r = factorize(c, c.ws.M.p, rows, cols, false, s.r[k], k == 1 ? &c.ws.other : nullptr);
+      }
+      reuse = false;
       sync(c);
       c.t_factor += secs(t0);
       t0 = Clock::now();
@@ -543,15 +667,17 @@ int cross_chi(Ctx& c, int chi, Heldout& ho) {
         upload_idx(c, Q);
         s.core[0].ensure(rows * r);
         launch_gather_cols(c.ws.M.p, rows, rows, c.ws.idx.p, nullptr, r, s.core[0].p, rows, false, c.st);
-        reuse = true;  // the next L->R starts with the same M_1
+        reuse = true;  // the next L->R starts with the same M_1 (left basis in ws.other)
+        reuse_r = r;
       }
       s.r[k] = r;
     }
     sync(c);
     const double e = heldout_error(c, s, ho);
     if (c.o.verbose)
-      fprintf(stderr, "[vsie cross] chi %d sweep %d ranks (%d, %d, %d) heldout %.3e  (entry %.2fs factor %.2fs maxvol %.2fs, jacobi sweeps %ld)\n",
-              chi, sweep, s.r[1], s.r[2], s.r[3], e, c.t_entry, c.t_factor, c.t_maxvol, (long)c.jacobi_sweeps);
+      fprintf(stderr, "[vsie cross] chi %d sweep %d ranks (%d, %d, %d) heldout %.3e  (entry %.2fs factor %.2fs [gram %.2f chol %.2f jsmall %.2f gemm %.2f jtall %.2f] maxvol %.2fs, jacobi sweeps %ld)\n",
+              chi, sweep, s.r[1], s.r[2], s.r[3], e, c.t_entry, c.t_factor, c.t_gram, c.t_chol, c.t_jsmall, c.t_gemm,
+              c.t_jtall, c.t_maxvol, (long)c.jacobi_sweeps);
     if (e < best_e) {
       best_e = e;
       for (int k = 0; k < 5; ++k) best_r[k] = s.r[k];

@@ -11,6 +11,8 @@
 //   ties broken towards the smallest (original row, column) as in the oracle.
 #include "crosskern.cuh"
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 
 namespace vsie {
@@ -58,11 +60,10 @@ __device__ __forceinline__ void block_sum(double (&v)[N], double* sh /* >= 8 * N
   }
 }
 
-__global__ void __launch_bounds__(NT) k_jacobi_round(cplx* A, int64_t p, int64_t lda, cplx* V, int64_t q,
-                                                     const int2* pairs, double thr, unsigned* cnt) {
-  const int2 pr = pairs[blockIdx.x];
-  const int i = pr.x, j = pr.y;
-  if (i >= q || j >= q) return;
+// one Jacobi rotation of columns (i, j) of A (and V), by one CTA; returns 1 if rotated
+__device__ int jacobi_pair(cplx* A, int64_t p, int64_t lda, cplx* V, int64_t q, int i, int j, double thr,
+                           double small2, double* sh) {
+  if (i >= q || j >= q) return 0;
   cplx* Ai = A + lda * i;
   cplx* Aj = A + lda * j;
   double v[4] = {0, 0, 0, 0};
@@ -73,11 +74,12 @@ __global__ void __launch_bounds__(NT) k_jacobi_round(cplx* A, int64_t p, int64_t
     v[2] += x.x * y.x + x.y * y.y;  // Re(conj(x) y)
     v[3] += x.x * y.y - x.y * y.x;  // Im(conj(x) y)
   }
-  __shared__ double sh[8 * 4];
   block_sum<4>(v, sh);
   const double a = v[0], b = v[1];
   const double cabs = sqrt(v[2] * v[2] + v[3] * v[3]);
-  if (!(a > 0 && b > 0) || !(cabs > thr * sqrt(a) * sqrt(b))) return;
+  // columns below the noise floor (||a||^2 <= small2) are treated as zero (as in
+  // LAPACK xGESVJ): rotating them against large columns only re-injects rounding noise
+  if (!(a > small2 && b > small2) || !(cabs > thr * sqrt(a) * sqrt(b))) return 0;
   const double zeta = (b - a) / (2.0 * cabs);
   const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
   const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
@@ -99,7 +101,42 @@ __global__ void __launch_bounds__(NT) k_jacobi_round(cplx* A, int64_t p, int64_t
       Vj[r] = cmk(sn * x.x + qy.x, sn * x.y + qy.y);
     }
   }
-  if (threadIdx.x == 0) atomicAdd(cnt, 1u);
+  return 1;
+}
+
+__global__ void __launch_bounds__(NT) k_jacobi_round(cplx* A, int64_t p, int64_t lda, cplx* V, int64_t q,
+                                                     const int2* pairs, double thr, double small2, unsigned* cnt) {
+  __shared__ double sh[8 * 4];
+  const int2 pr = pairs[blockIdx.x];
+  if (jacobi_pair(A, p, lda, V, q, pr.x, pr.y, thr, small2, sh) && threadIdx.x == 0) atomicAdd(cnt, 1u);
+}
+
+// All sweeps of a cyclic one-sided Jacobi in ONE cooperative launch: CTA k owns
+// pair slot k of every round, rounds are separated by grid-wide barriers, and
+// the sweep loop ends (uniformly) when a sweep applied no rotation.
+// cnt[0..1]: alternating per-sweep rotation counters (zeroed by the host);
+// cnt[2] receives the number of sweeps.
+__global__ void __launch_bounds__(NT) k_jacobi_coop(cplx* A, int64_t p, int64_t lda, cplx* V, int64_t q,
+                                                    const int2* pairs, int nrounds, double thr, double small2,
+                                                    int max_sweeps, unsigned* cnt) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[8 * 4];
+  const int half = gridDim.x;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    unsigned* mine = cnt + (sweep & 1);
+    if (blockIdx.x == 0 && threadIdx.x == 0) cnt[(sweep + 1) & 1] = 0;
+    for (int t = 0; t < nrounds; ++t) {
+      const int2 pr = pairs[(int64_t)t * half + blockIdx.x];
+      if (jacobi_pair(A, p, lda, V, q, pr.x, pr.y, thr, small2, sh) && threadIdx.x == 0) atomicAdd(mine, 1u);
+      grid.sync();
+    }
+    const unsigned rot = *((volatile unsigned*)mine);
+    if (rot == 0) break;
+    grid.sync();  // everyone has read `mine` before it is zeroed in the next-but-one sweep
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) cnt[2] = (unsigned)(sweep + 1);
 }
 
 __global__ void __launch_bounds__(NT) k_col_norms(const cplx* A, int64_t p, int64_t lda, double* out) {
@@ -381,6 +418,95 @@ __global__ void k_scatter_rows(const cplx* B, int64_t n, int r, const int* perm,
   }
 }
 
+__global__ void k_add_diag(cplx* G, int q, double s) {
+  for (int i = blockIdx.x * NT + threadIdx.x; i < q; i += gridDim.x * NT) G[i + (int64_t)q * i].x += s;
+}
+
+__global__ void k_trace_real(const cplx* G, int q, double* out) {
+  double v[1] = {0};
+  for (int i = threadIdx.x; i < q; i += NT) v[0] += G[i + (int64_t)q * i].x;
+  __shared__ double sh[8];
+  block_sum<1>(v, sh);
+  if (threadIdx.x == 0) *out = v[0];
+}
+
+// one right-looking step j of the upper Cholesky on the unscaled rows:
+// G[a, b] -= conj(G[j, a]) G[j, b] / G[j, j] for j < a <= b (upper part)
+__global__ void k_chol_step(cplx* G, int q, int j) {
+  const int64_t n = q - j - 1;
+  const int64_t total = n * n;
+  const double d = G[j + (int64_t)q * j].x;
+  const double inv = d > 0 ? 1.0 / d : 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)NT + threadIdx.x; e < total; e += (int64_t)gridDim.x * NT) {
+    const int64_t a = j + 1 + e % n, b = j + 1 + e / n;
+    if (a > b) continue;
+    const cplx ga = G[j + (int64_t)q * a], gb = G[j + (int64_t)q * b];
+    cplx v = G[a + (int64_t)q * b];
+    // conj(ga) * gb * inv
+    const double re = (ga.x * gb.x + ga.y * gb.y) * inv, im = (ga.x * gb.y - ga.y * gb.x) * inv;
+    v.x -= re;
+    v.y -= im;
+    G[a + (int64_t)q * b] = v;
+  }
+}
+
+// final scaling: R[j, c] = G[j, c] / sqrt(G[j, j]) (c >= j), zero below the diagonal
+__global__ void k_chol_finish(cplx* G, int q, int* bad) {
+  const int64_t total = (int64_t)q * q;
+  for (int64_t e = blockIdx.x * (int64_t)NT + threadIdx.x; e < total; e += (int64_t)gridDim.x * NT) {
+    const int64_t j = e % q, c = e / q;
+    if (j > c) {
+      G[e] = cmk(0, 0);
+      continue;
+    }
+    const double d = G[j + (int64_t)q * j].x;
+    if (!(d > 0)) {
+      if (bad) *bad = 1;
+      continue;
+    }
+    const double s = 1.0 / sqrt(d);
+    if (j == c) {
+      G[e] = cmk(sqrt(d), 0.0);
+    } else {
+      const cplx v = G[e];
+      G[e] = cmk(v.x * s, v.y * s);
+    }
+  }
+}
+
+// X[:, c] = R^{-1} e_c, back substitution on the row-major copy Rt (Rt[i q + k] = R[i, k])
+__global__ void __launch_bounds__(128) k_upper_inverse(const cplx* Rt, int q, cplx* X) {
+  extern __shared__ cplx xcol[];
+  __shared__ double sh[8 * 2];
+  const int c = blockIdx.x;
+  for (int k = threadIdx.x; k < q; k += blockDim.x) xcol[k] = cmk(0, 0);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const cplx d = Rt[(int64_t)c * q + c];
+    const double n2 = cabs2(d);
+    xcol[c] = cmk(d.x / n2, -d.y / n2);
+  }
+  __syncthreads();
+  for (int i = c - 1; i >= 0; --i) {
+    double v[2] = {0, 0};
+    const cplx* row = Rt + (int64_t)i * q;
+    for (int k = i + 1 + threadIdx.x; k <= c; k += blockDim.x) {
+      const cplx r = row[k], x = xcol[k];
+      v[0] += r.x * x.x - r.y * x.y;
+      v[1] += r.x * x.y + r.y * x.x;
+    }
+    block_sum<2>(v, sh);
+    if (threadIdx.x == 0) {
+      const cplx d = row[i];
+      const double n2 = cabs2(d);
+      const cplx di = cmk(d.x / n2, -d.y / n2);
+      xcol[i] = cmul(cmk(-v[0], -v[1]), di);
+    }
+    __syncthreads();
+  }
+  for (int k = threadIdx.x; k < q; k += blockDim.x) X[k + (int64_t)q * c] = xcol[k];
+}
+
 unsigned grid1(int64_t work) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, NT), 148 * 16)); }
 
 }  // namespace
@@ -392,9 +518,26 @@ void launch_gaussian(cplx* out, int64_t n, uint64_t seed, cudaStream_t st) {
 }
 
 void launch_jacobi_round(cplx* A, int64_t p, int64_t lda, cplx* V, int64_t q, const int2* pairs, int npairs,
-                         double thr, unsigned* cnt, cudaStream_t st) {
-  k_jacobi_round<<<npairs, NT, 0, st>>>(A, p, lda, V, q, pairs, thr, cnt);
+                         double thr, double small2, unsigned* cnt, cudaStream_t st) {
+  k_jacobi_round<<<npairs, NT, 0, st>>>(A, p, lda, V, q, pairs, thr, small2, cnt);
   VSIE_CHECK_LAUNCH();
+}
+
+bool launch_jacobi_coop(cplx* A, int64_t p, int64_t lda, cplx* V, int64_t q, const int2* pairs, int npairs,
+                        int nrounds, double thr, double small2, int max_sweeps, unsigned* cnt, cudaStream_t st) {
+  static int max_blocks = -1;
+  if (max_blocks < 0) {
+    int per_sm = 0, dev = 0, sms = 0;
+    VSIE_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi_coop, NT, 0));
+    VSIE_CHECK_CUDA(cudaGetDevice(&dev));
+    VSIE_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    max_blocks = per_sm * sms;
+  }
+  if (npairs > max_blocks) return false;
+  void* args[] = {&A, &p, &lda, &V, &q, (void*)&pairs, &nrounds, &thr, &small2, &max_sweeps, &cnt};
+  VSIE_CHECK_CUDA(cudaLaunchCooperativeKernel((void*)k_jacobi_coop, dim3(npairs), dim3(NT), args, 0, st));
+  VSIE_COUNT_LAUNCH();
+  return true;
 }
 
 void launch_col_norms(const cplx* A, int64_t p, int64_t q, int64_t lda, double* out, cudaStream_t st) {
@@ -429,6 +572,37 @@ void launch_transpose(const cplx* src, int64_t R, int64_t C, cplx* dst, bool con
   if (R <= 0 || C <= 0) return;
   dim3 g((unsigned)ceil_div(R, 32), (unsigned)ceil_div(C, 32));
   k_transpose<<<g, NT, 0, st>>>(src, R, C, dst, conj ? 1 : 0);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_add_diag(cplx* G, int q, double s, cudaStream_t st) {
+  k_add_diag<<<grid1(q), NT, 0, st>>>(G, q, s);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_trace_real(const cplx* G, int q, double* out, cudaStream_t st) {
+  k_trace_real<<<1, NT, 0, st>>>(G, q, out);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_cholesky_upper(cplx* G, int q, int* bad, cudaStream_t st) {
+  for (int j = 0; j + 1 < q; ++j) {
+    const int64_t n = q - j - 1;
+    k_chol_step<<<grid1(n * n), NT, 0, st>>>(G, q, j);
+    VSIE_CHECK_LAUNCH();
+  }
+  k_chol_finish<<<grid1((int64_t)q * q), NT, 0, st>>>(G, q, bad);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_upper_inverse(const cplx* R, int q, cplx* Rt, cplx* X, cudaStream_t st) {
+  launch_transpose(R, q, q, Rt, false, st);
+  static bool configured = false;
+  if (!configured) {
+    VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_upper_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    configured = true;
+  }
+  k_upper_inverse<<<q, 128, (size_t)q * sizeof(cplx), st>>>(Rt, q, X);
   VSIE_CHECK_LAUNCH();
 }
 

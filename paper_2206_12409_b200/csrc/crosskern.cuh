@@ -14,7 +14,12 @@ void launch_gaussian(cplx* out, int64_t n, uint64_t seed, cudaStream_t st);
 // A (p x q, ld lda), accumulating the same rotations into V (q x q, ld q) if V != null.
 // pairs: int2[npairs] column pairs; rotations applied counted into *rot_count.
 void launch_jacobi_round(cplx* A, int64_t p, int64_t lda, cplx* V, int64_t q, const int2* pairs, int npairs,
-                         double thr, unsigned* rot_count, cudaStream_t st);
+                         double thr, double small2, unsigned* rot_count, cudaStream_t st);
+// all sweeps in one cooperative launch (npairs CTAs must be co-resident; returns
+// false without launching otherwise).  cnt: 3 unsigned, zeroed by the caller;
+// cnt[2] = sweeps performed.
+bool launch_jacobi_coop(cplx* A, int64_t p, int64_t lda, cplx* V, int64_t q, const int2* pairs, int npairs,
+                        int nrounds, double thr, double small2, int max_sweeps, unsigned* cnt, cudaStream_t st);
 // out[j] = ||A[:, j]||_2
 void launch_col_norms(const cplx* A, int64_t p, int64_t q, int64_t lda, double* out, cudaStream_t st);
 // sum |a_i|^2 (deterministic two-pass) -> *out (device)
@@ -28,6 +33,18 @@ void launch_gather_rows(const cplx* src, int64_t lds, const int* idx, int nr, in
                         cudaStream_t st);
 // dst (C x R) = op(src (R x C)), op = transpose or conj-transpose
 void launch_transpose(const cplx* src, int64_t R, int64_t C, cplx* dst, bool conj, cudaStream_t st);
+
+// ---- Cholesky QR pieces (shifted CholeskyQR3 preconditioning of the Jacobi SVD)
+// G[i + q i] += s for i < q
+void launch_add_diag(cplx* G, int q, double s, cudaStream_t st);
+// in-place upper Cholesky of the Hermitian q x q matrix G (upper triangle used):
+// on exit G holds R (upper, G = R^H R), strictly lower part zeroed.  *bad set if a
+// pivot was not positive.
+void launch_cholesky_upper(cplx* G, int q, int* bad, cudaStream_t st);
+// X = R^{-1} for upper triangular R (q x q, column-major); Rt = scratch q x q
+void launch_upper_inverse(const cplx* R, int q, cplx* Rt, cplx* X, cudaStream_t st);
+// sum of the real diagonal of G -> *out (device)
+void launch_trace_real(const cplx* G, int q, double* out, cudaStream_t st);
 
 // ---- maxvol -------------------------------------------------------------
 struct ArgMax {

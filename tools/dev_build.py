@@ -8,7 +8,7 @@ from paper_2206_12409_b200 import Coupling, grid_of
 ci = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 cfg = synth.get_config(ci)
 t = time.time()
-h = Coupling.build(grid_of(cfg), cfg.meshes(), cfg.freq, cfg.tol, verbose=1, nrhs_max=1)
+h = Coupling.build(grid_of(cfg), cfg.meshes(), cfg.freq, cfg.tol, verbose=int(os.environ.get("VSIE_VERBOSE", "1")), nrhs_max=1, max_sweeps=int(os.environ.get("VSIE_SWEEPS", "8")))
 print("build", time.time() - t, "status", h.status)
 inf = h.info(); print({k: inf[k] for k in ("ranks", "sweeps", "heldout_err", "entries_evaluated", "build_s", "build_entry_s", "build_factor_s", "build_maxvol_s", "compression")})
 tts = h.export_cores()

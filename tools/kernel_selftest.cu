@@ -159,7 +159,14 @@ void test_reduce(int n1, int r1, int64_t ncol, int64_t cpr, bool cj) {
   report(buf, relerr(got, ref));
 }
 
-int main() {
+void jacobi_probe(int64_t p, int q, double decades);
+int main(int argc, char** argv) {
+  if (argc > 1) {
+    jacobi_probe(7370, 272, 4);
+    jacobi_probe(7370, 272, 14);
+    jacobi_probe(272, 272, 7);
+    return 0;
+  }
   for (int ta = 0; ta < 3; ++ta)
     for (int tb = 0; tb < 3; ++tb) test_zgemm(ta, tb, 84, 12, 31, false);
   test_zgemm(0, 0, 130, 70, 300, true);
@@ -190,4 +197,40 @@ int main() {
   printf("cuda: %s\n", cudaGetErrorString(e));
   printf("%s (%d failures)\n", fails ? "SELFTEST FAILED" : "SELFTEST PASSED", fails);
   return fails ? 1 : 0;
+}
+
+// ---- Jacobi convergence / timing probe (developer tool, not a test)
+#include "../paper_2206_12409_b200/csrc/crosskern.cuh"
+#include <chrono>
+void jacobi_probe(int64_t p, int q, double decades) {
+  // A = random (p x q) with columns scaled by 10^(-decades j / q): graded
+  auto A = randv(p * q);
+  for (int j = 0; j < q; ++j) {
+    double s = std::pow(10.0, -decades * j / q);
+    for (int64_t i = 0; i < p; ++i) A[i + p * j] *= s;
+  }
+  cplx* dA = up(A);
+  int Q = q + (q & 1);
+  std::vector<int2> pairs;
+  std::vector<int> L(Q);
+  for (int t = 0; t < Q - 1; ++t) {
+    L[0] = 0;
+    for (int i = 0; i < Q - 1; ++i) L[i + 1] = (t + i) % (Q - 1) + 1;
+    for (int k = 0; k < Q / 2; ++k) pairs.push_back(make_int2(L[k], L[Q - 1 - k]));
+  }
+  int2* dp; cudaMalloc(&dp, pairs.size() * sizeof(int2));
+  cudaMemcpy(dp, pairs.data(), pairs.size() * sizeof(int2), cudaMemcpyHostToDevice);
+  unsigned* cnt; cudaMalloc(&cnt, 4);
+  auto t0 = std::chrono::steady_clock::now();
+  int sweeps = 0;
+  for (; sweeps < 40; ++sweeps) {
+    cudaMemset(cnt, 0, 4);
+    for (int t = 0; t < Q - 1; ++t) launch_jacobi_round(dA, p, p, nullptr, q, dp + (int64_t)t * (Q / 2), Q / 2, 1e-12, 0.0, cnt, 0);
+    unsigned h = 0; cudaMemcpy(&h, cnt, 4, cudaMemcpyDeviceToHost);
+    printf("   sweep %d rotations %u\n", sweeps, h);
+    if (!h) break;
+  }
+  double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  printf("jacobi probe p=%ld q=%d decades=%.0f: %d sweeps, %.3f s, %.1f us/round\n", (long)p, q, decades, sweeps + 1, s, 1e6 * s / ((sweeps + 1) * (Q - 1)));
+  cudaFree(dA); cudaFree(dp); cudaFree(cnt);
 }
