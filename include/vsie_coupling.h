@@ -198,10 +198,24 @@ int32_t vsie_coupling_tt_eval(vsie_coupling_t h, const int64_t* idx, int64_t cou
 int32_t vsie_coupling_info(vsie_coupling_t h, vsie_info* out);
 
 /* Per-kernel CUDA-event timing of subsequent apply calls: enable = 1 starts
- * (and resets) it, 0 stops it.  vsie_coupling_timers copies up to `max`
+ * (and resets) it with the chains serialised on the caller's stream (clean per-kernel
+ * durations), enable = 2 keeps the chains concurrent (timeline, vsie_coupling_trace),
+ * 0 stops it.  vsie_coupling_timers copies up to `max`
  * accumulated timers (synchronises the handle's streams). */
 int32_t vsie_coupling_set_timing(vsie_coupling_t h, int32_t enable);
 int32_t vsie_coupling_timers(vsie_coupling_t h, vsie_timer* out, int32_t max, int32_t* n_out);
+
+/* Timeline of apply calls made with vsie_coupling_set_timing(h, 2): the chi chains run
+ * concurrently (as in the captured graph, but launched eagerly) with a CUDA event pair
+ * around every kernel; each record gives the kernel's start / end in ms relative to the
+ * start of its apply call.  Copies up to `max` records, clears them, *n_out = count. */
+typedef struct {
+  char name[32];
+  int32_t chi;                  /* chain (0..2), -1 for the join / combine steps      */
+  int32_t call;                 /* index of the apply call since timing was enabled   */
+  double t0_ms, t1_ms;
+} vsie_trace;
+int32_t vsie_coupling_trace(vsie_coupling_t h, vsie_trace* out, int32_t max, int32_t* n_out);
 
 void vsie_coupling_destroy(vsie_coupling_t h);
 

@@ -49,6 +49,11 @@ class vsie_timer(C.Structure):
                 ("bytes_per_launch", C.c_int64), ("flops_per_launch", C.c_int64)]
 
 
+class vsie_trace(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("chi", C.c_int32), ("call", C.c_int32), ("t0_ms", C.c_double),
+                ("t1_ms", C.c_double)]
+
+
 HANDLE = C.c_void_p
 
 _SIGS = {
@@ -72,6 +77,7 @@ _SIGS = {
     "vsie_coupling_info": (C.c_int32, [HANDLE, C.POINTER(vsie_info)]),
     "vsie_coupling_set_timing": (C.c_int32, [HANDLE, C.c_int32]),
     "vsie_coupling_timers": (C.c_int32, [HANDLE, C.POINTER(vsie_timer), C.c_int32, C.POINTER(C.c_int32)]),
+    "vsie_coupling_trace": (C.c_int32, [HANDLE, C.POINTER(vsie_trace), C.c_int32, C.POINTER(C.c_int32)]),
     "vsie_coupling_destroy": (None, [HANDLE]),
 }
 

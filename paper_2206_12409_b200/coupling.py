@@ -248,8 +248,16 @@ class Coupling:
         return self._idx_call(lib().vsie_coupling_tt_eval, rows, cols, stream)
 
     # ------------------------------------------------------------------ timing
-    def set_timing(self, enable: bool):
-        check(lib().vsie_coupling_set_timing(self._h, int(bool(enable))))
+    def set_timing(self, enable):
+        """0/False off, 1/True serialised per-kernel timing, 2 concurrent timeline (trace())."""
+        check(lib().vsie_coupling_set_timing(self._h, int(enable)))
+
+    def trace(self, max_records=4096):
+        n = C.c_int32()
+        arr = (_lib.vsie_trace * max_records)()
+        check(lib().vsie_coupling_trace(self._h, arr, max_records, C.byref(n)))
+        return [dict(name=arr[i].name.decode(), chi=arr[i].chi, call=arr[i].call, t0_ms=arr[i].t0_ms,
+                     t1_ms=arr[i].t1_ms) for i in range(n.value)]
 
     def timers(self):
         n = C.c_int32()

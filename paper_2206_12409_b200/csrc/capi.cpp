@@ -291,7 +291,12 @@ int32_t vsie_coupling_set_timing(vsie_coupling_t h, int32_t enable) {
     }
     h->pending.clear();
     h->timers.clear();
-    h->timing = enable != 0;
+    for (cudaEvent_t e : h->origins) cudaEventDestroy(e);
+    h->origins.clear();
+    h->trace_origin = nullptr;
+    h->trace_call = 0;
+    VSIE_REQUIRE(enable >= 0 && enable <= 2, VSIE_ERR_ARG, "timing mode must be 0, 1 or 2");
+    h->timing = enable;
     return VSIE_OK;
   });
 }
@@ -326,6 +331,33 @@ int32_t vsie_coupling_timers(vsie_coupling_t h, vsie_timer* out, int32_t max, in
       out[i].bytes_per_launch = h->timers[i].bytes;
       out[i].flops_per_launch = h->timers[i].flops;
     }
+    return VSIE_OK;
+  });
+}
+
+int32_t vsie_coupling_trace(vsie_coupling_t h, vsie_trace* out, int32_t max, int32_t* n_out) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr && n_out != nullptr, VSIE_ERR_ARG, "NULL argument");
+    VSIE_CHECK_CUDA(cudaDeviceSynchronize());
+    int n = 0;
+    for (auto& t : h->pending) {
+      if (t.origin && out && n < max) {
+        float a = 0, b = 0;
+        VSIE_CHECK_CUDA(cudaEventElapsedTime(&a, t.origin, t.e0));
+        VSIE_CHECK_CUDA(cudaEventElapsedTime(&b, t.origin, t.e1));
+        std::memset(&out[n], 0, sizeof(vsie_trace));
+        std::strncpy(out[n].name, t.name.c_str(), sizeof(out[n].name) - 1);
+        out[n].chi = t.chi;
+        out[n].call = t.call;
+        out[n].t0_ms = a;
+        out[n].t1_ms = b;
+        ++n;
+      }
+      h->event_pool.push_back(t.e0);
+      h->event_pool.push_back(t.e1);
+    }
+    h->pending.clear();
+    *n_out = n;
     return VSIE_OK;
   });
 }

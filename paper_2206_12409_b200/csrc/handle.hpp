@@ -24,6 +24,7 @@ struct Shard {
   DevBuf<cplx> Y2;      // [3][r1 * n2 * n3loc * nrhs]   (also W1 in the adjoint)
   DevBuf<cplx> W2;      // [3][r2 * n3loc * nrhs]
   DevBuf<cplx> z3;      // [3][r3max * nrhs]
+  DevBuf<cplx> zpart;   // [3][mloc_max * nrhs]  transpose: per-chi G4_chi^T z3_chi
   int n3loc() const { return i3e - i3b; }
   int64_t mloc() const { return ce - cb; }
 };
@@ -32,6 +33,19 @@ struct Timed {
   std::string name;
   cudaEvent_t e0, e1;
   int64_t bytes, flops;
+  int chi = -1;
+  int call = 0;
+  cudaEvent_t origin = nullptr;  // start of the apply call (trace mode)
+};
+
+// A captured apply (CUDA graph) for one (op, nrhs, x, y) combination.
+struct GraphEntry {
+  int op = 0, nrhs = 0;
+  const void* x = nullptr;
+  void* y = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int64_t launches = 0;
+  uint64_t last_use = 0;
 };
 
 }  // namespace vsie
@@ -51,9 +65,17 @@ struct vsie_coupling_s {
   int rank = 0, world = 1, loopback = 0, device = 0;
   int nrhs_max = 64;
   std::unique_ptr<vsie::Comm> comm;
-  vsie::DevBuf<vsie::cplx> partials;
-  vsie::DevBuf<unsigned> counters;
-  vsie::DevBuf<vsie::cplx> zgemm_ws;
+  vsie::DevBuf<vsie::cplx> partials;       // [3][partials_per_chi]
+  int64_t partials_per_chi = 0;
+  vsie::DevBuf<vsie::cplx> zgemm_ws;       // [3][zgemm_ws_per_chi]
+  int64_t zgemm_ws_per_chi = 0;
+  // apply orchestration: one stream per chi chain, fork/join events, graph cache
+  cudaStream_t chi_stream[3] = {nullptr, nullptr, nullptr};
+  cudaStream_t cap_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
+  std::vector<vsie::GraphEntry> graphs;
+  uint64_t graph_clock = 0;
+  int use_graphs = 1;
   vsie::DevBuf<vsie::cplx> gather_buf;     // allgather staging of z
   vsie::DevBuf<vsie::cplx> io_x, io_y;     // apply_host staging
   vsie::DevBuf<int64_t> io_idx;
@@ -65,7 +87,11 @@ struct vsie_coupling_s {
   double build_s = 0, build_entry_s = 0, build_factor_s = 0, build_maxvol_s = 0;
   int64_t apply_launches = 0, apply_calls = 0;
   // timing
-  bool timing = false;
+  int timing = 0;                 // 0 off, 1 serialised per-kernel timing, 2 concurrent timeline
+  int scope_chi = -1;             // chain of the kernels being launched (trace records)
+  int trace_call = 0;
+  cudaEvent_t trace_origin = nullptr;
+  std::vector<cudaEvent_t> origins;
   std::vector<vsie::Timed> pending;
   std::vector<vsie::TimerSlot> timers;
   std::vector<cudaEvent_t> event_pool;
@@ -87,6 +113,9 @@ void handle_set_cores_device(vsie_coupling_s* h, int chi, const int r[3], const 
 void handle_alloc_workspace(vsie_coupling_s* h);
 
 void apply(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int nrhs, cudaStream_t st);
+// drops the cached apply graphs (cores / workspaces changed)
+void apply_reset_graphs(vsie_coupling_s* h);
+void apply_destroy(vsie_coupling_s* h);
 void tt_eval(vsie_coupling_s* h, const int64_t* idx, int64_t count, cplx* out, cudaStream_t st);
 void launch_tt_eval(const cplx* const G[4], const int r[3], const int n[3], int64_t m, int chi_sel,
                     const int64_t* idx, int64_t count, int64_t nv, cplx* out, cudaStream_t st);

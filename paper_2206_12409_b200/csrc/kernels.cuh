@@ -96,6 +96,11 @@ struct ReduceArgs {
 };
 void launch_reduce_g1(const ReduceArgs& a, cudaStream_t st);
 
+// out[i + ld_out j] = sum_{c<3} in[c * chi_stride + i + ld_in j] (fixed order), conj if asked;
+// i < rows, j < k  (the Eq. 18 sum over chi of the per-chi transposes)
+void launch_sum3(const cplx* in, int64_t chi_stride, int64_t ld_in, int64_t rows, int k, cplx* out, int64_t ld_out,
+                 bool conj_out, cudaStream_t st);
+
 // ------------------------------------------------------------------ dense complex LA (linalg.cu)
 enum Trans { kN = 0, kT = 1, kC = 2 };
 // C = alpha op(A) op(B) + beta C, column-major; batched over up to 3 problems with

@@ -159,73 +159,98 @@ __global__ void k_axpy1(const cplx* __restrict__ x, cplx* __restrict__ y, int64_
 
 
 // ---------------------------------------------------------------------------------------
-// Small / skinny ZGEMM on FP64 tensor cores (mma.sync.m8n8k4.f64): one warp per 16 x 16
-// output tile (2 x 2 DMMA tiles, 4 real DMMAs per complex product), fragments loaded
-// straight from global memory (operands of the apply's G2 contractions are L2-resident),
-// deterministic split-K through the partial workspace.
+// Small / skinny ZGEMM on FP64 tensor cores (mma.sync.m8n8k4.f64, SASS DMMA; tcgen05 has
+// no f64 kind): a CTA of 4 warps owns a 32 x 32 output tile (warp: 16 x 16 = 2 x 2 DMMA
+// tiles, 4 real DMMAs per complex product).  K is walked in chunks of 32: every thread
+// loads 8 + 8 elements of the next A / B chunk into registers (coalesced, all in flight)
+// while the warps run the current chunk's 8 k-steps out of shared memory.  Padded smem
+// rows make both the fragment reads and the stores bank-conflict free.  Deterministic
+// split-K through the partial workspace (fixed-order reduction kernel).
 __device__ __forceinline__ void dmma_acc(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
 
-template <int TA, int TB>
+constexpr int TCM = 32, TCN = 32, TCK = 32;
+constexpr int TCA = TCM + 2;  // As row stride (complex): 544 B -> fragment reads conflict free
+constexpr int TCB = TCK + 4;  // Bs row stride (complex): 576 B
+
+template <int TA>
 __global__ void __launch_bounds__(128) k_zgemm_dmma(const __grid_constant__ Zgemm g, int splits, int64_t mt, int64_t nt,
                                                     cplx* __restrict__ ws, int64_t ws_stride) {
-  const int lane = threadIdx.x & 31;
-  const int64_t wid = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
-  const int64_t per_b = mt * nt * splits;
-  const int b = (int)(wid / per_b);
-  if (b >= g.nbatch) return;
-  int64_t rem = wid - b * per_b;
-  const int sp = (int)(rem / (mt * nt));
-  rem -= (int64_t)sp * mt * nt;
-  const int64_t m0 = (rem % mt) * 16, n0 = (rem / mt) * 16;
+  __shared__ cplx As[TCK][TCA];   // As[k][m] = op(A)[m0 + m, kc + k]
+  __shared__ cplx Bs[TCN][TCB];   // Bs[n][k] = B[kc + k, n0 + n]
+  const int b = blockIdx.y;
+  const int64_t tiles = mt * nt;
+  const int64_t tile = blockIdx.x % tiles;
+  const int sp = (int)(blockIdx.x / tiles);
   const int64_t M = g.M[b], N = g.N[b], K = g.K[b];
+  const int64_t m0 = (tile % mt) * TCM, n0 = (tile / mt) * TCN;
   if (m0 >= M || n0 >= N) return;
-  const int64_t ksteps = (K + 3) / 4;
-  const int64_t ks0 = ksteps * sp / splits, ks1 = ksteps * (sp + 1) / splits;
+  const int64_t chunks = (K + TCK - 1) / TCK;
+  const int64_t kc0 = chunks * sp / splits * TCK, kc1 = min(K, chunks * (sp + 1) / splits * TCK);
   const cplx* __restrict__ A = g.A[b];
   const cplx* __restrict__ B = g.B[b];
   const int64_t lda = g.lda[b], ldb = g.ldb[b];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 1) * 16, wn = (warp >> 1) * 16;
   const int gq = lane >> 2, t = lane & 3;
+  cplx ra[8], rb[8];
+  auto load = [&](int64_t kc) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = tid + 128 * i;
+      int mm, kk;
+      if (TA == kN) { mm = e & 31; kk = e >> 5; } else { kk = e & 31; mm = e >> 5; }
+      const int64_t m = m0 + mm, k = kc + kk;
+      cplx v = cmk(0, 0);
+      if (m < M && k < kc1) {
+        v = TA == kN ? __ldg(A + m + lda * k) : __ldg(A + k + lda * m);
+        if (TA == kC) v.y = -v.y;
+      }
+      ra[i] = v;
+      const int kb = e & 31, nb = e >> 5;
+      const int64_t n = n0 + nb, k2 = kc + kb;
+      rb[i] = (n < N && k2 < kc1) ? __ldg(B + k2 + ldb * n) : cmk(0, 0);
+    }
+  };
+  auto store = [&]() {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = tid + 128 * i;
+      if (TA == kN) As[e >> 5][e & 31] = ra[i]; else As[e & 31][e >> 5] = ra[i];
+      Bs[e >> 5][e & 31] = rb[i];
+    }
+  };
   double cr[2][2][2], ci[2][2][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 2; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0;
-  for (int64_t ks = ks0; ks < ks1; ++ks) {
-    const int64_t k = 4 * ks + t;
-    cplx av[2], bv[2];
+  if (kc0 < kc1) load(kc0);
+  for (int64_t kc = kc0; kc < kc1; kc += TCK) {
+    __syncthreads();
+    store();
+    __syncthreads();
+    if (kc + TCK < kc1) load(kc + TCK);   // next chunk in flight during this chunk's DMMAs
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int64_t m = m0 + 8 * i + gq;
-      cplx v = cmk(0, 0);
-      if (m < M && k < K) {
-        v = TA == kN ? __ldg(A + m + lda * k) : __ldg(A + k + lda * m);
-        if (TA == kC) v.y = -v.y;
-      }
-      av[i] = v;
+    for (int ks = 0; ks < TCK / 4; ++ks) {
+      cplx av[2], bv[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) av[i] = As[4 * ks + t][wm + 8 * i + gq];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bv[j] = Bs[wn + 8 * j + gq][4 * ks + t];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          dmma_acc(cr[i][j][0], cr[i][j][1], av[i].x, bv[j].x);
+          dmma_acc(cr[i][j][0], cr[i][j][1], -av[i].y, bv[j].y);
+          dmma_acc(ci[i][j][0], ci[i][j][1], av[i].x, bv[j].y);
+          dmma_acc(ci[i][j][0], ci[i][j][1], av[i].y, bv[j].x);
+        }
     }
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int64_t n = n0 + 8 * j + gq;
-      cplx v = cmk(0, 0);
-      if (n < N && k < K) {
-        v = TB == kN ? __ldg(B + k + ldb * n) : __ldg(B + n + ldb * k);
-        if (TB == kC) v.y = -v.y;
-      }
-      bv[j] = v;
-    }
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        dmma_acc(cr[i][j][0], cr[i][j][1], av[i].x, bv[j].x);
-        dmma_acc(cr[i][j][0], cr[i][j][1], -av[i].y, bv[j].y);
-        dmma_acc(ci[i][j][0], ci[i][j][1], av[i].x, bv[j].y);
-        dmma_acc(ci[i][j][0], ci[i][j][1], av[i].y, bv[j].x);
-      }
   }
   const bool has_beta = g.beta.x != 0.0 || g.beta.y != 0.0;
 #pragma unroll
@@ -234,7 +259,7 @@ __global__ void __launch_bounds__(128) k_zgemm_dmma(const __grid_constant__ Zgem
     for (int j = 0; j < 2; ++j)
 #pragma unroll
       for (int jj = 0; jj < 2; ++jj) {
-        const int64_t m = m0 + 8 * i + gq, n = n0 + 8 * j + 2 * t + jj;
+        const int64_t m = m0 + wm + 8 * i + gq, n = n0 + wn + 8 * j + 2 * t + jj;
         if (m >= M || n >= N) continue;
         const cplx acc = cmk(cr[i][j][jj], ci[i][j][jj]);
         if (splits > 1) {
@@ -295,28 +320,29 @@ void launch_zgemm(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t st) {
 void launch_zgemm_dmma(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t st) {
   int64_t mt = 0, nt = 0, kmax = 0, mn = 0;
   for (int b = 0; b < g.nbatch; ++b) {
-    mt = std::max(mt, ceil_div(g.M[b], 16));
-    nt = std::max(nt, ceil_div(g.N[b], 16));
+    mt = std::max(mt, ceil_div(g.M[b], TCM));
+    nt = std::max(nt, ceil_div(g.N[b], TCN));
     kmax = std::max(kmax, g.K[b]);
     mn = std::max(mn, g.M[b] * g.N[b]);
   }
   if (mt == 0 || nt == 0) return;
+  VSIE_REQUIRE(g.tb == kN, VSIE_ERR_ARG, "zgemm_dmma: op(B) must be N");
   const int64_t tiles = mt * nt * g.nbatch;
+  const int64_t chunks = ceil_div(kmax, TCK);
   int splits = 1;
-  if (ws != nullptr && tiles < 148 * 16) {
-    splits = (int)std::min<int64_t>(std::min<int64_t>(148 * 16 / tiles, std::max<int64_t>(1, kmax / 32)), 64);
+  if (ws != nullptr && tiles < 148 * 2) {
+    // >= 2 K chunks per split so that the register prefetch overlaps something
+    splits = (int)std::min<int64_t>(std::min<int64_t>(ceil_div(148 * 2, tiles), std::max<int64_t>(1, chunks / 2)), 64);
     while (splits > 1 && (int64_t)splits * mn * g.nbatch > ws_elems) --splits;
     splits = std::max(splits, 1);
   }
-  const int64_t warps = tiles * splits;
-  const unsigned blocks = (unsigned)ceil_div(warps, 4);
-  VSIE_REQUIRE(g.tb == kN, VSIE_ERR_ARG, "zgemm_dmma: op(B) must be N");
+  dim3 grid((unsigned)(mt * nt * splits), (unsigned)g.nbatch);
   if (g.ta == kN)
-    k_zgemm_dmma<kN, kN><<<blocks, 128, 0, st>>>(g, splits, mt, nt, ws, mn);
+    k_zgemm_dmma<kN><<<grid, 128, 0, st>>>(g, splits, mt, nt, ws, mn);
   else if (g.ta == kT)
-    k_zgemm_dmma<kT, kN><<<blocks, 128, 0, st>>>(g, splits, mt, nt, ws, mn);
+    k_zgemm_dmma<kT><<<grid, 128, 0, st>>>(g, splits, mt, nt, ws, mn);
   else
-    k_zgemm_dmma<kC, kN><<<blocks, 128, 0, st>>>(g, splits, mt, nt, ws, mn);
+    k_zgemm_dmma<kC><<<grid, 128, 0, st>>>(g, splits, mt, nt, ws, mn);
   VSIE_CHECK_LAUNCH();
   if (splits > 1) {
     dim3 rg((unsigned)std::min<int64_t>(ceil_div(mn, 256), 148 * 8), g.nbatch);

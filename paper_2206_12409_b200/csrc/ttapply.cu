@@ -26,70 +26,73 @@ constexpr int kXChunk = 512;
 
 __device__ __forceinline__ cplx ldg_c(const cplx* p) { return __ldg(p); }
 
-// y[r] = sum_c A[r + R c] x[c]: each thread owns rows t + 256 g (g < G) of a
-// row tile of 256 G rows and a column range of its split; x values are warp-uniform
-// broadcast loads; 4 columns x G rows of loads in flight per thread.
-template <int G>
-__global__ void __launch_bounds__(kThreads) k_gemv_n(const __grid_constant__ GemvN a, cplx* __restrict__ partials,
-                                                     int64_t rmax) {
+// Streaming 16-B load (evict-first).  asm volatile keeps a batch of these in program
+// order ahead of the arithmetic that consumes them, so a thread really has U loads in
+// flight (ptxas otherwise interleaves load/FMA pairs and keeps only two outstanding).
+__device__ __forceinline__ cplx ld_stream(const cplx* p) {
+  cplx v;
+  asm volatile("ld.global.cs.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
+// y[r] = sum_c A[r + R c] x[c] (A column-major, HBM-streamed once).  A CTA owns a row
+// tile of blockDim.x rows (blockDim = R rounded up to a warp multiple when R <= 512, so
+// a column of a short G4 is read by exactly one CTA row-tile) and a column range of
+// its split; thread t owns row t of the tile and keeps U independent 16-B streaming
+// loads (ld.global.cs) in flight; x values are warp-uniform broadcasts from L1.
+template <int U>
+__global__ void __launch_bounds__(512) k_gemv_n(const __grid_constant__ GemvN a, cplx* __restrict__ partials,
+                                                int64_t rmax) {
   const int b = blockIdx.z;
   const int64_t R = a.R[b], C = a.C[b];
-  const int64_t rt = blockIdx.y;
-  const int64_t row0 = rt * kThreads * G;
-  if (row0 >= R) return;
+  const int64_t row = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
+  const bool act = row < R;
   const int nsplit = gridDim.x, s = blockIdx.x;
   const int64_t c0 = C * s / nsplit, c1 = C * (s + 1) / nsplit;
   const cplx* __restrict__ X = a.x[b];
-  const cplx* __restrict__ A = a.A[b];
-  cplx acc[G], acc2[G];
-#pragma unroll
-  for (int g = 0; g < G; ++g) acc[g] = acc2[g] = cmk(0, 0);
-  int64_t rows[G];
-  bool act[G];
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    rows[g] = row0 + threadIdx.x + kThreads * g;
-    act[g] = rows[g] < R;
-  }
+  const cplx* __restrict__ p = a.A[b] + (act ? row : R - 1);  // inactive lanes re-read a valid row
+  cplx acc = cmk(0, 0), acc2 = cmk(0, 0);
   int64_t c = c0;
-  for (; c + 4 <= c1; c += 4) {
-    const cplx x0 = __ldg(X + c), x1 = __ldg(X + c + 1), x2 = __ldg(X + c + 2), x3 = __ldg(X + c + 3);
-    cplx v[G][4];
+  // software pipeline: the next batch of U columns is in flight while this one is consumed
+  if (c + U <= c1) {
+    cplx v[U], xv[U];
 #pragma unroll
-    for (int g = 0; g < G; ++g)
-      if (act[g]) {
-        const cplx* p = A + rows[g] + R * c;
-        v[g][0] = __ldcs(p);
-        v[g][1] = __ldcs(p + R);
-        v[g][2] = __ldcs(p + 2 * R);
-        v[g][3] = __ldcs(p + 3 * R);
+    for (int u = 0; u < U; ++u) {
+      v[u] = ld_stream(p + R * (c + u));
+      xv[u] = __ldg(X + c + u);
+    }
+    c += U;
+    for (; c + U <= c1; c += U) {
+      cplx w[U], xw[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        w[u] = ld_stream(p + R * (c + u));
+        xw[u] = __ldg(X + c + u);
       }
 #pragma unroll
-    for (int g = 0; g < G; ++g)
-      if (act[g]) {
-        cfma(acc[g], v[g][0], x0);
-        cfma(acc2[g], v[g][1], x1);
-        cfma(acc[g], v[g][2], x2);
-        cfma(acc2[g], v[g][3], x3);
+      for (int u = 0; u < U; u += 2) {
+        cfma(acc, v[u], xv[u]);
+        cfma(acc2, v[u + 1], xv[u + 1]);
       }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        v[u] = w[u];
+        xv[u] = xw[u];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u += 2) {
+      cfma(acc, v[u], xv[u]);
+      cfma(acc2, v[u + 1], xv[u + 1]);
+    }
   }
-  for (; c < c1; ++c) {
-    const cplx xv = __ldg(X + c);
-#pragma unroll
-    for (int g = 0; g < G; ++g)
-      if (act[g]) cfma(acc[g], __ldcs(A + rows[g] + R * c), xv);
-  }
-#pragma unroll
-  for (int g = 0; g < G; ++g) acc[g] = cadd(acc[g], acc2[g]);
-  if (nsplit == 1) {
-#pragma unroll
-    for (int g = 0; g < G; ++g)
-      if (act[g]) a.y[b][rows[g]] = acc[g];
-    return;
-  }
-#pragma unroll
-  for (int g = 0; g < G; ++g)
-    if (act[g]) partials[((int64_t)b * nsplit + s) * rmax + rows[g]] = acc[g];
+  for (; c < c1; ++c) cfma(acc, __ldcs(p + R * c), __ldg(X + c));
+  acc = cadd(acc, acc2);
+  if (!act) return;
+  if (nsplit == 1)
+    a.y[b][row] = acc;
+  else
+    partials[((int64_t)b * nsplit + s) * rmax + row] = acc;
 }
 
 struct SumArgs {
@@ -149,6 +152,7 @@ __global__ void __launch_bounds__(kThreads) k_sum_partials(const __grid_constant
 constexpr int kWarps = kThreads / 32;
 constexpr int kCPW = 2;                     // columns per warp
 constexpr int kColsPerCta = kWarps * kCPW;  // 16
+constexpr int kTU = 2;                      // row groups of 32 in flight per column
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -156,7 +160,10 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// y[c] = sum_r A[r + R c] x[r]  over rows [r0, r1) of this split.
+// y[c] = sum_r A[r + R c] x[r]  over rows [r0, r1) of this split: a warp owns kCPW
+// columns, lanes stride the rows with kTU x kCPW independent 16-B streaming loads in
+// flight; fixed-order lane sums (butterfly) -> deterministic.  In sum_batch mode the
+// batches share the output columns (Eq. 18 sum over chi inside the kernel).
 __global__ void __launch_bounds__(kThreads) k_gemv_t(const __grid_constant__ GemvT a, cplx* __restrict__ partials,
                                                      int64_t cmax) {
   const bool conj_out = a.conj_out;
@@ -165,45 +172,63 @@ __global__ void __launch_bounds__(kThreads) k_gemv_t(const __grid_constant__ Gem
   const int nsplit = gridDim.y, s = blockIdx.y;
   const int bz = blockIdx.z;
   const int nb = a.sum_batch ? a.nbatch : 1;
-  // in sum_batch mode all batches share the output columns (same C)
   const int64_t Cout = a.C[a.sum_batch ? 0 : bz];
   if ((int64_t)ct * kColsPerCta >= Cout) return;
   const int64_t cbase = (int64_t)ct * kColsPerCta + warp * kCPW;
   cplx acc[kCPW];
 #pragma unroll
   for (int j = 0; j < kCPW; ++j) acc[j] = cmk(0, 0);
+  bool cok[kCPW];
+#pragma unroll
+  for (int j = 0; j < kCPW; ++j) cok[j] = cbase + j < Cout;
   for (int bb = 0; bb < nb; ++bb) {
     const int b = a.sum_batch ? bb : bz;
     const int64_t R = a.R[b];
     const int64_t r0 = R * s / nsplit, r1 = R * (s + 1) / nsplit;
     const cplx* __restrict__ A = a.A[b];
     const cplx* __restrict__ X = a.x[b];
-    int64_t r = r0 + lane;
-    for (; r + 32 < r1; r += 64) {
-      const cplx xa = ldg_c(X + r), xb = ldg_c(X + r + 32);
-      cplx va[kCPW], vb[kCPW];
+    const cplx* __restrict__ col[kCPW];
 #pragma unroll
-      for (int j = 0; j < kCPW; ++j) {
-        const int64_t c = cbase + j;
-        if (c < Cout) {
-          va[j] = __ldcs(A + r + R * c);
-          vb[j] = __ldcs(A + r + 32 + R * c);
+    for (int j = 0; j < kCPW; ++j) col[j] = A + R * (cok[j] ? cbase + j : Cout - 1);
+    int64_t r = r0 + lane;
+    // software pipeline: the next kTU row groups are in flight while this batch is consumed
+    if (r + 32 * (kTU - 1) < r1) {
+      cplx v[kTU][kCPW], xv[kTU];
+#pragma unroll
+      for (int u = 0; u < kTU; ++u) {
+        xv[u] = __ldg(X + r + 32 * u);
+#pragma unroll
+        for (int j = 0; j < kCPW; ++j) v[u][j] = ld_stream(col[j] + r + 32 * u);
+      }
+      r += 32 * kTU;
+      for (; r + 32 * (kTU - 1) < r1; r += 32 * kTU) {
+        cplx w[kTU][kCPW], xw[kTU];
+#pragma unroll
+        for (int u = 0; u < kTU; ++u) {
+          xw[u] = __ldg(X + r + 32 * u);
+#pragma unroll
+          for (int j = 0; j < kCPW; ++j) w[u][j] = ld_stream(col[j] + r + 32 * u);
+        }
+#pragma unroll
+        for (int u = 0; u < kTU; ++u)
+#pragma unroll
+          for (int j = 0; j < kCPW; ++j) cfma(acc[j], v[u][j], xv[u]);
+#pragma unroll
+        for (int u = 0; u < kTU; ++u) {
+          xv[u] = xw[u];
+#pragma unroll
+          for (int j = 0; j < kCPW; ++j) v[u][j] = w[u][j];
         }
       }
 #pragma unroll
-      for (int j = 0; j < kCPW; ++j)
-        if (cbase + j < Cout) {
-          cfma(acc[j], va[j], xa);
-          cfma(acc[j], vb[j], xb);
-        }
+      for (int u = 0; u < kTU; ++u)
+#pragma unroll
+        for (int j = 0; j < kCPW; ++j) cfma(acc[j], v[u][j], xv[u]);
     }
     for (; r < r1; r += 32) {
-      const cplx xv = ldg_c(X + r);
+      const cplx xv = __ldg(X + r);
 #pragma unroll
-      for (int j = 0; j < kCPW; ++j) {
-        const int64_t c = cbase + j;
-        if (c < Cout) cfma(acc[j], __ldcs(A + r + R * c), xv);
-      }
+      for (int j = 0; j < kCPW; ++j) cfma(acc[j], __ldcs(col[j] + r), xv);
     }
   }
 #pragma unroll
@@ -211,24 +236,18 @@ __global__ void __launch_bounds__(kThreads) k_gemv_t(const __grid_constant__ Gem
     acc[j].x = warp_sum(acc[j].x);
     acc[j].y = warp_sum(acc[j].y);
   }
-  if (nsplit == 1) {
-    if (lane < kCPW) {
-      cplx v = acc[0];
-#pragma unroll
-      for (int j = 1; j < kCPW; ++j)
-        if (lane == j) v = acc[j];
-      const int64_t c = cbase + lane;
-      if (c < Cout) a.y[bz][c] = conj_out ? cconj(v) : v;
-    }
-    return;
-  }
   if (lane < kCPW) {
     cplx v = acc[0];
 #pragma unroll
     for (int j = 1; j < kCPW; ++j)
       if (lane == j) v = acc[j];
     const int64_t c = cbase + lane;
-    if (c < Cout) partials[((int64_t)bz * nsplit + s) * cmax + c] = v;
+    if (c < Cout) {
+      if (nsplit == 1)
+        a.y[bz][c] = conj_out ? cconj(v) : v;
+      else
+        partials[((int64_t)bz * nsplit + s) * cmax + c] = v;
+    }
   }
 }
 
@@ -379,12 +398,33 @@ __global__ void __launch_bounds__(kG1Threads) k_reduce_g1(const __grid_constant_
   }
 }
 
-int pick_splits(int64_t other_ctas, int64_t len, int min_len, int max_splits) {
-  const int64_t target = 148 * 6;
-  int64_t s = target / std::max<int64_t>(1, other_ctas);
-  s = std::min<int64_t>(s, len / std::max(1, min_len));
-  s = std::min<int64_t>(s, max_splits);
-  return (int)std::max<int64_t>(1, s);
+__global__ void __launch_bounds__(kThreads) k_sum3(const cplx* __restrict__ in, int64_t chi_stride, int64_t ld_in,
+                                                   int64_t rows, int k, cplx* __restrict__ out, int64_t ld_out,
+                                                   bool conj_out) {
+  const int64_t n = rows * k;
+  for (int64_t e = blockIdx.x * (int64_t)kThreads + threadIdx.x; e < n; e += (int64_t)gridDim.x * kThreads) {
+    const int64_t j = e / rows, i = e - j * rows;
+    const cplx* p = in + i + ld_in * j;
+    cplx v = cadd(cadd(p[0], p[chi_stride]), p[2 * chi_stride]);
+    if (conj_out) v.y = -v.y;
+    out[i + ld_out * j] = v;
+  }
+}
+
+int pick_splits(int64_t other_ctas, int64_t len, int min_len, int max_splits, int64_t target) {
+  int64_t sp = target / std::max<int64_t>(1, other_ctas);
+  sp = std::min<int64_t>(sp, len / std::max(1, min_len));
+  sp = std::min<int64_t>(sp, max_splits);
+  return (int)std::max<int64_t>(1, sp);
+}
+
+int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
 }
 
 }  // namespace
@@ -396,14 +436,22 @@ void launch_gemv_n(const GemvN& a, cplx* partials, int64_t partials_cap, int max
     cmax = std::max(cmax, a.C[b]);
   }
   if (rmax == 0) return;
-  const int G = 1;
-  const int64_t rtiles = ceil_div(rmax, (int64_t)kThreads * G);
-  int ns = pick_splits(rtiles * a.nbatch, cmax, 16, max_splits);
+  constexpr int U = 4;
+  // row tiles of <= 512 rows, as equal as possible, warp-multiple block
+  const int64_t ntile = ceil_div(rmax, 512);
+  const int T = (int)(ceil_div(ceil_div(rmax, ntile), 32) * 32);
+  const int64_t rtiles = ceil_div(rmax, T);
+  static int occ = 0;
+  if (!occ) {
+    VSIE_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gemv_n<U>, 512, 0));
+    occ = std::max(1, occ) * 512;  // resident threads per SM
+  }
+  const int64_t slots = (int64_t)sm_count() * std::max(1, occ / T);
+  int ns = pick_splits(rtiles * a.nbatch, cmax, 24, max_splits, 2 * slots);
   while (ns > 1 && (int64_t)a.nbatch * ns * rmax > partials_cap) --ns;
   dim3 grid(ns, (unsigned)rtiles, a.nbatch);
-  k_gemv_n<1><<<grid, kThreads, 0, st>>>(a, partials, rmax);
+  k_gemv_n<U><<<grid, T, 0, st>>>(a, partials, rmax);
   VSIE_CHECK_LAUNCH();
-  (void)G;
   if (ns > 1) {
     SumArgs sa{};
     sa.nbatch = a.nbatch;
@@ -422,6 +470,15 @@ void launch_gemv_n(const GemvN& a, cplx* partials, int64_t partials_cap, int max
   }
 }
 
+void launch_sum3(const cplx* in, int64_t chi_stride, int64_t ld_in, int64_t rows, int k, cplx* out, int64_t ld_out,
+                 bool conj_out, cudaStream_t st) {
+  const int64_t n = rows * k;
+  if (n <= 0) return;
+  k_sum3<<<(unsigned)std::min<int64_t>(ceil_div(n, kThreads), 148 * 8), kThreads, 0, st>>>(in, chi_stride, ld_in, rows, k,
+                                                                                          out, ld_out, conj_out);
+  VSIE_CHECK_LAUNCH();
+}
+
 void launch_gemv_t(const GemvT& a, cplx* partials, int64_t partials_cap, int max_splits, cudaStream_t st) {
   int64_t rmax = 0, cmax = 0;
   for (int b = 0; b < a.nbatch; ++b) {
@@ -431,7 +488,7 @@ void launch_gemv_t(const GemvT& a, cplx* partials, int64_t partials_cap, int max
   if (cmax == 0) return;
   const int64_t ctiles = ceil_div(cmax, kColsPerCta);
   const int nz = a.sum_batch ? 1 : a.nbatch;
-  int ns = a.sum_batch ? 1 : pick_splits(ctiles * nz, rmax, 256, max_splits);
+  int ns = a.sum_batch ? 1 : pick_splits(ctiles * nz, rmax, 256, max_splits, (int64_t)sm_count() * 8 * 2);
   while (ns > 1 && (int64_t)nz * ns * cmax > partials_cap) --ns;
   dim3 grid((unsigned)ctiles, ns, nz);
   k_gemv_t<<<grid, kThreads, 0, st>>>(a, partials, cmax);
