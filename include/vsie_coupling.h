@@ -205,6 +205,26 @@ int32_t vsie_coupling_info(vsie_coupling_t h, vsie_info* out);
 int32_t vsie_coupling_set_timing(vsie_coupling_t h, int32_t enable);
 int32_t vsie_coupling_timers(vsie_coupling_t h, vsie_timer* out, int32_t max, int32_t* n_out);
 
+/* Execution strategy of vsie_coupling_apply (results agree to rounding; both are
+ * deterministic): use_graphs = 1 (default) replays each (op, nrhs, x, y) as a captured
+ * CUDA graph; use_persistent = 1 runs single-RHS applies as one persistent dataflow
+ * kernel per direction, 0 (default) as three concurrent per-chi kernel chains (faster on
+ * B200 at the BASELINE configs).  Negative = keep. */
+int32_t vsie_coupling_configure(vsie_coupling_t h, int32_t use_graphs, int32_t use_persistent);
+
+/* Diagnostics of the persistent single-RHS apply: with enable = 1 every tile of the
+ * following applies records its start / end (globaltimer) and SM; records of the last
+ * launch of direction dir (0 forward, 1 transpose) on shard 0 are copied out with
+ * vsie_coupling_tile_trace (phase = queue phase, chi, idx = tile index in its phase). */
+typedef struct {
+  int32_t phase, chi;
+  int64_t idx;
+  int32_t sm;
+  double t0_us, t1_us, ready_us;   /* claimed, finished, dependencies satisfied */
+} vsie_tile_rec;
+int32_t vsie_coupling_set_tile_trace(vsie_coupling_t h, int32_t enable);
+int32_t vsie_coupling_tile_trace(vsie_coupling_t h, int32_t dir, vsie_tile_rec* out, int64_t max, int64_t* n_out);
+
 /* Timeline of apply calls made with vsie_coupling_set_timing(h, 2): the chi chains run
  * concurrently (as in the captured graph, but launched eagerly) with a CUDA event pair
  * around every kernel; each record gives the kernel's start / end in ms relative to the

@@ -54,6 +54,11 @@ class vsie_trace(C.Structure):
                 ("t1_ms", C.c_double)]
 
 
+class vsie_tile_rec(C.Structure):
+    _fields_ = [("phase", C.c_int32), ("chi", C.c_int32), ("idx", C.c_int64), ("sm", C.c_int32),
+                ("t0_us", C.c_double), ("t1_us", C.c_double), ("ready_us", C.c_double)]
+
+
 HANDLE = C.c_void_p
 
 _SIGS = {
@@ -77,6 +82,10 @@ _SIGS = {
     "vsie_coupling_info": (C.c_int32, [HANDLE, C.POINTER(vsie_info)]),
     "vsie_coupling_set_timing": (C.c_int32, [HANDLE, C.c_int32]),
     "vsie_coupling_timers": (C.c_int32, [HANDLE, C.POINTER(vsie_timer), C.c_int32, C.POINTER(C.c_int32)]),
+    "vsie_coupling_set_tile_trace": (C.c_int32, [HANDLE, C.c_int32]),
+    "vsie_coupling_tile_trace": (C.c_int32, [HANDLE, C.c_int32, C.POINTER(vsie_tile_rec), C.c_int64,
+                                             C.POINTER(C.c_int64)]),
+    "vsie_coupling_configure": (C.c_int32, [HANDLE, C.c_int32, C.c_int32]),
     "vsie_coupling_trace": (C.c_int32, [HANDLE, C.POINTER(vsie_trace), C.c_int32, C.POINTER(C.c_int32)]),
     "vsie_coupling_destroy": (None, [HANDLE]),
 }

@@ -252,6 +252,23 @@ class Coupling:
         """0/False off, 1/True serialised per-kernel timing, 2 concurrent timeline (trace())."""
         check(lib().vsie_coupling_set_timing(self._h, int(enable)))
 
+    def configure(self, graphs=None, persistent=None):
+        """Apply strategy: CUDA-graph replay and the persistent single-RHS kernel (None = keep)."""
+        g = -1 if graphs is None else int(bool(graphs))
+        p = -1 if persistent is None else int(bool(persistent))
+        check(lib().vsie_coupling_configure(self._h, g, p))
+
+    def set_tile_trace(self, enable):
+        check(lib().vsie_coupling_set_tile_trace(self._h, int(bool(enable))))
+
+    def tile_trace(self, direction, max_records=65536):
+        """Per-tile timeline of the last persistent launch (direction 0 forward, 1 transpose)."""
+        n = C.c_int64()
+        arr = (_lib.vsie_tile_rec * max_records)()
+        check(lib().vsie_coupling_tile_trace(self._h, int(direction), arr, max_records, C.byref(n)))
+        return [dict(phase=arr[i].phase, chi=arr[i].chi, idx=arr[i].idx, sm=arr[i].sm, t0_us=arr[i].t0_us,
+                     t1_us=arr[i].t1_us, ready_us=arr[i].ready_us) for i in range(min(n.value, max_records))]
+
     def trace(self, max_records=4096):
         n = C.c_int32()
         arr = (_lib.vsie_trace * max_records)()

@@ -355,8 +355,99 @@ void join(vsie_coupling_s* h, const Streams& S) {
   }
 }
 
+// ------------------------------------------------------------------ persistent single-RHS apply
+bool mega_ready(vsie_coupling_s* h) {
+  static const int env = [] {
+    const char* e = std::getenv("VSIE_MEGA");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (!env || !h->use_mega) return false;
+  for (const Shard& s : h->shards)
+    if (!s.mega.sync) return false;
+  return true;
+}
+
+// algorithmic bytes of one direction on one shard
+int64_t mega_bytes(vsie_coupling_s* h, const Shard& s) {
+  int64_t b = 16 * (s.mloc() + 3 * (int64_t)h->grid.n[0] * h->grid.n[1] * s.n3loc());
+  for (int c = 0; c < 3; ++c) {
+    const int64_t r1 = h->ranks[c][0], r2 = h->ranks[c][1], r3 = h->ranks[c][2];
+    b += 16 * (h->grid.n[0] * r1 + r1 * h->grid.n[1] * r2 + r2 * s.n3loc() * r3 + r3 * s.mloc());
+  }
+  return b;
+}
+
+void mega_launch(vsie_coupling_s* h, Shard& s, const cplx* x, cplx* y, bool fwd, int conj, int pb, int pe,
+                 const IoLayout& L, cudaStream_t st) {
+  MegaArgs a = s.mega;
+  a.x = fwd ? x + s.cb : x;
+  a.y = y;
+  a.chi_stride = L.chi_stride;
+  a.vox_off = shard_voxel_offset(h, s, L);
+  a.conj = conj;
+  a.phase_begin = pb;
+  a.phase_end = pe;
+  const bool whole = pb == 0 && pe == kMegaPhases;
+  Scope sc(h, fwd ? (whole ? "fwd_mega" : "fwd_mega_part") : (whole ? "adj_mega" : "adj_mega_part"),
+           whole ? mega_bytes(h, s) : 0, 0, st);
+  if (h->tile_trace) {
+    const int d = fwd ? 0 : 1;
+    VSIE_REQUIRE(s.mega_trace[d].p != nullptr, VSIE_ERR_STATE, "tile trace buffers not allocated");
+    VSIE_CHECK_CUDA(cudaMemsetAsync(s.mega_trace[d].p, 0, s.mega_trace[d].bytes(), st));
+    a.trace = s.mega_trace[d].p;
+    launch_mega(a, fwd, st, &s.mega_traced[d]);
+    return;
+  }
+  launch_mega(a, fwd, st);
+}
+
+void apply_mega(vsie_coupling_s* h, const cplx* x, cplx* y, int op, cudaStream_t st) {
+  const IoLayout L = voxel_layout(h);
+  const bool exchange = h->comm != nullptr || h->shards.size() > 1;
+  int r3m = 1;
+  for (int c = 0; c < 3; ++c) r3m = std::max(r3m, h->ranks[c][2]);
+  if (op == VSIE_OP_N) {
+    if (!exchange) {
+      mega_launch(h, h->shards[0], x, y, true, 0, 0, kMegaPhases, L, st);
+      return;
+    }
+    for (Shard& s : h->shards) mega_launch(h, s, x, y, true, 0, 0, 1, L, st);
+    combine_r3(h, &Shard::y4, 3 * (int64_t)r3m, st);   // allreduce of y4
+    for (Shard& s : h->shards) mega_launch(h, s, x, y, true, 0, 1, kMegaPhases, L, st);
+    return;
+  }
+  const int cj = op == VSIE_OP_C;
+  const int64_t m = h->m, mp = ceil_div(m, h->world);
+  auto out_of = [&](Shard& s) -> cplx* {
+    return h->comm ? h->gather_buf.p + (int64_t)h->world * mp : y + s.cb;
+  };
+  if (!exchange) {
+    mega_launch(h, h->shards[0], x, out_of(h->shards[0]), false, cj, 0, kMegaPhases, L, st);
+    return;
+  }
+  for (Shard& s : h->shards) mega_launch(h, s, x, out_of(s), false, cj, 0, kMegaPhases - 1, L, st);
+  combine_r3(h, &Shard::y4, 3 * (int64_t)r3m, st);     // allreduce of z3
+  for (Shard& s : h->shards) mega_launch(h, s, x, out_of(s), false, cj, kMegaPhases - 1, kMegaPhases, L, st);
+  if (h->comm) {
+    Scope sc(h, "nccl_allgather", 0, 0, st);
+    cplx* seg = h->gather_buf.p + (int64_t)h->world * mp;
+    const Shard& s = h->shards[0];
+    if (s.mloc() < mp) VSIE_CHECK_CUDA(cudaMemsetAsync(seg + s.mloc(), 0, (mp - s.mloc()) * sizeof(cplx), st));
+    h->comm->allgather(reinterpret_cast<const double*>(seg), reinterpret_cast<double*>(h->gather_buf.p), 2 * (size_t)mp,
+                       st);
+    for (int p = 0; p < h->world; ++p) {
+      const int64_t cb = std::min(m, mp * p), ce = std::min(m, mp * (p + 1));
+      copy2d(y + cb, m, h->gather_buf.p + (int64_t)p * mp, mp, ce - cb, 1, st);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ the apply DAG
 void apply_dag(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int nrhs, const Streams& S) {
+  if (nrhs == 1 && mega_ready(h)) {
+    apply_mega(h, x, y, op, S.main);
+    return;
+  }
   Ctx X;
   X.h = h;
   X.k = nrhs;
@@ -442,7 +533,7 @@ bool graphs_enabled(vsie_coupling_s* h) {
     return e ? std::atoi(e) : -1;
   }();
   if (env == 0) return false;
-  if (!h->use_graphs || h->timing) return false;
+  if (!h->use_graphs || h->timing || h->tile_trace) return false;
   // NCCL collectives inside captured graphs are not exercised on this pool's
   // 1-GPU boxes: the multi-rank path runs the same DAG eagerly unless forced on.
   if (h->comm && env != 1) return false;

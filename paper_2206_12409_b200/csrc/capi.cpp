@@ -335,6 +335,61 @@ int32_t vsie_coupling_timers(vsie_coupling_t h, vsie_timer* out, int32_t max, in
   });
 }
 
+int32_t vsie_coupling_configure(vsie_coupling_t h, int32_t use_graphs, int32_t use_persistent) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "handle is NULL");
+    VSIE_CHECK_CUDA(cudaDeviceSynchronize());
+    if (use_graphs >= 0) h->use_graphs = use_graphs != 0;
+    if (use_persistent >= 0) h->use_mega = use_persistent != 0;
+    apply_reset_graphs(h);
+    return VSIE_OK;
+  });
+}
+
+int32_t vsie_coupling_set_tile_trace(vsie_coupling_t h, int32_t enable) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "handle is NULL");
+    VSIE_CHECK_CUDA(cudaDeviceSynchronize());
+    h->tile_trace = enable != 0;
+    if (h->tile_trace)
+      for (Shard& s : h->shards)
+        for (int d = 0; d < 2; ++d) s.mega_trace[d].ensure((size_t)4 * 65536);
+    apply_reset_graphs(h);
+    return VSIE_OK;
+  });
+}
+
+int32_t vsie_coupling_tile_trace(vsie_coupling_t h, int32_t dir, vsie_tile_rec* out, int64_t max, int64_t* n_out) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr && n_out != nullptr && (dir == 0 || dir == 1), VSIE_ERR_ARG, "bad argument");
+    VSIE_CHECK_CUDA(cudaDeviceSynchronize());
+    *n_out = 0;
+    Shard& s = h->shards[0];
+    const MegaPlan& p = s.mega_traced[dir];
+    if (!s.mega_trace[dir].p || p.nseg == 0) return VSIE_OK;
+    const int64_t n = p.seg_off[p.nseg];
+    std::vector<unsigned long long> host((size_t)4 * n);
+    VSIE_CHECK_CUDA(cudaMemcpy(host.data(), s.mega_trace[dir].p, host.size() * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost));
+    const auto recs = mega_decode_trace(p, host.data());
+    int64_t k = 0;
+    for (const auto& r : recs) {
+      if (out && k < max) {
+        out[k].phase = r.phase;
+        out[k].chi = r.chi;
+        out[k].idx = r.idx;
+        out[k].sm = r.sm;
+        out[k].t0_us = r.t0_us;
+        out[k].t1_us = r.t1_us;
+        out[k].ready_us = r.tr_us;
+      }
+      ++k;
+    }
+    *n_out = k;
+    return VSIE_OK;
+  });
+}
+
 int32_t vsie_coupling_trace(vsie_coupling_t h, vsie_trace* out, int32_t max, int32_t* n_out) {
   return guarded([&] {
     VSIE_REQUIRE(h != nullptr && n_out != nullptr, VSIE_ERR_ARG, "NULL argument");

@@ -174,6 +174,40 @@ void handle_alloc_workspace(vsie_coupling_s* h) {
   int64_t mloc_max = 1;
   for (Shard& s : h->shards) mloc_max = std::max<int64_t>(mloc_max, s.mloc());
   for (Shard& s : h->shards) s.zpart.alloc((size_t)3 * mloc_max * k);
+  // persistent single-RHS apply: plan + self-resetting sync words (zeroed once here)
+  for (Shard& s : h->shards) {
+    MegaArgs& a = s.mega;
+    a = MegaArgs{};
+    for (int c = 0; c < 3; ++c) {
+      a.c[c].G1 = h->G1[c].p;
+      a.c[c].G2 = h->G2[c].p;
+      a.c[c].G3 = s.G3[c].p;
+      a.c[c].G4 = s.G4[c].p;
+      a.c[c].r1 = h->ranks[c][0];
+      a.c[c].r2 = h->ranks[c][1];
+      a.c[c].r3 = h->ranks[c][2];
+    }
+    a.n1 = n1;
+    a.n2 = n2;
+    a.n3l = std::max(0, s.n3loc());
+    a.mloc = s.mloc();
+    a.r1max = r1m;
+    a.r2max = r2m;
+    a.r3max = r3m;
+    a.y4 = s.y4.p;
+    a.Y3 = s.Y3.p;
+    a.Y2 = s.Y2.p;
+    a.zpart = s.zpart.p;
+    const bool ok = r1m <= 32 && r3m <= 2048 && a.n3l > 0 && a.mloc > 0;
+    if (ok) {
+      mega_plan(a);
+      s.mega_part.alloc((size_t)std::max<int64_t>(1, a.p.part_elems));
+      s.mega_sync.alloc((size_t)a.p.sync_words);
+      VSIE_CHECK_CUDA(cudaMemset(s.mega_sync.p, 0, s.mega_sync.bytes()));
+      a.part = s.mega_part.p;
+      a.sync = s.mega_sync.p;
+    }
+  }
   apply_reset_graphs(h);
   if (h->comm) {
     const int64_t mp = ceil_div(h->m, h->world);

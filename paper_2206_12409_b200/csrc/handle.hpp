@@ -9,6 +9,7 @@
 #include "comm.hpp"
 #include "geometry.hpp"
 #include "kernels.cuh"
+#include "mega.cuh"
 
 namespace vsie {
 
@@ -25,6 +26,12 @@ struct Shard {
   DevBuf<cplx> W2;      // [3][r2 * n3loc * nrhs]
   DevBuf<cplx> z3;      // [3][r3max * nrhs]
   DevBuf<cplx> zpart;   // [3][mloc_max * nrhs]  transpose: per-chi G4_chi^T z3_chi
+  // single-RHS persistent apply (mega.cu): plan, partials, sync words
+  MegaArgs mega{};
+  DevBuf<cplx> mega_part;
+  DevBuf<unsigned> mega_sync;
+  DevBuf<unsigned long long> mega_trace[2];   // diagnostics (vsie_coupling_set_tile_trace)
+  MegaPlan mega_traced[2]{};
   int n3loc() const { return i3e - i3b; }
   int64_t mloc() const { return ce - cb; }
 };
@@ -76,6 +83,8 @@ struct vsie_coupling_s {
   std::vector<vsie::GraphEntry> graphs;
   uint64_t graph_clock = 0;
   int use_graphs = 1;
+  int use_mega = 0;                          // single-RHS applies through the persistent kernel (opt-in)
+  int tile_trace = 0;
   vsie::DevBuf<vsie::cplx> gather_buf;     // allgather staging of z
   vsie::DevBuf<vsie::cplx> io_x, io_y;     // apply_host staging
   vsie::DevBuf<int64_t> io_idx;

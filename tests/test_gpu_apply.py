@@ -136,3 +136,31 @@ def test_tt_eval_matches_oracle(cfg1):
         got = h.tt_eval(torch.from_numpy(chi * cfg1.n_v + v), torch.from_numpy(idx[:, 3])).cpu().numpy()
         ref = ttmv.eval_at(tts[chi], idx)
         assert validate.rel_l2(got, ref) <= 1e-13
+
+
+@pytest.mark.parametrize("ci", [1, 2, 4])
+def test_persistent_vs_chains(ci):
+    """The persistent dataflow apply and the per-chi kernel chains compute the same
+    result (to rounding) for every op; each is bitwise reproducible run to run."""
+    from paper_2206_12409_b200 import Coupling
+    import torch
+    cfg = synth.get_config(ci)
+    r = cfg.ranks_probe
+    ranks = [r, (max(1, r[0] - 1), r[1] + 3, r[2] - 5), (r[0] + 1, max(1, r[1] - 2), r[2] + 7)]
+    tts = rand_tts(cfg, ranks, 60 + ci)
+    h = Coupling.from_cores(grid_of(cfg), cfg.meshes(), cfg.freq, tts, nrhs_max=1)
+    x = _cuda(synth.complex_gaussian(cfg.m, 11))
+    u = _cuda(synth.complex_gaussian(3 * cfg.n_v, 12))
+    out = {}
+    for persistent in (True, False):
+        h.configure(persistent=persistent)
+        for op, v in (("N", x), ("T", u), ("C", u)):
+            a = h.apply(v, op)
+            b = h.apply(v, op)
+            assert torch.equal(a, b), (persistent, op)
+            out[(persistent, op)] = a.cpu().numpy()
+    for op, v in (("N", x), ("T", u), ("C", u)):
+        assert validate.rel_l2(out[(True, op)], out[(False, op)]) <= 1e-13, op
+    if ci == 1:
+        for op, v in (("N", x), ("T", u), ("C", u)):
+            assert validate.rel_l2(out[(True, op)], ttmv.apply(tts, v.cpu().numpy(), op)) <= TOL

@@ -46,11 +46,33 @@ def timed(n, flush_l2=True):
     return float(np.median(ts)), float(np.mean(ts))
 
 
+def timed_stream(n, flush_l2):
+    """bench.py-style: back-to-back steps on the stream, events per step, one sync."""
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+    for i in range(n):
+        if flush_l2:
+            flush.fill_(i & 255)
+        ev[i][0].record(); step(); ev[i][1].record()
+    torch.cuda.synchronize()
+    t = [a.elapsed_time(b) for a, b in ev]
+    return float(np.median(t)), float(np.mean(t))
+
+
 for _ in range(5):
     step()
 torch.cuda.synchronize()
 med, mean = timed(steps)
 med_nf, _ = timed(steps, flush_l2=False)
+for persistent in (True, False):
+    h.configure(persistent=persistent)
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    a = timed_stream(steps, True)
+    b = timed_stream(steps, False)
+    print(json.dumps(dict(persistent=persistent, stream_flush_ms=a, stream_noflush_ms=b,
+                          gbs_flush=B / (a[1] * 1e-3) / 1e9, gbs_noflush=B / (b[1] * 1e-3) / 1e9)))
+h.configure(persistent=True)
 print(json.dumps(dict(cfg=ci, ranks=ranks, graph_ms_median=med, graph_ms_mean=mean, gbs=B / (mean * 1e-3) / 1e9,
                       graph_ms_median_noflush=med_nf, bytes_per_step=B)))
 # serialised per-kernel
