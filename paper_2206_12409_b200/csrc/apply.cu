@@ -24,19 +24,15 @@ struct Scope {
   size_t slot = 0;
   bool on;
   cudaStream_t stream = nullptr;
+  unsigned flags = cudaEventRecordDefault;   // external event nodes inside captures
   Scope(vsie_coupling_s* hh, const char* name, int64_t bytes, int64_t flops, cudaStream_t st) : h(hh), on(hh->timing) {
     if (!on) return;
     Timed t;
     t.name = name;
     t.bytes = bytes;
     t.flops = flops;
-    if (h->event_pool.size() < 2) {
-      for (int i = 0; i < 64; ++i) {
-        cudaEvent_t e;
-        VSIE_CHECK_CUDA(cudaEventCreate(&e));
-        h->event_pool.push_back(e);
-      }
-    }
+    VSIE_REQUIRE(h->event_pool.size() >= 2, VSIE_ERR_STATE,
+                 "timing event pool exhausted: read the timers (vsie_coupling_timers / _trace) more often");
     t.e0 = h->event_pool.back();
     h->event_pool.pop_back();
     t.e1 = h->event_pool.back();
@@ -44,13 +40,16 @@ struct Scope {
     t.chi = h->scope_chi;
     t.call = h->trace_call;
     t.origin = h->trace_origin;
-    VSIE_CHECK_CUDA(cudaEventRecord(t.e0, st));
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    VSIE_CHECK_CUDA(cudaStreamIsCapturing(st, &cs));
+    flags = cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+    VSIE_CHECK_CUDA(cudaEventRecordWithFlags(t.e0, st, flags));
     h->pending.push_back(t);
     slot = h->pending.size() - 1;
     stream = st;
   }
   ~Scope() {
-    if (on) cudaEventRecord(h->pending[slot].e1, stream);
+    if (on) cudaEventRecordWithFlags(h->pending[slot].e1, stream, flags);
   }
 };
 
@@ -580,10 +579,28 @@ void apply(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int nrhs, cudaStr
     return;
   }
   if (h->timing) {
-    // per-kernel CUDA-event timing: the same DAG serialised on the caller's stream
-    Streams S{st, {st, st, st}, false};
+    // per-kernel CUDA-event timing: the same DAG serialised on one stream, captured with
+    // its event records into a one-shot graph so that host submission gaps do not enter
+    // the per-kernel durations
+    Streams S{h->cap_stream, {h->cap_stream, h->cap_stream, h->cap_stream}, false};
     const int64_t before = launch_counter();
-    apply_dag(h, x, y, op, nrhs, S);
+    VSIE_CHECK_CUDA(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
+    cudaGraph_t graph = nullptr;
+    try {
+      apply_dag(h, x, y, op, nrhs, S);
+    } catch (...) {
+      cudaStreamEndCapture(h->cap_stream, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    VSIE_CHECK_CUDA(cudaStreamEndCapture(h->cap_stream, &graph));
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    VSIE_CHECK_CUDA(e);
+    e = cudaGraphLaunch(exec, st);
+    cudaGraphExecDestroy(exec);
+    VSIE_CHECK_CUDA(e);
     h->apply_launches += launch_counter() - before;
     return;
   }

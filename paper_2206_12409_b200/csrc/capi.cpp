@@ -297,6 +297,12 @@ int32_t vsie_coupling_set_timing(vsie_coupling_t h, int32_t enable) {
     h->trace_call = 0;
     VSIE_REQUIRE(enable >= 0 && enable <= 2, VSIE_ERR_ARG, "timing mode must be 0, 1 or 2");
     h->timing = enable;
+    // events are recorded inside stream captures, where they cannot be created
+    while (enable && h->event_pool.size() < 4096) {
+      cudaEvent_t e;
+      VSIE_CHECK_CUDA(cudaEventCreate(&e));
+      h->event_pool.push_back(e);
+    }
     return VSIE_OK;
   });
 }

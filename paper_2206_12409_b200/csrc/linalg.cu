@@ -7,6 +7,7 @@
 // to three problems (the chi components) with individual shapes; deterministic
 // split-K through a partial workspace.
 #include "kernels.cuh"
+#include "dmma_tile.cuh"
 
 #include <algorithm>
 
@@ -273,6 +274,37 @@ __global__ void __launch_bounds__(128) k_zgemm_dmma(const __grid_constant__ Zgem
       }
 }
 
+// 8-warp smem-staged 3M-DMMA tile (dmma_tile.cuh) per CTA; op(A) in {N, T}, op(B) = N.
+template <int WA, int WB, bool TA>
+__global__ void __launch_bounds__(tc::kThreads) k_zgemm_tc(const __grid_constant__ Zgemm g, int splits, int64_t mt,
+                                                           int64_t nt, cplx* __restrict__ ws, int64_t ws_stride,
+                                                           int direct) {
+  extern __shared__ __align__(16) unsigned char raw[];
+  tc::GemmSmem& sm = *reinterpret_cast<tc::GemmSmem*>(raw);
+  constexpr int TM = 16 * WA, TN = 16 * WB;
+  const int b = blockIdx.y;
+  if (b >= g.nbatch) return;
+  const int64_t tiles = mt * nt;
+  const int64_t tile = blockIdx.x % tiles;
+  const int sp = (int)(blockIdx.x / tiles);
+  const int64_t M = g.M[b], N = g.N[b], K = g.K[b];
+  const int64_t m0 = (tile % mt) * TM, n0 = (tile / mt) * TN;
+  if (m0 >= M || n0 >= N) return;
+  const int64_t chunks = (K + tc::GKC - 1) / tc::GKC;
+  const int64_t k0 = std::min<int64_t>(K, chunks * sp / splits * tc::GKC);
+  const int64_t k1 = std::min<int64_t>(K, chunks * (sp + 1) / splits * tc::GKC);
+  cplx* C;
+  int64_t ldc;
+  if (direct) {
+    C = g.C[b] + m0 + g.ldc[b] * n0;
+    ldc = g.ldc[b];
+  } else {
+    C = ws + ((int64_t)b * splits + sp) * ws_stride + m0 + M * n0;
+    ldc = M;
+  }
+  tc::gemm_tile<WA, WB, TA>(g.A[b], g.lda[b], g.B[b], g.ldb[b], M, N, m0, n0, k0, k1, sm, C, ldc);
+}
+
 template <int TA, int TB>
 void zgemm_t(const Zgemm& g, int splits, dim3 grid, cplx* ws, int64_t stride, cudaStream_t st) {
   k_zgemm<TA, TB><<<grid, NT, 0, st>>>(g, splits, ws, stride);
@@ -318,33 +350,50 @@ void launch_zgemm(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t st) {
 }
 
 void launch_zgemm_dmma(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t st) {
-  int64_t mt = 0, nt = 0, kmax = 0, mn = 0;
+  VSIE_REQUIRE(g.tb == kN && g.ta != kC, VSIE_ERR_ARG, "zgemm_dmma: op(A) in {N, T}, op(B) = N");
+  int64_t mmax = 0, nmax = 0, kmax = 0, mn = 0;
   for (int b = 0; b < g.nbatch; ++b) {
-    mt = std::max(mt, ceil_div(g.M[b], TCM));
-    nt = std::max(nt, ceil_div(g.N[b], TCN));
+    mmax = std::max(mmax, g.M[b]);
+    nmax = std::max(nmax, g.N[b]);
     kmax = std::max(kmax, g.K[b]);
     mn = std::max(mn, g.M[b] * g.N[b]);
   }
-  if (mt == 0 || nt == 0) return;
-  VSIE_REQUIRE(g.tb == kN, VSIE_ERR_ARG, "zgemm_dmma: op(B) must be N");
+  if (mmax == 0 || nmax == 0) return;
+  // warp layout: tall (4 x 2 -> 64 x 32) or wide (2 x 4 -> 32 x 64) output tiles
+  const bool tall = mmax >= 2 * nmax;
+  const int TM = tall ? tc::FTM : tc::ATM, TN = tall ? tc::FTN : tc::ATN;
+  const int64_t mt = ceil_div(mmax, TM), nt = ceil_div(nmax, TN);
   const int64_t tiles = mt * nt * g.nbatch;
-  const int64_t chunks = ceil_div(kmax, TCK);
+  const int64_t chunks = ceil_div(kmax, tc::GKC);
+  const bool unit = g.alpha.x == 1.0 && g.alpha.y == 0.0 && g.beta.x == 0.0 && g.beta.y == 0.0;
   int splits = 1;
-  if (ws != nullptr && tiles < 148 * 2) {
-    // >= 2 K chunks per split so that the register prefetch overlaps something
-    splits = (int)std::min<int64_t>(std::min<int64_t>(ceil_div(148 * 2, tiles), std::max<int64_t>(1, chunks / 2)), 64);
+  if (ws != nullptr && tiles < 40) {
+    splits = (int)std::min<int64_t>(std::min<int64_t>(ceil_div(100, tiles), std::max<int64_t>(1, chunks / 2)), 64);
     while (splits > 1 && (int64_t)splits * mn * g.nbatch > ws_elems) --splits;
     splits = std::max(splits, 1);
   }
+  const int direct = (splits == 1 && unit) ? 1 : 0;
+  VSIE_REQUIRE(direct || (ws != nullptr && (int64_t)splits * mn * g.nbatch <= ws_elems), VSIE_ERR_ARG,
+               "zgemm_dmma: workspace too small");
+  static bool attr = false;
+  const size_t smem = sizeof(tc::GemmSmem);
+  if (!attr) {
+    VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_zgemm_tc<tc::FWA, tc::FWB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_zgemm_tc<tc::FWA, tc::FWB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_zgemm_tc<tc::AWA, tc::AWB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_zgemm_tc<tc::AWA, tc::AWB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
   dim3 grid((unsigned)(mt * nt * splits), (unsigned)g.nbatch);
-  if (g.ta == kN)
-    k_zgemm_dmma<kN><<<grid, 128, 0, st>>>(g, splits, mt, nt, ws, mn);
-  else if (g.ta == kT)
-    k_zgemm_dmma<kT><<<grid, 128, 0, st>>>(g, splits, mt, nt, ws, mn);
+  const bool ta = g.ta == kT;
+  if (tall)
+    ta ? k_zgemm_tc<tc::FWA, tc::FWB, true><<<grid, tc::kThreads, smem, st>>>(g, splits, mt, nt, ws, mn, direct)
+       : k_zgemm_tc<tc::FWA, tc::FWB, false><<<grid, tc::kThreads, smem, st>>>(g, splits, mt, nt, ws, mn, direct);
   else
-    k_zgemm_dmma<kC><<<grid, 128, 0, st>>>(g, splits, mt, nt, ws, mn);
+    ta ? k_zgemm_tc<tc::AWA, tc::AWB, true><<<grid, tc::kThreads, smem, st>>>(g, splits, mt, nt, ws, mn, direct)
+       : k_zgemm_tc<tc::AWA, tc::AWB, false><<<grid, tc::kThreads, smem, st>>>(g, splits, mt, nt, ws, mn, direct);
   VSIE_CHECK_LAUNCH();
-  if (splits > 1) {
+  if (!direct) {
     dim3 rg((unsigned)std::min<int64_t>(ceil_div(mn, 256), 148 * 8), g.nbatch);
     k_splitk_reduce<<<rg, 256, 0, st>>>(g, splits, ws, mn);
     VSIE_CHECK_LAUNCH();

@@ -16,6 +16,8 @@
 #include "kernels.cuh"
 
 #include <algorithm>
+#include <utility>
+#include <vector>
 
 namespace vsie {
 
@@ -322,15 +324,24 @@ __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant_
     oaddr[j] = ok[j] ? col_addr(c, a.cols_per_rhs, a.ld_rhs, n1) : 0;
   }
   cplx* __restrict__ Y = a.y[b];
-  for (int m = 0; m < mt; ++m) {
-    double cr[2] = {0, 0}, ci[2] = {0, 0};
+  double bsum[KT];
 #pragma unroll
-    for (int ks = 0; ks < KT; ++ks) zmma(cr, ci, Af[(m * KT + ks) * 32 + lane], bf[ks]);
+  for (int ks = 0; ks < KT; ++ks) bsum[ks] = bf[ks].x + bf[ks].y;
+  for (int m = 0; m < mt; ++m) {
+    // 3 real DMMAs per complex product: P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi)
+    double p1[2] = {0, 0}, p2[2] = {0, 0}, p3[2] = {0, 0};
+#pragma unroll
+    for (int ks = 0; ks < KT; ++ks) {
+      const cplx av = Af[(m * KT + ks) * 32 + lane];
+      dmma(p1[0], p1[1], av.x, bf[ks].x);
+      dmma(p2[0], p2[1], av.y, bf[ks].y);
+      dmma(p3[0], p3[1], av.x + av.y, bsum[ks]);
+    }
     const int i1 = 8 * m + g;
     if (i1 < n1) {
 #pragma unroll
       for (int j = 0; j < 2; ++j)
-        if (ok[j]) __stcs(Y + oaddr[j] + i1, cmk(cr[j], ci[j]));
+        if (ok[j]) __stcs(Y + oaddr[j] + i1, cmk(p1[j] - p2[j], p3[j] - p1[j] - p2[j]));
     }
   }
 }
@@ -359,10 +370,11 @@ __global__ void __launch_bounds__(kG1Threads) k_reduce_g1(const __grid_constant_
   const bool cok = cg < a.ncol;
   const cplx* __restrict__ U = a.u[b] + (cok ? col_addr(cg, a.cols_per_rhs, a.ld_rhs, n1) : 0);
   const double sgn = a.conj_u ? -1.0 : 1.0;
-  double cr[NT][2], ci[NT][2];
+  // 3 real DMMAs per complex product (P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi))
+  double p1[NT][2], p2[NT][2], p3[NT][2];
 #pragma unroll
-  for (int nt = 0; nt < NT; ++nt) cr[nt][0] = cr[nt][1] = ci[nt][0] = ci[nt][1] = 0;
-  constexpr int UNR = 4;
+  for (int nt = 0; nt < NT; ++nt) p1[nt][0] = p1[nt][1] = p2[nt][0] = p2[nt][1] = p3[nt][0] = p3[nt][1] = 0;
+  constexpr int UNR = 8;
   int ks = 0;
   for (; ks + UNR <= ks_n; ks += UNR) {
     cplx av[UNR];
@@ -373,17 +385,27 @@ __global__ void __launch_bounds__(kG1Threads) k_reduce_g1(const __grid_constant_
     }
 #pragma unroll
     for (int q = 0; q < UNR; ++q) {
-      const cplx av2 = cmk(av[q].x, sgn * av[q].y);
+      const double ar = av[q].x, ai = sgn * av[q].y, as = ar + ai;
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) zmma(cr[nt], ci[nt], av2, Bf[((ks + q) * NT + nt) * 32 + lane]);
+      for (int nt = 0; nt < NT; ++nt) {
+        const cplx bv = Bf[((ks + q) * NT + nt) * 32 + lane];
+        dmma(p1[nt][0], p1[nt][1], ar, bv.x);
+        dmma(p2[nt][0], p2[nt][1], ai, bv.y);
+        dmma(p3[nt][0], p3[nt][1], as, bv.x + bv.y);
+      }
     }
   }
   for (; ks < ks_n; ++ks) {
     const int k = 4 * ks + t;
     cplx av = (cok && k < n1) ? __ldcs(U + k) : cmk(0, 0);
-    av.y *= sgn;
+    const double ar = av.x, ai = sgn * av.y, as = ar + ai;
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) zmma(cr[nt], ci[nt], av, Bf[(ks * NT + nt) * 32 + lane]);
+    for (int nt = 0; nt < NT; ++nt) {
+      const cplx bv = Bf[(ks * NT + nt) * 32 + lane];
+      dmma(p1[nt][0], p1[nt][1], ar, bv.x);
+      dmma(p2[nt][0], p2[nt][1], ai, bv.y);
+      dmma(p3[nt][0], p3[nt][1], as, bv.x + bv.y);
+    }
   }
   // lane holds rows c = c0 + g, columns a = 8 nt + 2 t + j
   if (cok) {
@@ -393,7 +415,7 @@ __global__ void __launch_bounds__(kG1Threads) k_reduce_g1(const __grid_constant_
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int aa = 8 * nt + 2 * t + j;
-        if (aa < r1) W[aa] = cmk(cr[nt][j], ci[nt][j]);
+        if (aa < r1) W[aa] = cmk(p1[nt][j] - p2[nt][j], p3[nt][j] - p1[nt][j] - p2[nt][j]);
       }
   }
 }
@@ -418,6 +440,18 @@ int pick_splits(int64_t other_ctas, int64_t len, int min_len, int max_splits, in
   return (int)std::max<int64_t>(1, sp);
 }
 
+// resident blocks per SM of a kernel at a block size (cached)
+int gemv_occupancy(const void* fn, int threads) {
+  static std::vector<std::pair<std::pair<const void*, int>, int>> cache;
+  for (auto& e : cache)
+    if (e.first.first == fn && e.first.second == threads) return e.second;
+  int occ = 1;
+  VSIE_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, 0));
+  occ = std::max(1, occ);
+  cache.push_back({{fn, threads}, occ});
+  return occ;
+}
+
 int sm_count() {
   static int n = [] {
     int dev = 0, v = 148;
@@ -437,17 +471,17 @@ void launch_gemv_n(const GemvN& a, cplx* partials, int64_t partials_cap, int max
   }
   if (rmax == 0) return;
   constexpr int U = 4;
-  // row tiles of <= 512 rows, as equal as possible, warp-multiple block
-  const int64_t ntile = ceil_div(rmax, 512);
-  const int T = (int)(ceil_div(ceil_div(rmax, ntile), 32) * 32);
+  // one row tile when R <= 320 (block = R rounded to a warp), else 256-row tiles
+  const int T = rmax <= 320 ? (int)(ceil_div(rmax, 32) * 32) : 256;
   const int64_t rtiles = ceil_div(rmax, T);
-  static int occ = 0;
-  if (!occ) {
-    VSIE_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gemv_n<U>, 512, 0));
-    occ = std::max(1, occ) * 512;  // resident threads per SM
-  }
-  const int64_t slots = (int64_t)sm_count() * std::max(1, occ / T);
-  int ns = pick_splits(rtiles * a.nbatch, cmax, 24, max_splits, 2 * slots);
+  // column splits: fill whole waves of resident CTAs (2 waves when a split keeps >= 24
+  // columns, else 1) -- a partial last wave is a straggler tail for the whole kernel
+  const int64_t slots = (int64_t)sm_count() * gemv_occupancy((const void*)k_gemv_n<U>, T);
+  const int64_t per = rtiles * a.nbatch;
+  int64_t nsl = std::max<int64_t>(1, 2 * slots / per);
+  if (cmax / nsl < 24) nsl = std::max<int64_t>(1, slots / per);
+  nsl = std::min<int64_t>(nsl, std::max<int64_t>(1, cmax / 16));
+  int ns = (int)std::min<int64_t>(nsl, max_splits);
   while (ns > 1 && (int64_t)a.nbatch * ns * rmax > partials_cap) --ns;
   dim3 grid(ns, (unsigned)rtiles, a.nbatch);
   k_gemv_n<U><<<grid, T, 0, st>>>(a, partials, rmax);
@@ -488,7 +522,9 @@ void launch_gemv_t(const GemvT& a, cplx* partials, int64_t partials_cap, int max
   if (cmax == 0) return;
   const int64_t ctiles = ceil_div(cmax, kColsPerCta);
   const int nz = a.sum_batch ? 1 : a.nbatch;
-  int ns = a.sum_batch ? 1 : pick_splits(ctiles * nz, rmax, 256, max_splits, (int64_t)sm_count() * 8 * 2);
+  // row splits: fill two waves of resident CTAs when a split keeps >= 128 rows
+  const int64_t slots = (int64_t)sm_count() * gemv_occupancy((const void*)k_gemv_t, kThreads);
+  int ns = a.sum_batch ? 1 : pick_splits(ctiles * nz, rmax, 128, max_splits, 2 * slots);
   while (ns > 1 && (int64_t)nz * ns * cmax > partials_cap) --ns;
   dim3 grid((unsigned)ctiles, ns, nz);
   k_gemv_t<<<grid, kThreads, 0, st>>>(a, partials, cmax);

@@ -72,7 +72,7 @@ for persistent in (True, False):
     b = timed_stream(steps, False)
     print(json.dumps(dict(persistent=persistent, stream_flush_ms=a, stream_noflush_ms=b,
                           gbs_flush=B / (a[1] * 1e-3) / 1e9, gbs_noflush=B / (b[1] * 1e-3) / 1e9)))
-h.configure(persistent=True)
+h.configure(persistent=False)
 print(json.dumps(dict(cfg=ci, ranks=ranks, graph_ms_median=med, graph_ms_mean=mean, gbs=B / (mean * 1e-3) / 1e9,
                       graph_ms_median_noflush=med_nf, bytes_per_step=B)))
 # serialised per-kernel
