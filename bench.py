@@ -34,14 +34,14 @@ import synth  # noqa: E402
 METRIC = "Z_bc TT matvec+adjoint ms & HBM GB/s per GMRES step; Z_bc entries/sec (FP64)"
 
 
-def step_bytes_flops(n, m, ranks):
-    """SURVEY §8d: B_fwd = 16 [sum_chi (n1 r1 + r1 n2 r2 + r2 n3 r3 + r3 m) + m + 3 n_v], B_adj = B_fwd;
-    F = 8 sum_chi (r3 m + r2 n3 r3 + r1 n2 r2 n3 + n_v r1) per direction."""
+def step_bytes_flops(n, m, ranks, k=1):
+    """SURVEY §8d: B_fwd = 16 [sum_chi (n1 r1 + r1 n2 r2 + r2 n3 r3 + r3 m) + k (m + 3 n_v)], B_adj = B_fwd;
+    F = 8 k sum_chi (r3 m + r2 n3 r3 + r1 n2 r2 n3 + n_v r1) per direction (block: cores once, vectors x k)."""
     n1, n2, n3 = n
     nv = n1 * n2 * n3
     cores = sum(n1 * r1 + r1 * n2 * r2 + r2 * n3 * r3 + r3 * m for (r1, r2, r3) in ranks)
-    b_fwd = 16 * (cores + m + 3 * nv)
-    f_fwd = 8 * sum(r3 * m + r2 * n3 * r3 + r1 * n2 * r2 * n3 + nv * r1 for (r1, r2, r3) in ranks)
+    b_fwd = 16 * (cores + k * (m + 3 * nv))
+    f_fwd = 8 * k * sum(r3 * m + r2 * n3 * r3 + r1 * n2 * r2 * n3 + nv * r1 for (r1, r2, r3) in ranks)
     return 2 * b_fwd, 2 * f_fwd
 
 
@@ -115,20 +115,32 @@ def cpu_cores():
 
 def oracle_step_rate(cfg, ranks, steps=2, seed=5):
     """The CPU oracle (oracle/ttmv.py, as it stands) timed on the host cores on the
-    same workload: random cores with the GPU build's ranks (matvec cost does not
-    depend on the core values)."""
+    same workload: cores with the GPU build's ranks (matvec cost does not depend on the
+    core values).  Large configs (n_v > 5e6) time chi 0 only (forward +
+    transpose of one chi TT, constant-valued cores) and scale by 3 -- the three chi
+    components are identical work -- to bound the sample to ~10-30 s."""
     from oracle import ttmv
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from gpu_common import rand_tts
-    tts = rand_tts(cfg, ranks, seed)
-    x = synth.complex_gaussian(cfg.m, synth.SEEDS["x"])
-    u = synth.complex_gaussian(3 * cfg.n_v, synth.SEEDS["u"])
+    big = cfg.n_v > 5_000_000
+    if big:
+        dims = tuple(cfg.n) + (cfg.m,)
+        rr = (1,) + tuple(ranks[0]) + (1,)
+        tts = [[np.full((rr[k], dims[k], rr[k + 1]), 0.5 + 0.25j) / np.sqrt(rr[k]) for k in range(4)]]
+        x = np.full(cfg.m, 1.0 + 0.5j)
+        u = np.full(cfg.n_v, 0.5 - 1.0j)
+        scale = 3.0
+    else:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from gpu_common import rand_tts
+        tts = rand_tts(cfg, ranks, seed)
+        x = synth.complex_gaussian(cfg.m, synth.SEEDS["x"])
+        u = synth.complex_gaussian(3 * cfg.n_v, synth.SEEDS["u"])
+        scale = 1.0
     ts = []
     for _ in range(steps):
         t0 = time.perf_counter()
         ttmv.apply(tts, x, "N")
         ttmv.apply(tts, u, "T")
-        ts.append(time.perf_counter() - t0)
+        ts.append((time.perf_counter() - t0) * scale)
     return statistics.median(ts), ts
 
 
@@ -142,8 +154,9 @@ def oracle_entry_rate(cfg, count=20000):
 
 
 def ranks_hint(cfg):
-    """Ranks of the last GPU build of this config (committed under profiles/), else the probe ranks."""
-    p = os.path.join(ROOT, "profiles", f"ranks_cfg{cfg.idx}.json")
+    """Ranks of the last GPU build of this config (committed under profiles/; the block
+    workload cfg 5 has the geometry of cfg 3), else the probe ranks."""
+    p = os.path.join(ROOT, "profiles", f"ranks_cfg{3 if cfg.idx == 5 else cfg.idx}.json")
     if os.path.exists(p):
         with open(p) as f:
             return [tuple(r) for r in json.load(f)["ranks"]]
@@ -180,6 +193,36 @@ def run_reference(args):
     return 0
 
 
+def device_cores(cfg, ranks, seed, dev):
+    """Seeded random complex TT cores at the given ranks, drawn on the device (the core
+    values do not change the matvec cost) and returned as host arrays."""
+    import torch
+    g = torch.Generator(device=dev)
+    dims = tuple(cfg.n) + (cfg.m,)
+    out = []
+    for c in range(3):
+        rr = (1,) + tuple(ranks[c]) + (1,)
+        g.manual_seed(seed + 101 * c)
+        cores = []
+        for k in range(4):
+            shp = (rr[k], dims[k], rr[k + 1])
+            a = torch.randn(shp + (2,), generator=g, device=dev, dtype=torch.float64) / np.sqrt(2 * rr[k])
+            cores.append(torch.view_as_complex(a).cpu().numpy())
+        out.append(cores)
+    return out
+
+
+def device_gaussian(n, k, seed, dev):
+    """(a + ib)/sqrt 2 complex Gaussian (n x k, column-major) drawn on the device with a
+    seeded generator -- used for the block-RHS workload whose 30 GB voxel block is not
+    built on the host (SURVEY §8d recipe, torch generator instead of PCG64)."""
+    import torch
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    a = torch.randn((k, n, 2), generator=g, device=dev, dtype=torch.float64) / np.sqrt(2.0)
+    return torch.view_as_complex(a).reshape(-1)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -187,6 +230,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cores", default="auto", choices=["auto", "build", "random"],
+                    help="build = TT-cross build (default for configs 1, 2, 4); random = seeded cores at the "
+                         "ranks of the recorded build (configs 3, 5: the build takes minutes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -210,30 +256,42 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
     cfg = synth.get_config(args.config)
+    k = cfg.nrhs
+    mode = args.cores if args.cores != "auto" else ("build" if cfg.idx in (1, 2, 4) else "random")
     t0 = time.perf_counter()
-    h = Coupling.build(grid_of(cfg), cfg.meshes(), cfg.freq, cfg.tol, nrhs_max=1, rank=rank, world=world,
-                       nccl_unique_id=uid, device=local)
+    if mode == "build":
+        h = Coupling.build(grid_of(cfg), cfg.meshes(), cfg.freq, cfg.tol, nrhs_max=k, rank=rank, world=world,
+                           nccl_unique_id=uid, device=local)
+    else:
+        ranks0 = ranks_hint(cfg)
+        h = Coupling.from_cores(grid_of(cfg), cfg.meshes(), cfg.freq, device_cores(cfg, ranks0, 7, dev), nrhs_max=k,
+                                rank=rank, world=world, nccl_unique_id=uid, device=local)
     build_s = time.perf_counter() - t0
     inf = h.info()
     ranks = inf["ranks"]
     if rank == 0:
         os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    B, F = step_bytes_flops(cfg.n, cfg.m, ranks)
+    B, F = step_bytes_flops(cfg.n, cfg.m, ranks, k)
     n1, n2, n3 = cfg.n
     n3loc = inf["slab"][1] - inf["slab"][0]
     vox_loc = 3 * n1 * n2 * n3loc
-    x = torch.from_numpy(synth.complex_gaussian(cfg.m, synth.SEEDS["x"])).to(dev)
-    u_full = synth.complex_gaussian(3 * cfg.n_v, synth.SEEDS["u"]).reshape(3, -1)
-    u_np = np.ascontiguousarray(u_full[:, n1 * n2 * inf["slab"][0]:n1 * n2 * inf["slab"][1]].reshape(-1))
-    u = torch.from_numpy(u_np).to(dev)
-    y = torch.empty(vox_loc, dtype=torch.complex128, device=dev)
-    z = torch.empty(cfg.m, dtype=torch.complex128, device=dev)
+    if k == 1:
+        x = torch.from_numpy(synth.complex_gaussian(cfg.m, synth.SEEDS["x"])).to(dev)
+        u_full = synth.complex_gaussian(3 * cfg.n_v, synth.SEEDS["u"]).reshape(3, -1)
+        u_np = np.ascontiguousarray(u_full[:, n1 * n2 * inf["slab"][0]:n1 * n2 * inf["slab"][1]].reshape(-1))
+        u = torch.from_numpy(u_np).to(dev)
+    else:
+        x = device_gaussian(cfg.m, k, synth.SEEDS["X"], dev)
+        u = device_gaussian(vox_loc, k, synth.SEEDS["U"], dev)
+        u_np = None
+    y = torch.empty(vox_loc * k, dtype=torch.complex128, device=dev)
+    z = torch.empty(cfg.m * k, dtype=torch.complex128, device=dev)
     flush = torch.empty(512 * 2 ** 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream()
 
     def step():
-        h.apply_raw(x.data_ptr(), y.data_ptr(), "N", 1, stream)
-        h.apply_raw(u.data_ptr(), z.data_ptr(), "T", 1, stream)
+        h.apply_raw(x.data_ptr(), y.data_ptr(), "N", k, stream)
+        h.apply_raw(u.data_ptr(), z.data_ptr(), "T", k, stream)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -246,7 +304,7 @@ def main():
         # samples see it (untimed), then the timed region
         t_end = time.perf_counter() + 0.6
         while time.perf_counter() < t_end:
-            for _ in range(20):
+            for _ in range(20 if k == 1 else 1):
                 flush.fill_(1)
                 step()
             torch.cuda.synchronize()
@@ -281,26 +339,35 @@ def main():
     value = B / (ms * 1e-3) / 1e9
 
     # ---- end to end: host buffers through the C ABI (H2D + apply + D2H inside)
-    xh = torch.from_numpy(synth.complex_gaussian(cfg.m, synth.SEEDS["x"])).pin_memory()
-    uh = torch.from_numpy(u_np).pin_memory()
-    yh = torch.empty(vox_loc, dtype=torch.complex128).pin_memory()
-    zh = torch.empty(cfg.m, dtype=torch.complex128).pin_memory()
-    for _ in range(2):
-        h.apply_host_raw(xh.data_ptr(), yh.data_ptr(), "N", 1)
-        h.apply_host_raw(uh.data_ptr(), zh.data_ptr(), "T", 1)
-    e2e = []
-    for _ in range(max(3, min(args.steps, 20))):
+    e2e = None
+    if vox_loc * k * 16 <= (4 << 30):
+        xh = (torch.from_numpy(synth.complex_gaussian(cfg.m, synth.SEEDS["x"])) if k == 1 else x.cpu()).pin_memory()
+        uh = (torch.from_numpy(u_np) if k == 1 else u.cpu()).pin_memory()
+        yh = torch.empty(vox_loc * k, dtype=torch.complex128).pin_memory()
+        zh = torch.empty(cfg.m * k, dtype=torch.complex128).pin_memory()
+        for _ in range(2):
+            h.apply_host_raw(xh.data_ptr(), yh.data_ptr(), "N", k)
+            h.apply_host_raw(uh.data_ptr(), zh.data_ptr(), "T", k)
+        tl = []
+        for _ in range(max(3, min(args.steps, 20))):
+            if world > 1:
+                dist.barrier()
+            t1 = time.perf_counter()
+            h.apply_host_raw(xh.data_ptr(), yh.data_ptr(), "N", k)
+            h.apply_host_raw(uh.data_ptr(), zh.data_ptr(), "T", k)
+            tl.append(time.perf_counter() - t1)
+        e2e_s = float(np.mean(tl))
         if world > 1:
-            dist.barrier()
-        t1 = time.perf_counter()
-        h.apply_host_raw(xh.data_ptr(), yh.data_ptr(), "N", 1)
-        h.apply_host_raw(uh.data_ptr(), zh.data_ptr(), "T", 1)
-        e2e.append(time.perf_counter() - t1)
-    e2e_s = float(np.mean(e2e))
-    if world > 1:
-        tt = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_s = float(tt.item())
+            tt = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt.item())
+        h2d = 16 * (cfg.m + vox_loc) * k
+        e2e = {"value": B / e2e_s / 1e9, "unit": "GB/s", "ms_per_step": e2e_s * 1e3,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": h2d}
+    else:
+        e2e = {"value": None, "unit": "GB/s", "h2d_bytes_per_step": 16 * (cfg.m + vox_loc) * k,
+               "d2h_bytes_per_step": 16 * (cfg.m + vox_loc) * k,
+               "note": "not run: the pinned host copies of this block workload exceed 4 GiB"}
 
     # ---- entries/s (FP64): 1e6 uniform random (row, col) through vsie_coupling_entries
     ne = 1_000_000
@@ -339,40 +406,46 @@ def main():
         roof = {"bound": "hbm", "kernel": dom["name"], "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": ach / peak, "traffic": traffic, "peak_source": peak_kind,
                 "share_of_step": dom["total_ms"] / max(1e-9, sum(t["total_ms"] for t in timers)),
-                "bytes_per_launch": dom["bytes_per_launch"], "avg_us": avg_ms * 1e3}
+                "bytes_per_launch": dom["bytes_per_launch"], "avg_us": avg_ms * 1e3,
+                "step_frac": value / peak}
     kern_table = {t["name"]: {"avg_us": 1e3 * t["total_ms"] / max(1, t["launches"]),
+                              "launches_per_step": t["launches"] / max(1, args.steps),
                               "gbs": (t["bytes_per_launch"] / (t["total_ms"] / t["launches"] * 1e-3) / 1e9)
                               if t["bytes_per_launch"] else None} for t in timers}
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        t_cpu, ts = oracle_step_rate(cfg, ranks, steps=2)
-        cpu = {"value": B / t_cpu / 1e9, "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
-               "sample": "2 full GMRES steps (oracle TT fwd + transpose, NumPy) of the same cfg and ranks, "
-                         "random cores", "ms_per_step": t_cpu * 1e3,
-               "entries_per_s": oracle_entry_rate(cfg)}
-    h2d = 16 * (cfg.m + vox_loc)
-    d2h = 16 * (vox_loc + cfg.m)
+        t_cpu, ts = oracle_step_rate(cfg, ranks, steps=1 if cfg.n_v > 5e6 else 2)
+        B1, _ = step_bytes_flops(cfg.n, cfg.m, ranks, 1)
+        cpu = {"value": B1 / t_cpu / 1e9, "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
+               "sample": ("single-RHS GMRES step(s) (oracle TT fwd + transpose, NumPy) of the same cfg and ranks"
+                          + (", chi 0 timed and x3" if cfg.n_v > 5_000_000 else ", random cores")
+                          + (" (per RHS column of the block workload)" if k > 1 else "")),
+               "ms_per_step": t_cpu * 1e3, "entries_per_s": oracle_entry_rate(cfg)}
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": f"cfg{cfg.idx} {cfg.name}: grid {cfg.n}, h {cfg.h[0]*1e3:.0f} mm, m={cfg.m} RWG "
-                               f"(shield {cfg.surfaces[0].n_az}x{cfg.surfaces[0].n_ax}), f=298.2 MHz, tol {cfg.tol}",
-                   "step": "1 forward (y = Z x) + 1 transpose (z = Z^T u) TT apply", "ranks": ranks,
+                               f"({' + '.join(f'{s.name} {s.n_az}x{s.n_ax}' for s in cfg.surfaces)}), "
+                               f"f=298.2 MHz, tol {cfg.tol}, nrhs {k}",
+                   "step": f"1 forward (Y = Z X) + 1 transpose (Z^T U) TT apply, {k} RHS",
+                   "cores": ("TT-cross build on this GPU" if mode == "build"
+                             else "seeded random cores at the ranks of the recorded B200 build (profiles/)"),
+                   "ranks": ranks,
                    "parallelism": f"slab{world} (i3 planes + G4 columns, NCCL)" if world > 1 else "1 GPU",
                    "l2": "flushed between timed steps (512 MiB write)",
                    "bytes_per_step": B, "flops_per_step": F, "build_s": build_s,
                    "build_breakdown_s": {"entries": inf["build_entry_s"], "factor": inf["build_factor_s"],
-                                         "maxvol": inf["build_maxvol_s"]},
-                   "heldout_err": inf["heldout_err"], "sweeps": inf["sweeps"],
+                                         "maxvol": inf["build_maxvol_s"]} if mode == "build" else None,
+                   "heldout_err": inf["heldout_err"] if mode == "build" else None,
+                   "sweeps": inf["sweeps"] if mode == "build" else None,
                    "compression": float(inf["compression"]) if inf["compression"] else None},
         "entries": {"value": ent_s, "unit": "entries/s", "pair_interactions_per_s": 48 * ent_s,
                     "sample": "1e6 uniform random (row, col), 5 reps"},
         "roofline": roof,
         "kernels": kern_table,
         "cpu_baseline": cpu,
-        "e2e": {"value": B / e2e_s / 1e9, "unit": "GB/s", "ms_per_step": e2e_s * 1e3,
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e": e2e,
         "gpu_launches": int(launches),
         "gpu_launches_note": "kernel launches of this library inside the K timed steps (count from the library's launch counter; includes split-K sum kernels)",
         "clocks": clk.summary(),
@@ -380,8 +453,9 @@ def main():
     print(json.dumps(line))
     with open(os.path.join(ROOT, "gpurun_out", f"bench_cfg{cfg.idx}_n{world}.json"), "w") as f:
         json.dump(line, f, indent=1)
-    with open(os.path.join(ROOT, "gpurun_out", f"ranks_cfg{cfg.idx}.json"), "w") as f:
-        json.dump({"ranks": ranks, "source": "vsie_coupling_build on B200"}, f)
+    if mode == "build":
+        with open(os.path.join(ROOT, "gpurun_out", f"ranks_cfg{cfg.idx}.json"), "w") as f:
+            json.dump({"ranks": ranks, "source": "vsie_coupling_build on B200"}, f)
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -205,12 +205,12 @@ int32_t vsie_coupling_info(vsie_coupling_t h, vsie_info* out);
 int32_t vsie_coupling_set_timing(vsie_coupling_t h, int32_t enable);
 int32_t vsie_coupling_timers(vsie_coupling_t h, vsie_timer* out, int32_t max, int32_t* n_out);
 
-/* Execution strategy of vsie_coupling_apply (results agree to rounding; both are
+/* Execution strategy of vsie_coupling_apply (all results agree to rounding and each is
  * deterministic): use_graphs = 1 (default) replays each (op, nrhs, x, y) as a captured
- * CUDA graph; use_persistent = 1 runs single-RHS applies as one persistent dataflow
- * kernel per direction, 0 (default) as three concurrent per-chi kernel chains (faster on
- * B200 at the BASELINE configs).  Negative = keep. */
-int32_t vsie_coupling_configure(vsie_coupling_t h, int32_t use_graphs, int32_t use_persistent);
+ * CUDA graph.  mode selects the single-RHS schedule: 0 (default) three concurrent per-chi
+ * kernel chains, 1 one persistent dataflow kernel per direction, 2 one batched kernel per
+ * contraction step (see DESIGN.md for the measured comparison).  Negative = keep. */
+int32_t vsie_coupling_configure(vsie_coupling_t h, int32_t use_graphs, int32_t mode);
 
 /* Diagnostics of the persistent single-RHS apply: with enable = 1 every tile of the
  * following applies records its start / end (globaltimer) and SM; records of the last

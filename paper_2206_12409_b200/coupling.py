@@ -252,11 +252,17 @@ class Coupling:
         """0/False off, 1/True serialised per-kernel timing, 2 concurrent timeline (trace())."""
         check(lib().vsie_coupling_set_timing(self._h, int(enable)))
 
-    def configure(self, graphs=None, persistent=None):
-        """Apply strategy: CUDA-graph replay and the persistent single-RHS kernel (None = keep)."""
+    MODES = {"chains": 0, "persistent": 1, "batched": 2}
+
+    def configure(self, graphs=None, mode=None, persistent=None):
+        """Apply strategy: CUDA-graph replay and the single-RHS schedule (None = keep):
+        mode 'chains' (default), 'persistent' or 'batched'; persistent=True/False is a
+        shorthand for mode 'persistent' / 'chains'."""
         g = -1 if graphs is None else int(bool(graphs))
-        p = -1 if persistent is None else int(bool(persistent))
-        check(lib().vsie_coupling_configure(self._h, g, p))
+        if persistent is not None:
+            mode = "persistent" if persistent else "chains"
+        m = -1 if mode is None else (self.MODES[mode] if isinstance(mode, str) else int(mode))
+        check(lib().vsie_coupling_configure(self._h, g, m))
 
     def set_tile_trace(self, enable):
         check(lib().vsie_coupling_set_tile_trace(self._h, int(bool(enable))))

@@ -360,7 +360,7 @@ bool mega_ready(vsie_coupling_s* h) {
     const char* e = std::getenv("VSIE_MEGA");
     return e ? std::atoi(e) : 1;
   }();
-  if (!env || !h->use_mega) return false;
+  if (!env || h->apply_mode != 1) return false;
   for (const Shard& s : h->shards)
     if (!s.mega.sync) return false;
   return true;
@@ -441,10 +441,209 @@ void apply_mega(vsie_coupling_s* h, const cplx* x, cplx* y, int op, cudaStream_t
   }
 }
 
+// ------------------------------------------------------------------ batched single-stream apply
+// One launch per contraction step covering all three chi (nbatch = 3): fewer, larger
+// kernels than the per-chi chains (each kernel's launch / ramp / tail is paid once per
+// step for the three components), in the order of Eq. 17 / Eqs. 18-19; the transpose's
+// last GEMV sums over chi inside the kernel (Eq. 18).
+void apply_batched(vsie_coupling_s* h, const cplx* x, cplx* y, int op, cudaStream_t st) {
+  const int n1 = h->grid.n[0], n2 = h->grid.n[1];
+  const int64_t m = h->m;
+  int r1m = 1, r2m = 1, r3m = 1;
+  for (int c = 0; c < 3; ++c) {
+    r1m = std::max(r1m, h->ranks[c][0]);
+    r2m = std::max(r2m, h->ranks[c][1]);
+    r3m = std::max(r3m, h->ranks[c][2]);
+  }
+  const IoLayout L = voxel_layout(h);
+  auto R = [&](int c, int j) { return (int64_t)h->ranks[c][j]; };
+  const bool exchange = h->comm != nullptr || h->shards.size() > 1;
+  cplx* part = h->partials.p;
+  const int64_t pcap = 3 * h->partials_per_chi;
+  cplx* zws = h->zgemm_ws.p;
+  const int64_t zcap = 3 * h->zgemm_ws_per_chi;
+  if (op == VSIE_OP_N) {
+    for (Shard& s : h->shards) {
+      if (s.mloc() == 0) {
+        VSIE_CHECK_CUDA(cudaMemsetAsync(s.y4.p, 0, s.y4.bytes(), st));
+        continue;
+      }
+      GemvN g{};
+      g.nbatch = 3;
+      int64_t bytes = 16 * s.mloc(), fl = 0;
+      for (int c = 0; c < 3; ++c) {
+        g.A[c] = s.G4[c].p;
+        g.x[c] = x + s.cb;
+        g.y[c] = s.y4.p + c * r3m;
+        g.R[c] = R(c, 2);
+        g.C[c] = s.mloc();
+        bytes += 16 * (R(c, 2) * s.mloc() + R(c, 2));
+        fl += 8 * R(c, 2) * s.mloc();
+      }
+      Scope sc(h, "fwd_g4_gemv", bytes, fl, st);
+      launch_gemv_n(g, part, pcap, kMaxSplits, st);
+    }
+    if (exchange) combine_r3(h, &Shard::y4, 3 * (int64_t)r3m, st);
+    for (Shard& s : h->shards) {
+      const int64_t n3l = s.n3loc();
+      if (n3l == 0) continue;
+      {
+        GemvN g{};
+        g.nbatch = 3;
+        int64_t bytes = 0, fl = 0;
+        for (int c = 0; c < 3; ++c) {
+          g.A[c] = s.G3[c].p;
+          g.x[c] = s.y4.p + c * r3m;
+          g.y[c] = s.Y3.p + c * r2m * n3l;
+          g.R[c] = R(c, 1) * n3l;
+          g.C[c] = R(c, 2);
+          bytes += 16 * (R(c, 1) * n3l * R(c, 2) + R(c, 1) * n3l + R(c, 2));
+          fl += 8 * R(c, 1) * n3l * R(c, 2);
+        }
+        Scope sc(h, "fwd_g3_gemv", bytes, fl, st);
+        launch_gemv_n(g, part, pcap, kMaxSplits, st);
+      }
+      {
+        Zgemm z{};
+        z.nbatch = 3;
+        int64_t bytes = 0, fl = 0;
+        for (int c = 0; c < 3; ++c) {
+          z.M[c] = R(c, 0) * n2; z.N[c] = n3l; z.K[c] = R(c, 1);
+          z.A[c] = h->G2[c].p; z.lda[c] = R(c, 0) * n2;
+          z.B[c] = s.Y3.p + c * r2m * n3l; z.ldb[c] = R(c, 1);
+          z.C[c] = s.Y2.p + c * r1m * n2 * n3l; z.ldc[c] = R(c, 0) * n2;
+          bytes += 16 * (R(c, 0) * n2 * R(c, 1) + R(c, 1) * n3l + R(c, 0) * n2 * n3l);
+          fl += 8 * R(c, 0) * n2 * R(c, 1) * n3l;
+        }
+        Scope sc(h, "fwd_g2_zgemm", bytes, fl, st);
+        launch_zgemm_dmma(z, zws, zcap, st);
+      }
+      {
+        ExpandArgs e{};
+        e.nbatch = 3;
+        e.n1 = n1;
+        e.ncol = (int64_t)n2 * n3l;
+        e.cols_per_rhs = e.ncol;
+        e.ld_rhs = L.ld;
+        int64_t bytes = 0, fl = 0;
+        for (int c = 0; c < 3; ++c) {
+          e.G1[c] = h->G1[c].p;
+          e.Y2[c] = s.Y2.p + c * r1m * n2 * n3l;
+          e.y[c] = y + c * L.chi_stride + shard_voxel_offset(h, s, L);
+          e.r1[c] = (int)R(c, 0);
+          bytes += 16 * ((int64_t)n1 * R(c, 0) + R(c, 0) * n2 * n3l + (int64_t)n1 * n2 * n3l);
+          fl += 8 * (int64_t)n1 * R(c, 0) * n2 * n3l;
+        }
+        Scope sc(h, "fwd_g1_expand", bytes, fl, st);
+        launch_expand_g1(e, st);
+      }
+    }
+    return;
+  }
+  const bool cj = op == VSIE_OP_C;
+  for (Shard& s : h->shards) {
+    const int64_t n3l = s.n3loc();
+    if (n3l == 0) {
+      VSIE_CHECK_CUDA(cudaMemsetAsync(s.z3.p, 0, s.z3.bytes(), st));
+      continue;
+    }
+    {
+      ReduceArgs r{};
+      r.nbatch = 3;
+      r.n1 = n1;
+      r.ncol = (int64_t)n2 * n3l;
+      r.cols_per_rhs = r.ncol;
+      r.ld_rhs = L.ld;
+      r.conj_u = cj;
+      int64_t bytes = 0, fl = 0;
+      for (int c = 0; c < 3; ++c) {
+        r.G1[c] = h->G1[c].p;
+        r.u[c] = x + c * L.chi_stride + shard_voxel_offset(h, s, L);
+        r.W1[c] = s.Y2.p + c * r1m * n2 * n3l;
+        r.r1[c] = (int)R(c, 0);
+        bytes += 16 * ((int64_t)n1 * R(c, 0) + R(c, 0) * n2 * n3l + (int64_t)n1 * n2 * n3l);
+        fl += 8 * (int64_t)n1 * R(c, 0) * n2 * n3l;
+      }
+      Scope sc(h, "adj_g1_reduce", bytes, fl, st);
+      launch_reduce_g1(r, st);
+    }
+    {
+      Zgemm z{};
+      z.nbatch = 3;
+      z.ta = kT;
+      int64_t bytes = 0, fl = 0;
+      for (int c = 0; c < 3; ++c) {
+        z.M[c] = R(c, 1); z.N[c] = n3l; z.K[c] = R(c, 0) * n2;
+        z.A[c] = h->G2[c].p; z.lda[c] = R(c, 0) * n2;
+        z.B[c] = s.Y2.p + c * r1m * n2 * n3l; z.ldb[c] = R(c, 0) * n2;
+        z.C[c] = s.W2.p + c * r2m * n3l; z.ldc[c] = R(c, 1);
+        bytes += 16 * (R(c, 0) * n2 * R(c, 1) + R(c, 1) * n3l + R(c, 0) * n2 * n3l);
+        fl += 8 * R(c, 0) * n2 * R(c, 1) * n3l;
+      }
+      Scope sc(h, "adj_g2_zgemm", bytes, fl, st);
+      launch_zgemm_dmma(z, zws, zcap, st);
+    }
+    {
+      GemvT g{};
+      g.nbatch = 3;
+      int64_t bytes = 0, fl = 0;
+      for (int c = 0; c < 3; ++c) {
+        g.A[c] = s.G3[c].p;
+        g.x[c] = s.W2.p + c * r2m * n3l;
+        g.y[c] = s.z3.p + c * r3m;
+        g.R[c] = R(c, 1) * n3l;
+        g.C[c] = R(c, 2);
+        bytes += 16 * (R(c, 1) * n3l * R(c, 2) + R(c, 1) * n3l + R(c, 2));
+        fl += 8 * R(c, 1) * n3l * R(c, 2);
+      }
+      Scope sc(h, "adj_g3_gemv", bytes, fl, st);
+      launch_gemv_t(g, part, pcap, kMaxSplits, st);
+    }
+  }
+  if (exchange) combine_r3(h, &Shard::z3, 3 * (int64_t)r3m, st);
+  const int64_t mp = ceil_div(m, h->world);
+  for (Shard& s : h->shards) {
+    if (s.mloc() == 0) continue;
+    GemvT g{};
+    g.nbatch = 3;
+    g.sum_batch = true;
+    g.conj_out = cj;
+    int64_t bytes = 16 * s.mloc(), fl = 0;
+    cplx* zout = h->comm ? h->gather_buf.p + (int64_t)h->world * mp : y + s.cb;
+    for (int c = 0; c < 3; ++c) {
+      g.A[c] = s.G4[c].p;
+      g.x[c] = s.z3.p + c * r3m;
+      g.y[c] = zout;
+      g.R[c] = R(c, 2);
+      g.C[c] = s.mloc();
+      bytes += 16 * (R(c, 2) * s.mloc() + R(c, 2));
+      fl += 8 * R(c, 2) * s.mloc();
+    }
+    Scope sc(h, "adj_g4_gemv", bytes, fl, st);
+    launch_gemv_t(g, part, pcap, kMaxSplits, st);
+  }
+  if (h->comm) {
+    Scope sc(h, "nccl_allgather", 0, 0, st);
+    cplx* seg = h->gather_buf.p + (int64_t)h->world * mp;
+    const Shard& s = h->shards[0];
+    if (s.mloc() < mp) VSIE_CHECK_CUDA(cudaMemsetAsync(seg + s.mloc(), 0, (mp - s.mloc()) * sizeof(cplx), st));
+    h->comm->allgather(reinterpret_cast<const double*>(seg), reinterpret_cast<double*>(h->gather_buf.p), 2 * (size_t)mp,
+                       st);
+    for (int p = 0; p < h->world; ++p) {
+      const int64_t cb = std::min(m, mp * p), ce = std::min(m, mp * (p + 1));
+      copy2d(y + cb, m, h->gather_buf.p + (int64_t)p * mp, mp, ce - cb, 1, st);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ the apply DAG
 void apply_dag(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int nrhs, const Streams& S) {
   if (nrhs == 1 && mega_ready(h)) {
     apply_mega(h, x, y, op, S.main);
+    return;
+  }
+  if (nrhs == 1 && h->apply_mode == 2) {
+    apply_batched(h, x, y, op, S.main);
     return;
   }
   Ctx X;

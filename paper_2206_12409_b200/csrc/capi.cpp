@@ -341,12 +341,13 @@ int32_t vsie_coupling_timers(vsie_coupling_t h, vsie_timer* out, int32_t max, in
   });
 }
 
-int32_t vsie_coupling_configure(vsie_coupling_t h, int32_t use_graphs, int32_t use_persistent) {
+int32_t vsie_coupling_configure(vsie_coupling_t h, int32_t use_graphs, int32_t mode) {
   return guarded([&] {
     VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "handle is NULL");
     VSIE_CHECK_CUDA(cudaDeviceSynchronize());
     if (use_graphs >= 0) h->use_graphs = use_graphs != 0;
-    if (use_persistent >= 0) h->use_mega = use_persistent != 0;
+    VSIE_REQUIRE(mode <= 2, VSIE_ERR_ARG, "mode must be 0 (chains), 1 (persistent) or 2 (batched)");
+    if (mode >= 0) h->apply_mode = mode;
     apply_reset_graphs(h);
     return VSIE_OK;
   });

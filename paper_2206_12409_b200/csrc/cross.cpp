@@ -89,7 +89,10 @@ const int2* schedule(Ctx& c, int Q) {
 }
 
 // Orthogonalises the columns of A (p x q, ld p); accumulates rotations into V (q x q) if given.
-void jacobi(Ctx& c, cplx* A, int64_t p, int q, cplx* V) {
+// small_rel: columns with norm below small_rel ||A||_F are left unrotated (numerical zeros
+// for 1e-14; for the truncated factorisations of the cross, columns 100x below the
+// truncation level delta can neither be kept nor move the kept singular values)
+void jacobi(Ctx& c, cplx* A, int64_t p, int q, cplx* V, double small_rel = 1e-14) {
   if (q <= 1) return;
   const int Q = q + (q & 1);
   const int2* sch = schedule(c, Q);
@@ -106,8 +109,7 @@ void jacobi(Ctx& c, cplx* A, int64_t p, int q, cplx* V) {
   double fro2 = 0;
   VSIE_CHECK_CUDA(cudaMemcpyAsync(&fro2, c.ws.frob.p, sizeof(double), cudaMemcpyDeviceToHost, c.st));
   sync(c);
-  // columns below 1e-14 ||A||_F are numerical zeros (never rotated)
-  const double small2 = 1e-28 * fro2;
+  const double small2 = small_rel * small_rel * fro2;
   c.ws.rotcnt.ensure(3);
   VSIE_CHECK_CUDA(cudaMemsetAsync(c.ws.rotcnt.p, 0, 3 * sizeof(unsigned), c.st));
   if (launch_jacobi_coop(A, p, p, V, q, sch, Q / 2, Q - 1, thr, small2, 40, c.ws.rotcnt.p, c.st)) {
@@ -145,6 +147,7 @@ std::vector<std::pair<double, int>> sorted_norms(Ctx& c, const cplx* A, int64_t 
 }
 
 // Truncation rule: smallest r with ||sigma[r:]||_2 <= delta ||M||_F.
+// randomized: the sketch may miss mass, so the tail is also bounded by ||M||_F^2 - head.
 int choose_rank(const std::vector<std::pair<double, int>>& s, double total2, bool randomized, double delta, int cap) {
   const int q = (int)s.size();
   std::vector<double> tail(q + 1, 0.0);
@@ -186,6 +189,10 @@ void set_identity(Ctx& c, DevBuf<cplx>& V, int q) {
   VSIE_CHECK_CUDA(cudaMemcpyAsync(V.p, I.data(), I.size() * sizeof(cplx), cudaMemcpyHostToDevice, c.st));
   sync(c);
 }
+
+// Columns (singular values) below this fraction of ||A||_F are irrelevant to the
+// truncation at delta (reading R6): 1e-2 delta, never below 1e-14.
+double trunc_small(const Ctx& c) { return std::max(1e-14, 1e-2 * c.delta); }
 
 // Gram-preconditioned one-sided Jacobi SVD of a tall A (p x q): the eigenvectors
 // V1 of G = A^H A (one-sided Jacobi on the q x q Cholesky factor of G + s I; the
@@ -235,7 +242,7 @@ void precond_jacobi(Ctx& c, cplx* A, int64_t p, int q, cplx* V) {
   cplx* V1 = w.Ra.p;
   if (!bad) {
     t0 = Clock::now();
-    jacobi(c, w.G.p, q, q, V1);  // G now holds R V1 (not needed)
+    jacobi(c, w.G.p, q, q, V1, trunc_small(c));  // G now holds R V1 (not needed)
     c.t_jsmall += secs(t0);
     t0 = Clock::now();
     zgemm1(c, kN, kN, p, q, q, A, p, V1, q, w.Atmp.p, p);
@@ -246,7 +253,7 @@ void precond_jacobi(Ctx& c, cplx* A, int64_t p, int q, cplx* V) {
   w.Rb.ensure(qq);
   set_identity(c, w.Rb, q);
   t0 = Clock::now();
-  jacobi(c, A, p, q, w.Rb.p);
+  jacobi(c, A, p, q, w.Rb.p, trunc_small(c));
   c.t_jtall += secs(t0);
   if (V) zgemm1(c, kN, kN, q, q, q, V1, q, w.Rb.p, q, V, q);
 }
@@ -683,12 +690,12 @@ int cross_chi(Ctx& c, int chi, Heldout& ho) {
       for (int k = 0; k < 5; ++k) best_r[k] = s.r[k];
       for (int k = 0; k < 4; ++k) copy_core(best[k], s.core[k], core_elems(h, s.r, k), c.st);
     }
-    // DESIGN.md reading R2: stop when every rank moved by at most max(1, 1%)
+    // DESIGN.md reading R2: stop when every rank moved by at most max(1, 5%)
     // over the sweep and the held-out error is within the acceptance bound
     bool same = true;
     for (int k = 0; k < 3; ++k) {
       const int d = std::abs(prev[k] - s.r[k + 1]);
-      if (prev[k] < 0 || d > std::max(1, s.r[k + 1] / 100)) same = false;
+      if (prev[k] < 0 || d > std::max(1, s.r[k + 1] / 20)) same = false;
     }
     if (same && e <= 10 * c.tol) break;
     prev[0] = s.r[1];

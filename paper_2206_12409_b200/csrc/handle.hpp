@@ -83,7 +83,7 @@ struct vsie_coupling_s {
   std::vector<vsie::GraphEntry> graphs;
   uint64_t graph_clock = 0;
   int use_graphs = 1;
-  int use_mega = 0;                          // single-RHS applies through the persistent kernel (opt-in)
+  int apply_mode = 0;   // single RHS: 0 per-chi kernel chains, 1 persistent kernel, 2 batched kernels
   int tile_trace = 0;
   vsie::DevBuf<vsie::cplx> gather_buf;     // allgather staging of z
   vsie::DevBuf<vsie::cplx> io_x, io_y;     // apply_host staging

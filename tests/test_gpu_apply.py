@@ -139,9 +139,10 @@ def test_tt_eval_matches_oracle(cfg1):
 
 
 @pytest.mark.parametrize("ci", [1, 2, 4])
-def test_persistent_vs_chains(ci):
-    """The persistent dataflow apply and the per-chi kernel chains compute the same
-    result (to rounding) for every op; each is bitwise reproducible run to run."""
+def test_apply_modes_agree(ci):
+    """The three single-RHS schedules (per-chi chains, persistent dataflow kernel, batched
+    kernels) compute the same result (to rounding) for every op; each is bitwise
+    reproducible run to run."""
     from paper_2206_12409_b200 import Coupling
     import torch
     cfg = synth.get_config(ci)
@@ -152,15 +153,17 @@ def test_persistent_vs_chains(ci):
     x = _cuda(synth.complex_gaussian(cfg.m, 11))
     u = _cuda(synth.complex_gaussian(3 * cfg.n_v, 12))
     out = {}
-    for persistent in (True, False):
-        h.configure(persistent=persistent)
+    for mode in ("persistent", "chains", "batched"):
+        h.configure(mode=mode)
         for op, v in (("N", x), ("T", u), ("C", u)):
             a = h.apply(v, op)
             b = h.apply(v, op)
-            assert torch.equal(a, b), (persistent, op)
-            out[(persistent, op)] = a.cpu().numpy()
+            assert torch.equal(a, b), (mode, op)
+            out[(mode, op)] = a.cpu().numpy()
     for op, v in (("N", x), ("T", u), ("C", u)):
-        assert validate.rel_l2(out[(True, op)], out[(False, op)]) <= 1e-13, op
+        for mode in ("persistent", "batched"):
+            assert validate.rel_l2(out[(mode, op)], out[("chains", op)]) <= 1e-13, (mode, op)
     if ci == 1:
         for op, v in (("N", x), ("T", u), ("C", u)):
-            assert validate.rel_l2(out[(True, op)], ttmv.apply(tts, v.cpu().numpy(), op)) <= TOL
+            for mode in ("persistent", "chains", "batched"):
+                assert validate.rel_l2(out[(mode, op)], ttmv.apply(tts, v.cpu().numpy(), op)) <= TOL

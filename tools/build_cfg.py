@@ -19,7 +19,8 @@ sweeps = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 cfg = synth.get_config(ci)
 torch.cuda.set_device(0)
 t0 = time.perf_counter()
-h = Coupling.build(grid_of(cfg), cfg.meshes(), cfg.freq, cfg.tol, nrhs_max=1, max_sweeps=sweeps)
+h = Coupling.build(grid_of(cfg), cfg.meshes(), cfg.freq, cfg.tol, nrhs_max=1, max_sweeps=sweeps,
+                   verbose=int(os.environ.get("VSIE_VERBOSE", "0")))
 build_s = time.perf_counter() - t0
 inf = h.info()
 print("built", ci, "status", h.status, "in", round(build_s, 2), "s; ranks", inf["ranks"], "heldout", inf["heldout_err"],

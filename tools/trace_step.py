@@ -63,16 +63,16 @@ for _ in range(5):
 torch.cuda.synchronize()
 med, mean = timed(steps)
 med_nf, _ = timed(steps, flush_l2=False)
-for persistent in (True, False):
-    h.configure(persistent=persistent)
+for mode in ("persistent", "batched", "chains"):
+    h.configure(mode=mode)
     for _ in range(3):
         step()
     torch.cuda.synchronize()
     a = timed_stream(steps, True)
     b = timed_stream(steps, False)
-    print(json.dumps(dict(persistent=persistent, stream_flush_ms=a, stream_noflush_ms=b,
+    print(json.dumps(dict(mode=mode, stream_flush_ms=a, stream_noflush_ms=b,
                           gbs_flush=B / (a[1] * 1e-3) / 1e9, gbs_noflush=B / (b[1] * 1e-3) / 1e9)))
-h.configure(persistent=False)
+h.configure(mode=os.environ.get('VSIE_MODE', 'chains'))
 print(json.dumps(dict(cfg=ci, ranks=ranks, graph_ms_median=med, graph_ms_mean=mean, gbs=B / (mean * 1e-3) / 1e9,
                       graph_ms_median_noflush=med_nf, bytes_per_step=B)))
 # serialised per-kernel
