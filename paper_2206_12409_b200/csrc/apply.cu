@@ -326,8 +326,19 @@ void combine_r3(vsie_coupling_s* h, DevBuf<cplx> Shard::*buf, int64_t n, cudaStr
 // ------------------------------------------------------------------ fork / join
 void ensure_streams(vsie_coupling_s* h) {
   if (h->chi_stream[0]) return;
+  // chain chi gets stream priority rank chi (0 highest): the block scheduler then runs
+  // chain 0 at full width and lets chains 1, 2 fill its ramp / tail / dependency bubbles
+  int least = 0, greatest = 0;
+  VSIE_CHECK_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  static const int prio_on = [] {
+    const char* e = std::getenv("VSIE_CHAIN_PRIORITY");
+    return e ? std::atoi(e) : 1;
+  }();
   for (int c = 0; c < 3; ++c) {
-    VSIE_CHECK_CUDA(cudaStreamCreateWithFlags(&h->chi_stream[c], cudaStreamNonBlocking));
+    int prio = greatest + c;
+    if (prio > least) prio = least;
+    if (!prio_on) prio = least;
+    VSIE_CHECK_CUDA(cudaStreamCreateWithPriority(&h->chi_stream[c], cudaStreamNonBlocking, prio));
     VSIE_CHECK_CUDA(cudaEventCreateWithFlags(&h->ev_join[c], cudaEventDisableTiming));
   }
   VSIE_CHECK_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));

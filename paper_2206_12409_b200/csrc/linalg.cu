@@ -368,7 +368,9 @@ void launch_zgemm_dmma(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t 
   const bool unit = g.alpha.x == 1.0 && g.alpha.y == 0.0 && g.beta.x == 0.0 && g.beta.y == 0.0;
   int splits = 1;
   if (ws != nullptr && tiles < 40) {
-    splits = (int)std::min<int64_t>(std::min<int64_t>(ceil_div(100, tiles), std::max<int64_t>(1, chunks / 2)), 64);
+    // few output tiles (the transpose G2 step: M = r2, N = n3): split K so that about two
+    // CTAs per SM run, each on >= 2 chunks of 16
+    splits = (int)std::min<int64_t>(std::min<int64_t>(ceil_div(2 * 148, tiles), std::max<int64_t>(1, chunks / 2)), 64);
     while (splits > 1 && (int64_t)splits * mn * g.nbatch > ws_elems) --splits;
     splits = std::max(splits, 1);
   }

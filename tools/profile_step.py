@@ -13,6 +13,7 @@ cfg = synth.get_config(ci)
 p = os.path.join(ROOT, "profiles", f"ranks_cfg{ci}.json")
 ranks = json.load(open(p))["ranks"] if os.path.exists(p) else [cfg.ranks_probe] * 3
 h = Coupling.from_cores(grid_of(cfg), cfg.meshes(), cfg.freq, rand_tts(cfg, ranks, 1), nrhs_max=1)
+h.configure(mode=os.environ.get("VSIE_MODE", "chains"))
 x = torch.from_numpy(synth.complex_gaussian(cfg.m, 1)).cuda()
 u = torch.from_numpy(synth.complex_gaussian(3 * cfg.n_v, 2)).cuda()
 y = torch.empty(3 * cfg.n_v, dtype=torch.complex128, device="cuda")
