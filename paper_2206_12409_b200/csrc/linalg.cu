@@ -133,13 +133,27 @@ __global__ void __launch_bounds__(NT) k_zgemm(Zgemm g, int splits, cplx* __restr
     }
 }
 
+// C = alpha sum_q ws[q] + beta C over the split-K partials: 8 partial loads in flight per
+// thread, summed in a fixed order (deterministic)
 __global__ void k_splitk_reduce(Zgemm g, int splits, const cplx* __restrict__ ws, int64_t ws_stride) {
   const int b = blockIdx.y;
   const int64_t M = g.M[b], N = g.N[b];
   const bool has_beta = g.beta.x != 0.0 || g.beta.y != 0.0;
+  const cplx* __restrict__ base = ws + (int64_t)b * splits * ws_stride;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M * N; e += (int64_t)gridDim.x * blockDim.x) {
-    cplx s = cmk(0, 0);
-    for (int q = 0; q < splits; ++q) s = cadd(s, ws[((int64_t)b * splits + q) * ws_stride + e]);
+    cplx acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = cmk(0, 0);
+    int q = 0;
+    for (; q + 8 <= splits; q += 8) {
+      cplx v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __ldcg(base + (int64_t)(q + j) * ws_stride + e);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = cadd(acc[j], v[j]);
+    }
+    for (int j = 0; q < splits; ++q, ++j) acc[j] = cadd(acc[j], __ldcg(base + (int64_t)q * ws_stride + e));
+    cplx s = cadd(cadd(cadd(acc[0], acc[1]), cadd(acc[2], acc[3])), cadd(cadd(acc[4], acc[5]), cadd(acc[6], acc[7])));
     const int64_t m = e % M, n = e / M;
     cplx* c = g.C[b] + m + g.ldc[b] * n;
     cplx v = cmul(g.alpha, s);
