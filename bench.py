@@ -408,10 +408,23 @@ def main():
                 "share_of_step": dom["total_ms"] / max(1e-9, sum(t["total_ms"] for t in timers)),
                 "bytes_per_launch": dom["bytes_per_launch"], "avg_us": avg_ms * 1e3,
                 "step_frac": value / peak}
+        if k > 1 and dom.get("flops_per_launch"):
+            # block RHS: the contractions are dense complex GEMMs on the FP64 tensor cores
+            # (AI ~ 15 flop/B); peak = the DMMA rate measured on this pool
+            # (tools/microbench/fp64_peaks.cu -> profiles/r01/fp64_peaks.json)
+            with open(os.path.join(ROOT, "profiles", "r01", "fp64_peaks.json")) as f:
+                dmma = float(json.load(f)["dmma_f64_tflops"])
+            tf = dom["flops_per_launch"] / (avg_ms * 1e-3) / 1e12
+            roof.update({"bound": "tensor", "achieved": tf, "peak": dmma, "unit": "TFLOP/s", "frac": tf / dmma,
+                         "peak_source": "measured FP64 DMMA (profiles/r01/fp64_peaks.json)",
+                         "flops_per_launch": dom["flops_per_launch"],
+                         "step_frac": F / (ms * 1e-3) / 1e12 / dmma})
     kern_table = {t["name"]: {"avg_us": 1e3 * t["total_ms"] / max(1, t["launches"]),
                               "launches_per_step": t["launches"] / max(1, args.steps),
                               "gbs": (t["bytes_per_launch"] / (t["total_ms"] / t["launches"] * 1e-3) / 1e9)
-                              if t["bytes_per_launch"] else None} for t in timers}
+                              if t["bytes_per_launch"] else None,
+                              "tflops": (t["flops_per_launch"] / (t["total_ms"] / t["launches"] * 1e-3) / 1e12)
+                              if t.get("flops_per_launch") else None} for t in timers}
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         t_cpu, ts = oracle_step_rate(cfg, ranks, steps=1 if cfg.n_v > 5e6 else 2)

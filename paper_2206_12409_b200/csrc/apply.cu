@@ -131,7 +131,7 @@ void fwd_g4(const Ctx& X, Shard& s, int c, const cplx* x, cudaStream_t st) {
     z.C[0] = y4; z.ldc[0] = X.R(c, 2);
     const int64_t bytes = 16 * (X.R(c, 2) * s.mloc() + (s.mloc() + X.R(c, 2)) * k);
     Scope sc(h, "fwd_g4_zgemm", bytes, 8 * X.R(c, 2) * s.mloc() * k, st);
-    launch_zgemm(z, X.zws(c), h->zgemm_ws_per_chi, st);
+    launch_zgemm_dmma(z, X.zws(c), h->zgemm_ws_per_chi, st);
   }
 }
 
@@ -166,7 +166,7 @@ void fwd_rest(const Ctx& X, Shard& s, int c, cplx* y, cudaStream_t st) {
     z.C[0] = Y3; z.ldc[0] = r2 * n3l;
     const int64_t bytes = 16 * (r2 * n3l * r3 + (r2 * n3l + r3) * k);
     Scope sc(h, "fwd_g3_zgemm", bytes, 8 * r2 * n3l * r3 * k, st);
-    launch_zgemm(z, X.zws(c), h->zgemm_ws_per_chi, st);
+    launch_zgemm_dmma(z, X.zws(c), h->zgemm_ws_per_chi, st);
   }
   {
     Zgemm z{};
@@ -260,7 +260,7 @@ void adj_front(const Ctx& X, Shard& s, int c, const cplx* u, bool cj, cudaStream
     z.C[0] = z3; z.ldc[0] = r3;
     const int64_t bytes = 16 * (r2 * n3l * r3 + (r2 * n3l + r3) * k);
     Scope sc(h, "adj_g3_zgemm", bytes, 8 * r2 * n3l * r3 * k, st);
-    launch_zgemm(z, X.zws(c), h->zgemm_ws_per_chi, st);
+    launch_zgemm_dmma(z, X.zws(c), h->zgemm_ws_per_chi, st);
   }
 }
 
@@ -295,7 +295,7 @@ void adj_g4(const Ctx& X, Shard& s, int c, cudaStream_t st) {
     z.C[0] = zp; z.ldc[0] = ldz;
     const int64_t bytes = 16 * (r3 * ml + (r3 + ml) * k);
     Scope sc(h, "adj_g4_zgemm", bytes, 8 * r3 * ml * k, st);
-    launch_zgemm(z, X.zws(c), h->zgemm_ws_per_chi, st);
+    launch_zgemm_dmma(z, X.zws(c), h->zgemm_ws_per_chi, st);
   }
 }
 

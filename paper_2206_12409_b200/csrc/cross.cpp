@@ -190,9 +190,10 @@ void set_identity(Ctx& c, DevBuf<cplx>& V, int q) {
   sync(c);
 }
 
-// Columns (singular values) below this fraction of ||A||_F are irrelevant to the
-// truncation at delta (reading R6): 1e-2 delta, never below 1e-14.
-double trunc_small(const Ctx& c) { return std::max(1e-14, 1e-2 * c.delta); }
+// Columns below this fraction of ||A||_F are numerical zeros of the Jacobi SVDs.  (A
+// truncation-relative threshold, 1e-2 delta, was tried in round 1 and left the sketch
+// bases non-orthogonal -- held-out errors of 2e-3 at cfg 3 -- so it is 1e-14 again.)
+double trunc_small(const Ctx&) { return 1e-14; }
 
 // Gram-preconditioned one-sided Jacobi SVD of a tall A (p x q): the eigenvectors
 // V1 of G = A^H A (one-sided Jacobi on the q x q Cholesky factor of G + s I; the

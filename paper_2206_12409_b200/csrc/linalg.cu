@@ -381,10 +381,10 @@ void launch_zgemm_dmma(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t 
   const int64_t chunks = ceil_div(kmax, tc::GKC);
   const bool unit = g.alpha.x == 1.0 && g.alpha.y == 0.0 && g.beta.x == 0.0 && g.beta.y == 0.0;
   int splits = 1;
-  if (ws != nullptr && tiles < 40) {
-    // few output tiles (the transpose G2 step: M = r2, N = n3): split K so that about two
-    // CTAs per SM run, each on >= 2 chunks of 16
-    splits = (int)std::min<int64_t>(std::min<int64_t>(ceil_div(2 * 148, tiles), std::max<int64_t>(1, chunks / 2)), 64);
+  if (ws != nullptr && tiles < 2 * 148) {
+    // few output tiles with a long K (the transpose G2 step, the block-RHS G4 / G3^T
+    // products): split K towards two CTAs per SM, each on >= 8 chunks of 16
+    splits = (int)std::min<int64_t>(std::min<int64_t>(ceil_div(2 * 148, tiles), std::max<int64_t>(1, chunks / 8)), 64);
     while (splits > 1 && (int64_t)splits * mn * g.nbatch > ws_elems) --splits;
     splits = std::max(splits, 1);
   }
