@@ -136,7 +136,7 @@ void fwd_g4(const Ctx& X, Shard& s, int c, const cplx* x, cudaStream_t st) {
 }
 
 // steps 2-4 on the owned planes: Y3 = G3 y4, Y2 = G2 Y3, y = G1 Y2
-void fwd_rest(const Ctx& X, Shard& s, int c, cplx* y, cudaStream_t st) {
+void fwd_rest(const Ctx& X, Shard& s, int c, cplx* y, cudaStream_t st, cudaEvent_t mid = nullptr) {
   vsie_coupling_s* h = X.h;
   const int k = X.k;
   const int n1 = h->grid.n[0], n2 = h->grid.n[1];
@@ -168,6 +168,7 @@ void fwd_rest(const Ctx& X, Shard& s, int c, cplx* y, cudaStream_t st) {
     Scope sc(h, "fwd_g3_zgemm", bytes, 8 * r2 * n3l * r3 * k, st);
     launch_zgemm_dmma(z, X.zws(c), h->zgemm_ws_per_chi, st);
   }
+  if (mid) VSIE_CHECK_CUDA(cudaEventRecord(mid, st));   // chain staggering: G3 stream done
   {
     Zgemm z{};
     z.nbatch = 1;
@@ -198,7 +199,7 @@ void fwd_rest(const Ctx& X, Shard& s, int c, cplx* y, cudaStream_t st) {
 
 // ------------------------------------------------------------------ transpose chain pieces (one chi)
 // W1 = G1^T u, W2 = G2^T W1, z3 = G3^T W2: partial z3 per shard
-void adj_front(const Ctx& X, Shard& s, int c, const cplx* u, bool cj, cudaStream_t st) {
+void adj_front(const Ctx& X, Shard& s, int c, const cplx* u, bool cj, cudaStream_t st, cudaEvent_t mid = nullptr) {
   vsie_coupling_s* h = X.h;
   const int k = X.k;
   const int n1 = h->grid.n[0], n2 = h->grid.n[1];
@@ -239,6 +240,7 @@ void adj_front(const Ctx& X, Shard& s, int c, const cplx* u, bool cj, cudaStream
     Scope sc(h, "adj_g2_zgemm", bytes, 8 * r1 * n2 * r2 * n3l * k, st);
     launch_zgemm_dmma(z, X.zws(c), h->zgemm_ws_per_chi, st);
   }
+  if (mid) VSIE_CHECK_CUDA(cudaEventRecord(mid, st));   // chain staggering: G1/G2 steps done
   if (k == 1) {
     GemvT g{};
     g.nbatch = 1;
@@ -323,6 +325,15 @@ void combine_r3(vsie_coupling_s* h, DevBuf<cplx> Shard::*buf, int64_t n, cudaStr
     VSIE_CHECK_CUDA(cudaMemcpyAsync((h->shards[s].*buf).p, acc, n * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
 }
 
+bool stagger_on() {
+  // measured at cfg 2: staggered chains 0.29 ms vs 0.20 ms concurrent -- off by default
+  static const int v = [] {
+    const char* e = std::getenv("VSIE_STAGGER");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v != 0;
+}
+
 // ------------------------------------------------------------------ fork / join
 void ensure_streams(vsie_coupling_s* h) {
   if (h->chi_stream[0]) return;
@@ -342,6 +353,7 @@ void ensure_streams(vsie_coupling_s* h) {
     VSIE_CHECK_CUDA(cudaEventCreateWithFlags(&h->ev_join[c], cudaEventDisableTiming));
   }
   VSIE_CHECK_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+  for (int c = 0; c < 3; ++c) VSIE_CHECK_CUDA(cudaEventCreateWithFlags(&h->ev_stage[c], cudaEventDisableTiming));
   VSIE_CHECK_CUDA(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
 }
 
@@ -416,9 +428,13 @@ void apply_mega(vsie_coupling_s* h, const cplx* x, cplx* y, int op, cudaStream_t
   const bool exchange = h->comm != nullptr || h->shards.size() > 1;
   int r3m = 1;
   for (int c = 0; c < 3; ++c) r3m = std::max(r3m, h->ranks[c][2]);
+  static const int dbg_pe = [] {   // diagnostics: run only phases [0, VSIE_MEGA_PHASE_END)
+    const char* e = std::getenv("VSIE_MEGA_PHASE_END");
+    return e ? std::atoi(e) : kMegaPhases;
+  }();
   if (op == VSIE_OP_N) {
     if (!exchange) {
-      mega_launch(h, h->shards[0], x, y, true, 0, 0, kMegaPhases, L, st);
+      mega_launch(h, h->shards[0], x, y, true, 0, 0, dbg_pe, L, st);
       return;
     }
     for (Shard& s : h->shards) mega_launch(h, s, x, y, true, 0, 0, 1, L, st);
@@ -432,7 +448,7 @@ void apply_mega(vsie_coupling_s* h, const cplx* x, cplx* y, int op, cudaStream_t
     return h->comm ? h->gather_buf.p + (int64_t)h->world * mp : y + s.cb;
   };
   if (!exchange) {
-    mega_launch(h, h->shards[0], x, out_of(h->shards[0]), false, cj, 0, kMegaPhases, L, st);
+    mega_launch(h, h->shards[0], x, out_of(h->shards[0]), false, cj, 0, dbg_pe, L, st);
     return;
   }
   for (Shard& s : h->shards) mega_launch(h, s, x, out_of(s), false, cj, 0, kMegaPhases - 1, L, st);
@@ -671,6 +687,19 @@ void apply_dag(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int nrhs, con
   const bool exchange = h->comm != nullptr || h->shards.size() > 1;
   fork(h, S);
   if (op == VSIE_OP_N) {
+    if (!exchange && stagger_on() && S.parallel) {
+      // staggered chains: chain c+1 starts streaming G4 when chain c has finished its G3
+      // stream, so one chain's tensor-core G2 / G1 steps overlap the next chain's HBM streams
+      for (int c = 0; c < 3; ++c) {
+        h->scope_chi = c;
+        if (c > 0) VSIE_CHECK_CUDA(cudaStreamWaitEvent(S.chi[c], h->ev_stage[c - 1], 0));
+        fwd_g4(X, h->shards[0], c, x, S.chi[c]);
+        fwd_rest(X, h->shards[0], c, y, S.chi[c], h->ev_stage[c]);
+      }
+      h->scope_chi = -1;
+      join(h, S);
+      return;
+    }
     for (int c = 0; c < 3; ++c) {
       h->scope_chi = c;
       for (Shard& s : h->shards) fwd_g4(X, s, c, x, S.chi[c]);
@@ -691,9 +720,11 @@ void apply_dag(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int nrhs, con
     return;
   }
   const bool cj = op == VSIE_OP_C;
+  const bool stag = !exchange && stagger_on() && S.parallel;
   for (int c = 0; c < 3; ++c) {
     h->scope_chi = c;
-    for (Shard& s : h->shards) adj_front(X, s, c, x, cj, S.chi[c]);
+    if (stag && c > 0) VSIE_CHECK_CUDA(cudaStreamWaitEvent(S.chi[c], h->ev_stage[c - 1], 0));
+    for (Shard& s : h->shards) adj_front(X, s, c, x, cj, S.chi[c], stag ? h->ev_stage[c] : nullptr);
   }
   h->scope_chi = -1;
   if (exchange) {
@@ -764,6 +795,8 @@ void apply_destroy(vsie_coupling_s* h) {
     if (h->ev_join[c]) cudaEventDestroy(h->ev_join[c]);
   }
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  for (int c = 0; c < 3; ++c)
+    if (h->ev_stage[c]) cudaEventDestroy(h->ev_stage[c]);
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
 }
 

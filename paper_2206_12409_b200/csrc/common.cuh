@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <string>
 #include <stdexcept>
+#include <utility>
 #include <vector>
 
 #include "../../include/vsie_coupling.h"
@@ -102,5 +103,31 @@ struct TimerSlot {
   double total_ms = 0;
   int64_t bytes = 0, flops = 0;
 };
+
+// ----------------------------------------------------------------- programmatic dependent launch
+// Kernels of the apply path call pdl_wait() before touching anything their stream
+// predecessor wrote and pdl_trigger() once their main loop is done; launched through
+// launch_pdl (programmatic stream serialization) the next kernel of a chain is scheduled
+// onto SMs while this one drains instead of after it has fully retired.  Both are no-ops
+// for ordinary launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  VSIE_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 
 }  // namespace vsie

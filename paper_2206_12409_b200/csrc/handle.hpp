@@ -80,6 +80,7 @@ struct vsie_coupling_s {
   cudaStream_t chi_stream[3] = {nullptr, nullptr, nullptr};
   cudaStream_t cap_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev_stage[3] = {nullptr, nullptr, nullptr};   // chain staggering
   std::vector<vsie::GraphEntry> graphs;
   uint64_t graph_clock = 0;
   int use_graphs = 1;

@@ -10,8 +10,17 @@
 #include "dmma_tile.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace vsie {
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("VSIE_PDL");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return on;
+}
 
 int64_t& launch_counter() {
   static thread_local int64_t n = 0;
@@ -136,6 +145,7 @@ __global__ void __launch_bounds__(NT) k_zgemm(Zgemm g, int splits, cplx* __restr
 // C = alpha sum_q ws[q] + beta C over the split-K partials: 8 partial loads in flight per
 // thread, summed in a fixed order (deterministic)
 __global__ void k_splitk_reduce(Zgemm g, int splits, const cplx* __restrict__ ws, int64_t ws_stride) {
+  pdl_wait();
   const int b = blockIdx.y;
   const int64_t M = g.M[b], N = g.N[b];
   const bool has_beta = g.beta.x != 0.0 || g.beta.y != 0.0;
@@ -296,6 +306,7 @@ __global__ void __launch_bounds__(tc::kThreads) k_zgemm_tc(const __grid_constant
   extern __shared__ __align__(16) unsigned char raw[];
   tc::GemmSmem& sm = *reinterpret_cast<tc::GemmSmem*>(raw);
   constexpr int TM = 16 * WA, TN = 16 * WB;
+  pdl_wait();
   const int b = blockIdx.y;
   if (b >= g.nbatch) return;
   const int64_t tiles = mt * nt;
@@ -317,6 +328,7 @@ __global__ void __launch_bounds__(tc::kThreads) k_zgemm_tc(const __grid_constant
     ldc = M;
   }
   tc::gemm_tile<WA, WB, TA>(g.A[b], g.lda[b], g.B[b], g.ldb[b], M, N, m0, n0, k0, k1, sm, C, ldc);
+  pdl_trigger();
 }
 
 template <int TA, int TB>
@@ -402,16 +414,18 @@ void launch_zgemm_dmma(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t 
   }
   dim3 grid((unsigned)(mt * nt * splits), (unsigned)g.nbatch);
   const bool ta = g.ta == kT;
-  if (tall)
-    ta ? k_zgemm_tc<tc::FWA, tc::FWB, true><<<grid, tc::kThreads, smem, st>>>(g, splits, mt, nt, ws, mn, direct)
-       : k_zgemm_tc<tc::FWA, tc::FWB, false><<<grid, tc::kThreads, smem, st>>>(g, splits, mt, nt, ws, mn, direct);
-  else
-    ta ? k_zgemm_tc<tc::AWA, tc::AWB, true><<<grid, tc::kThreads, smem, st>>>(g, splits, mt, nt, ws, mn, direct)
-       : k_zgemm_tc<tc::AWA, tc::AWB, false><<<grid, tc::kThreads, smem, st>>>(g, splits, mt, nt, ws, mn, direct);
+  const dim3 blk(tc::kThreads);
+  if (tall) {
+    if (ta) launch_pdl(k_zgemm_tc<tc::FWA, tc::FWB, true>, grid, blk, smem, st, g, splits, mt, nt, ws, mn, direct);
+    else launch_pdl(k_zgemm_tc<tc::FWA, tc::FWB, false>, grid, blk, smem, st, g, splits, mt, nt, ws, mn, direct);
+  } else {
+    if (ta) launch_pdl(k_zgemm_tc<tc::AWA, tc::AWB, true>, grid, blk, smem, st, g, splits, mt, nt, ws, mn, direct);
+    else launch_pdl(k_zgemm_tc<tc::AWA, tc::AWB, false>, grid, blk, smem, st, g, splits, mt, nt, ws, mn, direct);
+  }
   VSIE_CHECK_LAUNCH();
   if (!direct) {
     dim3 rg((unsigned)std::min<int64_t>(ceil_div(mn, 256), 148 * 8), g.nbatch);
-    k_splitk_reduce<<<rg, 256, 0, st>>>(g, splits, ws, mn);
+    launch_pdl(k_splitk_reduce, rg, dim3(256), 0, st, g, splits, (const cplx*)ws, mn);
     VSIE_CHECK_LAUNCH();
   }
 }

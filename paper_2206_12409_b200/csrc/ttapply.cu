@@ -45,6 +45,7 @@ __device__ __forceinline__ cplx ld_stream(const cplx* p) {
 template <int U>
 __global__ void __launch_bounds__(512) k_gemv_n(const __grid_constant__ GemvN a, cplx* __restrict__ partials,
                                                 int64_t rmax) {
+  pdl_wait();
   const int b = blockIdx.z;
   const int64_t R = a.R[b], C = a.C[b];
   const int64_t row = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
@@ -89,6 +90,7 @@ __global__ void __launch_bounds__(512) k_gemv_n(const __grid_constant__ GemvN a,
     }
   }
   for (; c < c1; ++c) cfma(acc, __ldcs(p + R * c), __ldg(X + c));
+  pdl_trigger();
   acc = cadd(acc, acc2);
   if (!act) return;
   if (nsplit == 1)
@@ -108,6 +110,7 @@ struct SumArgs {
 __global__ void __launch_bounds__(kThreads) k_sum_partials_warp(const __grid_constant__ SumArgs a,
                                                                 const cplx* __restrict__ partials, int nsplit,
                                                                 int64_t stride) {
+  pdl_wait();
   const int b = blockIdx.y;
   const int64_t r = blockIdx.x * (int64_t)(kThreads / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -133,6 +136,7 @@ __global__ void __launch_bounds__(kThreads) k_sum_partials_warp(const __grid_con
 __global__ void __launch_bounds__(kThreads) k_sum_partials(const __grid_constant__ SumArgs a,
                                                            const cplx* __restrict__ partials, int nsplit,
                                                            int64_t stride) {
+  pdl_wait();
   const int b = blockIdx.y;
   const int64_t r = blockIdx.x * (int64_t)kThreads + threadIdx.x;
   if (r >= a.n[b]) return;
@@ -168,6 +172,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 // batches share the output columns (Eq. 18 sum over chi inside the kernel).
 __global__ void __launch_bounds__(kThreads) k_gemv_t(const __grid_constant__ GemvT a, cplx* __restrict__ partials,
                                                      int64_t cmax) {
+  pdl_wait();
   const bool conj_out = a.conj_out;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ct = blockIdx.x;
@@ -233,6 +238,7 @@ __global__ void __launch_bounds__(kThreads) k_gemv_t(const __grid_constant__ Gem
       for (int j = 0; j < kCPW; ++j) cfma(acc[j], __ldcs(col[j] + r), xv);
     }
   }
+  pdl_trigger();
 #pragma unroll
   for (int j = 0; j < kCPW; ++j) {
     acc[j].x = warp_sum(acc[j].x);
@@ -290,6 +296,7 @@ __device__ __forceinline__ void zmma(double (&cr)[2], double (&ci)[2], cplx a, c
 // 8 x 8 output tile is stored as 4 whole 128-B lines per warp instruction.
 template <int KT>
 __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant__ ExpandArgs a) {
+  pdl_wait();
   const int b = blockIdx.y;
   const int n1 = a.n1, r1 = a.r1[b];
   const int mt = (n1 + 7) / 8;
@@ -351,6 +358,7 @@ __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant_
 // lane 16 B, 64 contiguous bytes per column), G1 fragments from shared memory.
 template <int NT>
 __global__ void __launch_bounds__(kG1Threads) k_reduce_g1(const __grid_constant__ ReduceArgs a) {
+  pdl_wait();
   const int b = blockIdx.y;
   const int n1 = a.n1, r1 = a.r1[b];
   const int ks_n = (n1 + 3) / 4;
@@ -423,6 +431,7 @@ __global__ void __launch_bounds__(kG1Threads) k_reduce_g1(const __grid_constant_
 __global__ void __launch_bounds__(kThreads) k_sum3(const cplx* __restrict__ in, int64_t chi_stride, int64_t ld_in,
                                                    int64_t rows, int k, cplx* __restrict__ out, int64_t ld_out,
                                                    bool conj_out) {
+  pdl_wait();
   const int64_t n = rows * k;
   for (int64_t e = blockIdx.x * (int64_t)kThreads + threadIdx.x; e < n; e += (int64_t)gridDim.x * kThreads) {
     const int64_t j = e / rows, i = e - j * rows;
@@ -470,13 +479,17 @@ void launch_gemv_n(const GemvN& a, cplx* partials, int64_t partials_cap, int max
     cmax = std::max(cmax, a.C[b]);
   }
   if (rmax == 0) return;
-  constexpr int U = 4;
+  static const int u_sel = [] {
+    const char* e = std::getenv("VSIE_GEMV_U");
+    return e ? std::atoi(e) : 4;
+  }();
+  const void* fn = u_sel == 2 ? (const void*)k_gemv_n<2> : (u_sel == 8 ? (const void*)k_gemv_n<8> : (const void*)k_gemv_n<4>);
   // one row tile when R <= 320 (block = R rounded to a warp), else 256-row tiles
   const int T = rmax <= 320 ? (int)(ceil_div(rmax, 32) * 32) : 256;
   const int64_t rtiles = ceil_div(rmax, T);
   // column splits: fill whole waves of resident CTAs (2 waves when a split keeps >= 24
   // columns, else 1) -- a partial last wave is a straggler tail for the whole kernel
-  const int64_t slots = (int64_t)sm_count() * gemv_occupancy((const void*)k_gemv_n<U>, T);
+  const int64_t slots = (int64_t)sm_count() * gemv_occupancy(fn, T);
   const int64_t per = rtiles * a.nbatch;
   int64_t nsl = std::max<int64_t>(1, 2 * slots / per);
   if (cmax / nsl < 24) nsl = std::max<int64_t>(1, slots / per);
@@ -484,7 +497,12 @@ void launch_gemv_n(const GemvN& a, cplx* partials, int64_t partials_cap, int max
   int ns = (int)std::min<int64_t>(nsl, max_splits);
   while (ns > 1 && (int64_t)a.nbatch * ns * rmax > partials_cap) --ns;
   dim3 grid(ns, (unsigned)rtiles, a.nbatch);
-  k_gemv_n<U><<<grid, T, 0, st>>>(a, partials, rmax);
+  if (u_sel == 2)
+    launch_pdl(k_gemv_n<2>, grid, dim3(T), 0, st, a, partials, rmax);
+  else if (u_sel == 8)
+    launch_pdl(k_gemv_n<8>, grid, dim3(T), 0, st, a, partials, rmax);
+  else
+    launch_pdl(k_gemv_n<4>, grid, dim3(T), 0, st, a, partials, rmax);
   VSIE_CHECK_LAUNCH();
   if (ns > 1) {
     SumArgs sa{};
@@ -495,10 +513,10 @@ void launch_gemv_n(const GemvN& a, cplx* partials, int64_t partials_cap, int max
     }
     if (ns >= 16) {
       dim3 g2((unsigned)ceil_div(rmax, kThreads / 32), a.nbatch);
-      k_sum_partials_warp<<<g2, kThreads, 0, st>>>(sa, partials, ns, rmax);
+      launch_pdl(k_sum_partials_warp, g2, dim3(kThreads), 0, st, sa, (const cplx*)partials, ns, rmax);
     } else {
       dim3 g2((unsigned)ceil_div(rmax, kThreads), a.nbatch);
-      k_sum_partials<<<g2, kThreads, 0, st>>>(sa, partials, ns, rmax);
+      launch_pdl(k_sum_partials, g2, dim3(kThreads), 0, st, sa, (const cplx*)partials, ns, rmax);
     }
     VSIE_CHECK_LAUNCH();
   }
@@ -508,8 +526,8 @@ void launch_sum3(const cplx* in, int64_t chi_stride, int64_t ld_in, int64_t rows
                  bool conj_out, cudaStream_t st) {
   const int64_t n = rows * k;
   if (n <= 0) return;
-  k_sum3<<<(unsigned)std::min<int64_t>(ceil_div(n, kThreads), 148 * 8), kThreads, 0, st>>>(in, chi_stride, ld_in, rows, k,
-                                                                                          out, ld_out, conj_out);
+  launch_pdl(k_sum3, dim3((unsigned)std::min<int64_t>(ceil_div(n, kThreads), 148 * 8)), dim3(kThreads), 0, st, in,
+             chi_stride, ld_in, rows, k, out, ld_out, conj_out);
   VSIE_CHECK_LAUNCH();
 }
 
@@ -527,7 +545,7 @@ void launch_gemv_t(const GemvT& a, cplx* partials, int64_t partials_cap, int max
   int ns = a.sum_batch ? 1 : pick_splits(ctiles * nz, rmax, 128, max_splits, 2 * slots);
   while (ns > 1 && (int64_t)nz * ns * cmax > partials_cap) --ns;
   dim3 grid((unsigned)ctiles, ns, nz);
-  k_gemv_t<<<grid, kThreads, 0, st>>>(a, partials, cmax);
+  launch_pdl(k_gemv_t, grid, dim3(kThreads), 0, st, a, partials, cmax);
   VSIE_CHECK_LAUNCH();
   if (ns > 1) {
     SumArgs sa{};
@@ -539,10 +557,10 @@ void launch_gemv_t(const GemvT& a, cplx* partials, int64_t partials_cap, int max
     }
     if (ns >= 16) {
       dim3 g2((unsigned)ceil_div(cmax, kThreads / 32), nz);
-      k_sum_partials_warp<<<g2, kThreads, 0, st>>>(sa, partials, ns, cmax);
+      launch_pdl(k_sum_partials_warp, g2, dim3(kThreads), 0, st, sa, (const cplx*)partials, ns, cmax);
     } else {
       dim3 g2((unsigned)ceil_div(cmax, kThreads), nz);
-      k_sum_partials<<<g2, kThreads, 0, st>>>(sa, partials, ns, cmax);
+      launch_pdl(k_sum_partials, g2, dim3(kThreads), 0, st, sa, (const cplx*)partials, ns, cmax);
     }
     VSIE_CHECK_LAUNCH();
   }
@@ -568,7 +586,7 @@ void launch_expand_g1(const ExpandArgs& a, cudaStream_t st) {
   case K: {                                                          \
     static bool d = false;                                           \
     set_smem_attr_once(k_expand_g1<K>, d);                           \
-    k_expand_g1<K><<<grid, kG1Threads, smem, st>>>(a);               \
+    launch_pdl(k_expand_g1<K>, grid, dim3(kG1Threads), smem, st, a); \
     break;                                                           \
   }
   switch (KT) {
@@ -590,7 +608,7 @@ void launch_reduce_g1(const ReduceArgs& a, cudaStream_t st) {
   case K: {                                                          \
     static bool d = false;                                           \
     set_smem_attr_once(k_reduce_g1<K>, d);                           \
-    k_reduce_g1<K><<<grid, kG1Threads, smem, st>>>(a);               \
+    launch_pdl(k_reduce_g1<K>, grid, dim3(kG1Threads), smem, st, a); \
     break;                                                           \
   }
   switch (NT) {
