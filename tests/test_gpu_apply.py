@@ -167,3 +167,21 @@ def test_apply_modes_agree(ci):
         for op, v in (("N", x), ("T", u), ("C", u)):
             for mode in ("persistent", "chains", "batched"):
                 assert validate.rel_l2(out[(mode, op)], ttmv.apply(tts, v.cpu().numpy(), op)) <= TOL
+
+
+def test_cfg3_full_grid_parity():
+    """Config 3 geometry at full size (200 x 120 x 400 voxels, m = 30000 over two
+    surfaces) with random cores: r3 > 512 exercises the 256-row-tile GEMV path, n1 = 200
+    the long G1 contractions, and every schedule is checked against the oracle (T2)."""
+    from paper_2206_12409_b200 import Coupling
+    cfg = synth.get_config(3)
+    ranks = [(16, 124, 600), (15, 120, 640), (17, 130, 580)]
+    tts = rand_tts(cfg, ranks, 303)
+    h = Coupling.from_cores(grid_of(cfg), cfg.meshes(), cfg.freq, tts, nrhs_max=1)
+    x = synth.complex_gaussian(cfg.m, 31)
+    u = synth.complex_gaussian(3 * cfg.n_v, 32)
+    ref = {op: ttmv.apply(tts, v, op) for op, v in (("N", x), ("T", u), ("C", u))}
+    for mode in ("chains", "batched", "persistent"):
+        h.configure(mode=mode)
+        for op, v in (("N", x), ("T", u), ("C", u)):
+            assert validate.rel_l2(h.apply(_cuda(v), op).cpu().numpy(), ref[op]) <= TOL, (mode, op)
