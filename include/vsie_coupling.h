@@ -179,10 +179,23 @@ int32_t vsie_coupling_export_cores(vsie_coupling_t h, int32_t chi, int32_t k, vo
 int32_t vsie_coupling_apply(vsie_coupling_t h, const void* x, void* y, int32_t op, int32_t nrhs,
                             void* stream);
 
+/* The coupling pair of one GMRES matvec of the hybrid system (Eq. 11 / 15: the
+ * body rows need Z_bc j_c, the conductor rows Z_cb j_b = Z_bc^T j_b, Eqs. 17-19):
+ * y = Z x (layouts as OP_N above) and z = Z^T u (adj_op = OP_T) or Z^H u (OP_C) (layouts
+ * as OP_T), single right-hand side, in one call.  The transpose's G1-G3 steps run first
+ * so that both directions' G4 products share one pass over the largest core.  Results
+ * equal two vsie_coupling_apply calls to rounding.  Asynchronous; collective when world > 1. */
+int32_t vsie_coupling_apply_pair(vsie_coupling_t h, const void* x, void* y, const void* u, void* z, int32_t adj_op,
+                                 void* stream);
+
 /* Same as apply but x and y are HOST buffers: H2D copy, apply, D2H copy,
  * synchronous (the end-to-end call of a CPU-resident GMRES). */
 int32_t vsie_coupling_apply_host(vsie_coupling_t h, const void* x_host, void* y_host, int32_t op,
                                  int32_t nrhs);
+
+/* apply_pair with HOST buffers (H2D of x and u, the pair, D2H of y and z; synchronous). */
+int32_t vsie_coupling_apply_pair_host(vsie_coupling_t h, const void* x_host, void* y_host, const void* u_host,
+                                      void* z_host, int32_t adj_op);
 
 /* Exact quadrature entries (the cross's black box, not the TT value):
  * idx = device int64 [count][2] (row, col), out = device complex128 [count].

@@ -208,6 +208,26 @@ class Coupling:
         check(lib().vsie_coupling_apply(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr), _lib.OPS[op], nrhs,
                                         _stream_ptr(stream)))
 
+    def apply_pair(self, x, u, adj: str = "T", out_y=None, out_z=None, stream=None):
+        """vsie_coupling_apply_pair: (Z x, Z^T u) or (Z x, Z^H u) in one call (single RHS)."""
+        torch = _torch()
+        x = x.contiguous()
+        u = u.contiguous()
+        y = out_y if out_y is not None else torch.empty(self.out_len("N"), dtype=torch.complex128, device=x.device)
+        z = out_z if out_z is not None else torch.empty(self.out_len("T"), dtype=torch.complex128, device=x.device)
+        check(lib().vsie_coupling_apply_pair(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
+                                             C.c_void_p(u.data_ptr()), C.c_void_p(z.data_ptr()), _lib.OPS[adj],
+                                             _stream_ptr(stream)))
+        return y, z
+
+    def apply_pair_raw(self, x_ptr: int, y_ptr: int, u_ptr: int, z_ptr: int, adj: str = "T", stream=None):
+        check(lib().vsie_coupling_apply_pair(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr), C.c_void_p(u_ptr),
+                                             C.c_void_p(z_ptr), _lib.OPS[adj], _stream_ptr(stream)))
+
+    def apply_pair_host_raw(self, x_ptr: int, y_ptr: int, u_ptr: int, z_ptr: int, adj: str = "T"):
+        check(lib().vsie_coupling_apply_pair_host(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr), C.c_void_p(u_ptr),
+                                                  C.c_void_p(z_ptr), _lib.OPS[adj]))
+
     def apply_host(self, x: np.ndarray, op: str = "N") -> np.ndarray:
         """vsie_coupling_apply_host: host in, host out (H2D + apply + D2H)."""
         X = np.asarray(x, dtype=np.complex128)

@@ -800,11 +800,13 @@ void apply_destroy(vsie_coupling_s* h) {
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
 }
 
-void apply(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int nrhs, cudaStream_t st) {
-  VSIE_REQUIRE(h->has_cores, VSIE_ERR_STATE, "handle has no TT cores");
-  VSIE_REQUIRE(op == VSIE_OP_N || op == VSIE_OP_T || op == VSIE_OP_C, VSIE_ERR_ARG, "bad op");
-  VSIE_REQUIRE(nrhs >= 1 && nrhs <= h->nrhs_max, VSIE_ERR_ARG, "nrhs out of range");
-  VSIE_REQUIRE(x != nullptr && y != nullptr, VSIE_ERR_ARG, "x / y is NULL");
+namespace {
+
+// Runs an apply DAG under the current timing / graph policy.  `dag(S)` enqueues the
+// work on the Streams it is given; graphs are cached by (op, nrhs, x, y, u, z).
+template <class Dag>
+void run_dag(vsie_coupling_s* h, int op, int nrhs, const void* x, void* y, const void* u, void* z, cudaStream_t st,
+             Dag&& dag) {
   ensure_streams(h);
   h->apply_calls += 1;
   if (h->timing == 2) {
@@ -816,27 +818,33 @@ void apply(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int nrhs, cudaStr
     h->trace_origin = o;
     Streams S{st, {h->chi_stream[0], h->chi_stream[1], h->chi_stream[2]}, true};
     const int64_t before = launch_counter();
-    apply_dag(h, x, y, op, nrhs, S);
+    dag(S);
     h->apply_launches += launch_counter() - before;
     h->trace_call += 1;
     return;
   }
-  if (h->timing) {
-    // per-kernel CUDA-event timing: the same DAG serialised on one stream, captured with
-    // its event records into a one-shot graph so that host submission gaps do not enter
-    // the per-kernel durations
-    Streams S{h->cap_stream, {h->cap_stream, h->cap_stream, h->cap_stream}, false};
+  auto capture = [&](const Streams& S, int64_t& launches) -> cudaGraph_t {
     const int64_t before = launch_counter();
     VSIE_CHECK_CUDA(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
     cudaGraph_t graph = nullptr;
     try {
-      apply_dag(h, x, y, op, nrhs, S);
+      dag(S);
     } catch (...) {
       cudaStreamEndCapture(h->cap_stream, &graph);
       if (graph) cudaGraphDestroy(graph);
       throw;
     }
     VSIE_CHECK_CUDA(cudaStreamEndCapture(h->cap_stream, &graph));
+    launches = launch_counter() - before;
+    return graph;
+  };
+  if (h->timing) {
+    // per-kernel CUDA-event timing: the same DAG serialised on one stream, captured with
+    // its event records into a one-shot graph so that host submission gaps do not enter
+    // the per-kernel durations
+    Streams S{h->cap_stream, {h->cap_stream, h->cap_stream, h->cap_stream}, false};
+    int64_t launches = 0;
+    cudaGraph_t graph = capture(S, launches);
     cudaGraphExec_t exec = nullptr;
     cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
@@ -844,19 +852,19 @@ void apply(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int nrhs, cudaStr
     e = cudaGraphLaunch(exec, st);
     cudaGraphExecDestroy(exec);
     VSIE_CHECK_CUDA(e);
-    h->apply_launches += launch_counter() - before;
+    h->apply_launches += launches;
     return;
   }
   if (!graphs_enabled(h)) {
     Streams S{st, {h->chi_stream[0], h->chi_stream[1], h->chi_stream[2]}, true};
     const int64_t before = launch_counter();
-    apply_dag(h, x, y, op, nrhs, S);
+    dag(S);
     h->apply_launches += launch_counter() - before;
     return;
   }
   GraphEntry* ge = nullptr;
   for (GraphEntry& g : h->graphs)
-    if (g.op == op && g.nrhs == nrhs && g.x == x && g.y == y) ge = &g;
+    if (g.op == op && g.nrhs == nrhs && g.x == x && g.y == y && g.u == u && g.z == z) ge = &g;
   if (!ge) {
     if (h->graphs.size() >= 16) {
       auto lru = std::min_element(h->graphs.begin(), h->graphs.end(),
@@ -869,19 +877,10 @@ void apply(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int nrhs, cudaStr
     g.nrhs = nrhs;
     g.x = x;
     g.y = y;
+    g.u = u;
+    g.z = z;
     Streams S{h->cap_stream, {h->chi_stream[0], h->chi_stream[1], h->chi_stream[2]}, true};
-    const int64_t before = launch_counter();
-    VSIE_CHECK_CUDA(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
-    cudaGraph_t graph = nullptr;
-    try {
-      apply_dag(h, x, y, op, nrhs, S);
-    } catch (...) {
-      cudaStreamEndCapture(h->cap_stream, &graph);
-      if (graph) cudaGraphDestroy(graph);
-      throw;
-    }
-    VSIE_CHECK_CUDA(cudaStreamEndCapture(h->cap_stream, &graph));
-    g.launches = launch_counter() - before;
+    cudaGraph_t graph = capture(S, g.launches);
     cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
     cudaGraphDestroy(graph);
     VSIE_CHECK_CUDA(e);
@@ -891,6 +890,118 @@ void apply(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int nrhs, cudaStr
   ge->last_use = ++h->graph_clock;
   VSIE_CHECK_CUDA(cudaGraphLaunch(ge->exec, st));
   h->apply_launches += ge->launches;
+}
+
+// The coupling pair of one GMRES matvec of the hybrid system (Eq. 11 / 15: the body rows
+// need Z_bc j_c, the conductor rows Z_bc^T j_b): y = Z x and z = Z^T u (Z^H u).  The
+// transpose front (G1^T, G2^T, G3^T) runs first, so that both directions' G4 products
+// share ONE stream of the largest core (k_gemv_nt); the forward finishes from y4.
+void pair_dag(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z, bool cj, const Streams& S) {
+  Ctx X;
+  X.h = h;
+  X.k = 1;
+  X.r1m = X.r2m = X.r3m = 1;
+  for (int c = 0; c < 3; ++c) {
+    X.r1m = std::max(X.r1m, h->ranks[c][0]);
+    X.r2m = std::max(X.r2m, h->ranks[c][1]);
+    X.r3m = std::max(X.r3m, h->ranks[c][2]);
+  }
+  X.r3stride = X.r3m;
+  X.L = voxel_layout(h);
+  const bool exchange = h->comm != nullptr || h->shards.size() > 1;
+  fork(h, S);
+  for (int c = 0; c < 3; ++c) {
+    h->scope_chi = c;
+    for (Shard& s : h->shards) adj_front(X, s, c, u, cj, S.chi[c]);
+  }
+  if (exchange) {
+    join(h, S);
+    combine_r3(h, &Shard::z3, 3 * X.r3stride, S.main);
+    fork(h, S);
+  }
+  for (int c = 0; c < 3; ++c) {
+    h->scope_chi = c;
+    for (Shard& s : h->shards) {
+      const int64_t ml = s.mloc();
+      const int64_t ldz = s.zpart.n / 3;   // nrhs_max columns per chi block; single RHS here
+      if (ml == 0) {
+        VSIE_CHECK_CUDA(cudaMemsetAsync(s.y4.p + c * X.r3stride, 0, X.r3stride * sizeof(cplx), S.chi[c]));
+        continue;
+      }
+      const int64_t r3 = X.R(c, 2);
+      GemvNT g{};
+      g.nbatch = 1;
+      g.A[0] = s.G4[c].p;
+      g.x[0] = x + s.cb;
+      g.z3[0] = s.z3.p + c * X.r3stride;
+      g.z[0] = s.zpart.p + c * ldz;
+      g.y4[0] = s.y4.p + c * X.r3stride;
+      g.R[0] = r3;
+      g.C[0] = ml;
+      bool fused;
+      {
+        Scope sc(h, "pair_g4_nt", 16 * (r3 * ml + 2 * ml + 2 * r3), 16 * r3 * ml, S.chi[c]);
+        fused = launch_gemv_nt(g, X.partials(c), h->partials_per_chi, S.chi[c]);
+      }
+      if (!fused) {   // r3 > 320: the two G4 products as separate passes
+        fwd_g4(X, s, c, x, S.chi[c]);
+        adj_g4(X, s, c, S.chi[c]);
+      }
+    }
+  }
+  if (exchange) {
+    join(h, S);
+    combine_r3(h, &Shard::y4, 3 * X.r3stride, S.main);
+    fork(h, S);
+  }
+  for (int c = 0; c < 3; ++c) {
+    h->scope_chi = c;
+    for (Shard& s : h->shards) fwd_rest(X, s, c, y, S.chi[c]);
+  }
+  h->scope_chi = -1;
+  join(h, S);
+  const int64_t m = h->m, mp = ceil_div(m, h->world);
+  for (Shard& s : h->shards) {
+    if (h->comm)
+      adj_sum_chi(X, s, h->gather_buf.p + (int64_t)h->world * mp, mp, cj, S.main);
+    else
+      adj_sum_chi(X, s, z + s.cb, m, cj, S.main);
+  }
+  if (h->comm) {
+    Scope sc(h, "nccl_allgather", 0, 0, S.main);
+    cplx* seg = h->gather_buf.p + (int64_t)h->world * mp;
+    const Shard& s = h->shards[0];
+    if (s.mloc() < mp) VSIE_CHECK_CUDA(cudaMemsetAsync(seg + s.mloc(), 0, (mp - s.mloc()) * sizeof(cplx), S.main));
+    h->comm->allgather(reinterpret_cast<const double*>(seg), reinterpret_cast<double*>(h->gather_buf.p), 2 * (size_t)mp,
+                       S.main);
+    for (int p = 0; p < h->world; ++p) {
+      const int64_t cb = std::min(m, mp * p), ce = std::min(m, mp * (p + 1));
+      copy2d(z + cb, m, h->gather_buf.p + (int64_t)p * mp, mp, ce - cb, 1, S.main);
+    }
+  }
+}
+
+}  // namespace
+
+void apply(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int nrhs, cudaStream_t st) {
+  VSIE_REQUIRE(h->has_cores, VSIE_ERR_STATE, "handle has no TT cores");
+  VSIE_REQUIRE(op == VSIE_OP_N || op == VSIE_OP_T || op == VSIE_OP_C, VSIE_ERR_ARG, "bad op");
+  VSIE_REQUIRE(nrhs >= 1 && nrhs <= h->nrhs_max, VSIE_ERR_ARG, "nrhs out of range");
+  VSIE_REQUIRE(x != nullptr && y != nullptr, VSIE_ERR_ARG, "x / y is NULL");
+  run_dag(h, op, nrhs, x, y, nullptr, nullptr, st, [&](const Streams& S) { apply_dag(h, x, y, op, nrhs, S); });
+}
+
+void apply_pair(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z, int adj_op, cudaStream_t st) {
+  VSIE_REQUIRE(h->has_cores, VSIE_ERR_STATE, "handle has no TT cores");
+  VSIE_REQUIRE(adj_op == VSIE_OP_T || adj_op == VSIE_OP_C, VSIE_ERR_ARG, "adj_op must be OP_T or OP_C");
+  VSIE_REQUIRE(x && y && u && z, VSIE_ERR_ARG, "x / y / u / z is NULL");
+  if (h->apply_mode != 0) {   // the fused pair is built on the chain schedule
+    apply(h, x, y, VSIE_OP_N, 1, st);
+    apply(h, u, z, adj_op, 1, st);
+    return;
+  }
+  run_dag(h, 100 + adj_op, 1, x, y, u, z, st,
+          [&](const Streams& S) { pair_dag(h, x, y, u, z, adj_op == VSIE_OP_C, S); });
 }
 
 }  // namespace vsie

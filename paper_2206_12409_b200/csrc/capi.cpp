@@ -217,6 +217,39 @@ int32_t vsie_coupling_apply_host(vsie_coupling_t h, const void* x_host, void* y_
   });
 }
 
+int32_t vsie_coupling_apply_pair(vsie_coupling_t h, const void* x, void* y, const void* u, void* z, int32_t adj_op,
+                                 void* stream) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "handle is NULL");
+    apply_pair(h, static_cast<const cplx*>(x), static_cast<cplx*>(y), static_cast<const cplx*>(u), static_cast<cplx*>(z),
+               adj_op, static_cast<cudaStream_t>(stream));
+    return VSIE_OK;
+  });
+}
+
+int32_t vsie_coupling_apply_pair_host(vsie_coupling_t h, const void* x_host, void* y_host, const void* u_host,
+                                      void* z_host, int32_t adj_op) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr && x_host && y_host && u_host && z_host, VSIE_ERR_ARG, "NULL argument");
+    const int64_t n12 = (int64_t)h->grid.n[0] * h->grid.n[1];
+    const int64_t vox = h->comm ? 3 * n12 * h->shards[0].n3loc() : 3 * h->grid.nv();
+    h->io_x.ensure(h->m + vox);
+    h->io_y.ensure(vox + h->m);
+    if (!h->io_stream) VSIE_CHECK_CUDA(cudaStreamCreateWithFlags(&h->io_stream, cudaStreamNonBlocking));
+    cplx* dx = h->io_x.p;
+    cplx* du = h->io_x.p + h->m;
+    cplx* dy = h->io_y.p;
+    cplx* dz = h->io_y.p + vox;
+    VSIE_CHECK_CUDA(cudaMemcpyAsync(dx, x_host, h->m * sizeof(cplx), cudaMemcpyHostToDevice, h->io_stream));
+    VSIE_CHECK_CUDA(cudaMemcpyAsync(du, u_host, vox * sizeof(cplx), cudaMemcpyHostToDevice, h->io_stream));
+    apply_pair(h, dx, dy, du, dz, adj_op, h->io_stream);
+    VSIE_CHECK_CUDA(cudaMemcpyAsync(y_host, dy, vox * sizeof(cplx), cudaMemcpyDeviceToHost, h->io_stream));
+    VSIE_CHECK_CUDA(cudaMemcpyAsync(z_host, dz, h->m * sizeof(cplx), cudaMemcpyDeviceToHost, h->io_stream));
+    VSIE_CHECK_CUDA(cudaStreamSynchronize(h->io_stream));
+    return VSIE_OK;
+  });
+}
+
 int32_t vsie_coupling_entries(vsie_coupling_t h, const int64_t* idx, int64_t count, void* out, void* stream) {
   return guarded([&] {
     VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "handle is NULL");

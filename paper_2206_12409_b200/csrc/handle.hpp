@@ -50,6 +50,8 @@ struct GraphEntry {
   int op = 0, nrhs = 0;
   const void* x = nullptr;
   void* y = nullptr;
+  const void* u = nullptr;   // second input / output of the fused pair
+  void* z = nullptr;
   cudaGraphExec_t exec = nullptr;
   int64_t launches = 0;
   uint64_t last_use = 0;
@@ -123,6 +125,8 @@ void handle_set_cores_device(vsie_coupling_s* h, int chi, const int r[3], const 
 void handle_alloc_workspace(vsie_coupling_s* h);
 
 void apply(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int nrhs, cudaStream_t st);
+// y = Z x and z = Z^T u (adj_op OP_T) or Z^H u (OP_C) in one call, single RHS
+void apply_pair(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z, int adj_op, cudaStream_t st);
 // drops the cached apply graphs (cores / workspaces changed)
 void apply_reset_graphs(vsie_coupling_s* h);
 void apply_destroy(vsie_coupling_s* h);

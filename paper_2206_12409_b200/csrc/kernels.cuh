@@ -60,6 +60,21 @@ struct GemvT {
   bool conj_out;  // store conj(y) (op C post-conjugation)
 };
 
+// Fused pair on the surface-side core (the off-diagonal coupling pair of one GMRES
+// matvec): ypart[s][r] = sum_{c in split s} A[r + R c] x[c] (forward y4 partials) and
+// z[c] = sum_r A[r + R c] z3[r] (transpose) from ONE pass over A (R <= 320).
+struct GemvNT {
+  const cplx* A[3];
+  const cplx* x[3];
+  const cplx* z3[3];
+  cplx* z[3];
+  cplx* y4[3];
+  int64_t R[3], C[3];
+  int nbatch;
+};
+// false when R > 320 (the caller falls back to separate passes)
+bool launch_gemv_nt(const GemvNT& a, cplx* partials, int64_t partials_cap, cudaStream_t st);
+
 struct ApplyWorkspace;  // split-K partials + counters (handle-owned)
 
 // partials_cap: capacity (elements) of the split-K partial buffer; the split is

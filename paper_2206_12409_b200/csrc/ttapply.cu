@@ -259,6 +259,73 @@ __global__ void __launch_bounds__(kThreads) k_gemv_t(const __grid_constant__ Gem
   }
 }
 
+// ----------------------------------------------------------------------------- fused N + T pass
+// Warp w of a CTA takes columns c0 + w + 8 j of its split; lane l holds rows l + 32 q
+// (q < NQ, R <= 32 NQ).  Per column: the transpose dot product with z3 (lane partials,
+// butterfly warp sum -> z[c]) and the forward accumulation acc[q] += A[r, c] x[c] (y4
+// partial of the split).  The next column's NQ streaming loads are in flight while this
+// one is consumed.  Split partials of y4 are reduced by k_sum_partials_warp (fixed order).
+template <int NQ>
+__global__ void __launch_bounds__(kThreads) k_gemv_nt(const __grid_constant__ GemvNT a, cplx* __restrict__ partials,
+                                                      int64_t rstride) {
+  __shared__ cplx red[kWarps][32 * NQ];
+  pdl_wait();
+  const int b = blockIdx.z;
+  const int64_t R = a.R[b], C = a.C[b];
+  const int nsplit = gridDim.x, s = blockIdx.x;
+  const int64_t c0 = C * s / nsplit, c1 = C * (s + 1) / nsplit;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const cplx* __restrict__ A = a.A[b];
+  const cplx* __restrict__ X = a.x[b];
+  cplx* __restrict__ Z = a.z[b];
+  const cplx* p[NQ];
+  cplx zv[NQ], acc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int64_t r = lane + 32 * q;
+    const bool act = r < R;
+    p[q] = A + (act ? r : R - 1);
+    zv[q] = act ? __ldcg(a.z3[b] + r) : cmk(0, 0);   // inactive rows: zero weight
+    acc[q] = cmk(0, 0);
+  }
+  int64_t c = c0 + warp;
+  if (c < c1) {
+    cplx v[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) v[q] = ld_stream(p[q] + R * c);
+    for (; c < c1; c += kWarps) {
+      cplx w[NQ];
+      const int64_t cn = c + kWarps < c1 ? c + kWarps : c;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) w[q] = ld_stream(p[q] + R * cn);
+      const cplx xv = __ldg(X + c);
+      cplx d = cmk(0, 0);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        cfma(d, v[q], zv[q]);
+        cfma(acc[q], v[q], xv);
+        v[q] = w[q];
+      }
+      d.x = warp_sum(d.x);
+      d.y = warp_sum(d.y);
+      if (lane == 0) Z[c] = d;
+    }
+  }
+  pdl_trigger();
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) red[warp][lane + 32 * q] = acc[q];
+  __syncthreads();
+  for (int r = threadIdx.x; r < R; r += kThreads) {
+    cplx t = red[0][r];
+#pragma unroll
+    for (int ww = 1; ww < kWarps; ++ww) t = cadd(t, red[ww][r]);
+    if (nsplit == 1)
+      a.y4[b][r] = t;
+    else
+      partials[((int64_t)b * nsplit + s) * rstride + r] = t;
+  }
+}
+
 // ----------------------------------------------------------------------------- G1 steps on FP64 tensor cores
 // Both G1 contractions are dense skinny GEMMs (K = r1 for the expansion, K = n1
 // for the transpose reduction), so they run on the sm_100a FP64 tensor cores
@@ -520,6 +587,41 @@ void launch_gemv_n(const GemvN& a, cplx* partials, int64_t partials_cap, int max
     }
     VSIE_CHECK_LAUNCH();
   }
+}
+
+bool launch_gemv_nt(const GemvNT& a, cplx* partials, int64_t partials_cap, cudaStream_t st) {
+  int64_t rmax = 0, cmax = 0;
+  for (int b = 0; b < a.nbatch; ++b) {
+    rmax = std::max(rmax, a.R[b]);
+    cmax = std::max(cmax, a.C[b]);
+  }
+  if (rmax > 320) return false;
+  if (cmax == 0) return true;
+  const int nq = (int)ceil_div(std::max<int64_t>(rmax, 1), 32);
+  // >= 8 columns per warp keep the per-warp pipeline full
+  int ns = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cmax, 8 * kWarps), 1024));
+  while (ns > 1 && (int64_t)a.nbatch * ns * rmax > partials_cap) --ns;
+  dim3 grid(ns, 1, a.nbatch);
+  switch (nq) {
+#define VSIE_NT(K) \
+  case K: launch_pdl(k_gemv_nt<K>, grid, dim3(kThreads), 0, st, a, partials, rmax); break;
+    VSIE_NT(1) VSIE_NT(2) VSIE_NT(3) VSIE_NT(4) VSIE_NT(5) VSIE_NT(6) VSIE_NT(7) VSIE_NT(8) VSIE_NT(9)
+    default: launch_pdl(k_gemv_nt<10>, grid, dim3(kThreads), 0, st, a, partials, rmax); break;
+#undef VSIE_NT
+  }
+  VSIE_CHECK_LAUNCH();
+  if (ns > 1) {
+    SumArgs sa{};
+    sa.nbatch = a.nbatch;
+    for (int b = 0; b < a.nbatch; ++b) {
+      sa.y[b] = a.y4[b];
+      sa.n[b] = a.R[b];
+    }
+    dim3 g2((unsigned)ceil_div(rmax, kThreads / 32), a.nbatch);
+    launch_pdl(k_sum_partials_warp, g2, dim3(kThreads), 0, st, sa, (const cplx*)partials, ns, rmax);
+    VSIE_CHECK_LAUNCH();
+  }
+  return true;
 }
 
 void launch_sum3(const cplx* in, int64_t chi_stride, int64_t ld_in, int64_t rows, int k, cplx* out, int64_t ld_out,

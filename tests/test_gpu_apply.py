@@ -185,3 +185,43 @@ def test_cfg3_full_grid_parity():
         h.configure(mode=mode)
         for op, v in (("N", x), ("T", u), ("C", u)):
             assert validate.rel_l2(h.apply(_cuda(v), op).cpu().numpy(), ref[op]) <= TOL, (mode, op)
+
+
+@pytest.mark.parametrize("ci", [1, 2, 4])
+def test_apply_pair(ci):
+    """vsie_coupling_apply_pair (one GMRES coupling matvec: Z x and Z^T u / Z^H u sharing
+    the G4 pass) equals the two separate applies and the oracle; bitwise reproducible."""
+    from paper_2206_12409_b200 import Coupling
+    import torch
+    cfg = synth.get_config(ci)
+    r = cfg.ranks_probe
+    ranks = [r, (max(1, r[0] - 1), r[1] + 3, r[2] - 5), (r[0] + 1, max(1, r[1] - 2), r[2] + 7)]
+    tts = rand_tts(cfg, ranks, 80 + ci)
+    h = Coupling.from_cores(grid_of(cfg), cfg.meshes(), cfg.freq, tts, nrhs_max=1)
+    x = _cuda(synth.complex_gaussian(cfg.m, 21))
+    u = _cuda(synth.complex_gaussian(3 * cfg.n_v, 22))
+    for adj in ("T", "C"):
+        y, z = h.apply_pair(x, u, adj)
+        y2, z2 = h.apply_pair(x, u, adj)
+        assert torch.equal(y, y2) and torch.equal(z, z2)
+        assert validate.rel_l2(y.cpu().numpy(), h.apply(x, "N").cpu().numpy()) <= 1e-13
+        assert validate.rel_l2(z.cpu().numpy(), h.apply(u, adj).cpu().numpy()) <= 1e-13
+        if ci == 1:
+            assert validate.rel_l2(y.cpu().numpy(), ttmv.apply(tts, x.cpu().numpy(), "N")) <= TOL
+            assert validate.rel_l2(z.cpu().numpy(), ttmv.apply(tts, u.cpu().numpy(), adj)) <= TOL
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_apply_pair_loopback(dense1, cfg1, world):
+    """The pair on the emulated slab partition (collectives around z3 and y4) equals P = 1."""
+    from paper_2206_12409_b200 import Coupling
+    tts = [ttsvd.tt_svd(ttmv.tensor_of(dense1, cfg1.n, chi), cfg1.tol) for chi in range(3)]
+    h1 = Coupling.from_cores(grid_of(cfg1), cfg1.meshes(), cfg1.freq, tts, nrhs_max=1)
+    hp = Coupling.from_cores(grid_of(cfg1), cfg1.meshes(), cfg1.freq, tts, nrhs_max=1, world=world, loopback=1)
+    x = _cuda(synth.complex_gaussian(cfg1.m, 41))
+    u = _cuda(synth.complex_gaussian(3 * cfg1.n_v, 42))
+    ya, za = h1.apply_pair(x, u, "T")
+    yb, zb = hp.apply_pair(x, u, "T")
+    assert validate.rel_l2(yb.cpu().numpy(), ya.cpu().numpy()) <= 1e-13
+    assert validate.rel_l2(zb.cpu().numpy(), za.cpu().numpy()) <= 1e-13
+    assert validate.rel_l2(ya.cpu().numpy(), ttmv.apply(tts, x.cpu().numpy(), "N")) <= TOL

@@ -72,6 +72,19 @@ for mode in ("persistent", "batched", "chains"):
     b = timed_stream(steps, False)
     print(json.dumps(dict(mode=mode, stream_flush_ms=a, stream_noflush_ms=b,
                           gbs_flush=B / (a[1] * 1e-3) / 1e9, gbs_noflush=B / (b[1] * 1e-3) / 1e9)))
+h.configure(mode="chains")
+def step_pair():
+    h.apply_pair(x, u, "T", out_y=y, out_z=z)
+for _ in range(3):
+    step_pair()
+torch.cuda.synchronize()
+ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+for i in range(steps):
+    flush.fill_(i & 255)
+    ev[i][0].record(); step_pair(); ev[i][1].record()
+torch.cuda.synchronize()
+tp = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+print(json.dumps(dict(mode="pair (apply_pair, chains)", stream_flush_ms=tp, gbs_flush=B / (tp * 1e-3) / 1e9)))
 h.configure(mode=os.environ.get('VSIE_MODE', 'chains'))
 print(json.dumps(dict(cfg=ci, ranks=ranks, graph_ms_median=med, graph_ms_mean=mean, gbs=B / (mean * 1e-3) / 1e9,
                       graph_ms_median_noflush=med_nf, bytes_per_step=B)))
