@@ -234,6 +234,8 @@ def main():
                     help="build = TT-cross build (default for configs 1, 2, 4); random = seeded cores at the "
                          "ranks of the recorded build (configs 3, 5: the build takes minutes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--separate", action="store_true",
+                    help="time the step as two vsie_coupling_apply calls instead of vsie_coupling_apply_pair")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -289,9 +291,16 @@ def main():
     flush = torch.empty(512 * 2 ** 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream()
 
-    def step():
+    def step_separate():
         h.apply_raw(x.data_ptr(), y.data_ptr(), "N", k, stream)
         h.apply_raw(u.data_ptr(), z.data_ptr(), "T", k, stream)
+
+    def step_pair():
+        # one GMRES coupling matvec: y = Z x and z = Z^T u in one call (G4 streamed once)
+        h.apply_pair_raw(x.data_ptr(), y.data_ptr(), u.data_ptr(), z.data_ptr(), "T", stream)
+
+    use_pair = k == 1 and not args.separate
+    step = step_pair if use_pair else step_separate
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -322,6 +331,19 @@ def main():
     launches = h.info()["apply_launches"] - launches0
     per = [a.elapsed_time(b) for a, b in ev]
     ms = float(np.mean(per))
+    sep_ms = None
+    if use_pair:
+        # the same step as two separate applies (context for the fused pair)
+        for _ in range(3):
+            step_separate()
+        ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            ev2[i][0].record(stream)
+            step_separate()
+            ev2[i][1].record(stream)
+        torch.cuda.synchronize()
+        sep_ms = float(np.mean([a.elapsed_time(b) for a, b in ev2]))
     # per-kernel CUDA-event timing: a second pass of the same K steps (same stream,
     # same inputs, L2 flushed) directly after the timed region, so the headline is
     # not perturbed by the event records between kernels
@@ -345,16 +367,21 @@ def main():
         uh = (torch.from_numpy(u_np) if k == 1 else u.cpu()).pin_memory()
         yh = torch.empty(vox_loc * k, dtype=torch.complex128).pin_memory()
         zh = torch.empty(cfg.m * k, dtype=torch.complex128).pin_memory()
+        def host_step():
+            if use_pair:
+                h.apply_pair_host_raw(xh.data_ptr(), yh.data_ptr(), uh.data_ptr(), zh.data_ptr(), "T")
+            else:
+                h.apply_host_raw(xh.data_ptr(), yh.data_ptr(), "N", k)
+                h.apply_host_raw(uh.data_ptr(), zh.data_ptr(), "T", k)
+
         for _ in range(2):
-            h.apply_host_raw(xh.data_ptr(), yh.data_ptr(), "N", k)
-            h.apply_host_raw(uh.data_ptr(), zh.data_ptr(), "T", k)
+            host_step()
         tl = []
         for _ in range(max(3, min(args.steps, 20))):
             if world > 1:
                 dist.barrier()
             t1 = time.perf_counter()
-            h.apply_host_raw(xh.data_ptr(), yh.data_ptr(), "N", k)
-            h.apply_host_raw(uh.data_ptr(), zh.data_ptr(), "T", k)
+            host_step()
             tl.append(time.perf_counter() - t1)
         e2e_s = float(np.mean(tl))
         if world > 1:
@@ -395,6 +422,8 @@ def main():
     kern = [t for t in timers if t["bytes_per_launch"] > 0 and t["launches"] > 0]
     dom = max(kern, key=lambda t: t["total_ms"]) if kern else None
     roof = None
+    with open(os.path.join(ROOT, "profiles", "r01", "fp64_peaks.json")) as f:
+        dmma_peak = float(json.load(f)["dmma_f64_tflops"])
     if dom:
         avg_ms = dom["total_ms"] / dom["launches"]
         ach = dom["bytes_per_launch"] / (avg_ms * 1e-3) / 1e9
@@ -408,17 +437,17 @@ def main():
                 "share_of_step": dom["total_ms"] / max(1e-9, sum(t["total_ms"] for t in timers)),
                 "bytes_per_launch": dom["bytes_per_launch"], "avg_us": avg_ms * 1e3,
                 "step_frac": value / peak}
-        if k > 1 and dom.get("flops_per_launch"):
-            # block RHS: the contractions are dense complex GEMMs on the FP64 tensor cores
-            # (AI ~ 15 flop/B); peak = the DMMA rate measured on this pool
+        ai = dom.get("flops_per_launch", 0) / max(1, dom["bytes_per_launch"])
+        if k > 1 or ai > dmma_peak * 1e12 / (peak * 1e9):
+            # above the FP64 ridge (block RHS, SURVEY §8d AI ~ 15; the G2 contractions, AI ~ 20):
+            # a tensor-core bound kernel, against the DMMA rate measured on this pool
             # (tools/microbench/fp64_peaks.cu -> profiles/r01/fp64_peaks.json)
-            with open(os.path.join(ROOT, "profiles", "r01", "fp64_peaks.json")) as f:
-                dmma = float(json.load(f)["dmma_f64_tflops"])
+            dmma = dmma_peak
             tf = dom["flops_per_launch"] / (avg_ms * 1e-3) / 1e12
             roof.update({"bound": "tensor", "achieved": tf, "peak": dmma, "unit": "TFLOP/s", "frac": tf / dmma,
                          "peak_source": "measured FP64 DMMA (profiles/r01/fp64_peaks.json)",
                          "flops_per_launch": dom["flops_per_launch"],
-                         "step_frac": F / (ms * 1e-3) / 1e12 / dmma})
+                         "step_frac": (F / (ms * 1e-3) / 1e12 / dmma) if k > 1 else value / peak})
     kern_table = {t["name"]: {"avg_us": 1e3 * t["total_ms"] / max(1, t["launches"]),
                               "launches_per_step": t["launches"] / max(1, args.steps),
                               "gbs": (t["bytes_per_launch"] / (t["total_ms"] / t["launches"] * 1e-3) / 1e9)
@@ -441,7 +470,15 @@ def main():
         "config": {"workload": f"cfg{cfg.idx} {cfg.name}: grid {cfg.n}, h {cfg.h[0]*1e3:.0f} mm, m={cfg.m} RWG "
                                f"({' + '.join(f'{s.name} {s.n_az}x{s.n_ax}' for s in cfg.surfaces)}), "
                                f"f=298.2 MHz, tol {cfg.tol}, nrhs {k}",
-                   "step": f"1 forward (Y = Z X) + 1 transpose (Z^T U) TT apply, {k} RHS",
+                   "step": (f"1 forward (y = Z x) + 1 transpose (z = Z^T u) TT apply as ONE vsie_coupling_apply_pair "
+                            f"call (the coupling pair of a GMRES matvec; both G4 products share one pass over G4)"
+                            if use_pair else f"1 forward (Y = Z X) + 1 transpose (Z^T U) TT apply, {k} RHS"),
+                   "bytes_per_step_note": ("value = SURVEY 8d formula bytes (B_fwd + B_adj, G4 counted twice) / time; "
+                                           "the pair reads G4 once: bytes_pair_per_step / time = pair_hbm_gbs"
+                                           if use_pair else "SURVEY 8d formula bytes / time"),
+                   "bytes_pair_per_step": B - 16 * sum(r[2] * cfg.m for r in ranks) if use_pair else None,
+                   "pair_hbm_gbs": ((B - 16 * sum(r[2] * cfg.m for r in ranks)) / (ms * 1e-3) / 1e9) if use_pair else None,
+                   "separate_applies": ({"ms_per_step": sep_ms, "gbs": B / (sep_ms * 1e-3) / 1e9} if sep_ms else None),
                    "cores": ("TT-cross build on this GPU" if mode == "build"
                              else "seeded random cores at the ranks of the recorded B200 build (profiles/)"),
                    "ranks": ranks,

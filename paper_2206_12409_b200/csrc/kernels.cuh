@@ -46,6 +46,7 @@ struct GemvN {
   const cplx* x[3];
   cplx* y[3];
   int64_t R[3], C[3];
+  int64_t lda[3];   // column stride of A (0 = R: a contiguous matrix)
   int nbatch;
 };
 // y[chi][c] = sum_r A[chi][r + R c] x[chi][r]  (plain transpose); if sum_batch,
@@ -55,6 +56,7 @@ struct GemvT {
   const cplx* x[3];
   cplx* y[3];
   int64_t R[3], C[3];
+  int64_t lda[3];   // column stride of A (0 = R)
   int nbatch;
   bool sum_batch;
   bool conj_out;  // store conj(y) (op C post-conjugation)
@@ -67,6 +69,7 @@ struct GemvNT {
   const cplx* A[3];
   const cplx* x[3];
   const cplx* z3[3];
+  const cplx* z3b[3];   // optional second partial of z3 (summed on load), may be null
   cplx* z[3];
   cplx* y4[3];
   int64_t R[3], C[3];

@@ -395,8 +395,8 @@ void launch_zgemm_dmma(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t 
   int splits = 1;
   if (ws != nullptr && tiles < 2 * 148) {
     // few output tiles with a long K (the transpose G2 step, the block-RHS G4 / G3^T
-    // products): split K towards two CTAs per SM, each on >= 8 chunks of 16
-    splits = (int)std::min<int64_t>(std::min<int64_t>(ceil_div(2 * 148, tiles), std::max<int64_t>(1, chunks / 8)), 64);
+    // products): split K towards two CTAs per SM, each on >= 3 chunks of 16
+    splits = (int)std::min<int64_t>(std::min<int64_t>(ceil_div(2 * 148, tiles), std::max<int64_t>(1, chunks / 3)), 64);
     while (splits > 1 && (int64_t)splits * mn * g.nbatch > ws_elems) --splits;
     splits = std::max(splits, 1);
   }

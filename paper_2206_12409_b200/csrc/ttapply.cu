@@ -14,8 +14,10 @@
 // by the last-arriving CTA (threadfence + ticket counter), so results are
 // bitwise reproducible run to run.
 #include "kernels.cuh"
+#include "dmma_tile.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <utility>
 #include <vector>
 
@@ -48,6 +50,7 @@ __global__ void __launch_bounds__(512) k_gemv_n(const __grid_constant__ GemvN a,
   pdl_wait();
   const int b = blockIdx.z;
   const int64_t R = a.R[b], C = a.C[b];
+  const int64_t LD = a.lda[b] ? a.lda[b] : R;
   const int64_t row = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
   const bool act = row < R;
   const int nsplit = gridDim.x, s = blockIdx.x;
@@ -61,7 +64,7 @@ __global__ void __launch_bounds__(512) k_gemv_n(const __grid_constant__ GemvN a,
     cplx v[U], xv[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      v[u] = ld_stream(p + R * (c + u));
+      v[u] = ld_stream(p + LD * (c + u));
       xv[u] = __ldg(X + c + u);
     }
     c += U;
@@ -69,7 +72,7 @@ __global__ void __launch_bounds__(512) k_gemv_n(const __grid_constant__ GemvN a,
       cplx w[U], xw[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        w[u] = ld_stream(p + R * (c + u));
+        w[u] = ld_stream(p + LD * (c + u));
         xw[u] = __ldg(X + c + u);
       }
 #pragma unroll
@@ -89,7 +92,54 @@ __global__ void __launch_bounds__(512) k_gemv_n(const __grid_constant__ GemvN a,
       cfma(acc2, v[u + 1], xv[u + 1]);
     }
   }
-  for (; c < c1; ++c) cfma(acc, __ldcs(p + R * c), __ldg(X + c));
+  for (; c < c1; ++c) cfma(acc, __ldcs(p + LD * c), __ldg(X + c));
+  pdl_trigger();
+  acc = cadd(acc, acc2);
+  if (!act) return;
+  if (nsplit == 1)
+    a.y[b][row] = acc;
+  else
+    partials[((int64_t)b * nsplit + s) * rmax + row] = acc;
+}
+
+// cp.async variant: thread t owns row t of its tile and keeps the next S - 1 columns of
+// that row in flight as 16-B cp.async copies into its own smem slots (ring[slot][t]; no
+// registers held, no barrier -- every slot is written and read by the same thread), so a
+// CTA has S x blockDim x 16 B in flight: with 3 CTAs per SM ~190 KB per SM, the depth the
+// loaded HBM latency (~5 us at 6 TB/s) needs.  x of the split staged in smem once.
+template <int S>
+__global__ void __launch_bounds__(320) k_gemv_n_cp(const __grid_constant__ GemvN a, cplx* __restrict__ partials,
+                                                   int64_t rmax) {
+  extern __shared__ __align__(16) cplx cp_smem[];
+  pdl_wait();
+  const int b = blockIdx.z;
+  const int64_t R = a.R[b], C = a.C[b];
+  const int T = blockDim.x, t = threadIdx.x;
+  const int64_t row = (int64_t)blockIdx.y * T + t;
+  const bool act = row < R;
+  const int nsplit = gridDim.x, s = blockIdx.x;
+  const int64_t c0 = C * s / nsplit, c1 = C * (s + 1) / nsplit;
+  const int nc = (int)(c1 - c0);
+  cplx* ring = cp_smem;                 // [S][T]
+  cplx* xs = cp_smem + (size_t)S * T;   // [nc]
+  const int64_t LD = a.lda[b] ? a.lda[b] : R;
+  const cplx* __restrict__ p = a.A[b] + (act ? row : R - 1) + LD * c0;
+  for (int j = t; j < nc; j += T) xs[j] = __ldcg(a.x[b] + c0 + j);
+#pragma unroll
+  for (int j = 0; j < S - 1; ++j) {
+    if (j < nc) tc::cp_async16(ring + j * T + t, p + LD * j, 16);
+    tc::cp_async_commit();
+  }
+  __syncthreads();   // xs visible
+  cplx acc = cmk(0, 0), acc2 = cmk(0, 0);
+  for (int j = 0; j < nc; ++j) {
+    const int jn = j + S - 1;
+    if (jn < nc) tc::cp_async16(ring + (jn % S) * T + t, p + LD * jn, 16);
+    tc::cp_async_commit();
+    tc::cp_async_wait<S - 1>();
+    const cplx v = ring[(j % S) * T + t];
+    if (j & 1) cfma(acc2, v, xs[j]); else cfma(acc, v, xs[j]);
+  }
   pdl_trigger();
   acc = cadd(acc, acc2);
   if (!act) return;
@@ -196,7 +246,8 @@ __global__ void __launch_bounds__(kThreads) k_gemv_t(const __grid_constant__ Gem
     const cplx* __restrict__ X = a.x[b];
     const cplx* __restrict__ col[kCPW];
 #pragma unroll
-    for (int j = 0; j < kCPW; ++j) col[j] = A + R * (cok[j] ? cbase + j : Cout - 1);
+    const int64_t LD = a.lda[b] ? a.lda[b] : R;
+    for (int j = 0; j < kCPW; ++j) col[j] = A + LD * (cok[j] ? cbase + j : Cout - 1);
     int64_t r = r0 + lane;
     // software pipeline: the next kTU row groups are in flight while this batch is consumed
     if (r + 32 * (kTU - 1) < r1) {
@@ -278,26 +329,32 @@ __global__ void __launch_bounds__(kThreads) k_gemv_nt(const __grid_constant__ Ge
   const cplx* __restrict__ A = a.A[b];
   const cplx* __restrict__ X = a.x[b];
   cplx* __restrict__ Z = a.z[b];
-  const cplx* p[NQ];
   cplx zv[NQ], acc[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     const int64_t r = lane + 32 * q;
-    const bool act = r < R;
-    p[q] = A + (act ? r : R - 1);
-    zv[q] = act ? __ldcg(a.z3[b] + r) : cmk(0, 0);   // inactive rows: zero weight
+    zv[q] = cmk(0, 0);   // inactive rows: zero weight
+    if (r < R) {
+      zv[q] = __ldcg(a.z3[b] + r);
+      if (a.z3b[b]) zv[q] = cadd(zv[q], __ldcg(a.z3b[b] + r));
+    }
     acc[q] = cmk(0, 0);
   }
+  // rows past R re-read row R - 1 (zero weight in the dot product, discarded for y4)
+  const int last = (int)(R - 1 - lane);
+  auto row = [&](int q) { return min(32 * q, last) + lane; };
   int64_t c = c0 + warp;
   if (c < c1) {
     cplx v[NQ];
+    const cplx* col = A + R * c;
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) v[q] = ld_stream(p[q] + R * c);
+    for (int q = 0; q < NQ; ++q) v[q] = ld_stream(col + row(q));
     for (; c < c1; c += kWarps) {
       cplx w[NQ];
       const int64_t cn = c + kWarps < c1 ? c + kWarps : c;
+      const cplx* coln = A + R * cn;
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) w[q] = ld_stream(p[q] + R * cn);
+      for (int q = 0; q < NQ; ++q) w[q] = ld_stream(coln + row(q));
       const cplx xv = __ldg(X + c);
       cplx d = cmk(0, 0);
 #pragma unroll
@@ -539,6 +596,24 @@ int sm_count() {
 
 }  // namespace
 
+void launch_gemv_sum(const GemvN& a, cplx* partials, int ns, int64_t rmax, cudaStream_t st) {
+  if (ns <= 1) return;
+  SumArgs sa{};
+  sa.nbatch = a.nbatch;
+  for (int b = 0; b < a.nbatch; ++b) {
+    sa.y[b] = a.y[b];
+    sa.n[b] = a.R[b];
+  }
+  if (ns >= 16) {
+    dim3 g2((unsigned)ceil_div(rmax, kThreads / 32), a.nbatch);
+    launch_pdl(k_sum_partials_warp, g2, dim3(kThreads), 0, st, sa, (const cplx*)partials, ns, rmax);
+  } else {
+    dim3 g2((unsigned)ceil_div(rmax, kThreads), a.nbatch);
+    launch_pdl(k_sum_partials, g2, dim3(kThreads), 0, st, sa, (const cplx*)partials, ns, rmax);
+  }
+  VSIE_CHECK_LAUNCH();
+}
+
 void launch_gemv_n(const GemvN& a, cplx* partials, int64_t partials_cap, int max_splits, cudaStream_t st) {
   int64_t rmax = 0, cmax = 0;
   for (int b = 0; b < a.nbatch; ++b) {
@@ -546,6 +621,36 @@ void launch_gemv_n(const GemvN& a, cplx* partials, int64_t partials_cap, int max
     cmax = std::max(cmax, a.C[b]);
   }
   if (rmax == 0) return;
+  static const int cp_sel = [] {
+    const char* e = std::getenv("VSIE_GEMV_CP");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (cp_sel) {
+    constexpr int S = 16;
+    const int T = rmax <= 320 ? (int)(ceil_div(rmax, 32) * 32) : 256;
+    const int64_t rtiles = ceil_div(rmax, T);
+    static bool attr = false;
+    if (!attr) {
+      VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_gemv_n_cp<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+    // splits: fill the resident slots once (>= 32 columns per CTA)
+    const int64_t per = rtiles * a.nbatch;
+    const size_t smem_est = ((size_t)S * T + ceil_div(cmax, 64)) * sizeof(cplx);
+    int occ = 1;
+    VSIE_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gemv_n_cp<S>, T, smem_est));
+    occ = std::max(1, occ);
+    int64_t nsl = std::max<int64_t>(1, std::min<int64_t>((int64_t)occ * sm_count() / per, cmax / 32));
+    int ns = (int)std::min<int64_t>(nsl, max_splits);
+    while (ns > 1 && (int64_t)a.nbatch * ns * rmax > partials_cap) --ns;
+    const int64_t ncmax = ceil_div(cmax, ns);
+    const size_t smem = ((size_t)S * T + ncmax) * sizeof(cplx);
+    dim3 grid(ns, (unsigned)rtiles, a.nbatch);
+    launch_pdl(k_gemv_n_cp<S>, grid, dim3(T), smem, st, a, partials, rmax);
+    VSIE_CHECK_LAUNCH();
+    launch_gemv_sum(a, partials, ns, rmax, st);
+    return;
+  }
   static const int u_sel = [] {
     const char* e = std::getenv("VSIE_GEMV_U");
     return e ? std::atoi(e) : 4;
@@ -598,8 +703,13 @@ bool launch_gemv_nt(const GemvNT& a, cplx* partials, int64_t partials_cap, cudaS
   if (rmax > 320) return false;
   if (cmax == 0) return true;
   const int nq = (int)ceil_div(std::max<int64_t>(rmax, 1), 32);
-  // >= 8 columns per warp keep the per-warp pipeline full
-  int ns = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cmax, 8 * kWarps), 1024));
+  // one full wave of resident CTAs, >= 8 columns per warp
+  const void* fn = nq <= 1 ? (const void*)k_gemv_nt<1> : nq == 2 ? (const void*)k_gemv_nt<2> : nq == 3 ? (const void*)k_gemv_nt<3>
+                 : nq == 4 ? (const void*)k_gemv_nt<4> : nq == 5 ? (const void*)k_gemv_nt<5> : nq == 6 ? (const void*)k_gemv_nt<6>
+                 : nq == 7 ? (const void*)k_gemv_nt<7> : nq == 8 ? (const void*)k_gemv_nt<8> : nq == 9 ? (const void*)k_gemv_nt<9>
+                 : (const void*)k_gemv_nt<10>;
+  const int64_t slots = (int64_t)sm_count() * gemv_occupancy(fn, kThreads);
+  int ns = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cmax, 8 * kWarps), slots / a.nbatch));
   while (ns > 1 && (int64_t)a.nbatch * ns * rmax > partials_cap) --ns;
   dim3 grid(ns, 1, a.nbatch);
   switch (nq) {

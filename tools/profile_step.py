@@ -19,6 +19,6 @@ u = torch.from_numpy(synth.complex_gaussian(3 * cfg.n_v, 2)).cuda()
 y = torch.empty(3 * cfg.n_v, dtype=torch.complex128, device="cuda")
 z = torch.empty(cfg.m, dtype=torch.complex128, device="cuda")
 for _ in range(steps):
-    h.apply(x, "N", out=y); h.apply(u, "T", out=z)
+    h.apply_pair(x, u, "T", out_y=y, out_z=z)
 torch.cuda.synchronize()
 print("ok", h.info()["apply_launches"] // steps, "launches per step")
