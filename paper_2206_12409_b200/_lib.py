@@ -116,7 +116,8 @@ def lib():
             raise ImportError(
                 f"{LIB_PATH} is missing: build it with `python -m paper_2206_12409_b200._build` "
                 "(there is no CPU fallback)")
-        L = C.CDLL(LIB_PATH)
+        # RTLD_NOW: an unresolved symbol fails the load here, not at first call
+        L = C.CDLL(LIB_PATH, mode=os.RTLD_NOW | os.RTLD_LOCAL)
         for name, (res, args) in _SIGS.items():
             f = getattr(L, name)
             f.restype = res

@@ -101,6 +101,16 @@ struct Ctx {
 
 constexpr int kMaxSplits = 256;
 
+bool fuse_g21() {
+  // fused G2 + G1 forward tail (k_g21_fwd): measured 0.173 vs 0.167 ms per pair step at
+  // cfg 2 (its 110 KB of smem leave one CTA per SM) -- opt-in
+  static const int v = [] {
+    const char* e = std::getenv("VSIE_FUSE_G21");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v != 0;
+}
+
 // ------------------------------------------------------------------ forward chain pieces (one chi)
 // step 1: y4 = G4[:, owned] x[owned], partial per shard
 void fwd_g4(const Ctx& X, Shard& s, int c, const cplx* x, cudaStream_t st) {
@@ -169,6 +179,26 @@ void fwd_rest(const Ctx& X, Shard& s, int c, cplx* y, cudaStream_t st, cudaEvent
     launch_zgemm_dmma(z, X.zws(c), h->zgemm_ws_per_chi, st);
   }
   if (mid) VSIE_CHECK_CUDA(cudaEventRecord(mid, st));   // chain staggering: G3 stream done
+  if (k == 1 && fuse_g21()) {
+    // Y2 = G2 Y3 and y = G1 Y2 in one kernel (Y2 tiles stay in shared memory)
+    G21Args f{};
+    f.G1 = h->G1[c].p;
+    f.G2 = h->G2[c].p;
+    f.Y3 = Y3;
+    f.y = y + c * X.L.chi_stride + shard_voxel_offset(h, s, X.L);
+    f.n1 = n1;
+    f.n2 = n2;
+    f.n3l = (int)n3l;
+    f.r1 = (int)r1;
+    f.r2 = (int)r2;
+    bool done;
+    {
+      const int64_t bytes = 16 * ((int64_t)n1 * r1 + r1 * n2 * r2 + r2 * n3l + (int64_t)n1 * n2 * n3l);
+      Scope sc(h, "fwd_g21_fused", bytes, 8 * (r1 * n2 * r2 * n3l + (int64_t)n1 * r1 * n2 * n3l), st);
+      done = launch_g21_fwd(f, st);
+    }
+    if (done) return;
+  }
   {
     Zgemm z{};
     z.nbatch = 1;

@@ -119,6 +119,19 @@ void launch_reduce_g1(const ReduceArgs& a, cudaStream_t st);
 void launch_sum3(const cplx* in, int64_t chi_stride, int64_t ld_in, int64_t rows, int k, cplx* out, int64_t ld_out,
                  bool conj_out, cudaStream_t st);
 
+// Fused forward tail of one chi (single RHS): Y2 = G2 Y3 on a tile of (i2, i3) planes
+// into shared memory, then y = G1 Y2 for the tile's voxel columns (Eq. 17 steps
+// 3-4).  y points at the chi block (and slab offset) of the voxel output.
+struct G21Args {
+  const cplx* G1;   // n1 x r1
+  const cplx* G2;   // (r1 n2) x r2
+  const cplx* Y3;   // r2 x n3l
+  cplx* y;
+  int n1, n2, n3l, r1, r2;
+};
+// false if r1 > 32 (caller falls back to the two-kernel path)
+bool launch_g21_fwd(const G21Args& a, cudaStream_t st);
+
 // ------------------------------------------------------------------ dense complex LA (linalg.cu)
 enum Trans { kN = 0, kT = 1, kC = 2 };
 // C = alpha op(A) op(B) + beta C, column-major; batched over up to 3 problems with

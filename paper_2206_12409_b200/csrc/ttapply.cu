@@ -566,6 +566,82 @@ __global__ void __launch_bounds__(kThreads) k_sum3(const cplx* __restrict__ in, 
   }
 }
 
+// ----------------------------------------------------------------------------- fused G2 + G1 (forward)
+// Tile = i2 block of B2 (r1 B2 <= 64) x i3 block of 32 planes.  Step A: the (r1 B2) x 32
+// block of Y2 = G2[rows of the i2 block, :] Y3[:, planes] by one 64 x 32 3M-DMMA GEMM
+// tile (dmma_tile.cuh) written to shared memory; step B: the G1 expansion of the tile's
+// B2 x 32 voxel columns straight from that smem block (Y2 never touches HBM).
+constexpr int kG21B3 = 32;
+
+template <int KT>
+__global__ void __launch_bounds__(kG1Threads) k_g21_fwd(const __grid_constant__ G21Args a, int B2) {
+  extern __shared__ __align__(16) unsigned char g21_smem[];
+  tc::GemmSmem& gsm = *reinterpret_cast<tc::GemmSmem*>(g21_smem);
+  cplx* Y2t = reinterpret_cast<cplx*>(g21_smem + ((sizeof(tc::GemmSmem) + 127) / 128) * 128);   // [64 x 32]
+  cplx* Af = Y2t + 64 * kG21B3;                                                                   // G1 fragments
+  const int n1 = a.n1, r1 = a.r1, n2 = a.n2;
+  const int mt = (n1 + 7) / 8;
+  // G1 fragments (a constant core): staged before waiting for the producer of Y3
+  for (int e = threadIdx.x; e < mt * KT * 32; e += kG1Threads) {
+    const int lane = e % 32, ks = (e / 32) % KT, m = e / (32 * KT);
+    const int i1 = 8 * m + (lane >> 2), k = 4 * ks + (lane & 3);
+    Af[e] = (i1 < n1 && k < r1) ? __ldg(a.G1 + i1 + (int64_t)n1 * k) : cmk(0, 0);
+  }
+  pdl_wait();
+  const int nb2 = (n2 + B2 - 1) / B2;
+  const int i2b = (blockIdx.x % nb2) * B2, i3b = (blockIdx.x / nb2) * kG21B3;
+  const int b2 = min(B2, n2 - i2b), b3 = min(kG21B3, a.n3l - i3b);
+  const int64_t M = (int64_t)r1 * b2;
+  // step A: Y2t (M x b3, ld M) = G2[r1 i2b + (0..M), :] Y3[:, i3b + (0..b3)]
+  tc::gemm_tile<tc::FWA, tc::FWB, false>(a.G2 + (int64_t)r1 * i2b, (int64_t)r1 * n2, a.Y3 + (int64_t)a.r2 * i3b, a.r2, M,
+                                         b3, 0, 0, 0, a.r2, gsm, Y2t, M);
+  __syncthreads();
+  pdl_trigger();
+  // step B: columns col = i2l + b2 i3l (Y2 column stride r1 in Y2t)
+  const int ncol = b2 * b3;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  for (int c0 = warp * kColsPerWarp; c0 < ncol; c0 += kWarpsG1 * kColsPerWarp) {
+    cplx bf[KT];
+    {
+      const int c = c0 + g;
+#pragma unroll
+      for (int ks = 0; ks < KT; ++ks) {
+        const int k = 4 * ks + t;
+        bf[ks] = (c < ncol && k < r1) ? Y2t[r1 * c + k] : cmk(0, 0);
+      }
+    }
+    int64_t oaddr[2];
+    bool ok[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int c = c0 + 2 * t + j;
+      ok[j] = c < ncol;
+      const int i2l = ok[j] ? c % b2 : 0, i3l = ok[j] ? c / b2 : 0;
+      oaddr[j] = (int64_t)n1 * ((i2b + i2l) + (int64_t)n2 * (i3b + i3l));
+    }
+    double bsum[KT];
+#pragma unroll
+    for (int ks = 0; ks < KT; ++ks) bsum[ks] = bf[ks].x + bf[ks].y;
+    for (int m = 0; m < mt; ++m) {
+      double p1[2] = {0, 0}, p2[2] = {0, 0}, p3[2] = {0, 0};
+#pragma unroll
+      for (int ks = 0; ks < KT; ++ks) {
+        const cplx av = Af[(m * KT + ks) * 32 + lane];
+        dmma(p1[0], p1[1], av.x, bf[ks].x);
+        dmma(p2[0], p2[1], av.y, bf[ks].y);
+        dmma(p3[0], p3[1], av.x + av.y, bsum[ks]);
+      }
+      const int i1 = 8 * m + g;
+      if (i1 < n1) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          if (ok[j]) __stcs(a.y + oaddr[j] + i1, cmk(p1[j] - p2[j], p3[j] - p1[j] - p2[j]));
+      }
+    }
+  }
+}
+
 int pick_splits(int64_t other_ctas, int64_t len, int min_len, int max_splits, int64_t target) {
   int64_t sp = target / std::max<int64_t>(1, other_ctas);
   sp = std::min<int64_t>(sp, len / std::max(1, min_len));
@@ -828,6 +904,33 @@ void launch_reduce_g1(const ReduceArgs& a, cudaStream_t st) {
   }
 #undef VSIE_RED
   VSIE_CHECK_LAUNCH();
+}
+
+bool launch_g21_fwd(const G21Args& a, cudaStream_t st) {
+  if (a.r1 > 32 || a.r1 < 1) return false;
+  const int B2 = std::max(1, std::min(a.n2, 64 / a.r1));
+  const int KT = (a.r1 + 3) / 4;
+  const size_t smem = ((sizeof(tc::GemmSmem) + 127) / 128) * 128 + (size_t)64 * kG21B3 * sizeof(cplx) +
+                      (size_t)((a.n1 + 7) / 8) * KT * 32 * sizeof(cplx);
+  if (smem > 220 * 1024) return false;
+  const int nb2 = (a.n2 + B2 - 1) / B2, nb3 = (a.n3l + kG21B3 - 1) / kG21B3;
+  dim3 grid((unsigned)(nb2 * nb3));
+#define VSIE_G21(K)                                                                                \
+  case K: {                                                                                        \
+    static bool d = false;                                                                         \
+    if (!d) {                                                                                      \
+      VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_g21_fwd<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024)); \
+      d = true;                                                                                    \
+    }                                                                                              \
+    launch_pdl(k_g21_fwd<K>, grid, dim3(kG1Threads), smem, st, a, B2);                             \
+    break;                                                                                         \
+  }
+  switch (KT) {
+    VSIE_G21(1) VSIE_G21(2) VSIE_G21(3) VSIE_G21(4) VSIE_G21(5) VSIE_G21(6) VSIE_G21(7) default: VSIE_G21(8)
+  }
+#undef VSIE_G21
+  VSIE_CHECK_LAUNCH();
+  return true;
 }
 
 }  // namespace vsie

@@ -225,3 +225,28 @@ def test_apply_pair_loopback(dense1, cfg1, world):
     assert validate.rel_l2(yb.cpu().numpy(), ya.cpu().numpy()) <= 1e-13
     assert validate.rel_l2(zb.cpu().numpy(), za.cpu().numpy()) <= 1e-13
     assert validate.rel_l2(ya.cpu().numpy(), ttmv.apply(tts, x.cpu().numpy(), "N")) <= TOL
+
+
+def test_fused_g21_forward(monkeypatch):
+    """The opt-in fused forward tail (Y2 = G2 Y3 and y = G1 Y2 in one kernel, Y2 tiles in
+    shared memory) matches the oracle; run in a subprocess because the switch is read once."""
+    import subprocess, sys, textwrap, os
+    code = textwrap.dedent('''
+        import sys; sys.path.insert(0, "tests")
+        import synth, numpy as np, torch
+        from oracle import ttmv, validate
+        from gpu_common import grid_of, rand_tts
+        from paper_2206_12409_b200 import Coupling
+        for ci in (1, 2):
+            cfg = synth.get_config(ci)
+            tts = rand_tts(cfg, [cfg.ranks_probe] * 3, 90 + ci)
+            h = Coupling.from_cores(grid_of(cfg), cfg.meshes(), cfg.freq, tts, nrhs_max=1)
+            x = synth.complex_gaussian(cfg.m, 5)
+            y = h.apply(torch.from_numpy(x).cuda(), "N").cpu().numpy()
+            assert validate.rel_l2(y, ttmv.apply(tts, x, "N")) <= 1e-12, ci
+        print("fused ok")
+    ''')
+    env = dict(os.environ, VSIE_FUSE_G21="1")
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert p.returncode == 0 and "fused ok" in p.stdout, p.stderr[-2000:]
