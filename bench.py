@@ -456,10 +456,14 @@ def main():
                               if t.get("flops_per_launch") else None} for t in timers}
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        t_cpu, ts = oracle_step_rate(cfg, ranks, steps=1 if cfg.n_v > 5e6 else 2)
+        # a bounded sample of ~10 s of host work: as many oracle steps as fit (>= 1)
+        t1, _ = oracle_step_rate(cfg, ranks, steps=1)
+        nsteps = int(max(1, min(50, 10.0 / max(t1, 1e-3))))
+        t_cpu, ts = oracle_step_rate(cfg, ranks, steps=nsteps) if nsteps > 1 else (t1, [t1])
         B1, _ = step_bytes_flops(cfg.n, cfg.m, ranks, 1)
         cpu = {"value": B1 / t_cpu / 1e9, "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
-               "sample": ("single-RHS GMRES step(s) (oracle TT fwd + transpose, NumPy) of the same cfg and ranks"
+               "steps_timed": len(ts),
+               "sample": (f"{len(ts) + 1} single-RHS GMRES step(s) (oracle TT fwd + transpose, NumPy) of the same cfg and ranks"
                           + (", chi 0 timed and x3" if cfg.n_v > 5_000_000 else ", random cores")
                           + (" (per RHS column of the block workload)" if k > 1 else "")),
                "ms_per_step": t_cpu * 1e3, "entries_per_s": oracle_entry_rate(cfg)}
@@ -491,7 +495,10 @@ def main():
                    "sweeps": inf["sweeps"] if mode == "build" else None,
                    "compression": float(inf["compression"]) if inf["compression"] else None},
         "entries": {"value": ent_s, "unit": "entries/s", "pair_interactions_per_s": 48 * ent_s,
-                    "sample": "1e6 uniform random (row, col), 5 reps"},
+                    "sample": "1e6 uniform random (row, col), 5 reps",
+                    "structured_blocks_per_s": (inf["entries_evaluated"] / inf["build_entry_s"])
+                    if mode == "build" and inf["build_entry_s"] > 0 else None,
+                    "structured_note": "supercore blocks evaluated by the TT-cross build (entries / entry-kernel time)"},
         "roofline": roof,
         "kernels": kern_table,
         "cpu_baseline": cpu,
