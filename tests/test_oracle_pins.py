@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 
 import synth
-from oracle import entries, geometry, greens, maxvol, ttcross, ttmv, ttsvd, validate
+from oracle import entries, geometry, greens, maxvol, ttcross, ttmv, ttround, ttsvd, validate
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 K0 = 2 * np.pi * synth.configs.FREQ_7T / synth.configs.C0
@@ -542,3 +542,85 @@ def test_T1_entry_parity_metric():
     bad = ref.copy(); bad[2] += 1e-10
     ok, w = validate.entry_parity(bad, ref)
     assert not ok and w["elementwise_rel"] > 1e-12
+
+
+# ---------------------------------------------------------------- TT rounding (§8f NEXT-1)
+
+def _inflate(cores, extra, seed):
+    """Same tensor with each inner rank grown by `extra` (redundant directions):
+    G_k <- [G_k, G_k M_k] on the right, G_{k+1} <- [G_{k+1}; 0] on the left."""
+    rng = np.random.default_rng(seed)
+    G = [np.array(c) for c in cores]
+    for k in range(len(G) - 1):
+        a, n, b = G[k].shape
+        M = rng.normal(size=(b, extra)) + 1j * rng.normal(size=(b, extra))
+        L = G[k].reshape((a * n, b), order="F")
+        G[k] = np.concatenate([L, L @ M], axis=1).reshape((a, n, b + extra), order="F")
+        b2, n2, c2 = G[k + 1].shape
+        G[k + 1] = np.concatenate([G[k + 1], np.zeros((extra, n2, c2), complex)], axis=0)
+    return G
+
+
+def test_P36_round_recovers_inflated_ranks():
+    # a TT padded with redundant (linearly dependent) rank directions is the same tensor;
+    # rounding at 1e-12 must return the minimal ranks and the tensor (vs dense expansion)
+    for ranks, seed in (((2, 3, 2), 36), ((3, 5, 4), 37)):
+        cores = _rand_tt((6, 7, 8, 20), ranks, seed)
+        T = ttmv.full(cores)
+        fat = _inflate(cores, 3, seed)
+        assert np.linalg.norm(ttmv.full(fat) - T) <= 1e-12 * np.linalg.norm(T)
+        out = ttround.tt_round(fat, 1e-12)
+        assert ttmv.ranks_of(out) == ranks
+        assert np.linalg.norm(ttmv.full(out) - T) <= 1e-12 * np.linalg.norm(T)
+
+
+def test_P37_round_equals_ttsvd_ranks_and_bound():
+    # rounding a TT is the TT-SVD of the tensor it represents (same unfoldings' singular
+    # values): ranks equal TT-SVD's of the dense tensor, error within tol ||A||
+    i = np.arange(9)
+    H = 1.0 / (i[:, None, None, None] + i[None, :, None, None] + 2 * i[None, None, :, None]
+               + 0.5 * i[None, None, None, :] + 1.0) + 0.0j
+    exact = ttsvd.tt_svd(H, 1e-15)
+    fat = _inflate(exact, 2, 38)
+    for tol in (1e-3, 1e-6, 1e-9):
+        out = ttround.tt_round(fat, tol)
+        ref = ttsvd.tt_svd(H, tol)
+        assert ttmv.ranks_of(out) == ttmv.ranks_of(ref), (tol, ttmv.ranks_of(out), ttmv.ranks_of(ref))
+        assert np.linalg.norm(ttmv.full(out) - H) <= tol * np.linalg.norm(H)
+
+
+def test_P38_orthogonalization_invariants():
+    cores = _rand_tt((5, 6, 7, 11), (3, 4, 5), 39)
+    T = ttmv.full(cores)
+    G = ttround.orthogonalize_rl(cores)
+    assert np.linalg.norm(ttmv.full(G) - T) <= 1e-13 * np.linalg.norm(T)
+    for k in range(1, 4):
+        a, n, b = G[k].shape
+        R = G[k].reshape((a, n * b), order="F")
+        assert np.allclose(R @ R.conj().T, np.eye(a), atol=1e-13)
+    assert abs(np.linalg.norm(G[0]) - np.linalg.norm(T)) <= 1e-13 * np.linalg.norm(T)
+    # Gram-chain norm / inner product / difference vs the dense tensor
+    other = _rand_tt((5, 6, 7, 11), (2, 2, 3), 40)
+    T2 = ttmv.full(other)
+    assert abs(ttround.tt_norm(cores) - np.linalg.norm(T)) <= 1e-12 * np.linalg.norm(T)
+    assert abs(ttround.tt_inner(cores, other) - np.vdot(T2, T)) <= 1e-12 * np.linalg.norm(T) * np.linalg.norm(T2)
+    assert abs(ttround.tt_diff_norm(cores, other) - np.linalg.norm(T - T2)) <= 1e-10 * np.linalg.norm(T)
+
+
+def test_P39_round_special_cases_and_idempotence():
+    dims = (5, 6, 7, 8)
+    vs = [np.random.default_rng(k).normal(size=d) + 1j for k, d in enumerate(dims)]
+    rank1 = _inflate([v.reshape((1, -1, 1)).astype(complex) for v in vs], 4, 41)
+    out = ttround.tt_round(rank1, 1e-12)
+    assert ttmv.ranks_of(out) == (1, 1, 1)
+    S = np.einsum("i,j,k,l->ijkl", *vs)
+    assert np.linalg.norm(ttmv.full(out) - S) <= 1e-13 * np.linalg.norm(S)
+    zero = [np.zeros((1 if k == 0 else 3, d, 1 if k == 3 else 3), complex) for k, d in enumerate(dims)]
+    z = ttround.tt_round(zero, 1e-6)
+    assert ttmv.ranks_of(z) == (1, 1, 1) and np.all(ttmv.full(z) == 0)
+    cores = _rand_tt(dims, (3, 4, 3), 42)
+    once = ttround.tt_round(cores, 1e-8)
+    twice = ttround.tt_round(once, 1e-8)
+    assert ttmv.ranks_of(once) == ttmv.ranks_of(twice)
+    T1 = ttmv.full(once)
+    assert np.linalg.norm(ttmv.full(twice) - T1) <= 1e-12 * np.linalg.norm(T1)
