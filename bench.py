@@ -233,6 +233,9 @@ def main():
     ap.add_argument("--cores", default="auto", choices=["auto", "build", "random"],
                     help="build = TT-cross build (default for configs 1, 2, 4); random = seeded cores at the "
                          "ranks of the recorded build (configs 3, 5: the build takes minutes)")
+    ap.add_argument("--round", type=float, default=None, metavar="TOL",
+                    help="TT-round the cores (vsie_coupling_round, SURVEY 8f NEXT-1) at TOL before timing "
+                         "(single process only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--separate", action="store_true",
                     help="time the step as two vsie_coupling_apply calls instead of vsie_coupling_apply_pair")
@@ -269,6 +272,13 @@ def main():
         h = Coupling.from_cores(grid_of(cfg), cfg.meshes(), cfg.freq, device_cores(cfg, ranks0, 7, dev), nrhs_max=k,
                                 rank=rank, world=world, nccl_unique_id=uid, device=local)
     build_s = time.perf_counter() - t0
+    round_info = None
+    if args.round is not None:
+        assert world == 1, "--round needs a single-process handle"
+        r_before = h.info()["ranks"]
+        t1 = time.perf_counter()
+        h.round(args.round)
+        round_info = {"tol": args.round, "ranks_before": r_before, "round_s": time.perf_counter() - t1}
     inf = h.info()
     ranks = inf["ranks"]
     if rank == 0:
@@ -486,6 +496,7 @@ def main():
                    "cores": ("TT-cross build on this GPU" if mode == "build"
                              else "seeded random cores at the ranks of the recorded B200 build (profiles/)"),
                    "ranks": ranks,
+                   "rounded": round_info,
                    "parallelism": f"slab{world} (i3 planes + G4 columns, NCCL)" if world > 1 else "1 GPU",
                    "l2": "flushed between timed steps (512 MiB write)",
                    "bytes_per_step": B, "flops_per_step": F, "build_s": build_s,

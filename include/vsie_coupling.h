@@ -163,11 +163,25 @@ int32_t vsie_coupling_import_cores(const vsie_grid* grid, const vsie_mesh* meshe
                                    const void* const host_cores[12], const vsie_build_opts* opts,
                                    vsie_coupling_t* out);
 
-/* Copy core k (0..3) of component chi (0..2) to host (full core; all ranks
- * must call it together when world > 1).  With host_dst == NULL only
- * *nelems is written. */
+/* Copy core k (0..3) of component chi (0..2) to host (full core, assembled from
+ * the loopback shards).  Single-process handles only (VSIE_ERR_STATE for a
+ * multi-process handle, whose ranks hold only their slabs).  With host_dst ==
+ * NULL only *nelems is written. */
 int32_t vsie_coupling_export_cores(vsie_coupling_t h, int32_t chi, int32_t k, void* host_dst,
                                    int64_t* nelems);
+
+/* TT rounding (recompression) of the handle's cores in place: SURVEY §8(f) NEXT-1,
+ * motivated by PAPER.md P:389 ("[cross] might overestimate the TT-ranks") and built
+ * from the unfolding SVDs of P:126 (TT-SVD of the tensor already in TT form, the
+ * "TT-rounding" of the cited Oseledets 2011; restated in oracle/ttround.py):
+ * right-to-left orthogonalisation of cores 4..2, then left-to-right truncated SVDs
+ * with per-bond threshold tol / sqrt(3) * ||Z~chi||_F, so that the rounded TT is
+ * within tol ||Z~chi||_F of the unrounded one for each chi, at the TT-SVD ranks of
+ * that tensor.  tol in [0, 1); tol = 0 removes only numerically redundant ranks
+ * (singular values <= 1e-14 of the largest).  Synchronous; afterwards vsie_info
+ * reports the new ranks and previously captured apply graphs are dropped.
+ * Single-process handles only (world 1 or loopback): VSIE_ERR_STATE otherwise. */
+int32_t vsie_coupling_round(vsie_coupling_t h, double tol);
 
 /* Apply the TT operator on `stream` (cudaStream_t, NULL = legacy default).
  *  OP_N: x = device complex128 [m x nrhs] (column-major, ld = m, replicated on

@@ -75,6 +75,7 @@ _SIGS = {
                                                C.POINTER(C.c_int32), C.POINTER(C.c_void_p),
                                                C.POINTER(vsie_build_opts), C.POINTER(HANDLE)]),
     "vsie_coupling_export_cores": (C.c_int32, [HANDLE, C.c_int32, C.c_int32, C.c_void_p, C.POINTER(C.c_int64)]),
+    "vsie_coupling_round": (C.c_int32, [HANDLE, C.c_double]),
     "vsie_coupling_apply": (C.c_int32, [HANDLE, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
     "vsie_coupling_apply_host": (C.c_int32, [HANDLE, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32]),
     "vsie_coupling_entries": (C.c_int32, [HANDLE, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),

@@ -181,6 +181,13 @@ class Coupling:
             out.append(cs)
         return out
 
+    def round(self, tol: float):
+        """vsie_coupling_round: TT rounding of the cores in place.
+
+        Returns the new ranks [chi][k]."""
+        check(lib().vsie_coupling_round(self._h, float(tol)))
+        return [tuple(r) for r in self.info()["ranks"]]
+
     # ------------------------------------------------------------------ compute
     def apply(self, x, op: str = "N", out=None, stream=None):
         """vsie_coupling_apply on device tensors (complex128, column-major RHS blocks).

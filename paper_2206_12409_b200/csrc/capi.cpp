@@ -186,6 +186,13 @@ int32_t vsie_coupling_export_cores(vsie_coupling_t h, int32_t chi, int32_t k, vo
   });
 }
 
+int32_t vsie_coupling_round(vsie_coupling_t h, double tol) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "handle is NULL");
+    return tt_round(h, tol);
+  });
+}
+
 int32_t vsie_coupling_apply(vsie_coupling_t h, const void* x, void* y, int32_t op, int32_t nrhs, void* stream) {
   return guarded([&] {
     VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "handle is NULL");

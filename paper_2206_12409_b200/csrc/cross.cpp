@@ -712,7 +712,167 @@ int cross_chi(Ctx& c, int chi, Heldout& ho) {
   return best_e <= 10 * c.tol ? VSIE_OK : VSIE_WARN_NOT_CONVERGED;
 }
 
+// ------------------------------------------------------------------ TT rounding
+// the cross "might overestimate the TT-ranks";
+// rounding = the TT-SVD of the tensor the cores already represent, done on
+// the cores (algorithm of the cited [Oseledets 2011]; oracle/ttround.py restates it):
+//   1. right-to-left, k = 3..1: core_k^T (as (n_k r_k) x r_{k-1}) = Q R, core_k <- Q^T,
+//      core_{k-1} <- core_{k-1} R^T.  Q R comes from the Jacobi SVD X = (X V) V^H:
+//      Q = (X V) S^{-1} over the numerically non-zero columns, R = S V^H (so R^T =
+//      conj(V) S).  After this ||A||_F = ||core_0||_F.
+//   2. left-to-right, k = 0..2: core_k (as (r_{k-1} n_k) x r_k) = U S V^H, keep the
+//      smallest r with ||S[r:]|| <= tol / sqrt 3 ||A||_F, core_k <- U_r,
+//      core_{k+1} <- S_r V_r^H core_{k+1}.
+// cores: full column-major cores of one chi (core_k is r_{k-1} x n_k x r_k); r[0..2] the
+// inner ranks; both are replaced.
+void round_chi(Ctx& c, const int n[4], int r[3], DevBuf<cplx> core[4]) {
+  Ws& w = c.ws;
+  int rk[5] = {1, r[0], r[1], r[2], 1};
+  // kept columns (and their scales) of a Jacobi-orthogonalised X (p x q, columns U S)
+  auto select = [&](const cplx* X, int64_t p, int q, bool truncate, double abs2) {
+    auto s = sorted_norms(c, X, p, q);
+    int keep;
+    if (truncate) {
+      keep = q;
+      std::vector<double> tail(q + 1, 0.0);
+      for (int j = q - 1; j >= 0; --j) tail[j] = tail[j + 1] + s[j].first * s[j].first;
+      for (int k = 1; k <= q; ++k)
+        if (tail[k] <= abs2) { keep = k; break; }
+    } else {
+      keep = 0;
+      for (auto& e : s)
+        if (e.first > 1e-14 * s[0].first) ++keep;
+    }
+    keep = std::max(keep, 1);
+    s.resize(keep);
+    return s;
+  };
+  auto upload_scales = [&](const std::vector<double>& v) {
+    w.norms.ensure(std::max<size_t>(1, v.size()));
+    VSIE_CHECK_CUDA(cudaMemcpyAsync(w.norms.p, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice, c.st));
+  };
+  DevBuf<cplx> nxt;
+  // ---- 1. right-to-left orthogonalisation
+  for (int k = 3; k >= 1; --k) {
+    const int64_t a = rk[k], nb = (int64_t)n[k] * rk[k + 1];
+    const int q = (int)a;
+    w.J.ensure(nb * a);
+    launch_transpose(core[k].p, a, nb, w.J.p, false, c.st);  // X = core_k^T: (n_k r_k) x r_{k-1}
+    w.V.ensure((int64_t)q * q);
+    precond_jacobi(c, w.J.p, nb, q, w.V.p);
+    auto s = select(w.J.p, nb, q, false, 0);
+    const int rp = (int)s.size();
+    std::vector<int> sel(rp);
+    std::vector<double> inv(rp), sv(rp);
+    for (int j = 0; j < rp; ++j) {
+      sel[j] = s[j].second;
+      sv[j] = s[j].first;
+      inv[j] = s[j].first > 0 ? 1.0 / s[j].first : 0.0;
+    }
+    upload_idx(c, sel);
+    upload_scales(inv);
+    w.Q.ensure(nb * rp);
+    launch_gather_cols(w.J.p, nb, nb, c.ws.idx.p, w.norms.p, rp, w.Q.p, nb, false, c.st);  // Q = (X V) S^-1
+    nxt.alloc(rp * nb);
+    launch_transpose(w.Q.p, nb, rp, nxt.p, false, c.st);                                  // core_k <- Q^T
+    std::swap(core[k], nxt);
+    upload_scales(sv);
+    w.Vr.ensure((int64_t)q * rp);
+    launch_gather_cols(w.V.p, q, q, c.ws.idx.p, w.norms.p, rp, w.Vr.p, q, true, c.st);   // R^T = conj(V) S
+    const int64_t rows = (int64_t)rk[k - 1] * n[k - 1];
+    nxt.alloc(rows * rp);
+    zgemm1(c, kN, kN, rows, rp, a, core[k - 1].p, rows, w.Vr.p, q, nxt.p, rows);         // core_{k-1} R^T
+    std::swap(core[k - 1], nxt);
+    rk[k] = rp;
+    sync(c);
+  }
+  // ---- 2. left-to-right truncation, delta = tol / sqrt(d - 1) ||A||_F, d = 4
+  w.frob_partial.ensure(1024);
+  w.frob.ensure(1);
+  launch_frob2(core[0].p, (int64_t)n[0] * rk[1], w.frob_partial.p, w.frob.p, c.st);
+  double nrm2 = 0;
+  VSIE_CHECK_CUDA(cudaMemcpyAsync(&nrm2, w.frob.p, sizeof(double), cudaMemcpyDeviceToHost, c.st));
+  sync(c);
+  const double abs2 = c.tol * c.tol / 3.0 * nrm2;
+  for (int k = 0; k < 3; ++k) {
+    const int64_t rows = (int64_t)rk[k] * n[k];
+    const int q = rk[k + 1];
+    w.J.ensure(rows * q);
+    VSIE_CHECK_CUDA(cudaMemcpyAsync(w.J.p, core[k].p, rows * q * sizeof(cplx), cudaMemcpyDeviceToDevice, c.st));
+    w.V.ensure((int64_t)q * q);
+    precond_jacobi(c, w.J.p, rows, q, w.V.p);
+    auto s = nrm2 > 0 ? select(w.J.p, rows, q, true, abs2) : select(w.J.p, rows, q, false, 0);
+    const int rp = (int)s.size();
+    std::vector<int> sel(rp);
+    std::vector<double> inv(rp), sv(rp);
+    for (int j = 0; j < rp; ++j) {
+      sel[j] = s[j].second;
+      sv[j] = s[j].first;
+      inv[j] = s[j].first > 0 ? 1.0 / s[j].first : 0.0;
+    }
+    upload_idx(c, sel);
+    upload_scales(inv);
+    nxt.alloc(rows * rp);
+    launch_gather_cols(w.J.p, rows, rows, c.ws.idx.p, w.norms.p, rp, nxt.p, rows, false, c.st);  // U_r
+    std::swap(core[k], nxt);
+    upload_scales(sv);
+    w.Vr.ensure((int64_t)q * rp);
+    launch_gather_cols(w.V.p, q, q, c.ws.idx.p, w.norms.p, rp, w.Vr.p, q, false, c.st);  // V_r S_r
+    const int64_t ncols = (int64_t)n[k + 1] * rk[k + 2];
+    nxt.alloc(rp * ncols);
+    zgemm1(c, kC, kN, rp, ncols, q, w.Vr.p, q, core[k + 1].p, q, nxt.p, rp);  // S_r V_r^H core_{k+1}
+    std::swap(core[k + 1], nxt);
+    rk[k + 1] = rp;
+    sync(c);
+  }
+  r[0] = rk[1];
+  r[1] = rk[2];
+  r[2] = rk[3];
+}
+
 }  // namespace
+
+int tt_round(vsie_coupling_s* h, double tol) {
+  VSIE_REQUIRE(h->has_cores, VSIE_ERR_STATE, "handle has no TT cores");
+  VSIE_REQUIRE(h->comm == nullptr, VSIE_ERR_STATE,
+               "round of a multi-process handle: round the full cores before sharding");
+  VSIE_REQUIRE(tol >= 0 && tol < 1, VSIE_ERR_ARG, "tol must be in [0, 1)");
+  vsie_build_opts o{};
+  Ctx c{h, o, nullptr, {}, tol, tol / std::sqrt(3.0), 0};
+  VSIE_CHECK_CUDA(cudaDeviceSynchronize());
+  VSIE_CHECK_CUDA(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() { cudaStreamDestroy(s); }
+  } guard{c.st};
+  const int n[4] = {h->grid.n[0], h->grid.n[1], h->grid.n[2], (int)h->m};
+  for (int chi = 0; chi < 3; ++chi) {
+    int r[3] = {h->ranks[chi][0], h->ranks[chi][1], h->ranks[chi][2]};
+    DevBuf<cplx> core[4];
+    // assemble the full cores (G3 / G4 may be split over loopback shards)
+    core[0].alloc((size_t)n[0] * r[0]);
+    core[1].alloc((size_t)r[0] * n[1] * r[1]);
+    core[2].alloc((size_t)r[1] * n[2] * r[2]);
+    core[3].alloc((size_t)r[2] * n[3]);
+    VSIE_CHECK_CUDA(cudaMemcpy(core[0].p, h->G1[chi].p, core[0].bytes(), cudaMemcpyDeviceToDevice));
+    VSIE_CHECK_CUDA(cudaMemcpy(core[1].p, h->G2[chi].p, core[1].bytes(), cudaMemcpyDeviceToDevice));
+    for (const Shard& s : h->shards) {
+      const int64_t r2 = r[1], r3 = r[2], n3l = s.n3loc();
+      if (n3l > 0)
+        VSIE_CHECK_CUDA(cudaMemcpy2D(core[2].p + r2 * s.i3b, r2 * n[2] * sizeof(cplx), s.G3[chi].p,
+                                     r2 * n3l * sizeof(cplx), r2 * n3l * sizeof(cplx), r3, cudaMemcpyDeviceToDevice));
+      if (s.mloc() > 0)
+        VSIE_CHECK_CUDA(cudaMemcpy(core[3].p + r3 * s.cb, s.G4[chi].p, r3 * s.mloc() * sizeof(cplx),
+                                   cudaMemcpyDeviceToDevice));
+    }
+    round_chi(c, n, r, core);
+    const cplx* dev[4] = {core[0].p, core[1].p, core[2].p, core[3].p};
+    handle_set_cores_device(h, chi, r, dev);
+  }
+  handle_alloc_workspace(h);
+  VSIE_CHECK_CUDA(cudaDeviceSynchronize());
+  return VSIE_OK;
+}
 
 int cross_build(vsie_coupling_s* h, double tol, const vsie_build_opts& o) {
   Ctx c{h, o, nullptr, {}, tol, tol / std::sqrt(3.0), o.seed};

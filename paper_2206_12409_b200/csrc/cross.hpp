@@ -9,4 +9,8 @@ namespace vsie {
 // kernel.  Returns VSIE_OK or VSIE_WARN_NOT_CONVERGED; throws on errors.
 int cross_build(vsie_coupling_s* h, double tol, const vsie_build_opts& o);
 
+// TT rounding (recompression) of the handle's cores in place, relative Frobenius
+// accuracy tol per chi (algorithm in cross.cpp).  World 1 / loopback.
+int tt_round(vsie_coupling_s* h, double tol);
+
 }  // namespace vsie

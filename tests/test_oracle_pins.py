@@ -15,6 +15,7 @@ import numpy as np
 import pytest
 
 import synth
+from gpu_common import inflate as _inflate
 from oracle import entries, geometry, greens, maxvol, ttcross, ttmv, ttround, ttsvd, validate
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
@@ -545,21 +546,6 @@ def test_T1_entry_parity_metric():
 
 
 # ---------------------------------------------------------------- TT rounding (§8f NEXT-1)
-
-def _inflate(cores, extra, seed):
-    """Same tensor with each inner rank grown by `extra` (redundant directions):
-    G_k <- [G_k, G_k M_k] on the right, G_{k+1} <- [G_{k+1}; 0] on the left."""
-    rng = np.random.default_rng(seed)
-    G = [np.array(c) for c in cores]
-    for k in range(len(G) - 1):
-        a, n, b = G[k].shape
-        M = rng.normal(size=(b, extra)) + 1j * rng.normal(size=(b, extra))
-        L = G[k].reshape((a * n, b), order="F")
-        G[k] = np.concatenate([L, L @ M], axis=1).reshape((a, n, b + extra), order="F")
-        b2, n2, c2 = G[k + 1].shape
-        G[k + 1] = np.concatenate([G[k + 1], np.zeros((extra, n2, c2), complex)], axis=0)
-    return G
-
 
 def test_P36_round_recovers_inflated_ranks():
     # a TT padded with redundant (linearly dependent) rank directions is the same tensor;
