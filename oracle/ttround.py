@@ -72,12 +72,18 @@ def tt_round(cores, tol):
     return G
 
 
+def _gram_step(M, Ga, Gb):
+    """M'[c, d] = sum_{a, b, i} M[a, b] Ga[a, i, c] conj(Gb[b, i, d]) (two pairwise
+    contractions: the single 5-index einsum would loop over all indices at once)."""
+    T = np.tensordot(M, Ga, axes=([0], [0]))                # (b, i, c)
+    return np.tensordot(T, np.conj(Gb), axes=([0, 1], [0, 1]))  # (c, d)
+
+
 def tt_norm(cores):
     """||A||_F of a TT by contracting the Gram chain (no dense expansion)."""
     M = np.ones((1, 1), dtype=np.complex128)
     for G in cores:
-        # M'[b, b'] = sum_{a, a', i} M[a, a'] G[a, i, b] conj(G[a', i, b'])
-        M = np.einsum("ab,aic,bid->cd", M, G, np.conj(G))
+        M = _gram_step(M, G, G)
     return float(np.sqrt(abs(M[0, 0].real)))
 
 
@@ -85,13 +91,31 @@ def tt_inner(cores_a, cores_b):
     """<A, B> = sum A conj(B) of two TTs of equal dims."""
     M = np.ones((1, 1), dtype=np.complex128)
     for Ga, Gb in zip(cores_a, cores_b):
-        M = np.einsum("ab,aic,bid->cd", M, Ga, np.conj(Gb))
+        M = _gram_step(M, Ga, Gb)
     return complex(M[0, 0])
 
 
+def tt_sum(cores_a, cores_b, beta=1.0):
+    """TT of A + beta B: block cores [A1 B1], diag(A_k, B_k), [A_d; beta B_d]."""
+    d = len(cores_a)
+    out = []
+    for k, (Ga, Gb) in enumerate(zip(cores_a, cores_b)):
+        a1, n, b1 = Ga.shape
+        a2, _, b2 = Gb.shape
+        if k == 0:
+            out.append(np.concatenate([Ga, Gb], axis=2))
+        elif k == d - 1:
+            out.append(np.concatenate([Ga, beta * Gb], axis=0))
+        else:
+            G = np.zeros((a1 + a2, n, b1 + b2), dtype=np.complex128)
+            G[:a1, :, :b1] = Ga
+            G[a1:, :, b1:] = Gb
+            out.append(G)
+    return out
+
+
 def tt_diff_norm(cores_a, cores_b):
-    """||A - B||_F from Gram chains: sqrt(|A|^2 + |B|^2 - 2 Re<A, B>)."""
-    na2 = tt_norm(cores_a) ** 2
-    nb2 = tt_norm(cores_b) ** 2
-    v = na2 + nb2 - 2.0 * tt_inner(cores_a, cores_b).real
-    return float(np.sqrt(max(v, 0.0)))
+    """||A - B||_F: the TT of A - B orthogonalised right-to-left (QR, backward stable),
+    then ||core_1||_F.  (The Gram identity |A|^2 + |B|^2 - 2 Re<A, B> would lose half
+    the digits to cancellation when A and B are close.)"""
+    return float(np.linalg.norm(orthogonalize_rl(tt_sum(cores_a, cores_b, -1.0))[0]))

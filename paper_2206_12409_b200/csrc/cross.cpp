@@ -19,6 +19,7 @@
 #include <array>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <map>
 #include <numeric>
 #include <set>
@@ -762,6 +763,9 @@ void round_chi(Ctx& c, const int n[4], int r[3], DevBuf<cplx> core[4]) {
     precond_jacobi(c, w.J.p, nb, q, w.V.p);
     auto s = select(w.J.p, nb, q, false, 0);
     const int rp = (int)s.size();
+    if (c.o.verbose)
+      fprintf(stderr, "[vsie round] R->L k=%d X %ldx%d kept %d s[0] %.6e s[last] %.6e\n", k, (long)nb, q, rp,
+              s[0].first, s.back().first);
     std::vector<int> sel(rp);
     std::vector<double> inv(rp), sv(rp);
     for (int j = 0; j < rp; ++j) {
@@ -803,6 +807,9 @@ void round_chi(Ctx& c, const int n[4], int r[3], DevBuf<cplx> core[4]) {
     precond_jacobi(c, w.J.p, rows, q, w.V.p);
     auto s = nrm2 > 0 ? select(w.J.p, rows, q, true, abs2) : select(w.J.p, rows, q, false, 0);
     const int rp = (int)s.size();
+    if (c.o.verbose)
+      fprintf(stderr, "[vsie round] L->R k=%d core %ldx%d ||A||^2 %.6e kept %d s[0] %.6e s[last] %.6e\n", k,
+              (long)rows, q, nrm2, rp, s[0].first, s.back().first);
     std::vector<int> sel(rp);
     std::vector<double> inv(rp), sv(rp);
     for (int j = 0; j < rp; ++j) {
@@ -838,6 +845,8 @@ int tt_round(vsie_coupling_s* h, double tol) {
                "round of a multi-process handle: round the full cores before sharding");
   VSIE_REQUIRE(tol >= 0 && tol < 1, VSIE_ERR_ARG, "tol must be in [0, 1)");
   vsie_build_opts o{};
+  const char* ev = std::getenv("VSIE_ROUND_VERBOSE");
+  o.verbose = ev ? std::atoi(ev) : 0;
   Ctx c{h, o, nullptr, {}, tol, tol / std::sqrt(3.0), 0};
   VSIE_CHECK_CUDA(cudaDeviceSynchronize());
   VSIE_CHECK_CUDA(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking));
@@ -849,25 +858,29 @@ int tt_round(vsie_coupling_s* h, double tol) {
   for (int chi = 0; chi < 3; ++chi) {
     int r[3] = {h->ranks[chi][0], h->ranks[chi][1], h->ranks[chi][2]};
     DevBuf<cplx> core[4];
-    // assemble the full cores (G3 / G4 may be split over loopback shards)
+    // assemble the full cores (G3 / G4 may be split over loopback shards) on c.st (a
+    // non-blocking stream: plain cudaMemcpy D2D would not be ordered before its kernels)
     core[0].alloc((size_t)n[0] * r[0]);
     core[1].alloc((size_t)r[0] * n[1] * r[1]);
     core[2].alloc((size_t)r[1] * n[2] * r[2]);
     core[3].alloc((size_t)r[2] * n[3]);
-    VSIE_CHECK_CUDA(cudaMemcpy(core[0].p, h->G1[chi].p, core[0].bytes(), cudaMemcpyDeviceToDevice));
-    VSIE_CHECK_CUDA(cudaMemcpy(core[1].p, h->G2[chi].p, core[1].bytes(), cudaMemcpyDeviceToDevice));
+    VSIE_CHECK_CUDA(cudaMemcpyAsync(core[0].p, h->G1[chi].p, core[0].bytes(), cudaMemcpyDeviceToDevice, c.st));
+    VSIE_CHECK_CUDA(cudaMemcpyAsync(core[1].p, h->G2[chi].p, core[1].bytes(), cudaMemcpyDeviceToDevice, c.st));
     for (const Shard& s : h->shards) {
       const int64_t r2 = r[1], r3 = r[2], n3l = s.n3loc();
       if (n3l > 0)
-        VSIE_CHECK_CUDA(cudaMemcpy2D(core[2].p + r2 * s.i3b, r2 * n[2] * sizeof(cplx), s.G3[chi].p,
-                                     r2 * n3l * sizeof(cplx), r2 * n3l * sizeof(cplx), r3, cudaMemcpyDeviceToDevice));
+        VSIE_CHECK_CUDA(cudaMemcpy2DAsync(core[2].p + r2 * s.i3b, r2 * n[2] * sizeof(cplx), s.G3[chi].p,
+                                          r2 * n3l * sizeof(cplx), r2 * n3l * sizeof(cplx), r3,
+                                          cudaMemcpyDeviceToDevice, c.st));
       if (s.mloc() > 0)
-        VSIE_CHECK_CUDA(cudaMemcpy(core[3].p + r3 * s.cb, s.G4[chi].p, r3 * s.mloc() * sizeof(cplx),
-                                   cudaMemcpyDeviceToDevice));
+        VSIE_CHECK_CUDA(cudaMemcpyAsync(core[3].p + r3 * s.cb, s.G4[chi].p, r3 * s.mloc() * sizeof(cplx),
+                                        cudaMemcpyDeviceToDevice, c.st));
     }
     round_chi(c, n, r, core);
     const cplx* dev[4] = {core[0].p, core[1].p, core[2].p, core[3].p};
+    sync(c);
     handle_set_cores_device(h, chi, r, dev);
+    VSIE_CHECK_CUDA(cudaDeviceSynchronize());
   }
   handle_alloc_workspace(h);
   VSIE_CHECK_CUDA(cudaDeviceSynchronize());
