@@ -94,12 +94,24 @@ struct Ctx {
   int r1m, r2m, r3m;
   int64_t r3stride;  // r3m * k
   IoLayout L;
-  cplx* partials(int c) const { return h->partials.p + c * h->partials_per_chi; }
-  cplx* zws(int c) const { return h->zgemm_ws.p + c * h->zgemm_ws_per_chi; }
+  int ws = 0;       // 0: forward workspaces, 3: the transpose's (both directions concurrently)
+  cplx* partials(int c) const { return h->partials.p + (c + ws) * h->partials_per_chi; }
+  cplx* zws(int c) const { return h->zgemm_ws.p + (c + ws) * h->zgemm_ws_per_chi; }
   int64_t R(int c, int j) const { return h->ranks[c][j]; }
 };
 
 constexpr int kMaxSplits = 256;
+
+// GMRES pair schedule: 0 = k_gemv_nt per chi chain, 2 = one TMA-streamed launch over the
+// three chi (k_pair_g4, chi sum of Eq. 18 fused), 3 = forward and transpose as six
+// independent concurrent chains (single shard only); VSIE_PAIR_G4 overrides
+int pair_g4_mode() {
+  static const int v = [] {
+    const char* e = std::getenv("VSIE_PAIR_G4");
+    return e ? std::atoi(e) : 2;
+  }();
+  return v;
+}
 
 bool fuse_g21() {
   // fused G2 + G1 forward tail (k_g21_fwd): measured 0.173 vs 0.167 ms per pair step at
@@ -240,7 +252,7 @@ void adj_front(const Ctx& X, Shard& s, int c, const cplx* u, bool cj, cudaStream
     return;
   }
   const int64_t r1 = X.R(c, 0), r2 = X.R(c, 1), r3 = X.R(c, 2);
-  cplx* W1 = s.Y2.p + c * X.r1m * n2 * n3l * k;
+  cplx* W1 = s.W1.p + c * X.r1m * n2 * n3l * k;
   cplx* W2 = s.W2.p + c * X.r2m * n3l * k;
   {
     ReduceArgs r{};
@@ -381,6 +393,8 @@ void ensure_streams(vsie_coupling_s* h) {
     if (!prio_on) prio = least;
     VSIE_CHECK_CUDA(cudaStreamCreateWithPriority(&h->chi_stream[c], cudaStreamNonBlocking, prio));
     VSIE_CHECK_CUDA(cudaEventCreateWithFlags(&h->ev_join[c], cudaEventDisableTiming));
+    VSIE_CHECK_CUDA(cudaStreamCreateWithPriority(&h->chi_stream2[c], cudaStreamNonBlocking, prio));
+    VSIE_CHECK_CUDA(cudaEventCreateWithFlags(&h->ev_join2[c], cudaEventDisableTiming));
   }
   VSIE_CHECK_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
   for (int c = 0; c < 3; ++c) VSIE_CHECK_CUDA(cudaEventCreateWithFlags(&h->ev_stage[c], cudaEventDisableTiming));
@@ -391,20 +405,34 @@ struct Streams {
   cudaStream_t main;
   cudaStream_t chi[3];
   bool parallel;
+  cudaStream_t chi2[3];   // second chain set (set only where a DAG uses it)
 };
 
-void fork(vsie_coupling_s* h, const Streams& S) {
+Streams make_streams(vsie_coupling_s* h, cudaStream_t main, bool parallel) {
+  if (!parallel) return Streams{main, {main, main, main}, false, {main, main, main}};
+  return Streams{main, {h->chi_stream[0], h->chi_stream[1], h->chi_stream[2]}, true,
+                 {h->chi_stream2[0], h->chi_stream2[1], h->chi_stream2[2]}};
+}
+
+void fork(vsie_coupling_s* h, const Streams& S, bool both = false) {
   if (!S.parallel) return;
   VSIE_CHECK_CUDA(cudaEventRecord(h->ev_fork, S.main));
   for (int c = 0; c < 3; ++c) VSIE_CHECK_CUDA(cudaStreamWaitEvent(S.chi[c], h->ev_fork, 0));
+  if (both)
+    for (int c = 0; c < 3; ++c) VSIE_CHECK_CUDA(cudaStreamWaitEvent(S.chi2[c], h->ev_fork, 0));
 }
 
-void join(vsie_coupling_s* h, const Streams& S) {
+void join(vsie_coupling_s* h, const Streams& S, bool both = false) {
   if (!S.parallel) return;
   for (int c = 0; c < 3; ++c) {
     VSIE_CHECK_CUDA(cudaEventRecord(h->ev_join[c], S.chi[c]));
     VSIE_CHECK_CUDA(cudaStreamWaitEvent(S.main, h->ev_join[c], 0));
   }
+  if (both)
+    for (int c = 0; c < 3; ++c) {
+      VSIE_CHECK_CUDA(cudaEventRecord(h->ev_join2[c], S.chi2[c]));
+      VSIE_CHECK_CUDA(cudaStreamWaitEvent(S.main, h->ev_join2[c], 0));
+    }
 }
 
 // ------------------------------------------------------------------ persistent single-RHS apply
@@ -823,6 +851,8 @@ void apply_destroy(vsie_coupling_s* h) {
   for (int c = 0; c < 3; ++c) {
     if (h->chi_stream[c]) cudaStreamDestroy(h->chi_stream[c]);
     if (h->ev_join[c]) cudaEventDestroy(h->ev_join[c]);
+    if (h->chi_stream2[c]) cudaStreamDestroy(h->chi_stream2[c]);
+    if (h->ev_join2[c]) cudaEventDestroy(h->ev_join2[c]);
   }
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   for (int c = 0; c < 3; ++c)
@@ -846,7 +876,7 @@ void run_dag(vsie_coupling_s* h, int op, int nrhs, const void* x, void* y, const
     h->origins.push_back(o);
     VSIE_CHECK_CUDA(cudaEventRecord(o, st));
     h->trace_origin = o;
-    Streams S{st, {h->chi_stream[0], h->chi_stream[1], h->chi_stream[2]}, true};
+    Streams S = make_streams(h, st, true);
     const int64_t before = launch_counter();
     dag(S);
     h->apply_launches += launch_counter() - before;
@@ -872,7 +902,7 @@ void run_dag(vsie_coupling_s* h, int op, int nrhs, const void* x, void* y, const
     // per-kernel CUDA-event timing: the same DAG serialised on one stream, captured with
     // its event records into a one-shot graph so that host submission gaps do not enter
     // the per-kernel durations
-    Streams S{h->cap_stream, {h->cap_stream, h->cap_stream, h->cap_stream}, false};
+    Streams S = make_streams(h, h->cap_stream, false);
     int64_t launches = 0;
     cudaGraph_t graph = capture(S, launches);
     cudaGraphExec_t exec = nullptr;
@@ -886,7 +916,7 @@ void run_dag(vsie_coupling_s* h, int op, int nrhs, const void* x, void* y, const
     return;
   }
   if (!graphs_enabled(h)) {
-    Streams S{st, {h->chi_stream[0], h->chi_stream[1], h->chi_stream[2]}, true};
+    Streams S = make_streams(h, st, true);
     const int64_t before = launch_counter();
     dag(S);
     h->apply_launches += launch_counter() - before;
@@ -909,7 +939,7 @@ void run_dag(vsie_coupling_s* h, int op, int nrhs, const void* x, void* y, const
     g.y = y;
     g.u = u;
     g.z = z;
-    Streams S{h->cap_stream, {h->chi_stream[0], h->chi_stream[1], h->chi_stream[2]}, true};
+    Streams S = make_streams(h, h->cap_stream, true);
     cudaGraph_t graph = capture(S, g.launches);
     cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
     cudaGraphDestroy(graph);
@@ -939,6 +969,26 @@ void pair_dag(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z
   X.r3stride = X.r3m;
   X.L = voxel_layout(h);
   const bool exchange = h->comm != nullptr || h->shards.size() > 1;
+  const int64_t m = h->m, mp = ceil_div(m, h->world);
+  if (pair_g4_mode() == 3 && !exchange) {
+    // both directions as six independent chains (transpose chains on S.chi, forward chains
+    // on S.chi2, separate workspaces): G4 is read twice but no chain waits for another
+    Ctx XA = X;
+    XA.ws = 3;
+    Shard& s = h->shards[0];
+    fork(h, S, true);
+    for (int c = 0; c < 3; ++c) {
+      h->scope_chi = c;
+      adj_front(XA, s, c, u, cj, S.chi[c]);
+      adj_g4(XA, s, c, S.chi[c]);
+      fwd_g4(X, s, c, x, S.chi2[c]);
+      fwd_rest(X, s, c, y, S.chi2[c]);
+    }
+    h->scope_chi = -1;
+    join(h, S, true);
+    adj_sum_chi(X, s, z + s.cb, m, cj, S.main);
+    return;
+  }
   fork(h, S);
   for (int c = 0; c < 3; ++c) {
     h->scope_chi = c;
@@ -949,6 +999,40 @@ void pair_dag(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z
     combine_r3(h, &Shard::z3, 3 * X.r3stride, S.main);
     fork(h, S);
   }
+  bool z_done = false;
+  if (pair_g4_mode() == 2) {
+    // one TMA-streamed pass over the three G4 cores: y4 (all chi) and z = sum_chi G4^T z3
+    join(h, S);
+    bool ok = true;
+    for (Shard& s : h->shards) {
+      PairG4 g{};
+      g.nbatch = 3;
+      g.C = s.mloc();
+      g.x = x + s.cb;
+      g.z = h->comm ? h->gather_buf.p + (int64_t)h->world * mp : z + s.cb;
+      g.conj_z = cj;
+      g.partials = X.partials(0);
+      g.rstride = X.r3m;
+      for (int c = 0; c < 3; ++c) {
+        g.A[c] = s.G4[c].p;
+        g.z3[c] = s.z3.p + c * X.r3stride;
+        g.y4[c] = s.y4.p + c * X.r3stride;
+        g.R[c] = X.R(c, 2);
+      }
+      if (g.C == 0) {
+        VSIE_CHECK_CUDA(cudaMemsetAsync(s.y4.p, 0, 3 * X.r3stride * sizeof(cplx), S.main));
+        continue;
+      }
+      Scope sc(h, "pair_g4_tma", 16 * (X.R(0, 2) + X.R(1, 2) + X.R(2, 2)) * (g.C + 2) + 16 * 2 * g.C,
+               16 * (X.R(0, 2) + X.R(1, 2) + X.R(2, 2)) * g.C, S.main);
+      ok = ok && launch_pair_g4(g, sm_count_dev(), S.main);
+    }
+    VSIE_REQUIRE(ok || h->shards.size() == 1, VSIE_ERR_STATE, "pair_g4 unsupported on a multi-shard handle");
+    z_done = ok;
+    if (z_done && exchange) combine_r3(h, &Shard::y4, 3 * X.r3stride, S.main);
+    fork(h, S);
+  }
+  if (!z_done) {
   for (int c = 0; c < 3; ++c) {
     h->scope_chi = c;
     for (Shard& s : h->shards) {
@@ -984,14 +1068,15 @@ void pair_dag(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z
     combine_r3(h, &Shard::y4, 3 * X.r3stride, S.main);
     fork(h, S);
   }
+  }   // !z_done
   for (int c = 0; c < 3; ++c) {
     h->scope_chi = c;
     for (Shard& s : h->shards) fwd_rest(X, s, c, y, S.chi[c]);
   }
   h->scope_chi = -1;
   join(h, S);
-  const int64_t m = h->m, mp = ceil_div(m, h->world);
   for (Shard& s : h->shards) {
+    if (z_done) break;
     if (h->comm)
       adj_sum_chi(X, s, h->gather_buf.p + (int64_t)h->world * mp, mp, cj, S.main);
     else

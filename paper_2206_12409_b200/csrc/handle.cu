@@ -159,6 +159,7 @@ void handle_alloc_workspace(vsie_coupling_s* h) {
     s.Y3.alloc(3 * (int64_t)r2m * n3l * k);
     s.W2.alloc(3 * (int64_t)r2m * n3l * k);
     s.Y2.alloc(3 * (int64_t)r1m * n2 * n3l * k);
+    s.W1.alloc(3 * (int64_t)r1m * n2 * n3l * k);
     rmax_gemv = std::max(rmax_gemv, (int64_t)r2m * n3l);
   }
   (void)n1;
@@ -166,10 +167,10 @@ void handle_alloc_workspace(vsie_coupling_s* h) {
   // per-chi split-K partials of the GEMVs (the launchers lower the split to fit)
   // and of the ZGEMMs: the three chi chains of an apply run concurrently
   h->partials_per_chi = 400000;
-  h->partials.alloc((size_t)3 * h->partials_per_chi);
+  h->partials.alloc((size_t)6 * h->partials_per_chi);   // [fwd chi 0..2][adj chi 0..2]
   int64_t wsz = 64 * std::max<int64_t>((int64_t)r2m * std::max(1, h->shards[0].n3loc()) * k, (int64_t)r3m * k);
   h->zgemm_ws_per_chi = std::min<int64_t>(wsz, (int64_t)16 << 20);
-  h->zgemm_ws.alloc((size_t)3 * h->zgemm_ws_per_chi);
+  h->zgemm_ws.alloc((size_t)6 * h->zgemm_ws_per_chi);
   // per-chi partial surface vectors of the transpose (z_chi = G4_chi^T z3_chi)
   int64_t mloc_max = 1;
   for (Shard& s : h->shards) mloc_max = std::max<int64_t>(mloc_max, s.mloc());

@@ -22,7 +22,8 @@ struct Shard {
   // apply workspaces (sized for nrhs_max)
   DevBuf<cplx> y4;      // [3][r3max * nrhs]  forward: G4 x partial / reduced
   DevBuf<cplx> Y3;      // [3][r2 * n3loc * nrhs]
-  DevBuf<cplx> Y2;      // [3][r1 * n2 * n3loc * nrhs]   (also W1 in the adjoint)
+  DevBuf<cplx> Y2;      // [3][r1 * n2 * n3loc * nrhs]
+  DevBuf<cplx> W1;      // [3][r1 * n2 * n3loc * nrhs]   (adjoint: G1^T u)
   DevBuf<cplx> W2;      // [3][r2 * n3loc * nrhs]
   DevBuf<cplx> z3;      // [3][r3max * nrhs]
   DevBuf<cplx> zpart;   // [3][mloc_max * nrhs]  transpose: per-chi G4_chi^T z3_chi
@@ -80,6 +81,8 @@ struct vsie_coupling_s {
   int64_t zgemm_ws_per_chi = 0;
   // apply orchestration: one stream per chi chain, fork/join events, graph cache
   cudaStream_t chi_stream[3] = {nullptr, nullptr, nullptr};
+  cudaStream_t chi_stream2[3] = {nullptr, nullptr, nullptr};   // second chain set (pair: fwd beside adj)
+  cudaEvent_t ev_join2[3] = {nullptr, nullptr, nullptr};
   cudaStream_t cap_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev_stage[3] = {nullptr, nullptr, nullptr};   // chain staggering

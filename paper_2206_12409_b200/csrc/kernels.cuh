@@ -78,6 +78,28 @@ struct GemvNT {
 // false when R > 320 (the caller falls back to separate passes)
 bool launch_gemv_nt(const GemvNT& a, cplx* partials, int64_t partials_cap, cudaStream_t st);
 
+// TMA-streamed G4 pass of the GMRES pair (pairg4.cu): for every chi b < nbatch,
+// y4[b] = A[b] x (CTA partials at partials[(b ns + s) rstride + r], summed in fixed order)
+// and z = sum_b A[b]^T z3[b] (conj if conj_z), one read of every A[b] (R[b] x C, R <= 320).
+struct PairG4 {
+  const cplx* A[3];
+  const cplx* z3[3];
+  cplx* y4[3];
+  const cplx* x;
+  cplx* z;
+  cplx* partials;
+  int64_t R[3];
+  int64_t C, rstride;
+  int64_t ccta;   // set by the launcher: max columns per CTA
+  int nbatch;
+  bool conj_z;
+};
+// false when the shape is unsupported (R > 320): the caller falls back
+bool launch_pair_g4(const PairG4& a, int max_ctas, cudaStream_t st);
+// fixed-order sum of ns split partials ([b][s][rmax]) into a.y[b][0 .. a.R[b])
+void launch_gemv_sum(const GemvN& a, cplx* partials, int ns, int64_t rmax, cudaStream_t st);
+int sm_count_dev();
+
 struct ApplyWorkspace;  // split-K partials + counters (handle-owned)
 
 // partials_cap: capacity (elements) of the split-K partial buffer; the split is

@@ -1,0 +1,274 @@
+// The G4 pass of one GMRES coupling matvec (SURVEY §8a A4 + A9), streamed by TMA.
+//
+// The forward's first step y4 = G4 x (Eq. 17) and the transpose's last step
+// z = sum_chi (G4^chi)^T z3^chi (Eqs. 18-19) both read all of G4 (r3 x m,
+// column-major, the largest core).  This kernel reads it ONCE for both, for up to the three
+// chi components in one launch, and also forms the chi sum of Eq. 18 in fixed order.
+//
+// Per CTA: one contiguous column range [c0, c1) of every chi (the same range: every chi has
+// m columns).  A producer warp streams that range, chi after chi, through a ring of 16
+// shared-memory stages of <= 10 KB with 1-D bulk copies (cp.async.bulk, mbarrier
+// complete_tx), so that ~160 KB per SM are in flight independent of how fast a column is
+// retired.  Stage i is consumed by warp i % 8 alone (two stages per warp in flight, no
+// cross-warp barrier per stage): lane l holds rows l + 32 q (q < NQ) of a column; columns
+// are taken in pairs, the transpose dot products d = G4[:, c] . z3 of the pair are reduced
+// by one half-exchange plus a 16-lane butterfly, the forward accumulation acc[q] +=
+// G4[r, c] x[c] stays in registers until the chi is done, then a fixed-order smem tree over
+// the warps gives the CTA's y4 partial (summed over CTAs by k_sum_partials_warp).  x and
+// z3 are staged in shared memory once.  The z chi sum runs in a per-CTA smem accumulator,
+// written once (conjugated for op C) after the last chi: deterministic, no atomics.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace vsie {
+namespace {
+
+constexpr int kConsumerWarps = 8;
+constexpr int kPairThreads = 32 * (kConsumerWarps + 1);   // + one producer warp
+constexpr int kStageBytes = 10240;                       // >= 2 columns of r3 <= 320
+constexpr int kSlots = 16;                               // two per consumer warp
+constexpr int kRingBytes = kSlots * kStageBytes;         // 160 KB
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, int n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n W:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W;\n}\n" ::"r"(
+          smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// barrier over the 256 consumer threads only (the producer warp keeps streaming)
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps) : "memory"); }
+
+struct StageMap {
+  int cps[3];      // columns per stage of chi b
+  int nst[3];      // stages of chi b
+  int off[3];      // first global stage of chi b
+};
+
+// d0 (column j, all lanes) and d1 (column j + 1): after the call lane l holds the full
+// column sum of column j + (l >= 16) -- one exchange of the other half's column, then a
+// 16-lane butterfly (10 shuffles of 64 bits for two columns instead of 20)
+__device__ __forceinline__ cplx pair_reduce(cplx d0, cplx d1, int lane) {
+  const bool hi = lane >= 16;
+  cplx keep = hi ? d1 : d0, send = hi ? d0 : d1;
+  keep.x += __shfl_xor_sync(0xffffffffu, send.x, 16);
+  keep.y += __shfl_xor_sync(0xffffffffu, send.y, 16);
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) {
+    keep.x += __shfl_xor_sync(0xffffffffu, keep.x, o);
+    keep.y += __shfl_xor_sync(0xffffffffu, keep.y, o);
+  }
+  return keep;
+}
+
+// Stage i (global over the chi sequence) lives in slot i % kSlots and is consumed by warp
+// i % kConsumerWarps alone: no cross-warp barrier per stage, each warp double-buffered.
+template <int NQ>
+__global__ void __launch_bounds__(kPairThreads, 1) k_pair_g4(const __grid_constant__ PairG4 a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  cplx* ring = reinterpret_cast<cplx*>(smem);
+  cplx* red = reinterpret_cast<cplx*>(smem + kRingBytes);                 // [4][32 NQ]
+  cplx* zacc = red + 4 * 32 * NQ;                                          // [c1 - c0]
+  cplx* xs = zacc + a.ccta;                                                // x[c0 .. c1)
+  cplx* zs = xs + a.ccta;                                                  // [3][32 NQ] z3
+  __shared__ uint64_t full[kSlots], empty[kSlots];
+
+  const int ns = gridDim.x, s = blockIdx.x;
+  const int64_t C = a.C;
+  const int64_t c0 = C * s / ns, c1 = C * (s + 1) / ns;
+  const int nc = (int)(c1 - c0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  StageMap mp;
+  int total = 0;
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    mp.cps[b] = 1;
+    mp.nst[b] = 0;
+    mp.off[b] = total;
+    if (b < a.nbatch) {
+      mp.cps[b] = max(1, kStageBytes / (int)(16 * a.R[b]));
+      mp.nst[b] = (nc + mp.cps[b] - 1) / mp.cps[b];
+      total += mp.nst[b];
+    }
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kSlots; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    // ---------------- producer: G4 is constant and x is the caller's input, so the ring
+    // is filled before waiting on the stream predecessor (programmatic dependent launch)
+    if (lane == 0) {
+      int i = 0;
+      for (int b = 0; b < a.nbatch; ++b) {
+        const int64_t R = a.R[b];
+        for (int t = 0; t < mp.nst[b]; ++t, ++i) {
+          const int slot = i % kSlots;
+          if (i >= kSlots) mbar_wait(&empty[slot], ((i / kSlots) - 1) & 1);
+          const int cb = t * mp.cps[b];
+          const int ncol = min(mp.cps[b], nc - cb);
+          const uint32_t bytes = (uint32_t)(16 * R * ncol);
+          mbar_expect_tx(&full[slot], bytes);
+          bulk_g2s(ring + (size_t)slot * (kStageBytes / 16), a.A[b] + R * (c0 + cb), bytes, &full[slot]);
+        }
+      }
+    }
+    pdl_wait();
+    return;
+  }
+
+  // ---------------- consumers
+  // x is the caller's input: staged before the wait (a per-column global load would sit
+  // behind the HBM stream's queues)
+  for (int j = threadIdx.x; j < nc; j += 32 * kConsumerWarps) xs[j] = __ldg(a.x + c0 + j);
+  pdl_wait();   // z3 comes from the stream predecessor
+  for (int b = 0; b < a.nbatch; ++b)
+    for (int r = threadIdx.x; r < 32 * NQ; r += 32 * kConsumerWarps)
+      zs[b * 32 * NQ + r] = r < a.R[b] ? __ldcg(a.z3[b] + r) : cmk(0, 0);   // rows past R: zero weight
+  consumers_sync();
+  for (int b = 0; b < a.nbatch; ++b) {
+    const int R = (int)a.R[b];
+    const int last = R - 1 - lane;
+    const int cps = mp.cps[b];
+    cplx zv[NQ], acc[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      zv[q] = zs[b * 32 * NQ + lane + 32 * q];
+      acc[q] = cmk(0, 0);
+    }
+    // this warp's stages of chi b: global index i = off + t, t = warp - off mod 8, step 8
+    const int off = mp.off[b];
+    for (int t = (warp - off % kConsumerWarps + kConsumerWarps) % kConsumerWarps; t < mp.nst[b];
+         t += kConsumerWarps) {
+      const int i = off + t;
+      const int slot = i % kSlots;
+      const int cb = t * cps;
+      const int ncol = min(cps, nc - cb);
+      mbar_wait(&full[slot], (i / kSlots) & 1);
+      const cplx* st = ring + (size_t)slot * (kStageBytes / 16);
+      for (int j = 0; j < ncol; j += 2) {
+        const bool two = j + 1 < ncol;
+        const cplx* col = st + R * j;
+        const cplx* col1 = two ? col + R : col;
+        const cplx xv0 = xs[cb + j], xv1 = two ? xs[cb + j + 1] : cmk(0, 0);
+        cplx d0 = cmk(0, 0), d1 = cmk(0, 0);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const int r = min(32 * q, last) + lane;   // rows past R re-read row R - 1 (zero weight)
+          const cplx v0 = col[r], v1 = col1[r];
+          cfma(d0, v0, zv[q]);
+          cfma(d1, v1, zv[q]);
+          cfma(acc[q], v0, xv0);
+          cfma(acc[q], v1, xv1);
+        }
+        const cplx d = pair_reduce(d0, d1, lane);
+        const int jj = cb + j + (lane >> 4);
+        if ((lane & 15) == 0 && (lane == 0 || two)) zacc[jj] = b == 0 ? d : cadd(zacc[jj], d);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+    // y4 partial of this CTA: fixed-order tree over the 8 warps (w += w + 4, w + 2, w + 1);
+    // the barriers also order this chi's zacc updates before the next chi's
+#pragma unroll
+    for (int half = kConsumerWarps / 2; half >= 1; half >>= 1) {
+      if (warp >= half && warp < 2 * half) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) red[(warp - half) * 32 * NQ + lane + 32 * q] = acc[q];
+      }
+      consumers_sync();
+      if (warp < half) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) acc[q] = cadd(acc[q], red[warp * 32 * NQ + lane + 32 * q]);
+      }
+      consumers_sync();
+    }
+    if (warp == 0) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int r = lane + 32 * q;
+        if (r < R) {
+          if (ns == 1)
+            a.y4[b][r] = acc[q];
+          else
+            a.partials[((int64_t)b * ns + s) * a.rstride + r] = acc[q];
+        }
+      }
+    }
+  }
+  pdl_trigger();
+  for (int j = threadIdx.x; j < nc; j += 32 * kConsumerWarps) {
+    const cplx v = zacc[j];
+    a.z[c0 + j] = a.conj_z ? cconj(v) : v;
+  }
+}
+
+}  // namespace
+
+int pair_g4_max_rank() { return 320; }
+
+bool launch_pair_g4(const PairG4& a, int max_ctas, cudaStream_t st) {
+  int64_t rmax = 0;
+  for (int b = 0; b < a.nbatch; ++b) rmax = std::max(rmax, a.R[b]);
+  if (rmax > 320 || rmax < 1) return false;
+  if (a.C == 0) return true;
+  VSIE_REQUIRE(a.rstride >= rmax, VSIE_ERR_ARG, "pair_g4: partial stride below r3");
+  const int nq = (int)ceil_div(rmax, 32);
+  const int ns = (int)std::max<int64_t>(1, std::min<int64_t>(max_ctas, ceil_div(a.C, 4)));
+  const int64_t ccta = ceil_div(a.C, ns);
+  const size_t smem = kRingBytes + (size_t)4 * 32 * nq * sizeof(cplx) + (size_t)2 * ccta * sizeof(cplx) +
+                      (size_t)3 * 32 * nq * sizeof(cplx);
+  PairG4 b = a;
+  b.ccta = ccta;
+  if (smem > 220 * 1024) return false;
+  switch (nq) {
+#define VSIE_PG4(K)                                                                                \
+  case K: {                                                                                        \
+    static size_t attr = 0;                                                                        \
+    if (smem > attr) {                                                                             \
+      VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_pair_g4<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+      attr = smem;                                                                                 \
+    }                                                                                              \
+    launch_pdl(k_pair_g4<K>, dim3(ns), dim3(kPairThreads), smem, st, b);                  \
+    break;                                                                                         \
+  }
+    VSIE_PG4(1) VSIE_PG4(2) VSIE_PG4(3) VSIE_PG4(4) VSIE_PG4(5) VSIE_PG4(6) VSIE_PG4(7) VSIE_PG4(8) VSIE_PG4(9)
+    VSIE_PG4(10)
+#undef VSIE_PG4
+    default: return false;
+  }
+  VSIE_CHECK_LAUNCH();
+  if (ns > 1) {
+    GemvN g{};
+    g.nbatch = a.nbatch;
+    for (int b = 0; b < a.nbatch; ++b) {
+      g.y[b] = a.y4[b];
+      g.R[b] = a.R[b];
+    }
+    launch_gemv_sum(g, a.partials, ns, a.rstride, st);
+  }
+  return true;
+}
+
+}  // namespace vsie

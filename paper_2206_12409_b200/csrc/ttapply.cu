@@ -672,6 +672,8 @@ int sm_count() {
 
 }  // namespace
 
+int sm_count_dev() { return sm_count(); }
+
 void launch_gemv_sum(const GemvN& a, cplx* partials, int ns, int64_t rmax, cudaStream_t st) {
   if (ns <= 1) return;
   SumArgs sa{};
