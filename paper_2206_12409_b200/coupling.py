@@ -235,6 +235,15 @@ class Coupling:
         check(lib().vsie_coupling_apply_pair_host(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr), C.c_void_p(u_ptr),
                                                   C.c_void_p(z_ptr), _lib.OPS[adj]))
 
+    def apply_pair_host(self, x: np.ndarray, u: np.ndarray, adj: str = "T"):
+        """vsie_coupling_apply_pair_host: (y = Z x, z = Z^T u or Z^H u) with host buffers."""
+        xc = np.ascontiguousarray(x, dtype=np.complex128)
+        uc = np.ascontiguousarray(u, dtype=np.complex128)
+        y = np.empty(self.out_len("N"), dtype=np.complex128)
+        z = np.empty(self.out_len("T"), dtype=np.complex128)
+        self.apply_pair_host_raw(xc.ctypes.data, y.ctypes.data, uc.ctypes.data, z.ctypes.data, adj)
+        return y, z
+
     def apply_host(self, x: np.ndarray, op: str = "N") -> np.ndarray:
         """vsie_coupling_apply_host: host in, host out (H2D + apply + D2H)."""
         X = np.asarray(x, dtype=np.complex128)

@@ -779,6 +779,7 @@ void apply_dag(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int nrhs, con
   }
   const bool cj = op == VSIE_OP_C;
   const bool stag = !exchange && stagger_on() && S.parallel;
+  X.ws = 3;   // the transpose's own workspaces: a forward apply may run beside it
   for (int c = 0; c < 3; ++c) {
     h->scope_chi = c;
     if (stag && c > 0) VSIE_CHECK_CUDA(cudaStreamWaitEvent(S.chi[c], h->ev_stage[c - 1], 0));

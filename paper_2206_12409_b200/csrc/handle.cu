@@ -306,5 +306,6 @@ vsie_coupling_s::~vsie_coupling_s() {
   }
   for (auto e : event_pool) cudaEventDestroy(e);
   if (io_stream) cudaStreamDestroy(io_stream);
+  if (io_stream2) cudaStreamDestroy(io_stream2);
   vsie::apply_destroy(this);
 }

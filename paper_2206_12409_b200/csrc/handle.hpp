@@ -95,6 +95,7 @@ struct vsie_coupling_s {
   vsie::DevBuf<vsie::cplx> io_x, io_y;     // apply_host staging
   vsie::DevBuf<int64_t> io_idx;
   cudaStream_t io_stream = nullptr;
+  cudaStream_t io_stream2 = nullptr;   // host pair: the transpose's copies + apply
   // info
   int64_t entries_evaluated = 0;
   int sweeps[3] = {0, 0, 0};

@@ -125,6 +125,31 @@ def test_apply_host_matches_device(dense1, cfg1):
     assert np.all(h.apply_host(np.zeros(cfg1.m, complex), "N") == 0)   # P30
 
 
+@pytest.mark.parametrize("ci", [1, 2])
+def test_apply_pair_host(ci):
+    """The host-buffer pair (forward copy-out overlapped with the transpose's copy-in on two
+    streams) equals the device pair and the separate applies, repeatedly (workspaces of the
+    two concurrent directions are disjoint), for op T and op C."""
+    from paper_2206_12409_b200 import Coupling
+    import torch
+    cfg = synth.get_config(ci)
+    r = cfg.ranks_probe
+    tts = rand_tts(cfg, [r, (r[0] + 1, r[1] - 2, r[2] + 3), (max(1, r[0] - 1), r[1] + 1, r[2] - 4)], 300 + ci)
+    h = Coupling.from_cores(grid_of(cfg), cfg.meshes(), cfg.freq, tts, nrhs_max=1)
+    x = synth.complex_gaussian(cfg.m, 31)
+    u = synth.complex_gaussian(3 * cfg.n_v, 32)
+    for adj in ("T", "C"):
+        yd, zd = h.apply_pair(_cuda(x), _cuda(u), adj)
+        yd, zd = yd.cpu().numpy(), zd.cpu().numpy()
+        for _ in range(3):
+            yh, zh = h.apply_pair_host(x, u, adj)
+            assert validate.rel_l2(yh, yd) <= 1e-13 and validate.rel_l2(zh, zd) <= 1e-13
+        assert validate.rel_l2(zh, h.apply(_cuda(u), adj).cpu().numpy()) <= 1e-13
+        if ci == 1:
+            assert validate.rel_l2(yh, ttmv.apply(tts, x, "N")) <= TOL
+            assert validate.rel_l2(zh, ttmv.apply(tts, u, adj)) <= TOL
+
+
 def test_tt_eval_matches_oracle(cfg1):
     from paper_2206_12409_b200 import Coupling
     import torch
