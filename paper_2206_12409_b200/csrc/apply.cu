@@ -113,6 +113,26 @@ int pair_g4_mode() {
   return v;
 }
 
+// batched TMA-streamed G3 steps in the pair (k_seg_gemv); VSIE_SEG_G3=0 keeps the per-chi GEMVs
+bool seg_g3_on() {
+  static const int v = [] {
+    const char* e = std::getenv("VSIE_SEG_G3");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
+// leave the G2^T split-K partials for the batched G3^T kernel to sum on load instead of a
+// split-K reduce launch: measured slower (cfg 2 pair 0.165 -> 0.171 ms: the partial loads
+// sit at the head of every CTA) -- opt-in, VSIE_W2_PARTS=1
+bool w2_parts_on() {
+  static const int v = [] {
+    const char* e = std::getenv("VSIE_W2_PARTS");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v != 0;
+}
+
 bool fuse_g21() {
   // fused G2 + G1 forward tail (k_g21_fwd): measured 0.173 vs 0.167 ms per pair step at
   // cfg 2 (its 110 KB of smem leave one CTA per SM) -- opt-in
@@ -158,7 +178,7 @@ void fwd_g4(const Ctx& X, Shard& s, int c, const cplx* x, cudaStream_t st) {
 }
 
 // steps 2-4 on the owned planes: Y3 = G3 y4, Y2 = G2 Y3, y = G1 Y2
-void fwd_rest(const Ctx& X, Shard& s, int c, cplx* y, cudaStream_t st, cudaEvent_t mid = nullptr) {
+void fwd_rest(const Ctx& X, Shard& s, int c, cplx* y, cudaStream_t st, cudaEvent_t mid = nullptr, bool with_g3 = true) {
   vsie_coupling_s* h = X.h;
   const int k = X.k;
   const int n1 = h->grid.n[0], n2 = h->grid.n[1];
@@ -168,7 +188,9 @@ void fwd_rest(const Ctx& X, Shard& s, int c, cplx* y, cudaStream_t st, cudaEvent
   cplx* y4 = s.y4.p + c * X.r3stride;
   cplx* Y3 = s.Y3.p + c * X.r2m * n3l * k;
   cplx* Y2 = s.Y2.p + c * X.r1m * n2 * n3l * k;
-  if (k == 1) {
+  if (!with_g3) {
+    // Y3 already formed (batched k_seg_gemv)
+  } else if (k == 1) {
     GemvN g{};
     g.nbatch = 1;
     g.A[0] = s.G3[c].p;
@@ -241,7 +263,8 @@ void fwd_rest(const Ctx& X, Shard& s, int c, cplx* y, cudaStream_t st, cudaEvent
 
 // ------------------------------------------------------------------ transpose chain pieces (one chi)
 // W1 = G1^T u, W2 = G2^T W1, z3 = G3^T W2: partial z3 per shard
-void adj_front(const Ctx& X, Shard& s, int c, const cplx* u, bool cj, cudaStream_t st, cudaEvent_t mid = nullptr) {
+void adj_front(const Ctx& X, Shard& s, int c, const cplx* u, bool cj, cudaStream_t st, cudaEvent_t mid = nullptr,
+               bool with_g3 = true) {
   vsie_coupling_s* h = X.h;
   const int k = X.k;
   const int n1 = h->grid.n[0], n2 = h->grid.n[1];
@@ -280,9 +303,18 @@ void adj_front(const Ctx& X, Shard& s, int c, const cplx* u, bool cj, cudaStream
     z.C[0] = W2; z.ldc[0] = r2;
     const int64_t bytes = 16 * (r1 * n2 * r2 + r2 * n3l * k + r1 * n2 * n3l * k);
     Scope sc(h, "adj_g2_zgemm", bytes, 8 * r1 * n2 * r2 * n3l * k, st);
-    launch_zgemm_dmma(z, X.zws(c), h->zgemm_ws_per_chi, st);
+    h->w2_parts[c] = 0;
+    if (!with_g3 && k == 1 && h->shards.size() == 1 && w2_parts_on()) {
+      // the batched G3^T kernel sums the split-K partials of W2 on load
+      int64_t stride = 0;
+      h->w2_parts[c] = launch_zgemm_dmma_parts(z, X.zws(c), h->zgemm_ws_per_chi, st, &stride);
+      h->w2_part_stride[c] = stride;
+    } else {
+      launch_zgemm_dmma(z, X.zws(c), h->zgemm_ws_per_chi, st);
+    }
   }
   if (mid) VSIE_CHECK_CUDA(cudaEventRecord(mid, st));   // chain staggering: G1/G2 steps done
+  if (!with_g3) return;   // z3 by the batched k_seg_gemv
   if (k == 1) {
     GemvT g{};
     g.nbatch = 1;
@@ -953,6 +985,156 @@ void run_dag(vsie_coupling_s* h, int op, int nrhs, const void* x, void* y, const
   h->apply_launches += ge->launches;
 }
 
+// The GMRES pair with every contraction step as ONE launch over the three chi on a single
+// stream (programmatic dependent launch between steps): G1^T, G2^T, G3^T (k_seg_gemv),
+// G4 both ways (k_pair_g4), G3 (k_seg_gemv), G2, G1.  false if a step's shape is not
+// supported by the batched kernels (the caller then runs the chain schedule).
+bool pair_batched(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z, bool cj, cudaStream_t st) {
+  const int n1 = h->grid.n[0], n2 = h->grid.n[1];
+  int r1m = 1, r2m = 1, r3m = 1;
+  for (int c = 0; c < 3; ++c) {
+    r1m = std::max(r1m, h->ranks[c][0]);
+    r2m = std::max(r2m, h->ranks[c][1]);
+    r3m = std::max(r3m, h->ranks[c][2]);
+  }
+  if (r3m > pair_g4_max_rank() || h->shards.size() != 1 || h->comm) return false;
+  Shard& s = h->shards[0];
+  const int64_t n3l = s.n3loc();
+  if (n3l == 0 || s.mloc() == 0) return false;
+  for (int c = 0; c < 3; ++c)
+    if (!seg_gemv_supported((int64_t)h->ranks[c][1] * n3l, h->ranks[c][2], s.g3b_ns)) return false;
+  int w2_splits = 0;
+  int64_t w2_stride = 0;
+  const IoLayout L = voxel_layout(h);
+  auto R = [&](int c, int j) { return (int64_t)h->ranks[c][j]; };
+  cplx* part = h->partials.p;
+  cplx* zws = h->zgemm_ws.p;
+  const int64_t zcap = 3 * h->zgemm_ws_per_chi;
+  {
+    ReduceArgs r{};
+    r.nbatch = 3;
+    r.n1 = n1;
+    r.ncol = (int64_t)n2 * n3l;
+    r.cols_per_rhs = r.ncol;
+    r.ld_rhs = L.ld;
+    r.conj_u = cj;
+    int64_t bytes = 0, fl = 0;
+    for (int c = 0; c < 3; ++c) {
+      r.G1[c] = h->G1[c].p;
+      r.u[c] = u + c * L.chi_stride;
+      r.W1[c] = s.W1.p + c * r1m * n2 * n3l;
+      r.r1[c] = (int)R(c, 0);
+      bytes += 16 * ((int64_t)n1 * R(c, 0) + R(c, 0) * n2 * n3l + (int64_t)n1 * n2 * n3l);
+      fl += 8 * (int64_t)n1 * R(c, 0) * n2 * n3l;
+    }
+    Scope sc(h, "adj_g1_reduce", bytes, fl, st);
+    launch_reduce_g1(r, st);
+  }
+  {
+    Zgemm zg{};
+    zg.nbatch = 3;
+    zg.ta = kT;
+    int64_t bytes = 0, fl = 0;
+    for (int c = 0; c < 3; ++c) {
+      zg.M[c] = R(c, 1); zg.N[c] = n3l; zg.K[c] = R(c, 0) * n2;
+      zg.A[c] = h->G2[c].p; zg.lda[c] = R(c, 0) * n2;
+      zg.B[c] = s.W1.p + c * r1m * n2 * n3l; zg.ldb[c] = R(c, 0) * n2;
+      zg.C[c] = s.W2.p + c * r2m * n3l; zg.ldc[c] = R(c, 1);
+      bytes += 16 * (R(c, 0) * n2 * R(c, 1) + R(c, 1) * n3l + R(c, 0) * n2 * n3l);
+      fl += 8 * R(c, 0) * n2 * R(c, 1) * n3l;
+    }
+    Scope sc(h, "adj_g2_zgemm", bytes, fl, st);
+    if (w2_parts_on())
+      w2_splits = launch_zgemm_dmma_parts(zg, zws, zcap, st, &w2_stride);
+    else
+      launch_zgemm_dmma(zg, zws, zcap, st);
+  }
+  SegGemv g{};
+  g.nbatch = 3;
+  g.nsb = s.g3b_ns;
+  g.partials = part;
+  g.rstride = r3m;
+  int64_t b3 = 0;
+  for (int c = 0; c < 3; ++c) {
+    g.A[c] = s.G3b[c].p;
+    g.x[c] = s.W2.p + c * r2m * n3l;
+    g.xparts[c] = w2_splits;
+    g.xpart[c] = zws + (int64_t)c * w2_splits * w2_stride;
+    g.xpart_stride[c] = w2_stride;
+    g.y[c] = s.z3.p + c * r3m;
+    g.R[c] = R(c, 1) * n3l;
+    g.C[c] = R(c, 2);
+    b3 += 16 * (g.R[c] * g.C[c] + g.R[c] + g.C[c]);
+  }
+  {
+    Scope sc(h, "adj_g3_seg", b3, b3 / 2, st);
+    VSIE_REQUIRE(launch_seg_gemv(g, true, st), VSIE_ERR_STATE, "pair_batched: G3 shape");
+  }
+  {
+    PairG4 p{};
+    p.nbatch = 3;
+    p.C = s.mloc();
+    p.x = x + s.cb;
+    p.z = z + s.cb;
+    p.conj_z = cj;
+    p.partials = part;
+    p.rstride = r3m;
+    for (int c = 0; c < 3; ++c) {
+      p.A[c] = s.G4[c].p;
+      p.z3[c] = s.z3.p + c * r3m;
+      p.y4[c] = s.y4.p + c * r3m;
+      p.R[c] = R(c, 2);
+    }
+    Scope sc(h, "pair_g4_tma", 16 * (R(0, 2) + R(1, 2) + R(2, 2)) * (p.C + 2) + 16 * 2 * p.C,
+             16 * (R(0, 2) + R(1, 2) + R(2, 2)) * p.C, st);
+    VSIE_REQUIRE(launch_pair_g4(p, sm_count_dev(), st), VSIE_ERR_STATE, "pair_batched: G4 shape");
+  }
+  for (int c = 0; c < 3; ++c) {
+    g.x[c] = s.y4.p + c * r3m;
+    g.y[c] = s.Y3.p + c * r2m * n3l;
+    g.xparts[c] = 0;
+  }
+  {
+    Scope sc(h, "fwd_g3_seg", b3, b3 / 2, st);
+    VSIE_REQUIRE(launch_seg_gemv(g, false, st), VSIE_ERR_STATE, "pair_batched: G3 shape");
+  }
+  {
+    Zgemm zg{};
+    zg.nbatch = 3;
+    int64_t bytes = 0, fl = 0;
+    for (int c = 0; c < 3; ++c) {
+      zg.M[c] = R(c, 0) * n2; zg.N[c] = n3l; zg.K[c] = R(c, 1);
+      zg.A[c] = h->G2[c].p; zg.lda[c] = R(c, 0) * n2;
+      zg.B[c] = s.Y3.p + c * r2m * n3l; zg.ldb[c] = R(c, 1);
+      zg.C[c] = s.Y2.p + c * r1m * n2 * n3l; zg.ldc[c] = R(c, 0) * n2;
+      bytes += 16 * (R(c, 0) * n2 * R(c, 1) + R(c, 1) * n3l + R(c, 0) * n2 * n3l);
+      fl += 8 * R(c, 0) * n2 * R(c, 1) * n3l;
+    }
+    Scope sc(h, "fwd_g2_zgemm", bytes, fl, st);
+    launch_zgemm_dmma(zg, zws, zcap, st);
+  }
+  {
+    ExpandArgs e{};
+    e.nbatch = 3;
+    e.n1 = n1;
+    e.ncol = (int64_t)n2 * n3l;
+    e.cols_per_rhs = e.ncol;
+    e.ld_rhs = L.ld;
+    int64_t bytes = 0, fl = 0;
+    for (int c = 0; c < 3; ++c) {
+      e.G1[c] = h->G1[c].p;
+      e.Y2[c] = s.Y2.p + c * r1m * n2 * n3l;
+      e.y[c] = y + c * L.chi_stride;
+      e.r1[c] = (int)R(c, 0);
+      bytes += 16 * ((int64_t)n1 * R(c, 0) + R(c, 0) * n2 * n3l + (int64_t)n1 * n2 * n3l);
+      fl += 8 * (int64_t)n1 * R(c, 0) * n2 * n3l;
+    }
+    Scope sc(h, "fwd_g1_expand", bytes, fl, st);
+    launch_expand_g1(e, st);
+  }
+  return true;
+}
+
 // The coupling pair of one GMRES matvec of the hybrid system (Eq. 11 / 15: the body rows
 // need Z_bc j_c, the conductor rows Z_bc^T j_b): y = Z x and z = Z^T u (Z^H u).  The
 // transpose front (G1^T, G2^T, G3^T) runs first, so that both directions' G4 products
@@ -971,6 +1153,7 @@ void pair_dag(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z
   X.L = voxel_layout(h);
   const bool exchange = h->comm != nullptr || h->shards.size() > 1;
   const int64_t m = h->m, mp = ceil_div(m, h->world);
+  if (pair_g4_mode() == 4 && pair_batched(h, x, y, u, z, cj, S.main)) return;
   if (pair_g4_mode() == 3 && !exchange) {
     // both directions as six independent chains (transpose chains on S.chi, forward chains
     // on S.chi2, separate workspaces): G4 is read twice but no chain waits for another
@@ -990,12 +1173,67 @@ void pair_dag(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z
     adj_sum_chi(X, s, z + s.cb, m, cj, S.main);
     return;
   }
+  // mode 2: the G3 and G4 steps as batched TMA-streamed launches on the main stream
+  // (both directions), the G1 / G2 steps as per-chi chains around them
+  bool seg = pair_g4_mode() == 2 && seg_g3_on();
+  for (Shard& s : h->shards)
+    for (int c = 0; c < 3 && seg; ++c)
+      seg = seg_gemv_supported(X.R(c, 1) * s.n3loc(), X.R(c, 2), s.g3b_ns) && s.n3loc() > 0;
   fork(h, S);
   for (int c = 0; c < 3; ++c) {
     h->scope_chi = c;
-    for (Shard& s : h->shards) adj_front(X, s, c, u, cj, S.chi[c]);
+    for (Shard& s : h->shards) adj_front(X, s, c, u, cj, S.chi[c], nullptr, !seg);
   }
-  if (exchange) {
+  h->scope_chi = -1;
+  if (seg) {
+    join(h, S);
+    for (Shard& s : h->shards) {
+      const int64_t n3l = s.n3loc();
+      SegGemv g{};
+      g.nbatch = 3;
+      g.nsb = s.g3b_ns;
+      g.partials = X.partials(0);
+      g.rstride = X.r3m;
+      int64_t bytes = 0;
+      for (int c = 0; c < 3; ++c) {
+        g.A[c] = s.G3b[c].p;
+        g.x[c] = s.W2.p + c * X.r2m * n3l;
+        g.xparts[c] = h->shards.size() == 1 ? h->w2_parts[c] : 0;
+        g.xpart[c] = X.zws(c);
+        g.xpart_stride[c] = h->w2_part_stride[c];
+        g.y[c] = s.z3.p + c * X.r3stride;
+        g.R[c] = X.R(c, 1) * n3l;
+        g.C[c] = X.R(c, 2);
+        bytes += 16 * (g.R[c] * g.C[c] + g.R[c] + g.C[c]);
+      }
+      bool ok;
+      {
+        Scope sc(h, "adj_g3_seg", bytes, bytes / 2, S.main);
+        ok = n3l > 0 && launch_seg_gemv(g, true, S.main);
+      }
+      if (!ok) {
+        // unsupported shape: the per-chi column GEMVs
+        for (int c = 0; c < 3; ++c) {
+          cplx* z3 = s.z3.p + c * X.r3stride;
+          if (n3l == 0) {
+            VSIE_CHECK_CUDA(cudaMemsetAsync(z3, 0, X.r3stride * sizeof(cplx), S.main));
+            continue;
+          }
+          GemvT t{};
+          t.nbatch = 1;
+          t.A[0] = s.G3[c].p;
+          t.x[0] = g.x[c];
+          t.y[0] = z3;
+          t.R[0] = g.R[c];
+          t.C[0] = g.C[c];
+          Scope sc(h, "adj_g3_gemv", 16 * (g.R[c] * g.C[c] + g.R[c] + g.C[c]), 8 * g.R[c] * g.C[c], S.main);
+          launch_gemv_t(t, X.partials(c), h->partials_per_chi, kMaxSplits, S.main);
+        }
+      }
+    }
+    if (exchange) combine_r3(h, &Shard::z3, 3 * X.r3stride, S.main);
+    fork(h, S);
+  } else if (exchange) {
     join(h, S);
     combine_r3(h, &Shard::z3, 3 * X.r3stride, S.main);
     fork(h, S);
@@ -1031,6 +1269,42 @@ void pair_dag(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z
     VSIE_REQUIRE(ok || h->shards.size() == 1, VSIE_ERR_STATE, "pair_g4 unsupported on a multi-shard handle");
     z_done = ok;
     if (z_done && exchange) combine_r3(h, &Shard::y4, 3 * X.r3stride, S.main);
+    if (z_done && seg) {
+      for (Shard& s : h->shards) {
+        const int64_t n3l = s.n3loc();
+        if (n3l == 0) continue;
+        SegGemv g{};
+        g.nbatch = 3;
+        g.nsb = s.g3b_ns;
+        int64_t bytes = 0;
+        for (int c = 0; c < 3; ++c) {
+          g.A[c] = s.G3b[c].p;
+          g.x[c] = s.y4.p + c * X.r3stride;
+          g.y[c] = s.Y3.p + c * X.r2m * n3l;
+          g.R[c] = X.R(c, 1) * n3l;
+          g.C[c] = X.R(c, 2);
+          bytes += 16 * (g.R[c] * g.C[c] + g.R[c] + g.C[c]);
+        }
+        bool ok3;
+        {
+          Scope sc(h, "fwd_g3_seg", bytes, bytes / 2, S.main);
+          ok3 = launch_seg_gemv(g, false, S.main);
+        }
+        if (!ok3) {
+          for (int c = 0; c < 3; ++c) {
+            GemvN t{};
+            t.nbatch = 1;
+            t.A[0] = s.G3[c].p;
+            t.x[0] = g.x[c];
+            t.y[0] = g.y[c];
+            t.R[0] = g.R[c];
+            t.C[0] = g.C[c];
+            Scope sc(h, "fwd_g3_gemv", 16 * (g.R[c] * g.C[c] + g.R[c] + g.C[c]), 8 * g.R[c] * g.C[c], S.main);
+            launch_gemv_n(t, X.partials(c), h->partials_per_chi, kMaxSplits, S.main);
+          }
+        }
+      }
+    }
     fork(h, S);
   }
   if (!z_done) {
@@ -1072,7 +1346,7 @@ void pair_dag(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z
   }   // !z_done
   for (int c = 0; c < 3; ++c) {
     h->scope_chi = c;
-    for (Shard& s : h->shards) fwd_rest(X, s, c, y, S.chi[c]);
+    for (Shard& s : h->shards) fwd_rest(X, s, c, y, S.chi[c], nullptr, !(z_done && seg));
   }
   h->scope_chi = -1;
   join(h, S);

@@ -152,6 +152,22 @@ void handle_alloc_workspace(vsie_coupling_s* h) {
     r3m = std::max(r3m, h->ranks[c][2]);
   }
   int64_t rmax_gemv = 1;
+  // row-blocked copies of the G3 slices (k_seg_gemv)
+  const int nsb = sm_count_dev();
+  for (Shard& s : h->shards) {
+    s.g3b_ns = nsb;
+    for (int c = 0; c < 3; ++c) {
+      const int64_t R = (int64_t)h->ranks[c][1] * s.n3loc(), C = h->ranks[c][2];
+      s.G3b[c].alloc((size_t)std::max<int64_t>(1, R * C));
+      if (R == 0) continue;
+      for (int q = 0; q < nsb; ++q) {
+        const int64_t r0 = R * q / nsb, L = R * (q + 1) / nsb - r0;
+        if (L == 0) continue;
+        VSIE_CHECK_CUDA(cudaMemcpy2D(s.G3b[c].p + C * r0, L * sizeof(cplx), s.G3[c].p + r0, R * sizeof(cplx),
+                                     L * sizeof(cplx), C, cudaMemcpyDeviceToDevice));
+      }
+    }
+  }
   for (Shard& s : h->shards) {
     const int64_t n3l = std::max(1, s.n3loc());
     s.y4.alloc(3 * (int64_t)r3m * k);

@@ -19,6 +19,11 @@ struct Shard {
   int64_t cb = 0, ce = 0;
   DevBuf<cplx> G3[3];   // (r2, i3e - i3b, r3) column-major: the owned i3 slice of G3
   DevBuf<cplx> G4[3];   // (r3, ce - cb): the owned columns of G4
+  // G3 slice re-blocked for k_seg_gemv: g3b_ns row blocks [R q / ns, R (q + 1) / ns) of the
+  // (r2 n3loc) x r3 matrix, block q stored column-major (L_q x r3) at offset r3 * row0_q,
+  // so that every CTA streams one contiguous range
+  DevBuf<cplx> G3b[3];
+  int g3b_ns = 0;
   // apply workspaces (sized for nrhs_max)
   DevBuf<cplx> y4;      // [3][r3max * nrhs]  forward: G4 x partial / reduced
   DevBuf<cplx> Y3;      // [3][r2 * n3loc * nrhs]
@@ -89,6 +94,8 @@ struct vsie_coupling_s {
   std::vector<vsie::GraphEntry> graphs;
   uint64_t graph_clock = 0;
   int use_graphs = 1;
+  int w2_parts[3] = {0, 0, 0};          // pair: split-K partials of W2 left for k_seg_gemv
+  int64_t w2_part_stride[3] = {0, 0, 0};
   int apply_mode = 0;   // single RHS: 0 per-chi kernel chains, 1 persistent kernel, 2 batched kernels
   int tile_trace = 0;
   vsie::DevBuf<vsie::cplx> gather_buf;     // allgather staging of z

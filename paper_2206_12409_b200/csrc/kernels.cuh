@@ -96,6 +96,28 @@ struct PairG4 {
 };
 // false when the shape is unsupported (R > 320): the caller falls back
 bool launch_pair_g4(const PairG4& a, int max_ctas, cudaStream_t st);
+int pair_g4_max_rank();
+// TMA-streamed GEMV on column-major R[b] x C[b] matrices, batched over b < nbatch
+// (segemv.cu, the G3 steps): op N y[b] = A[b] x[b]; op T y[b] = A[b]^T x[b] through
+// per-CTA partials ([b][ns][rstride], rstride >= max C) summed in fixed order.
+// false when the shape is unsupported (the caller falls back to k_gemv_n / k_gemv_t).
+struct SegGemv {
+  const cplx* A[3];   // row-blocked (Shard::G3b): block q = rows [R q / nsb, R (q + 1) / nsb)
+  const cplx* x[3];
+  cplx* y[3];
+  cplx* partials;
+  int64_t R[3], C[3];
+  int64_t rstride;
+  int nbatch;
+  int nsb;            // row blocks of the layout (= CTAs)
+  // op T: when xparts[b] > 0, x[b][r] = sum_{q < xparts[b]} xpart[b][q * xpart_stride[b] + r]
+  // (the split-K partials of the producing GEMM, summed in fixed order on load)
+  const cplx* xpart[3];
+  int xparts[3];
+  int64_t xpart_stride[3];
+};
+bool launch_seg_gemv(const SegGemv& a, bool transpose, cudaStream_t st);
+bool seg_gemv_supported(int64_t R, int64_t C, int nsb);
 // fixed-order sum of ns split partials ([b][s][rmax]) into a.y[b][0 .. a.R[b])
 void launch_gemv_sum(const GemvN& a, cplx* partials, int ns, int64_t rmax, cudaStream_t st);
 int sm_count_dev();
@@ -174,6 +196,9 @@ void launch_zgemm(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t st);
 // same contract on FP64 tensor cores (DMMA), warp-tiled, for small / skinny
 // problems; op(B) must be N.
 void launch_zgemm_dmma(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t st);
+// same, but a split-K result is left as partials for the consumer to sum: returns 0 when C
+// was written, else the number of splits S with C_b = sum_q ws[(b S + q) *part_stride + m + M n]
+int launch_zgemm_dmma_parts(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t st, int64_t* part_stride);
 
 // conj in place
 void launch_conj(cplx* x, int64_t n, cudaStream_t st);

@@ -376,6 +376,10 @@ void launch_zgemm(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t st) {
 }
 
 void launch_zgemm_dmma(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t st) {
+  launch_zgemm_dmma_parts(g, ws, ws_elems, st, nullptr);
+}
+
+int launch_zgemm_dmma_parts(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t st, int64_t* part_stride) {
   VSIE_REQUIRE(g.tb == kN && g.ta != kC, VSIE_ERR_ARG, "zgemm_dmma: op(A) in {N, T}, op(B) = N");
   int64_t mmax = 0, nmax = 0, kmax = 0, mn = 0;
   for (int b = 0; b < g.nbatch; ++b) {
@@ -384,7 +388,7 @@ void launch_zgemm_dmma(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t 
     kmax = std::max(kmax, g.K[b]);
     mn = std::max(mn, g.M[b] * g.N[b]);
   }
-  if (mmax == 0 || nmax == 0) return;
+  if (mmax == 0 || nmax == 0) return 1;
   // warp layout: tall (4 x 2 -> 64 x 32) or wide (2 x 4 -> 32 x 64) output tiles
   const bool tall = mmax >= 2 * nmax;
   const int TM = tall ? tc::FTM : tc::ATM, TN = tall ? tc::FTN : tc::ATN;
@@ -423,11 +427,16 @@ void launch_zgemm_dmma(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t 
     else launch_pdl(k_zgemm_tc<tc::AWA, tc::AWB, false>, grid, blk, smem, st, g, splits, mt, nt, ws, mn, direct);
   }
   VSIE_CHECK_LAUNCH();
-  if (!direct) {
-    dim3 rg((unsigned)std::min<int64_t>(ceil_div(mn, 256), 148 * 8), g.nbatch);
-    launch_pdl(k_splitk_reduce, rg, dim3(256), 0, st, g, splits, (const cplx*)ws, mn);
-    VSIE_CHECK_LAUNCH();
+  if (direct) return 0;
+  if (part_stride && unit) {
+    // the caller sums the split partials (ws[(b splits + q) mn + m + M n]) on load
+    *part_stride = mn;
+    return splits;
   }
+  dim3 rg((unsigned)std::min<int64_t>(ceil_div(mn, 256), 148 * 8), g.nbatch);
+  launch_pdl(k_splitk_reduce, rg, dim3(256), 0, st, g, splits, (const cplx*)ws, mn);
+  VSIE_CHECK_LAUNCH();
+  return 0;
 }
 
 void launch_conj(cplx* x, int64_t n, cudaStream_t st) {

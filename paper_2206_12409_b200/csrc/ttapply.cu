@@ -420,61 +420,74 @@ __device__ __forceinline__ void zmma(double (&cr)[2], double (&ci)[2], cplx a, c
 // 8 x 8 output tile is stored as 4 whole 128-B lines per warp instruction.
 template <int KT>
 __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant__ ExpandArgs a) {
-  pdl_wait();
   const int b = blockIdx.y;
   const int n1 = a.n1, r1 = a.r1[b];
   const int mt = (n1 + 7) / 8;
   extern __shared__ cplx Af[];   // [mt][KT][32] fragments of G1
   const cplx* __restrict__ G1 = a.G1[b];
+  // G1 is a constant core: staged before waiting on the producer of Y2 (PDL overlap)
   for (int e = threadIdx.x; e < mt * KT * 32; e += kG1Threads) {
     const int lane = e % 32, ks = (e / 32) % KT, m = e / (32 * KT);
     const int i1 = 8 * m + (lane >> 2), k = 4 * ks + (lane & 3);
     Af[e] = (i1 < n1 && k < r1) ? __ldg(G1 + i1 + (int64_t)n1 * k) : cmk(0, 0);
   }
   __syncthreads();
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int64_t c0 = ((int64_t)blockIdx.x * kWarpsG1 + warp) * kColsPerWarp;
-  if (c0 >= a.ncol) return;
-  cplx bf[KT];
-  {
-    const int64_t c = c0 + g;
+  cplx* __restrict__ Y = a.y[b];
+  // persistent: warp tasks of 8 columns, the next task's Y2 fragments loaded before the
+  // current task's DMMAs and stores
+  const int64_t ntask = (a.ncol + kColsPerWarp - 1) / kColsPerWarp;
+  const int64_t stride = (int64_t)gridDim.x * kWarpsG1;
+  int64_t task = (int64_t)blockIdx.x * kWarpsG1 + warp;
+  auto load_bf = [&](int64_t tk, cplx (&bf)[KT]) {
+    const int64_t c = tk * kColsPerWarp + g;
     const cplx* __restrict__ Y2 = a.Y2[b] + (int64_t)r1 * c;
 #pragma unroll
     for (int ks = 0; ks < KT; ++ks) {
       const int k = 4 * ks + t;
-      bf[ks] = (c < a.ncol && k < r1) ? __ldg(Y2 + k) : cmk(0, 0);
+      bf[ks] = (tk < ntask && c < a.ncol && k < r1) ? __ldg(Y2 + k) : cmk(0, 0);
     }
-  }
-  int64_t oaddr[2];
-  bool ok[2];
+  };
+  cplx bf[KT];
+  load_bf(task, bf);
+  for (; task < ntask; task += stride) {
+    cplx bn[KT];
+    load_bf(task + stride, bn);
+    const int64_t c0 = task * kColsPerWarp;
+    int64_t oaddr[2];
+    bool ok[2];
 #pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const int64_t c = c0 + 2 * t + j;
-    ok[j] = c < a.ncol;
-    oaddr[j] = ok[j] ? col_addr(c, a.cols_per_rhs, a.ld_rhs, n1) : 0;
-  }
-  cplx* __restrict__ Y = a.y[b];
-  double bsum[KT];
-#pragma unroll
-  for (int ks = 0; ks < KT; ++ks) bsum[ks] = bf[ks].x + bf[ks].y;
-  for (int m = 0; m < mt; ++m) {
-    // 3 real DMMAs per complex product: P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi)
-    double p1[2] = {0, 0}, p2[2] = {0, 0}, p3[2] = {0, 0};
-#pragma unroll
-    for (int ks = 0; ks < KT; ++ks) {
-      const cplx av = Af[(m * KT + ks) * 32 + lane];
-      dmma(p1[0], p1[1], av.x, bf[ks].x);
-      dmma(p2[0], p2[1], av.y, bf[ks].y);
-      dmma(p3[0], p3[1], av.x + av.y, bsum[ks]);
+    for (int j = 0; j < 2; ++j) {
+      const int64_t c = c0 + 2 * t + j;
+      ok[j] = c < a.ncol;
+      oaddr[j] = ok[j] ? col_addr(c, a.cols_per_rhs, a.ld_rhs, n1) : 0;
     }
-    const int i1 = 8 * m + g;
-    if (i1 < n1) {
+    double bsum[KT];
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
-        if (ok[j]) __stcs(Y + oaddr[j] + i1, cmk(p1[j] - p2[j], p3[j] - p1[j] - p2[j]));
+    for (int ks = 0; ks < KT; ++ks) bsum[ks] = bf[ks].x + bf[ks].y;
+    for (int m = 0; m < mt; ++m) {
+      // 3 real DMMAs per complex product: P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi)
+      double p1[2] = {0, 0}, p2[2] = {0, 0}, p3[2] = {0, 0};
+#pragma unroll
+      for (int ks = 0; ks < KT; ++ks) {
+        const cplx av = Af[(m * KT + ks) * 32 + lane];
+        dmma(p1[0], p1[1], av.x, bf[ks].x);
+        dmma(p2[0], p2[1], av.y, bf[ks].y);
+        dmma(p3[0], p3[1], av.x + av.y, bsum[ks]);
+      }
+      const int i1 = 8 * m + g;
+      if (i1 < n1) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          if (ok[j]) __stcs(Y + oaddr[j] + i1, cmk(p1[j] - p2[j], p3[j] - p1[j] - p2[j]));
+      }
     }
+#pragma unroll
+    for (int ks = 0; ks < KT; ++ks) bf[ks] = bn[ks];
   }
+  pdl_trigger();
 }
 
 // W1[a + r1 c] = sum_i1 G1[i1 + n1 a] u[i1 + n1 c] (conj(u) for op C): warp task =
@@ -482,74 +495,67 @@ __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant_
 // lane 16 B, 64 contiguous bytes per column), G1 fragments from shared memory.
 template <int NT>
 __global__ void __launch_bounds__(kG1Threads) k_reduce_g1(const __grid_constant__ ReduceArgs a) {
-  pdl_wait();
   const int b = blockIdx.y;
   const int n1 = a.n1, r1 = a.r1[b];
   const int ks_n = (n1 + 3) / 4;
   extern __shared__ cplx Bf[];   // [ks_n][NT][32] fragments of G1
   const cplx* __restrict__ G1 = a.G1[b];
+  // G1 is a constant core: staged before waiting on the stream predecessor (PDL overlap)
   for (int e = threadIdx.x; e < ks_n * NT * 32; e += kG1Threads) {
     const int lane = e % 32, nt = (e / 32) % NT, ks = e / (32 * NT);
     const int k = 4 * ks + (lane & 3), n = 8 * nt + (lane >> 2);
     Bf[e] = (k < n1 && n < r1) ? __ldg(G1 + k + (int64_t)n1 * n) : cmk(0, 0);
   }
   __syncthreads();
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int64_t c0 = ((int64_t)blockIdx.x * kWarpsG1 + warp) * kColsPerWarp;
-  if (c0 >= a.ncol) return;
-  const int64_t cg = c0 + g;
-  const bool cok = cg < a.ncol;
-  const cplx* __restrict__ U = a.u[b] + (cok ? col_addr(cg, a.cols_per_rhs, a.ld_rhs, n1) : 0);
   const double sgn = a.conj_u ? -1.0 : 1.0;
-  // 3 real DMMAs per complex product (P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi))
-  double p1[NT][2], p2[NT][2], p3[NT][2];
+  // persistent: warp tasks of 8 columns x all i1, UNR k-steps of loads in flight
+  const int64_t ntask = (a.ncol + kColsPerWarp - 1) / kColsPerWarp;
+  for (int64_t task = (int64_t)blockIdx.x * kWarpsG1 + warp; task < ntask; task += (int64_t)gridDim.x * kWarpsG1) {
+    const int64_t cg = task * kColsPerWarp + g;
+    const bool cok = cg < a.ncol;
+    const cplx* __restrict__ U = a.u[b] + (cok ? col_addr(cg, a.cols_per_rhs, a.ld_rhs, n1) : 0);
+    // 3 real DMMAs per complex product (P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi))
+    double p1[NT][2], p2[NT][2], p3[NT][2];
 #pragma unroll
-  for (int nt = 0; nt < NT; ++nt) p1[nt][0] = p1[nt][1] = p2[nt][0] = p2[nt][1] = p3[nt][0] = p3[nt][1] = 0;
-  constexpr int UNR = 8;
-  int ks = 0;
-  for (; ks + UNR <= ks_n; ks += UNR) {
-    cplx av[UNR];
+    for (int nt = 0; nt < NT; ++nt) p1[nt][0] = p1[nt][1] = p2[nt][0] = p2[nt][1] = p3[nt][0] = p3[nt][1] = 0;
+    constexpr int UNR = 13;
+    for (int ks = 0; ks < ks_n; ks += UNR) {
+      cplx av[UNR];
 #pragma unroll
-    for (int q = 0; q < UNR; ++q) {
-      const int k = 4 * (ks + q) + t;
-      av[q] = (cok && k < n1) ? __ldcs(U + k) : cmk(0, 0);
-    }
+      for (int q = 0; q < UNR; ++q) {
+        const int k = 4 * (ks + q) + t;
+        av[q] = (cok && k < n1) ? __ldcs(U + k) : cmk(0, 0);
+      }
 #pragma unroll
-    for (int q = 0; q < UNR; ++q) {
-      const double ar = av[q].x, ai = sgn * av[q].y, as = ar + ai;
+      for (int q = 0; q < UNR; ++q) {
+        if (ks + q < ks_n) {
+          const double ar = av[q].x, ai = sgn * av[q].y, as = ar + ai;
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const cplx bv = Bf[((ks + q) * NT + nt) * 32 + lane];
-        dmma(p1[nt][0], p1[nt][1], ar, bv.x);
-        dmma(p2[nt][0], p2[nt][1], ai, bv.y);
-        dmma(p3[nt][0], p3[nt][1], as, bv.x + bv.y);
+          for (int nt = 0; nt < NT; ++nt) {
+            const cplx bv = Bf[((ks + q) * NT + nt) * 32 + lane];
+            dmma(p1[nt][0], p1[nt][1], ar, bv.x);
+            dmma(p2[nt][0], p2[nt][1], ai, bv.y);
+            dmma(p3[nt][0], p3[nt][1], as, bv.x + bv.y);
+          }
+        }
       }
     }
-  }
-  for (; ks < ks_n; ++ks) {
-    const int k = 4 * ks + t;
-    cplx av = (cok && k < n1) ? __ldcs(U + k) : cmk(0, 0);
-    const double ar = av.x, ai = sgn * av.y, as = ar + ai;
+    // lane holds rows c = c0 + g, columns a = 8 nt + 2 t + j
+    if (cok) {
+      cplx* __restrict__ W = a.W1[b] + (int64_t)r1 * cg;
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const cplx bv = Bf[(ks * NT + nt) * 32 + lane];
-      dmma(p1[nt][0], p1[nt][1], ar, bv.x);
-      dmma(p2[nt][0], p2[nt][1], ai, bv.y);
-      dmma(p3[nt][0], p3[nt][1], as, bv.x + bv.y);
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int aa = 8 * nt + 2 * t + j;
+          if (aa < r1) W[aa] = cmk(p1[nt][j] - p2[nt][j], p3[nt][j] - p1[nt][j] - p2[nt][j]);
+        }
     }
   }
-  // lane holds rows c = c0 + g, columns a = 8 nt + 2 t + j
-  if (cok) {
-    cplx* __restrict__ W = a.W1[b] + (int64_t)r1 * cg;
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int aa = 8 * nt + 2 * t + j;
-        if (aa < r1) W[aa] = cmk(p1[nt][j] - p2[nt][j], p3[nt][j] - p1[nt][j] - p2[nt][j]);
-      }
-  }
+  pdl_trigger();
 }
 
 __global__ void __launch_bounds__(kThreads) k_sum3(const cplx* __restrict__ in, int64_t chi_stride, int64_t ld_in,
@@ -864,6 +870,21 @@ void set_smem_attr_once(F* f, bool& done) {
   }
 }
 
+// persistent G1-step grids: 4 resident CTAs of 256 threads per SM over the batch
+// (VSIE_G1_CTAS_PER_SM overrides)
+int64_t g1_ctas_per_chi(int nbatch, const void* fn, size_t smem) {
+  static const int per_sm_env = [] {
+    const char* e = std::getenv("VSIE_G1_CTAS_PER_SM");
+    return e ? std::max(1, std::atoi(e)) : 0;
+  }();
+  int occ = per_sm_env;
+  if (!occ) {
+    VSIE_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kG1Threads, smem));
+    occ = std::max(1, occ);
+  }
+  return std::max<int64_t>(1, (int64_t)sm_count() * occ / std::max(1, nbatch));
+}
+
 void launch_expand_g1(const ExpandArgs& a, cudaStream_t st) {
   int r1max = 0;
   for (int b = 0; b < a.nbatch; ++b) r1max = std::max(r1max, a.r1[b]);
@@ -871,13 +892,14 @@ void launch_expand_g1(const ExpandArgs& a, cudaStream_t st) {
   const int KT = (r1max + 3) / 4;
   const size_t smem = (size_t)((a.n1 + 7) / 8) * KT * 32 * sizeof(cplx);
   VSIE_REQUIRE(smem <= 200 * 1024, VSIE_ERR_ARG, "expand: n1 * r1 too large for shared memory");
-  dim3 grid((unsigned)ceil_div(a.ncol, kColsPerCtaG1), a.nbatch);
-#define VSIE_EXP(K)                                                  \
-  case K: {                                                          \
-    static bool d = false;                                           \
-    set_smem_attr_once(k_expand_g1<K>, d);                           \
-    launch_pdl(k_expand_g1<K>, grid, dim3(kG1Threads), smem, st, a); \
-    break;                                                           \
+#define VSIE_EXP(K)                                                                                        \
+  case K: {                                                                                                \
+    static bool d = false;                                                                                 \
+    set_smem_attr_once(k_expand_g1<K>, d);                                                                 \
+    dim3 grid((unsigned)std::min<int64_t>(ceil_div(a.ncol, kColsPerCtaG1),                                 \
+                                          g1_ctas_per_chi(a.nbatch, (const void*)k_expand_g1<K>, smem)), a.nbatch); \
+    launch_pdl(k_expand_g1<K>, grid, dim3(kG1Threads), smem, st, a);                                       \
+    break;                                                                                                 \
   }
   switch (KT) {
     VSIE_EXP(1) VSIE_EXP(2) VSIE_EXP(3) VSIE_EXP(4) VSIE_EXP(5) VSIE_EXP(6) VSIE_EXP(7) default: VSIE_EXP(8)
@@ -893,13 +915,14 @@ void launch_reduce_g1(const ReduceArgs& a, cudaStream_t st) {
   const int NT = (r1max + 7) / 8;
   const size_t smem = (size_t)((a.n1 + 3) / 4) * NT * 32 * sizeof(cplx);
   VSIE_REQUIRE(smem <= 200 * 1024, VSIE_ERR_ARG, "reduce: n1 * r1 too large for shared memory");
-  dim3 grid((unsigned)ceil_div(a.ncol, kColsPerCtaG1), a.nbatch);
-#define VSIE_RED(K)                                                  \
-  case K: {                                                          \
-    static bool d = false;                                           \
-    set_smem_attr_once(k_reduce_g1<K>, d);                           \
-    launch_pdl(k_reduce_g1<K>, grid, dim3(kG1Threads), smem, st, a); \
-    break;                                                           \
+#define VSIE_RED(K)                                                                                        \
+  case K: {                                                                                                \
+    static bool d = false;                                                                                 \
+    set_smem_attr_once(k_reduce_g1<K>, d);                                                                 \
+    dim3 grid((unsigned)std::min<int64_t>(ceil_div(a.ncol, kColsPerCtaG1),                                 \
+                                          g1_ctas_per_chi(a.nbatch, (const void*)k_reduce_g1<K>, smem)), a.nbatch); \
+    launch_pdl(k_reduce_g1<K>, grid, dim3(kG1Threads), smem, st, a);                                       \
+    break;                                                                                                 \
   }
   switch (NT) {
     VSIE_RED(1) VSIE_RED(2) VSIE_RED(3) default: VSIE_RED(4)

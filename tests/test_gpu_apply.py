@@ -275,3 +275,45 @@ def test_fused_g21_forward(monkeypatch):
     p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert p.returncode == 0 and "fused ok" in p.stdout, p.stderr[-2000:]
+
+
+@pytest.mark.parametrize("mode,seg,parts", [("0", "1", "0"), ("2", "0", "0"), ("2", "1", "1"), ("3", "1", "0"),
+                                            ("4", "1", "0"), ("4", "1", "1")])
+def test_pair_schedules(mode, seg, parts):
+    """Every GMRES-pair schedule (VSIE_PAIR_G4: 0 per-chi k_gemv_nt chains, 2 batched TMA G4
+    pass with (VSIE_SEG_G3=1) or without the batched TMA G3 steps, 3 six concurrent chains,
+    4 every step one batched launch; VSIE_W2_PARTS=1 leaves the G2^T split-K partials to the
+    G3^T kernel) equals the oracle matvecs and the separate applies,
+    at cfg 1 (ragged ranks) and cfg 2 (several tiles, 148-CTA row blocks); op T and op C.
+    Subprocess: the switches are read once per process."""
+    import subprocess, sys, textwrap, os
+    code = textwrap.dedent('''
+        import sys; sys.path.insert(0, "tests")
+        import synth, numpy as np, torch
+        from oracle import ttmv, validate
+        from gpu_common import grid_of, rand_tts
+        from paper_2206_12409_b200 import Coupling
+        for ci in (1, 2):
+            cfg = synth.get_config(ci)
+            r = cfg.ranks_probe
+            tts = rand_tts(cfg, [r, (r[0] + 1, r[1] - 3, r[2] + 5), (max(1, r[0] - 1), r[1] + 2, r[2] - 7)], 700 + ci)
+            h = Coupling.from_cores(grid_of(cfg), cfg.meshes(), cfg.freq, tts, nrhs_max=1)
+            x = synth.complex_gaussian(cfg.m, 51)
+            u = synth.complex_gaussian(3 * cfg.n_v, 52)
+            xd, ud = torch.from_numpy(x).cuda(), torch.from_numpy(u).cuda()
+            for adj in ("T", "C"):
+                y, z = h.apply_pair(xd, ud, adj)
+                y2, z2 = h.apply_pair(xd, ud, adj)
+                assert torch.equal(y, y2) and torch.equal(z, z2), "not reproducible"
+                y, z = y.cpu().numpy(), z.cpu().numpy()
+                assert validate.rel_l2(y, h.apply(xd, "N").cpu().numpy()) <= 1e-13, (ci, adj)
+                assert validate.rel_l2(z, h.apply(ud, adj).cpu().numpy()) <= 1e-13, (ci, adj)
+                if ci == 1 or adj == "T":
+                    assert validate.rel_l2(y, ttmv.apply(tts, x, "N")) <= 1e-12, (ci, adj)
+                    assert validate.rel_l2(z, ttmv.apply(tts, u, adj)) <= 1e-12, (ci, adj)
+        print("schedule ok")
+    ''')
+    env = dict(os.environ, VSIE_PAIR_G4=mode, VSIE_SEG_G3=seg, VSIE_W2_PARTS=parts)
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert p.returncode == 0 and "schedule ok" in p.stdout, p.stderr[-2000:]
