@@ -197,8 +197,14 @@ int32_t vsie_coupling_apply(vsie_coupling_t h, const void* x, void* y, int32_t o
  * body rows need Z_bc j_c, the conductor rows Z_cb j_b = Z_bc^T j_b, Eqs. 17-19):
  * y = Z x (layouts as OP_N above) and z = Z^T u (adj_op = OP_T) or Z^H u (OP_C) (layouts
  * as OP_T), single right-hand side, in one call.  The transpose's G1-G3 steps run first
- * so that both directions' G4 products share one pass over the largest core.  Results
- * equal two vsie_coupling_apply calls to rounding.  Asynchronous; collective when world > 1. */
+ * so that both directions' G4 products share one pass over the largest core (one TMA-
+ * streamed launch over the three chi, which also forms the chi sum of Eq. 18); the G3
+ * steps of both directions are likewise one batched launch each.  Results equal two
+ * vsie_coupling_apply calls to rounding and are bitwise reproducible.  The schedule is
+ * selected by the environment (read once per process): VSIE_PAIR_G4 = 2
+ * (default, as described), 0 (per-chi chains, G4 pair per chain), 3 (forward and
+ * transpose as six independent chains), 4 (every step one batched launch on the stream).
+ * Asynchronous; collective when world > 1. */
 int32_t vsie_coupling_apply_pair(vsie_coupling_t h, const void* x, void* y, const void* u, void* z, int32_t adj_op,
                                  void* stream);
 
@@ -207,7 +213,12 @@ int32_t vsie_coupling_apply_pair(vsie_coupling_t h, const void* x, void* y, cons
 int32_t vsie_coupling_apply_host(vsie_coupling_t h, const void* x_host, void* y_host, int32_t op,
                                  int32_t nrhs);
 
-/* apply_pair with HOST buffers (H2D of x and u, the pair, D2H of y and z; synchronous). */
+/* apply_pair with HOST buffers (H2D of x and u, the pair, D2H of y and z; synchronous).
+ * Pinned host buffers are strongly recommended (pageable ones serialise the copies).
+ * Single process, chain schedule: the forward (needs only x) runs first on one stream and
+ * its voxel result is copied out while u is copied in on a second stream for the
+ * transpose, so the two large copies overlap; the results equal apply_pair's to rounding
+ * (the G4 pass is not shared in this schedule).  Otherwise the fused device pair. */
 int32_t vsie_coupling_apply_pair_host(vsie_coupling_t h, const void* x_host, void* y_host, const void* u_host,
                                       void* z_host, int32_t adj_op);
 

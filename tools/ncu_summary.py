@@ -38,7 +38,9 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__block_size", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_fp64.sum", "lts__t_bytes.sum", "launch__occupancy_limit_registers",
         "sm__pipe_tensor_op_dmma_cycles_active.avg.pct_of_peak_sustained_active",
-        "smsp__average_warp_latency_issue_stalled_long_scoreboard.ratio"]
+        "smsp__average_warp_latency_issue_stalled_long_scoreboard.ratio",
+        "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active"]
 
 
 def full(path):
