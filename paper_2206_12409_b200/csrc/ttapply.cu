@@ -493,15 +493,18 @@ __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant_
 // W1[a + r1 c] = sum_i1 G1[i1 + n1 a] u[i1 + n1 c] (conj(u) for op C): warp task =
 // 8 columns x all a (NT n-tiles of 8); u fragments streamed from global (each
 // lane 16 B, 64 contiguous bytes per column), G1 fragments from shared memory.
+constexpr int kRedWarps = 4;                  // 128-thread CTAs: 3 resident per SM
+constexpr int kRedThreads = 32 * kRedWarps;
+
 template <int NT>
-__global__ void __launch_bounds__(kG1Threads) k_reduce_g1(const __grid_constant__ ReduceArgs a) {
+__global__ void __launch_bounds__(kRedThreads) k_reduce_g1(const __grid_constant__ ReduceArgs a) {
   const int b = blockIdx.y;
   const int n1 = a.n1, r1 = a.r1[b];
   const int ks_n = (n1 + 3) / 4;
   extern __shared__ cplx Bf[];   // [ks_n][NT][32] fragments of G1
   const cplx* __restrict__ G1 = a.G1[b];
   // G1 is a constant core: staged before waiting on the stream predecessor (PDL overlap)
-  for (int e = threadIdx.x; e < ks_n * NT * 32; e += kG1Threads) {
+  for (int e = threadIdx.x; e < ks_n * NT * 32; e += kRedThreads) {
     const int lane = e % 32, nt = (e / 32) % NT, ks = e / (32 * NT);
     const int k = 4 * ks + (lane & 3), n = 8 * nt + (lane >> 2);
     Bf[e] = (k < n1 && n < r1) ? __ldg(G1 + k + (int64_t)n1 * n) : cmk(0, 0);
@@ -511,9 +514,9 @@ __global__ void __launch_bounds__(kG1Threads) k_reduce_g1(const __grid_constant_
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const double sgn = a.conj_u ? -1.0 : 1.0;
-  // persistent: warp tasks of 8 columns x all i1, UNR k-steps of loads in flight
+  // persistent: warp tasks of 8 columns x all i1, UNR k-steps (100 rows) of loads in flight
   const int64_t ntask = (a.ncol + kColsPerWarp - 1) / kColsPerWarp;
-  for (int64_t task = (int64_t)blockIdx.x * kWarpsG1 + warp; task < ntask; task += (int64_t)gridDim.x * kWarpsG1) {
+  for (int64_t task = (int64_t)blockIdx.x * kRedWarps + warp; task < ntask; task += (int64_t)gridDim.x * kRedWarps) {
     const int64_t cg = task * kColsPerWarp + g;
     const bool cok = cg < a.ncol;
     const cplx* __restrict__ U = a.u[b] + (cok ? col_addr(cg, a.cols_per_rhs, a.ld_rhs, n1) : 0);
@@ -521,7 +524,7 @@ __global__ void __launch_bounds__(kG1Threads) k_reduce_g1(const __grid_constant_
     double p1[NT][2], p2[NT][2], p3[NT][2];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) p1[nt][0] = p1[nt][1] = p2[nt][0] = p2[nt][1] = p3[nt][0] = p3[nt][1] = 0;
-    constexpr int UNR = 13;
+    constexpr int UNR = 25;   // n1 <= 100: the whole column tile in flight at once
     for (int ks = 0; ks < ks_n; ks += UNR) {
       cplx av[UNR];
 #pragma unroll
@@ -872,14 +875,14 @@ void set_smem_attr_once(F* f, bool& done) {
 
 // persistent G1-step grids: 4 resident CTAs of 256 threads per SM over the batch
 // (VSIE_G1_CTAS_PER_SM overrides)
-int64_t g1_ctas_per_chi(int nbatch, const void* fn, size_t smem) {
+int64_t g1_ctas_per_chi(int nbatch, const void* fn, size_t smem, int threads) {
   static const int per_sm_env = [] {
     const char* e = std::getenv("VSIE_G1_CTAS_PER_SM");
     return e ? std::max(1, std::atoi(e)) : 0;
   }();
   int occ = per_sm_env;
   if (!occ) {
-    VSIE_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kG1Threads, smem));
+    VSIE_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem));
     occ = std::max(1, occ);
   }
   return std::max<int64_t>(1, (int64_t)sm_count() * occ / std::max(1, nbatch));
@@ -897,7 +900,7 @@ void launch_expand_g1(const ExpandArgs& a, cudaStream_t st) {
     static bool d = false;                                                                                 \
     set_smem_attr_once(k_expand_g1<K>, d);                                                                 \
     dim3 grid((unsigned)std::min<int64_t>(ceil_div(a.ncol, kColsPerCtaG1),                                 \
-                                          g1_ctas_per_chi(a.nbatch, (const void*)k_expand_g1<K>, smem)), a.nbatch); \
+                                          g1_ctas_per_chi(a.nbatch, (const void*)k_expand_g1<K>, smem, kG1Threads)), a.nbatch); \
     launch_pdl(k_expand_g1<K>, grid, dim3(kG1Threads), smem, st, a);                                       \
     break;                                                                                                 \
   }
@@ -919,9 +922,9 @@ void launch_reduce_g1(const ReduceArgs& a, cudaStream_t st) {
   case K: {                                                                                                \
     static bool d = false;                                                                                 \
     set_smem_attr_once(k_reduce_g1<K>, d);                                                                 \
-    dim3 grid((unsigned)std::min<int64_t>(ceil_div(a.ncol, kColsPerCtaG1),                                 \
-                                          g1_ctas_per_chi(a.nbatch, (const void*)k_reduce_g1<K>, smem)), a.nbatch); \
-    launch_pdl(k_reduce_g1<K>, grid, dim3(kG1Threads), smem, st, a);                                       \
+    dim3 grid((unsigned)std::min<int64_t>(ceil_div(a.ncol, kColsPerWarp * kRedWarps),                      \
+                                          g1_ctas_per_chi(a.nbatch, (const void*)k_reduce_g1<K>, smem, kRedThreads)), a.nbatch); \
+    launch_pdl(k_reduce_g1<K>, grid, dim3(kRedThreads), smem, st, a);                                      \
     break;                                                                                                 \
   }
   switch (NT) {
