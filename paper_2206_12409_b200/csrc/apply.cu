@@ -133,6 +133,18 @@ bool w2_parts_on() {
   return v != 0;
 }
 
+// fused transpose front (k_adj12: G1^T and G2^T in one launch over the three chi) in the
+// pair, opt-in VSIE_ADJ_FUSED=1: measured slower (cfg 2 pair 0.167 -> 0.195 ms): the G2
+// slices of the three resident CTAs per SM (3 x 91 KB) do not stay in L1 (65% hit rate)
+// and the lanes-over-beta contraction waits on L2
+bool adj_fused_on() {
+  static const int v = [] {
+    const char* e = std::getenv("VSIE_ADJ_FUSED");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v != 0;
+}
+
 bool fuse_g21() {
   // fused G2 + G1 forward tail (k_g21_fwd): measured 0.173 vs 0.167 ms per pair step at
   // cfg 2 (its 110 KB of smem leave one CTA per SM) -- opt-in
@@ -1179,14 +1191,46 @@ void pair_dag(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z
   for (Shard& s : h->shards)
     for (int c = 0; c < 3 && seg; ++c)
       seg = seg_gemv_supported(X.R(c, 1) * s.n3loc(), X.R(c, 2), s.g3b_ns) && s.n3loc() > 0;
-  fork(h, S);
-  for (int c = 0; c < 3; ++c) {
-    h->scope_chi = c;
-    for (Shard& s : h->shards) adj_front(X, s, c, u, cj, S.chi[c], nullptr, !seg);
+  // the fused G1^T + G2^T kernel (one launch over the three chi) replaces the chains
+  const bool fused_front = seg && adj_fused_on() && adj_front_supported(h->grid.n[0], X.r1m);
+  if (fused_front) {
+    const int n2 = h->grid.n[1];
+    for (Shard& s : h->shards) {
+      const int64_t n3l = s.n3loc();
+      AdjFrontArgs f{};
+      f.nbatch = 3;
+      f.n1 = h->grid.n[0];
+      f.n2 = n2;
+      f.n3l = (int)n3l;
+      f.conj_u = cj;
+      f.w2p_stride = (int64_t)X.r2m * n3l;
+      int64_t bytes = 0, fl = 0;
+      for (int c = 0; c < 3; ++c) {
+        f.G1[c] = h->G1[c].p;
+        f.G2[c] = h->G2[c].p;
+        f.u[c] = u + c * X.L.chi_stride + shard_voxel_offset(h, s, X.L);
+        f.W2p[c] = s.W2p.p + c * (int64_t)((n2 + 7) / 8) * X.r2m * n3l;
+        f.W2[c] = s.W2.p + c * X.r2m * n3l;
+        f.r1[c] = (int)X.R(c, 0);
+        f.r2[c] = (int)X.R(c, 1);
+        h->w2_parts[c] = 0;
+        bytes += 16 * ((int64_t)f.n1 * X.R(c, 0) + X.R(c, 0) * n2 * X.R(c, 1) + (int64_t)f.n1 * n2 * n3l +
+                       X.R(c, 1) * n3l);
+        fl += 8 * ((int64_t)f.n1 * X.R(c, 0) * n2 * n3l + X.R(c, 0) * n2 * X.R(c, 1) * n3l);
+      }
+      Scope sc(h, "adj_g12_fused", bytes, fl, S.main);
+      launch_adj_front(f, S.main);
+    }
+  } else {
+    fork(h, S);
+    for (int c = 0; c < 3; ++c) {
+      h->scope_chi = c;
+      for (Shard& s : h->shards) adj_front(X, s, c, u, cj, S.chi[c], nullptr, !seg);
+    }
+    h->scope_chi = -1;
   }
-  h->scope_chi = -1;
   if (seg) {
-    join(h, S);
+    if (!fused_front) join(h, S);
     for (Shard& s : h->shards) {
       const int64_t n3l = s.n3loc();
       SegGemv g{};

@@ -174,6 +174,7 @@ void handle_alloc_workspace(vsie_coupling_s* h) {
     s.z3.alloc(3 * (int64_t)r3m * k);
     s.Y3.alloc(3 * (int64_t)r2m * n3l * k);
     s.W2.alloc(3 * (int64_t)r2m * n3l * k);
+    s.W2p.alloc(3 * (int64_t)((n2 + 7) / 8) * r2m * n3l);
     s.Y2.alloc(3 * (int64_t)r1m * n2 * n3l * k);
     s.W1.alloc(3 * (int64_t)r1m * n2 * n3l * k);
     rmax_gemv = std::max(rmax_gemv, (int64_t)r2m * n3l);

@@ -30,6 +30,7 @@ struct Shard {
   DevBuf<cplx> Y2;      // [3][r1 * n2 * n3loc * nrhs]
   DevBuf<cplx> W1;      // [3][r1 * n2 * n3loc * nrhs]   (adjoint: G1^T u)
   DevBuf<cplx> W2;      // [3][r2 * n3loc * nrhs]
+  DevBuf<cplx> W2p;     // [3][ceil(n2 / 8)][r2 * n3loc]  fused transpose front: W2 partials
   DevBuf<cplx> z3;      // [3][r3max * nrhs]
   DevBuf<cplx> zpart;   // [3][mloc_max * nrhs]  transpose: per-chi G4_chi^T z3_chi
   // single-RHS persistent apply (mega.cu): plan, partials, sync words

@@ -118,6 +118,23 @@ struct SegGemv {
 };
 bool launch_seg_gemv(const SegGemv& a, bool transpose, cudaStream_t st);
 bool seg_gemv_supported(int64_t R, int64_t C, int nsb);
+// Fused transpose front (adjfront.cu), single RHS, batched over chi: W1 = G1^T u and
+// W2p[blk] = G2[:, blk, :]^T W1[:, blk, :] per block of 8 i2 values (W2p[b][blk *
+// w2p_stride + beta + r2 i3]), then W2[b] = sum_blk W2p[b][blk] in fixed order.
+struct AdjFrontArgs {
+  const cplx* G1[3];
+  const cplx* G2[3];
+  const cplx* u[3];     // voxel column (i2, i3) at u + n1 (i2 + n2 i3)
+  cplx* W2p[3];
+  cplx* W2[3];          // r2 x n3l column-major
+  int64_t w2p_stride;   // >= r2 n3l
+  int n1, n2, n3l;
+  int r1[3], r2[3];
+  int nbatch;
+  bool conj_u;
+};
+bool adj_front_supported(int n1, int r1max);
+void launch_adj_front(const AdjFrontArgs& a, cudaStream_t st);
 // fixed-order sum of ns split partials ([b][s][rmax]) into a.y[b][0 .. a.R[b])
 void launch_gemv_sum(const GemvN& a, cplx* partials, int ns, int64_t rmax, cudaStream_t st);
 int sm_count_dev();
