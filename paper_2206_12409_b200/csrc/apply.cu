@@ -314,15 +314,23 @@ void adj_front(const Ctx& X, Shard& s, int c, const cplx* u, bool cj, cudaStream
     z.B[0] = W1; z.ldb[0] = r1 * n2;
     z.C[0] = W2; z.ldc[0] = r2;
     const int64_t bytes = 16 * (r1 * n2 * r2 + r2 * n3l * k + r1 * n2 * n3l * k);
-    Scope sc(h, "adj_g2_zgemm", bytes, 8 * r1 * n2 * r2 * n3l * k, st);
     h->w2_parts[c] = 0;
-    if (!with_g3 && k == 1 && h->shards.size() == 1 && w2_parts_on()) {
-      // the batched G3^T kernel sums the split-K partials of W2 on load
-      int64_t stride = 0;
-      h->w2_parts[c] = launch_zgemm_dmma_parts(z, X.zws(c), h->zgemm_ws_per_chi, st, &stride);
-      h->w2_part_stride[c] = stride;
-    } else {
-      launch_zgemm_dmma(z, X.zws(c), h->zgemm_ws_per_chi, st);
+    int parts = 0;
+    int64_t stride = 0;
+    {
+      // the GEMM and its split-K sum are timed as two kernels (bench roofline per kernel)
+      Scope sc(h, "adj_g2_zgemm", bytes, 8 * r1 * n2 * r2 * n3l * k, st);
+      parts = launch_zgemm_dmma_parts(z, X.zws(c), h->zgemm_ws_per_chi, st, &stride);
+    }
+    if (parts > 0) {
+      if (!with_g3 && k == 1 && h->shards.size() == 1 && w2_parts_on()) {
+        // the batched G3^T kernel sums the split-K partials of W2 on load
+        h->w2_parts[c] = parts;
+        h->w2_part_stride[c] = stride;
+      } else {
+        Scope sc(h, "adj_g2_splitk_sum", 16 * (parts + 1) * r2 * n3l * k, 8 * parts * r2 * n3l * k, st);
+        launch_splitk_sum(z, X.zws(c), parts, stride, st);
+      }
     }
   }
   if (mid) VSIE_CHECK_CUDA(cudaEventRecord(mid, st));   // chain staggering: G1/G2 steps done

@@ -216,6 +216,8 @@ void launch_zgemm_dmma(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t 
 // same, but a split-K result is left as partials for the consumer to sum: returns 0 when C
 // was written, else the number of splits S with C_b = sum_q ws[(b S + q) *part_stride + m + M n]
 int launch_zgemm_dmma_parts(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t st, int64_t* part_stride);
+// C = sum of the split partials left by launch_zgemm_dmma_parts (fixed order)
+void launch_splitk_sum(const Zgemm& g, const cplx* ws, int splits, int64_t stride, cudaStream_t st);
 
 // conj in place
 void launch_conj(cplx* x, int64_t n, cudaStream_t st);

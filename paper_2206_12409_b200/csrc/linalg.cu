@@ -542,6 +542,15 @@ int launch_zgemm_dmma_parts(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStre
   return 0;
 }
 
+void launch_splitk_sum(const Zgemm& g, const cplx* ws, int splits, int64_t stride, cudaStream_t st) {
+  if (splits <= 0) return;
+  int64_t mn = 0;
+  for (int b = 0; b < g.nbatch; ++b) mn = std::max(mn, g.M[b] * g.N[b]);
+  dim3 rg((unsigned)std::min<int64_t>(ceil_div(mn, 256), 148 * 8), g.nbatch);
+  launch_pdl(k_splitk_reduce, rg, dim3(256), 0, st, g, splits, ws, stride);
+  VSIE_CHECK_LAUNCH();
+}
+
 void launch_conj(cplx* x, int64_t n, cudaStream_t st) {
   if (n <= 0) return;
   k_conj<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 148 * 8), 256, 0, st>>>(x, n);
