@@ -163,6 +163,13 @@ def ranks_hint(cfg):
     return [tuple(cfg.ranks_probe)] * 3
 
 
+def workload_name(cfg, k):
+    """The config.workload string of both arms (identical for the driver's ratio)."""
+    return (f"cfg{cfg.idx} {cfg.name}: grid {cfg.n}, h {cfg.h[0]*1e3:.0f} mm, m={cfg.m} RWG "
+            f"({' + '.join(f'{s.name} {s.n_az}x{s.n_ax}' for s in cfg.surfaces)}), "
+            f"f=298.2 MHz, tol {cfg.tol}, nrhs {k}")
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle on the host cores (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -182,7 +189,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": val, "unit": "GB/s", "n_gpus": 0, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": f"cfg{cfg.idx} {cfg.name}", "grid": list(cfg.n), "m": cfg.m, "tol": cfg.tol,
+        "config": {"workload": workload_name(cfg, cfg.nrhs), "grid": list(cfg.n), "m": cfg.m, "tol": cfg.tol,
                    "ranks": ranks, "step": "TT forward + transpose apply (oracle/ttmv.py, NumPy einsum)"},
         "cpu_baseline": {"value": val, "unit": "GB/s", "cores": cores, "kind": "oracle",
                          "sample": f"{args.steps} full GMRES steps of cfg{cfg.idx} with random cores at the GPU ranks",
@@ -481,9 +488,7 @@ def main():
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": f"cfg{cfg.idx} {cfg.name}: grid {cfg.n}, h {cfg.h[0]*1e3:.0f} mm, m={cfg.m} RWG "
-                               f"({' + '.join(f'{s.name} {s.n_az}x{s.n_ax}' for s in cfg.surfaces)}), "
-                               f"f=298.2 MHz, tol {cfg.tol}, nrhs {k}",
+        "config": {"workload": workload_name(cfg, k),
                    "step": (f"1 forward (y = Z x) + 1 transpose (z = Z^T u) TT apply as ONE vsie_coupling_apply_pair "
                             f"call (the coupling pair of a GMRES matvec; both G4 products share one pass over G4)"
                             if use_pair else f"1 forward (Y = Z X) + 1 transpose (Z^T U) TT apply, {k} RHS"),
