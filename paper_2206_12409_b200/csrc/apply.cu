@@ -276,7 +276,7 @@ void fwd_rest(const Ctx& X, Shard& s, int c, cplx* y, cudaStream_t st, cudaEvent
 // ------------------------------------------------------------------ transpose chain pieces (one chi)
 // W1 = G1^T u, W2 = G2^T W1, z3 = G3^T W2: partial z3 per shard
 void adj_front(const Ctx& X, Shard& s, int c, const cplx* u, bool cj, cudaStream_t st, cudaEvent_t mid = nullptr,
-               bool with_g3 = true) {
+               bool with_g3 = true, bool with_g1 = true) {
   vsie_coupling_s* h = X.h;
   const int k = X.k;
   const int n1 = h->grid.n[0], n2 = h->grid.n[1];
@@ -289,7 +289,7 @@ void adj_front(const Ctx& X, Shard& s, int c, const cplx* u, bool cj, cudaStream
   const int64_t r1 = X.R(c, 0), r2 = X.R(c, 1), r3 = X.R(c, 2);
   cplx* W1 = s.W1.p + c * X.r1m * n2 * n3l * k;
   cplx* W2 = s.W2.p + c * X.r2m * n3l * k;
-  {
+  if (with_g1) {
     ReduceArgs r{};
     r.nbatch = 1;
     r.n1 = n1;
@@ -1230,10 +1230,38 @@ void pair_dag(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z
       launch_adj_front(f, S.main);
     }
   } else {
+    // W1 = G1^T u for the three chi as one TMA-streamed launch when supported, then the
+    // G2^T steps as per-chi chains
+    bool g1_done = false;
+    if (seg && reduce_tma_on()) {
+      g1_done = true;
+      for (Shard& s : h->shards) {
+        const int64_t n3l = s.n3loc();
+        ReduceArgs r{};
+        r.nbatch = 3;
+        r.n1 = h->grid.n[0];
+        r.ncol = (int64_t)h->grid.n[1] * n3l;
+        r.cols_per_rhs = r.ncol;
+        r.ld_rhs = X.L.ld;
+        r.conj_u = cj;
+        int64_t bytes = 0, fl = 0;
+        for (int c = 0; c < 3; ++c) {
+          r.G1[c] = h->G1[c].p;
+          r.u[c] = u + c * X.L.chi_stride + shard_voxel_offset(h, s, X.L);
+          r.W1[c] = s.W1.p + c * X.r1m * h->grid.n[1] * n3l;
+          r.r1[c] = (int)X.R(c, 0);
+          bytes += 16 * ((int64_t)r.n1 * X.R(c, 0) + X.R(c, 0) * r.ncol + (int64_t)r.n1 * r.ncol);
+          fl += 8 * (int64_t)r.n1 * X.R(c, 0) * r.ncol;
+        }
+        Scope sc(h, "adj_g1_reduce_tma", bytes, fl, S.main);
+        g1_done = g1_done && n3l > 0 && launch_reduce_g1_tma(r, S.main);
+      }
+      VSIE_REQUIRE(g1_done || h->shards.size() == 1, VSIE_ERR_STATE, "reduce_tma on a partial shard set");
+    }
     fork(h, S);
     for (int c = 0; c < 3; ++c) {
       h->scope_chi = c;
-      for (Shard& s : h->shards) adj_front(X, s, c, u, cj, S.chi[c], nullptr, !seg);
+      for (Shard& s : h->shards) adj_front(X, s, c, u, cj, S.chi[c], nullptr, !seg, !g1_done);
     }
     h->scope_chi = -1;
   }

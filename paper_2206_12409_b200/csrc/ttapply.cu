@@ -911,7 +911,18 @@ void launch_expand_g1(const ExpandArgs& a, cudaStream_t st) {
   VSIE_CHECK_LAUNCH();
 }
 
+// the TMA-streamed batched reduction (reduce_tma.cu) for batched single-RHS calls;
+// VSIE_REDUCE_TMA=0 keeps k_reduce_g1
+bool reduce_tma_on() {
+  static const int v = [] {
+    const char* e = std::getenv("VSIE_REDUCE_TMA");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
 void launch_reduce_g1(const ReduceArgs& a, cudaStream_t st) {
+  if (a.nbatch > 1 && reduce_tma_on() && launch_reduce_g1_tma(a, st)) return;
   int r1max = 0;
   for (int b = 0; b < a.nbatch; ++b) r1max = std::max(r1max, a.r1[b]);
   VSIE_REQUIRE(r1max <= 32, VSIE_ERR_ARG, "reduce: r1 > 32 not supported");
