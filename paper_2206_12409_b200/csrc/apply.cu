@@ -1233,7 +1233,7 @@ void pair_dag(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z
     // W1 = G1^T u for the three chi as one TMA-streamed launch when supported, then the
     // G2^T steps as per-chi chains
     bool g1_done = false;
-    if (seg && reduce_tma_on()) {
+    if (seg && reduce_tma_on() && reduce_tma_fits(h->grid.n[0], X.r1m)) {
       g1_done = true;
       for (Shard& s : h->shards) {
         const int64_t n3l = s.n3loc();

@@ -177,6 +177,7 @@ void launch_reduce_g1(const ReduceArgs& a, cudaStream_t st);
 // TMA-streamed W1 = G1^T u over the batch in one persistent launch (reduce_tma.cu), single
 // RHS; false when unsupported (the caller uses launch_reduce_g1)
 bool launch_reduce_g1_tma(const ReduceArgs& a, cudaStream_t st);
+bool reduce_tma_fits(int n1, int r1max);
 bool reduce_tma_on();
 
 // out[i + ld_out j] = sum_{c<3} in[c * chi_stride + i + ld_in j] (fixed order), conj if asked;

@@ -161,41 +161,53 @@ void launch_rt(const ReduceArgs& a, int ns, size_t smem, cudaStream_t st) {
 
 }  // namespace
 
-// false when unsupported (the caller uses k_reduce_g1): single RHS only, r1 <= 18
-bool launch_reduce_g1_tma(const ReduceArgs& a, cudaStream_t st) {
-  int r1max = 0, r1min = 1 << 30;
-  for (int b = 0; b < a.nbatch; ++b) {
-    r1max = std::max(r1max, a.r1[b]);
-    r1min = std::min(r1min, a.r1[b]);
-  }
-  if (a.cols_per_rhs != a.ncol || r1max > 18 || r1max < 1 || a.n1 < 1) return false;
-  if (a.ncol == 0) return true;
-  // DMMA tiles for 8 NTD values of a, DFMA for the rest (<= 2)
-  int ntd = r1max / 8, rem = r1max % 8;
+namespace {
+// ring geometry: consumer warps x slots per warp within the ring budget, at least two slots
+// per warp (a single-buffered warp waits a full refill latency after every stage);
+// VSIE_RT_CW overrides the number of consumer warps (2, 4 or 8).  false if it cannot fit.
+bool rt_geometry(int n1, int r1max, int& ntd, int& rem, int& cw, int& spw, size_t& smem) {
+  if (r1max > 18 || r1max < 1 || n1 < 1) return false;
+  ntd = r1max / 8;
+  rem = r1max % 8;
   if (rem > 2) {
     ntd += 1;
     rem = 0;
   }
-  const int ks_n = (a.n1 + 3) / 4;
-  const size_t stage = (size_t)16 * 8 * a.n1;
+  const int ks_n = (n1 + 3) / 4;
+  const size_t stage = (size_t)16 * 8 * n1;
   const size_t fr = (size_t)3 * ks_n * std::max(ntd, 1) * 32 * 16 + (size_t)3 * 4 * ks_n * rem * 16;
-  // consumer warps x slots per warp within the ring budget: at least two slots per warp
-  // (a single-buffered warp waits a full refill latency after every stage); VSIE_RT_CW
-  // overrides the number of consumer warps (2, 4 or 8)
   static const int cw_env = [] {
     const char* e = std::getenv("VSIE_RT_CW");
     return e ? std::atoi(e) : 0;
   }();
-  int cw = cw_env == 2 || cw_env == 4 || cw_env == 8 ? cw_env : 8;
-  int spw = 3;
+  cw = cw_env == 2 || cw_env == 4 || cw_env == 8 ? cw_env : 8;
+  spw = 3;
   while (spw > 1 && cw * spw * stage > (size_t)kRTRing) --spw;
   while (cw > 2 && (cw * spw * stage > (size_t)kRTRing || (spw < 2 && cw_env == 0))) {
     cw /= 2;
     spw = 3;
     while (spw > 1 && cw * spw * stage > (size_t)kRTRing) --spw;
   }
-  const size_t smem = cw * spw * stage + fr;
-  if (cw * spw * stage > (size_t)kRTRing || smem > 220 * 1024) return false;
+  smem = cw * spw * stage + fr;
+  return cw * spw * stage <= (size_t)kRTRing && smem <= 220 * 1024;
+}
+}  // namespace
+
+bool reduce_tma_fits(int n1, int r1max) {
+  int ntd, rem, cw, spw;
+  size_t smem;
+  return rt_geometry(n1, r1max, ntd, rem, cw, spw, smem);
+}
+
+// false when unsupported (the caller uses k_reduce_g1): single RHS only, r1 <= 18
+bool launch_reduce_g1_tma(const ReduceArgs& a, cudaStream_t st) {
+  int r1max = 0;
+  for (int b = 0; b < a.nbatch; ++b) r1max = std::max(r1max, a.r1[b]);
+  if (a.cols_per_rhs != a.ncol) return false;
+  if (a.ncol == 0) return true;
+  int ntd, rem, cw, spw;
+  size_t smem;
+  if (!rt_geometry(a.n1, r1max, ntd, rem, cw, spw, smem)) return false;
   const int ns = sm_count_dev();
 #define VSIE_RT(NTD, REM)                                                                    \
   if (ntd == NTD && rem == REM) {                                                            \
