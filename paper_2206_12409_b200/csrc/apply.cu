@@ -104,7 +104,9 @@ constexpr int kMaxSplits = 256;
 
 // GMRES pair schedule: 0 = k_gemv_nt per chi chain, 2 = one TMA-streamed launch over the
 // three chi (k_pair_g4, chi sum of Eq. 18 fused), 3 = forward and transpose as six
-// independent concurrent chains (single shard only); VSIE_PAIR_G4 overrides
+// independent concurrent chains (single shard only), 4 = every step one batched launch,
+// 5 = streaming passes overlapped with the other direction's G1 / G2 chains (G4 read
+// twice, G3 once for both directions; single shard); VSIE_PAIR_G4 overrides
 int pair_g4_mode() {
   static const int v = [] {
     const char* e = std::getenv("VSIE_PAIR_G4");
@@ -1174,6 +1176,87 @@ void pair_dag(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z
   const bool exchange = h->comm != nullptr || h->shards.size() > 1;
   const int64_t m = h->m, mp = ceil_div(m, h->world);
   if (pair_g4_mode() == 4 && pair_batched(h, x, y, u, z, cj, S.main)) return;
+  if (pair_g4_mode() == 5 && !exchange && X.r3m <= pair_g4_max_rank()) {
+    // overlap schedule: the forward's G4 pass (needs only x) streams while the transpose's
+    // G1 / G2 steps compute in the chi chains; one pass over G3 serves both directions;
+    // the transpose's G4 pass streams while the forward's G2 / G1 steps compute
+    Shard& s = h->shards[0];
+    const int64_t n3l = s.n3loc();
+    bool ok = n3l > 0 && s.mloc() > 0;
+    for (int c = 0; c < 3 && ok; ++c) ok = seg_gemv_supported(X.R(c, 1) * n3l, X.R(c, 2), s.g3b_ns);
+    if (ok) {
+      cplx* part2 = h->partials.p + 3 * h->partials_per_chi;   // not used by the chains
+      fork(h, S);
+      {
+        PairG4 p{};
+        p.nbatch = 3;
+        p.C = s.mloc();
+        p.x = x + s.cb;
+        p.partials = part2;
+        p.rstride = X.r3m;
+        for (int c = 0; c < 3; ++c) {
+          p.A[c] = s.G4[c].p;
+          p.y4[c] = s.y4.p + c * X.r3stride;
+          p.R[c] = X.R(c, 2);
+        }
+        Scope sc(h, "fwd_g4_tma", 16 * (X.R(0, 2) + X.R(1, 2) + X.R(2, 2)) * (p.C + 1) + 16 * p.C,
+                 8 * (X.R(0, 2) + X.R(1, 2) + X.R(2, 2)) * p.C, S.main);
+        VSIE_REQUIRE(launch_pair_g4(p, sm_count_dev(), S.main), VSIE_ERR_STATE, "pair mode 5: G4 shape");
+      }
+      for (int c = 0; c < 3; ++c) {
+        h->scope_chi = c;
+        adj_front(X, s, c, u, cj, S.chi[c], nullptr, false, true);
+      }
+      h->scope_chi = -1;
+      join(h, S);
+      {
+        SegGemv g{};
+        g.nbatch = 3;
+        g.nsb = s.g3b_ns;
+        g.partials = part2;
+        g.rstride = X.r3m;
+        int64_t bytes = 0;
+        for (int c = 0; c < 3; ++c) {
+          g.A[c] = s.G3b[c].p;
+          g.x[c] = s.y4.p + c * X.r3stride;
+          g.y[c] = s.Y3.p + c * X.r2m * n3l;
+          g.xt[c] = s.W2.p + c * X.r2m * n3l;
+          g.yt[c] = s.z3.p + c * X.r3stride;
+          g.xparts[c] = 0;
+          g.R[c] = X.R(c, 1) * n3l;
+          g.C[c] = X.R(c, 2);
+          bytes += 16 * (g.R[c] * g.C[c] + 2 * (g.R[c] + g.C[c]));
+        }
+        Scope sc(h, "g3_seg_both", bytes, bytes, S.main);
+        VSIE_REQUIRE(launch_seg_gemv_mode(g, 3, S.main), VSIE_ERR_STATE, "pair mode 5: G3 shape");
+      }
+      fork(h, S);
+      {
+        PairG4 p{};
+        p.nbatch = 3;
+        p.C = s.mloc();
+        p.z = z + s.cb;
+        p.conj_z = cj;
+        p.partials = part2;
+        p.rstride = X.r3m;
+        for (int c = 0; c < 3; ++c) {
+          p.A[c] = s.G4[c].p;
+          p.z3[c] = s.z3.p + c * X.r3stride;
+          p.R[c] = X.R(c, 2);
+        }
+        Scope sc(h, "adj_g4_tma", 16 * (X.R(0, 2) + X.R(1, 2) + X.R(2, 2)) * (p.C + 1) + 16 * p.C,
+                 8 * (X.R(0, 2) + X.R(1, 2) + X.R(2, 2)) * p.C, S.main);
+        VSIE_REQUIRE(launch_pair_g4(p, sm_count_dev(), S.main), VSIE_ERR_STATE, "pair mode 5: G4 shape");
+      }
+      for (int c = 0; c < 3; ++c) {
+        h->scope_chi = c;
+        fwd_rest(X, s, c, y, S.chi[c], nullptr, false);
+      }
+      h->scope_chi = -1;
+      join(h, S);
+      return;
+    }
+  }
   if (pair_g4_mode() == 3 && !exchange) {
     // both directions as six independent chains (transpose chains on S.chi, forward chains
     // on S.chi2, separate workspaces): G4 is read twice but no chain waits for another

@@ -81,6 +81,7 @@ bool launch_gemv_nt(const GemvNT& a, cplx* partials, int64_t partials_cap, cudaS
 // TMA-streamed G4 pass of the GMRES pair (pairg4.cu): for every chi b < nbatch,
 // y4[b] = A[b] x (CTA partials at partials[(b ns + s) rstride + r], summed in fixed order)
 // and z = sum_b A[b]^T z3[b] (conj if conj_z), one read of every A[b] (R[b] x C, R <= 320).
+// x == nullptr: transpose only; z3[0] == nullptr: forward only.
 struct PairG4 {
   const cplx* A[3];
   const cplx* z3[3];
@@ -115,7 +116,12 @@ struct SegGemv {
   const cplx* xpart[3];
   int xparts[3];
   int64_t xpart_stride[3];
+  // mode 3 (both directions from one pass): op T input xt (W2) and output yt (z3)
+  const cplx* xt[3];
+  cplx* yt[3];
+  int64_t cmax;       // set by the launcher
 };
+bool launch_seg_gemv_mode(const SegGemv& a, int mode, cudaStream_t st);
 bool launch_seg_gemv(const SegGemv& a, bool transpose, cudaStream_t st);
 bool seg_gemv_supported(int64_t R, int64_t C, int nsb);
 // Fused transpose front (adjfront.cu), single RHS, batched over chi: W1 = G1^T u and

@@ -42,8 +42,12 @@ struct StageMap {
 
 // Stage i (global over the chi sequence) lives in slot i % kSlots and is consumed by warp
 // i % kConsumerWarps alone: no cross-warp barrier per stage, each warp double-buffered.
-template <int NQ>
+// MODE: 3 both products (the GMRES pair), 1 forward only (y4 = G4 x), 2 transpose only
+// (z = sum_chi G4^T z3) -- the single-direction variants let a pass run beside the other
+// direction's compute-bound steps (VSIE_PAIR_G4=5)
+template <int NQ, int MODE>
 __global__ void __launch_bounds__(kPairThreads, 1) k_pair_g4(const __grid_constant__ PairG4 a) {
+  constexpr bool FW = (MODE & 1) != 0, TR = (MODE & 2) != 0;
   extern __shared__ __align__(128) unsigned char smem[];
   cplx* ring = reinterpret_cast<cplx*>(smem);
   cplx* red = reinterpret_cast<cplx*>(smem + kRingBytes);                 // [4][32 NQ]
@@ -104,11 +108,13 @@ __global__ void __launch_bounds__(kPairThreads, 1) k_pair_g4(const __grid_consta
   // ---------------- consumers
   // x is the caller's input: staged before the wait (a per-column global load would sit
   // behind the HBM stream's queues)
-  for (int j = threadIdx.x; j < nc; j += 32 * kConsumerWarps) xs[j] = __ldg(a.x + c0 + j);
+  if (FW)
+    for (int j = threadIdx.x; j < nc; j += 32 * kConsumerWarps) xs[j] = __ldg(a.x + c0 + j);
   pdl_wait();   // z3 comes from the stream predecessor
-  for (int b = 0; b < a.nbatch; ++b)
-    for (int r = threadIdx.x; r < 32 * NQ; r += 32 * kConsumerWarps)
-      zs[b * 32 * NQ + r] = r < a.R[b] ? __ldcg(a.z3[b] + r) : cmk(0, 0);   // rows past R: zero weight
+  if (TR)
+    for (int b = 0; b < a.nbatch; ++b)
+      for (int r = threadIdx.x; r < 32 * NQ; r += 32 * kConsumerWarps)
+        zs[b * 32 * NQ + r] = r < a.R[b] ? __ldcg(a.z3[b] + r) : cmk(0, 0);   // rows past R: zero weight
   consumers_sync();
   for (int b = 0; b < a.nbatch; ++b) {
     const int R = (int)a.R[b];
@@ -117,7 +123,7 @@ __global__ void __launch_bounds__(kPairThreads, 1) k_pair_g4(const __grid_consta
     cplx zv[NQ], acc[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-      zv[q] = zs[b * 32 * NQ + lane + 32 * q];
+      zv[q] = TR ? zs[b * 32 * NQ + lane + 32 * q] : cmk(0, 0);
       acc[q] = cmk(0, 0);
     }
     // this warp's stages of chi b: global index i = off + t, t = warp - off mod 8, step 8
@@ -134,26 +140,36 @@ __global__ void __launch_bounds__(kPairThreads, 1) k_pair_g4(const __grid_consta
         const bool two = j + 1 < ncol;
         const cplx* col = st + R * j;
         const cplx* col1 = two ? col + R : col;
-        const cplx xv0 = xs[cb + j], xv1 = two ? xs[cb + j + 1] : cmk(0, 0);
+        const cplx xv0 = FW ? xs[cb + j] : cmk(0, 0), xv1 = FW && two ? xs[cb + j + 1] : cmk(0, 0);
         cplx d0 = cmk(0, 0), d1 = cmk(0, 0);
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
           const int r = min(32 * q, last) + lane;   // rows past R re-read row R - 1 (zero weight)
           const cplx v0 = col[r], v1 = col1[r];
-          cfma(d0, v0, zv[q]);
-          cfma(d1, v1, zv[q]);
-          cfma(acc[q], v0, xv0);
-          cfma(acc[q], v1, xv1);
+          if (TR) {
+            cfma(d0, v0, zv[q]);
+            cfma(d1, v1, zv[q]);
+          }
+          if (FW) {
+            cfma(acc[q], v0, xv0);
+            cfma(acc[q], v1, xv1);
+          }
         }
-        const cplx d = pair_reduce(d0, d1, lane);
-        const int jj = cb + j + (lane >> 4);
-        if ((lane & 15) == 0 && (lane == 0 || two)) zacc[jj] = b == 0 ? d : cadd(zacc[jj], d);
+        if (TR) {
+          const cplx d = pair_reduce(d0, d1, lane);
+          const int jj = cb + j + (lane >> 4);
+          if ((lane & 15) == 0 && (lane == 0 || two)) zacc[jj] = b == 0 ? d : cadd(zacc[jj], d);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
     }
     // y4 partial of this CTA: fixed-order tree over the 8 warps (w += w + 4, w + 2, w + 1);
     // the barriers also order this chi's zacc updates before the next chi's
+    if (!FW) {
+      consumers_sync();   // orders this chi's zacc updates before the next chi's
+      continue;
+    }
 #pragma unroll
     for (int half = kConsumerWarps / 2; half >= 1; half >>= 1) {
       if (warp >= half && warp < 2 * half) {
@@ -181,10 +197,11 @@ __global__ void __launch_bounds__(kPairThreads, 1) k_pair_g4(const __grid_consta
     }
   }
   pdl_trigger();
-  for (int j = threadIdx.x; j < nc; j += 32 * kConsumerWarps) {
-    const cplx v = zacc[j];
-    a.z[c0 + j] = a.conj_z ? cconj(v) : v;
-  }
+  if (TR)
+    for (int j = threadIdx.x; j < nc; j += 32 * kConsumerWarps) {
+      const cplx v = zacc[j];
+      a.z[c0 + j] = a.conj_z ? cconj(v) : v;
+    }
 }
 
 }  // namespace
@@ -205,24 +222,28 @@ bool launch_pair_g4(const PairG4& a, int max_ctas, cudaStream_t st) {
   PairG4 b = a;
   b.ccta = ccta;
   if (smem > 220 * 1024) return false;
-  switch (nq) {
-#define VSIE_PG4(K)                                                                                \
-  case K: {                                                                                        \
+  const int mode = (a.x ? 1 : 0) | (a.z3[0] ? 2 : 0);
+  if (mode == 0) return true;
+  switch (nq * 4 + mode) {
+#define VSIE_PG4M(K, M)                                                                            \
+  case K * 4 + M: {                                                                                \
     static size_t attr = 0;                                                                        \
     if (smem > attr) {                                                                             \
-      VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_pair_g4<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+      VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_pair_g4<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
       attr = smem;                                                                                 \
     }                                                                                              \
-    launch_pdl(k_pair_g4<K>, dim3(ns), dim3(kPairThreads), smem, st, b);                  \
+    launch_pdl(k_pair_g4<K, M>, dim3(ns), dim3(kPairThreads), smem, st, b);                        \
     break;                                                                                         \
   }
+#define VSIE_PG4(K) VSIE_PG4M(K, 1) VSIE_PG4M(K, 2) VSIE_PG4M(K, 3)
     VSIE_PG4(1) VSIE_PG4(2) VSIE_PG4(3) VSIE_PG4(4) VSIE_PG4(5) VSIE_PG4(6) VSIE_PG4(7) VSIE_PG4(8) VSIE_PG4(9)
     VSIE_PG4(10)
 #undef VSIE_PG4
+#undef VSIE_PG4M
     default: return false;
   }
   VSIE_CHECK_LAUNCH();
-  if (ns > 1) {
+  if (ns > 1 && a.x) {
     GemvN g{};
     g.nbatch = a.nbatch;
     for (int b = 0; b < a.nbatch; ++b) {

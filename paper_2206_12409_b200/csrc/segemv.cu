@@ -30,12 +30,15 @@ constexpr int kRing = kSlotsS * kStage;
 
 __device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kCW) : "memory"); }
 
-template <int NQ, bool OPT>
+// M: 1 op N (x -> y), 2 op T (xt -> yt through partials), 3 both from ONE pass over the core
+template <int NQ, int M>
 __global__ void __launch_bounds__(kSegThreads, 1) k_seg_gemv(const __grid_constant__ SegGemv a) {
+  constexpr bool FW = (M & 1) != 0, OPT = (M & 2) != 0;
   extern __shared__ __align__(128) unsigned char smem[];
   cplx* ring = reinterpret_cast<cplx*>(smem);
   cplx* red = reinterpret_cast<cplx*>(smem + kRing);   // [4][32 NQ]      (op N)
-  cplx* vec = red + 4 * 32 * NQ;                        // [Cmax]: x (op N) / partial z (op T)
+  cplx* vec = red + 4 * 32 * NQ;                        // [Cmax]: partial z (op T)
+  cplx* vecx = vec + a.cmax;                            // [Cmax]: x (op N)
   __shared__ uint64_t full[kSlotsS], empty[kSlotsS];
   const int ns = gridDim.x, s = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -123,12 +126,12 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_seg_gemv(const __grid_consta
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
           const int r = lane + 32 * q;
-          if (r < Lb) w[q] = __ldcg(a.x[b] + r0[b] + r);
+          if (r < Lb) w[q] = __ldcg(a.xt[b] + r0[b] + r);
         }
       }
     }
-    if (!OPT)
-      for (int c = threadIdx.x; c < C; c += 32 * kCW) vec[c] = __ldcg(a.x[b] + c);
+    if (FW)
+      for (int c = threadIdx.x; c < C; c += 32 * kCW) vecx[c] = __ldcg(a.x[b] + c);
     csync();
     if (Lb > 0) {
       for (int t = (warp - off[b] % kCW + kCW) % kCW; t < nst[b]; t += kCW) {
@@ -143,12 +146,18 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_seg_gemv(const __grid_consta
             const bool two = j + 1 < ncol;
             const cplx* col = st + Lb * j;
             const cplx* col1 = two ? col + Lb : col;
+            const cplx xv0 = FW ? vecx[cb + j] : cmk(0, 0), xv1 = FW && two ? vecx[cb + j + 1] : cmk(0, 0);
             cplx d0 = cmk(0, 0), d1 = cmk(0, 0);
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
               const int r = min(32 * q, last) + lane;
-              cfma(d0, col[r], w[q]);
-              cfma(d1, col1[r], w[q]);
+              const cplx v0 = col[r], v1 = col1[r];
+              cfma(d0, v0, w[q]);
+              cfma(d1, v1, w[q]);
+              if (FW) {
+                cfma(acc[q], v0, xv0);
+                cfma(acc[q], v1, xv1);
+              }
             }
             const cplx d = pair_reduce(d0, d1, lane);
             if ((lane & 15) == 0 && (lane == 0 || two)) vec[cb + j + (lane >> 4)] = d;
@@ -156,7 +165,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_seg_gemv(const __grid_consta
         } else {
           for (int j = 0; j < ncol; ++j) {
             const cplx* col = st + Lb * j;
-            const cplx xv = vec[cb + j];
+            const cplx xv = vecx[cb + j];
 #pragma unroll
             for (int q = 0; q < NQ; ++q) cfma(acc[q], col[min(32 * q, last) + lane], xv);
           }
@@ -170,7 +179,8 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_seg_gemv(const __grid_consta
       cplx* out = a.partials + ((int64_t)b * ns + s) * a.rstride;
       for (int c = threadIdx.x; c < C; c += 32 * kCW) out[c] = Lb > 0 ? vec[c] : cmk(0, 0);
       csync();   // vec is rewritten by the next chi
-    } else {
+    }
+    if (FW) {
 #pragma unroll
       for (int half = kCW / 2; half >= 1; half >>= 1) {
         if (warp >= half && warp < 2 * half) {
@@ -196,17 +206,17 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_seg_gemv(const __grid_consta
   pdl_trigger();
 }
 
-template <bool OPT>
+template <int M>
 bool launch_seg(const SegGemv& a, int ns, int nq, size_t smem, cudaStream_t st) {
   switch (nq) {
 #define VSIE_SEG(K)                                                                                  \
   case K: {                                                                                          \
     static size_t attr = 0;                                                                          \
     if (smem > attr) {                                                                               \
-      VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_seg_gemv<K, OPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+      VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_seg_gemv<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
       attr = smem;                                                                                   \
     }                                                                                                \
-    launch_pdl(k_seg_gemv<K, OPT>, dim3(ns), dim3(kSegThreads), smem, st, a);                        \
+    launch_pdl(k_seg_gemv<K, M>, dim3(ns), dim3(kSegThreads), smem, st, a);                          \
     return true;                                                                                     \
   }
     VSIE_SEG(1) VSIE_SEG(2) VSIE_SEG(3) VSIE_SEG(4) VSIE_SEG(5) VSIE_SEG(6) VSIE_SEG(7) VSIE_SEG(8)
@@ -224,10 +234,18 @@ bool seg_gemv_supported(int64_t R, int64_t C, int nsb) {
   if (L > 512 || 16 * L > kStage) return false;
   int nq = (int)ceil_div(L, 32);
   if (nq > 8) nq = nq <= 10 ? 10 : nq <= 12 ? 12 : 16;
-  return kRing + (size_t)4 * 32 * nq * sizeof(cplx) + (size_t)C * sizeof(cplx) <= 220 * 1024;
+  return kRing + (size_t)4 * 32 * nq * sizeof(cplx) + (size_t)2 * C * sizeof(cplx) <= 220 * 1024;
 }
 
-bool launch_seg_gemv(const SegGemv& a, bool transpose, cudaStream_t st) {
+// mode 1: op N (x -> y); 2: op T (x -> y through partials); 3: both from one pass
+// (op N x -> y, op T xt -> yt)
+bool launch_seg_gemv_mode(const SegGemv& a0, int mode, cudaStream_t st) {
+  SegGemv a = a0;
+  if (mode == 2)
+    for (int b = 0; b < a.nbatch; ++b) {
+      a.xt[b] = a0.x[b];
+      a.yt[b] = a0.y[b];
+    }
   int64_t rmax = 0, cmax = 0;
   for (int b = 0; b < a.nbatch; ++b) {
     rmax = std::max(rmax, a.R[b]);
@@ -240,24 +258,29 @@ bool launch_seg_gemv(const SegGemv& a, bool transpose, cudaStream_t st) {
   if (L > 512 || 16 * L > kStage) return false;
   int nq = (int)ceil_div(L, 32);
   if (nq > 8) nq = nq <= 10 ? 10 : nq <= 12 ? 12 : 16;
-  const size_t smem = kRing + (size_t)4 * 32 * nq * sizeof(cplx) + (size_t)cmax * sizeof(cplx);
+  a.cmax = cmax;
+  const size_t smem = kRing + (size_t)4 * 32 * nq * sizeof(cplx) + (size_t)2 * cmax * sizeof(cplx);
   if (smem > 220 * 1024) return false;
-  if (transpose) {
-    VSIE_REQUIRE(a.rstride >= cmax && a.partials != nullptr, VSIE_ERR_ARG, "seg_gemv: partial buffer");
-    if (!launch_seg<true>(a, ns, nq, smem, st)) return false;
-    VSIE_CHECK_LAUNCH();
+  if (mode & 2) VSIE_REQUIRE(a.rstride >= cmax && a.partials != nullptr, VSIE_ERR_ARG, "seg_gemv: partial buffer");
+  const bool ok = mode == 1 ? launch_seg<1>(a, ns, nq, smem, st)
+                : mode == 2 ? launch_seg<2>(a, ns, nq, smem, st)
+                            : launch_seg<3>(a, ns, nq, smem, st);
+  if (!ok) return false;
+  VSIE_CHECK_LAUNCH();
+  if (mode & 2) {
     GemvN g{};
     g.nbatch = a.nbatch;
     for (int b = 0; b < a.nbatch; ++b) {
-      g.y[b] = a.y[b];
+      g.y[b] = a.yt[b];
       g.R[b] = a.C[b];
     }
     launch_gemv_sum(g, a.partials, ns, a.rstride, st);
-  } else {
-    if (!launch_seg<false>(a, ns, nq, smem, st)) return false;
-    VSIE_CHECK_LAUNCH();
   }
   return true;
+}
+
+bool launch_seg_gemv(const SegGemv& a, bool transpose, cudaStream_t st) {
+  return launch_seg_gemv_mode(a, transpose ? 2 : 1, st);
 }
 
 }  // namespace vsie

@@ -280,11 +280,13 @@ def test_fused_g21_forward(monkeypatch):
 @pytest.mark.parametrize("mode,seg,parts,zc,af,rt", [("0", "1", "0", "1", "1", "1"), ("2", "0", "0", "1", "1", "1"),
                                                      ("2", "1", "1", "1", "0", "1"), ("2", "1", "0", "1", "0", "0"),
                                                      ("2", "1", "0", "0", "1", "1"), ("3", "1", "0", "1", "1", "1"),
-                                                     ("4", "1", "0", "1", "1", "1"), ("4", "1", "1", "1", "1", "0")])
+                                                     ("4", "1", "0", "1", "1", "1"), ("4", "1", "1", "1", "1", "0"),
+                                                     ("5", "1", "0", "0", "0", "1")])
 def test_pair_schedules(mode, seg, parts, zc, af, rt):
     """Every GMRES-pair schedule (VSIE_PAIR_G4: 0 per-chi k_gemv_nt chains, 2 batched TMA G4
     pass with (VSIE_SEG_G3=1) or without the batched TMA G3 steps, 3 six concurrent chains,
-    4 every step one batched launch; VSIE_W2_PARTS=1 leaves the G2^T split-K partials to the
+    4 every step one batched launch, 5 streaming passes beside the other direction's chains;
+    VSIE_W2_PARTS=1 leaves the G2^T split-K partials to the
     G3^T kernel; VSIE_ZGEMM_CLUSTER=0 split-K through global partials instead of the cluster /
     DSMEM reduction; VSIE_ADJ_FUSED=1 the fused G1^T + G2^T kernel k_adj12; VSIE_REDUCE_TMA=0
     the per-chi k_reduce_g1 instead of the batched TMA-streamed G1^T) equals the oracle matvecs and the separate applies,
