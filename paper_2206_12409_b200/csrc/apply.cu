@@ -776,6 +776,160 @@ void apply_batched(vsie_coupling_s* h, const cplx* x, cplx* y, int op, cudaStrea
 }
 
 // ------------------------------------------------------------------ the apply DAG
+// single applies (one RHS) on the batched TMA passes: forward = ONE G4 pass (y4, three chi)
+// -> ONE G3 pass (Y3) -> per-chi G2 / G1 chains; transpose = G1^T (one TMA launch when it
+// fits, else in the chains) -> per-chi G2^T chains -> ONE G3^T pass -> ONE G4^T pass with
+// the Eq. 18 chi sum.  VSIE_SINGLE_TMA=0 keeps the per-chi chains of k_gemv_n / k_gemv_t.
+bool single_tma_on() {
+  static const int v = [] {
+    const char* e = std::getenv("VSIE_SINGLE_TMA");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
+bool tma_shapes_ok(vsie_coupling_s* h, const Ctx& X) {
+  if (X.r3m > pair_g4_max_rank()) return false;
+  for (Shard& s : h->shards) {
+    if (s.n3loc() == 0 || s.mloc() == 0) return false;
+    for (int c = 0; c < 3; ++c)
+      if (!seg_gemv_supported(X.R(c, 1) * s.n3loc(), X.R(c, 2), s.g3b_ns)) return false;
+  }
+  return true;
+}
+
+void apply_single_tma(vsie_coupling_s* h, Ctx X, const cplx* x, cplx* y, int op, const Streams& S) {
+  const bool exchange = h->comm != nullptr || h->shards.size() > 1;
+  const int64_t m = h->m, mp = ceil_div(m, h->world);
+  const int64_t rsum = X.R(0, 2) + X.R(1, 2) + X.R(2, 2);
+  if (op == VSIE_OP_N) {
+    for (Shard& s : h->shards) {
+      PairG4 p{};
+      p.nbatch = 3;
+      p.C = s.mloc();
+      p.x = x + s.cb;
+      p.partials = X.partials(0);
+      p.rstride = X.r3m;
+      for (int c = 0; c < 3; ++c) {
+        p.A[c] = s.G4[c].p;
+        p.y4[c] = s.y4.p + c * X.r3stride;
+        p.R[c] = X.R(c, 2);
+      }
+      Scope sc(h, "fwd_g4_tma", 16 * rsum * (p.C + 1) + 16 * p.C, 8 * rsum * p.C, S.main);
+      VSIE_REQUIRE(launch_pair_g4(p, sm_count_dev(), S.main), VSIE_ERR_STATE, "single apply: G4 shape");
+    }
+    if (exchange) combine_r3(h, &Shard::y4, 3 * X.r3stride, S.main);
+    for (Shard& s : h->shards) {
+      const int64_t n3l = s.n3loc();
+      SegGemv g{};
+      g.nbatch = 3;
+      g.nsb = s.g3b_ns;
+      int64_t bytes = 0;
+      for (int c = 0; c < 3; ++c) {
+        g.A[c] = s.G3b[c].p;
+        g.x[c] = s.y4.p + c * X.r3stride;
+        g.y[c] = s.Y3.p + c * X.r2m * n3l;
+        g.R[c] = X.R(c, 1) * n3l;
+        g.C[c] = X.R(c, 2);
+        bytes += 16 * (g.R[c] * g.C[c] + g.R[c] + g.C[c]);
+      }
+      Scope sc(h, "fwd_g3_seg", bytes, bytes / 2, S.main);
+      VSIE_REQUIRE(launch_seg_gemv(g, false, S.main), VSIE_ERR_STATE, "single apply: G3 shape");
+    }
+    fork(h, S);
+    for (int c = 0; c < 3; ++c) {
+      h->scope_chi = c;
+      for (Shard& s : h->shards) fwd_rest(X, s, c, y, S.chi[c], nullptr, false);
+    }
+    h->scope_chi = -1;
+    join(h, S);
+    return;
+  }
+  const bool cj = op == VSIE_OP_C;
+  X.ws = 3;   // the transpose's own workspaces: a forward apply may run beside it
+  bool g1_done = false;
+  if (reduce_tma_on() && reduce_tma_fits(h->grid.n[0], X.r1m)) {
+    g1_done = true;
+    for (Shard& s : h->shards) {
+      const int64_t n3l = s.n3loc();
+      ReduceArgs r{};
+      r.nbatch = 3;
+      r.n1 = h->grid.n[0];
+      r.ncol = (int64_t)h->grid.n[1] * n3l;
+      r.cols_per_rhs = r.ncol;
+      r.ld_rhs = X.L.ld;
+      r.conj_u = cj;
+      int64_t bytes = 0, fl = 0;
+      for (int c = 0; c < 3; ++c) {
+        r.G1[c] = h->G1[c].p;
+        r.u[c] = x + c * X.L.chi_stride + shard_voxel_offset(h, s, X.L);
+        r.W1[c] = s.W1.p + c * X.r1m * h->grid.n[1] * n3l;
+        r.r1[c] = (int)X.R(c, 0);
+        bytes += 16 * ((int64_t)r.n1 * X.R(c, 0) + X.R(c, 0) * r.ncol + (int64_t)r.n1 * r.ncol);
+        fl += 8 * (int64_t)r.n1 * X.R(c, 0) * r.ncol;
+      }
+      Scope sc(h, "adj_g1_reduce_tma", bytes, fl, S.main);
+      VSIE_REQUIRE(launch_reduce_g1_tma(r, S.main), VSIE_ERR_STATE, "single apply: G1 shape");
+    }
+  }
+  fork(h, S);
+  for (int c = 0; c < 3; ++c) {
+    h->scope_chi = c;
+    for (Shard& s : h->shards) adj_front(X, s, c, x, cj, S.chi[c], nullptr, false, !g1_done);
+  }
+  h->scope_chi = -1;
+  join(h, S);
+  for (Shard& s : h->shards) {
+    const int64_t n3l = s.n3loc();
+    SegGemv g{};
+    g.nbatch = 3;
+    g.nsb = s.g3b_ns;
+    g.partials = X.partials(0);
+    g.rstride = X.r3m;
+    int64_t bytes = 0;
+    for (int c = 0; c < 3; ++c) {
+      g.A[c] = s.G3b[c].p;
+      g.x[c] = s.W2.p + c * X.r2m * n3l;
+      g.xparts[c] = 0;
+      g.y[c] = s.z3.p + c * X.r3stride;
+      g.R[c] = X.R(c, 1) * n3l;
+      g.C[c] = X.R(c, 2);
+      bytes += 16 * (g.R[c] * g.C[c] + g.R[c] + g.C[c]);
+    }
+    Scope sc(h, "adj_g3_seg", bytes, bytes / 2, S.main);
+    VSIE_REQUIRE(launch_seg_gemv(g, true, S.main), VSIE_ERR_STATE, "single apply: G3 shape");
+  }
+  if (exchange) combine_r3(h, &Shard::z3, 3 * X.r3stride, S.main);
+  for (Shard& s : h->shards) {
+    PairG4 p{};
+    p.nbatch = 3;
+    p.C = s.mloc();
+    p.z = h->comm ? h->gather_buf.p + (int64_t)h->world * mp : y + s.cb;
+    p.conj_z = cj;
+    p.partials = X.partials(0);
+    p.rstride = X.r3m;
+    for (int c = 0; c < 3; ++c) {
+      p.A[c] = s.G4[c].p;
+      p.z3[c] = s.z3.p + c * X.r3stride;
+      p.R[c] = X.R(c, 2);
+    }
+    Scope sc(h, "adj_g4_tma", 16 * rsum * (p.C + 1) + 16 * p.C, 8 * rsum * p.C, S.main);
+    VSIE_REQUIRE(launch_pair_g4(p, sm_count_dev(), S.main), VSIE_ERR_STATE, "single apply: G4 shape");
+  }
+  if (h->comm) {
+    Scope sc(h, "nccl_allgather", 0, 0, S.main);
+    cplx* seg = h->gather_buf.p + (int64_t)h->world * mp;
+    const Shard& s = h->shards[0];
+    if (s.mloc() < mp) VSIE_CHECK_CUDA(cudaMemsetAsync(seg + s.mloc(), 0, (mp - s.mloc()) * sizeof(cplx), S.main));
+    h->comm->allgather(reinterpret_cast<const double*>(seg), reinterpret_cast<double*>(h->gather_buf.p), 2 * (size_t)mp,
+                       S.main);
+    for (int p = 0; p < h->world; ++p) {
+      const int64_t cb = std::min(m, mp * p), ce = std::min(m, mp * (p + 1));
+      copy2d(y + cb, m, h->gather_buf.p + (int64_t)p * mp, mp, ce - cb, 1, S.main);
+    }
+  }
+}
+
 void apply_dag(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int nrhs, const Streams& S) {
   if (nrhs == 1 && mega_ready(h)) {
     apply_mega(h, x, y, op, S.main);
@@ -797,6 +951,10 @@ void apply_dag(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int nrhs, con
   X.r3stride = (int64_t)X.r3m * nrhs;
   X.L = voxel_layout(h);
   const bool exchange = h->comm != nullptr || h->shards.size() > 1;
+  if (nrhs == 1 && single_tma_on() && tma_shapes_ok(h, X)) {
+    apply_single_tma(h, X, x, y, op, S);
+    return;
+  }
   fork(h, S);
   if (op == VSIE_OP_N) {
     if (!exchange && stagger_on() && S.parallel) {
