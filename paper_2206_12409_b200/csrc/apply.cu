@@ -1315,6 +1315,56 @@ bool pair_batched(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cpl
   return true;
 }
 
+// the forward's G2 and G1 steps for the three chi as one batched launch each (Y3 formed)
+// instead of per-chi chains; VSIE_FWD_TAIL_BATCHED=1
+bool fwd_tail_batched_on() {
+  static const int v = [] {
+    const char* e = std::getenv("VSIE_FWD_TAIL_BATCHED");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v != 0;
+}
+
+void fwd_tail_batched(vsie_coupling_s* h, const Ctx& X, Shard& s, cplx* y, cudaStream_t st) {
+  const int n1 = h->grid.n[0], n2 = h->grid.n[1];
+  const int64_t n3l = s.n3loc();
+  if (n3l == 0) return;
+  {
+    Zgemm zg{};
+    zg.nbatch = 3;
+    int64_t bytes = 0, fl = 0;
+    for (int c = 0; c < 3; ++c) {
+      zg.M[c] = X.R(c, 0) * n2; zg.N[c] = n3l; zg.K[c] = X.R(c, 1);
+      zg.A[c] = h->G2[c].p; zg.lda[c] = X.R(c, 0) * n2;
+      zg.B[c] = s.Y3.p + c * X.r2m * n3l; zg.ldb[c] = X.R(c, 1);
+      zg.C[c] = s.Y2.p + c * X.r1m * n2 * n3l; zg.ldc[c] = X.R(c, 0) * n2;
+      bytes += 16 * (X.R(c, 0) * n2 * X.R(c, 1) + X.R(c, 1) * n3l + X.R(c, 0) * n2 * n3l);
+      fl += 8 * X.R(c, 0) * n2 * X.R(c, 1) * n3l;
+    }
+    Scope sc(h, "fwd_g2_zgemm_b", bytes, fl, st);
+    launch_zgemm_dmma(zg, h->zgemm_ws.p, 3 * h->zgemm_ws_per_chi, st);
+  }
+  {
+    ExpandArgs e{};
+    e.nbatch = 3;
+    e.n1 = n1;
+    e.ncol = (int64_t)n2 * n3l;
+    e.cols_per_rhs = e.ncol;
+    e.ld_rhs = X.L.ld;
+    int64_t bytes = 0, fl = 0;
+    for (int c = 0; c < 3; ++c) {
+      e.G1[c] = h->G1[c].p;
+      e.Y2[c] = s.Y2.p + c * X.r1m * n2 * n3l;
+      e.y[c] = y + c * X.L.chi_stride + shard_voxel_offset(h, s, X.L);
+      e.r1[c] = (int)X.R(c, 0);
+      bytes += 16 * ((int64_t)n1 * X.R(c, 0) + X.R(c, 0) * n2 * n3l + (int64_t)n1 * n2 * n3l);
+      fl += 8 * (int64_t)n1 * X.R(c, 0) * n2 * n3l;
+    }
+    Scope sc(h, "fwd_g1_expand_b", bytes, fl, st);
+    launch_expand_g1(e, st);
+  }
+}
+
 // The coupling pair of one GMRES matvec of the hybrid system (Eq. 11 / 15: the body rows
 // need Z_bc j_c, the conductor rows Z_bc^T j_b): y = Z x and z = Z^T u (Z^H u).  The
 // transpose front (G1^T, G2^T, G3^T) runs first, so that both directions' G4 products
@@ -1665,9 +1715,13 @@ void pair_dag(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z
     fork(h, S);
   }
   }   // !z_done
-  for (int c = 0; c < 3; ++c) {
-    h->scope_chi = c;
-    for (Shard& s : h->shards) fwd_rest(X, s, c, y, S.chi[c], nullptr, !(z_done && seg));
+  if (z_done && seg && fwd_tail_batched_on()) {
+    for (Shard& s : h->shards) fwd_tail_batched(h, X, s, y, S.main);
+  } else {
+    for (int c = 0; c < 3; ++c) {
+      h->scope_chi = c;
+      for (Shard& s : h->shards) fwd_rest(X, s, c, y, S.chi[c], nullptr, !(z_done && seg));
+    }
   }
   h->scope_chi = -1;
   join(h, S);

@@ -277,19 +277,24 @@ def test_fused_g21_forward(monkeypatch):
     assert p.returncode == 0 and "fused ok" in p.stdout, p.stderr[-2000:]
 
 
-@pytest.mark.parametrize("mode,seg,parts,zc,af,rt", [("0", "1", "0", "1", "1", "1"), ("2", "0", "0", "1", "1", "1"),
-                                                     ("2", "1", "1", "1", "0", "1"), ("2", "1", "0", "1", "0", "0"),
-                                                     ("2", "1", "0", "0", "1", "1"), ("3", "1", "0", "1", "1", "1"),
-                                                     ("4", "1", "0", "1", "1", "1"), ("4", "1", "1", "1", "1", "0"),
-                                                     ("5", "1", "0", "0", "0", "1")])
-def test_pair_schedules(mode, seg, parts, zc, af, rt):
+@pytest.mark.parametrize("mode,seg,parts,zc,af,rt,ft", [("0", "1", "0", "1", "1", "1", "0"),
+                                                        ("2", "0", "0", "1", "1", "1", "0"),
+                                                        ("2", "1", "1", "1", "0", "1", "1"),
+                                                        ("2", "1", "0", "1", "0", "0", "0"),
+                                                        ("2", "1", "0", "0", "1", "1", "0"),
+                                                        ("3", "1", "0", "1", "1", "1", "0"),
+                                                        ("4", "1", "0", "1", "1", "1", "0"),
+                                                        ("4", "1", "1", "1", "1", "0", "0"),
+                                                        ("5", "1", "0", "0", "0", "1", "0")])
+def test_pair_schedules(mode, seg, parts, zc, af, rt, ft):
     """Every GMRES-pair schedule (VSIE_PAIR_G4: 0 per-chi k_gemv_nt chains, 2 batched TMA G4
     pass with (VSIE_SEG_G3=1) or without the batched TMA G3 steps, 3 six concurrent chains,
     4 every step one batched launch, 5 streaming passes beside the other direction's chains;
     VSIE_W2_PARTS=1 leaves the G2^T split-K partials to the
     G3^T kernel; VSIE_ZGEMM_CLUSTER=0 split-K through global partials instead of the cluster /
     DSMEM reduction; VSIE_ADJ_FUSED=1 the fused G1^T + G2^T kernel k_adj12; VSIE_REDUCE_TMA=0
-    the per-chi k_reduce_g1 instead of the batched TMA-streamed G1^T) equals the oracle matvecs and the separate applies,
+    the per-chi k_reduce_g1 instead of the batched TMA-streamed G1^T; VSIE_FWD_TAIL_BATCHED=1
+    the forward's G2 / G1 steps as batched launches) equals the oracle matvecs and the separate applies,
     at cfg 1 (ragged ranks) and cfg 2 (several tiles, 148-CTA row blocks); op T and op C.
     Subprocess: the switches are read once per process."""
     import subprocess, sys, textwrap, os
@@ -320,7 +325,8 @@ def test_pair_schedules(mode, seg, parts, zc, af, rt):
         print("schedule ok")
     ''')
     env = dict(os.environ, VSIE_PAIR_G4=mode, VSIE_SEG_G3=seg, VSIE_W2_PARTS=parts, VSIE_ZGEMM_CLUSTER=zc,
-               VSIE_ADJ_FUSED=af, VSIE_REDUCE_TMA=rt)
+               VSIE_ADJ_FUSED=af, VSIE_REDUCE_TMA=rt,
+               VSIE_FWD_TAIL_BATCHED=ft)
     p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert p.returncode == 0 and "schedule ok" in p.stdout, p.stderr[-2000:]
