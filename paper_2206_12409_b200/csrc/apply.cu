@@ -278,7 +278,7 @@ void fwd_rest(const Ctx& X, Shard& s, int c, cplx* y, cudaStream_t st, cudaEvent
 // ------------------------------------------------------------------ transpose chain pieces (one chi)
 // W1 = G1^T u, W2 = G2^T W1, z3 = G3^T W2: partial z3 per shard
 void adj_front(const Ctx& X, Shard& s, int c, const cplx* u, bool cj, cudaStream_t st, cudaEvent_t mid = nullptr,
-               bool with_g3 = true, bool with_g1 = true) {
+               bool with_g3 = true, bool with_g1 = true, bool with_g2 = true) {
   vsie_coupling_s* h = X.h;
   const int k = X.k;
   const int n1 = h->grid.n[0], n2 = h->grid.n[1];
@@ -291,6 +291,24 @@ void adj_front(const Ctx& X, Shard& s, int c, const cplx* u, bool cj, cudaStream
   const int64_t r1 = X.R(c, 0), r2 = X.R(c, 1), r3 = X.R(c, 2);
   cplx* W1 = s.W1.p + c * X.r1m * n2 * n3l * k;
   cplx* W2 = s.W2.p + c * X.r2m * n3l * k;
+  if (!with_g2) {
+    // G2^T by the batched k_g2t after the chains (only G1^T here)
+    ReduceArgs r{};
+    r.nbatch = 1;
+    r.n1 = n1;
+    r.ncol = (int64_t)n2 * n3l * k;
+    r.cols_per_rhs = (int64_t)n2 * n3l;
+    r.ld_rhs = X.L.ld;
+    r.conj_u = cj;
+    r.G1[0] = h->G1[c].p;
+    r.u[0] = u + c * X.L.chi_stride + shard_voxel_offset(h, s, X.L);
+    r.W1[0] = W1;
+    r.r1[0] = (int)r1;
+    const int64_t bytes = 16 * ((int64_t)n1 * r1 + r1 * n2 * n3l * k + (int64_t)n1 * n2 * n3l * k);
+    Scope sc(h, "adj_g1_reduce", bytes, 8 * (int64_t)n1 * r1 * n2 * n3l * k, st);
+    launch_reduce_g1(r, st);
+    return;
+  }
   if (with_g1) {
     ReduceArgs r{};
     r.nbatch = 1;
@@ -776,6 +794,38 @@ void apply_batched(vsie_coupling_s* h, const cplx* x, cplx* y, int op, cudaStrea
 }
 
 // ------------------------------------------------------------------ the apply DAG
+// batched W2 = G2^T W1 (k_g2t) instead of the per-chi split-K ZGEMM chains; VSIE_G2T=0
+bool g2t_on() {
+  static const int v = [] {
+    const char* e = std::getenv("VSIE_G2T");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
+void launch_g2t_shard(vsie_coupling_s* h, const Ctx& X, Shard& s, cudaStream_t st) {
+  const int n2 = h->grid.n[1];
+  const int64_t n3l = s.n3loc();
+  if (n3l == 0) return;
+  G2tArgs g{};
+  g.nbatch = 3;
+  g.N = (int)n3l;
+  int64_t bytes = 0, fl = 0;
+  for (int c = 0; c < 3; ++c) {
+    g.G2[c] = h->G2[c].p;
+    g.W1[c] = s.W1.p + c * X.r1m * n2 * n3l;
+    g.W2[c] = s.W2.p + c * X.r2m * n3l;
+    g.M[c] = (int)X.R(c, 1);
+    g.K[c] = (int)(X.R(c, 0) * n2);
+    g.ldw[c] = (int)X.R(c, 1);
+    h->w2_parts[c] = 0;
+    bytes += 16 * (X.R(c, 0) * n2 * X.R(c, 1) + X.R(c, 1) * n3l + X.R(c, 0) * n2 * n3l);
+    fl += 8 * X.R(c, 0) * n2 * X.R(c, 1) * n3l;
+  }
+  Scope sc(h, "adj_g2_g2t", bytes, fl, st);
+  launch_g2t(g, st);
+}
+
 // single applies (one RHS) on the batched TMA passes: forward = ONE G4 pass (y4, three chi)
 // -> ONE G3 pass (Y3) -> per-chi G2 / G1 chains; transpose = G1^T (one TMA launch when it
 // fits, else in the chains) -> per-chi G2^T chains -> ONE G3^T pass -> ONE G4^T pass with
@@ -872,13 +922,18 @@ void apply_single_tma(vsie_coupling_s* h, Ctx X, const cplx* x, cplx* y, int op,
       VSIE_REQUIRE(launch_reduce_g1_tma(r, S.main), VSIE_ERR_STATE, "single apply: G1 shape");
     }
   }
-  fork(h, S);
-  for (int c = 0; c < 3; ++c) {
-    h->scope_chi = c;
-    for (Shard& s : h->shards) adj_front(X, s, c, x, cj, S.chi[c], nullptr, false, !g1_done);
+  const bool g2b = g2t_on();
+  if (!(g1_done && g2b)) {
+    fork(h, S);
+    for (int c = 0; c < 3; ++c) {
+      h->scope_chi = c;
+      for (Shard& s : h->shards) adj_front(X, s, c, x, cj, S.chi[c], nullptr, false, !g1_done, !g2b);
+    }
+    h->scope_chi = -1;
+    join(h, S);
   }
-  h->scope_chi = -1;
-  join(h, S);
+  if (g2b)
+    for (Shard& s : h->shards) launch_g2t_shard(h, X, s, S.main);
   for (Shard& s : h->shards) {
     const int64_t n3l = s.n3loc();
     SegGemv g{};
@@ -1549,15 +1604,22 @@ void pair_dag(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z
       }
       VSIE_REQUIRE(g1_done || h->shards.size() == 1, VSIE_ERR_STATE, "reduce_tma on a partial shard set");
     }
-    fork(h, S);
-    for (int c = 0; c < 3; ++c) {
-      h->scope_chi = c;
-      for (Shard& s : h->shards) adj_front(X, s, c, u, cj, S.chi[c], nullptr, !seg, !g1_done);
+    const bool g2b = seg && g2t_on() && X.k == 1;
+    if (!(g1_done && g2b)) {
+      fork(h, S);
+      for (int c = 0; c < 3; ++c) {
+        h->scope_chi = c;
+        for (Shard& s : h->shards) adj_front(X, s, c, u, cj, S.chi[c], nullptr, !seg, !g1_done, !g2b);
+      }
+      h->scope_chi = -1;
+      if (g2b) join(h, S);
     }
-    h->scope_chi = -1;
+    if (g2b) {
+      for (Shard& s : h->shards) launch_g2t_shard(h, X, s, S.main);
+    }
   }
   if (seg) {
-    if (!fused_front) join(h, S);
+    if (!fused_front && !(seg && g2t_on())) join(h, S);
     for (Shard& s : h->shards) {
       const int64_t n3l = s.n3loc();
       SegGemv g{};

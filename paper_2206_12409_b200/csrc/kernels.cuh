@@ -141,6 +141,18 @@ struct AdjFrontArgs {
 };
 bool adj_front_supported(int n1, int r1max);
 void launch_adj_front(const AdjFrontArgs& a, cudaStream_t st);
+// W2[b] = G2[b]^T W1[b] (g2t.cu): M[b] = r2, K[b] = r1 n2 rows of the column-major
+// (r1 n2) x r2 core, N = n3l columns of W1 (ld K); one launch over the batch, no split-K
+// partials (K split over the 8 warps of a CTA, fixed-order smem tree)
+struct G2tArgs {
+  const cplx* G2[3];
+  const cplx* W1[3];
+  cplx* W2[3];
+  int M[3], K[3], ldw[3];
+  int N;
+  int nbatch;
+};
+void launch_g2t(const G2tArgs& a, cudaStream_t st);
 // fixed-order sum of ns split partials ([b][s][rmax]) into a.y[b][0 .. a.R[b])
 void launch_gemv_sum(const GemvN& a, cplx* partials, int ns, int64_t rmax, cudaStream_t st);
 int sm_count_dev();

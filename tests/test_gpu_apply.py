@@ -277,16 +277,23 @@ def test_fused_g21_forward(monkeypatch):
     assert p.returncode == 0 and "fused ok" in p.stdout, p.stderr[-2000:]
 
 
-@pytest.mark.parametrize("mode,seg,parts,zc,af,rt,ft", [("0", "1", "0", "1", "1", "1", "0"),
-                                                        ("2", "0", "0", "1", "1", "1", "0"),
-                                                        ("2", "1", "1", "1", "0", "1", "1"),
-                                                        ("2", "1", "0", "1", "0", "0", "0"),
-                                                        ("2", "1", "0", "0", "1", "1", "0"),
-                                                        ("3", "1", "0", "1", "1", "1", "0"),
-                                                        ("4", "1", "0", "1", "1", "1", "0"),
-                                                        ("4", "1", "1", "1", "1", "0", "0"),
-                                                        ("5", "1", "0", "0", "0", "1", "0")])
-def test_pair_schedules(mode, seg, parts, zc, af, rt, ft):
+_SCHEDULES = [
+    dict(VSIE_PAIR_G4="0"),
+    dict(VSIE_PAIR_G4="2", VSIE_SEG_G3="0"),
+    dict(VSIE_PAIR_G4="2", VSIE_W2_PARTS="1", VSIE_ZGEMM_CLUSTER="1", VSIE_FWD_TAIL_BATCHED="1", VSIE_G2T="0"),
+    dict(VSIE_PAIR_G4="2", VSIE_REDUCE_TMA="0"),
+    dict(VSIE_PAIR_G4="2", VSIE_G2T="0", VSIE_ADJ_FUSED="0"),
+    dict(VSIE_PAIR_G4="2", VSIE_ADJ_FUSED="1"),
+    dict(VSIE_PAIR_G4="3"),
+    dict(VSIE_PAIR_G4="4"),
+    dict(VSIE_PAIR_G4="4", VSIE_W2_PARTS="1", VSIE_REDUCE_TMA="0"),
+    dict(VSIE_PAIR_G4="5"),
+    dict(VSIE_PAIR_G4="2", VSIE_SINGLE_TMA="0", VSIE_G2T="0"),
+]
+
+
+@pytest.mark.parametrize("env", _SCHEDULES, ids=lambda e: ",".join(f"{k[5:]}={v}" for k, v in e.items()))
+def test_pair_schedules(env):
     """Every GMRES-pair schedule (VSIE_PAIR_G4: 0 per-chi k_gemv_nt chains, 2 batched TMA G4
     pass with (VSIE_SEG_G3=1) or without the batched TMA G3 steps, 3 six concurrent chains,
     4 every step one batched launch, 5 streaming passes beside the other direction's chains;
@@ -294,7 +301,9 @@ def test_pair_schedules(mode, seg, parts, zc, af, rt, ft):
     G3^T kernel; VSIE_ZGEMM_CLUSTER=0 split-K through global partials instead of the cluster /
     DSMEM reduction; VSIE_ADJ_FUSED=1 the fused G1^T + G2^T kernel k_adj12; VSIE_REDUCE_TMA=0
     the per-chi k_reduce_g1 instead of the batched TMA-streamed G1^T; VSIE_FWD_TAIL_BATCHED=1
-    the forward's G2 / G1 steps as batched launches) equals the oracle matvecs and the separate applies,
+    the forward's G2 / G1 steps as batched launches; VSIE_G2T=0 the split-K ZGEMM for G2^T
+    instead of k_g2t; VSIE_SINGLE_TMA=0 the per-chi GEMV chains in the single applies)
+    equals the oracle matvecs and the separate applies,
     at cfg 1 (ragged ranks) and cfg 2 (several tiles, 148-CTA row blocks); op T and op C.
     Subprocess: the switches are read once per process."""
     import subprocess, sys, textwrap, os
@@ -324,9 +333,7 @@ def test_pair_schedules(mode, seg, parts, zc, af, rt, ft):
                     assert validate.rel_l2(z, ttmv.apply(tts, u, adj)) <= 1e-12, (ci, adj)
         print("schedule ok")
     ''')
-    env = dict(os.environ, VSIE_PAIR_G4=mode, VSIE_SEG_G3=seg, VSIE_W2_PARTS=parts, VSIE_ZGEMM_CLUSTER=zc,
-               VSIE_ADJ_FUSED=af, VSIE_REDUCE_TMA=rt,
-               VSIE_FWD_TAIL_BATCHED=ft)
+    env = dict(os.environ, **env)
     p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert p.returncode == 0 and "schedule ok" in p.stdout, p.stderr[-2000:]
