@@ -794,6 +794,61 @@ void apply_batched(vsie_coupling_s* h, const cplx* x, cplx* y, int op, cudaStrea
 }
 
 // ------------------------------------------------------------------ the apply DAG
+// forward G2 step for the three chi as one k_g2n launch (pair and single applies), opt-in
+// VSIE_G2N=1: measured slower than the per-chi ZGEMM chains (cfg 2 pair 0.160 -> 0.166 ms:
+// one warp per 8 x 8 tile re-reads G2 from L2 for every n-tile)
+bool g2n_on() {
+  static const int v = [] {
+    const char* e = std::getenv("VSIE_G2N");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v != 0;
+}
+
+void launch_g2n_shard(vsie_coupling_s* h, const Ctx& X, Shard& s, cudaStream_t st) {
+  const int n2 = h->grid.n[1];
+  const int64_t n3l = s.n3loc();
+  if (n3l == 0) return;
+  G2tArgs g{};
+  g.nbatch = 3;
+  g.N = (int)n3l;
+  int64_t bytes = 0, fl = 0;
+  for (int c = 0; c < 3; ++c) {
+    g.G2[c] = h->G2[c].p;
+    g.W1[c] = s.Y3.p + c * X.r2m * n3l;
+    g.W2[c] = s.Y2.p + c * X.r1m * n2 * n3l;
+    g.M[c] = (int)(X.R(c, 0) * n2);
+    g.K[c] = (int)X.R(c, 1);
+    g.ldw[c] = (int)(X.R(c, 0) * n2);
+    bytes += 16 * (X.R(c, 0) * n2 * X.R(c, 1) + X.R(c, 1) * n3l + X.R(c, 0) * n2 * n3l);
+    fl += 8 * X.R(c, 0) * n2 * X.R(c, 1) * n3l;
+  }
+  Scope sc(h, "fwd_g2_g2n", bytes, fl, st);
+  launch_g2n(g, st);
+}
+
+// the G1 expansion of one chi (Y2 formed)
+void fwd_expand(const Ctx& X, Shard& s, int c, cplx* y, cudaStream_t st) {
+  vsie_coupling_s* h = X.h;
+  const int n1 = h->grid.n[0], n2 = h->grid.n[1];
+  const int64_t n3l = s.n3loc();
+  if (n3l == 0) return;
+  const int64_t r1 = X.R(c, 0);
+  ExpandArgs e{};
+  e.nbatch = 1;
+  e.n1 = n1;
+  e.ncol = (int64_t)n2 * n3l;
+  e.cols_per_rhs = e.ncol;
+  e.ld_rhs = X.L.ld;
+  e.G1[0] = h->G1[c].p;
+  e.Y2[0] = s.Y2.p + c * X.r1m * n2 * n3l;
+  e.y[0] = y + c * X.L.chi_stride + shard_voxel_offset(h, s, X.L);
+  e.r1[0] = (int)r1;
+  const int64_t bytes = 16 * ((int64_t)n1 * r1 + r1 * n2 * n3l + (int64_t)n1 * n2 * n3l);
+  Scope sc(h, "fwd_g1_expand", bytes, 8 * (int64_t)n1 * r1 * n2 * n3l, st);
+  launch_expand_g1(e, st);
+}
+
 // batched W2 = G2^T W1 (k_g2t) instead of the per-chi split-K ZGEMM chains; VSIE_G2T=0
 bool g2t_on() {
   static const int v = [] {
@@ -886,10 +941,17 @@ void apply_single_tma(vsie_coupling_s* h, Ctx X, const cplx* x, cplx* y, int op,
       Scope sc(h, "fwd_g3_seg", bytes, bytes / 2, S.main);
       VSIE_REQUIRE(launch_seg_gemv(g, false, S.main), VSIE_ERR_STATE, "single apply: G3 shape");
     }
+    if (g2n_on())
+      for (Shard& s : h->shards) launch_g2n_shard(h, X, s, S.main);
     fork(h, S);
     for (int c = 0; c < 3; ++c) {
       h->scope_chi = c;
-      for (Shard& s : h->shards) fwd_rest(X, s, c, y, S.chi[c], nullptr, false);
+      for (Shard& s : h->shards) {
+        if (g2n_on())
+          fwd_expand(X, s, c, y, S.chi[c]);
+        else
+          fwd_rest(X, s, c, y, S.chi[c], nullptr, false);
+      }
     }
     h->scope_chi = -1;
     join(h, S);
@@ -1779,6 +1841,15 @@ void pair_dag(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z
   }   // !z_done
   if (z_done && seg && fwd_tail_batched_on()) {
     for (Shard& s : h->shards) fwd_tail_batched(h, X, s, y, S.main);
+  } else if (z_done && seg && g2n_on()) {
+    // Y2 = G2 Y3 for the three chi in one launch (k_g2n), then the G1 expansions per chi
+    join(h, S);
+    for (Shard& s : h->shards) launch_g2n_shard(h, X, s, S.main);
+    fork(h, S);
+    for (int c = 0; c < 3; ++c) {
+      h->scope_chi = c;
+      for (Shard& s : h->shards) fwd_expand(X, s, c, y, S.chi[c]);
+    }
   } else {
     for (int c = 0; c < 3; ++c) {
       h->scope_chi = c;

@@ -153,6 +153,9 @@ struct G2tArgs {
   int nbatch;
 };
 void launch_g2t(const G2tArgs& a, cudaStream_t st);
+// forward Y2[b] = G2[b] Y3[b] with the same argument block read as: G2 (M = r1 n2 rows,
+// K = r2), W1 := Y3 (K x N, ld K), W2 := Y2 (ld ldw = r1 n2); one warp per 8 x 8 tile
+void launch_g2n(const G2tArgs& a, cudaStream_t st);
 // fixed-order sum of ns split partials ([b][s][rmax]) into a.y[b][0 .. a.R[b])
 void launch_gemv_sum(const GemvN& a, cplx* partials, int ns, int64_t rmax, cudaStream_t st);
 int sm_count_dev();

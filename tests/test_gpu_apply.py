@@ -283,6 +283,7 @@ _SCHEDULES = [
     dict(VSIE_PAIR_G4="2", VSIE_W2_PARTS="1", VSIE_ZGEMM_CLUSTER="1", VSIE_FWD_TAIL_BATCHED="1", VSIE_G2T="0"),
     dict(VSIE_PAIR_G4="2", VSIE_REDUCE_TMA="0"),
     dict(VSIE_PAIR_G4="2", VSIE_G2T="0", VSIE_ADJ_FUSED="0"),
+    dict(VSIE_PAIR_G4="2", VSIE_G2N="1"),
     dict(VSIE_PAIR_G4="2", VSIE_ADJ_FUSED="1"),
     dict(VSIE_PAIR_G4="3"),
     dict(VSIE_PAIR_G4="4"),
@@ -302,7 +303,8 @@ def test_pair_schedules(env):
     DSMEM reduction; VSIE_ADJ_FUSED=1 the fused G1^T + G2^T kernel k_adj12; VSIE_REDUCE_TMA=0
     the per-chi k_reduce_g1 instead of the batched TMA-streamed G1^T; VSIE_FWD_TAIL_BATCHED=1
     the forward's G2 / G1 steps as batched launches; VSIE_G2T=0 the split-K ZGEMM for G2^T
-    instead of k_g2t; VSIE_SINGLE_TMA=0 the per-chi GEMV chains in the single applies)
+    instead of k_g2t; VSIE_G2N=1 the batched k_g2n for the forward G2 step instead of
+    the per-chi ZGEMMs; VSIE_SINGLE_TMA=0 the per-chi GEMV chains in the single applies)
     equals the oracle matvecs and the separate applies,
     at cfg 1 (ragged ranks) and cfg 2 (several tiles, 148-CTA row blocks); op T and op C.
     Subprocess: the switches are read once per process."""
