@@ -23,62 +23,94 @@ __device__ __forceinline__ void dmma_g2(double& d0, double& d1, double a, double
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(kG2Threads) k_g2t(const __grid_constant__ G2tArgs a) {
-  __shared__ cplx red[kG2Warps / 2][64];
+template <int TM, int TN, int NW>
+__global__ void __launch_bounds__(32 * NW) k_g2t(const __grid_constant__ G2tArgs a) {
+  __shared__ cplx red[NW / 2][64 * TM * TN];
   pdl_wait();
   const int b = blockIdx.z;
   const int M = a.M[b], N = a.N, K = a.K[b];
-  const int m0 = blockIdx.x * 8, n0 = blockIdx.y * 8;
+  const int m0 = blockIdx.x * 8 * TM, n0 = blockIdx.y * 8 * TN;
   if (m0 >= M || n0 >= N) return;   // uniform per CTA
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int ksn = (K + 3) / 4;
-  const int ks0 = ksn * warp / kG2Warps, ks1 = ksn * (warp + 1) / kG2Warps;
+  const int ks0 = ksn * warp / NW, ks1 = ksn * (warp + 1) / NW;
   // A[m][k] = G2[k + K m] (op T of the column-major (r1 n2) x r2 core), B[k][n] = W1[k + K n]
-  const int mrow = min(m0 + g, M - 1), ncol = min(n0 + g, N - 1);   // clamped rows / cols: discarded
-  const cplx* __restrict__ Ar = a.G2[b] + (int64_t)K * mrow;
-  const cplx* __restrict__ Bc = a.W1[b] + (int64_t)K * ncol;
-  double p1[2] = {0, 0}, p2[2] = {0, 0}, p3[2] = {0, 0};
-  constexpr int UNR = 10;
+  const cplx* Ar[TM];
+  const cplx* Bc[TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i) Ar[i] = a.G2[b] + (int64_t)K * min(m0 + 8 * i + g, M - 1);   // clamped: discarded
+#pragma unroll
+  for (int j = 0; j < TN; ++j) Bc[j] = a.W1[b] + (int64_t)K * min(n0 + 8 * j + g, N - 1);
+  double p1[TM][TN][2], p2[TM][TN][2], p3[TM][TN][2];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) p1[i][j][0] = p1[i][j][1] = p2[i][j][0] = p2[i][j][1] = p3[i][j][0] = p3[i][j][1] = 0;
+  constexpr int UNR = TM * TN > 1 ? 5 : 10;
   for (int ks = ks0; ks < ks1; ks += UNR) {
-    cplx av[UNR], bv[UNR];
+    cplx av[UNR][TM], bv[UNR][TN];
 #pragma unroll
     for (int q = 0; q < UNR; ++q) {
       const int k = 4 * (ks + q) + t;
       const bool ok = ks + q < ks1 && k < K;
-      av[q] = ok ? __ldg(Ar + k) : cmk(0, 0);
-      bv[q] = ok ? __ldcg(Bc + k) : cmk(0, 0);
+#pragma unroll
+      for (int i = 0; i < TM; ++i) av[q][i] = ok ? __ldg(Ar[i] + k) : cmk(0, 0);
+#pragma unroll
+      for (int j = 0; j < TN; ++j) bv[q][j] = ok ? __ldcg(Bc[j] + k) : cmk(0, 0);
     }
 #pragma unroll
-    for (int q = 0; q < UNR; ++q) {
-      dmma_g2(p1[0], p1[1], av[q].x, bv[q].x);
-      dmma_g2(p2[0], p2[1], av[q].y, bv[q].y);
-      dmma_g2(p3[0], p3[1], av[q].x + av[q].y, bv[q].x + bv[q].y);
-    }
+    for (int q = 0; q < UNR; ++q)
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+          dmma_g2(p1[i][j][0], p1[i][j][1], av[q][i].x, bv[q][j].x);
+          dmma_g2(p2[i][j][0], p2[i][j][1], av[q][i].y, bv[q][j].y);
+          dmma_g2(p3[i][j][0], p3[i][j][1], av[q][i].x + av[q][i].y, bv[q][j].x + bv[q][j].y);
+        }
   }
-  // lane holds C[g][2 t + j]; fixed-order tree over the 8 warps
-  cplx c[2];
+  // lane holds C[8 i + g][8 j + 2 t + jj]; fixed-order tree over the warps
+  cplx c[TM][TN][2];
 #pragma unroll
-  for (int j = 0; j < 2; ++j) c[j] = cmk(p1[j] - p2[j], p3[j] - p1[j] - p2[j]);
+  for (int i = 0; i < TM; ++i)
 #pragma unroll
-  for (int half = kG2Warps / 2; half >= 1; half >>= 1) {
+    for (int j = 0; j < TN; ++j)
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj)
+        c[i][j][jj] = cmk(p1[i][j][jj] - p2[i][j][jj], p3[i][j][jj] - p1[i][j][jj] - p2[i][j][jj]);
+#pragma unroll
+  for (int half = NW / 2; half >= 1; half >>= 1) {
     if (warp >= half && warp < 2 * half) {
 #pragma unroll
-      for (int j = 0; j < 2; ++j) red[warp - half][g * 8 + 2 * t + j] = c[j];
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj) red[warp - half][((i * TN + j) * 8 + g) * 8 + 2 * t + jj] = c[i][j][jj];
     }
     __syncthreads();
     if (warp < half) {
 #pragma unroll
-      for (int j = 0; j < 2; ++j) c[j] = cadd(c[j], red[warp][g * 8 + 2 * t + j]);
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj)
+            c[i][j][jj] = cadd(c[i][j][jj], red[warp][((i * TN + j) * 8 + g) * 8 + 2 * t + jj]);
     }
     __syncthreads();
   }
   if (warp == 0) {
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int m = m0 + g, n = n0 + 2 * t + j;
-      if (m < M && n < N) a.W2[b][m + (int64_t)a.ldw[b] * n] = c[j];
-    }
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          const int m = m0 + 8 * i + g, n = n0 + 8 * j + 2 * t + jj;
+          if (m < M && n < N) a.W2[b][m + (int64_t)a.ldw[b] * n] = c[i][j][jj];
+        }
   }
   pdl_trigger();
 }
@@ -137,12 +169,26 @@ void launch_g2n(const G2tArgs& a, cudaStream_t st) {
   VSIE_CHECK_LAUNCH();
 }
 
+// VSIE_G2T_TILE: 1 = 8 x 8 tiles, 8 warps (default); 2 = 16 x 16 tiles, 16 warps;
+// 3 = 8 x 16 tiles, 8 warps
 void launch_g2t(const G2tArgs& a, cudaStream_t st) {
   int mmax = 0;
   for (int b = 0; b < a.nbatch; ++b) mmax = std::max(mmax, a.M[b]);
   if (mmax == 0 || a.N == 0) return;
-  dim3 grid((unsigned)ceil_div(mmax, 8), (unsigned)ceil_div(a.N, 8), a.nbatch);
-  launch_pdl(k_g2t, grid, dim3(kG2Threads), 0, st, a);
+  static const int tile = [] {
+    const char* e = std::getenv("VSIE_G2T_TILE");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (tile == 2) {
+    dim3 grid((unsigned)ceil_div(mmax, 16), (unsigned)ceil_div(a.N, 16), a.nbatch);
+    launch_pdl(k_g2t<2, 2, 16>, grid, dim3(32 * 16), 0, st, a);
+  } else if (tile == 3) {
+    dim3 grid((unsigned)ceil_div(mmax, 8), (unsigned)ceil_div(a.N, 16), a.nbatch);
+    launch_pdl(k_g2t<1, 2, 8>, grid, dim3(32 * 8), 0, st, a);
+  } else {
+    dim3 grid((unsigned)ceil_div(mmax, 8), (unsigned)ceil_div(a.N, 8), a.nbatch);
+    launch_pdl(k_g2t<1, 1, 8>, grid, dim3(32 * 8), 0, st, a);
+  }
   VSIE_CHECK_LAUNCH();
 }
 
