@@ -9,6 +9,6 @@ timeout 900 python bench.py --config 4 --steps 30 --warmup 5 > $out/bench_cfg4.l
 timeout 1200 python bench.py --config 5 --steps 5 --warmup 3 --no-cpu-baseline > $out/bench_cfg5.log 2>&1; echo "bench5 rc=$?"
 timeout 300 python tools/profile_step.py 2 3 > $out/plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv python tools/profile_step.py 2 3 > $out/ncu_launch.log 2>&1; echo "launches rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_reduce_tma|k_pair_g4|k_seg_gemv|k_expand_g1|k_zgemm_tc|k_splitk" -s 10 -c 10 -o $out/prof python tools/profile_step.py 2 3 > $out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -s 10 -c 13 -o $out/prof python tools/profile_step.py 2 3 > $out/ncu_full.log 2>&1; echo "ncu full rc=$?"
 timeout 300 python tools/trace_pair.py 2 > $out/trace2.txt 2>&1
 ls $out
