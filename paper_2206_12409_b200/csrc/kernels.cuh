@@ -193,6 +193,7 @@ struct ReduceArgs {
   int64_t ncol, cols_per_rhs, ld_rhs;
   int nbatch;
   bool conj_u;
+  int diag;   // k_reduce_tma diagnostics (VSIE_RT_DIAG): 1 = stream only, no arithmetic
 };
 void launch_reduce_g1(const ReduceArgs& a, cudaStream_t st);
 // TMA-streamed W1 = G1^T u over the batch in one persistent launch (reduce_tma.cu), single

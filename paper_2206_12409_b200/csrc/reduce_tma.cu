@@ -46,21 +46,6 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_reduce_tma(const __grid_co
   const int64_t c0 = a.ncol * s / ns, c1 = a.ncol * (s + 1) / ns;
   const int nc = (int)(c1 - c0);
   const int nst = (nc + 7) / 8;   // stages per chi (same for every chi)
-  // constant cores: G1 of every chi staged before the PDL wait
-  for (int b = 0; b < a.nbatch; ++b) {
-    const cplx* __restrict__ G1 = a.G1[b];
-    const int r1 = a.r1[b];
-    if (NTD > 0)
-      for (int e = threadIdx.x; e < ks_n * NTD * 32; e += 32 * (CW + 1)) {
-        const int ln = e % 32, nt = (e / 32) % NTD, ks = e / (32 * NTD);
-        const int k = 4 * ks + (ln & 3), n = 8 * nt + (ln >> 2);
-        Bf[(size_t)b * ks_n * NTD * 32 + e] = (k < n1 && n < r1) ? __ldg(G1 + k + (int64_t)n1 * n) : cmk(0, 0);
-      }
-    for (int e = threadIdx.x; e < 4 * ks_n * REM; e += 32 * (CW + 1)) {
-      const int j = e % REM, k = e / REM, n = 8 * NTD + j;
-      Gr[(size_t)b * 4 * ks_n * REM + e] = (k < n1 && n < r1) ? __ldg(G1 + k + (int64_t)n1 * n) : cmk(0, 0);
-    }
-  }
   if (threadIdx.x == 0) {
     for (int i = 0; i < kSlots; ++i) {
       mbar_init(&full[i], 1);
@@ -87,6 +72,23 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_reduce_tma(const __grid_co
     }
     return;
   }
+  // constant cores: G1 of every chi staged by the consumer warps while the producer already
+  // streams u (the fragments are needed only once the first stage has landed)
+  for (int b = 0; b < a.nbatch; ++b) {
+    const cplx* __restrict__ G1 = a.G1[b];
+    const int r1 = a.r1[b];
+    if (NTD > 0)
+      for (int e = threadIdx.x; e < ks_n * NTD * 32; e += 32 * CW) {
+        const int ln = e % 32, nt = (e / 32) % NTD, ks = e / (32 * NTD);
+        const int k = 4 * ks + (ln & 3), n = 8 * nt + (ln >> 2);
+        Bf[(size_t)b * ks_n * NTD * 32 + e] = (k < n1 && n < r1) ? __ldg(G1 + k + (int64_t)n1 * n) : cmk(0, 0);
+      }
+    for (int e = threadIdx.x; e < 4 * ks_n * REM; e += 32 * CW) {
+      const int j = e % REM, k = e / REM, n = 8 * NTD + j;
+      Gr[(size_t)b * 4 * ks_n * REM + e] = (k < n1 && n < r1) ? __ldg(G1 + k + (int64_t)n1 * n) : cmk(0, 0);
+    }
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * CW) : "memory");   // consumers only
   pdl_wait();
   const int g = lane >> 2, t = lane & 3;
   const double sgn = a.conj_u ? -1.0 : 1.0;
@@ -106,8 +108,9 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_reduce_tma(const __grid_co
 #pragma unroll
     for (int j = 0; j < REM; ++j) rem[j] = cmk(0, 0);
     const bool gok = g < ncol;   // columns past the CTA's range hold stale data: rows g discarded
+    const int ks_end = a.diag == 1 ? 0 : ks_n;
 #pragma unroll 4
-    for (int ks = 0; ks < ks_n; ++ks) {
+    for (int ks = 0; ks < ks_end; ++ks) {
       const int k = 4 * ks + t;
       cplx av = (k < n1) ? st[k] : cmk(0, 0);
       av.y *= sgn;
@@ -156,7 +159,7 @@ void launch_rt(const ReduceArgs& a, int ns, size_t smem, cudaStream_t st) {
                                          (int)smem));
     attr = smem;
   }
-  launch_pdl(k_reduce_tma<NTD, REM, CW, SPW>, dim3(ns), dim3(32 * (CW + 1)), smem, st, a);
+  launch_pdl(k_reduce_tma<NTD, REM, CW, SPW>, dim3(ns), dim3(32 * (CW + 1)), smem, st, a);  // a.diag set by the caller
 }
 
 }  // namespace
@@ -209,17 +212,23 @@ bool launch_reduce_g1_tma(const ReduceArgs& a, cudaStream_t st) {
   size_t smem;
   if (!rt_geometry(a.n1, r1max, ntd, rem, cw, spw, smem)) return false;
   const int ns = sm_count_dev();
+  static const int diag = [] {
+    const char* e = std::getenv("VSIE_RT_DIAG");
+    return e ? std::atoi(e) : 0;
+  }();
+  ReduceArgs ad = a;
+  ad.diag = diag;
 #define VSIE_RT(NTD, REM)                                                                    \
   if (ntd == NTD && rem == REM) {                                                            \
-    if (cw == 8 && spw == 3) launch_rt<NTD, REM, 8, 3>(a, ns, smem, st);                     \
-    else if (cw == 8 && spw == 2) launch_rt<NTD, REM, 8, 2>(a, ns, smem, st);                \
-    else if (cw == 8) launch_rt<NTD, REM, 8, 1>(a, ns, smem, st);                            \
-    else if (cw == 4 && spw == 3) launch_rt<NTD, REM, 4, 3>(a, ns, smem, st);                \
-    else if (cw == 4 && spw == 2) launch_rt<NTD, REM, 4, 2>(a, ns, smem, st);                \
-    else if (cw == 4) launch_rt<NTD, REM, 4, 1>(a, ns, smem, st);                            \
-    else if (spw == 3) launch_rt<NTD, REM, 2, 3>(a, ns, smem, st);                           \
-    else if (spw == 2) launch_rt<NTD, REM, 2, 2>(a, ns, smem, st);                           \
-    else launch_rt<NTD, REM, 2, 1>(a, ns, smem, st);                                         \
+    if (cw == 8 && spw == 3) launch_rt<NTD, REM, 8, 3>(ad, ns, smem, st);                     \
+    else if (cw == 8 && spw == 2) launch_rt<NTD, REM, 8, 2>(ad, ns, smem, st);                \
+    else if (cw == 8) launch_rt<NTD, REM, 8, 1>(ad, ns, smem, st);                            \
+    else if (cw == 4 && spw == 3) launch_rt<NTD, REM, 4, 3>(ad, ns, smem, st);                \
+    else if (cw == 4 && spw == 2) launch_rt<NTD, REM, 4, 2>(ad, ns, smem, st);                \
+    else if (cw == 4) launch_rt<NTD, REM, 4, 1>(ad, ns, smem, st);                            \
+    else if (spw == 3) launch_rt<NTD, REM, 2, 3>(ad, ns, smem, st);                           \
+    else if (spw == 2) launch_rt<NTD, REM, 2, 2>(ad, ns, smem, st);                           \
+    else launch_rt<NTD, REM, 2, 1>(ad, ns, smem, st);                                         \
     VSIE_CHECK_LAUNCH();                                                                     \
     return true;                                                                             \
   }
