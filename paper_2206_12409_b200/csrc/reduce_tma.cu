@@ -43,7 +43,10 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_reduce_tma(const __grid_co
   __shared__ uint64_t full[kSlots], empty[kSlots];
   const int ns = gridDim.x, s = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t c0 = a.ncol * s / ns, c1 = a.ncol * (s + 1) / ns;
+  // CTA column ranges start on multiples of 8 columns: every stage is one whole M tile and
+  // (for n1 = 4 mod 8) its bulk copy starts on a 128-B boundary
+  const int64_t c0 = s == 0 ? 0 : a.ncol * s / ns / 8 * 8;
+  const int64_t c1 = s == ns - 1 ? a.ncol : a.ncol * (s + 1) / ns / 8 * 8;
   const int nc = (int)(c1 - c0);
   const int nst = (nc + 7) / 8;   // stages per chi (same for every chi)
   if (threadIdx.x == 0) {
