@@ -496,18 +496,28 @@ __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant_
 constexpr int kRedWarps = 4;                  // 128-thread CTAs: 3 resident per SM
 constexpr int kRedThreads = 32 * kRedWarps;
 
-template <int NT>
+// NT DMMA n-tiles cover a < 8 NT; the REM <= 2 values a = 8 NT .. 8 NT + REM - 1 (r1 = 9, 10,
+// 17, 18) run as exact DFMA on the same u registers (DMMA and DFMA share the FP64 pipe, so
+// padding r1 = 10 to 16 or 17 to 24 would cost 1.6x / 1.4x the FP64 cycles)
+template <int NT, int REM>
 __global__ void __launch_bounds__(kRedThreads) k_reduce_g1(const __grid_constant__ ReduceArgs a) {
   const int b = blockIdx.y;
   const int n1 = a.n1, r1 = a.r1[b];
   const int ks_n = (n1 + 3) / 4;
-  extern __shared__ cplx Bf[];   // [ks_n][NT][32] fragments of G1
+  constexpr int NTA = NT > 0 ? NT : 1;
+  extern __shared__ cplx Bf[];   // [ks_n][NT][32] fragments of G1, then [4 ks_n][REM] columns
+  cplx* Gr = Bf + (size_t)ks_n * NTA * 32;
   const cplx* __restrict__ G1 = a.G1[b];
   // G1 is a constant core: staged before waiting on the stream predecessor (PDL overlap)
-  for (int e = threadIdx.x; e < ks_n * NT * 32; e += kRedThreads) {
-    const int lane = e % 32, nt = (e / 32) % NT, ks = e / (32 * NT);
-    const int k = 4 * ks + (lane & 3), n = 8 * nt + (lane >> 2);
-    Bf[e] = (k < n1 && n < r1) ? __ldg(G1 + k + (int64_t)n1 * n) : cmk(0, 0);
+  if (NT > 0)
+    for (int e = threadIdx.x; e < ks_n * NT * 32; e += kRedThreads) {
+      const int lane = e % 32, nt = (e / 32) % NTA, ks = e / (32 * NTA);
+      const int k = 4 * ks + (lane & 3), n = 8 * nt + (lane >> 2);
+      Bf[e] = (k < n1 && n < r1) ? __ldg(G1 + k + (int64_t)n1 * n) : cmk(0, 0);
+    }
+  for (int e = threadIdx.x; e < 4 * ks_n * REM; e += kRedThreads) {
+    const int j = e % (REM > 0 ? REM : 1), k = e / (REM > 0 ? REM : 1), n = 8 * NT + j;
+    Gr[e] = (k < n1 && n < r1) ? __ldg(G1 + k + (int64_t)n1 * n) : cmk(0, 0);
   }
   __syncthreads();
   pdl_wait();
@@ -521,9 +531,12 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce_g1(const __grid_constant
     const bool cok = cg < a.ncol;
     const cplx* __restrict__ U = a.u[b] + (cok ? col_addr(cg, a.cols_per_rhs, a.ld_rhs, n1) : 0);
     // 3 real DMMAs per complex product (P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi))
-    double p1[NT][2], p2[NT][2], p3[NT][2];
+    double p1[NTA][2], p2[NTA][2], p3[NTA][2];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) p1[nt][0] = p1[nt][1] = p2[nt][0] = p2[nt][1] = p3[nt][0] = p3[nt][1] = 0;
+    for (int nt = 0; nt < NTA; ++nt) p1[nt][0] = p1[nt][1] = p2[nt][0] = p2[nt][1] = p3[nt][0] = p3[nt][1] = 0;
+    cplx rem[REM > 0 ? REM : 1];
+#pragma unroll
+    for (int j = 0; j < REM; ++j) rem[j] = cmk(0, 0);
     constexpr int UNR = 25;   // n1 <= 100: the whole column tile in flight at once
     for (int ks = 0; ks < ks_n; ks += UNR) {
       cplx av[UNR];
@@ -538,17 +551,19 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce_g1(const __grid_constant
           const double ar = av[q].x, ai = sgn * av[q].y, as = ar + ai;
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
-            const cplx bv = Bf[((ks + q) * NT + nt) * 32 + lane];
+            const cplx bv = Bf[((ks + q) * NTA + nt) * 32 + lane];
             dmma(p1[nt][0], p1[nt][1], ar, bv.x);
             dmma(p2[nt][0], p2[nt][1], ai, bv.y);
             dmma(p3[nt][0], p3[nt][1], as, bv.x + bv.y);
           }
+#pragma unroll
+          for (int j = 0; j < REM; ++j) cfma(rem[j], Gr[(4 * (ks + q) + t) * REM + j], cmk(ar, ai));
         }
       }
     }
     // lane holds rows c = c0 + g, columns a = 8 nt + 2 t + j
+    cplx* __restrict__ W = a.W1[b] + (int64_t)r1 * cg;
     if (cok) {
-      cplx* __restrict__ W = a.W1[b] + (int64_t)r1 * cg;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -556,6 +571,16 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce_g1(const __grid_constant
           const int aa = 8 * nt + 2 * t + j;
           if (aa < r1) W[aa] = cmk(p1[nt][j] - p2[nt][j], p3[nt][j] - p1[nt][j] - p2[nt][j]);
         }
+    }
+#pragma unroll
+    for (int j = 0; j < REM; ++j) {
+      cplx v = rem[j];   // sum over the four k lanes t of this column
+      v.x += __shfl_xor_sync(0xffffffffu, v.x, 1);
+      v.y += __shfl_xor_sync(0xffffffffu, v.y, 1);
+      v.x += __shfl_xor_sync(0xffffffffu, v.x, 2);
+      v.y += __shfl_xor_sync(0xffffffffu, v.y, 2);
+      const int aa = 8 * NT + j;
+      if (cok && t == 0 && aa < r1) W[aa] = v;
     }
   }
   pdl_trigger();
@@ -926,23 +951,34 @@ void launch_reduce_g1(const ReduceArgs& a, cudaStream_t st) {
   int r1max = 0;
   for (int b = 0; b < a.nbatch; ++b) r1max = std::max(r1max, a.r1[b]);
   VSIE_REQUIRE(r1max <= 32, VSIE_ERR_ARG, "reduce: r1 > 32 not supported");
-  const int NT = (r1max + 7) / 8;
-  const size_t smem = (size_t)((a.n1 + 3) / 4) * NT * 32 * sizeof(cplx);
+  // DMMA n-tiles for 8 NT values of a, exact DFMA for r1 % 8 <= 2 more (VSIE_REDUCE_REM=0:
+  // pad to whole DMMA tiles)
+  static const int rem_on = [] {
+    const char* e = std::getenv("VSIE_REDUCE_REM");
+    return e ? std::atoi(e) : 1;
+  }();
+  int NT = r1max / 8, REM = r1max % 8;
+  if (REM > 2 || !rem_on) {
+    NT = (r1max + 7) / 8;
+    REM = 0;
+  }
+  const int ks_n = (a.n1 + 3) / 4;
+  const size_t smem = ((size_t)ks_n * std::max(NT, 1) * 32 + (size_t)4 * ks_n * REM) * sizeof(cplx);
   VSIE_REQUIRE(smem <= 200 * 1024, VSIE_ERR_ARG, "reduce: n1 * r1 too large for shared memory");
-#define VSIE_RED(K)                                                                                        \
-  case K: {                                                                                                \
+#define VSIE_RED(K, R)                                                                                     \
+  if (NT == K && REM == R) {                                                                               \
     static bool d = false;                                                                                 \
-    set_smem_attr_once(k_reduce_g1<K>, d);                                                                 \
+    set_smem_attr_once(k_reduce_g1<K, R>, d);                                                              \
     dim3 grid((unsigned)std::min<int64_t>(ceil_div(a.ncol, kColsPerWarp * kRedWarps),                      \
-                                          g1_ctas_per_chi(a.nbatch, (const void*)k_reduce_g1<K>, smem, kRedThreads)), a.nbatch); \
-    launch_pdl(k_reduce_g1<K>, grid, dim3(kRedThreads), smem, st, a);                                      \
-    break;                                                                                                 \
+                                          g1_ctas_per_chi(a.nbatch, (const void*)k_reduce_g1<K, R>, smem, kRedThreads)), a.nbatch); \
+    launch_pdl(k_reduce_g1<K, R>, grid, dim3(kRedThreads), smem, st, a);                                   \
+    VSIE_CHECK_LAUNCH();                                                                                   \
+    return;                                                                                                \
   }
-  switch (NT) {
-    VSIE_RED(1) VSIE_RED(2) VSIE_RED(3) default: VSIE_RED(4)
-  }
+  VSIE_RED(0, 1) VSIE_RED(0, 2) VSIE_RED(1, 0) VSIE_RED(1, 1) VSIE_RED(1, 2) VSIE_RED(2, 0) VSIE_RED(2, 1)
+  VSIE_RED(2, 2) VSIE_RED(3, 0) VSIE_RED(3, 1) VSIE_RED(3, 2) VSIE_RED(4, 0)
+  VSIE_REQUIRE(false, VSIE_ERR_ARG, "reduce: unsupported r1");
 #undef VSIE_RED
-  VSIE_CHECK_LAUNCH();
 }
 
 bool launch_g21_fwd(const G21Args& a, cudaStream_t st) {
