@@ -418,30 +418,40 @@ __device__ __forceinline__ void zmma(double (&cr)[2], double (&ci)[2], cplx a, c
 // y[i1 + n1 c] = sum_a G1[i1 + n1 a] Y2[a + r1 c]: warp task = 8 columns x all i1;
 // Y2 fragments in registers (KT k-steps), G1 fragments from shared memory; each
 // 8 x 8 output tile is stored as 4 whole 128-B lines per warp instruction.
-template <int KT>
+// KT DMMA k-steps cover k < 4 KT; the REMK <= 2 remaining k = 4 KT .. (r1 = 10, 17, 18 at
+// the measured ranks) run as exact DFMA (shared FP64 pipe: no padding of K to 4 KT + 4)
+template <int KT, int REMK>
 __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant__ ExpandArgs a) {
   const int b = blockIdx.y;
   const int n1 = a.n1, r1 = a.r1[b];
   const int mt = (n1 + 7) / 8;
-  extern __shared__ cplx Af[];   // [mt][KT][32] fragments of G1
+  constexpr int KTA = KT > 0 ? KT : 1, RA = REMK > 0 ? REMK : 1;
+  extern __shared__ cplx Af[];   // [mt][KT][32] fragments of G1, then [8 mt][REMK] columns
+  cplx* Gk = Af + (size_t)mt * KTA * 32;
   const cplx* __restrict__ G1 = a.G1[b];
   // G1 is a constant core: staged before waiting on the producer of Y2 (PDL overlap)
-  for (int e = threadIdx.x; e < mt * KT * 32; e += kG1Threads) {
-    const int lane = e % 32, ks = (e / 32) % KT, m = e / (32 * KT);
-    const int i1 = 8 * m + (lane >> 2), k = 4 * ks + (lane & 3);
-    Af[e] = (i1 < n1 && k < r1) ? __ldg(G1 + i1 + (int64_t)n1 * k) : cmk(0, 0);
+  if (KT > 0)
+    for (int e = threadIdx.x; e < mt * KT * 32; e += kG1Threads) {
+      const int lane = e % 32, ks = (e / 32) % KTA, m = e / (32 * KTA);
+      const int i1 = 8 * m + (lane >> 2), k = 4 * ks + (lane & 3);
+      Af[e] = (i1 < n1 && k < r1) ? __ldg(G1 + i1 + (int64_t)n1 * k) : cmk(0, 0);
+    }
+  for (int e = threadIdx.x; e < 8 * mt * REMK; e += kG1Threads) {
+    const int j = e % RA, i1 = e / RA, k = 4 * KT + j;
+    Gk[e] = (i1 < n1 && k < r1) ? __ldg(G1 + i1 + (int64_t)n1 * k) : cmk(0, 0);
   }
   __syncthreads();
   pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   cplx* __restrict__ Y = a.y[b];
-  // persistent: warp tasks of 8 columns, the next task's Y2 fragments loaded before the
+  // persistent: warp tasks of 8 columns, the next task's Y2 values loaded before the
   // current task's DMMAs and stores
   const int64_t ntask = (a.ncol + kColsPerWarp - 1) / kColsPerWarp;
   const int64_t stride = (int64_t)gridDim.x * kWarpsG1;
   int64_t task = (int64_t)blockIdx.x * kWarpsG1 + warp;
-  auto load_bf = [&](int64_t tk, cplx (&bf)[KT]) {
+  // DMMA fragments bf[ks] = Y2[4 ks + t][col g]; DFMA values yr[j][jj] = Y2[4 KT + j][col 2 t + jj]
+  auto load_bf = [&](int64_t tk, cplx (&bf)[KTA], cplx (&yr)[RA][2]) {
     const int64_t c = tk * kColsPerWarp + g;
     const cplx* __restrict__ Y2 = a.Y2[b] + (int64_t)r1 * c;
 #pragma unroll
@@ -449,12 +459,20 @@ __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant_
       const int k = 4 * ks + t;
       bf[ks] = (tk < ntask && c < a.ncol && k < r1) ? __ldg(Y2 + k) : cmk(0, 0);
     }
+#pragma unroll
+    for (int j = 0; j < REMK; ++j)
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {
+        const int64_t cc = tk * kColsPerWarp + 2 * t + jj;
+        const int k = 4 * KT + j;
+        yr[j][jj] = (tk < ntask && cc < a.ncol && k < r1) ? __ldg(a.Y2[b] + (int64_t)r1 * cc + k) : cmk(0, 0);
+      }
   };
-  cplx bf[KT];
-  load_bf(task, bf);
+  cplx bf[KTA], yr[RA][2];
+  load_bf(task, bf, yr);
   for (; task < ntask; task += stride) {
-    cplx bn[KT];
-    load_bf(task + stride, bn);
+    cplx bn[KTA], yn[RA][2];
+    load_bf(task + stride, bn, yn);
     const int64_t c0 = task * kColsPerWarp;
     int64_t oaddr[2];
     bool ok[2];
@@ -464,7 +482,7 @@ __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant_
       ok[j] = c < a.ncol;
       oaddr[j] = ok[j] ? col_addr(c, a.cols_per_rhs, a.ld_rhs, n1) : 0;
     }
-    double bsum[KT];
+    double bsum[KTA];
 #pragma unroll
     for (int ks = 0; ks < KT; ++ks) bsum[ks] = bf[ks].x + bf[ks].y;
     for (int m = 0; m < mt; ++m) {
@@ -472,20 +490,34 @@ __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant_
       double p1[2] = {0, 0}, p2[2] = {0, 0}, p3[2] = {0, 0};
 #pragma unroll
       for (int ks = 0; ks < KT; ++ks) {
-        const cplx av = Af[(m * KT + ks) * 32 + lane];
+        const cplx av = Af[(m * KTA + ks) * 32 + lane];
         dmma(p1[0], p1[1], av.x, bf[ks].x);
         dmma(p2[0], p2[1], av.y, bf[ks].y);
         dmma(p3[0], p3[1], av.x + av.y, bsum[ks]);
       }
       const int i1 = 8 * m + g;
+      cplx o[2];
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) o[jj] = cmk(p1[jj] - p2[jj], p3[jj] - p1[jj] - p2[jj]);
+#pragma unroll
+      for (int j = 0; j < REMK; ++j) {
+        const cplx gv = Gk[i1 * RA + j];
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) cfma(o[jj], gv, yr[j][jj]);
+      }
       if (i1 < n1) {
 #pragma unroll
         for (int j = 0; j < 2; ++j)
-          if (ok[j]) __stcs(Y + oaddr[j] + i1, cmk(p1[j] - p2[j], p3[j] - p1[j] - p2[j]));
+          if (ok[j]) __stcs(Y + oaddr[j] + i1, o[j]);
       }
     }
 #pragma unroll
     for (int ks = 0; ks < KT; ++ks) bf[ks] = bn[ks];
+#pragma unroll
+    for (int j = 0; j < REMK; ++j) {
+      yr[j][0] = yn[j][0];
+      yr[j][1] = yn[j][1];
+    }
   }
   pdl_trigger();
 }
@@ -917,23 +949,38 @@ void launch_expand_g1(const ExpandArgs& a, cudaStream_t st) {
   int r1max = 0;
   for (int b = 0; b < a.nbatch; ++b) r1max = std::max(r1max, a.r1[b]);
   VSIE_REQUIRE(r1max <= 32, VSIE_ERR_ARG, "expand: r1 > 32 not supported");
-  const int KT = (r1max + 3) / 4;
-  const size_t smem = (size_t)((a.n1 + 7) / 8) * KT * 32 * sizeof(cplx);
+  // DMMA k-steps for 4 KT values of k, exact DFMA for r1 % 4 == 1 more (r1 = 17: 4 + 1
+  // instead of 5 padded k-steps, cfg 5 expansion 2.62 -> 2.53 ms per chi); with r1 % 4 == 2
+  // (r1 = 10) the padded DMMA step measured faster than two DFMA columns (14.6 vs 15.4 us at
+  // cfg 2), so VSIE_EXPAND_REM: 1 (default) remainder 1 only, 2 remainders 1 and 2, 0 never
+  static const int rem_on = [] {
+    const char* e = std::getenv("VSIE_EXPAND_REM");
+    return e ? std::atoi(e) : 1;
+  }();
+  int KT = r1max / 4, REMK = r1max % 4;
+  if (REMK > rem_on || rem_on == 0) {
+    KT = (r1max + 3) / 4;
+    REMK = 0;
+  }
+  const int mt = (a.n1 + 7) / 8;
+  const size_t smem = ((size_t)mt * std::max(KT, 1) * 32 + (size_t)8 * mt * REMK) * sizeof(cplx);
   VSIE_REQUIRE(smem <= 200 * 1024, VSIE_ERR_ARG, "expand: n1 * r1 too large for shared memory");
-#define VSIE_EXP(K)                                                                                        \
-  case K: {                                                                                                \
+#define VSIE_EXP(K, R)                                                                                     \
+  if (KT == K && REMK == R) {                                                                              \
     static bool d = false;                                                                                 \
-    set_smem_attr_once(k_expand_g1<K>, d);                                                                 \
+    set_smem_attr_once(k_expand_g1<K, R>, d);                                                              \
     dim3 grid((unsigned)std::min<int64_t>(ceil_div(a.ncol, kColsPerCtaG1),                                 \
-                                          g1_ctas_per_chi(a.nbatch, (const void*)k_expand_g1<K>, smem, kG1Threads)), a.nbatch); \
-    launch_pdl(k_expand_g1<K>, grid, dim3(kG1Threads), smem, st, a);                                       \
-    break;                                                                                                 \
+                                          g1_ctas_per_chi(a.nbatch, (const void*)k_expand_g1<K, R>, smem, kG1Threads)), a.nbatch); \
+    launch_pdl(k_expand_g1<K, R>, grid, dim3(kG1Threads), smem, st, a);                                    \
+    VSIE_CHECK_LAUNCH();                                                                                   \
+    return;                                                                                                \
   }
-  switch (KT) {
-    VSIE_EXP(1) VSIE_EXP(2) VSIE_EXP(3) VSIE_EXP(4) VSIE_EXP(5) VSIE_EXP(6) VSIE_EXP(7) default: VSIE_EXP(8)
-  }
+  VSIE_EXP(0, 1) VSIE_EXP(0, 2) VSIE_EXP(1, 0) VSIE_EXP(1, 1) VSIE_EXP(1, 2) VSIE_EXP(2, 0) VSIE_EXP(2, 1)
+  VSIE_EXP(2, 2) VSIE_EXP(3, 0) VSIE_EXP(3, 1) VSIE_EXP(3, 2) VSIE_EXP(4, 0) VSIE_EXP(4, 1) VSIE_EXP(4, 2)
+  VSIE_EXP(5, 0) VSIE_EXP(5, 1) VSIE_EXP(5, 2) VSIE_EXP(6, 0) VSIE_EXP(6, 1) VSIE_EXP(6, 2) VSIE_EXP(7, 0)
+  VSIE_EXP(7, 1) VSIE_EXP(7, 2) VSIE_EXP(8, 0)
+  VSIE_REQUIRE(false, VSIE_ERR_ARG, "expand: unsupported r1");
 #undef VSIE_EXP
-  VSIE_CHECK_LAUNCH();
 }
 
 // the TMA-streamed batched reduction (reduce_tma.cu) for batched single-RHS calls;

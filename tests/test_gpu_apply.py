@@ -290,7 +290,8 @@ _SCHEDULES = [
     dict(VSIE_PAIR_G4="4", VSIE_W2_PARTS="1", VSIE_REDUCE_TMA="0"),
     dict(VSIE_PAIR_G4="5"),
     dict(VSIE_PAIR_G4="2", VSIE_SINGLE_TMA="0", VSIE_G2T="0"),
-    dict(VSIE_PAIR_G4="0", VSIE_REDUCE_REM="0"),
+    dict(VSIE_PAIR_G4="0", VSIE_REDUCE_REM="0", VSIE_EXPAND_REM="0"),
+    dict(VSIE_PAIR_G4="2", VSIE_EXPAND_REM="2"),
 ]
 
 
