@@ -448,7 +448,7 @@ def main():
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tp):
             with open(tp) as f:
-                traffic = json.load(f).get(dom["name"])
+                traffic = json.load(f).get(f"cfg{cfg.idx}", {}).get(dom["name"])
         roof = {"bound": "hbm", "kernel": dom["name"], "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": ach / peak, "traffic": traffic, "peak_source": peak_kind,
                 "share_of_step": dom["total_ms"] / max(1e-9, sum(t["total_ms"] for t in timers)),
