@@ -429,13 +429,25 @@ __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant_
   extern __shared__ cplx Af[];   // [mt][KT][32] fragments of G1, then [8 mt][REMK] columns
   cplx* Gk = Af + (size_t)mt * KTA * 32;
   const cplx* __restrict__ G1 = a.G1[b];
-  // G1 is a constant core: staged before waiting on the producer of Y2 (PDL overlap)
-  if (KT > 0)
-    for (int e = threadIdx.x; e < mt * KT * 32; e += kG1Threads) {
-      const int lane = e % 32, ks = (e / 32) % KTA, m = e / (32 * KTA);
-      const int i1 = 8 * m + (lane >> 2), k = 4 * ks + (lane & 3);
-      Af[e] = (i1 < n1 && k < r1) ? __ldg(G1 + i1 + (int64_t)n1 * k) : cmk(0, 0);
+  // G1 is a constant core: staged before waiting on the producer of Y2 (PDL overlap), all
+  // of a thread's loads in flight before its stores (a load -> store per element costs one
+  // global latency per element, ~5 us of the kernel when nothing overlaps it)
+  if (KT > 0) {
+    const int tot = mt * KT * 32;
+    for (int e0 = threadIdx.x; e0 < tot; e0 += 8 * kG1Threads) {
+      cplx v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int e = e0 + q * kG1Threads;
+        const int lane = e % 32, ks = (e / 32) % KTA, m = e / (32 * KTA);
+        const int i1 = 8 * m + (lane >> 2), k = 4 * ks + (lane & 3);
+        v[q] = (e < tot && i1 < n1 && k < r1) ? __ldg(G1 + i1 + (int64_t)n1 * k) : cmk(0, 0);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (e0 + q * kG1Threads < tot) Af[e0 + q * kG1Threads] = v[q];
     }
+  }
   for (int e = threadIdx.x; e < 8 * mt * REMK; e += kG1Threads) {
     const int j = e % RA, i1 = e / RA, k = 4 * KT + j;
     Gk[e] = (i1 < n1 && k < r1) ? __ldg(G1 + i1 + (int64_t)n1 * k) : cmk(0, 0);
@@ -540,13 +552,24 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce_g1(const __grid_constant
   extern __shared__ cplx Bf[];   // [ks_n][NT][32] fragments of G1, then [4 ks_n][REM] columns
   cplx* Gr = Bf + (size_t)ks_n * NTA * 32;
   const cplx* __restrict__ G1 = a.G1[b];
-  // G1 is a constant core: staged before waiting on the stream predecessor (PDL overlap)
-  if (NT > 0)
-    for (int e = threadIdx.x; e < ks_n * NT * 32; e += kRedThreads) {
-      const int lane = e % 32, nt = (e / 32) % NTA, ks = e / (32 * NTA);
-      const int k = 4 * ks + (lane & 3), n = 8 * nt + (lane >> 2);
-      Bf[e] = (k < n1 && n < r1) ? __ldg(G1 + k + (int64_t)n1 * n) : cmk(0, 0);
+  // G1 is a constant core: staged before waiting on the stream predecessor (PDL overlap),
+  // all of a thread's loads in flight before its stores
+  if (NT > 0) {
+    const int tot = ks_n * NT * 32;
+    for (int e0 = threadIdx.x; e0 < tot; e0 += 8 * kRedThreads) {
+      cplx v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int e = e0 + q * kRedThreads;
+        const int lane = e % 32, nt = (e / 32) % NTA, ks = e / (32 * NTA);
+        const int k = 4 * ks + (lane & 3), n = 8 * nt + (lane >> 2);
+        v[q] = (e < tot && k < n1 && n < r1) ? __ldg(G1 + k + (int64_t)n1 * n) : cmk(0, 0);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (e0 + q * kRedThreads < tot) Bf[e0 + q * kRedThreads] = v[q];
     }
+  }
   for (int e = threadIdx.x; e < 4 * ks_n * REM; e += kRedThreads) {
     const int j = e % (REM > 0 ? REM : 1), k = e / (REM > 0 ? REM : 1), n = 8 * NT + j;
     Gr[e] = (k < n1 && n < r1) ? __ldg(G1 + k + (int64_t)n1 * n) : cmk(0, 0);
