@@ -111,10 +111,22 @@ __global__ void __launch_bounds__(kPairThreads, 1) k_pair_g4(const __grid_consta
   if (FW)
     for (int j = threadIdx.x; j < nc; j += 32 * kConsumerWarps) xs[j] = __ldg(a.x + c0 + j);
   pdl_wait();   // z3 comes from the stream predecessor
-  if (TR)
-    for (int b = 0; b < a.nbatch; ++b)
-      for (int r = threadIdx.x; r < 32 * NQ; r += 32 * kConsumerWarps)
-        zs[b * 32 * NQ + r] = r < a.R[b] ? __ldcg(a.z3[b] + r) : cmk(0, 0);   // rows past R: zero weight
+  if (TR) {
+    // all of a thread's z3 loads in flight before its stores (this sits after the PDL wait,
+    // on the critical path)
+    constexpr int PER = (3 * 32 * NQ + 32 * kConsumerWarps - 1) / (32 * kConsumerWarps);
+    cplx v[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int e = threadIdx.x + q * 32 * kConsumerWarps, b = e / (32 * NQ), r = e - b * 32 * NQ;
+      v[q] = (b < a.nbatch && r < a.R[b]) ? __ldcg(a.z3[b] + r) : cmk(0, 0);   // rows past R: zero weight
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int e = threadIdx.x + q * 32 * kConsumerWarps;
+      if (e < 3 * 32 * NQ) zs[e] = v[q];
+    }
+  }
   consumers_sync();
   for (int b = 0; b < a.nbatch; ++b) {
     const int R = (int)a.R[b];

@@ -130,8 +130,20 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_seg_gemv(const __grid_consta
         }
       }
     }
-    if (FW)
-      for (int c = threadIdx.x; c < C; c += 32 * kCW) vecx[c] = __ldcg(a.x[b] + c);
+    if (FW) {
+      // x of this chi (r3 <= ~2k values): a thread's loads in flight before its stores
+      for (int c0 = threadIdx.x; c0 < C; c0 += 4 * 32 * kCW) {
+        cplx v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int c = c0 + q * 32 * kCW;
+          v[q] = c < C ? __ldcg(a.x[b] + c) : cmk(0, 0);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (c0 + q * 32 * kCW < C) vecx[c0 + q * 32 * kCW] = v[q];
+      }
+    }
     csync();
     if (Lb > 0) {
       for (int t = (warp - off[b] % kCW + kCW) % kCW; t < nst[b]; t += kCW) {
