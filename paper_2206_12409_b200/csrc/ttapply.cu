@@ -1006,12 +1006,14 @@ void launch_expand_g1(const ExpandArgs& a, cudaStream_t st) {
 #undef VSIE_EXP
 }
 
-// the TMA-streamed batched reduction (reduce_tma.cu) for batched single-RHS calls;
-// VSIE_REDUCE_TMA=0 keeps k_reduce_g1
+// the TMA-streamed batched reduction (reduce_tma.cu) for batched single-RHS calls, opt-in
+// VSIE_REDUCE_TMA=1: once k_reduce_g1 ran exact DFMA for the r1 % 8 remainder, three
+// concurrent per-chi reductions (15.7 us each) beat the single 63 MB pass (cfg 2 pair
+// 0.1625 vs 0.1640 ms)
 bool reduce_tma_on() {
   static const int v = [] {
     const char* e = std::getenv("VSIE_REDUCE_TMA");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 0;
   }();
   return v != 0;
 }

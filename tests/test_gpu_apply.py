@@ -281,13 +281,14 @@ _SCHEDULES = [
     dict(VSIE_PAIR_G4="0"),
     dict(VSIE_PAIR_G4="2", VSIE_SEG_G3="0"),
     dict(VSIE_PAIR_G4="2", VSIE_W2_PARTS="1", VSIE_ZGEMM_CLUSTER="1", VSIE_FWD_TAIL_BATCHED="1", VSIE_G2T="0"),
-    dict(VSIE_PAIR_G4="2", VSIE_REDUCE_TMA="0"),
+    dict(VSIE_PAIR_G4="2", VSIE_REDUCE_TMA="1"),
+    dict(VSIE_PAIR_G4="2", VSIE_REDUCE_TMA="1", VSIE_RT_CW="8"),
     dict(VSIE_PAIR_G4="2", VSIE_G2T="0", VSIE_ADJ_FUSED="0"),
     dict(VSIE_PAIR_G4="2", VSIE_G2N="1"),
     dict(VSIE_PAIR_G4="2", VSIE_ADJ_FUSED="1"),
     dict(VSIE_PAIR_G4="3"),
     dict(VSIE_PAIR_G4="4"),
-    dict(VSIE_PAIR_G4="4", VSIE_W2_PARTS="1", VSIE_REDUCE_TMA="0"),
+    dict(VSIE_PAIR_G4="4", VSIE_W2_PARTS="1", VSIE_REDUCE_TMA="1"),
     dict(VSIE_PAIR_G4="5"),
     dict(VSIE_PAIR_G4="2", VSIE_SINGLE_TMA="0", VSIE_G2T="0"),
     dict(VSIE_PAIR_G4="0", VSIE_REDUCE_REM="0", VSIE_EXPAND_REM="0"),
@@ -302,8 +303,8 @@ def test_pair_schedules(env):
     4 every step one batched launch, 5 streaming passes beside the other direction's chains;
     VSIE_W2_PARTS=1 leaves the G2^T split-K partials to the
     G3^T kernel; VSIE_ZGEMM_CLUSTER=0 split-K through global partials instead of the cluster /
-    DSMEM reduction; VSIE_ADJ_FUSED=1 the fused G1^T + G2^T kernel k_adj12; VSIE_REDUCE_TMA=0
-    the per-chi k_reduce_g1 instead of the batched TMA-streamed G1^T; VSIE_FWD_TAIL_BATCHED=1
+    DSMEM reduction; VSIE_ADJ_FUSED=1 the fused G1^T + G2^T kernel k_adj12; VSIE_REDUCE_TMA=1
+    the batched TMA-streamed G1^T instead of the per-chi k_reduce_g1; VSIE_FWD_TAIL_BATCHED=1
     the forward's G2 / G1 steps as batched launches; VSIE_G2T=0 the split-K ZGEMM for G2^T
     instead of k_g2t; VSIE_G2N=1 the batched k_g2n for the forward G2 step instead of
     the per-chi ZGEMMs; VSIE_SINGLE_TMA=0 the per-chi GEMV chains in the single applies)
