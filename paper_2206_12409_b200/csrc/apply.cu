@@ -858,21 +858,33 @@ bool g2t_on() {
   return v != 0;
 }
 
-void launch_g2t_shard(vsie_coupling_s* h, const Ctx& X, Shard& s, cudaStream_t st) {
+// k_g2t per chi inside the chains (right after that chi's G1^T) instead of one batched
+// launch after the join; VSIE_G2T_CHAIN=1
+bool g2t_chain_on() {
+  static const int v = [] {
+    const char* e = std::getenv("VSIE_G2T_CHAIN");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v != 0;
+}
+
+// chi_only >= 0: the single chi chi_only (nbatch 1), else the three chi in one launch
+void launch_g2t_shard(vsie_coupling_s* h, const Ctx& X, Shard& s, cudaStream_t st, int chi_only = -1) {
   const int n2 = h->grid.n[1];
   const int64_t n3l = s.n3loc();
   if (n3l == 0) return;
   G2tArgs g{};
-  g.nbatch = 3;
+  g.nbatch = chi_only >= 0 ? 1 : 3;
   g.N = (int)n3l;
   int64_t bytes = 0, fl = 0;
-  for (int c = 0; c < 3; ++c) {
-    g.G2[c] = h->G2[c].p;
-    g.W1[c] = s.W1.p + c * X.r1m * n2 * n3l;
-    g.W2[c] = s.W2.p + c * X.r2m * n3l;
-    g.M[c] = (int)X.R(c, 1);
-    g.K[c] = (int)(X.R(c, 0) * n2);
-    g.ldw[c] = (int)X.R(c, 1);
+  for (int i = 0; i < g.nbatch; ++i) {
+    const int c = chi_only >= 0 ? chi_only : i;
+    g.G2[i] = h->G2[c].p;
+    g.W1[i] = s.W1.p + c * X.r1m * n2 * n3l;
+    g.W2[i] = s.W2.p + c * X.r2m * n3l;
+    g.M[i] = (int)X.R(c, 1);
+    g.K[i] = (int)(X.R(c, 0) * n2);
+    g.ldw[i] = (int)X.R(c, 1);
     h->w2_parts[c] = 0;
     bytes += 16 * (X.R(c, 0) * n2 * X.R(c, 1) + X.R(c, 1) * n3l + X.R(c, 0) * n2 * n3l);
     fl += 8 * X.R(c, 0) * n2 * X.R(c, 1) * n3l;
@@ -1667,16 +1679,20 @@ void pair_dag(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z
       VSIE_REQUIRE(g1_done || h->shards.size() == 1, VSIE_ERR_STATE, "reduce_tma on a partial shard set");
     }
     const bool g2b = seg && g2t_on() && X.k == 1;
+    const bool g2chain = g2b && !g1_done && g2t_chain_on();
     if (!(g1_done && g2b)) {
       fork(h, S);
       for (int c = 0; c < 3; ++c) {
         h->scope_chi = c;
-        for (Shard& s : h->shards) adj_front(X, s, c, u, cj, S.chi[c], nullptr, !seg, !g1_done, !g2b);
+        for (Shard& s : h->shards) {
+          adj_front(X, s, c, u, cj, S.chi[c], nullptr, !seg, !g1_done, !g2b);
+          if (g2chain) launch_g2t_shard(h, X, s, S.chi[c], c);   // this chi's G2^T in its chain
+        }
       }
       h->scope_chi = -1;
       if (g2b) join(h, S);
     }
-    if (g2b) {
+    if (g2b && !g2chain) {
       for (Shard& s : h->shards) launch_g2t_shard(h, X, s, S.main);
     }
   }
