@@ -148,6 +148,9 @@ __global__ void __launch_bounds__(NT) k_zgemm(Zgemm g, int splits, cplx* __restr
 // thread, summed in a fixed order (deterministic)
 __global__ void k_splitk_reduce(Zgemm g, int splits, const cplx* __restrict__ ws, int64_t ws_stride) {
   pdl_wait();
+  // tiny kernel: let the next (streaming) kernel launch now, so that it prefetches its
+  // constant core while this one runs (it still waits for our completion to read us)
+  pdl_trigger();
   const int b = blockIdx.y;
   const int64_t M = g.M[b], N = g.N[b];
   const bool has_beta = g.beta.x != 0.0 || g.beta.y != 0.0;

@@ -161,6 +161,9 @@ __global__ void __launch_bounds__(kThreads) k_sum_partials_warp(const __grid_con
                                                                 const cplx* __restrict__ partials, int nsplit,
                                                                 int64_t stride) {
   pdl_wait();
+  // tiny kernel: let the next (streaming) kernel launch now, so that it prefetches its
+  // constant core while this one runs (it still waits for our completion to read us)
+  pdl_trigger();
   const int b = blockIdx.y;
   const int64_t r = blockIdx.x * (int64_t)(kThreads / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -187,6 +190,9 @@ __global__ void __launch_bounds__(kThreads) k_sum_partials(const __grid_constant
                                                            const cplx* __restrict__ partials, int nsplit,
                                                            int64_t stride) {
   pdl_wait();
+  // tiny kernel: let the next (streaming) kernel launch now, so that it prefetches its
+  // constant core while this one runs (it still waits for our completion to read us)
+  pdl_trigger();
   const int b = blockIdx.y;
   const int64_t r = blockIdx.x * (int64_t)kThreads + threadIdx.x;
   if (r >= a.n[b]) return;
@@ -645,6 +651,9 @@ __global__ void __launch_bounds__(kThreads) k_sum3(const cplx* __restrict__ in, 
                                                    int64_t rows, int k, cplx* __restrict__ out, int64_t ld_out,
                                                    bool conj_out) {
   pdl_wait();
+  // tiny kernel: let the next (streaming) kernel launch now, so that it prefetches its
+  // constant core while this one runs (it still waits for our completion to read us)
+  pdl_trigger();
   const int64_t n = rows * k;
   for (int64_t e = blockIdx.x * (int64_t)kThreads + threadIdx.x; e < n; e += (int64_t)gridDim.x * kThreads) {
     const int64_t j = e / rows, i = e - j * rows;
