@@ -115,6 +115,33 @@ int pair_g4_mode() {
   return v;
 }
 
+// the transpose's G1^T, G2^T and G3^T per chi inside the chains (small-ring k_seg_gemv);
+// VSIE_ADJ_CHAIN_SEG=1
+bool adj_chain_seg_on() {
+  static const int v = [] {
+    const char* e = std::getenv("VSIE_ADJ_CHAIN_SEG");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v != 0;
+}
+
+// the forward's G3 pass per chi inside the chains (small-ring k_seg_gemv) instead of one
+// batched pass before them, so one chi's G2 / G1 work runs beside the next chi's G3 stream.
+// Measured: cfg 2 (34 MB of G3 per chi) 0.1606 -> 0.1565 ms; cfg 4 (64 MB per chi) 0.4553 ->
+// 0.4594 ms.  Default: on when the largest per-chi G3 slice is <= 48 MB;
+// VSIE_FWD_CHAIN_SEG=1 / 0 forces it on / off.
+bool fwd_chain_seg_on(const vsie_coupling_s* h) {
+  static const int v = [] {
+    const char* e = std::getenv("VSIE_FWD_CHAIN_SEG");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (v >= 0) return v != 0;
+  int64_t mx = 0;
+  for (const Shard& s : h->shards)
+    for (int c = 0; c < 3; ++c) mx = std::max<int64_t>(mx, 16LL * h->ranks[c][1] * s.n3loc() * h->ranks[c][2]);
+  return mx <= (48LL << 20);
+}
+
 // batched TMA-streamed G3 steps in the pair (k_seg_gemv); VSIE_SEG_G3=0 keeps the per-chi GEMVs
 bool seg_g3_on() {
   static const int v = [] {
@@ -1619,135 +1646,167 @@ void pair_dag(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z
   for (Shard& s : h->shards)
     for (int c = 0; c < 3 && seg; ++c)
       seg = seg_gemv_supported(X.R(c, 1) * s.n3loc(), X.R(c, 2), s.g3b_ns) && s.n3loc() > 0;
-  // the fused G1^T + G2^T kernel (one launch over the three chi) replaces the chains
-  const bool fused_front = seg && adj_fused_on() && adj_front_supported(h->grid.n[0], X.r1m);
-  if (fused_front) {
-    const int n2 = h->grid.n[1];
-    for (Shard& s : h->shards) {
-      const int64_t n3l = s.n3loc();
-      AdjFrontArgs f{};
-      f.nbatch = 3;
-      f.n1 = h->grid.n[0];
-      f.n2 = n2;
-      f.n3l = (int)n3l;
-      f.conj_u = cj;
-      f.w2p_stride = (int64_t)X.r2m * n3l;
-      int64_t bytes = 0, fl = 0;
-      for (int c = 0; c < 3; ++c) {
-        f.G1[c] = h->G1[c].p;
-        f.G2[c] = h->G2[c].p;
-        f.u[c] = u + c * X.L.chi_stride + shard_voxel_offset(h, s, X.L);
-        f.W2p[c] = s.W2p.p + c * (int64_t)((n2 + 7) / 8) * X.r2m * n3l;
-        f.W2[c] = s.W2.p + c * X.r2m * n3l;
-        f.r1[c] = (int)X.R(c, 0);
-        f.r2[c] = (int)X.R(c, 1);
-        h->w2_parts[c] = 0;
-        bytes += 16 * ((int64_t)f.n1 * X.R(c, 0) + X.R(c, 0) * n2 * X.R(c, 1) + (int64_t)f.n1 * n2 * n3l +
-                       X.R(c, 1) * n3l);
-        fl += 8 * ((int64_t)f.n1 * X.R(c, 0) * n2 * n3l + X.R(c, 0) * n2 * X.R(c, 1) * n3l);
-      }
-      Scope sc(h, "adj_g12_fused", bytes, fl, S.main);
-      launch_adj_front(f, S.main);
+  // transpose front entirely in the chi chains (G1^T, G2^T and a small-ring G3^T pass per
+  // chi), VSIE_ADJ_CHAIN_SEG=1
+  const bool adj_chain = seg && adj_chain_seg_on() && !exchange && g2t_on() && !reduce_tma_on() &&
+                         !adj_fused_on();
+  if (adj_chain) {
+    Shard& s = h->shards[0];
+    const int64_t n3l = s.n3loc();
+    fork(h, S);
+    for (int c = 0; c < 3; ++c) {
+      h->scope_chi = c;
+      adj_front(X, s, c, u, cj, S.chi[c], nullptr, false, true, false);   // G1^T only
+      launch_g2t_shard(h, X, s, S.chi[c], c);
+      SegGemv g{};
+      g.nbatch = 1;
+      g.nsb = s.g3b_ns;
+      g.partials = X.partials(c);   // per chain: the chains run concurrently
+      g.rstride = X.r3m;
+      g.A[0] = s.G3b[c].p;
+      g.x[0] = s.W2.p + c * X.r2m * n3l;
+      g.xparts[0] = 0;
+      g.y[0] = s.z3.p + c * X.r3stride;
+      g.R[0] = X.R(c, 1) * n3l;
+      g.C[0] = X.R(c, 2);
+      const int64_t bytes = 16 * (g.R[0] * g.C[0] + g.R[0] + g.C[0]);
+      Scope sc(h, "adj_g3_seg_chi", bytes, bytes / 2, S.chi[c]);
+      VSIE_REQUIRE(launch_seg_gemv_mode(g, 2, S.chi[c], true), VSIE_ERR_STATE, "pair: G3 shape");
     }
+    h->scope_chi = -1;
+    join(h, S);
+    fork(h, S);
   } else {
-    // W1 = G1^T u for the three chi as one TMA-streamed launch when supported, then the
-    // G2^T steps as per-chi chains
-    bool g1_done = false;
-    if (seg && reduce_tma_on() && reduce_tma_fits(h->grid.n[0], X.r1m)) {
-      g1_done = true;
+    // the fused G1^T + G2^T kernel (one launch over the three chi) replaces the chains
+    const bool fused_front = seg && adj_fused_on() && adj_front_supported(h->grid.n[0], X.r1m);
+    if (fused_front) {
+      const int n2 = h->grid.n[1];
       for (Shard& s : h->shards) {
         const int64_t n3l = s.n3loc();
-        ReduceArgs r{};
-        r.nbatch = 3;
-        r.n1 = h->grid.n[0];
-        r.ncol = (int64_t)h->grid.n[1] * n3l;
-        r.cols_per_rhs = r.ncol;
-        r.ld_rhs = X.L.ld;
-        r.conj_u = cj;
+        AdjFrontArgs f{};
+        f.nbatch = 3;
+        f.n1 = h->grid.n[0];
+        f.n2 = n2;
+        f.n3l = (int)n3l;
+        f.conj_u = cj;
+        f.w2p_stride = (int64_t)X.r2m * n3l;
         int64_t bytes = 0, fl = 0;
         for (int c = 0; c < 3; ++c) {
-          r.G1[c] = h->G1[c].p;
-          r.u[c] = u + c * X.L.chi_stride + shard_voxel_offset(h, s, X.L);
-          r.W1[c] = s.W1.p + c * X.r1m * h->grid.n[1] * n3l;
-          r.r1[c] = (int)X.R(c, 0);
-          bytes += 16 * ((int64_t)r.n1 * X.R(c, 0) + X.R(c, 0) * r.ncol + (int64_t)r.n1 * r.ncol);
-          fl += 8 * (int64_t)r.n1 * X.R(c, 0) * r.ncol;
+          f.G1[c] = h->G1[c].p;
+          f.G2[c] = h->G2[c].p;
+          f.u[c] = u + c * X.L.chi_stride + shard_voxel_offset(h, s, X.L);
+          f.W2p[c] = s.W2p.p + c * (int64_t)((n2 + 7) / 8) * X.r2m * n3l;
+          f.W2[c] = s.W2.p + c * X.r2m * n3l;
+          f.r1[c] = (int)X.R(c, 0);
+          f.r2[c] = (int)X.R(c, 1);
+          h->w2_parts[c] = 0;
+          bytes += 16 * ((int64_t)f.n1 * X.R(c, 0) + X.R(c, 0) * n2 * X.R(c, 1) + (int64_t)f.n1 * n2 * n3l +
+                         X.R(c, 1) * n3l);
+          fl += 8 * ((int64_t)f.n1 * X.R(c, 0) * n2 * n3l + X.R(c, 0) * n2 * X.R(c, 1) * n3l);
         }
-        Scope sc(h, "adj_g1_reduce_tma", bytes, fl, S.main);
-        g1_done = g1_done && n3l > 0 && launch_reduce_g1_tma(r, S.main);
+        Scope sc(h, "adj_g12_fused", bytes, fl, S.main);
+        launch_adj_front(f, S.main);
       }
-      VSIE_REQUIRE(g1_done || h->shards.size() == 1, VSIE_ERR_STATE, "reduce_tma on a partial shard set");
-    }
-    const bool g2b = seg && g2t_on() && X.k == 1;
-    const bool g2chain = g2b && !g1_done && g2t_chain_on();
-    if (!(g1_done && g2b)) {
-      fork(h, S);
-      for (int c = 0; c < 3; ++c) {
-        h->scope_chi = c;
+    } else {
+      // W1 = G1^T u for the three chi as one TMA-streamed launch when supported, then the
+      // G2^T steps as per-chi chains
+      bool g1_done = false;
+      if (seg && reduce_tma_on() && reduce_tma_fits(h->grid.n[0], X.r1m)) {
+        g1_done = true;
         for (Shard& s : h->shards) {
-          adj_front(X, s, c, u, cj, S.chi[c], nullptr, !seg, !g1_done, !g2b);
-          if (g2chain) launch_g2t_shard(h, X, s, S.chi[c], c);   // this chi's G2^T in its chain
-        }
-      }
-      h->scope_chi = -1;
-      if (g2b) join(h, S);
-    }
-    if (g2b && !g2chain) {
-      for (Shard& s : h->shards) launch_g2t_shard(h, X, s, S.main);
-    }
-  }
-  if (seg) {
-    if (!fused_front && !(seg && g2t_on())) join(h, S);
-    for (Shard& s : h->shards) {
-      const int64_t n3l = s.n3loc();
-      SegGemv g{};
-      g.nbatch = 3;
-      g.nsb = s.g3b_ns;
-      g.partials = X.partials(0);
-      g.rstride = X.r3m;
-      int64_t bytes = 0;
-      for (int c = 0; c < 3; ++c) {
-        g.A[c] = s.G3b[c].p;
-        g.x[c] = s.W2.p + c * X.r2m * n3l;
-        g.xparts[c] = h->shards.size() == 1 ? h->w2_parts[c] : 0;
-        g.xpart[c] = X.zws(c);
-        g.xpart_stride[c] = h->w2_part_stride[c];
-        g.y[c] = s.z3.p + c * X.r3stride;
-        g.R[c] = X.R(c, 1) * n3l;
-        g.C[c] = X.R(c, 2);
-        bytes += 16 * (g.R[c] * g.C[c] + g.R[c] + g.C[c]);
-      }
-      bool ok;
-      {
-        Scope sc(h, "adj_g3_seg", bytes, bytes / 2, S.main);
-        ok = n3l > 0 && launch_seg_gemv(g, true, S.main);
-      }
-      if (!ok) {
-        // unsupported shape: the per-chi column GEMVs
-        for (int c = 0; c < 3; ++c) {
-          cplx* z3 = s.z3.p + c * X.r3stride;
-          if (n3l == 0) {
-            VSIE_CHECK_CUDA(cudaMemsetAsync(z3, 0, X.r3stride * sizeof(cplx), S.main));
-            continue;
+          const int64_t n3l = s.n3loc();
+          ReduceArgs r{};
+          r.nbatch = 3;
+          r.n1 = h->grid.n[0];
+          r.ncol = (int64_t)h->grid.n[1] * n3l;
+          r.cols_per_rhs = r.ncol;
+          r.ld_rhs = X.L.ld;
+          r.conj_u = cj;
+          int64_t bytes = 0, fl = 0;
+          for (int c = 0; c < 3; ++c) {
+            r.G1[c] = h->G1[c].p;
+            r.u[c] = u + c * X.L.chi_stride + shard_voxel_offset(h, s, X.L);
+            r.W1[c] = s.W1.p + c * X.r1m * h->grid.n[1] * n3l;
+            r.r1[c] = (int)X.R(c, 0);
+            bytes += 16 * ((int64_t)r.n1 * X.R(c, 0) + X.R(c, 0) * r.ncol + (int64_t)r.n1 * r.ncol);
+            fl += 8 * (int64_t)r.n1 * X.R(c, 0) * r.ncol;
           }
-          GemvT t{};
-          t.nbatch = 1;
-          t.A[0] = s.G3[c].p;
-          t.x[0] = g.x[c];
-          t.y[0] = z3;
-          t.R[0] = g.R[c];
-          t.C[0] = g.C[c];
-          Scope sc(h, "adj_g3_gemv", 16 * (g.R[c] * g.C[c] + g.R[c] + g.C[c]), 8 * g.R[c] * g.C[c], S.main);
-          launch_gemv_t(t, X.partials(c), h->partials_per_chi, kMaxSplits, S.main);
+          Scope sc(h, "adj_g1_reduce_tma", bytes, fl, S.main);
+          g1_done = g1_done && n3l > 0 && launch_reduce_g1_tma(r, S.main);
         }
+        VSIE_REQUIRE(g1_done || h->shards.size() == 1, VSIE_ERR_STATE, "reduce_tma on a partial shard set");
+      }
+      const bool g2b = seg && g2t_on() && X.k == 1;
+      const bool g2chain = g2b && !g1_done && g2t_chain_on();
+      if (!(g1_done && g2b)) {
+        fork(h, S);
+        for (int c = 0; c < 3; ++c) {
+          h->scope_chi = c;
+          for (Shard& s : h->shards) {
+            adj_front(X, s, c, u, cj, S.chi[c], nullptr, !seg, !g1_done, !g2b);
+            if (g2chain) launch_g2t_shard(h, X, s, S.chi[c], c);   // this chi's G2^T in its chain
+          }
+        }
+        h->scope_chi = -1;
+        if (g2b) join(h, S);
+      }
+      if (g2b && !g2chain) {
+        for (Shard& s : h->shards) launch_g2t_shard(h, X, s, S.main);
       }
     }
-    if (exchange) combine_r3(h, &Shard::z3, 3 * X.r3stride, S.main);
-    fork(h, S);
-  } else if (exchange) {
-    join(h, S);
-    combine_r3(h, &Shard::z3, 3 * X.r3stride, S.main);
-    fork(h, S);
+    if (seg) {
+      if (!fused_front && !(seg && g2t_on())) join(h, S);
+      for (Shard& s : h->shards) {
+        const int64_t n3l = s.n3loc();
+        SegGemv g{};
+        g.nbatch = 3;
+        g.nsb = s.g3b_ns;
+        g.partials = X.partials(0);
+        g.rstride = X.r3m;
+        int64_t bytes = 0;
+        for (int c = 0; c < 3; ++c) {
+          g.A[c] = s.G3b[c].p;
+          g.x[c] = s.W2.p + c * X.r2m * n3l;
+          g.xparts[c] = h->shards.size() == 1 ? h->w2_parts[c] : 0;
+          g.xpart[c] = X.zws(c);
+          g.xpart_stride[c] = h->w2_part_stride[c];
+          g.y[c] = s.z3.p + c * X.r3stride;
+          g.R[c] = X.R(c, 1) * n3l;
+          g.C[c] = X.R(c, 2);
+          bytes += 16 * (g.R[c] * g.C[c] + g.R[c] + g.C[c]);
+        }
+        bool ok;
+        {
+          Scope sc(h, "adj_g3_seg", bytes, bytes / 2, S.main);
+          ok = n3l > 0 && launch_seg_gemv(g, true, S.main);
+        }
+        if (!ok) {
+          // unsupported shape: the per-chi column GEMVs
+          for (int c = 0; c < 3; ++c) {
+            cplx* z3 = s.z3.p + c * X.r3stride;
+            if (n3l == 0) {
+              VSIE_CHECK_CUDA(cudaMemsetAsync(z3, 0, X.r3stride * sizeof(cplx), S.main));
+              continue;
+            }
+            GemvT t{};
+            t.nbatch = 1;
+            t.A[0] = s.G3[c].p;
+            t.x[0] = g.x[c];
+            t.y[0] = z3;
+            t.R[0] = g.R[c];
+            t.C[0] = g.C[c];
+            Scope sc(h, "adj_g3_gemv", 16 * (g.R[c] * g.C[c] + g.R[c] + g.C[c]), 8 * g.R[c] * g.C[c], S.main);
+            launch_gemv_t(t, X.partials(c), h->partials_per_chi, kMaxSplits, S.main);
+          }
+        }
+      }
+      if (exchange) combine_r3(h, &Shard::z3, 3 * X.r3stride, S.main);
+      fork(h, S);
+    } else if (exchange) {
+      join(h, S);
+      combine_r3(h, &Shard::z3, 3 * X.r3stride, S.main);
+      fork(h, S);
+    }
   }
   bool z_done = false;
   if (pair_g4_mode() == 2) {
@@ -1780,7 +1839,7 @@ void pair_dag(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z
     VSIE_REQUIRE(ok || h->shards.size() == 1, VSIE_ERR_STATE, "pair_g4 unsupported on a multi-shard handle");
     z_done = ok;
     if (z_done && exchange) combine_r3(h, &Shard::y4, 3 * X.r3stride, S.main);
-    if (z_done && seg) {
+    if (z_done && seg && !(fwd_chain_seg_on(h) && !fwd_tail_batched_on() && !g2n_on())) {
       for (Shard& s : h->shards) {
         const int64_t n3l = s.n3loc();
         if (n3l == 0) continue;
@@ -1869,7 +1928,28 @@ void pair_dag(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z
   } else {
     for (int c = 0; c < 3; ++c) {
       h->scope_chi = c;
-      for (Shard& s : h->shards) fwd_rest(X, s, c, y, S.chi[c], nullptr, !(z_done && seg));
+      for (Shard& s : h->shards) {
+        if (z_done && seg && fwd_chain_seg_on(h) && !fwd_tail_batched_on() && !g2n_on()) {
+          // this chi's G3 pass in its chain (small ring: the chain's G2 / G1 kernels of the
+          // previous chi fit beside it on the SMs)
+          const int64_t n3l = s.n3loc();
+          if (n3l == 0) continue;
+          SegGemv g{};
+          g.nbatch = 1;
+          g.nsb = s.g3b_ns;
+          g.A[0] = s.G3b[c].p;
+          g.x[0] = s.y4.p + c * X.r3stride;
+          g.y[0] = s.Y3.p + c * X.r2m * n3l;
+          g.R[0] = X.R(c, 1) * n3l;
+          g.C[0] = X.R(c, 2);
+          const int64_t bytes = 16 * (g.R[0] * g.C[0] + g.R[0] + g.C[0]);
+          {
+            Scope sc(h, "fwd_g3_seg_chi", bytes, bytes / 2, S.chi[c]);
+            VSIE_REQUIRE(launch_seg_gemv_mode(g, 1, S.chi[c], true), VSIE_ERR_STATE, "pair: G3 shape");
+          }
+        }
+        fwd_rest(X, s, c, y, S.chi[c], nullptr, !(z_done && seg));
+      }
     }
   }
   h->scope_chi = -1;

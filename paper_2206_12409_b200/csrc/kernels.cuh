@@ -121,7 +121,7 @@ struct SegGemv {
   cplx* yt[3];
   int64_t cmax;       // set by the launcher
 };
-bool launch_seg_gemv_mode(const SegGemv& a, int mode, cudaStream_t st);
+bool launch_seg_gemv_mode(const SegGemv& a, int mode, cudaStream_t st, bool small_ring = false);
 bool launch_seg_gemv(const SegGemv& a, bool transpose, cudaStream_t st);
 bool seg_gemv_supported(int64_t R, int64_t C, int nsb);
 // Fused transpose front (adjfront.cu), single RHS, batched over chi: W1 = G1^T u and

@@ -25,14 +25,17 @@ using namespace tma;
 constexpr int kCW = 8;                      // consumer warps
 constexpr int kSegThreads = 32 * (kCW + 1);
 constexpr int kStage = 10240;
-constexpr int kSlotsS = 16;
-constexpr int kRing = kSlotsS * kStage;
+constexpr int kRingMax = 16 * kStage;
 
 __device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kCW) : "memory"); }
 
-// M: 1 op N (x -> y), 2 op T (xt -> yt through partials), 3 both from ONE pass over the core
-template <int NQ, int M>
+// M: 1 op N (x -> y), 2 op T (xt -> yt through partials), 3 both from ONE pass over the core.
+// SL ring slots (16: 160 KB, one CTA per SM; 8: 80 KB, leaves room beside it for the CTAs of
+// a concurrent compute kernel)
+template <int NQ, int M, int SL>
 __global__ void __launch_bounds__(kSegThreads, 1) k_seg_gemv(const __grid_constant__ SegGemv a) {
+  constexpr int kSlotsS = SL;
+  constexpr int kRing = SL * kStage;
   constexpr bool FW = (M & 1) != 0, OPT = (M & 2) != 0;
   extern __shared__ __align__(128) unsigned char smem[];
   cplx* ring = reinterpret_cast<cplx*>(smem);
@@ -218,17 +221,17 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_seg_gemv(const __grid_consta
   pdl_trigger();
 }
 
-template <int M>
+template <int M, int SL>
 bool launch_seg(const SegGemv& a, int ns, int nq, size_t smem, cudaStream_t st) {
   switch (nq) {
 #define VSIE_SEG(K)                                                                                  \
   case K: {                                                                                          \
     static size_t attr = 0;                                                                          \
     if (smem > attr) {                                                                               \
-      VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_seg_gemv<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+      VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_seg_gemv<K, M, SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
       attr = smem;                                                                                   \
     }                                                                                                \
-    launch_pdl(k_seg_gemv<K, M>, dim3(ns), dim3(kSegThreads), smem, st, a);                          \
+    launch_pdl(k_seg_gemv<K, M, SL>, dim3(ns), dim3(kSegThreads), smem, st, a);                      \
     return true;                                                                                     \
   }
     VSIE_SEG(1) VSIE_SEG(2) VSIE_SEG(3) VSIE_SEG(4) VSIE_SEG(5) VSIE_SEG(6) VSIE_SEG(7) VSIE_SEG(8)
@@ -246,12 +249,12 @@ bool seg_gemv_supported(int64_t R, int64_t C, int nsb) {
   if (L > 512 || 16 * L > kStage) return false;
   int nq = (int)ceil_div(L, 32);
   if (nq > 8) nq = nq <= 10 ? 10 : nq <= 12 ? 12 : 16;
-  return kRing + (size_t)4 * 32 * nq * sizeof(cplx) + (size_t)2 * C * sizeof(cplx) <= 220 * 1024;
+  return kRingMax + (size_t)4 * 32 * nq * sizeof(cplx) + (size_t)2 * C * sizeof(cplx) <= 220 * 1024;
 }
 
 // mode 1: op N (x -> y); 2: op T (x -> y through partials); 3: both from one pass
 // (op N x -> y, op T xt -> yt)
-bool launch_seg_gemv_mode(const SegGemv& a0, int mode, cudaStream_t st) {
+bool launch_seg_gemv_mode(const SegGemv& a0, int mode, cudaStream_t st, bool small_ring) {
   SegGemv a = a0;
   if (mode == 2)
     for (int b = 0; b < a.nbatch; ++b) {
@@ -271,12 +274,16 @@ bool launch_seg_gemv_mode(const SegGemv& a0, int mode, cudaStream_t st) {
   int nq = (int)ceil_div(L, 32);
   if (nq > 8) nq = nq <= 10 ? 10 : nq <= 12 ? 12 : 16;
   a.cmax = cmax;
-  const size_t smem = kRing + (size_t)4 * 32 * nq * sizeof(cplx) + (size_t)2 * cmax * sizeof(cplx);
+  const size_t smem = (small_ring ? kRingMax / 2 : kRingMax) + (size_t)4 * 32 * nq * sizeof(cplx) +
+                      (size_t)2 * cmax * sizeof(cplx);
   if (smem > 220 * 1024) return false;
   if (mode & 2) VSIE_REQUIRE(a.rstride >= cmax && a.partials != nullptr, VSIE_ERR_ARG, "seg_gemv: partial buffer");
-  const bool ok = mode == 1 ? launch_seg<1>(a, ns, nq, smem, st)
-                : mode == 2 ? launch_seg<2>(a, ns, nq, smem, st)
-                            : launch_seg<3>(a, ns, nq, smem, st);
+  const bool ok = small_ring ? (mode == 1 ? launch_seg<1, 8>(a, ns, nq, smem, st)
+                                : mode == 2 ? launch_seg<2, 8>(a, ns, nq, smem, st)
+                                            : launch_seg<3, 8>(a, ns, nq, smem, st))
+                             : (mode == 1 ? launch_seg<1, 16>(a, ns, nq, smem, st)
+                                : mode == 2 ? launch_seg<2, 16>(a, ns, nq, smem, st)
+                                            : launch_seg<3, 16>(a, ns, nq, smem, st));
   if (!ok) return false;
   VSIE_CHECK_LAUNCH();
   if (mode & 2) {
@@ -292,7 +299,7 @@ bool launch_seg_gemv_mode(const SegGemv& a0, int mode, cudaStream_t st) {
 }
 
 bool launch_seg_gemv(const SegGemv& a, bool transpose, cudaStream_t st) {
-  return launch_seg_gemv_mode(a, transpose ? 2 : 1, st);
+  return launch_seg_gemv_mode(a, transpose ? 2 : 1, st, false);
 }
 
 }  // namespace vsie
