@@ -963,7 +963,9 @@ void apply_single_tma(vsie_coupling_s* h, Ctx X, const cplx* x, cplx* y, int op,
       VSIE_REQUIRE(launch_pair_g4(p, sm_count_dev(), S.main), VSIE_ERR_STATE, "single apply: G4 shape");
     }
     if (exchange) combine_r3(h, &Shard::y4, 3 * X.r3stride, S.main);
+    const bool chain_seg = fwd_chain_seg_on(h) && !g2n_on();   // as in the pair (pair_dag)
     for (Shard& s : h->shards) {
+      if (chain_seg) break;
       const int64_t n3l = s.n3loc();
       SegGemv g{};
       g.nbatch = 3;
@@ -986,6 +988,20 @@ void apply_single_tma(vsie_coupling_s* h, Ctx X, const cplx* x, cplx* y, int op,
     for (int c = 0; c < 3; ++c) {
       h->scope_chi = c;
       for (Shard& s : h->shards) {
+        if (chain_seg) {
+          const int64_t n3l = s.n3loc();
+          SegGemv g{};
+          g.nbatch = 1;
+          g.nsb = s.g3b_ns;
+          g.A[0] = s.G3b[c].p;
+          g.x[0] = s.y4.p + c * X.r3stride;
+          g.y[0] = s.Y3.p + c * X.r2m * n3l;
+          g.R[0] = X.R(c, 1) * n3l;
+          g.C[0] = X.R(c, 2);
+          const int64_t bytes = 16 * (g.R[0] * g.C[0] + g.R[0] + g.C[0]);
+          Scope sc(h, "fwd_g3_seg_chi", bytes, bytes / 2, S.chi[c]);
+          VSIE_REQUIRE(launch_seg_gemv_mode(g, 1, S.chi[c], true), VSIE_ERR_STATE, "single apply: G3 shape");
+        }
         if (g2n_on())
           fwd_expand(X, s, c, y, S.chi[c]);
         else
