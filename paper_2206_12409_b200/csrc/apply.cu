@@ -115,6 +115,16 @@ int pair_g4_mode() {
   return v;
 }
 
+// the GMRES pair's G4 pass per chi inside the chains (small ring), followed there by that
+// chi's G3 / G2 / G1 steps; VSIE_G4_CHAIN=1
+bool g4_chain_on() {
+  static const int v = [] {
+    const char* e = std::getenv("VSIE_G4_CHAIN");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v != 0;
+}
+
 // the transpose's G1^T, G2^T and G3^T per chi inside the chains (small-ring k_seg_gemv);
 // VSIE_ADJ_CHAIN_SEG=1
 bool adj_chain_seg_on() {
@@ -1823,6 +1833,49 @@ void pair_dag(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z
       combine_r3(h, &Shard::z3, 3 * X.r3stride, S.main);
       fork(h, S);
     }
+  }
+  if (pair_g4_mode() == 2 && seg && g4_chain_on() && !exchange && X.r3m <= pair_g4_max_rank()) {
+    // per chi in its chain: the G4 pass (both products, small ring), the G3 pass, G2 and G1
+    // -- chi c's G2 / G1 kernels run beside chi c + 1's G4 / G3 streams; Eq. 18 sum at the end
+    Shard& s = h->shards[0];
+    const int64_t n3l = s.n3loc(), ldz = s.zpart.n / 3;
+    for (int c = 0; c < 3; ++c) {
+      h->scope_chi = c;
+      PairG4 p{};
+      p.nbatch = 1;
+      p.C = s.mloc();
+      p.x = x + s.cb;
+      p.z = s.zpart.p + c * ldz;
+      p.partials = X.partials(c);
+      p.rstride = X.r3m;
+      p.small_ring = true;
+      p.A[0] = s.G4[c].p;
+      p.z3[0] = s.z3.p + c * X.r3stride;
+      p.y4[0] = s.y4.p + c * X.r3stride;
+      p.R[0] = X.R(c, 2);
+      {
+        Scope sc(h, "pair_g4_chi", 16 * X.R(c, 2) * (p.C + 2) + 16 * 2 * p.C, 16 * X.R(c, 2) * p.C, S.chi[c]);
+        VSIE_REQUIRE(launch_pair_g4(p, sm_count_dev(), S.chi[c]), VSIE_ERR_STATE, "pair: G4 shape");
+      }
+      SegGemv g{};
+      g.nbatch = 1;
+      g.nsb = s.g3b_ns;
+      g.A[0] = s.G3b[c].p;
+      g.x[0] = s.y4.p + c * X.r3stride;
+      g.y[0] = s.Y3.p + c * X.r2m * n3l;
+      g.R[0] = X.R(c, 1) * n3l;
+      g.C[0] = X.R(c, 2);
+      {
+        const int64_t bytes = 16 * (g.R[0] * g.C[0] + g.R[0] + g.C[0]);
+        Scope sc(h, "fwd_g3_seg_chi", bytes, bytes / 2, S.chi[c]);
+        VSIE_REQUIRE(launch_seg_gemv_mode(g, 1, S.chi[c], true), VSIE_ERR_STATE, "pair: G3 shape");
+      }
+      fwd_rest(X, s, c, y, S.chi[c], nullptr, false);
+    }
+    h->scope_chi = -1;
+    join(h, S);
+    adj_sum_chi(X, s, z + s.cb, m, cj, S.main);
+    return;
   }
   bool z_done = false;
   if (pair_g4_mode() == 2) {

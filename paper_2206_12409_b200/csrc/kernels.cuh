@@ -94,6 +94,7 @@ struct PairG4 {
   int64_t ccta;   // set by the launcher: max columns per CTA
   int nbatch;
   bool conj_z;
+  bool small_ring;   // 80 KB ring (per-chi launches beside compute kernels) instead of 160 KB
 };
 // false when the shape is unsupported (R > 320): the caller falls back
 bool launch_pair_g4(const PairG4& a, int max_ctas, cudaStream_t st);

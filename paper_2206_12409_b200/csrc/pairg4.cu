@@ -28,8 +28,7 @@ using namespace tma;
 constexpr int kConsumerWarps = 8;
 constexpr int kPairThreads = 32 * (kConsumerWarps + 1);   // + one producer warp
 constexpr int kStageBytes = 10240;                       // >= 2 columns of r3 <= 320
-constexpr int kSlots = 16;                               // two per consumer warp
-constexpr int kRingBytes = kSlots * kStageBytes;         // 160 KB
+constexpr int kRingMaxBytes = 16 * kStageBytes;          // 160 KB: two slots per consumer warp
 
 // barrier over the 256 consumer threads only (the producer warp keeps streaming)
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps) : "memory"); }
@@ -45,9 +44,11 @@ struct StageMap {
 // MODE: 3 both products (the GMRES pair), 1 forward only (y4 = G4 x), 2 transpose only
 // (z = sum_chi G4^T z3) -- the single-direction variants let a pass run beside the other
 // direction's compute-bound steps (VSIE_PAIR_G4=5)
-template <int NQ, int MODE>
+template <int NQ, int MODE, int SL>
 __global__ void __launch_bounds__(kPairThreads, 1) k_pair_g4(const __grid_constant__ PairG4 a) {
   constexpr bool FW = (MODE & 1) != 0, TR = (MODE & 2) != 0;
+  constexpr int kSlots = SL;                       // 16 (160 KB) or 8 (80 KB, per-chi chains)
+  constexpr int kRingBytes = SL * kStageBytes;
   extern __shared__ __align__(128) unsigned char smem[];
   cplx* ring = reinterpret_cast<cplx*>(smem);
   cplx* red = reinterpret_cast<cplx*>(smem + kRingBytes);                 // [4][32 NQ]
@@ -229,7 +230,9 @@ bool launch_pair_g4(const PairG4& a, int max_ctas, cudaStream_t st) {
   const int nq = (int)ceil_div(rmax, 32);
   const int ns = (int)std::max<int64_t>(1, std::min<int64_t>(max_ctas, ceil_div(a.C, 4)));
   const int64_t ccta = ceil_div(a.C, ns);
-  const size_t smem = kRingBytes + (size_t)4 * 32 * nq * sizeof(cplx) + (size_t)2 * ccta * sizeof(cplx) +
+  const bool small = a.small_ring;
+  const size_t smem = (small ? kRingMaxBytes / 2 : kRingMaxBytes) + (size_t)4 * 32 * nq * sizeof(cplx) +
+                      (size_t)2 * ccta * sizeof(cplx) +
                       (size_t)3 * 32 * nq * sizeof(cplx);
   PairG4 b = a;
   b.ccta = ccta;
@@ -239,12 +242,20 @@ bool launch_pair_g4(const PairG4& a, int max_ctas, cudaStream_t st) {
   switch (nq * 4 + mode) {
 #define VSIE_PG4M(K, M)                                                                            \
   case K * 4 + M: {                                                                                \
-    static size_t attr = 0;                                                                        \
-    if (smem > attr) {                                                                             \
-      VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_pair_g4<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-      attr = smem;                                                                                 \
+    static size_t attr = 0, attr8 = 0;                                                             \
+    if (small) {                                                                                   \
+      if (smem > attr8) {                                                                          \
+        VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_pair_g4<K, M, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        attr8 = smem;                                                                              \
+      }                                                                                            \
+      launch_pdl(k_pair_g4<K, M, 8>, dim3(ns), dim3(kPairThreads), smem, st, b);                   \
+    } else {                                                                                       \
+      if (smem > attr) {                                                                           \
+        VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_pair_g4<K, M, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        attr = smem;                                                                               \
+      }                                                                                            \
+      launch_pdl(k_pair_g4<K, M, 16>, dim3(ns), dim3(kPairThreads), smem, st, b);                  \
     }                                                                                              \
-    launch_pdl(k_pair_g4<K, M>, dim3(ns), dim3(kPairThreads), smem, st, b);                        \
     break;                                                                                         \
   }
 #define VSIE_PG4(K) VSIE_PG4M(K, 1) VSIE_PG4M(K, 2) VSIE_PG4M(K, 3)

@@ -294,6 +294,7 @@ _SCHEDULES = [
     dict(VSIE_PAIR_G4="0", VSIE_REDUCE_REM="0", VSIE_EXPAND_REM="0"),
     dict(VSIE_PAIR_G4="2", VSIE_EXPAND_REM="2"),
     dict(VSIE_PAIR_G4="2", VSIE_FWD_CHAIN_SEG="0"),
+    dict(VSIE_PAIR_G4="2", VSIE_G4_CHAIN="1"),
     dict(VSIE_PAIR_G4="2", VSIE_FWD_CHAIN_SEG="1", VSIE_ADJ_CHAIN_SEG="1", VSIE_G2T_CHAIN="1"),
 ]
 
@@ -309,8 +310,8 @@ def test_pair_schedules(env):
     the batched TMA-streamed G1^T instead of the per-chi k_reduce_g1; VSIE_FWD_TAIL_BATCHED=1
     the forward's G2 / G1 steps as batched launches; VSIE_G2T=0 the split-K ZGEMM for G2^T
     instead of k_g2t; VSIE_G2N=1 the batched k_g2n for the forward G2 step instead of
-    the per-chi ZGEMMs; VSIE_FWD_CHAIN_SEG / VSIE_ADJ_CHAIN_SEG the G3 passes per chi in
-    the chains (small ring); VSIE_SINGLE_TMA=0 the per-chi GEMV chains in the single applies)
+    the per-chi ZGEMMs; VSIE_FWD_CHAIN_SEG / VSIE_ADJ_CHAIN_SEG / VSIE_G4_CHAIN the G3 / G4 passes per
+    chi in the chains (small rings); VSIE_SINGLE_TMA=0 the per-chi GEMV chains in the single applies)
     equals the oracle matvecs and the separate applies,
     at cfg 1 (ragged ranks) and cfg 2 (several tiles, 148-CTA row blocks); op T and op C.
     Subprocess: the switches are read once per process."""
