@@ -9,6 +9,13 @@ P:90 PWC testing, P:78 RWG basis; quadrature per §8c-L7):
   col n   = RWG id in canonical order           (§8c-L10)
 
 No approximation beyond the fixed quadrature; 48 pair interactions per entry.
+
+PWL testing (P:90: q = 12 unknowns per voxel; P:381 "linear terms"; SURVEY §8f NEXT-2;
+DESIGN.md reading R-PWL): the 12 test functions of a voxel are chi x {1, (x-c_x)/h_x,
+(y-c_y)/h_y, (z-c_z)/h_z}.  `moment` l = 0 is the PWC block above; l = 1, 2, 3 multiply
+every node weight w_p by the linear function at the node, (r_p - c)_l / h_l.  With one
+node per voxel (ng = 1, the paper's far-block rule) the linear blocks vanish
+identically, which is the "neglected" contribution of P:381.
 """
 from __future__ import annotations
 
@@ -33,6 +40,7 @@ class Problem:
     offs: np.ndarray    # [8, 3] voxel node offsets
     wts: np.ndarray     # [8] voxel node weights
     scale: complex = 1.0 + 0.0j
+    moment: int = 0     # PWL test moment (0 = PWC; 1, 2, 3 = linear in x, y, z)
 
     @property
     def n_v(self):
@@ -47,12 +55,18 @@ class Problem:
         return (3 * self.n_v, self.m)
 
 
-def make_problem(n, h, origin, meshes, freq, scale=1.0 + 0.0j, ng=2, bary=None):
-    """k0 = 2 pi f / c0 (§8c-L19); sources from geometry.mesh_sources."""
+def make_problem(n, h, origin, meshes, freq, scale=1.0 + 0.0j, ng=2, bary=None, moment=0):
+    """k0 = 2 pi f / c0 (§8c-L19); sources from geometry.mesh_sources.
+
+    moment l in 1..3: node weights w_p (r_p - c)_l / h_l (PWL test function, module header)."""
+    if moment not in (0, 1, 2, 3):
+        raise ValueError("moment must be 0 (PWC) or 1..3 (linear in x, y, z)")
     rs, js = geometry.mesh_sources(meshes, geometry.TRI_BARY if bary is None else bary)
     offs, wts = geometry.gauss_legendre_offsets(h, ng)
+    if moment:
+        wts = wts * (offs[:, moment - 1] / h[moment - 1])
     return Problem(tuple(n), tuple(h), tuple(origin), 2.0 * math.pi * freq / C0, rs, js, offs, wts,
-                   complex(scale))
+                   complex(scale), moment)
 
 
 def problem_from_config(cfg, **kw):

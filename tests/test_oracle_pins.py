@@ -614,3 +614,57 @@ def test_P39_round_special_cases_and_idempotence():
     assert ttmv.ranks_of(once) == ttmv.ranks_of(twice)
     T1 = ttmv.full(once)
     assert np.linalg.norm(ttmv.full(twice) - T1) <= 1e-12 * np.linalg.norm(T1)
+
+
+# ---------------------------------------------------------------- PWL test moments (NEXT-2)
+
+def _one_rwg_problem(D, moment, ng=2, h=(3e-3, 4e-3, 5e-3), origin=(0.0, 0.0, 0.0)):
+    xyz = np.array([[0, -0.01, 0], [0, 0.01, 0], [0.015, 0, 0.002], [-0.012, 0.001, 0]], dtype=float)
+    tri = np.array([[0, 1, 2], [1, 0, 3]], dtype=np.int32)
+    shifted = xyz + D * np.array([0.8, 0.5, -0.33])
+    return entries.make_problem((1, 1, 1), h, origin, [(shifted, tri)], 298e6, ng=ng, moment=moment)
+
+
+def test_P40_pwl_one_point_rule_neglects_linear_terms(cfg1):
+    """P:381 / P:287: with one volume node per voxel the linear PWL blocks vanish
+    identically (the node sits at the centre, where (r - c)_l = 0), while the PWC block
+    equals the midpoint rule V f(c)."""
+    meshes = cfg1.meshes()
+    rows = np.arange(0, 3 * cfg1.n_v, 997)
+    cols = (rows * 7) % (sum(len(t) for _, t in meshes) // 2)
+    for l in (1, 2, 3):
+        p = entries.make_problem(cfg1.n, cfg1.h, cfg1.origin, meshes, cfg1.freq, ng=1, moment=l)
+        assert np.all(entries.entries(p, rows, cols) == 0)
+    p0 = entries.make_problem(cfg1.n, cfg1.h, cfg1.origin, meshes, cfg1.freq, ng=1)
+    assert np.all(np.abs(entries.entries(p0, rows, cols)) > 0)
+    with pytest.raises(ValueError):
+        entries.make_problem(cfg1.n, cfg1.h, cfg1.origin, meshes, cfg1.freq, moment=4)
+
+
+def test_P41_pwl_moment_is_h_over_12_times_centre_gradient():
+    """Taylor expansion of the integrand f about the voxel centre c: the odd parts of
+    (r - c)_l / h_l f(r) integrate to zero and int_V ((r - c)_l)^2 / h_l = V h_l / 12, so
+    Z_l(c) = (h_l / 12) d/dc_l Z_0(c) + O((h / D)^2) relative, with D the source distance.
+    The derivative is a central difference of the PWC entry in the voxel origin (an
+    independent route through the PWC arithmetic).  Anisotropic h catches an axis mix-up,
+    the sign of the difference a sign error, the h_l / 12 factor a scale error; the error
+    must fall ~ D^-2."""
+    h = (3e-3, 4e-3, 5e-3)
+    errs = []
+    for D in (0.05, 0.1, 0.2):
+        for l in (1, 2, 3):
+            Zl = entries.field_vectors(_one_rwg_problem(D, l, h=h), [0], [0])[0]
+            dlt = 1e-3 * h[l - 1]
+            e = np.zeros(3)
+            e[l - 1] = dlt
+            Zp = entries.field_vectors(_one_rwg_problem(D, 0, h=h, origin=tuple(e)), [0], [0])[0]
+            Zm = entries.field_vectors(_one_rwg_problem(D, 0, h=h, origin=tuple(-e)), [0], [0])[0]
+            pred = h[l - 1] / 12.0 * (Zp - Zm) / (2 * dlt)
+            errs.append((D, l, np.max(np.abs(Zl - pred)) / np.max(np.abs(pred))))
+    by_d = {}
+    for D, l, e in errs:
+        by_d[D] = max(by_d.get(D, 0.0), e)
+    ds = sorted(by_d)
+    assert by_d[ds[-1]] < 0.5 * (max(h) / ds[-1]) ** 2, errs   # O((h / D)^2)
+    for a, b in zip(ds, ds[1:]):
+        assert 2.5 < by_d[a] / by_d[b] < 6.0, by_d    # ~4 per doubling of D
