@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define VSIE_ABI_VERSION 1
+#define VSIE_ABI_VERSION 2
 
 /* status codes */
 #define VSIE_OK 0
@@ -101,6 +101,11 @@ typedef struct {
   const void* nccl_unique_id; /* 128 bytes from vsie_nccl_unique_id() on rank 0, world > 1 */
   int32_t device;        /* CUDA device ordinal, -1 = current device                      */
   int32_t verbose;       /* 1: progress lines on stderr                                   */
+  int32_t test_moment;   /* PWL test moment of the handle's 3 chi blocks (P:90 q = 12; P:381
+                          * "linear terms"): 0 = PWC testing (default); l = 1, 2, 3 weights
+                          * every voxel node p by (r_p - c)_l / h_l, the linear PWL test
+                          * function along axis l.  The q = 12 coupling is the four handles
+                          * l = 0..3 (vsie_coupling_apply_pwl).  Out of range: VSIE_ERR_ARG. */
 } vsie_build_opts;
 
 typedef struct {
@@ -120,6 +125,7 @@ typedef struct {
   double k0;
   int64_t apply_launches;       /* kernel launches made by vsie_coupling_apply* so far (this handle) */
   int64_t apply_calls;
+  int32_t test_moment;          /* vsie_build_opts.test_moment of the build / import         */
 } vsie_info;
 
 /* Per-kernel device timing of apply calls (opt-in, see vsie_coupling_set_timing). */
@@ -221,6 +227,21 @@ int32_t vsie_coupling_apply_host(vsie_coupling_t h, const void* x_host, void* y_
  * (the G4 pass is not shared in this schedule).  Otherwise the fused device pair. */
 int32_t vsie_coupling_apply_pair_host(vsie_coupling_t h, const void* x_host, void* y_host, const void* u_host,
                                       void* z_host, int32_t adj_op);
+
+/* PWL (q = 12) coupling: the four handles h[l] built with
+ * test_moment = l (l = 0..3) on the same grid, meshes, frequency and partition.
+ * The 12 n_v-row operator stacks their blocks moment-major:
+ *   OP_N:       y = [Z_0 x; Z_1 x; Z_2 x; Z_3 x]; y holds 4 consecutive blocks, block l
+ *               = Z_l X as in vsie_coupling_apply (3 n_v,loc x nrhs, ld 3 n_v,loc).  For
+ *               nrhs = 1 this is the vector ordered (moment, chi, voxel).
+ *   OP_T/OP_C:  z = sum_l Z_l^op u_l, u in the same 4-block layout, z m x nrhs; the four
+ *               partial products are summed in the order l = 0, 1, 2, 3 on device.
+ * Device pointers, stream-ordered on `stream`; x, y, u, z as in vsie_coupling_apply.  A
+ * device scratch of 3 m nrhs complex128 is held by h[0].  Errors: VSIE_ERR_ARG for a NULL
+ * handle, handles with moments other than 0, 1, 2, 3 in that order, or mismatched
+ * geometry / partition; otherwise as vsie_coupling_apply. */
+int32_t vsie_coupling_apply_pwl(const vsie_coupling_t h[4], const void* x, void* y, int32_t op, int32_t nrhs,
+                                void* stream);
 
 /* Exact quadrature entries (the cross's black box, not the TT value):
  * idx = device int64 [count][2] (row, col), out = device complex128 [count].

@@ -31,7 +31,8 @@ class vsie_build_opts(C.Structure):
                 ("direct_svd_max", C.c_int32), ("heldout", C.c_int32), ("nrhs_max", C.c_int32),
                 ("seed", C.c_uint64), ("scale_re", C.c_double), ("scale_im", C.c_double),
                 ("rank", C.c_int32), ("world", C.c_int32), ("loopback", C.c_int32),
-                ("nccl_unique_id", C.c_void_p), ("device", C.c_int32), ("verbose", C.c_int32)]
+                ("nccl_unique_id", C.c_void_p), ("device", C.c_int32), ("verbose", C.c_int32),
+                ("test_moment", C.c_int32)]
 
 
 class vsie_info(C.Structure):
@@ -41,7 +42,7 @@ class vsie_info(C.Structure):
                 ("build_s", C.c_double), ("build_entry_s", C.c_double), ("build_factor_s", C.c_double),
                 ("build_maxvol_s", C.c_double), ("slab", C.c_int32 * 2), ("cols", C.c_int64 * 2),
                 ("world", C.c_int32), ("rank", C.c_int32), ("loopback", C.c_int32), ("k0", C.c_double),
-                ("apply_launches", C.c_int64), ("apply_calls", C.c_int64)]
+                ("apply_launches", C.c_int64), ("apply_calls", C.c_int64), ("test_moment", C.c_int32)]
 
 
 class vsie_timer(C.Structure):
@@ -89,6 +90,8 @@ _SIGS = {
     "vsie_coupling_apply_pair": (C.c_int32, [HANDLE, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                              C.c_void_p]),
     "vsie_coupling_apply_pair_host": (C.c_int32, [HANDLE, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
+    "vsie_coupling_apply_pwl": (C.c_int32, [C.POINTER(HANDLE), C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
+                                            C.c_void_p]),
     "vsie_coupling_configure": (C.c_int32, [HANDLE, C.c_int32, C.c_int32]),
     "vsie_coupling_trace": (C.c_int32, [HANDLE, C.POINTER(vsie_trace), C.c_int32, C.POINTER(C.c_int32)]),
     "vsie_coupling_destroy": (None, [HANDLE]),

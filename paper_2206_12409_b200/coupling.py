@@ -158,7 +158,7 @@ class Coupling:
             build_s=i.build_s, build_entry_s=i.build_entry_s, build_factor_s=i.build_factor_s,
             build_maxvol_s=i.build_maxvol_s, slab=tuple(i.slab), cols=tuple(i.cols), world=i.world,
             rank=i.rank, loopback=i.loopback, k0=i.k0, apply_launches=i.apply_launches,
-            apply_calls=i.apply_calls)
+            apply_calls=i.apply_calls, test_moment=i.test_moment)
 
     @property
     def m(self):
@@ -325,3 +325,54 @@ class Coupling:
         return [dict(name=arr[i].name.decode(), launches=arr[i].launches, total_ms=arr[i].total_ms,
                      bytes_per_launch=arr[i].bytes_per_launch, flops_per_launch=arr[i].flops_per_launch)
                 for i in range(min(n.value, 64))]
+
+
+class PWLCoupling:
+    """The PWL (q = 12) coupling: four Coupling handles built with test_moment
+    l = 0..3 (PWC block and the three linear test moments), applied through
+    vsie_coupling_apply_pwl.  Vectors on the voxel side stack the four 3 n_v blocks
+    moment-major (include/vsie_coupling.h)."""
+
+    def __init__(self, handles):
+        assert len(handles) == 4
+        self.handles = list(handles)
+
+    @classmethod
+    def build(cls, grid: Grid, meshes, freq: float, tol: float, **opts):
+        return cls([Coupling.build(grid, meshes, freq, tol, test_moment=l, **opts) for l in range(4)])
+
+    @classmethod
+    def from_cores(cls, grid: Grid, meshes, freq: float, cores4, **opts):
+        """cores4[l][chi][k] as in Coupling.from_cores, one set per test moment."""
+        return cls([Coupling.from_cores(grid, meshes, freq, cores4[l], test_moment=l, **opts) for l in range(4)])
+
+    def close(self):
+        for h in self.handles:
+            h.close()
+
+    def out_len(self, op: str) -> int:
+        n = self.handles[0].out_len(op)
+        return 4 * n if op == "N" else n
+
+    def apply(self, x, op: str = "N", stream=None):
+        """vsie_coupling_apply_pwl on device tensors (layouts as Coupling.apply)."""
+        torch = _torch()
+        vec = x.dim() == 1
+        X = x.reshape(-1, 1) if vec else x
+        nrhs = X.shape[1]
+        n_out = self.out_len(op)
+        if op == "N":
+            Xc = X.t().contiguous()
+        else:
+            # moment-major blocks, each column-major (3 n_v, nrhs)
+            nv = X.shape[0] // 4
+            Xc = X.reshape(4, nv, nrhs).permute(0, 2, 1).contiguous()
+        Y = torch.empty((nrhs, n_out), dtype=torch.complex128, device=x.device)
+        hs = (_lib.HANDLE * 4)(*[h._h for h in self.handles])
+        check(lib().vsie_coupling_apply_pwl(hs, C.c_void_p(Xc.data_ptr()), C.c_void_p(Y.data_ptr()),
+                                            _lib.OPS[op], nrhs, _stream_ptr(stream)))
+        if op == "N":
+            nv = n_out // 4
+            Y = Y.reshape(4, nrhs, nv).permute(0, 2, 1).reshape(n_out, nrhs) if nrhs > 1 else Y.t()
+            return Y[:, 0] if vec else Y
+        return Y[0] if vec else Y.t()

@@ -75,6 +75,7 @@ void vsie_build_opts_default(vsie_build_opts* o) {
   o->nccl_unique_id = nullptr;
   o->device = -1;
   o->verbose = 0;
+  o->test_moment = 0;
 }
 
 const char* vsie_status_string(int32_t s) {
@@ -224,6 +225,16 @@ int32_t vsie_coupling_apply_host(vsie_coupling_t h, const void* x_host, void* y_
   });
 }
 
+int32_t vsie_coupling_apply_pwl(const vsie_coupling_t h[4], const void* x, void* y, int32_t op, int32_t nrhs,
+                                void* stream) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "handle array is NULL");
+    vsie_coupling_s* hs[4] = {h[0], h[1], h[2], h[3]};
+    apply_pwl(hs, static_cast<const cplx*>(x), static_cast<cplx*>(y), op, nrhs, static_cast<cudaStream_t>(stream));
+    return VSIE_OK;
+  });
+}
+
 int32_t vsie_coupling_apply_pair(vsie_coupling_t h, const void* x, void* y, const void* u, void* z, int32_t adj_op,
                                  void* stream) {
   return guarded([&] {
@@ -334,6 +345,7 @@ int32_t vsie_coupling_info(vsie_coupling_t h, vsie_info* out) {
     out->k0 = h->k0;
     out->apply_launches = h->apply_launches;
     out->apply_calls = h->apply_calls;
+    out->test_moment = h->test_moment;
     return VSIE_OK;
   });
 }

@@ -17,9 +17,8 @@ namespace vsie {
 
 namespace {
 
-constexpr double kInv4Pi = 0.079577471545947667884441881686257181;  // 1/(4 pi)
-
-// Accumulates sum_{p, s} [G(r_p - r_s) J_s]_chi / (4 pi) * (without w, scale)
+// Accumulates sum_{p, s} pw_p [G(r_p - r_s) J_s]_chi (without w, scale); pw_p = 1/(4 pi)
+// times the PWL test function at node p (1 for PWC testing, +-1/(2 sqrt 3) for a linear one)
 // for one voxel centre (cx, cy, cz) and one RWG source record s36.
 template <int CHI>
 __device__ __forceinline__ void entry_acc(const EntryGeom& g, double cx, double cy, double cz,
@@ -47,7 +46,7 @@ __device__ __forceinline__ void entry_acc(const EntryGeom& g, double cx, double 
       const double t = rj * rc * (ir * ir);                 // Rhat_chi (Rhat . J)
       const double A = fma(1.0 - u2, jc, (3.0 * u2 - 1.0) * t);  // Re(alpha J_chi + beta t)
       const double B = u * (3.0 * t - jc);                       // Im(...)
-      const double qq = ir * kInv4Pi;
+      const double qq = ir * g.pw[p];
       // g * (A + iB) = qq (cs - i sn)(A + i B)
       ar = fma(qq, fma(cs, A, sn * B), ar);
       ai = fma(qq, fma(cs, B, -sn * A), ai);

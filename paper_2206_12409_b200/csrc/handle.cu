@@ -102,6 +102,15 @@ void handle_init_geometry(vsie_coupling_s* h, const vsie_grid* grid, const vsie_
   g.dy = g.hy / s3;
   g.dz = g.hz / s3;
   g.w = g.hx * g.hy * g.hz / 8.0;
+  // node p = (sigma1, sigma2, sigma3) with bit l-1 of p set for +h_l / (2 sqrt 3): the linear
+  // PWL test function (r_p - c)_l / h_l is +-1 / (2 sqrt 3) there (DESIGN.md R-PWL)
+  h->test_moment = o->test_moment;
+  VSIE_REQUIRE(h->test_moment >= 0 && h->test_moment <= 3, VSIE_ERR_ARG, "test_moment must be 0..3");
+  const double inv4pi = 0.079577471545947667884441881686257181;   // 1/(4 pi)
+  for (int p = 0; p < 8; ++p) {
+    const int l = h->test_moment;
+    g.pw[p] = l == 0 ? inv4pi : (((p >> (l - 1)) & 1) ? inv4pi / s3 : -inv4pi / s3);
+  }
   g.k0 = h->k0;
   g.inv_k0 = 1.0 / h->k0;
   g.scale_re = h->scale_re;

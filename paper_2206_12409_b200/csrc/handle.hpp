@@ -80,6 +80,7 @@ struct vsie_coupling_s {
   std::vector<vsie::Shard> shards;         // 1 shard (own rank) or `world` (loopback)
   int rank = 0, world = 1, loopback = 0, device = 0;
   int nrhs_max = 64;
+  int test_moment = 0;                     // PWL test moment (vsie_build_opts.test_moment)
   std::unique_ptr<vsie::Comm> comm;
   vsie::DevBuf<vsie::cplx> partials;       // [3][partials_per_chi]
   int64_t partials_per_chi = 0;
@@ -101,6 +102,7 @@ struct vsie_coupling_s {
   int tile_trace = 0;
   vsie::DevBuf<vsie::cplx> gather_buf;     // allgather staging of z
   vsie::DevBuf<vsie::cplx> io_x, io_y;     // apply_host staging
+  vsie::DevBuf<vsie::cplx> pwl_scratch;    // vsie_coupling_apply_pwl: Z_l^T u_l, l = 1..3
   vsie::DevBuf<int64_t> io_idx;
   cudaStream_t io_stream = nullptr;
   cudaStream_t io_stream2 = nullptr;   // host pair: the transpose's copies + apply
@@ -139,6 +141,8 @@ void handle_alloc_workspace(vsie_coupling_s* h);
 void apply(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int nrhs, cudaStream_t st);
 // y = Z x and z = Z^T u (adj_op OP_T) or Z^H u (OP_C) in one call, single RHS
 void apply_pair(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z, int adj_op, cudaStream_t st);
+// vsie_coupling_apply_pwl (pwl.cu)
+void apply_pwl(vsie_coupling_s* const hs[4], const cplx* x, cplx* y, int op, int nrhs, cudaStream_t st);
 // drops the cached apply graphs (cores / workspaces changed)
 void apply_reset_graphs(vsie_coupling_s* h);
 void apply_destroy(vsie_coupling_s* h);

@@ -12,6 +12,7 @@ struct EntryGeom {
   double hx, hy, hz;
   double dx, dy, dz;      // Gauss offsets h / (2 sqrt 3)
   double w;               // h1 h2 h3 / 8
+  double pw[8];           // per-node factor 1/(4 pi) x PWL test function at node p (1 for PWC)
   double k0, inv_k0;
   double scale_re, scale_im;
   const double* src;     // [m][36] device
