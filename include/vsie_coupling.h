@@ -243,6 +243,13 @@ int32_t vsie_coupling_apply_pair_host(vsie_coupling_t h, const void* x_host, voi
 int32_t vsie_coupling_apply_pwl(const vsie_coupling_t h[4], const void* x, void* y, int32_t op, int32_t nrhs,
                                 void* stream);
 
+/* The q = 12 GMRES coupling pair (single RHS): y = Z_pwl x and z = Z_pwl^T u (adj_op
+ * OP_T) or Z_pwl^H u (OP_C), layouts as vsie_coupling_apply_pwl; each moment handle runs
+ * its fused pair (vsie_coupling_apply_pair), then the z sum in the order l = 0..3.
+ * Errors as vsie_coupling_apply_pwl and vsie_coupling_apply_pair. */
+int32_t vsie_coupling_apply_pair_pwl(const vsie_coupling_t h[4], const void* x, void* y, const void* u, void* z,
+                                     int32_t adj_op, void* stream);
+
 /* Exact quadrature entries (the cross's black box, not the TT value):
  * idx = device int64 [count][2] (row, col), out = device complex128 [count].
  * Rows and columns are global indices (any rank may evaluate any entry). */

@@ -92,6 +92,8 @@ _SIGS = {
     "vsie_coupling_apply_pair_host": (C.c_int32, [HANDLE, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
     "vsie_coupling_apply_pwl": (C.c_int32, [C.POINTER(HANDLE), C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                             C.c_void_p]),
+    "vsie_coupling_apply_pair_pwl": (C.c_int32, [C.POINTER(HANDLE), C.c_void_p, C.c_void_p, C.c_void_p,
+                                                 C.c_void_p, C.c_int32, C.c_void_p]),
     "vsie_coupling_configure": (C.c_int32, [HANDLE, C.c_int32, C.c_int32]),
     "vsie_coupling_trace": (C.c_int32, [HANDLE, C.POINTER(vsie_trace), C.c_int32, C.POINTER(C.c_int32)]),
     "vsie_coupling_destroy": (None, [HANDLE]),

@@ -376,3 +376,21 @@ class PWLCoupling:
             Y = Y.reshape(4, nrhs, nv).permute(0, 2, 1).reshape(n_out, nrhs) if nrhs > 1 else Y.t()
             return Y[:, 0] if vec else Y
         return Y[0] if vec else Y.t()
+
+    def apply_pair(self, x, u, adj: str = "T", stream=None):
+        """vsie_coupling_apply_pair_pwl: (Z_pwl x, Z_pwl^T u) or (.., Z_pwl^H u), single RHS."""
+        torch = _torch()
+        x = x.contiguous()
+        u = u.contiguous()
+        y = torch.empty(self.out_len("N"), dtype=torch.complex128, device=x.device)
+        z = torch.empty(self.out_len("T"), dtype=torch.complex128, device=x.device)
+        hs = (_lib.HANDLE * 4)(*[h._h for h in self.handles])
+        check(lib().vsie_coupling_apply_pair_pwl(hs, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
+                                                 C.c_void_p(u.data_ptr()), C.c_void_p(z.data_ptr()), _lib.OPS[adj],
+                                                 _stream_ptr(stream)))
+        return y, z
+
+    def apply_pair_raw(self, x_ptr: int, y_ptr: int, u_ptr: int, z_ptr: int, adj: str = "T", stream=None):
+        hs = (_lib.HANDLE * 4)(*[h._h for h in self.handles])
+        check(lib().vsie_coupling_apply_pair_pwl(hs, C.c_void_p(x_ptr), C.c_void_p(y_ptr), C.c_void_p(u_ptr),
+                                                 C.c_void_p(z_ptr), _lib.OPS[adj], _stream_ptr(stream)))

@@ -235,6 +235,17 @@ int32_t vsie_coupling_apply_pwl(const vsie_coupling_t h[4], const void* x, void*
   });
 }
 
+int32_t vsie_coupling_apply_pair_pwl(const vsie_coupling_t h[4], const void* x, void* y, const void* u, void* z,
+                                     int32_t adj_op, void* stream) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "handle array is NULL");
+    vsie_coupling_s* hs[4] = {h[0], h[1], h[2], h[3]};
+    apply_pair_pwl(hs, static_cast<const cplx*>(x), static_cast<cplx*>(y), static_cast<const cplx*>(u),
+                   static_cast<cplx*>(z), adj_op, static_cast<cudaStream_t>(stream));
+    return VSIE_OK;
+  });
+}
+
 int32_t vsie_coupling_apply_pair(vsie_coupling_t h, const void* x, void* y, const void* u, void* z, int32_t adj_op,
                                  void* stream) {
   return guarded([&] {

@@ -333,5 +333,8 @@ vsie_coupling_s::~vsie_coupling_s() {
   for (auto e : event_pool) cudaEventDestroy(e);
   if (io_stream) cudaStreamDestroy(io_stream);
   if (io_stream2) cudaStreamDestroy(io_stream2);
+  if (pwl_stream) cudaStreamDestroy(pwl_stream);
+  if (pwl_ev_fork) cudaEventDestroy(pwl_ev_fork);
+  if (pwl_ev_done) cudaEventDestroy(pwl_ev_done);
   vsie::apply_destroy(this);
 }

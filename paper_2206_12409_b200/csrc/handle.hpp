@@ -105,6 +105,8 @@ struct vsie_coupling_s {
   vsie::DevBuf<vsie::cplx> pwl_scratch;    // vsie_coupling_apply_pwl: Z_l^T u_l, l = 1..3
   vsie::DevBuf<int64_t> io_idx;
   cudaStream_t io_stream = nullptr;
+  cudaStream_t pwl_stream = nullptr;   // apply_pair_pwl: this moment handle's pair runs here
+  cudaEvent_t pwl_ev_fork = nullptr, pwl_ev_done = nullptr;
   cudaStream_t io_stream2 = nullptr;   // host pair: the transpose's copies + apply
   // info
   int64_t entries_evaluated = 0;
@@ -143,6 +145,8 @@ void apply(vsie_coupling_s* h, const cplx* x, cplx* y, int op, int nrhs, cudaStr
 void apply_pair(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z, int adj_op, cudaStream_t st);
 // vsie_coupling_apply_pwl (pwl.cu)
 void apply_pwl(vsie_coupling_s* const hs[4], const cplx* x, cplx* y, int op, int nrhs, cudaStream_t st);
+void apply_pair_pwl(vsie_coupling_s* const hs[4], const cplx* x, cplx* y, const cplx* u, cplx* z, int adj_op,
+                    cudaStream_t st);
 // drops the cached apply graphs (cores / workspaces changed)
 void apply_reset_graphs(vsie_coupling_s* h);
 void apply_destroy(vsie_coupling_s* h);

@@ -105,3 +105,21 @@ def test_pwl_handle_order_checked(pwl1, cfg1):
     bad = PWLCoupling([pwl1.handles[1], pwl1.handles[0], pwl1.handles[2], pwl1.handles[3]])
     with pytest.raises(VsieError):
         bad.apply(torch.zeros(cfg1.m, dtype=torch.complex128, device="cuda"), "N")
+
+
+@pytest.mark.parametrize("adj", ["T", "C"])
+def test_pwl_pair_vs_separate_and_oracle(pwl1, cfg1, adj):
+    import torch
+    tts = [h.export_cores() for h in pwl1.handles]
+    nvox = 3 * cfg1.n_v
+    x = synth.complex_gaussian(cfg1.m, 8400)
+    u = synth.complex_gaussian(4 * nvox, 8401)
+    y, z = pwl1.apply_pair(torch.from_numpy(x).cuda(), torch.from_numpy(u).cuda(), adj)
+    y, z = y.cpu().numpy(), z.cpu().numpy()
+    yref = np.concatenate([ttmv.apply(tts[l], x, "N") for l in range(4)])
+    zref = sum(ttmv.apply(tts[l], u[l * nvox:(l + 1) * nvox], adj) for l in range(4))
+    assert validate.rel_l2(y, yref) <= 1e-12
+    assert validate.rel_l2(z, zref) <= 1e-12
+    ys = pwl1.apply(torch.from_numpy(x).cuda(), "N").cpu().numpy()
+    zs = pwl1.apply(torch.from_numpy(u).cuda(), adj).cpu().numpy()
+    assert validate.rel_l2(y, ys) <= 1e-13 and validate.rel_l2(z, zs) <= 1e-13
