@@ -237,7 +237,9 @@ int32_t vsie_coupling_apply_pair_host(vsie_coupling_t h, const void* x_host, voi
  *   OP_T/OP_C:  z = sum_l Z_l^op u_l, u in the same 4-block layout, z m x nrhs; the four
  *               partial products are summed in the order l = 0, 1, 2, 3 on device.
  * Device pointers, stream-ordered on `stream`; x, y, u, z as in vsie_coupling_apply.  A
- * device scratch of 3 m nrhs complex128 is held by h[0].  Errors: VSIE_ERR_ARG for a NULL
+ * device scratch of 3 m nrhs complex128 is held by h[0].  On one process the four handles
+ * run concurrently on four streams (VSIE_PWL_CONCURRENT=0: in turn); multi-process
+ * handles (world > 1, each with its own NCCL unique id) run in turn.  Errors: VSIE_ERR_ARG for a NULL
  * handle, handles with moments other than 0, 1, 2, 3 in that order, or mismatched
  * geometry / partition; otherwise as vsie_coupling_apply. */
 int32_t vsie_coupling_apply_pwl(const vsie_coupling_t h[4], const void* x, void* y, int32_t op, int32_t nrhs,

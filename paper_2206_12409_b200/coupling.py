@@ -337,14 +337,27 @@ class PWLCoupling:
         assert len(handles) == 4
         self.handles = list(handles)
 
-    @classmethod
-    def build(cls, grid: Grid, meshes, freq: float, tol: float, **opts):
-        return cls([Coupling.build(grid, meshes, freq, tol, test_moment=l, **opts) for l in range(4)])
+    @staticmethod
+    def _per_moment(opts, nccl_unique_ids):
+        # every moment handle of a multi-process group owns its own NCCL communicator, so
+        # it needs its own unique id (rank 0 creates four and broadcasts them)
+        if "nccl_unique_id" in opts and opts["nccl_unique_id"] is not None:
+            raise ValueError("PWLCoupling: pass nccl_unique_ids=[four ids], one per moment handle")
+        if nccl_unique_ids is None:
+            return [dict(opts) for _ in range(4)]
+        assert len(nccl_unique_ids) == 4
+        return [dict(opts, nccl_unique_id=nccl_unique_ids[l]) for l in range(4)]
 
     @classmethod
-    def from_cores(cls, grid: Grid, meshes, freq: float, cores4, **opts):
+    def build(cls, grid: Grid, meshes, freq: float, tol: float, nccl_unique_ids=None, **opts):
+        per = cls._per_moment(opts, nccl_unique_ids)
+        return cls([Coupling.build(grid, meshes, freq, tol, test_moment=l, **per[l]) for l in range(4)])
+
+    @classmethod
+    def from_cores(cls, grid: Grid, meshes, freq: float, cores4, nccl_unique_ids=None, **opts):
         """cores4[l][chi][k] as in Coupling.from_cores, one set per test moment."""
-        return cls([Coupling.from_cores(grid, meshes, freq, cores4[l], test_moment=l, **opts) for l in range(4)])
+        per = cls._per_moment(opts, nccl_unique_ids)
+        return cls([Coupling.from_cores(grid, meshes, freq, cores4[l], test_moment=l, **per[l]) for l in range(4)])
 
     def close(self):
         for h in self.handles:

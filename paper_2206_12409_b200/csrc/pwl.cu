@@ -54,7 +54,9 @@ void sum_moments(vsie_coupling_s* h0, cplx* z, const cplx* s, int64_t mm, cudaSt
 }
 
 // VSIE_PWL_CONCURRENT (default 1): the four moment handles run on four streams, so one
-// handle's latency-bound G1 / G2 phases overlap the others' HBM-bound G3 / G4 passes
+// handle's latency-bound G1 / G2 phases overlap the others' HBM-bound G3 / G4 passes.
+// Multi-process handles (own NCCL communicator each) run one after another: collectives
+// of different communicators issued concurrently may wait on each other's SMs.
 bool pwl_concurrent() {
   static const bool on = [] {
     const char* e = std::getenv("VSIE_PWL_CONCURRENT");
@@ -95,7 +97,7 @@ void apply_pwl(vsie_coupling_s* const hs[4], const cplx* x, cplx* y, int op, int
     hs[0]->pwl_scratch.ensure(3 * mm);
     s = hs[0]->pwl_scratch.p;
   }
-  const bool conc = pwl_concurrent();
+  const bool conc = pwl_concurrent() && !hs[0]->comm;
   if (conc) pwl_fork(hs, st);
   for (int l = 0; l < 4; ++l) {
     cudaStream_t sl = conc ? hs[l]->pwl_stream : st;
@@ -118,7 +120,7 @@ void apply_pair_pwl(vsie_coupling_s* const hs[4], const cplx* x, cplx* y, const 
   const int64_t vox = local_vox(hs[0]), mm = hs[0]->m;
   hs[0]->pwl_scratch.ensure(3 * mm);
   cplx* s = hs[0]->pwl_scratch.p;
-  if (!pwl_concurrent()) {
+  if (!pwl_concurrent() || hs[0]->comm) {
     apply_pair(hs[0], x, y, u, z, adj_op, st);
     for (int l = 1; l < 4; ++l) apply_pair(hs[l], x, y + l * vox, u + l * vox, s + (l - 1) * mm, adj_op, st);
   } else {

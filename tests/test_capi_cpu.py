@@ -81,3 +81,15 @@ def test_geometry_errors():
     oob[0, 0] = len(xyz) + 3
     st, _, _ = _import(grid, [(xyz, oob)])
     assert st == -2
+
+
+def test_pwl_per_moment_nccl_ids():
+    """Each PWL moment handle of a multi-process group gets its own NCCL unique id."""
+    import pytest
+    from paper_2206_12409_b200 import PWLCoupling
+    per = PWLCoupling._per_moment({"world": 2, "rank": 1}, [b"a", b"b", b"c", b"d"])
+    assert [p["nccl_unique_id"] for p in per] == [b"a", b"b", b"c", b"d"]
+    assert all(p["world"] == 2 and p["rank"] == 1 for p in per)
+    assert all("nccl_unique_id" not in p for p in PWLCoupling._per_moment({"world": 1}, None))
+    with pytest.raises(ValueError):
+        PWLCoupling._per_moment({"nccl_unique_id": b"x"}, None)

@@ -123,3 +123,21 @@ def test_pwl_pair_vs_separate_and_oracle(pwl1, cfg1, adj):
     ys = pwl1.apply(torch.from_numpy(x).cuda(), "N").cpu().numpy()
     zs = pwl1.apply(torch.from_numpy(u).cuda(), adj).cpu().numpy()
     assert validate.rel_l2(y, ys) <= 1e-13 and validate.rel_l2(z, zs) <= 1e-13
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_pwl_pair_loopback_slabs(pwl1, cfg1, world):
+    """The slab-sharded PWL pair (i3 planes and G4 columns over `world` ranks, emulated on
+    one GPU) equals the single-rank one."""
+    import torch
+    from paper_2206_12409_b200 import PWLCoupling
+    cores4 = [h.export_cores() for h in pwl1.handles]
+    hp = PWLCoupling.from_cores(grid_of(cfg1), cfg1.meshes(), cfg1.freq, cores4, nrhs_max=1, world=world,
+                                loopback=1)
+    x = torch.from_numpy(synth.complex_gaussian(cfg1.m, 8500)).cuda()
+    u = torch.from_numpy(synth.complex_gaussian(4 * 3 * cfg1.n_v, 8501)).cuda()
+    y1, z1 = pwl1.apply_pair(x, u, "T")
+    yp, zp = hp.apply_pair(x, u, "T")
+    assert validate.rel_l2(yp.cpu().numpy(), y1.cpu().numpy()) <= 1e-13
+    assert validate.rel_l2(zp.cpu().numpy(), z1.cpu().numpy()) <= 1e-13
+    hp.close()
