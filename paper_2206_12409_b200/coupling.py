@@ -363,6 +363,10 @@ class PWLCoupling:
         for h in self.handles:
             h.close()
 
+    def round(self, tol: float):
+        """vsie_coupling_round on each moment handle; returns the new ranks [l][chi][k]."""
+        return [h.round(tol) for h in self.handles]
+
     def out_len(self, op: str) -> int:
         n = self.handles[0].out_len(op)
         return 4 * n if op == "N" else n

@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--round", type=float, default=None, metavar="TOL",
+                    help="TT-round each moment handle (vsie_coupling_round) at TOL before timing")
     args = ap.parse_args()
     import torch
     import synth
@@ -30,6 +32,10 @@ def main():
     t0 = time.perf_counter()
     P = PWLCoupling.build(grid_of(cfg), cfg.meshes(), cfg.freq, cfg.tol, nrhs_max=1)
     build_s = time.perf_counter() - t0
+    ranks_before = None
+    if args.round is not None:
+        ranks_before = [h.info()["ranks"] for h in P.handles]
+        P.round(args.round)
     infos = [h.info() for h in P.handles]
     B = sum(step_bytes_flops(cfg.n, cfg.m, inf["ranks"], 1)[0] for inf in infos)
     dev = torch.device("cuda")
@@ -66,6 +72,7 @@ def main():
         "ms_separate_applies": ms_sep, "bytes_per_step": B, "workload": f"cfg{cfg.idx} PWL",
         "ranks": [inf["ranks"] for inf in infos], "heldout_err": [inf["heldout_err"] for inf in infos],
         "compression": [float(inf["compression"]) for inf in infos], "build_s": build_s, "steps": args.steps,
+        "round": None if args.round is None else {"tol": args.round, "ranks_before": ranks_before},
         "l2_flush": "512 MiB fill between steps"}))
 
 
