@@ -196,6 +196,16 @@ void set_identity(Ctx& c, DevBuf<cplx>& V, int q) {
 // bases non-orthogonal -- held-out errors of 2e-3 at cfg 3 -- so it is 1e-14 again.)
 double trunc_small(const Ctx&) { return 1e-14; }
 
+// noise floor of the range finder's sketch orthonormalisation (VSIE_RF_SMALL overrides
+// the factor 1e-3 of delta; 0 restores the 1e-14 floor of the exact factorisations)
+double rf_small_rel(const Ctx& c) {
+  static const double f = [] {
+    const char* e = std::getenv("VSIE_RF_SMALL");
+    return e ? std::atof(e) : 1e-3;
+  }();
+  return f > 0 ? std::max(1e-14, f * c.delta) : 1e-14;
+}
+
 // Gram-preconditioned one-sided Jacobi SVD of a tall A (p x q): the eigenvectors
 // V1 of G = A^H A (one-sided Jacobi on the q x q Cholesky factor of G + s I; the
 // shift only guards the factorisation, eigenvectors are unchanged) make the
@@ -203,7 +213,7 @@ double trunc_small(const Ctx&) { return 1e-14; }
 // so the final one-sided Jacobi on the tall A V1 converges in a few sweeps while
 // keeping the one-sided method's relative accuracy.  On exit A holds U S and
 // V (if given) the accumulated right singular vectors V1 V2.
-void precond_jacobi(Ctx& c, cplx* A, int64_t p, int q, cplx* V) {
+void precond_jacobi(Ctx& c, cplx* A, int64_t p, int q, cplx* V, double small_rel = 1e-14) {
   Ws& w = c.ws;
   if (q <= 1) {
     if (V) {
@@ -244,7 +254,7 @@ void precond_jacobi(Ctx& c, cplx* A, int64_t p, int q, cplx* V) {
   cplx* V1 = w.Ra.p;
   if (!bad) {
     t0 = Clock::now();
-    jacobi(c, w.G.p, q, q, V1, trunc_small(c));  // G now holds R V1 (not needed)
+    jacobi(c, w.G.p, q, q, V1, small_rel);  // G now holds R V1 (not needed)
     c.t_jsmall += secs(t0);
     t0 = Clock::now();
     zgemm1(c, kN, kN, p, q, q, A, p, V1, q, w.Atmp.p, p);
@@ -255,7 +265,7 @@ void precond_jacobi(Ctx& c, cplx* A, int64_t p, int q, cplx* V) {
   w.Rb.ensure(qq);
   set_identity(c, w.Rb, q);
   t0 = Clock::now();
-  jacobi(c, A, p, q, w.Rb.p, trunc_small(c));
+  jacobi(c, A, p, q, w.Rb.p, small_rel);
   c.t_jtall += secs(t0);
   if (V) zgemm1(c, kN, kN, q, q, q, V1, q, w.Rb.p, q, V, q);
 }
@@ -347,12 +357,22 @@ int factorize(Ctx& c, const cplx* M, int64_t rows, int64_t cols, bool left, int 
       zgemm1(c, kN, kN, rows, kk, cols, M, rows, w.omega.p, cols, w.Y.p, rows);
     else
       zgemm1(c, kC, kN, cols, kk, rows, M, rows, w.omega.p, rows, w.Y.p, cols);
-    precond_jacobi(c, w.Y.p, p1, kk, nullptr);
+    // Orthonormal basis of the sketch's dominant range.  Sketch directions whose norm
+    // stays below rf_small ||Y||_F (rf_small = 1e-3 delta) are noise far under the
+    // truncation level: Jacobi leaves them unrotated and they are dropped from Q, so Q
+    // stays orthonormal (every kept pair was rotated to the 1e-12 cosine) and the
+    // dropped energy is <= sqrt(kk) 1e-3 delta relative.  Orthogonalising that noise
+    // among itself cost up to the 40-sweep cap on the doubled sketches.
+    const double rf_small = rf_small_rel(c);
+    precond_jacobi(c, w.Y.p, p1, kk, nullptr, rf_small);
     auto sy = sorted_norms(c, w.Y.p, p1, kk);
+    double fy2 = 0;
+    for (auto& e : sy) fy2 += e.first * e.first;
+    const double cut = std::max(1e-13 * sy[0].first, 1.0001 * rf_small * std::sqrt(fy2));
     std::vector<int> keep;
     std::vector<double> inv;
     for (auto& e : sy)
-      if (e.first > 1e-13 * sy[0].first) {
+      if (e.first > cut) {
         keep.push_back(e.second);
         inv.push_back(1.0 / e.first);
       }
@@ -372,7 +392,10 @@ int factorize(Ctx& c, const cplx* M, int64_t rows, int64_t cols, bool left, int 
     precond_jacobi(c, w.Bh.p, p2, kq, w.V.p);
     auto s = sorted_norms(c, w.Bh.p, p2, kq);
     const int r = choose_rank(s, total2, true, c.delta, std::min(cap, kq));
-    if (r > kq - os && kk < mn) {
+    // grow the sketch only while it is still mostly above the noise floor: once more
+    // than `os` of its directions fell below rf_small, M's range at that level is
+    // already inside Q and a larger sketch adds only noise directions
+    if (r > kq - os && kq > kk - os && kk < mn) {
       kk = (int)std::min<int64_t>(2 * (int64_t)kk, mn);
       continue;
     }
