@@ -396,7 +396,11 @@ int factorize(Ctx& c, const cplx* M, int64_t rows, int64_t cols, bool left, int 
     // than `os` of its directions fell below rf_small, M's range at that level is
     // already inside Q and a larger sketch adds only noise directions
     if (r > kq - os && kq > kk - os && kk < mn) {
-      kk = (int)std::min<int64_t>(2 * (int64_t)kk, mn);
+      // rank found inside the sketch but with less than `os` oversampling: grow to
+      // r + 2 os (a rank drift of a few per sweep no longer doubles a ~300-column sketch,
+      // whose Jacobi cost grows as q^2); a saturated sketch (r == kq) doubles
+      const int64_t grow = r < kq ? (int64_t)r + 2 * os : 2 * (int64_t)kk;
+      kk = (int)std::min<int64_t>(std::max<int64_t>(grow, (int64_t)kk + os), mn);
       continue;
     }
     std::vector<int> sel(r);
