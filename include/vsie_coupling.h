@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define VSIE_ABI_VERSION 2
+#define VSIE_ABI_VERSION 3
 
 /* status codes */
 #define VSIE_OK 0
@@ -126,6 +126,10 @@ typedef struct {
   int64_t apply_launches;       /* kernel launches made by vsie_coupling_apply* so far (this handle) */
   int64_t apply_calls;
   int32_t test_moment;          /* vsie_build_opts.test_moment of the build / import         */
+  int32_t pair_schedule;        /* schedule of vsie_coupling_apply_pair: 1 = G4 read once (transpose
+                                 * front, one G4 pass for both products, forward tail), 2 = G3 read
+                                 * once (forward G4 pass, one G3 pass for both products, transpose
+                                 * G4 pass); chosen to move fewer bytes unless configured       */
 } vsie_info;
 
 /* Per-kernel device timing of apply calls (opt-in, see vsie_coupling_set_timing). */
@@ -202,15 +206,13 @@ int32_t vsie_coupling_apply(vsie_coupling_t h, const void* x, void* y, int32_t o
 /* The coupling pair of one GMRES matvec of the hybrid system (Eq. 11 / 15: the
  * body rows need Z_bc j_c, the conductor rows Z_cb j_b = Z_bc^T j_b, Eqs. 17-19):
  * y = Z x (layouts as OP_N above) and z = Z^T u (adj_op = OP_T) or Z^H u (OP_C) (layouts
- * as OP_T), single right-hand side, in one call.  The transpose's G1-G3 steps run first
- * so that both directions' G4 products share one pass over the largest core (one TMA-
- * streamed launch over the three chi, which also forms the chi sum of Eq. 18); the G3
- * steps of both directions are likewise one batched launch each.  Results equal two
- * vsie_coupling_apply calls to rounding and are bitwise reproducible.  The schedule is
- * selected by the environment (read once per process): VSIE_PAIR_G4 = 2
- * (default, as described), 0 (per-chi chains, G4 pair per chain), 3 (forward and
- * transpose as six independent chains), 4 (every step one batched launch on the stream).
- * Asynchronous; collective when world > 1. */
+ * as OP_T), single right-hand side, in one call.  One of the two large cores is streamed
+ * once for both directions (vsie_info.pair_schedule): G4 (r3 x m) when it is the larger,
+ * by running the transpose's G1-G3 steps first so that one TMA-streamed pass over G4 forms
+ * y4 = G4 x and z = sum_chi G4^T z3 (the chi sum of Eq. 18), else G3 ((r2 n3) x r3), by
+ * running the forward's G4 pass first so that one pass over G3 forms Y3 = G3 y4 and
+ * z3 = G3^T W2.  Results equal two vsie_coupling_apply calls to rounding and are bitwise
+ * reproducible.  Asynchronous; collective when world > 1. */
 int32_t vsie_coupling_apply_pair(vsie_coupling_t h, const void* x, void* y, const void* u, void* z, int32_t adj_op,
                                  void* stream);
 
@@ -273,25 +275,11 @@ int32_t vsie_coupling_info(vsie_coupling_t h, vsie_info* out);
 int32_t vsie_coupling_set_timing(vsie_coupling_t h, int32_t enable);
 int32_t vsie_coupling_timers(vsie_coupling_t h, vsie_timer* out, int32_t max, int32_t* n_out);
 
-/* Execution strategy of vsie_coupling_apply (all results agree to rounding and each is
- * deterministic): use_graphs = 1 (default) replays each (op, nrhs, x, y) as a captured
- * CUDA graph.  mode selects the single-RHS schedule: 0 (default) three concurrent per-chi
- * kernel chains, 1 one persistent dataflow kernel per direction, 2 one batched kernel per
- * contraction step (see DESIGN.md for the measured comparison).  Negative = keep. */
-int32_t vsie_coupling_configure(vsie_coupling_t h, int32_t use_graphs, int32_t mode);
-
-/* Diagnostics of the persistent single-RHS apply: with enable = 1 every tile of the
- * following applies records its start / end (globaltimer) and SM; records of the last
- * launch of direction dir (0 forward, 1 transpose) on shard 0 are copied out with
- * vsie_coupling_tile_trace (phase = queue phase, chi, idx = tile index in its phase). */
-typedef struct {
-  int32_t phase, chi;
-  int64_t idx;
-  int32_t sm;
-  double t0_us, t1_us, ready_us;   /* claimed, finished, dependencies satisfied */
-} vsie_tile_rec;
-int32_t vsie_coupling_set_tile_trace(vsie_coupling_t h, int32_t enable);
-int32_t vsie_coupling_tile_trace(vsie_coupling_t h, int32_t dir, vsie_tile_rec* out, int64_t max, int64_t* n_out);
+/* Execution strategy: use_graphs = 1 (default) replays each apply / pair (op, nrhs, pointers)
+ * as a captured CUDA graph (single-process handles), 0 launches eagerly.  pair_schedule
+ * selects the schedule of vsie_coupling_apply_pair: 0 (default) the one that moves fewer
+ * bytes, 1 G4 read once, 2 G3 read once.  Negative = keep.  Synchronises the device. */
+int32_t vsie_coupling_configure(vsie_coupling_t h, int32_t use_graphs, int32_t pair_schedule);
 
 /* Timeline of apply calls made with vsie_coupling_set_timing(h, 2): the chi chains run
  * concurrently (as in the captured graph, but launched eagerly) with a CUDA event pair

@@ -42,7 +42,8 @@ class vsie_info(C.Structure):
                 ("build_s", C.c_double), ("build_entry_s", C.c_double), ("build_factor_s", C.c_double),
                 ("build_maxvol_s", C.c_double), ("slab", C.c_int32 * 2), ("cols", C.c_int64 * 2),
                 ("world", C.c_int32), ("rank", C.c_int32), ("loopback", C.c_int32), ("k0", C.c_double),
-                ("apply_launches", C.c_int64), ("apply_calls", C.c_int64), ("test_moment", C.c_int32)]
+                ("apply_launches", C.c_int64), ("apply_calls", C.c_int64), ("test_moment", C.c_int32),
+                ("pair_schedule", C.c_int32)]
 
 
 class vsie_timer(C.Structure):
@@ -53,11 +54,6 @@ class vsie_timer(C.Structure):
 class vsie_trace(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("chi", C.c_int32), ("call", C.c_int32), ("t0_ms", C.c_double),
                 ("t1_ms", C.c_double)]
-
-
-class vsie_tile_rec(C.Structure):
-    _fields_ = [("phase", C.c_int32), ("chi", C.c_int32), ("idx", C.c_int64), ("sm", C.c_int32),
-                ("t0_us", C.c_double), ("t1_us", C.c_double), ("ready_us", C.c_double)]
 
 
 HANDLE = C.c_void_p
@@ -84,9 +80,6 @@ _SIGS = {
     "vsie_coupling_info": (C.c_int32, [HANDLE, C.POINTER(vsie_info)]),
     "vsie_coupling_set_timing": (C.c_int32, [HANDLE, C.c_int32]),
     "vsie_coupling_timers": (C.c_int32, [HANDLE, C.POINTER(vsie_timer), C.c_int32, C.POINTER(C.c_int32)]),
-    "vsie_coupling_set_tile_trace": (C.c_int32, [HANDLE, C.c_int32]),
-    "vsie_coupling_tile_trace": (C.c_int32, [HANDLE, C.c_int32, C.POINTER(vsie_tile_rec), C.c_int64,
-                                             C.POINTER(C.c_int64)]),
     "vsie_coupling_apply_pair": (C.c_int32, [HANDLE, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                              C.c_void_p]),
     "vsie_coupling_apply_pair_host": (C.c_int32, [HANDLE, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),

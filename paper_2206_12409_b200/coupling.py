@@ -158,7 +158,8 @@ class Coupling:
             build_s=i.build_s, build_entry_s=i.build_entry_s, build_factor_s=i.build_factor_s,
             build_maxvol_s=i.build_maxvol_s, slab=tuple(i.slab), cols=tuple(i.cols), world=i.world,
             rank=i.rank, loopback=i.loopback, k0=i.k0, apply_launches=i.apply_launches,
-            apply_calls=i.apply_calls, test_moment=i.test_moment)
+            apply_calls=i.apply_calls, test_moment=i.test_moment,
+            pair_schedule={1: "g4_shared", 2: "g3_shared"}.get(i.pair_schedule))
 
     @property
     def m(self):
@@ -288,28 +289,15 @@ class Coupling:
         """0/False off, 1/True serialised per-kernel timing, 2 concurrent timeline (trace())."""
         check(lib().vsie_coupling_set_timing(self._h, int(enable)))
 
-    MODES = {"chains": 0, "persistent": 1, "batched": 2}
+    PAIR_SCHEDULES = {"auto": 0, "g4_shared": 1, "g3_shared": 2}
 
-    def configure(self, graphs=None, mode=None, persistent=None):
-        """Apply strategy: CUDA-graph replay and the single-RHS schedule (None = keep):
-        mode 'chains' (default), 'persistent' or 'batched'; persistent=True/False is a
-        shorthand for mode 'persistent' / 'chains'."""
+    def configure(self, graphs=None, pair_schedule=None):
+        """CUDA-graph replay and the schedule of apply_pair (None = keep): pair_schedule
+        'auto' (the one moving fewer bytes), 'g4_shared' (G4 read once) or 'g3_shared'
+        (G3 read once)."""
         g = -1 if graphs is None else int(bool(graphs))
-        if persistent is not None:
-            mode = "persistent" if persistent else "chains"
-        m = -1 if mode is None else (self.MODES[mode] if isinstance(mode, str) else int(mode))
+        m = -1 if pair_schedule is None else self.PAIR_SCHEDULES[pair_schedule]
         check(lib().vsie_coupling_configure(self._h, g, m))
-
-    def set_tile_trace(self, enable):
-        check(lib().vsie_coupling_set_tile_trace(self._h, int(bool(enable))))
-
-    def tile_trace(self, direction, max_records=65536):
-        """Per-tile timeline of the last persistent launch (direction 0 forward, 1 transpose)."""
-        n = C.c_int64()
-        arr = (_lib.vsie_tile_rec * max_records)()
-        check(lib().vsie_coupling_tile_trace(self._h, int(direction), arr, max_records, C.byref(n)))
-        return [dict(phase=arr[i].phase, chi=arr[i].chi, idx=arr[i].idx, sm=arr[i].sm, t0_us=arr[i].t0_us,
-                     t1_us=arr[i].t1_us, ready_us=arr[i].ready_us) for i in range(min(n.value, max_records))]
 
     def trace(self, max_records=4096):
         n = C.c_int32()

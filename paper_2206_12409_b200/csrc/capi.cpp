@@ -269,7 +269,7 @@ int32_t vsie_coupling_apply_pair_host(vsie_coupling_t h, const void* x_host, voi
     cplx* du = h->io_x.p + h->m;
     cplx* dy = h->io_y.p;
     cplx* dz = h->io_y.p + vox;
-    if (h->apply_mode == 0 && !h->comm) {
+    if (!h->comm) {
       // Host buffers: the PCIe copies dominate (2 x 16 * 3 n_v bytes against ~0.1 ms of
       // device work), and y = Z x needs only x.  So the forward runs first on one stream
       // and its voxel result streams back (D2H) while u streams in (H2D) on a second
@@ -357,6 +357,7 @@ int32_t vsie_coupling_info(vsie_coupling_t h, vsie_info* out) {
     out->apply_launches = h->apply_launches;
     out->apply_calls = h->apply_calls;
     out->test_moment = h->test_moment;
+    out->pair_schedule = h->has_cores ? pair_schedule(h) : 0;
     return VSIE_OK;
   });
 }
@@ -421,58 +422,14 @@ int32_t vsie_coupling_timers(vsie_coupling_t h, vsie_timer* out, int32_t max, in
   });
 }
 
-int32_t vsie_coupling_configure(vsie_coupling_t h, int32_t use_graphs, int32_t mode) {
+int32_t vsie_coupling_configure(vsie_coupling_t h, int32_t use_graphs, int32_t pair_schedule) {
   return guarded([&] {
     VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "handle is NULL");
+    VSIE_REQUIRE(pair_schedule <= 2, VSIE_ERR_ARG, "pair_schedule must be 0 (auto), 1 (G4 shared) or 2 (G3 shared)");
     VSIE_CHECK_CUDA(cudaDeviceSynchronize());
     if (use_graphs >= 0) h->use_graphs = use_graphs != 0;
-    VSIE_REQUIRE(mode <= 2, VSIE_ERR_ARG, "mode must be 0 (chains), 1 (persistent) or 2 (batched)");
-    if (mode >= 0) h->apply_mode = mode;
+    if (pair_schedule >= 0) h->pair_sched = pair_schedule;
     apply_reset_graphs(h);
-    return VSIE_OK;
-  });
-}
-
-int32_t vsie_coupling_set_tile_trace(vsie_coupling_t h, int32_t enable) {
-  return guarded([&] {
-    VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "handle is NULL");
-    VSIE_CHECK_CUDA(cudaDeviceSynchronize());
-    h->tile_trace = enable != 0;
-    if (h->tile_trace)
-      for (Shard& s : h->shards)
-        for (int d = 0; d < 2; ++d) s.mega_trace[d].ensure((size_t)4 * 65536);
-    apply_reset_graphs(h);
-    return VSIE_OK;
-  });
-}
-
-int32_t vsie_coupling_tile_trace(vsie_coupling_t h, int32_t dir, vsie_tile_rec* out, int64_t max, int64_t* n_out) {
-  return guarded([&] {
-    VSIE_REQUIRE(h != nullptr && n_out != nullptr && (dir == 0 || dir == 1), VSIE_ERR_ARG, "bad argument");
-    VSIE_CHECK_CUDA(cudaDeviceSynchronize());
-    *n_out = 0;
-    Shard& s = h->shards[0];
-    const MegaPlan& p = s.mega_traced[dir];
-    if (!s.mega_trace[dir].p || p.nseg == 0) return VSIE_OK;
-    const int64_t n = p.seg_off[p.nseg];
-    std::vector<unsigned long long> host((size_t)4 * n);
-    VSIE_CHECK_CUDA(cudaMemcpy(host.data(), s.mega_trace[dir].p, host.size() * sizeof(unsigned long long),
-                               cudaMemcpyDeviceToHost));
-    const auto recs = mega_decode_trace(p, host.data());
-    int64_t k = 0;
-    for (const auto& r : recs) {
-      if (out && k < max) {
-        out[k].phase = r.phase;
-        out[k].chi = r.chi;
-        out[k].idx = r.idx;
-        out[k].sm = r.sm;
-        out[k].t0_us = r.t0_us;
-        out[k].t1_us = r.t1_us;
-        out[k].ready_us = r.tr_us;
-      }
-      ++k;
-    }
-    *n_out = k;
     return VSIE_OK;
   });
 }

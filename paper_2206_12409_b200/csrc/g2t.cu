@@ -115,94 +115,15 @@ __global__ void __launch_bounds__(32 * NW) k_g2t(const __grid_constant__ G2tArgs
   pdl_trigger();
 }
 
-// Forward G2 step Y2 = G2 Y3 (Eq. 17 step 3): M = r1 n2 rows, K = r2 (short), so
-// no K split: warp w of a CTA owns the 8 x (8 TN) tile (m-tile 8 blockIdx.x + w, n-tiles
-// TN blockIdx.y ..) over the whole K, 3M DMMA with fragments from L2 / L1 (A[m][k] =
-// G2[m + M k], B[k][n] = Y3[k + K n]) and writes it once.
-template <int TN>
-__global__ void __launch_bounds__(kG2Threads) k_g2n(const __grid_constant__ G2tArgs a) {
-  pdl_wait();
-  const int b = blockIdx.z;
-  const int M = a.M[b], N = a.N, K = a.K[b];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = (blockIdx.x * kG2Warps + warp) * 8, n0 = blockIdx.y * 8 * TN;
-  if (m0 < M && n0 < N) {
-    const int g = lane >> 2, t = lane & 3;
-    const int ksn = (K + 3) / 4;
-    const cplx* __restrict__ Am = a.G2[b] + min(m0 + g, M - 1);      // A[m][k] at Am[M k] (clamped: discarded)
-    const cplx* Bc[TN];
-#pragma unroll
-    for (int j = 0; j < TN; ++j) Bc[j] = a.W1[b] + (int64_t)K * min(n0 + 8 * j + g, N - 1);   // B[k][n] at Bc[k]
-    double p1[TN][2], p2[TN][2], p3[TN][2];
-#pragma unroll
-    for (int j = 0; j < TN; ++j) p1[j][0] = p1[j][1] = p2[j][0] = p2[j][1] = p3[j][0] = p3[j][1] = 0;
-    constexpr int UNR = 5;
-    for (int ks = 0; ks < ksn; ks += UNR) {
-      cplx av[UNR], bv[UNR][TN];
-#pragma unroll
-      for (int q = 0; q < UNR; ++q) {
-        const int k = 4 * (ks + q) + t;
-        const bool ok = k < K;
-        av[q] = ok ? __ldg(Am + (int64_t)M * k) : cmk(0, 0);
-#pragma unroll
-        for (int j = 0; j < TN; ++j) bv[q][j] = ok ? __ldg(Bc[j] + k) : cmk(0, 0);
-      }
-#pragma unroll
-      for (int q = 0; q < UNR; ++q) {
-        const double as = av[q].x + av[q].y;
-#pragma unroll
-        for (int j = 0; j < TN; ++j) {
-          dmma_g2(p1[j][0], p1[j][1], av[q].x, bv[q][j].x);
-          dmma_g2(p2[j][0], p2[j][1], av[q].y, bv[q][j].y);
-          dmma_g2(p3[j][0], p3[j][1], as, bv[q][j].x + bv[q][j].y);
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < TN; ++j)
-#pragma unroll
-      for (int jj = 0; jj < 2; ++jj) {
-        const int m = m0 + g, n = n0 + 8 * j + 2 * t + jj;
-        if (m < M && n < N) a.W2[b][m + (int64_t)a.ldw[b] * n] = cmk(p1[j][jj] - p2[j][jj], p3[j][jj] - p1[j][jj] - p2[j][jj]);
-      }
-  }
-  pdl_trigger();
-}
-
 }  // namespace
 
-void launch_g2n(const G2tArgs& a, cudaStream_t st) {
-  int mmax = 0;
-  for (int b = 0; b < a.nbatch; ++b) mmax = std::max(mmax, a.M[b]);
-  if (mmax == 0 || a.N == 0) return;
-  // four n-tiles per warp: A (G2) fragments loaded once for 32 columns; the warps of a CTA
-  // share their B (Y3) fragments through L1
-  constexpr int TN = 4;
-  dim3 grid((unsigned)ceil_div(mmax, 8 * kG2Warps), (unsigned)ceil_div(a.N, 8 * TN), a.nbatch);
-  launch_pdl(k_g2n<TN>, grid, dim3(kG2Threads), 0, st, a);
-  VSIE_CHECK_LAUNCH();
-}
-
-// VSIE_G2T_TILE: 1 = 8 x 8 tiles, 8 warps (default); 2 = 16 x 16 tiles, 16 warps;
-// 3 = 8 x 16 tiles, 8 warps
+// one CTA per 8 x 8 output tile, K split over its 8 warps (16 x 16 / 8 x 16 tiles measured slower)
 void launch_g2t(const G2tArgs& a, cudaStream_t st) {
   int mmax = 0;
   for (int b = 0; b < a.nbatch; ++b) mmax = std::max(mmax, a.M[b]);
   if (mmax == 0 || a.N == 0) return;
-  static const int tile = [] {
-    const char* e = std::getenv("VSIE_G2T_TILE");
-    return e ? std::atoi(e) : 1;
-  }();
-  if (tile == 2) {
-    dim3 grid((unsigned)ceil_div(mmax, 16), (unsigned)ceil_div(a.N, 16), a.nbatch);
-    launch_pdl(k_g2t<2, 2, 16>, grid, dim3(32 * 16), 0, st, a);
-  } else if (tile == 3) {
-    dim3 grid((unsigned)ceil_div(mmax, 8), (unsigned)ceil_div(a.N, 16), a.nbatch);
-    launch_pdl(k_g2t<1, 2, 8>, grid, dim3(32 * 8), 0, st, a);
-  } else {
-    dim3 grid((unsigned)ceil_div(mmax, 8), (unsigned)ceil_div(a.N, 8), a.nbatch);
-    launch_pdl(k_g2t<1, 1, 8>, grid, dim3(32 * 8), 0, st, a);
-  }
+  dim3 grid((unsigned)ceil_div(mmax, 8), (unsigned)ceil_div(a.N, 8), a.nbatch);
+  launch_pdl(k_g2t<1, 1, 8>, grid, dim3(32 * 8), 0, st, a);
   VSIE_CHECK_LAUNCH();
 }
 

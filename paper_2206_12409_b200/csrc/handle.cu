@@ -71,6 +71,12 @@ void handle_init_geometry(vsie_coupling_s* h, const vsie_grid* grid, const vsie_
   h->grid = make_grid(grid);
   h->sources = build_sources(meshes, n_meshes, h->grid);
   h->m = h->sources.m;
+  {
+    uint64_t f = 1469598103934665603ull;
+    const unsigned char* b = reinterpret_cast<const unsigned char*>(h->sources.table.data());
+    for (size_t i = 0; i < h->sources.table.size() * sizeof(double); ++i) f = (f ^ b[i]) * 1099511628211ull;
+    h->src_hash = f;
+  }
   const double c0 = 299792458.0;
   h->k0 = 2.0 * M_PI * freq / c0;
   h->scale_re = o->scale_re;
@@ -160,7 +166,6 @@ void handle_alloc_workspace(vsie_coupling_s* h) {
     r2m = std::max(r2m, h->ranks[c][1]);
     r3m = std::max(r3m, h->ranks[c][2]);
   }
-  int64_t rmax_gemv = 1;
   // row-blocked copies of the G3 slices (k_seg_gemv)
   const int nsb = sm_count_dev();
   for (Shard& s : h->shards) {
@@ -183,16 +188,14 @@ void handle_alloc_workspace(vsie_coupling_s* h) {
     s.z3.alloc(3 * (int64_t)r3m * k);
     s.Y3.alloc(3 * (int64_t)r2m * n3l * k);
     s.W2.alloc(3 * (int64_t)r2m * n3l * k);
-    s.W2p.alloc(3 * (int64_t)((n2 + 7) / 8) * r2m * n3l);
     s.Y2.alloc(3 * (int64_t)r1m * n2 * n3l * k);
     s.W1.alloc(3 * (int64_t)r1m * n2 * n3l * k);
-    rmax_gemv = std::max(rmax_gemv, (int64_t)r2m * n3l);
   }
   (void)n1;
-  (void)rmax_gemv;
-  // per-chi split-K partials of the GEMVs (the launchers lower the split to fit)
-  // and of the ZGEMMs: the three chi chains of an apply run concurrently
-  h->partials_per_chi = 400000;
+  // per-chi split-K partials of the GEMVs (the launchers lower the split to fit) and the
+  // per-CTA partials of the batched TMA passes ([chi][CTA][r3max] from partials(0), so a
+  // region of three chi holds 3 nsm r3max): the three chi chains of an apply run concurrently
+  h->partials_per_chi = std::max<int64_t>(400000, (int64_t)nsb * r3m);
   h->partials.alloc((size_t)6 * h->partials_per_chi);   // [fwd chi 0..2][adj chi 0..2]
   int64_t wsz = 64 * std::max<int64_t>((int64_t)r2m * std::max(1, h->shards[0].n3loc()) * k, (int64_t)r3m * k);
   h->zgemm_ws_per_chi = std::min<int64_t>(wsz, (int64_t)16 << 20);
@@ -201,40 +204,6 @@ void handle_alloc_workspace(vsie_coupling_s* h) {
   int64_t mloc_max = 1;
   for (Shard& s : h->shards) mloc_max = std::max<int64_t>(mloc_max, s.mloc());
   for (Shard& s : h->shards) s.zpart.alloc((size_t)3 * mloc_max * k);
-  // persistent single-RHS apply: plan + self-resetting sync words (zeroed once here)
-  for (Shard& s : h->shards) {
-    MegaArgs& a = s.mega;
-    a = MegaArgs{};
-    for (int c = 0; c < 3; ++c) {
-      a.c[c].G1 = h->G1[c].p;
-      a.c[c].G2 = h->G2[c].p;
-      a.c[c].G3 = s.G3[c].p;
-      a.c[c].G4 = s.G4[c].p;
-      a.c[c].r1 = h->ranks[c][0];
-      a.c[c].r2 = h->ranks[c][1];
-      a.c[c].r3 = h->ranks[c][2];
-    }
-    a.n1 = n1;
-    a.n2 = n2;
-    a.n3l = std::max(0, s.n3loc());
-    a.mloc = s.mloc();
-    a.r1max = r1m;
-    a.r2max = r2m;
-    a.r3max = r3m;
-    a.y4 = s.y4.p;
-    a.Y3 = s.Y3.p;
-    a.Y2 = s.Y2.p;
-    a.zpart = s.zpart.p;
-    const bool ok = r1m <= 32 && r3m <= 2048 && a.n3l > 0 && a.mloc > 0;
-    if (ok) {
-      mega_plan(a);
-      s.mega_part.alloc((size_t)std::max<int64_t>(1, a.p.part_elems));
-      s.mega_sync.alloc((size_t)a.p.sync_words);
-      VSIE_CHECK_CUDA(cudaMemset(s.mega_sync.p, 0, s.mega_sync.bytes()));
-      a.part = s.mega_part.p;
-      a.sync = s.mega_sync.p;
-    }
-  }
   apply_reset_graphs(h);
   if (h->comm) {
     const int64_t mp = ceil_div(h->m, h->world);

@@ -9,7 +9,6 @@
 #include "comm.hpp"
 #include "geometry.hpp"
 #include "kernels.cuh"
-#include "mega.cuh"
 
 namespace vsie {
 
@@ -30,15 +29,8 @@ struct Shard {
   DevBuf<cplx> Y2;      // [3][r1 * n2 * n3loc * nrhs]
   DevBuf<cplx> W1;      // [3][r1 * n2 * n3loc * nrhs]   (adjoint: G1^T u)
   DevBuf<cplx> W2;      // [3][r2 * n3loc * nrhs]
-  DevBuf<cplx> W2p;     // [3][ceil(n2 / 8)][r2 * n3loc]  fused transpose front: W2 partials
   DevBuf<cplx> z3;      // [3][r3max * nrhs]
   DevBuf<cplx> zpart;   // [3][mloc_max * nrhs]  transpose: per-chi G4_chi^T z3_chi
-  // single-RHS persistent apply (mega.cu): plan, partials, sync words
-  MegaArgs mega{};
-  DevBuf<cplx> mega_part;
-  DevBuf<unsigned> mega_sync;
-  DevBuf<unsigned long long> mega_trace[2];   // diagnostics (vsie_coupling_set_tile_trace)
-  MegaPlan mega_traced[2]{};
   int n3loc() const { return i3e - i3b; }
   int64_t mloc() const { return ce - cb; }
 };
@@ -72,6 +64,7 @@ struct vsie_coupling_s {
   double k0 = 0;
   double scale_re = 1, scale_im = 0;
   vsie::Sources sources;
+  uint64_t src_hash = 0;   // FNV-1a of the source table (PWL moment handles must agree)
   vsie::DevBuf<double> d_src;
   vsie::EntryGeom eg{};
   int ranks[3][3] = {{0}};
@@ -88,18 +81,12 @@ struct vsie_coupling_s {
   int64_t zgemm_ws_per_chi = 0;
   // apply orchestration: one stream per chi chain, fork/join events, graph cache
   cudaStream_t chi_stream[3] = {nullptr, nullptr, nullptr};
-  cudaStream_t chi_stream2[3] = {nullptr, nullptr, nullptr};   // second chain set (pair: fwd beside adj)
-  cudaEvent_t ev_join2[3] = {nullptr, nullptr, nullptr};
   cudaStream_t cap_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
-  cudaEvent_t ev_stage[3] = {nullptr, nullptr, nullptr};   // chain staggering
   std::vector<vsie::GraphEntry> graphs;
   uint64_t graph_clock = 0;
   int use_graphs = 1;
-  int w2_parts[3] = {0, 0, 0};          // pair: split-K partials of W2 left for k_seg_gemv
-  int64_t w2_part_stride[3] = {0, 0, 0};
-  int apply_mode = 0;   // single RHS: 0 per-chi kernel chains, 1 persistent kernel, 2 batched kernels
-  int tile_trace = 0;
+  int pair_sched = 0;   // GMRES pair: 0 auto (fewer bytes), 1 G4 read once, 2 G3 read once
   vsie::DevBuf<vsie::cplx> gather_buf;     // allgather staging of z
   vsie::DevBuf<vsie::cplx> io_x, io_y;     // apply_host staging
   vsie::DevBuf<vsie::cplx> pwl_scratch;    // vsie_coupling_apply_pwl: Z_l^T u_l, l = 1..3
@@ -147,6 +134,8 @@ void apply_pair(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx*
 void apply_pwl(vsie_coupling_s* const hs[4], const cplx* x, cplx* y, int op, int nrhs, cudaStream_t st);
 void apply_pair_pwl(vsie_coupling_s* const hs[4], const cplx* x, cplx* y, const cplx* u, cplx* z, int adj_op,
                     cudaStream_t st);
+// schedule the pair runs with: 1 = G4-shared, 2 = G3-shared (apply.cu)
+int pair_schedule(vsie_coupling_s* h);
 // drops the cached apply graphs (cores / workspaces changed)
 void apply_reset_graphs(vsie_coupling_s* h);
 void apply_destroy(vsie_coupling_s* h);

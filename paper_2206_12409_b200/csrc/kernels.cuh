@@ -63,25 +63,10 @@ struct GemvT {
   bool conj_out;  // store conj(y) (op C post-conjugation)
 };
 
-// Fused pair on the surface-side core (the off-diagonal coupling pair of one GMRES
-// matvec): ypart[s][r] = sum_{c in split s} A[r + R c] x[c] (forward y4 partials) and
-// z[c] = sum_r A[r + R c] z3[r] (transpose) from ONE pass over A (R <= 320).
-struct GemvNT {
-  const cplx* A[3];
-  const cplx* x[3];
-  const cplx* z3[3];
-  const cplx* z3b[3];   // optional second partial of z3 (summed on load), may be null
-  cplx* z[3];
-  cplx* y4[3];
-  int64_t R[3], C[3];
-  int nbatch;
-};
-// false when R > 320 (the caller falls back to separate passes)
-bool launch_gemv_nt(const GemvNT& a, cplx* partials, int64_t partials_cap, cudaStream_t st);
-
 // TMA-streamed G4 pass of the GMRES pair (pairg4.cu): for every chi b < nbatch,
 // y4[b] = A[b] x (CTA partials at partials[(b ns + s) rstride + r], summed in fixed order)
-// and z = sum_b A[b]^T z3[b] (conj if conj_z), one read of every A[b] (R[b] x C, R <= 320).
+// and z = sum_b A[b]^T z3[b] (conj if conj_z), one read of every A[b] (R[b] x C, R <= 2048;
+// R > 320 takes the row-band variant).
 // x == nullptr: transpose only; z3[0] == nullptr: forward only.
 struct PairG4 {
   const cplx* A[3];
@@ -93,11 +78,12 @@ struct PairG4 {
   int64_t R[3];
   int64_t C, rstride;
   int64_t ccta;   // set by the launcher: max columns per CTA
+  int nslots;      // set by the launcher (large-r3 band kernel): ring slots
+  int64_t slot_elems;  // set by the launcher (band kernel): complex elements per slot
   int nbatch;
   bool conj_z;
-  bool small_ring;   // 80 KB ring (per-chi launches beside compute kernels) instead of 160 KB
 };
-// false when the shape is unsupported (R > 320): the caller falls back
+// false when the shape is unsupported (R > 2048 or smem): the caller falls back
 bool launch_pair_g4(const PairG4& a, int max_ctas, cudaStream_t st);
 int pair_g4_max_rank();
 // TMA-streamed GEMV on column-major R[b] x C[b] matrices, batched over b < nbatch
@@ -126,23 +112,6 @@ struct SegGemv {
 bool launch_seg_gemv_mode(const SegGemv& a, int mode, cudaStream_t st, bool small_ring = false);
 bool launch_seg_gemv(const SegGemv& a, bool transpose, cudaStream_t st);
 bool seg_gemv_supported(int64_t R, int64_t C, int nsb);
-// Fused transpose front (adjfront.cu), single RHS, batched over chi: W1 = G1^T u and
-// W2p[blk] = G2[:, blk, :]^T W1[:, blk, :] per block of 8 i2 values (W2p[b][blk *
-// w2p_stride + beta + r2 i3]), then W2[b] = sum_blk W2p[b][blk] in fixed order.
-struct AdjFrontArgs {
-  const cplx* G1[3];
-  const cplx* G2[3];
-  const cplx* u[3];     // voxel column (i2, i3) at u + n1 (i2 + n2 i3)
-  cplx* W2p[3];
-  cplx* W2[3];          // r2 x n3l column-major
-  int64_t w2p_stride;   // >= r2 n3l
-  int n1, n2, n3l;
-  int r1[3], r2[3];
-  int nbatch;
-  bool conj_u;
-};
-bool adj_front_supported(int n1, int r1max);
-void launch_adj_front(const AdjFrontArgs& a, cudaStream_t st);
 // W2[b] = G2[b]^T W1[b] (g2t.cu): M[b] = r2, K[b] = r1 n2 rows of the column-major
 // (r1 n2) x r2 core, N = n3l columns of W1 (ld K); one launch over the batch, no split-K
 // partials (K split over the 8 warps of a CTA, fixed-order smem tree)
@@ -155,14 +124,9 @@ struct G2tArgs {
   int nbatch;
 };
 void launch_g2t(const G2tArgs& a, cudaStream_t st);
-// forward Y2[b] = G2[b] Y3[b] with the same argument block read as: G2 (M = r1 n2 rows,
-// K = r2), W1 := Y3 (K x N, ld K), W2 := Y2 (ld ldw = r1 n2); one warp per 8 x 8 tile
-void launch_g2n(const G2tArgs& a, cudaStream_t st);
 // fixed-order sum of ns split partials ([b][s][rmax]) into a.y[b][0 .. a.R[b])
 void launch_gemv_sum(const GemvN& a, cplx* partials, int ns, int64_t rmax, cudaStream_t st);
 int sm_count_dev();
-
-struct ApplyWorkspace;  // split-K partials + counters (handle-owned)
 
 // partials_cap: capacity (elements) of the split-K partial buffer; the split is
 // lowered so that it always fits.
@@ -195,32 +159,13 @@ struct ReduceArgs {
   int64_t ncol, cols_per_rhs, ld_rhs;
   int nbatch;
   bool conj_u;
-  int diag;   // k_reduce_tma diagnostics (VSIE_RT_DIAG): 1 = stream only, no arithmetic
 };
 void launch_reduce_g1(const ReduceArgs& a, cudaStream_t st);
-// TMA-streamed W1 = G1^T u over the batch in one persistent launch (reduce_tma.cu), single
-// RHS; false when unsupported (the caller uses launch_reduce_g1)
-bool launch_reduce_g1_tma(const ReduceArgs& a, cudaStream_t st);
-bool reduce_tma_fits(int n1, int r1max);
-bool reduce_tma_on();
 
 // out[i + ld_out j] = sum_{c<3} in[c * chi_stride + i + ld_in j] (fixed order), conj if asked;
 // i < rows, j < k  (the Eq. 18 sum over chi of the per-chi transposes)
 void launch_sum3(const cplx* in, int64_t chi_stride, int64_t ld_in, int64_t rows, int k, cplx* out, int64_t ld_out,
                  bool conj_out, cudaStream_t st);
-
-// Fused forward tail of one chi (single RHS): Y2 = G2 Y3 on a tile of (i2, i3) planes
-// into shared memory, then y = G1 Y2 for the tile's voxel columns (Eq. 17 steps
-// 3-4).  y points at the chi block (and slab offset) of the voxel output.
-struct G21Args {
-  const cplx* G1;   // n1 x r1
-  const cplx* G2;   // (r1 n2) x r2
-  const cplx* Y3;   // r2 x n3l
-  cplx* y;
-  int n1, n2, n3l, r1, r2;
-};
-// false if r1 > 32 (caller falls back to the two-kernel path)
-bool launch_g21_fwd(const G21Args& a, cudaStream_t st);
 
 // ------------------------------------------------------------------ dense complex LA (linalg.cu)
 enum Trans { kN = 0, kT = 1, kC = 2 };
@@ -242,12 +187,6 @@ void launch_zgemm(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t st);
 // same contract on FP64 tensor cores (DMMA), warp-tiled, for small / skinny
 // problems; op(B) must be N.
 void launch_zgemm_dmma(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t st);
-// same, but a split-K result is left as partials for the consumer to sum: returns 0 when C
-// was written, else the number of splits S with C_b = sum_q ws[(b S + q) *part_stride + m + M n]
-int launch_zgemm_dmma_parts(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t st, int64_t* part_stride);
-// C = sum of the split partials left by launch_zgemm_dmma_parts (fixed order)
-void launch_splitk_sum(const Zgemm& g, const cplx* ws, int splits, int64_t stride, cudaStream_t st);
-
 // conj in place
 void launch_conj(cplx* x, int64_t n, cudaStream_t st);
 // y[i] += x[i]

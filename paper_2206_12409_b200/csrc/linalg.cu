@@ -9,8 +9,6 @@
 #include "kernels.cuh"
 #include "dmma_tile.cuh"
 
-#include <cooperative_groups.h>
-
 #include <algorithm>
 #include <cstdlib>
 
@@ -341,43 +339,6 @@ __global__ void __launch_bounds__(tc::kThreads) k_zgemm_tc(const __grid_constant
 // own shared memory, and after a cluster barrier rank sp sums a 1/S slice of the tile over
 // the S peers' shared memory (distributed shared memory, fixed rank order: deterministic)
 // and writes C = alpha sum + beta C.  One launch, no global partials, no reduce kernel.
-template <int WA, int WB, bool TA>
-__global__ void __launch_bounds__(tc::kThreads) k_zgemm_tc_cl(const __grid_constant__ Zgemm g, int64_t mt, int64_t nt) {
-  namespace cg = cooperative_groups;
-  extern __shared__ __align__(16) unsigned char raw[];
-  tc::GemmSmem& sm = *reinterpret_cast<tc::GemmSmem*>(raw);
-  constexpr int TM = 16 * WA, TN = 16 * WB;
-  cplx* part = reinterpret_cast<cplx*>(raw + ((sizeof(tc::GemmSmem) + 127) / 128) * 128);   // [TN][TM]
-  cg::cluster_group cl = cg::this_cluster();
-  const int S = (int)cl.num_blocks(), sp = (int)cl.block_rank();
-  pdl_wait();
-  const int b = blockIdx.y;
-  const int64_t tile = blockIdx.x / S;
-  const int64_t M = g.M[b], N = g.N[b], K = g.K[b];
-  const int64_t m0 = (tile % mt) * TM, n0 = (tile / mt) * TN;
-  if (b >= g.nbatch || m0 >= M || n0 >= N) return;   // uniform over the cluster (same tile)
-  const int64_t chunks = (K + tc::GKC - 1) / tc::GKC;
-  const int64_t k0 = std::min<int64_t>(K, chunks * sp / S * tc::GKC);
-  const int64_t k1 = std::min<int64_t>(K, chunks * (sp + 1) / S * tc::GKC);
-  tc::gemm_tile<WA, WB, TA>(g.A[b], g.lda[b], g.B[b], g.ldb[b], M, N, m0, n0, k0, k1, sm, part, TM);
-  cl.sync();
-  const bool has_beta = g.beta.x != 0.0 || g.beta.y != 0.0;
-  const int e0 = TM * TN * sp / S, e1 = TM * TN * (sp + 1) / S;
-  for (int e = e0 + (int)threadIdx.x; e < e1; e += tc::kThreads) {
-    const int mm = e % TM, nn = e / TM;
-    const int64_t m = m0 + mm, n = n0 + nn;
-    if (m >= M || n >= N) continue;
-    cplx acc = cmk(0, 0);
-    for (int r = 0; r < S; ++r) acc = cadd(acc, cl.map_shared_rank(part, r)[e]);
-    cplx* c = g.C[b] + m + g.ldc[b] * n;
-    cplx v = cmul(g.alpha, acc);
-    if (has_beta) v = cadd(v, cmul(g.beta, *c));
-    *c = v;
-  }
-  cl.sync();   // peers' shared memory stays valid until every slice is read
-  pdl_trigger();
-}
-
 template <int TA, int TB>
 void zgemm_t(const Zgemm& g, int splits, dim3 grid, cplx* ws, int64_t stride, cudaStream_t st) {
   k_zgemm<TA, TB><<<grid, NT, 0, st>>>(g, splits, ws, stride);
@@ -422,23 +383,7 @@ void launch_zgemm(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t st) {
   }
 }
 
-// split-K of the DMMA ZGEMM inside thread-block clusters (k_zgemm_tc_cl), opt-in
-// VSIE_ZGEMM_CLUSTER=1: the G2^T ZGEMM itself gets faster (20 -> 17 us at cluster size 16)
-// but the cfg 2 pair step slower (0.167 -> 0.173 ms: 16-CTA clusters fit the concurrent
-// chains badly), so global split partials + k_splitk_reduce stay the default
-bool zgemm_cluster_on() {
-  static const int v = [] {
-    const char* e = std::getenv("VSIE_ZGEMM_CLUSTER");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v != 0;
-}
-
 void launch_zgemm_dmma(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t st) {
-  launch_zgemm_dmma_parts(g, ws, ws_elems, st, nullptr);
-}
-
-int launch_zgemm_dmma_parts(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStream_t st, int64_t* part_stride) {
   VSIE_REQUIRE(g.tb == kN && g.ta != kC, VSIE_ERR_ARG, "zgemm_dmma: op(A) in {N, T}, op(B) = N");
   int64_t mmax = 0, nmax = 0, kmax = 0, mn = 0;
   for (int b = 0; b < g.nbatch; ++b) {
@@ -447,7 +392,7 @@ int launch_zgemm_dmma_parts(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStre
     kmax = std::max(kmax, g.K[b]);
     mn = std::max(mn, g.M[b] * g.N[b]);
   }
-  if (mmax == 0 || nmax == 0) return 1;
+  if (mmax == 0 || nmax == 0) return;
   // warp layout: tall (4 x 2 -> 64 x 32) or wide (2 x 4 -> 32 x 64) output tiles
   const bool tall = mmax >= 2 * nmax;
   const int TM = tall ? tc::FTM : tc::ATM, TN = tall ? tc::FTN : tc::ATN;
@@ -462,53 +407,6 @@ int launch_zgemm_dmma_parts(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStre
     splits = (int)std::min<int64_t>(std::min<int64_t>(ceil_div(2 * 148, tiles), std::max<int64_t>(1, chunks / 3)), 64);
     while (splits > 1 && (int64_t)splits * mn * g.nbatch > ws_elems) --splits;
     splits = std::max(splits, 1);
-  }
-  if (splits > 1 && zgemm_cluster_on()) {
-    // split-K within a cluster (DSMEM reduction) when each split keeps <= 32 chunks
-    static const int smax = [] {
-      const char* e = std::getenv("VSIE_ZGEMM_CLUSTER_MAX");
-      return e ? std::max(2, std::min(16, std::atoi(e))) : 16;
-    }();
-    const int S = (int)std::min<int64_t>(std::min<int64_t>(smax, ceil_div(2 * 148, tiles)), std::max<int64_t>(1, chunks / 2));
-    if (S >= 2 && ceil_div(chunks, S) <= 32) {
-      const bool ta = g.ta == kT;
-      const size_t csmem = ((sizeof(tc::GemmSmem) + 127) / 128) * 128 + (size_t)std::max(tc::FTM * tc::FTN, tc::ATM * tc::ATN) * sizeof(cplx);
-      static bool cattr = false;
-      if (!cattr) {
-        VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_zgemm_tc_cl<tc::FWA, tc::FWB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
-        VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_zgemm_tc_cl<tc::FWA, tc::FWB, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_zgemm_tc_cl<tc::FWA, tc::FWB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
-        VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_zgemm_tc_cl<tc::FWA, tc::FWB, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_zgemm_tc_cl<tc::AWA, tc::AWB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
-        VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_zgemm_tc_cl<tc::AWA, tc::AWB, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_zgemm_tc_cl<tc::AWA, tc::AWB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
-        VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_zgemm_tc_cl<tc::AWA, tc::AWB, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        cattr = true;
-      }
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3((unsigned)(mt * nt * S), (unsigned)g.nbatch);
-      cfg.blockDim = dim3(tc::kThreads);
-      cfg.dynamicSmemBytes = csmem;
-      cfg.stream = st;
-      cudaLaunchAttribute attrs[2];
-      attrs[0].id = cudaLaunchAttributeClusterDimension;
-      attrs[0].val.clusterDim.x = S;
-      attrs[0].val.clusterDim.y = 1;
-      attrs[0].val.clusterDim.z = 1;
-      attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      attrs[1].val.programmaticStreamSerializationAllowed = 1;
-      cfg.attrs = attrs;
-      cfg.numAttrs = pdl_enabled() ? 2 : 1;
-      if (tall) {
-        if (ta) VSIE_CHECK_CUDA(cudaLaunchKernelEx(&cfg, k_zgemm_tc_cl<tc::FWA, tc::FWB, true>, g, mt, nt));
-        else VSIE_CHECK_CUDA(cudaLaunchKernelEx(&cfg, k_zgemm_tc_cl<tc::FWA, tc::FWB, false>, g, mt, nt));
-      } else {
-        if (ta) VSIE_CHECK_CUDA(cudaLaunchKernelEx(&cfg, k_zgemm_tc_cl<tc::AWA, tc::AWB, true>, g, mt, nt));
-        else VSIE_CHECK_CUDA(cudaLaunchKernelEx(&cfg, k_zgemm_tc_cl<tc::AWA, tc::AWB, false>, g, mt, nt));
-      }
-      VSIE_CHECK_LAUNCH();
-      return 0;
-    }
   }
   const int direct = (splits == 1 && unit) ? 1 : 0;
   VSIE_REQUIRE(direct || (ws != nullptr && (int64_t)splits * mn * g.nbatch <= ws_elems), VSIE_ERR_ARG,
@@ -533,24 +431,9 @@ int launch_zgemm_dmma_parts(const Zgemm& g, cplx* ws, int64_t ws_elems, cudaStre
     else launch_pdl(k_zgemm_tc<tc::AWA, tc::AWB, false>, grid, blk, smem, st, g, splits, mt, nt, ws, mn, direct);
   }
   VSIE_CHECK_LAUNCH();
-  if (direct) return 0;
-  if (part_stride && unit) {
-    // the caller sums the split partials (ws[(b splits + q) mn + m + M n]) on load
-    *part_stride = mn;
-    return splits;
-  }
+  if (direct) return;
   dim3 rg((unsigned)std::min<int64_t>(ceil_div(mn, 256), 148 * 8), g.nbatch);
   launch_pdl(k_splitk_reduce, rg, dim3(256), 0, st, g, splits, (const cplx*)ws, mn);
-  VSIE_CHECK_LAUNCH();
-  return 0;
-}
-
-void launch_splitk_sum(const Zgemm& g, const cplx* ws, int splits, int64_t stride, cudaStream_t st) {
-  if (splits <= 0) return;
-  int64_t mn = 0;
-  for (int b = 0; b < g.nbatch; ++b) mn = std::max(mn, g.M[b] * g.N[b]);
-  dim3 rg((unsigned)std::min<int64_t>(ceil_div(mn, 256), 148 * 8), g.nbatch);
-  launch_pdl(k_splitk_reduce, rg, dim3(256), 0, st, g, splits, ws, stride);
   VSIE_CHECK_LAUNCH();
 }
 

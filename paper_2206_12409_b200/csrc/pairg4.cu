@@ -21,6 +21,8 @@
 #include "kernels.cuh"
 #include "tma_ring.cuh"
 
+#include <algorithm>
+
 namespace vsie {
 namespace {
 using namespace tma;
@@ -41,13 +43,12 @@ struct StageMap {
 
 // Stage i (global over the chi sequence) lives in slot i % kSlots and is consumed by warp
 // i % kConsumerWarps alone: no cross-warp barrier per stage, each warp double-buffered.
-// MODE: 3 both products (the GMRES pair), 1 forward only (y4 = G4 x), 2 transpose only
-// (z = sum_chi G4^T z3) -- the single-direction variants let a pass run beside the other
-// direction's compute-bound steps (VSIE_PAIR_G4=5)
+// MODE: 3 both products (the GMRES pair, G4-shared schedule), 1 forward only (y4 = G4 x),
+// 2 transpose only (z = sum_chi G4^T z3) -- the single applies and the G3-shared pair
 template <int NQ, int MODE, int SL>
 __global__ void __launch_bounds__(kPairThreads, 1) k_pair_g4(const __grid_constant__ PairG4 a) {
   constexpr bool FW = (MODE & 1) != 0, TR = (MODE & 2) != 0;
-  constexpr int kSlots = SL;                       // 16 (160 KB) or 8 (80 KB, per-chi chains)
+  constexpr int kSlots = SL;                       // 16 slots: 160 KB in flight per SM
   constexpr int kRingBytes = SL * kStageBytes;
   extern __shared__ __align__(128) unsigned char smem[];
   cplx* ring = reinterpret_cast<cplx*>(smem);
@@ -107,11 +108,12 @@ __global__ void __launch_bounds__(kPairThreads, 1) k_pair_g4(const __grid_consta
   }
 
   // ---------------- consumers
-  // x is the caller's input: staged before the wait (a per-column global load would sit
-  // behind the HBM stream's queues)
+  // x may be written by the caller's preceding kernel (the single forward apply starts with
+  // this kernel): staged only after the PDL wait, from L2 (a per-column global load inside
+  // the stage loop would sit behind the HBM stream's queues)
+  pdl_wait();   // x / z3 come from the stream predecessor
   if (FW)
-    for (int j = threadIdx.x; j < nc; j += 32 * kConsumerWarps) xs[j] = __ldg(a.x + c0 + j);
-  pdl_wait();   // z3 comes from the stream predecessor
+    for (int j = threadIdx.x; j < nc; j += 32 * kConsumerWarps) xs[j] = __ldcg(a.x + c0 + j);
   if (TR) {
     // all of a thread's z3 loads in flight before its stores (this sits after the PDL wait,
     // on the critical path)
@@ -217,22 +219,224 @@ __global__ void __launch_bounds__(kPairThreads, 1) k_pair_g4(const __grid_consta
     }
 }
 
+
+// ---------------------------------------------------------------- large r3 (320 < R <= 2048)
+// Row-band variant for the r3 ~ 1500 cores of the two-surface configs (cfg 3 / 5): a lane
+// can no longer hold a whole column, so every stage (whole columns, <= 32 KB) is consumed
+// by ALL 8 consumer warps, warp w owning the row band [R w / 8, R (w + 1) / 8) (lane l:
+// rows band0 + l + 32 q, q < NQ).  The forward accumulators of a band stay in that warp's
+// registers (no cross-warp tree: the bands are disjoint); the transpose's per-column dot
+// product is reduced across the lanes of each warp and kept as a per-(warp, column) partial
+// in shared memory, summed over the chi (Eq. 18) and finally over the 8 warps in fixed
+// order.  The stage's empty barrier counts the 8 warps.  Deterministic, no atomics.
+constexpr int kBandMaxSlots = 16;
+
+template <int NQ, int MODE>
+__global__ void __launch_bounds__(kPairThreads, 1) k_pair_g4_band(const __grid_constant__ PairG4 a) {
+  constexpr bool FW = (MODE & 1) != 0, TR = (MODE & 2) != 0;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int nslots = a.nslots;
+  const int64_t se = a.slot_elems;
+  cplx* ring = reinterpret_cast<cplx*>(smem);
+  cplx* zw = ring + (size_t)nslots * se;            // [8][ccta] per-warp column partials
+  cplx* xs = zw + (size_t)kConsumerWarps * a.ccta;  // x[c0 .. c1)
+  __shared__ uint64_t full[kBandMaxSlots], empty[kBandMaxSlots];
+
+  const int ns = gridDim.x, s = blockIdx.x;
+  const int64_t C = a.C;
+  const int64_t c0 = C * s / ns, c1 = C * (s + 1) / ns;
+  const int nc = (int)(c1 - c0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  StageMap mp;
+  int total = 0;
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    mp.cps[b] = 1;
+    mp.nst[b] = 0;
+    mp.off[b] = total;
+    if (b < a.nbatch) {
+      mp.cps[b] = max(1, (int)(se / a.R[b]));
+      mp.nst[b] = (nc + mp.cps[b] - 1) / mp.cps[b];
+      total += mp.nst[b];
+    }
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nslots; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    // producer: G4 is constant -- the ring fills before the stream predecessor ends
+    if (lane == 0) {
+      int i = 0;
+      for (int b = 0; b < a.nbatch; ++b) {
+        const int64_t R = a.R[b];
+        for (int t = 0; t < mp.nst[b]; ++t, ++i) {
+          const int slot = i % nslots;
+          if (i >= nslots) mbar_wait(&empty[slot], ((i / nslots) - 1) & 1);
+          const int cb = t * mp.cps[b];
+          const int ncol = min(mp.cps[b], nc - cb);
+          const uint32_t bytes = (uint32_t)(16 * R * ncol);
+          mbar_expect_tx(&full[slot], bytes);
+          bulk_g2s(ring + (size_t)slot * se, a.A[b] + R * (c0 + cb), bytes, &full[slot]);
+        }
+      }
+    }
+    pdl_wait();
+    return;
+  }
+
+  pdl_wait();   // x / z3 come from the stream predecessor
+  if (FW)
+    for (int j = threadIdx.x; j < nc; j += 32 * kConsumerWarps) xs[j] = __ldcg(a.x + c0 + j);
+  consumers_sync();
+  for (int b = 0; b < a.nbatch; ++b) {
+    const int R = (int)a.R[b];
+    const int rb0 = R * warp / kConsumerWarps, B = R * (warp + 1) / kConsumerWarps - rb0;
+    const int last = B - 1 - lane;   // B >= 1 (R > 320)
+    const int cps = mp.cps[b];
+    cplx zv[NQ], acc[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      zv[q] = TR && lane + 32 * q < B ? __ldcg(a.z3[b] + rb0 + lane + 32 * q) : cmk(0, 0);   // past B: zero weight
+      acc[q] = cmk(0, 0);
+    }
+    for (int t = 0; t < mp.nst[b]; ++t) {
+      const int i = mp.off[b] + t;
+      const int slot = i % nslots;
+      const int cb = t * cps;
+      const int ncol = min(cps, nc - cb);
+      mbar_wait(&full[slot], (i / nslots) & 1);
+      const cplx* st = ring + (size_t)slot * se + rb0;
+      for (int j = 0; j < ncol; j += 2) {
+        const bool two = j + 1 < ncol;
+        const cplx* col = st + (int64_t)R * j;
+        const cplx* col1 = two ? col + R : col;
+        const cplx xv0 = FW ? xs[cb + j] : cmk(0, 0), xv1 = FW && two ? xs[cb + j + 1] : cmk(0, 0);
+        cplx d0 = cmk(0, 0), d1 = cmk(0, 0);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const int r = min(32 * q, last) + lane;   // rows past the band re-read its last row
+          const cplx v0 = col[r], v1 = col1[r];
+          if (TR) {
+            cfma(d0, v0, zv[q]);
+            cfma(d1, v1, zv[q]);
+          }
+          if (FW) {
+            cfma(acc[q], v0, xv0);
+            cfma(acc[q], v1, xv1);
+          }
+        }
+        if (TR) {
+          const cplx d = pair_reduce(d0, d1, lane);
+          const int jj = cb + j + (lane >> 4);
+          cplx* zp = zw + (size_t)warp * a.ccta + jj;
+          if ((lane & 15) == 0 && (lane == 0 || two)) *zp = b == 0 ? d : cadd(*zp, d);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+    if (FW) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int r = lane + 32 * q;
+        if (r < B) {
+          if (ns == 1)
+            a.y4[b][rb0 + r] = acc[q];
+          else
+            a.partials[((int64_t)b * ns + s) * a.rstride + rb0 + r] = acc[q];
+        }
+      }
+    }
+  }
+  pdl_trigger();
+  if (TR) {
+    consumers_sync();   // every warp's column partials complete
+    for (int j = threadIdx.x; j < nc; j += 32 * kConsumerWarps) {
+      cplx v = zw[j];
+#pragma unroll
+      for (int w = 1; w < kConsumerWarps; ++w) v = cadd(v, zw[(size_t)w * a.ccta + j]);
+      a.z[c0 + j] = a.conj_z ? cconj(v) : v;
+    }
+  }
+}
+
 }  // namespace
 
-int pair_g4_max_rank() { return 320; }
+int pair_g4_max_rank() { return 2048; }
+
+namespace {
+
+bool launch_pair_g4_band(const PairG4& a, int64_t rmax, int max_ctas, cudaStream_t st) {
+  int64_t rmin = rmax;
+  for (int b = 0; b < a.nbatch; ++b) rmin = std::min(rmin, a.R[b]);
+  // the band kernel needs a non-empty band per warp: every chi's R > 8 (R > 320 for some chi;
+  // a small R of another chi is handled too as long as it fills the 8 bands)
+  if (rmin < kConsumerWarps) return false;
+  const int nq = (int)ceil_div(ceil_div(rmax, kConsumerWarps), 32);
+  const int ns = (int)std::max<int64_t>(1, std::min<int64_t>(max_ctas, ceil_div(a.C, 4)));
+  const int64_t ccta = ceil_div(a.C, ns);
+  // stage = whole columns, >= 16 KB; as many slots as fit beside the partials (<= 16)
+  const int64_t se = std::max<int64_t>(rmax, 16384 / 16 / rmax * rmax);
+  const size_t extra = (size_t)(kConsumerWarps + 1) * ccta * sizeof(cplx);
+  const size_t budget = 225 * 1024;
+  if (extra + 2 * se * sizeof(cplx) > budget) return false;
+  const int nslots = (int)std::min<int64_t>(kBandMaxSlots, (budget - extra) / (se * sizeof(cplx)));
+  const size_t smem = (size_t)nslots * se * sizeof(cplx) + extra;
+  PairG4 b = a;
+  b.ccta = ccta;
+  b.nslots = nslots;
+  b.slot_elems = se;
+  const int mode = (a.x ? 1 : 0) | (a.z3[0] ? 2 : 0);
+  if (mode == 0) return true;
+  switch (nq * 4 + mode) {
+#define VSIE_PGB(K, M)                                                                             \
+  case K * 4 + M: {                                                                                \
+    static size_t attr = 0;                                                                        \
+    if (smem > attr) {                                                                             \
+      VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_pair_g4_band<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+      attr = smem;                                                                                 \
+    }                                                                                              \
+    launch_pdl(k_pair_g4_band<K, M>, dim3(ns), dim3(kPairThreads), smem, st, b);                   \
+    break;                                                                                         \
+  }
+#define VSIE_PGB3(K) VSIE_PGB(K, 1) VSIE_PGB(K, 2) VSIE_PGB(K, 3)
+    VSIE_PGB3(2) VSIE_PGB3(3) VSIE_PGB3(4) VSIE_PGB3(5) VSIE_PGB3(6) VSIE_PGB3(7) VSIE_PGB3(8)
+#undef VSIE_PGB3
+#undef VSIE_PGB
+    default: return false;
+  }
+  VSIE_CHECK_LAUNCH();
+  if (ns > 1 && a.x) {
+    GemvN g{};
+    g.nbatch = a.nbatch;
+    for (int q = 0; q < a.nbatch; ++q) {
+      g.y[q] = a.y4[q];
+      g.R[q] = a.R[q];
+    }
+    launch_gemv_sum(g, a.partials, ns, a.rstride, st);
+  }
+  return true;
+}
+
+}  // namespace
 
 bool launch_pair_g4(const PairG4& a, int max_ctas, cudaStream_t st) {
   int64_t rmax = 0;
   for (int b = 0; b < a.nbatch; ++b) rmax = std::max(rmax, a.R[b]);
-  if (rmax > 320 || rmax < 1) return false;
+  if (rmax > 2048 || rmax < 1) return false;
   if (a.C == 0) return true;
   VSIE_REQUIRE(a.rstride >= rmax, VSIE_ERR_ARG, "pair_g4: partial stride below r3");
+  if (rmax > 320) return launch_pair_g4_band(a, rmax, max_ctas, st);
   const int nq = (int)ceil_div(rmax, 32);
   const int ns = (int)std::max<int64_t>(1, std::min<int64_t>(max_ctas, ceil_div(a.C, 4)));
   const int64_t ccta = ceil_div(a.C, ns);
-  const bool small = a.small_ring;
-  const size_t smem = (small ? kRingMaxBytes / 2 : kRingMaxBytes) + (size_t)4 * 32 * nq * sizeof(cplx) +
-                      (size_t)2 * ccta * sizeof(cplx) +
+  const size_t smem = kRingMaxBytes + (size_t)4 * 32 * nq * sizeof(cplx) + (size_t)2 * ccta * sizeof(cplx) +
                       (size_t)3 * 32 * nq * sizeof(cplx);
   PairG4 b = a;
   b.ccta = ccta;
@@ -242,20 +446,12 @@ bool launch_pair_g4(const PairG4& a, int max_ctas, cudaStream_t st) {
   switch (nq * 4 + mode) {
 #define VSIE_PG4M(K, M)                                                                            \
   case K * 4 + M: {                                                                                \
-    static size_t attr = 0, attr8 = 0;                                                             \
-    if (small) {                                                                                   \
-      if (smem > attr8) {                                                                          \
-        VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_pair_g4<K, M, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-        attr8 = smem;                                                                              \
-      }                                                                                            \
-      launch_pdl(k_pair_g4<K, M, 8>, dim3(ns), dim3(kPairThreads), smem, st, b);                   \
-    } else {                                                                                       \
-      if (smem > attr) {                                                                           \
-        VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_pair_g4<K, M, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-        attr = smem;                                                                               \
-      }                                                                                            \
-      launch_pdl(k_pair_g4<K, M, 16>, dim3(ns), dim3(kPairThreads), smem, st, b);                  \
+    static size_t attr = 0;                                                                        \
+    if (smem > attr) {                                                                             \
+      VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_pair_g4<K, M, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+      attr = smem;                                                                                 \
     }                                                                                              \
+    launch_pdl(k_pair_g4<K, M, 16>, dim3(ns), dim3(kPairThreads), smem, st, b);                    \
     break;                                                                                         \
   }
 #define VSIE_PG4(K) VSIE_PG4M(K, 1) VSIE_PG4M(K, 2) VSIE_PG4M(K, 3)

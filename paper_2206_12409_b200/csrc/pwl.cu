@@ -36,7 +36,8 @@ void check_pwl(vsie_coupling_s* const hs[4], int nrhs) {
     const vsie_coupling_s* a = hs[0];
     const vsie_coupling_s* b = hs[l];
     bool same = a->m == b->m && a->world == b->world && a->rank == b->rank && a->loopback == b->loopback &&
-                a->k0 == b->k0 && a->shards.size() == b->shards.size();
+                a->k0 == b->k0 && a->scale_re == b->scale_re && a->scale_im == b->scale_im &&
+                a->src_hash == b->src_hash && a->shards.size() == b->shards.size();
     for (int d = 0; d < 3 && same; ++d)
       same = a->grid.n[d] == b->grid.n[d] && a->grid.h[d] == b->grid.h[d] && a->grid.origin[d] == b->grid.origin[d];
     for (size_t q = 0; q < a->shards.size() && same; ++q)
@@ -53,18 +54,10 @@ void sum_moments(vsie_coupling_s* h0, cplx* z, const cplx* s, int64_t mm, cudaSt
   ++h0->apply_launches;
 }
 
-// VSIE_PWL_CONCURRENT (default 1): the four moment handles run on four streams, so one
+// One process: the four moment handles run on four streams, so one
 // handle's latency-bound G1 / G2 phases overlap the others' HBM-bound G3 / G4 passes.
 // Multi-process handles (own NCCL communicator each) run one after another: collectives
 // of different communicators issued concurrently may wait on each other's SMs.
-bool pwl_concurrent() {
-  static const bool on = [] {
-    const char* e = std::getenv("VSIE_PWL_CONCURRENT");
-    return e ? std::atoi(e) != 0 : true;
-  }();
-  return on;
-}
-
 void pwl_fork(vsie_coupling_s* const hs[4], cudaStream_t st) {
   for (int l = 0; l < 4; ++l) {
     vsie_coupling_s* h = hs[l];
@@ -97,7 +90,7 @@ void apply_pwl(vsie_coupling_s* const hs[4], const cplx* x, cplx* y, int op, int
     hs[0]->pwl_scratch.ensure(3 * mm);
     s = hs[0]->pwl_scratch.p;
   }
-  const bool conc = pwl_concurrent() && !hs[0]->comm;
+  const bool conc = !hs[0]->comm;
   if (conc) pwl_fork(hs, st);
   for (int l = 0; l < 4; ++l) {
     cudaStream_t sl = conc ? hs[l]->pwl_stream : st;
@@ -120,7 +113,7 @@ void apply_pair_pwl(vsie_coupling_s* const hs[4], const cplx* x, cplx* y, const 
   const int64_t vox = local_vox(hs[0]), mm = hs[0]->m;
   hs[0]->pwl_scratch.ensure(3 * mm);
   cplx* s = hs[0]->pwl_scratch.p;
-  if (!pwl_concurrent() || hs[0]->comm) {
+  if (hs[0]->comm) {
     apply_pair(hs[0], x, y, u, z, adj_op, st);
     for (int l = 1; l < 4; ++l) apply_pair(hs[l], x, y + l * vox, u + l * vox, s + (l - 1) * mm, adj_op, st);
   } else {

@@ -25,7 +25,6 @@ using namespace tma;
 constexpr int kCW = 8;                      // consumer warps
 constexpr int kSegThreads = 32 * (kCW + 1);
 constexpr int kStage = 10240;
-constexpr int kRingMax = 16 * kStage;
 
 __device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kCW) : "memory"); }
 
@@ -40,8 +39,8 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_seg_gemv(const __grid_consta
   extern __shared__ __align__(128) unsigned char smem[];
   cplx* ring = reinterpret_cast<cplx*>(smem);
   cplx* red = reinterpret_cast<cplx*>(smem + kRing);   // [4][32 NQ]      (op N)
-  cplx* vec = red + 4 * 32 * NQ;                        // [Cmax]: partial z (op T)
-  cplx* vecx = vec + a.cmax;                            // [Cmax]: x (op N)
+  cplx* vec = red + (FW ? 4 * 32 * NQ : 0);             // [Cmax]: partial z (op T)
+  cplx* vecx = vec + (OPT ? a.cmax : 0);                // [Cmax]: x (op N)
   __shared__ uint64_t full[kSlotsS], empty[kSlotsS];
   const int ns = gridDim.x, s = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -241,15 +240,36 @@ bool launch_seg(const SegGemv& a, int ns, int nq, size_t smem, cudaStream_t st) 
   }
 }
 
+// shared memory of a launch: ring of SL stages + the op N tree and x (mode 1) and / or the op T
+// partial vector (mode 2); SL = 16, 12 or 8 slots, the largest that fits (0: none fits)
+int seg_slots(int nq, int64_t cmax, int mode, bool small_ring, size_t* smem_out) {
+  const size_t extra = ((mode & 1) ? (size_t)4 * 32 * nq * sizeof(cplx) + (size_t)cmax * sizeof(cplx) : 0) +
+                       ((mode & 2) ? (size_t)cmax * sizeof(cplx) : 0);
+  for (int sl : {16, 12, 8}) {
+    if (small_ring && sl > 8) continue;
+    const size_t smem = (size_t)sl * kStage + extra;
+    if (smem <= 220 * 1024) {
+      *smem_out = smem;
+      return sl;
+    }
+  }
+  return 0;
+}
+
+int seg_nq(int64_t L) {
+  int nq = (int)ceil_div(L, 32);
+  if (nq > 8) nq = nq <= 10 ? 10 : nq <= 12 ? 12 : 16;
+  return nq;
+}
+
 }  // namespace
 
 bool seg_gemv_supported(int64_t R, int64_t C, int nsb) {
   if (R <= 0 || C <= 0 || nsb < 1) return false;
   const int64_t L = ceil_div(R, nsb);
   if (L > 512 || 16 * L > kStage) return false;
-  int nq = (int)ceil_div(L, 32);
-  if (nq > 8) nq = nq <= 10 ? 10 : nq <= 12 ? 12 : 16;
-  return kRingMax + (size_t)4 * 32 * nq * sizeof(cplx) + (size_t)2 * C * sizeof(cplx) <= 220 * 1024;
+  size_t smem = 0;
+  return seg_slots(seg_nq(L), C, 3, false, &smem) > 0;
 }
 
 // mode 1: op N (x -> y); 2: op T (x -> y through partials); 3: both from one pass
@@ -271,19 +291,21 @@ bool launch_seg_gemv_mode(const SegGemv& a0, int mode, cudaStream_t st, bool sma
   if (ns < 1) return false;
   const int64_t L = ceil_div(rmax, ns);
   if (L > 512 || 16 * L > kStage) return false;
-  int nq = (int)ceil_div(L, 32);
-  if (nq > 8) nq = nq <= 10 ? 10 : nq <= 12 ? 12 : 16;
+  const int nq = seg_nq(L);
   a.cmax = cmax;
-  const size_t smem = (small_ring ? kRingMax / 2 : kRingMax) + (size_t)4 * 32 * nq * sizeof(cplx) +
-                      (size_t)2 * cmax * sizeof(cplx);
-  if (smem > 220 * 1024) return false;
+  size_t smem = 0;
+  const int sl = seg_slots(nq, cmax, mode, small_ring, &smem);
+  if (sl == 0) return false;
   if (mode & 2) VSIE_REQUIRE(a.rstride >= cmax && a.partials != nullptr, VSIE_ERR_ARG, "seg_gemv: partial buffer");
-  const bool ok = small_ring ? (mode == 1 ? launch_seg<1, 8>(a, ns, nq, smem, st)
-                                : mode == 2 ? launch_seg<2, 8>(a, ns, nq, smem, st)
-                                            : launch_seg<3, 8>(a, ns, nq, smem, st))
-                             : (mode == 1 ? launch_seg<1, 16>(a, ns, nq, smem, st)
-                                : mode == 2 ? launch_seg<2, 16>(a, ns, nq, smem, st)
-                                            : launch_seg<3, 16>(a, ns, nq, smem, st));
+  bool ok = false;
+  switch (sl * 4 + mode) {
+#define VSIE_SEGL(SL, M) \
+  case SL * 4 + M: ok = launch_seg<M, SL>(a, ns, nq, smem, st); break;
+    VSIE_SEGL(8, 1) VSIE_SEGL(8, 2) VSIE_SEGL(8, 3) VSIE_SEGL(12, 1) VSIE_SEGL(12, 2) VSIE_SEGL(12, 3)
+    VSIE_SEGL(16, 1) VSIE_SEGL(16, 2) VSIE_SEGL(16, 3)
+#undef VSIE_SEGL
+    default: break;
+  }
   if (!ok) return false;
   VSIE_CHECK_LAUNCH();
   if (mode & 2) {

@@ -1,8 +1,10 @@
-// TT-core contraction kernels of the Z_bc apply.
+// TT-core contraction kernels of the Z_bc apply: the per-chi chain
+// kernels (the single-RHS streaming steps normally run as the batched TMA passes of
+// pairg4.cu / segemv.cu, see apply.cu).
 //
 // Forward (Eq. 17), per chi:
-//   y4 = G4 x            -> k_gemv_n   (r3 x m GEMV, HBM stream of G4)
-//   Y3 = G3 y4           -> k_gemv_n   ((r2 n3) x r3 GEMV, HBM stream of G3)
+//   y4 = G4 x            -> k_gemv_n_cp (r3 x m GEMV, HBM stream of G4)
+//   Y3 = G3 y4           -> k_gemv_n_cp ((r2 n3) x r3 GEMV, HBM stream of G3)
 //   Y2 = G2 Y3           -> zgemm      ((r1 n2) x r2 times r2 x n3)
 //   y  = G1 Y2           -> k_expand_g1 (n1 x r1 times r1 x (n2 n3), coalesced voxel writes)
 // Transpose (Eqs. 18-19), per chi, then summed over chi:
@@ -10,9 +12,8 @@
 //   W2 = G2^T W1         -> zgemm (T)
 //   z3 = G3^T W2         -> k_gemv_t   (column dot products, deterministic split over rows)
 //   z  = sum_chi G4^T z3 -> k_gemv_t   (sum_batch)
-// All split reductions are deterministic: partials are summed in a fixed order
-// by the last-arriving CTA (threadfence + ticket counter), so results are
-// bitwise reproducible run to run.
+// All split reductions are deterministic: partials are summed in a fixed order by a
+// separate sum kernel, so results are bitwise reproducible run to run.
 #include "kernels.cuh"
 #include "dmma_tile.cuh"
 
@@ -37,69 +38,6 @@ __device__ __forceinline__ cplx ld_stream(const cplx* p) {
   cplx v;
   asm volatile("ld.global.cs.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
   return v;
-}
-
-// y[r] = sum_c A[r + R c] x[c] (A column-major, HBM-streamed once).  A CTA owns a row
-// tile of blockDim.x rows (blockDim = R rounded up to a warp multiple when R <= 512, so
-// a column of a short G4 is read by exactly one CTA row-tile) and a column range of
-// its split; thread t owns row t of the tile and keeps U independent 16-B streaming
-// loads (ld.global.cs) in flight; x values are warp-uniform broadcasts from L1.
-template <int U>
-__global__ void __launch_bounds__(512) k_gemv_n(const __grid_constant__ GemvN a, cplx* __restrict__ partials,
-                                                int64_t rmax) {
-  pdl_wait();
-  const int b = blockIdx.z;
-  const int64_t R = a.R[b], C = a.C[b];
-  const int64_t LD = a.lda[b] ? a.lda[b] : R;
-  const int64_t row = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
-  const bool act = row < R;
-  const int nsplit = gridDim.x, s = blockIdx.x;
-  const int64_t c0 = C * s / nsplit, c1 = C * (s + 1) / nsplit;
-  const cplx* __restrict__ X = a.x[b];
-  const cplx* __restrict__ p = a.A[b] + (act ? row : R - 1);  // inactive lanes re-read a valid row
-  cplx acc = cmk(0, 0), acc2 = cmk(0, 0);
-  int64_t c = c0;
-  // software pipeline: the next batch of U columns is in flight while this one is consumed
-  if (c + U <= c1) {
-    cplx v[U], xv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      v[u] = ld_stream(p + LD * (c + u));
-      xv[u] = __ldg(X + c + u);
-    }
-    c += U;
-    for (; c + U <= c1; c += U) {
-      cplx w[U], xw[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        w[u] = ld_stream(p + LD * (c + u));
-        xw[u] = __ldg(X + c + u);
-      }
-#pragma unroll
-      for (int u = 0; u < U; u += 2) {
-        cfma(acc, v[u], xv[u]);
-        cfma(acc2, v[u + 1], xv[u + 1]);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        v[u] = w[u];
-        xv[u] = xw[u];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; u += 2) {
-      cfma(acc, v[u], xv[u]);
-      cfma(acc2, v[u + 1], xv[u + 1]);
-    }
-  }
-  for (; c < c1; ++c) cfma(acc, __ldcs(p + LD * c), __ldg(X + c));
-  pdl_trigger();
-  acc = cadd(acc, acc2);
-  if (!act) return;
-  if (nsplit == 1)
-    a.y[b][row] = acc;
-  else
-    partials[((int64_t)b * nsplit + s) * rmax + row] = acc;
 }
 
 // cp.async variant: thread t owns row t of its tile and keeps the next S - 1 columns of
@@ -313,79 +251,6 @@ __global__ void __launch_bounds__(kThreads) k_gemv_t(const __grid_constant__ Gem
       else
         partials[((int64_t)bz * nsplit + s) * cmax + c] = v;
     }
-  }
-}
-
-// ----------------------------------------------------------------------------- fused N + T pass
-// Warp w of a CTA takes columns c0 + w + 8 j of its split; lane l holds rows l + 32 q
-// (q < NQ, R <= 32 NQ).  Per column: the transpose dot product with z3 (lane partials,
-// butterfly warp sum -> z[c]) and the forward accumulation acc[q] += A[r, c] x[c] (y4
-// partial of the split).  The next column's NQ streaming loads are in flight while this
-// one is consumed.  Split partials of y4 are reduced by k_sum_partials_warp (fixed order).
-template <int NQ>
-__global__ void __launch_bounds__(kThreads) k_gemv_nt(const __grid_constant__ GemvNT a, cplx* __restrict__ partials,
-                                                      int64_t rstride) {
-  __shared__ cplx red[kWarps][32 * NQ];
-  pdl_wait();
-  const int b = blockIdx.z;
-  const int64_t R = a.R[b], C = a.C[b];
-  const int nsplit = gridDim.x, s = blockIdx.x;
-  const int64_t c0 = C * s / nsplit, c1 = C * (s + 1) / nsplit;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const cplx* __restrict__ A = a.A[b];
-  const cplx* __restrict__ X = a.x[b];
-  cplx* __restrict__ Z = a.z[b];
-  cplx zv[NQ], acc[NQ];
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    const int64_t r = lane + 32 * q;
-    zv[q] = cmk(0, 0);   // inactive rows: zero weight
-    if (r < R) {
-      zv[q] = __ldcg(a.z3[b] + r);
-      if (a.z3b[b]) zv[q] = cadd(zv[q], __ldcg(a.z3b[b] + r));
-    }
-    acc[q] = cmk(0, 0);
-  }
-  // rows past R re-read row R - 1 (zero weight in the dot product, discarded for y4)
-  const int last = (int)(R - 1 - lane);
-  auto row = [&](int q) { return min(32 * q, last) + lane; };
-  int64_t c = c0 + warp;
-  if (c < c1) {
-    cplx v[NQ];
-    const cplx* col = A + R * c;
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) v[q] = ld_stream(col + row(q));
-    for (; c < c1; c += kWarps) {
-      cplx w[NQ];
-      const int64_t cn = c + kWarps < c1 ? c + kWarps : c;
-      const cplx* coln = A + R * cn;
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) w[q] = ld_stream(coln + row(q));
-      const cplx xv = __ldg(X + c);
-      cplx d = cmk(0, 0);
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        cfma(d, v[q], zv[q]);
-        cfma(acc[q], v[q], xv);
-        v[q] = w[q];
-      }
-      d.x = warp_sum(d.x);
-      d.y = warp_sum(d.y);
-      if (lane == 0) Z[c] = d;
-    }
-  }
-  pdl_trigger();
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) red[warp][lane + 32 * q] = acc[q];
-  __syncthreads();
-  for (int r = threadIdx.x; r < R; r += kThreads) {
-    cplx t = red[0][r];
-#pragma unroll
-    for (int ww = 1; ww < kWarps; ++ww) t = cadd(t, red[ww][r]);
-    if (nsplit == 1)
-      a.y4[b][r] = t;
-    else
-      partials[((int64_t)b * nsplit + s) * rstride + r] = t;
   }
 }
 
@@ -664,82 +529,6 @@ __global__ void __launch_bounds__(kThreads) k_sum3(const cplx* __restrict__ in, 
   }
 }
 
-// ----------------------------------------------------------------------------- fused G2 + G1 (forward)
-// Tile = i2 block of B2 (r1 B2 <= 64) x i3 block of 32 planes.  Step A: the (r1 B2) x 32
-// block of Y2 = G2[rows of the i2 block, :] Y3[:, planes] by one 64 x 32 3M-DMMA GEMM
-// tile (dmma_tile.cuh) written to shared memory; step B: the G1 expansion of the tile's
-// B2 x 32 voxel columns straight from that smem block (Y2 never touches HBM).
-constexpr int kG21B3 = 32;
-
-template <int KT>
-__global__ void __launch_bounds__(kG1Threads) k_g21_fwd(const __grid_constant__ G21Args a, int B2) {
-  extern __shared__ __align__(16) unsigned char g21_smem[];
-  tc::GemmSmem& gsm = *reinterpret_cast<tc::GemmSmem*>(g21_smem);
-  cplx* Y2t = reinterpret_cast<cplx*>(g21_smem + ((sizeof(tc::GemmSmem) + 127) / 128) * 128);   // [64 x 32]
-  cplx* Af = Y2t + 64 * kG21B3;                                                                   // G1 fragments
-  const int n1 = a.n1, r1 = a.r1, n2 = a.n2;
-  const int mt = (n1 + 7) / 8;
-  // G1 fragments (a constant core): staged before waiting for the producer of Y3
-  for (int e = threadIdx.x; e < mt * KT * 32; e += kG1Threads) {
-    const int lane = e % 32, ks = (e / 32) % KT, m = e / (32 * KT);
-    const int i1 = 8 * m + (lane >> 2), k = 4 * ks + (lane & 3);
-    Af[e] = (i1 < n1 && k < r1) ? __ldg(a.G1 + i1 + (int64_t)n1 * k) : cmk(0, 0);
-  }
-  pdl_wait();
-  const int nb2 = (n2 + B2 - 1) / B2;
-  const int i2b = (blockIdx.x % nb2) * B2, i3b = (blockIdx.x / nb2) * kG21B3;
-  const int b2 = min(B2, n2 - i2b), b3 = min(kG21B3, a.n3l - i3b);
-  const int64_t M = (int64_t)r1 * b2;
-  // step A: Y2t (M x b3, ld M) = G2[r1 i2b + (0..M), :] Y3[:, i3b + (0..b3)]
-  tc::gemm_tile<tc::FWA, tc::FWB, false>(a.G2 + (int64_t)r1 * i2b, (int64_t)r1 * n2, a.Y3 + (int64_t)a.r2 * i3b, a.r2, M,
-                                         b3, 0, 0, 0, a.r2, gsm, Y2t, M);
-  __syncthreads();
-  pdl_trigger();
-  // step B: columns col = i2l + b2 i3l (Y2 column stride r1 in Y2t)
-  const int ncol = b2 * b3;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, t = lane & 3;
-  for (int c0 = warp * kColsPerWarp; c0 < ncol; c0 += kWarpsG1 * kColsPerWarp) {
-    cplx bf[KT];
-    {
-      const int c = c0 + g;
-#pragma unroll
-      for (int ks = 0; ks < KT; ++ks) {
-        const int k = 4 * ks + t;
-        bf[ks] = (c < ncol && k < r1) ? Y2t[r1 * c + k] : cmk(0, 0);
-      }
-    }
-    int64_t oaddr[2];
-    bool ok[2];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int c = c0 + 2 * t + j;
-      ok[j] = c < ncol;
-      const int i2l = ok[j] ? c % b2 : 0, i3l = ok[j] ? c / b2 : 0;
-      oaddr[j] = (int64_t)n1 * ((i2b + i2l) + (int64_t)n2 * (i3b + i3l));
-    }
-    double bsum[KT];
-#pragma unroll
-    for (int ks = 0; ks < KT; ++ks) bsum[ks] = bf[ks].x + bf[ks].y;
-    for (int m = 0; m < mt; ++m) {
-      double p1[2] = {0, 0}, p2[2] = {0, 0}, p3[2] = {0, 0};
-#pragma unroll
-      for (int ks = 0; ks < KT; ++ks) {
-        const cplx av = Af[(m * KT + ks) * 32 + lane];
-        dmma(p1[0], p1[1], av.x, bf[ks].x);
-        dmma(p2[0], p2[1], av.y, bf[ks].y);
-        dmma(p3[0], p3[1], av.x + av.y, bsum[ks]);
-      }
-      const int i1 = 8 * m + g;
-      if (i1 < n1) {
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-          if (ok[j]) __stcs(a.y + oaddr[j] + i1, cmk(p1[j] - p2[j], p3[j] - p1[j] - p2[j]));
-      }
-    }
-  }
-}
-
 int pick_splits(int64_t other_ctas, int64_t len, int min_len, int max_splits, int64_t target) {
   int64_t sp = target / std::max<int64_t>(1, other_ctas);
   sp = std::min<int64_t>(sp, len / std::max(1, min_len));
@@ -797,11 +586,7 @@ void launch_gemv_n(const GemvN& a, cplx* partials, int64_t partials_cap, int max
     cmax = std::max(cmax, a.C[b]);
   }
   if (rmax == 0) return;
-  static const int cp_sel = [] {
-    const char* e = std::getenv("VSIE_GEMV_CP");
-    return e ? std::atoi(e) : 1;
-  }();
-  if (cp_sel) {
+  {
     constexpr int S = 16;
     const int T = rmax <= 320 ? (int)(ceil_div(rmax, 32) * 32) : 256;
     const int64_t rtiles = ceil_div(rmax, T);
@@ -827,87 +612,6 @@ void launch_gemv_n(const GemvN& a, cplx* partials, int64_t partials_cap, int max
     launch_gemv_sum(a, partials, ns, rmax, st);
     return;
   }
-  static const int u_sel = [] {
-    const char* e = std::getenv("VSIE_GEMV_U");
-    return e ? std::atoi(e) : 4;
-  }();
-  const void* fn = u_sel == 2 ? (const void*)k_gemv_n<2> : (u_sel == 8 ? (const void*)k_gemv_n<8> : (const void*)k_gemv_n<4>);
-  // one row tile when R <= 320 (block = R rounded to a warp), else 256-row tiles
-  const int T = rmax <= 320 ? (int)(ceil_div(rmax, 32) * 32) : 256;
-  const int64_t rtiles = ceil_div(rmax, T);
-  // column splits: fill whole waves of resident CTAs (2 waves when a split keeps >= 24
-  // columns, else 1) -- a partial last wave is a straggler tail for the whole kernel
-  const int64_t slots = (int64_t)sm_count() * gemv_occupancy(fn, T);
-  const int64_t per = rtiles * a.nbatch;
-  int64_t nsl = std::max<int64_t>(1, 2 * slots / per);
-  if (cmax / nsl < 24) nsl = std::max<int64_t>(1, slots / per);
-  nsl = std::min<int64_t>(nsl, std::max<int64_t>(1, cmax / 16));
-  int ns = (int)std::min<int64_t>(nsl, max_splits);
-  while (ns > 1 && (int64_t)a.nbatch * ns * rmax > partials_cap) --ns;
-  dim3 grid(ns, (unsigned)rtiles, a.nbatch);
-  if (u_sel == 2)
-    launch_pdl(k_gemv_n<2>, grid, dim3(T), 0, st, a, partials, rmax);
-  else if (u_sel == 8)
-    launch_pdl(k_gemv_n<8>, grid, dim3(T), 0, st, a, partials, rmax);
-  else
-    launch_pdl(k_gemv_n<4>, grid, dim3(T), 0, st, a, partials, rmax);
-  VSIE_CHECK_LAUNCH();
-  if (ns > 1) {
-    SumArgs sa{};
-    sa.nbatch = a.nbatch;
-    for (int b = 0; b < a.nbatch; ++b) {
-      sa.y[b] = a.y[b];
-      sa.n[b] = a.R[b];
-    }
-    if (ns >= 16) {
-      dim3 g2((unsigned)ceil_div(rmax, kThreads / 32), a.nbatch);
-      launch_pdl(k_sum_partials_warp, g2, dim3(kThreads), 0, st, sa, (const cplx*)partials, ns, rmax);
-    } else {
-      dim3 g2((unsigned)ceil_div(rmax, kThreads), a.nbatch);
-      launch_pdl(k_sum_partials, g2, dim3(kThreads), 0, st, sa, (const cplx*)partials, ns, rmax);
-    }
-    VSIE_CHECK_LAUNCH();
-  }
-}
-
-bool launch_gemv_nt(const GemvNT& a, cplx* partials, int64_t partials_cap, cudaStream_t st) {
-  int64_t rmax = 0, cmax = 0;
-  for (int b = 0; b < a.nbatch; ++b) {
-    rmax = std::max(rmax, a.R[b]);
-    cmax = std::max(cmax, a.C[b]);
-  }
-  if (rmax > 320) return false;
-  if (cmax == 0) return true;
-  const int nq = (int)ceil_div(std::max<int64_t>(rmax, 1), 32);
-  // one full wave of resident CTAs, >= 8 columns per warp
-  const void* fn = nq <= 1 ? (const void*)k_gemv_nt<1> : nq == 2 ? (const void*)k_gemv_nt<2> : nq == 3 ? (const void*)k_gemv_nt<3>
-                 : nq == 4 ? (const void*)k_gemv_nt<4> : nq == 5 ? (const void*)k_gemv_nt<5> : nq == 6 ? (const void*)k_gemv_nt<6>
-                 : nq == 7 ? (const void*)k_gemv_nt<7> : nq == 8 ? (const void*)k_gemv_nt<8> : nq == 9 ? (const void*)k_gemv_nt<9>
-                 : (const void*)k_gemv_nt<10>;
-  const int64_t slots = (int64_t)sm_count() * gemv_occupancy(fn, kThreads);
-  int ns = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cmax, 8 * kWarps), slots / a.nbatch));
-  while (ns > 1 && (int64_t)a.nbatch * ns * rmax > partials_cap) --ns;
-  dim3 grid(ns, 1, a.nbatch);
-  switch (nq) {
-#define VSIE_NT(K) \
-  case K: launch_pdl(k_gemv_nt<K>, grid, dim3(kThreads), 0, st, a, partials, rmax); break;
-    VSIE_NT(1) VSIE_NT(2) VSIE_NT(3) VSIE_NT(4) VSIE_NT(5) VSIE_NT(6) VSIE_NT(7) VSIE_NT(8) VSIE_NT(9)
-    default: launch_pdl(k_gemv_nt<10>, grid, dim3(kThreads), 0, st, a, partials, rmax); break;
-#undef VSIE_NT
-  }
-  VSIE_CHECK_LAUNCH();
-  if (ns > 1) {
-    SumArgs sa{};
-    sa.nbatch = a.nbatch;
-    for (int b = 0; b < a.nbatch; ++b) {
-      sa.y[b] = a.y4[b];
-      sa.n[b] = a.R[b];
-    }
-    dim3 g2((unsigned)ceil_div(rmax, kThreads / 32), a.nbatch);
-    launch_pdl(k_sum_partials_warp, g2, dim3(kThreads), 0, st, sa, (const cplx*)partials, ns, rmax);
-    VSIE_CHECK_LAUNCH();
-  }
-  return true;
 }
 
 void launch_sum3(const cplx* in, int64_t chi_stride, int64_t ld_in, int64_t rows, int k, cplx* out, int64_t ld_out,
@@ -962,18 +666,11 @@ void set_smem_attr_once(F* f, bool& done) {
   }
 }
 
-// persistent G1-step grids: 4 resident CTAs of 256 threads per SM over the batch
-// (VSIE_G1_CTAS_PER_SM overrides)
+// persistent G1-step grids: the resident CTAs of every SM over the batch
 int64_t g1_ctas_per_chi(int nbatch, const void* fn, size_t smem, int threads) {
-  static const int per_sm_env = [] {
-    const char* e = std::getenv("VSIE_G1_CTAS_PER_SM");
-    return e ? std::max(1, std::atoi(e)) : 0;
-  }();
-  int occ = per_sm_env;
-  if (!occ) {
-    VSIE_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem));
-    occ = std::max(1, occ);
-  }
+  int occ = 1;
+  VSIE_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem));
+  occ = std::max(1, occ);
   return std::max<int64_t>(1, (int64_t)sm_count() * occ / std::max(1, nbatch));
 }
 
@@ -984,13 +681,9 @@ void launch_expand_g1(const ExpandArgs& a, cudaStream_t st) {
   // DMMA k-steps for 4 KT values of k, exact DFMA for r1 % 4 == 1 more (r1 = 17: 4 + 1
   // instead of 5 padded k-steps, cfg 5 expansion 2.62 -> 2.53 ms per chi); with r1 % 4 == 2
   // (r1 = 10) the padded DMMA step measured faster than two DFMA columns (14.6 vs 15.4 us at
-  // cfg 2), so VSIE_EXPAND_REM: 1 (default) remainder 1 only, 2 remainders 1 and 2, 0 never
-  static const int rem_on = [] {
-    const char* e = std::getenv("VSIE_EXPAND_REM");
-    return e ? std::atoi(e) : 1;
-  }();
+  // cfg 2), so only the remainder 1 takes the DFMA path
   int KT = r1max / 4, REMK = r1max % 4;
-  if (REMK > rem_on || rem_on == 0) {
+  if (REMK > 1) {
     KT = (r1max + 3) / 4;
     REMK = 0;
   }
@@ -1015,31 +708,13 @@ void launch_expand_g1(const ExpandArgs& a, cudaStream_t st) {
 #undef VSIE_EXP
 }
 
-// the TMA-streamed batched reduction (reduce_tma.cu) for batched single-RHS calls, opt-in
-// VSIE_REDUCE_TMA=1: once k_reduce_g1 ran exact DFMA for the r1 % 8 remainder, three
-// concurrent per-chi reductions (15.7 us each) beat the single 63 MB pass (cfg 2 pair
-// 0.1625 vs 0.1640 ms)
-bool reduce_tma_on() {
-  static const int v = [] {
-    const char* e = std::getenv("VSIE_REDUCE_TMA");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v != 0;
-}
-
 void launch_reduce_g1(const ReduceArgs& a, cudaStream_t st) {
-  if (a.nbatch > 1 && reduce_tma_on() && launch_reduce_g1_tma(a, st)) return;
   int r1max = 0;
   for (int b = 0; b < a.nbatch; ++b) r1max = std::max(r1max, a.r1[b]);
   VSIE_REQUIRE(r1max <= 32, VSIE_ERR_ARG, "reduce: r1 > 32 not supported");
-  // DMMA n-tiles for 8 NT values of a, exact DFMA for r1 % 8 <= 2 more (VSIE_REDUCE_REM=0:
-  // pad to whole DMMA tiles)
-  static const int rem_on = [] {
-    const char* e = std::getenv("VSIE_REDUCE_REM");
-    return e ? std::atoi(e) : 1;
-  }();
+  // DMMA n-tiles for 8 NT values of a, exact DFMA for r1 % 8 <= 2 more
   int NT = r1max / 8, REM = r1max % 8;
-  if (REM > 2 || !rem_on) {
+  if (REM > 2) {
     NT = (r1max + 7) / 8;
     REM = 0;
   }
@@ -1060,33 +735,6 @@ void launch_reduce_g1(const ReduceArgs& a, cudaStream_t st) {
   VSIE_RED(2, 2) VSIE_RED(3, 0) VSIE_RED(3, 1) VSIE_RED(3, 2) VSIE_RED(4, 0)
   VSIE_REQUIRE(false, VSIE_ERR_ARG, "reduce: unsupported r1");
 #undef VSIE_RED
-}
-
-bool launch_g21_fwd(const G21Args& a, cudaStream_t st) {
-  if (a.r1 > 32 || a.r1 < 1) return false;
-  const int B2 = std::max(1, std::min(a.n2, 64 / a.r1));
-  const int KT = (a.r1 + 3) / 4;
-  const size_t smem = ((sizeof(tc::GemmSmem) + 127) / 128) * 128 + (size_t)64 * kG21B3 * sizeof(cplx) +
-                      (size_t)((a.n1 + 7) / 8) * KT * 32 * sizeof(cplx);
-  if (smem > 220 * 1024) return false;
-  const int nb2 = (a.n2 + B2 - 1) / B2, nb3 = (a.n3l + kG21B3 - 1) / kG21B3;
-  dim3 grid((unsigned)(nb2 * nb3));
-#define VSIE_G21(K)                                                                                \
-  case K: {                                                                                        \
-    static bool d = false;                                                                         \
-    if (!d) {                                                                                      \
-      VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_g21_fwd<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024)); \
-      d = true;                                                                                    \
-    }                                                                                              \
-    launch_pdl(k_g21_fwd<K>, grid, dim3(kG1Threads), smem, st, a, B2);                             \
-    break;                                                                                         \
-  }
-  switch (KT) {
-    VSIE_G21(1) VSIE_G21(2) VSIE_G21(3) VSIE_G21(4) VSIE_G21(5) VSIE_G21(6) VSIE_G21(7) default: VSIE_G21(8)
-  }
-#undef VSIE_G21
-  VSIE_CHECK_LAUNCH();
-  return true;
 }
 
 }  // namespace vsie

@@ -18,7 +18,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(L, s), s
     assert set(syms) <= set(_lib._SIGS), set(syms) - set(_lib._SIGS)
-    assert L.vsie_abi_version() == 2
+    assert L.vsie_abi_version() == 3
 
 
 def test_status_strings_and_defaults():

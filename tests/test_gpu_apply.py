@@ -163,77 +163,62 @@ def test_tt_eval_matches_oracle(cfg1):
         assert validate.rel_l2(got, ref) <= 1e-13
 
 
-@pytest.mark.parametrize("ci", [1, 2, 4])
-def test_apply_modes_agree(ci):
-    """The three single-RHS schedules (per-chi chains, persistent dataflow kernel, batched
-    kernels) compute the same result (to rounding) for every op; each is bitwise
-    reproducible run to run."""
-    from paper_2206_12409_b200 import Coupling
+def _pair_check(h, tts, cfg, x, u, oracle=True):
+    """apply_pair under every schedule: bitwise reproducible, equal to the separate applies
+    (1e-13) and, with `oracle`, to the oracle TT matvecs (T2, 1e-12), op T and op C."""
     import torch
-    cfg = synth.get_config(ci)
-    r = cfg.ranks_probe
-    ranks = [r, (max(1, r[0] - 1), r[1] + 3, r[2] - 5), (r[0] + 1, max(1, r[1] - 2), r[2] + 7)]
-    tts = rand_tts(cfg, ranks, 60 + ci)
-    h = Coupling.from_cores(grid_of(cfg), cfg.meshes(), cfg.freq, tts, nrhs_max=1)
-    x = _cuda(synth.complex_gaussian(cfg.m, 11))
-    u = _cuda(synth.complex_gaussian(3 * cfg.n_v, 12))
-    out = {}
-    for mode in ("persistent", "chains", "batched"):
-        h.configure(mode=mode)
-        for op, v in (("N", x), ("T", u), ("C", u)):
-            a = h.apply(v, op)
-            b = h.apply(v, op)
-            assert torch.equal(a, b), (mode, op)
-            out[(mode, op)] = a.cpu().numpy()
-    for op, v in (("N", x), ("T", u), ("C", u)):
-        for mode in ("persistent", "batched"):
-            assert validate.rel_l2(out[(mode, op)], out[("chains", op)]) <= 1e-13, (mode, op)
-    if ci == 1:
-        for op, v in (("N", x), ("T", u), ("C", u)):
-            for mode in ("persistent", "chains", "batched"):
-                assert validate.rel_l2(out[(mode, op)], ttmv.apply(tts, v.cpu().numpy(), op)) <= TOL
+    xd, ud = _cuda(x), _cuda(u)
+    ref = {op: ttmv.apply(tts, v, op) for op, v in (("N", x), ("T", u), ("C", u))} if oracle else None
+    sep = {op: h.apply(v, op).cpu().numpy() for op, v in (("N", xd), ("T", ud), ("C", ud))}
+    for sched in ("g4_shared", "g3_shared"):
+        h.configure(pair_schedule=sched)
+        assert h.info()["pair_schedule"] == sched
+        for adj in ("T", "C"):
+            y, z = h.apply_pair(xd, ud, adj)
+            y2, z2 = h.apply_pair(xd, ud, adj)
+            assert torch.equal(y, y2) and torch.equal(z, z2), (sched, adj)
+            y, z = y.cpu().numpy(), z.cpu().numpy()
+            assert validate.rel_l2(y, sep["N"]) <= 1e-13, (sched, adj)
+            assert validate.rel_l2(z, sep[adj]) <= 1e-13, (sched, adj)
+            if oracle:
+                assert validate.rel_l2(y, ref["N"]) <= TOL, (sched, adj)
+                assert validate.rel_l2(z, ref[adj]) <= TOL, (sched, adj)
+    h.configure(pair_schedule="auto")
+    return ref
 
 
-def test_cfg3_full_grid_parity():
-    """Config 3 geometry at full size (200 x 120 x 400 voxels, m = 30000 over two
-    surfaces) with random cores: r3 > 512 exercises the 256-row-tile GEMV path, n1 = 200
-    the long G1 contractions, and every schedule is checked against the oracle (T2)."""
+def test_cfg3_build_ranks_pair_and_applies():
+    """Config 3 geometry at full size (200 x 120 x 400 voxels, m = 30000 over shield + bore)
+    with random cores at the ranks of the cfg 3 TT-cross build (r3 ~ 1500 > 320: the row-band
+    G4 pass and the large-C G3 passes; r1 = 17: the DFMA remainder of the G1 steps).  Single
+    applies N / T / C and the pair under both schedules vs the oracle (T2, 1e-12)."""
     from paper_2206_12409_b200 import Coupling
     cfg = synth.get_config(3)
-    ranks = [(16, 124, 600), (15, 120, 640), (17, 130, 580)]
+    ranks = [(17, 137, 1541), (16, 128, 1482), (18, 131, 1509)]
     tts = rand_tts(cfg, ranks, 303)
     h = Coupling.from_cores(grid_of(cfg), cfg.meshes(), cfg.freq, tts, nrhs_max=1)
+    assert h.info()["pair_schedule"] == "g3_shared"   # |G3| > |G4| at these ranks
     x = synth.complex_gaussian(cfg.m, 31)
     u = synth.complex_gaussian(3 * cfg.n_v, 32)
-    ref = {op: ttmv.apply(tts, v, op) for op, v in (("N", x), ("T", u), ("C", u))}
-    for mode in ("chains", "batched", "persistent"):
-        h.configure(mode=mode)
-        for op, v in (("N", x), ("T", u), ("C", u)):
-            assert validate.rel_l2(h.apply(_cuda(v), op).cpu().numpy(), ref[op]) <= TOL, (mode, op)
+    ref = _pair_check(h, tts, cfg, x, u)
+    for op, v in (("N", x), ("T", u), ("C", u)):
+        assert validate.rel_l2(h.apply(_cuda(v), op).cpu().numpy(), ref[op]) <= TOL, op
 
 
 @pytest.mark.parametrize("ci", [1, 2, 4])
 def test_apply_pair(ci):
     """vsie_coupling_apply_pair (one GMRES coupling matvec: Z x and Z^T u / Z^H u sharing
-    the G4 pass) equals the two separate applies and the oracle; bitwise reproducible."""
+    one pass over G4 or over G3) equals the two separate applies and the oracle; bitwise
+    reproducible; both schedules."""
     from paper_2206_12409_b200 import Coupling
-    import torch
     cfg = synth.get_config(ci)
     r = cfg.ranks_probe
     ranks = [r, (max(1, r[0] - 1), r[1] + 3, r[2] - 5), (r[0] + 1, max(1, r[1] - 2), r[2] + 7)]
     tts = rand_tts(cfg, ranks, 80 + ci)
     h = Coupling.from_cores(grid_of(cfg), cfg.meshes(), cfg.freq, tts, nrhs_max=1)
-    x = _cuda(synth.complex_gaussian(cfg.m, 21))
-    u = _cuda(synth.complex_gaussian(3 * cfg.n_v, 22))
-    for adj in ("T", "C"):
-        y, z = h.apply_pair(x, u, adj)
-        y2, z2 = h.apply_pair(x, u, adj)
-        assert torch.equal(y, y2) and torch.equal(z, z2)
-        assert validate.rel_l2(y.cpu().numpy(), h.apply(x, "N").cpu().numpy()) <= 1e-13
-        assert validate.rel_l2(z.cpu().numpy(), h.apply(u, adj).cpu().numpy()) <= 1e-13
-        if ci == 1:
-            assert validate.rel_l2(y.cpu().numpy(), ttmv.apply(tts, x.cpu().numpy(), "N")) <= TOL
-            assert validate.rel_l2(z.cpu().numpy(), ttmv.apply(tts, u.cpu().numpy(), adj)) <= TOL
+    if ci in (2, 4):
+        assert h.info()["pair_schedule"] == "g4_shared"   # |G4| > |G3| at the head configs
+    _pair_check(h, tts, cfg, synth.complex_gaussian(cfg.m, 21), synth.complex_gaussian(3 * cfg.n_v, 22))
 
 
 @pytest.mark.parametrize("world", [2, 3])
@@ -245,104 +230,12 @@ def test_apply_pair_loopback(dense1, cfg1, world):
     hp = Coupling.from_cores(grid_of(cfg1), cfg1.meshes(), cfg1.freq, tts, nrhs_max=1, world=world, loopback=1)
     x = _cuda(synth.complex_gaussian(cfg1.m, 41))
     u = _cuda(synth.complex_gaussian(3 * cfg1.n_v, 42))
-    ya, za = h1.apply_pair(x, u, "T")
-    yb, zb = hp.apply_pair(x, u, "T")
-    assert validate.rel_l2(yb.cpu().numpy(), ya.cpu().numpy()) <= 1e-13
-    assert validate.rel_l2(zb.cpu().numpy(), za.cpu().numpy()) <= 1e-13
-    assert validate.rel_l2(ya.cpu().numpy(), ttmv.apply(tts, x.cpu().numpy(), "N")) <= TOL
-
-
-def test_fused_g21_forward(monkeypatch):
-    """The opt-in fused forward tail (Y2 = G2 Y3 and y = G1 Y2 in one kernel, Y2 tiles in
-    shared memory) matches the oracle; run in a subprocess because the switch is read once."""
-    import subprocess, sys, textwrap, os
-    code = textwrap.dedent('''
-        import sys; sys.path.insert(0, "tests")
-        import synth, numpy as np, torch
-        from oracle import ttmv, validate
-        from gpu_common import grid_of, rand_tts
-        from paper_2206_12409_b200 import Coupling
-        for ci in (1, 2):
-            cfg = synth.get_config(ci)
-            tts = rand_tts(cfg, [cfg.ranks_probe] * 3, 90 + ci)
-            h = Coupling.from_cores(grid_of(cfg), cfg.meshes(), cfg.freq, tts, nrhs_max=1)
-            x = synth.complex_gaussian(cfg.m, 5)
-            y = h.apply(torch.from_numpy(x).cuda(), "N").cpu().numpy()
-            assert validate.rel_l2(y, ttmv.apply(tts, x, "N")) <= 1e-12, ci
-        print("fused ok")
-    ''')
-    env = dict(os.environ, VSIE_FUSE_G21="1")
-    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
-                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    assert p.returncode == 0 and "fused ok" in p.stdout, p.stderr[-2000:]
-
-
-_SCHEDULES = [
-    dict(VSIE_PAIR_G4="0"),
-    dict(VSIE_PAIR_G4="2", VSIE_SEG_G3="0"),
-    dict(VSIE_PAIR_G4="2", VSIE_W2_PARTS="1", VSIE_ZGEMM_CLUSTER="1", VSIE_FWD_TAIL_BATCHED="1", VSIE_G2T="0"),
-    dict(VSIE_PAIR_G4="2", VSIE_REDUCE_TMA="1"),
-    dict(VSIE_PAIR_G4="2", VSIE_REDUCE_TMA="1", VSIE_RT_CW="8"),
-    dict(VSIE_PAIR_G4="2", VSIE_G2T="0", VSIE_ADJ_FUSED="0"),
-    dict(VSIE_PAIR_G4="2", VSIE_G2N="1"),
-    dict(VSIE_PAIR_G4="2", VSIE_ADJ_FUSED="1"),
-    dict(VSIE_PAIR_G4="3"),
-    dict(VSIE_PAIR_G4="4"),
-    dict(VSIE_PAIR_G4="4", VSIE_W2_PARTS="1", VSIE_REDUCE_TMA="1"),
-    dict(VSIE_PAIR_G4="5"),
-    dict(VSIE_PAIR_G4="2", VSIE_SINGLE_TMA="0", VSIE_G2T="0"),
-    dict(VSIE_PAIR_G4="0", VSIE_REDUCE_REM="0", VSIE_EXPAND_REM="0"),
-    dict(VSIE_PAIR_G4="2", VSIE_EXPAND_REM="2"),
-    dict(VSIE_PAIR_G4="2", VSIE_FWD_CHAIN_SEG="0"),
-    dict(VSIE_PAIR_G4="2", VSIE_G4_CHAIN="1"),
-    dict(VSIE_PAIR_G4="2", VSIE_FWD_CHAIN_SEG="1", VSIE_ADJ_CHAIN_SEG="1", VSIE_G2T_CHAIN="1"),
-]
-
-
-@pytest.mark.parametrize("env", _SCHEDULES, ids=lambda e: ",".join(f"{k[5:]}={v}" for k, v in e.items()))
-def test_pair_schedules(env):
-    """Every GMRES-pair schedule (VSIE_PAIR_G4: 0 per-chi k_gemv_nt chains, 2 batched TMA G4
-    pass with (VSIE_SEG_G3=1) or without the batched TMA G3 steps, 3 six concurrent chains,
-    4 every step one batched launch, 5 streaming passes beside the other direction's chains;
-    VSIE_W2_PARTS=1 leaves the G2^T split-K partials to the
-    G3^T kernel; VSIE_ZGEMM_CLUSTER=0 split-K through global partials instead of the cluster /
-    DSMEM reduction; VSIE_ADJ_FUSED=1 the fused G1^T + G2^T kernel k_adj12; VSIE_REDUCE_TMA=1
-    the batched TMA-streamed G1^T instead of the per-chi k_reduce_g1; VSIE_FWD_TAIL_BATCHED=1
-    the forward's G2 / G1 steps as batched launches; VSIE_G2T=0 the split-K ZGEMM for G2^T
-    instead of k_g2t; VSIE_G2N=1 the batched k_g2n for the forward G2 step instead of
-    the per-chi ZGEMMs; VSIE_FWD_CHAIN_SEG / VSIE_ADJ_CHAIN_SEG / VSIE_G4_CHAIN the G3 / G4 passes per
-    chi in the chains (small rings); VSIE_SINGLE_TMA=0 the per-chi GEMV chains in the single applies)
-    equals the oracle matvecs and the separate applies,
-    at cfg 1 (ragged ranks) and cfg 2 (several tiles, 148-CTA row blocks); op T and op C.
-    Subprocess: the switches are read once per process."""
-    import subprocess, sys, textwrap, os
-    code = textwrap.dedent('''
-        import sys; sys.path.insert(0, "tests")
-        import synth, numpy as np, torch
-        from oracle import ttmv, validate
-        from gpu_common import grid_of, rand_tts
-        from paper_2206_12409_b200 import Coupling
-        for ci in (1, 2):
-            cfg = synth.get_config(ci)
-            r = cfg.ranks_probe
-            tts = rand_tts(cfg, [r, (r[0] + 1, r[1] - 3, r[2] + 5), (max(1, r[0] - 1), r[1] + 2, r[2] - 7)], 700 + ci)
-            h = Coupling.from_cores(grid_of(cfg), cfg.meshes(), cfg.freq, tts, nrhs_max=1)
-            x = synth.complex_gaussian(cfg.m, 51)
-            u = synth.complex_gaussian(3 * cfg.n_v, 52)
-            xd, ud = torch.from_numpy(x).cuda(), torch.from_numpy(u).cuda()
-            for adj in ("T", "C"):
-                y, z = h.apply_pair(xd, ud, adj)
-                y2, z2 = h.apply_pair(xd, ud, adj)
-                assert torch.equal(y, y2) and torch.equal(z, z2), "not reproducible"
-                y, z = y.cpu().numpy(), z.cpu().numpy()
-                assert validate.rel_l2(y, h.apply(xd, "N").cpu().numpy()) <= 1e-13, (ci, adj)
-                assert validate.rel_l2(z, h.apply(ud, adj).cpu().numpy()) <= 1e-13, (ci, adj)
-                if ci == 1 or adj == "T":
-                    assert validate.rel_l2(y, ttmv.apply(tts, x, "N")) <= 1e-12, (ci, adj)
-                    assert validate.rel_l2(z, ttmv.apply(tts, u, adj)) <= 1e-12, (ci, adj)
-        print("schedule ok")
-    ''')
-    env = dict(os.environ, **env)
-    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
-                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    assert p.returncode == 0 and "schedule ok" in p.stdout, p.stderr[-2000:]
+    for sched in ("g4_shared", "g3_shared"):
+        hp.configure(pair_schedule=sched)
+        for adj in ("T", "C"):
+            ya, za = h1.apply_pair(x, u, adj)
+            yb, zb = hp.apply_pair(x, u, adj)
+            assert validate.rel_l2(yb.cpu().numpy(), ya.cpu().numpy()) <= 1e-13, (sched, adj)
+            assert validate.rel_l2(zb.cpu().numpy(), za.cpu().numpy()) <= 1e-13, (sched, adj)
+            assert validate.rel_l2(ya.cpu().numpy(), ttmv.apply(tts, x.cpu().numpy(), "N")) <= TOL
+            assert validate.rel_l2(za.cpu().numpy(), ttmv.apply(tts, u.cpu().numpy(), adj)) <= TOL
