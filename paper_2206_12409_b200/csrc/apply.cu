@@ -478,26 +478,28 @@ void g3_pass(const Ctx& X, Shard& s, int mode, cudaStream_t st, int chi_only = -
   VSIE_REQUIRE(launch_seg_gemv_mode(g, mode, st, chi_only >= 0), VSIE_ERR_STATE, "G3 pass: unsupported shape");
 }
 
-// W2 = G2^T W1 for the three chi of one shard in one launch (k_g2t, no split-K partials)
-void g2t_pass(const Ctx& X, Shard& s, cudaStream_t st) {
+// W2 = G2^T W1 for the three chi of one shard in one launch (k_g2t, no split-K partials);
+// chi_only >= 0: that chi alone (inside its chain)
+void g2t_pass(const Ctx& X, Shard& s, cudaStream_t st, int chi_only = -1) {
   vsie_coupling_s* h = X.h;
   const int n2 = h->grid.n[1];
   const int64_t n3l = s.n3loc();
   G2tArgs g{};
-  g.nbatch = 3;
+  g.nbatch = chi_only >= 0 ? 1 : 3;
   g.N = (int)n3l;
   int64_t bytes = 0, fl = 0;
-  for (int c = 0; c < 3; ++c) {
-    g.G2[c] = h->G2[c].p;
-    g.W1[c] = s.W1.p + c * X.r1m * n2 * n3l;
-    g.W2[c] = s.W2.p + c * X.r2m * n3l;
-    g.M[c] = (int)X.R(c, 1);
-    g.K[c] = (int)(X.R(c, 0) * n2);
-    g.ldw[c] = (int)X.R(c, 1);
+  for (int i = 0; i < g.nbatch; ++i) {
+    const int c = chi_only >= 0 ? chi_only : i;
+    g.G2[i] = h->G2[c].p;
+    g.W1[i] = s.W1.p + c * X.r1m * n2 * n3l;
+    g.W2[i] = s.W2.p + c * X.r2m * n3l;
+    g.M[i] = (int)X.R(c, 1);
+    g.K[i] = (int)(X.R(c, 0) * n2);
+    g.ldw[i] = (int)X.R(c, 1);
     bytes += 16 * (X.R(c, 0) * n2 * X.R(c, 1) + X.R(c, 1) * n3l + X.R(c, 0) * n2 * n3l);
     fl += 8 * X.R(c, 0) * n2 * X.R(c, 1) * n3l;
   }
-  Scope sc(h, "adj_g2_g2t", bytes, fl, st);
+  Scope sc(h, chi_only >= 0 ? "adj_g2_g2t_chi" : "adj_g2_g2t", bytes, fl, st);
   launch_g2t(g, st);
 }
 
@@ -666,17 +668,20 @@ void pair_dag(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z
     gather_z(h, z, 1, S.main);
     return;
   }
-  // G3-shared: the forward's G4 pass streams while the transpose's G1^T chains compute
+  // G3-shared: the forward's G4 pass streams while the transpose's G1^T / G2^T chains
+  // compute (per chi: chi c's G2^T runs beside chi c + 1's G1^T and the G4 stream)
   fork(h, S);
   for (Shard& s : h->shards) g4_pass(X, s, x, nullptr, false, S.main);
   for (int c = 0; c < 3; ++c) {
     h->scope_chi = c;
-    for (Shard& s : h->shards) adj_g1(X, s, c, u, cj, S.chi[c]);
+    for (Shard& s : h->shards) {
+      adj_g1(X, s, c, u, cj, S.chi[c]);
+      g2t_pass(X, s, S.chi[c], c);
+    }
   }
   h->scope_chi = -1;
   join(h, S);
   if (exchange) combine_r3(h, &Shard::y4, 3 * X.r3stride, S.main);
-  for (Shard& s : h->shards) g2t_pass(X, s, S.main);
   // ONE pass over G3: Y3 = G3 y4 and z3 = G3^T W2
   for (Shard& s : h->shards) g3_pass(X, s, 3, S.main);
   if (exchange) combine_r3(h, &Shard::z3, 3 * X.r3stride, S.main);

@@ -108,6 +108,8 @@ struct SegGemv {
   const cplx* xt[3];
   cplx* yt[3];
   int64_t cmax;       // set by the launcher
+  int nslots;         // set by the launcher: ring slots
+  int64_t stage_elems;  // set by the launcher: complex elements per ring stage
 };
 bool launch_seg_gemv_mode(const SegGemv& a, int mode, cudaStream_t st, bool small_ring = false);
 bool launch_seg_gemv(const SegGemv& a, bool transpose, cudaStream_t st);

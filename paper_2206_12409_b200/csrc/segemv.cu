@@ -24,24 +24,29 @@ using namespace tma;
 
 constexpr int kCW = 8;                      // consumer warps
 constexpr int kSegThreads = 32 * (kCW + 1);
-constexpr int kStage = 10240;
 
 __device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kCW) : "memory"); }
 
 // M: 1 op N (x -> y), 2 op T (xt -> yt through partials), 3 both from ONE pass over the core.
-// SL ring slots (16: 160 KB, one CTA per SM; 8: 80 KB, leaves room beside it for the CTAs of
-// a concurrent compute kernel)
-template <int NQ, int M, int SL>
+// The ring has a.nslots stages of a.stage_elems (whole column segments of the CTA's row
+// block, ~12 KB) chosen by the launcher to fill the shared memory left beside the vectors
+// (<= 16 slots; a chain's per-chi pass uses a small ring so that the neighbouring chain's
+// compute kernels fit beside it on the SMs).
+constexpr int kMaxSlots = 16;
+
+template <int NQ, int M>
 __global__ void __launch_bounds__(kSegThreads, 1) k_seg_gemv(const __grid_constant__ SegGemv a) {
-  constexpr int kSlotsS = SL;
-  constexpr int kRing = SL * kStage;
   constexpr bool FW = (M & 1) != 0, OPT = (M & 2) != 0;
+  const int kSlotsS = a.nslots;
+  const int64_t se = a.stage_elems;
   extern __shared__ __align__(128) unsigned char smem[];
   cplx* ring = reinterpret_cast<cplx*>(smem);
-  cplx* red = reinterpret_cast<cplx*>(smem + kRing);   // [4][32 NQ]      (op N)
-  cplx* vec = red + (FW ? 4 * 32 * NQ : 0);             // [Cmax]: partial z (op T)
-  cplx* vecx = vec + (OPT ? a.cmax : 0);                // [Cmax]: x (op N)
-  __shared__ uint64_t full[kSlotsS], empty[kSlotsS];
+  // [max(Cmax, 4 * 32 NQ)]: the op T partial z (vec) and the op N warp tree (red) share it
+  // (the partial is written out, behind a barrier, before the tree of the same chi)
+  cplx* vec = ring + (size_t)kSlotsS * se;
+  cplx* red = vec;
+  cplx* vecx = vec + (OPT ? max(a.cmax, (int64_t)(FW ? 4 * 32 * NQ : 0)) : 4 * 32 * NQ);   // [Cmax]: x (op N)
+  __shared__ uint64_t full[kMaxSlots], empty[kMaxSlots];
   const int ns = gridDim.x, s = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int r0[3], L[3], seg[3], nst[3], off[3];
@@ -56,7 +61,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_seg_gemv(const __grid_consta
       const int64_t R = a.R[b];
       r0[b] = (int)(R * s / ns);
       L[b] = (int)(R * (s + 1) / ns) - r0[b];
-      seg[b] = L[b] > 0 ? max(1, kStage / (16 * L[b])) : 1;   // column segments per stage
+      seg[b] = L[b] > 0 ? max(1, (int)(se / L[b])) : 1;   // column segments per stage
       nst[b] = L[b] > 0 ? (int)((a.C[b] + seg[b] - 1) / seg[b]) : 0;
       total += nst[b];
     }
@@ -83,7 +88,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_seg_gemv(const __grid_consta
           const int ncol = (int)min((int64_t)seg[b], a.C[b] - cb);
           mbar_expect_tx(&full[slot], sb * ncol);
           // the block's columns cb .. cb + ncol are one contiguous run of the blocked layout
-          bulk_g2s(ring + (size_t)slot * (kStage / 16), a.A[b] + a.C[b] * r0[b] + (int64_t)L[b] * cb, sb * ncol,
+          bulk_g2s(ring + (size_t)slot * se, a.A[b] + a.C[b] * r0[b] + (int64_t)L[b] * cb, sb * ncol,
                    &full[slot]);
         }
       }
@@ -154,7 +159,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_seg_gemv(const __grid_consta
         const int cb = t * seg[b];
         const int ncol = min(seg[b], C - cb);
         mbar_wait(&full[slot], (i / kSlotsS) & 1);
-        const cplx* st = ring + (size_t)slot * (kStage / 16);
+        const cplx* st = ring + (size_t)slot * se;
         if (OPT) {
           for (int j = 0; j < ncol; j += 2) {
             const bool two = j + 1 < ncol;
@@ -220,17 +225,17 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_seg_gemv(const __grid_consta
   pdl_trigger();
 }
 
-template <int M, int SL>
+template <int M>
 bool launch_seg(const SegGemv& a, int ns, int nq, size_t smem, cudaStream_t st) {
   switch (nq) {
 #define VSIE_SEG(K)                                                                                  \
   case K: {                                                                                          \
     static size_t attr = 0;                                                                          \
     if (smem > attr) {                                                                               \
-      VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_seg_gemv<K, M, SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+      VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_seg_gemv<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
       attr = smem;                                                                                   \
     }                                                                                                \
-    launch_pdl(k_seg_gemv<K, M, SL>, dim3(ns), dim3(kSegThreads), smem, st, a);                      \
+    launch_pdl(k_seg_gemv<K, M>, dim3(ns), dim3(kSegThreads), smem, st, a);                          \
     return true;                                                                                     \
   }
     VSIE_SEG(1) VSIE_SEG(2) VSIE_SEG(3) VSIE_SEG(4) VSIE_SEG(5) VSIE_SEG(6) VSIE_SEG(7) VSIE_SEG(8)
@@ -240,20 +245,33 @@ bool launch_seg(const SegGemv& a, int ns, int nq, size_t smem, cudaStream_t st) 
   }
 }
 
-// shared memory of a launch: ring of SL stages + the op N tree and x (mode 1) and / or the op T
-// partial vector (mode 2); SL = 16, 12 or 8 slots, the largest that fits (0: none fits)
-int seg_slots(int nq, int64_t cmax, int mode, bool small_ring, size_t* smem_out) {
-  const size_t extra = ((mode & 1) ? (size_t)4 * 32 * nq * sizeof(cplx) + (size_t)cmax * sizeof(cplx) : 0) +
-                       ((mode & 2) ? (size_t)cmax * sizeof(cplx) : 0);
-  for (int sl : {16, 12, 8}) {
-    if (small_ring && sl > 8) continue;
-    const size_t smem = (size_t)sl * kStage + extra;
-    if (smem <= 220 * 1024) {
-      *smem_out = smem;
-      return sl;
+// ring geometry of a launch: stages of whole column segments (~12 KB), as many slots (<= 16)
+// as fit beside the vectors (op T partial / op N tree, aliased, + op N x); the chains' per-chi
+// passes take an 80 KB ring.  false if not even two slots fit.
+bool seg_geometry(int64_t L, int nq, int64_t cmax, int mode, bool small_ring, int* nslots, int64_t* se,
+                  size_t* smem) {
+  const bool fw = mode & 1, opt = mode & 2;
+  const int64_t vec = opt ? std::max<int64_t>(cmax, fw ? 4 * 32 * nq : 0) : 4 * 32 * nq;
+  const size_t extra = (size_t)(vec + (fw ? cmax : 0)) * sizeof(cplx);
+  if (extra >= 220 * 1024) return false;
+  const size_t budget = small_ring ? 80 * 1024 : 220 * 1024 - extra;
+  // stage i is consumed by warp i % kCW alone, so the slot count is a multiple of kCW (8 or
+  // 16): every slot is then always consumed by the same warp, in order, and no warp can wait
+  // on a slot phase ahead of one another warp has not consumed.  Stages of whole segments,
+  // <= 24 KB; the slot count with more bytes in flight wins (16 on a tie).
+  int64_t n = 0, segb = 0;
+  for (int cand : {16, 8}) {
+    const int64_t sg = std::min<int64_t>((int64_t)(budget / (cand * 16 * L)), std::max<int64_t>(1, 24576 / (16 * L)));
+    if (sg >= 1 && cand * sg > n * segb) {
+      n = cand;
+      segb = sg;
     }
   }
-  return 0;
+  if (n == 0) return false;
+  *se = segb * L;
+  *nslots = (int)n;
+  *smem = (size_t)n * *se * sizeof(cplx) + extra;
+  return *smem <= 220 * 1024;
 }
 
 int seg_nq(int64_t L) {
@@ -267,9 +285,11 @@ int seg_nq(int64_t L) {
 bool seg_gemv_supported(int64_t R, int64_t C, int nsb) {
   if (R <= 0 || C <= 0 || nsb < 1) return false;
   const int64_t L = ceil_div(R, nsb);
-  if (L > 512 || 16 * L > kStage) return false;
-  size_t smem = 0;
-  return seg_slots(seg_nq(L), C, 3, false, &smem) > 0;
+  if (L > 512) return false;
+  int ns;
+  int64_t se;
+  size_t smem;
+  return seg_geometry(L, seg_nq(L), C, 3, false, &ns, &se, &smem);
 }
 
 // mode 1: op N (x -> y); 2: op T (x -> y through partials); 3: both from one pass
@@ -290,22 +310,15 @@ bool launch_seg_gemv_mode(const SegGemv& a0, int mode, cudaStream_t st, bool sma
   const int ns = a.nsb;
   if (ns < 1) return false;
   const int64_t L = ceil_div(rmax, ns);
-  if (L > 512 || 16 * L > kStage) return false;
+  if (L > 512) return false;
   const int nq = seg_nq(L);
   a.cmax = cmax;
   size_t smem = 0;
-  const int sl = seg_slots(nq, cmax, mode, small_ring, &smem);
-  if (sl == 0) return false;
+  if (!seg_geometry(L, nq, cmax, mode, small_ring, &a.nslots, &a.stage_elems, &smem)) return false;
   if (mode & 2) VSIE_REQUIRE(a.rstride >= cmax && a.partials != nullptr, VSIE_ERR_ARG, "seg_gemv: partial buffer");
-  bool ok = false;
-  switch (sl * 4 + mode) {
-#define VSIE_SEGL(SL, M) \
-  case SL * 4 + M: ok = launch_seg<M, SL>(a, ns, nq, smem, st); break;
-    VSIE_SEGL(8, 1) VSIE_SEGL(8, 2) VSIE_SEGL(8, 3) VSIE_SEGL(12, 1) VSIE_SEGL(12, 2) VSIE_SEGL(12, 3)
-    VSIE_SEGL(16, 1) VSIE_SEGL(16, 2) VSIE_SEGL(16, 3)
-#undef VSIE_SEGL
-    default: break;
-  }
+  const bool ok = mode == 1 ? launch_seg<1>(a, ns, nq, smem, st)
+                  : mode == 2 ? launch_seg<2>(a, ns, nq, smem, st)
+                              : launch_seg<3>(a, ns, nq, smem, st);
   if (!ok) return false;
   VSIE_CHECK_LAUNCH();
   if (mode & 2) {
