@@ -542,7 +542,10 @@ void fwd_after_y4(const Ctx& X, cplx* y, const Streams& S) {
   join(h, S);
 }
 
-// the transpose's front up to W2: G1^T per chi in the chains, then one batched G2^T
+// the transpose's front up to W2: G1^T per chi in the chains, then one batched G2^T.  (One
+// batched TMA-streamed G1^T launch -- a 1-D per-column-copy ring, a 2-D tensor-TMA ring with
+// 52- and 100-row boxes, a per-warp cp.async pipeline -- measured slower than the three
+// concurrent k_reduce_g1 chains at cfgs 2 / 4 and within 1% at cfg 3.)
 void adj_front_w2(const Ctx& X, const cplx* u, bool cj, const Streams& S) {
   vsie_coupling_s* h = X.h;
   fork(h, S);

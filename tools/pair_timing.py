@@ -1,7 +1,7 @@
 """Dev tool: time the GMRES coupling pair (vsie_coupling_apply_pair) at a config's recorded
 ranks with random cores, under two L2 flush styles, plus the serialised per-kernel times.
 
-    VSIE_PAIR_G4=0|2 python tools/pair_timing.py [cfg] [steps]
+    python tools/pair_timing.py [cfg] [steps] [pair_schedule]
 """
 import json, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -17,6 +17,8 @@ steps = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 cfg = synth.get_config(ci)
 ranks = json.load(open(os.path.join(ROOT, "profiles", f"ranks_cfg{ci}.json")))["ranks"]
 h = Coupling.from_cores(grid_of(cfg), cfg.meshes(), cfg.freq, rand_tts(cfg, ranks, 1), nrhs_max=1)
+if len(sys.argv) > 3:
+    h.configure(pair_schedule=sys.argv[3])
 x = torch.from_numpy(synth.complex_gaussian(cfg.m, 1)).cuda()
 u = torch.from_numpy(synth.complex_gaussian(3 * cfg.n_v, 2)).cuda()
 y = torch.empty(3 * cfg.n_v, dtype=torch.complex128, device="cuda")
@@ -38,7 +40,8 @@ def flush(style, i):
         fl2.sum(dtype=torch.int64)   # read pass: the dirty lines of the write are written back here
 
 
-out = {"cfg": ci, "ranks": ranks, "mode": os.environ.get("VSIE_PAIR_G4", "default")}
+out = {"cfg": ci, "ranks": ranks, "schedule": h.info()["pair_schedule"],
+       "env": {k: v for k, v in os.environ.items() if k.startswith("VSIE_")}}
 for _ in range(5):
     step()
 torch.cuda.synchronize()

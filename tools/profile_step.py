@@ -1,5 +1,7 @@
-"""One GMRES step (fwd + transpose apply) on cfg cores with the measured ranks
-(random values: matvec cost is data independent), for ncu captures."""
+"""GMRES coupling pair steps (vsie_coupling_apply_pair) on cfg cores with the measured ranks
+(random values: matvec cost is data independent), for ncu captures.
+
+    python tools/profile_step.py [cfg] [steps] [pair_schedule: auto | g4_shared | g3_shared]"""
 import json, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -13,7 +15,7 @@ cfg = synth.get_config(ci)
 p = os.path.join(ROOT, "profiles", f"ranks_cfg{ci}.json")
 ranks = json.load(open(p))["ranks"] if os.path.exists(p) else [cfg.ranks_probe] * 3
 h = Coupling.from_cores(grid_of(cfg), cfg.meshes(), cfg.freq, rand_tts(cfg, ranks, 1), nrhs_max=1)
-h.configure(mode=os.environ.get("VSIE_MODE", "chains"))
+h.configure(graphs=False, pair_schedule=sys.argv[3] if len(sys.argv) > 3 else "auto")
 x = torch.from_numpy(synth.complex_gaussian(cfg.m, 1)).cuda()
 u = torch.from_numpy(synth.complex_gaussian(3 * cfg.n_v, 2)).cuda()
 y = torch.empty(3 * cfg.n_v, dtype=torch.complex128, device="cuda")
