@@ -43,7 +43,7 @@ uint64_t host_splitmix(uint64_t& s) {
 
 struct Ws {
   DevBuf<cplx> M, J, V, Y, Q, Bh, basis, Bp, Bout, T, Lr, omega, Vr, rowbuf;
-  DevBuf<cplx> G, Rinv, Rt, Rtmp, Ra, Rb, Atmp, zws, other;
+  DevBuf<cplx> G, Rinv, Rt, Rtmp, Ra, Rb, Atmp, zws, other, V1;
   DevBuf<double> norms, frob_partial, frob;
   DevBuf<int> perm, piv_pos, idx, bad;
   DevBuf<ArgMax> partials;
@@ -64,7 +64,7 @@ struct Ctx {
   double t_entry = 0, t_factor = 0, t_maxvol = 0;
   int64_t n_eval = 0;
   int64_t jacobi_sweeps = 0;
-  double t_jsmall = 0, t_jtall = 0, t_gram = 0, t_chol = 0, t_gemm = 0;
+  double t_jsmall = 0, t_chol = 0, t_gemm = 0;
 };
 
 void sync(Ctx& c) { VSIE_CHECK_CUDA(cudaStreamSynchronize(c.st)); }
@@ -191,21 +191,6 @@ void set_identity(Ctx& c, DevBuf<cplx>& V, int q) {
   sync(c);
 }
 
-// Columns below this fraction of ||A||_F are numerical zeros of the Jacobi SVDs.  (A
-// truncation-relative threshold, 1e-2 delta, was tried in round 1 and left the sketch
-// bases non-orthogonal -- held-out errors of 2e-3 at cfg 3 -- so it is 1e-14 again.)
-double trunc_small(const Ctx&) { return 1e-14; }
-
-// noise floor of the range finder's sketch orthonormalisation (VSIE_RF_SMALL overrides
-// the factor 1e-3 of delta; 0 restores the 1e-14 floor of the exact factorisations)
-double rf_small_rel(const Ctx& c) {
-  static const double f = [] {
-    const char* e = std::getenv("VSIE_RF_SMALL");
-    return e ? std::atof(e) : 1e-3;
-  }();
-  return f > 0 ? std::max(1e-14, f * c.delta) : 1e-14;
-}
-
 // Gram-preconditioned one-sided Jacobi SVD of a tall A (p x q): the eigenvectors
 // V1 of G = A^H A (one-sided Jacobi on the q x q Cholesky factor of G + s I; the
 // shift only guards the factorisation, eigenvectors are unchanged) make the
@@ -242,7 +227,6 @@ void precond_jacobi(Ctx& c, cplx* A, int64_t p, int q, cplx* V, double small_rel
     }
     return;
   }
-  c.t_gram += secs(t0);
   t0 = Clock::now();
   launch_add_diag(w.G.p, q, 1e-13 * tr, c.st);
   launch_cholesky_upper(w.G.p, q, w.bad.p, c.st);
@@ -266,8 +250,120 @@ void precond_jacobi(Ctx& c, cplx* A, int64_t p, int q, cplx* V, double small_rel
   set_identity(c, w.Rb, q);
   t0 = Clock::now();
   jacobi(c, A, p, q, w.Rb.p, small_rel);
-  c.t_jtall += secs(t0);
   if (V) zgemm1(c, kN, kN, q, q, q, V1, q, w.Rb.p, q, V, q);
+}
+
+// Rank-revealing SVD of a tall A (p x q) with Jacobi sweeps only over q x q / k x k factors
+// (the randomized range finder of the large supercores: the tall one-sided Jacobi of
+// precond_jacobi was 87% of the round-1 cfg 3 build):
+//   1. R1 = chol(A^H A + s I), s = 11 (p q + q (q + 1)) u ||A||_F^2 (the shift of shifted
+//      CholeskyQR); one-sided Jacobi on R1: R1 V1 = U1 S1, so A^H A = V1 (S1^2 - s I) V1^H;
+//   2. keep the k directions with S1_j^2 - s > floor^2 max (floor = floor_rel, >= 2e-8: the
+//      kept A V1_k has condition <= 1 / floor, inside CholeskyQR2's ~u^{-1/2} range); the
+//      dropped ones are numerical zeros of the rank decision (A's energy there is <= k floor^2
+//      ||A||_2^2 and enters the randomized tail bound of choose_rank as missing mass);
+//   3. CholeskyQR2 of A V1_k (two passes of Gram, Cholesky, A R^{-1}): Q (p x k) orthonormal to
+//      working precision, A V1_k = Q R;
+//   4. want_svd: one-sided Jacobi on R: R V2 = U2 S2; A <- [Q U2 S2, 0], V <- [V1_k V2, V1_drop]
+//      (A = U S V^H with the dropped singular values 0); else A <- [Q, 0] (an orthonormal basis
+//      of A's numerical range, unit column norms).
+// false if a Cholesky factorisation failed (the caller falls back to precond_jacobi).
+bool svd_cholqr(Ctx& c, cplx* A, int64_t p, int q, cplx* V, double floor_rel, bool want_svd) {
+  Ws& w = c.ws;
+  if (q <= 1) return false;
+  const int64_t qq = (int64_t)q * q;
+  w.G.ensure(qq);
+  w.Rinv.ensure(qq);
+  w.Rt.ensure(qq);
+  w.Ra.ensure(qq);
+  w.Rb.ensure(qq);
+  w.Rtmp.ensure(qq);
+  w.Atmp.ensure(p * q);
+  w.frob.ensure(1);
+  w.bad.ensure(1);
+  w.V1.ensure(qq);
+  auto t0 = Clock::now();
+  // 1. shifted Cholesky factor of the Gram matrix and its SVD
+  zgemm1(c, kC, kN, q, q, p, A, p, A, p, w.G.p, q);
+  launch_trace_real(w.G.p, q, w.frob.p, c.st);
+  double tr = 0;
+  VSIE_CHECK_CUDA(cudaMemcpyAsync(&tr, w.frob.p, sizeof(double), cudaMemcpyDeviceToHost, c.st));
+  sync(c);
+  if (!(tr > 0)) return false;
+  const double shift = 11.0 * ((double)p * q + (double)q * (q + 1)) * 1.1102230246251565e-16 * tr;
+  launch_add_diag(w.G.p, q, shift, c.st);
+  VSIE_CHECK_CUDA(cudaMemsetAsync(w.bad.p, 0, sizeof(int), c.st));
+  launch_cholesky_upper(w.G.p, q, w.bad.p, c.st);
+  int bad = 0;
+  VSIE_CHECK_CUDA(cudaMemcpyAsync(&bad, w.bad.p, sizeof(int), cudaMemcpyDeviceToHost, c.st));
+  sync(c);
+  if (bad) return false;
+  c.t_chol += secs(t0);
+  t0 = Clock::now();
+  set_identity(c, w.V1, q);
+  jacobi(c, w.G.p, q, q, w.V1.p);
+  c.t_jsmall += secs(t0);
+  t0 = Clock::now();
+  // 2. numerical rank
+  auto s1 = sorted_norms(c, w.G.p, q, q);
+  std::vector<int> keep, drop;
+  const double lmax = s1[0].first * s1[0].first - shift;
+  for (auto& e : s1) {
+    const double lam = e.first * e.first - shift;
+    (lam > floor_rel * floor_rel * lmax && lam > 0 ? keep : drop).push_back(e.second);
+  }
+  const int k = (int)keep.size();
+  if (k == 0) return false;
+  std::vector<int> order(keep);
+  order.insert(order.end(), drop.begin(), drop.end());
+  upload_idx(c, order);
+  w.Rb.ensure(qq);
+  launch_gather_cols(w.V1.p, q, q, c.ws.idx.p, nullptr, q, w.Rb.p, q, false, c.st);   // [V1_k, V1_drop]
+  // 3. A V1_k -> Atmp (p x k), CholeskyQR2
+  zgemm1(c, kN, kN, p, k, q, A, p, w.Rb.p, q, w.Atmp.p, p);
+  cplx* Qb = w.Atmp.p;
+  cplx* Qn = A;   // A is free now: the second buffer of the passes
+  cplx* R = w.Ra.p;
+  const int64_t kk = (int64_t)k * k;
+  for (int pass = 0; pass < 2; ++pass) {
+    zgemm1(c, kC, kN, k, k, p, Qb, p, Qb, p, w.G.p, k);
+    VSIE_CHECK_CUDA(cudaMemsetAsync(w.bad.p, 0, sizeof(int), c.st));
+    launch_cholesky_upper(w.G.p, k, w.bad.p, c.st);
+    VSIE_CHECK_CUDA(cudaMemcpyAsync(&bad, w.bad.p, sizeof(int), cudaMemcpyDeviceToHost, c.st));
+    sync(c);
+    if (bad) return false;
+    launch_upper_inverse(w.G.p, k, w.Rt.p, w.Rinv.p, c.st);
+    zgemm1(c, kN, kN, p, k, k, Qb, p, w.Rinv.p, k, Qn, p);
+    std::swap(Qb, Qn);
+    if (pass == 0) {
+      VSIE_CHECK_CUDA(cudaMemcpyAsync(R, w.G.p, kk * sizeof(cplx), cudaMemcpyDeviceToDevice, c.st));
+    } else {
+      zgemm1(c, kN, kN, k, k, k, w.G.p, k, R, k, w.Rtmp.p, k);   // R <- R2 R1
+      VSIE_CHECK_CUDA(cudaMemcpyAsync(R, w.Rtmp.p, kk * sizeof(cplx), cudaMemcpyDeviceToDevice, c.st));
+    }
+  }
+  if (Qb != A) VSIE_CHECK_CUDA(cudaMemcpyAsync(A, Qb, p * k * sizeof(cplx), cudaMemcpyDeviceToDevice, c.st));
+  if (q > k) VSIE_CHECK_CUDA(cudaMemsetAsync(A + p * k, 0, p * (q - k) * sizeof(cplx), c.st));
+  sync(c);
+  c.t_chol += secs(t0);
+  if (!want_svd) return true;   // A = [Q, 0]
+  // 4. SVD of R
+  t0 = Clock::now();
+  set_identity(c, w.Rtmp, k);
+  jacobi(c, R, k, k, w.Rtmp.p);   // R <- U2 S2, Rtmp <- V2
+  c.t_jsmall += secs(t0);
+  t0 = Clock::now();
+  zgemm1(c, kN, kN, p, k, k, A, p, R, k, w.Atmp.p, p);   // U S = Q U2 S2
+  VSIE_CHECK_CUDA(cudaMemcpyAsync(A, w.Atmp.p, p * k * sizeof(cplx), cudaMemcpyDeviceToDevice, c.st));
+  if (V) {
+    zgemm1(c, kN, kN, q, k, k, w.Rb.p, q, w.Rtmp.p, k, V, q);   // V_k = V1_k V2
+    if (q > k)
+      VSIE_CHECK_CUDA(cudaMemcpyAsync(V + (int64_t)q * k, w.Rb.p + (int64_t)q * k, (int64_t)q * (q - k) * sizeof(cplx),
+                                      cudaMemcpyDeviceToDevice, c.st));
+  }
+  sync(c);
+  c.t_gemm += secs(t0);
+  return true;
 }
 
 // Rank-revealing factorisation of M (rows x cols, ld rows).
@@ -357,18 +453,21 @@ int factorize(Ctx& c, const cplx* M, int64_t rows, int64_t cols, bool left, int 
       zgemm1(c, kN, kN, rows, kk, cols, M, rows, w.omega.p, cols, w.Y.p, rows);
     else
       zgemm1(c, kC, kN, cols, kk, rows, M, rows, w.omega.p, rows, w.Y.p, cols);
-    // Orthonormal basis of the sketch's dominant range.  Sketch directions whose norm
-    // stays below rf_small ||Y||_F (rf_small = 1e-3 delta) are noise far under the
-    // truncation level: Jacobi leaves them unrotated and they are dropped from Q, so Q
-    // stays orthonormal (every kept pair was rotated to the 1e-12 cosine) and the
-    // dropped energy is <= sqrt(kk) 1e-3 delta relative.  Orthogonalising that noise
-    // among itself cost up to the 40-sweep cap on the doubled sketches.
-    const double rf_small = rf_small_rel(c);
-    precond_jacobi(c, w.Y.p, p1, kk, nullptr, rf_small);
+    // Orthonormal basis Q of the sketch's numerical range (svd_cholqr: directions below
+    // floor of the largest are dropped; precond_jacobi when the cholqr floor would reach
+    // into the truncation level or a factorisation fails)
+    const double floor_rel = 2e-8;
+    const bool cq = floor_rel <= 0.05 * c.delta && svd_cholqr(c, w.Y.p, p1, kk, nullptr, floor_rel, false);
+    if (!cq) {
+      launch_gaussian(w.omega.p, p2 * kk, c.seed ^ (0xABCDEF12345ull + 977 * c.sketch_counter), c.st);
+      if (left)
+        zgemm1(c, kN, kN, rows, kk, cols, M, rows, w.omega.p, cols, w.Y.p, rows);
+      else
+        zgemm1(c, kC, kN, cols, kk, rows, M, rows, w.omega.p, rows, w.Y.p, cols);
+      precond_jacobi(c, w.Y.p, p1, kk, nullptr);
+    }
     auto sy = sorted_norms(c, w.Y.p, p1, kk);
-    double fy2 = 0;
-    for (auto& e : sy) fy2 += e.first * e.first;
-    const double cut = std::max(1e-13 * sy[0].first, 1.0001 * rf_small * std::sqrt(fy2));
+    const double cut = (cq ? 0.5 : 1e-13) * sy[0].first;
     std::vector<int> keep;
     std::vector<double> inv;
     for (auto& e : sy)
@@ -389,12 +488,18 @@ int factorize(Ctx& c, const cplx* M, int64_t rows, int64_t cols, bool left, int 
     else
       zgemm1(c, kN, kN, rows, kq, cols, M, rows, w.Q.p, cols, w.Bh.p, rows);
     w.V.ensure((int64_t)kq * kq);
-    precond_jacobi(c, w.Bh.p, p2, kq, w.V.p);
+    w.J.ensure(p2 * kq);
+    VSIE_CHECK_CUDA(cudaMemcpyAsync(w.J.p, w.Bh.p, p2 * kq * sizeof(cplx), cudaMemcpyDeviceToDevice, c.st));
+    if (!(floor_rel <= 0.05 * c.delta && svd_cholqr(c, w.Bh.p, p2, kq, w.V.p, floor_rel, true))) {
+      VSIE_CHECK_CUDA(cudaMemcpyAsync(w.Bh.p, w.J.p, p2 * kq * sizeof(cplx), cudaMemcpyDeviceToDevice, c.st));
+      precond_jacobi(c, w.Bh.p, p2, kq, w.V.p);
+    }
     auto s = sorted_norms(c, w.Bh.p, p2, kq);
-    const int r = choose_rank(s, total2, true, c.delta, std::min(cap, kq));
-    // grow the sketch only while it is still mostly above the noise floor: once more
-    // than `os` of its directions fell below rf_small, M's range at that level is
-    // already inside Q and a larger sketch adds only noise directions
+    int nnz = 0;   // directions svd_cholqr dropped are exact zeros: never part of a basis
+    for (auto& e : s) nnz += e.first > 0 ? 1 : 0;
+    const int r = choose_rank(s, total2, true, c.delta, std::max(1, std::min({cap, kq, nnz})));
+    // grow the sketch while the rank leaves less than `os` oversampling inside it (a sketch
+    // whose range is exhausted -- kq well below kk -- already holds M's numerical range)
     if (r > kq - os && kq > kk - os && kk < mn) {
       // rank found inside the sketch but with less than `os` oversampling: grow to
       // r + 2 os (a rank drift of a few per sweep no longer doubles a ~300-column sketch,
@@ -711,9 +816,9 @@ int cross_chi(Ctx& c, int chi, Heldout& ho) {
     sync(c);
     const double e = heldout_error(c, s, ho);
     if (c.o.verbose)
-      fprintf(stderr, "[vsie cross] chi %d sweep %d ranks (%d, %d, %d) heldout %.3e  (entry %.2fs factor %.2fs [gram %.2f chol %.2f jsmall %.2f gemm %.2f jtall %.2f] maxvol %.2fs, jacobi sweeps %ld)\n",
-              chi, sweep, s.r[1], s.r[2], s.r[3], e, c.t_entry, c.t_factor, c.t_gram, c.t_chol, c.t_jsmall, c.t_gemm,
-              c.t_jtall, c.t_maxvol, (long)c.jacobi_sweeps);
+      fprintf(stderr, "[vsie cross] chi %d sweep %d ranks (%d, %d, %d) heldout %.3e  (entry %.2fs factor %.2fs [cholqr %.2f jacobi(R) %.2f gemm %.2f] maxvol %.2fs, jacobi sweeps %ld)\n",
+              chi, sweep, s.r[1], s.r[2], s.r[3], e, c.t_entry, c.t_factor, c.t_chol, c.t_jsmall, c.t_gemm,
+              c.t_maxvol, (long)c.jacobi_sweeps);
     if (e < best_e) {
       best_e = e;
       for (int k = 0; k < 5; ++k) best_r[k] = s.r[k];
