@@ -43,7 +43,10 @@ uint64_t host_splitmix(uint64_t& s) {
 
 struct Ws {
   DevBuf<cplx> M, J, V, Y, Q, Bh, basis, Bp, Bout, T, Lr, omega, Vr, rowbuf;
-  DevBuf<cplx> G, Rinv, Rt, Rtmp, Ra, Rb, Atmp, zws, other, V1;
+  DevBuf<cplx> G, Rinv, Rt, Rtmp, Ra, Rb, Atmp, zws, other;
+  DevBuf<cplx> tau, Th, Vh, W, W2, Gv;   // blocked Householder QR (hqr.cu)
+  DevBuf<cplx> Bc, Yraw;                 // conj(B) staging of zgemm_tc; raw sketch M Omega
+  DevBuf<double> hpart;
   DevBuf<double> norms, frob_partial, frob;
   DevBuf<int> perm, piv_pos, idx, bad;
   DevBuf<ArgMax> partials;
@@ -183,6 +186,32 @@ void zgemm1(Ctx& c, Trans ta, Trans tb, int64_t M, int64_t N, int64_t K, const c
   launch_zgemm(z, c.ws.zws.p, (int64_t)c.ws.zws.n, c.st);
 }
 
+// C = op(A) B on the FP64 tensor cores (3M DMMA, linalg.cu) for the large products of the
+// range finder; op(A) = A^H is computed as conj(A^T conj(B)) (conj(B) staged in ws.Bc)
+void zgemm_tc(Ctx& c, Trans ta, int64_t M, int64_t N, int64_t K, const cplx* A, int64_t lda, const cplx* B,
+              int64_t ldb, cplx* C, int64_t ldc) {
+  if (M <= 0 || N <= 0) return;
+  if (!c.ws.zws.p) c.ws.zws.alloc((size_t)16 << 20);
+  const cplx* Bu = B;
+  int64_t ldbu = ldb;
+  if (ta == kC) {
+    c.ws.Bc.ensure(K * N);
+    launch_copy_conj(B, ldb, K, N, c.ws.Bc.p, c.st);
+    Bu = c.ws.Bc.p;
+    ldbu = K;
+  }
+  Zgemm z{};
+  z.nbatch = 1;
+  z.ta = ta == kC ? kT : ta;
+  z.tb = kN;
+  z.M[0] = M; z.N[0] = N; z.K[0] = K;
+  z.A[0] = A; z.lda[0] = lda;
+  z.B[0] = Bu; z.ldb[0] = ldbu;
+  z.C[0] = C; z.ldc[0] = ldc;
+  launch_zgemm_dmma(z, c.ws.zws.p, (int64_t)c.ws.zws.n, c.st);
+  if (ta == kC) launch_conj_2d(C, ldc, M, N, c.st);
+}
+
 void set_identity(Ctx& c, DevBuf<cplx>& V, int q) {
   V.ensure((int64_t)q * q);
   std::vector<cplx> I((size_t)q * q, cmk(0, 0));
@@ -253,117 +282,59 @@ void precond_jacobi(Ctx& c, cplx* A, int64_t p, int q, cplx* V, double small_rel
   if (V) zgemm1(c, kN, kN, q, q, q, V1, q, w.Rb.p, q, V, q);
 }
 
-// Rank-revealing SVD of a tall A (p x q) with Jacobi sweeps only over q x q / k x k factors
-// (the randomized range finder of the large supercores: the tall one-sided Jacobi of
-// precond_jacobi was 87% of the round-1 cfg 3 build):
-//   1. R1 = chol(A^H A + s I), s = 11 (p q + q (q + 1)) u ||A||_F^2 (the shift of shifted
-//      CholeskyQR); one-sided Jacobi on R1: R1 V1 = U1 S1, so A^H A = V1 (S1^2 - s I) V1^H;
-//   2. keep the k directions with S1_j^2 - s > floor^2 max (floor = floor_rel, >= 2e-8: the
-//      kept A V1_k has condition <= 1 / floor, inside CholeskyQR2's ~u^{-1/2} range); the
-//      dropped ones are numerical zeros of the rank decision (A's energy there is <= k floor^2
-//      ||A||_2^2 and enters the randomized tail bound of choose_rank as missing mass);
-//   3. CholeskyQR2 of A V1_k (two passes of Gram, Cholesky, A R^{-1}): Q (p x k) orthonormal to
-//      working precision, A V1_k = Q R;
-//   4. want_svd: one-sided Jacobi on R: R V2 = U2 S2; A <- [Q U2 S2, 0], V <- [V1_k V2, V1_drop]
-//      (A = U S V^H with the dropped singular values 0); else A <- [Q, 0] (an orthonormal basis
-//      of A's numerical range, unit column norms).
-// false if a Cholesky factorisation failed (the caller falls back to precond_jacobi).
-bool svd_cholqr(Ctx& c, cplx* A, int64_t p, int q, cplx* V, double floor_rel, bool want_svd) {
+// SVD of a tall A (p x q) with Jacobi sweeps only over the small q x q factor (the large
+// factorisations of the randomized range finder: the tall one-sided Jacobi of precond_jacobi
+// was 87% of the round-1 cfg 3 build; Gram-based CholeskyQR cannot resolve the singular values
+// near 1e-8 of the largest that the cfg 3 truncation needs):
+//   1. blocked Householder QR A = Q R (hqr.cu; backward stable for any rank / condition);
+//   2. want_svd: one-sided Jacobi on R: R V = U_R S, A <- Q [U_R S; 0] = U S (precond_jacobi's
+//      contract: columns U S, unsorted, V the right singular vectors);
+//      else A <- Q [I; 0] (orthonormal columns spanning A's range).
+void svd_hqr(Ctx& c, cplx* A, int64_t p, int q, cplx* V, bool want_svd) {
   Ws& w = c.ws;
-  if (q <= 1) return false;
   const int64_t qq = (int64_t)q * q;
+  const int pw = hqr_panel_width();
+  w.tau.ensure(q);
+  w.Th.ensure((size_t)hqr_panels(q) * pw * pw);
+  w.Vh.ensure(p * pw);
+  w.W.ensure((int64_t)pw * q);
+  w.W2.ensure((int64_t)pw * q);
+  w.Gv.ensure((int64_t)pw * pw);
+  w.hpart.ensure(hqr_part_doubles());
   w.G.ensure(qq);
-  w.Rinv.ensure(qq);
-  w.Rt.ensure(qq);
-  w.Ra.ensure(qq);
-  w.Rb.ensure(qq);
-  w.Rtmp.ensure(qq);
   w.Atmp.ensure(p * q);
-  w.frob.ensure(1);
-  w.bad.ensure(1);
-  w.V1.ensure(qq);
+  if (!c.ws.zws.p) c.ws.zws.alloc((size_t)16 << 20);
+  const HqrWs hw{w.Vh.p, w.W.p, w.W2.p, w.Gv.p, w.hpart.p, w.zws.p, (int64_t)w.zws.n};
   auto t0 = Clock::now();
-  // 1. shifted Cholesky factor of the Gram matrix and its SVD
-  zgemm1(c, kC, kN, q, q, p, A, p, A, p, w.G.p, q);
-  launch_trace_real(w.G.p, q, w.frob.p, c.st);
-  double tr = 0;
-  VSIE_CHECK_CUDA(cudaMemcpyAsync(&tr, w.frob.p, sizeof(double), cudaMemcpyDeviceToHost, c.st));
-  sync(c);
-  if (!(tr > 0)) return false;
-  const double shift = 11.0 * ((double)p * q + (double)q * (q + 1)) * 1.1102230246251565e-16 * tr;
-  launch_add_diag(w.G.p, q, shift, c.st);
-  VSIE_CHECK_CUDA(cudaMemsetAsync(w.bad.p, 0, sizeof(int), c.st));
-  launch_cholesky_upper(w.G.p, q, w.bad.p, c.st);
-  int bad = 0;
-  VSIE_CHECK_CUDA(cudaMemcpyAsync(&bad, w.bad.p, sizeof(int), cudaMemcpyDeviceToHost, c.st));
-  sync(c);
-  if (bad) return false;
-  c.t_chol += secs(t0);
-  t0 = Clock::now();
-  set_identity(c, w.V1, q);
-  jacobi(c, w.G.p, q, q, w.V1.p);
-  c.t_jsmall += secs(t0);
-  t0 = Clock::now();
-  // 2. numerical rank
-  auto s1 = sorted_norms(c, w.G.p, q, q);
-  std::vector<int> keep, drop;
-  const double lmax = s1[0].first * s1[0].first - shift;
-  for (auto& e : s1) {
-    const double lam = e.first * e.first - shift;
-    (lam > floor_rel * floor_rel * lmax && lam > 0 ? keep : drop).push_back(e.second);
-  }
-  const int k = (int)keep.size();
-  if (k == 0) return false;
-  std::vector<int> order(keep);
-  order.insert(order.end(), drop.begin(), drop.end());
-  upload_idx(c, order);
-  w.Rb.ensure(qq);
-  launch_gather_cols(w.V1.p, q, q, c.ws.idx.p, nullptr, q, w.Rb.p, q, false, c.st);   // [V1_k, V1_drop]
-  // 3. A V1_k -> Atmp (p x k), CholeskyQR2
-  zgemm1(c, kN, kN, p, k, q, A, p, w.Rb.p, q, w.Atmp.p, p);
-  cplx* Qb = w.Atmp.p;
-  cplx* Qn = A;   // A is free now: the second buffer of the passes
-  cplx* R = w.Ra.p;
-  const int64_t kk = (int64_t)k * k;
-  for (int pass = 0; pass < 2; ++pass) {
-    zgemm1(c, kC, kN, k, k, p, Qb, p, Qb, p, w.G.p, k);
-    VSIE_CHECK_CUDA(cudaMemsetAsync(w.bad.p, 0, sizeof(int), c.st));
-    launch_cholesky_upper(w.G.p, k, w.bad.p, c.st);
-    VSIE_CHECK_CUDA(cudaMemcpyAsync(&bad, w.bad.p, sizeof(int), cudaMemcpyDeviceToHost, c.st));
-    sync(c);
-    if (bad) return false;
-    launch_upper_inverse(w.G.p, k, w.Rt.p, w.Rinv.p, c.st);
-    zgemm1(c, kN, kN, p, k, k, Qb, p, w.Rinv.p, k, Qn, p);
-    std::swap(Qb, Qn);
-    if (pass == 0) {
-      VSIE_CHECK_CUDA(cudaMemcpyAsync(R, w.G.p, kk * sizeof(cplx), cudaMemcpyDeviceToDevice, c.st));
-    } else {
-      zgemm1(c, kN, kN, k, k, k, w.G.p, k, R, k, w.Rtmp.p, k);   // R <- R2 R1
-      VSIE_CHECK_CUDA(cudaMemcpyAsync(R, w.Rtmp.p, kk * sizeof(cplx), cudaMemcpyDeviceToDevice, c.st));
-    }
-  }
-  if (Qb != A) VSIE_CHECK_CUDA(cudaMemcpyAsync(A, Qb, p * k * sizeof(cplx), cudaMemcpyDeviceToDevice, c.st));
-  if (q > k) VSIE_CHECK_CUDA(cudaMemsetAsync(A + p * k, 0, p * (q - k) * sizeof(cplx), c.st));
+  hqr_factor(A, p, p, q, w.tau.p, w.Th.p, hw, c.st);
   sync(c);
   c.t_chol += secs(t0);
-  if (!want_svd) return true;   // A = [Q, 0]
-  // 4. SVD of R
-  t0 = Clock::now();
-  set_identity(c, w.Rtmp, k);
-  jacobi(c, R, k, k, w.Rtmp.p);   // R <- U2 S2, Rtmp <- V2
-  c.t_jsmall += secs(t0);
-  t0 = Clock::now();
-  zgemm1(c, kN, kN, p, k, k, A, p, R, k, w.Atmp.p, p);   // U S = Q U2 S2
-  VSIE_CHECK_CUDA(cudaMemcpyAsync(A, w.Atmp.p, p * k * sizeof(cplx), cudaMemcpyDeviceToDevice, c.st));
-  if (V) {
-    zgemm1(c, kN, kN, q, k, k, w.Rb.p, q, w.Rtmp.p, k, V, q);   // V_k = V1_k V2
-    if (q > k)
-      VSIE_CHECK_CUDA(cudaMemcpyAsync(V + (int64_t)q * k, w.Rb.p + (int64_t)q * k, (int64_t)q * (q - k) * sizeof(cplx),
-                                      cudaMemcpyDeviceToDevice, c.st));
+  if (want_svd) {
+    t0 = Clock::now();
+    hqr_copy_r(A, p, q, w.G.p, c.st);
+    set_identity(c, w.Rtmp, q);
+    cplx* Vq = V ? V : w.Rtmp.p;
+    if (V) VSIE_CHECK_CUDA(cudaMemcpyAsync(V, w.Rtmp.p, qq * sizeof(cplx), cudaMemcpyDeviceToDevice, c.st));
+    jacobi(c, w.G.p, q, q, Vq);   // R <- U_R S
+    c.t_jsmall += secs(t0);
+    hqr_fill(w.G.p, q, q, p, q, w.Atmp.p, p, false, c.st);
+  } else {
+    hqr_fill(nullptr, 0, q, p, q, w.Atmp.p, p, true, c.st);
   }
+  t0 = Clock::now();
+  hqr_apply_q(A, p, p, q, w.Th.p, w.Atmp.p, p, q, hw, c.st);
+  VSIE_CHECK_CUDA(cudaMemcpyAsync(A, w.Atmp.p, p * q * sizeof(cplx), cudaMemcpyDeviceToDevice, c.st));
   sync(c);
   c.t_gemm += secs(t0);
-  return true;
+}
+
+// the tall SVD used by the factorisations: Householder + small Jacobi for wide factors,
+// the preconditioned tall Jacobi for q <= 384 (cheap there, and proven since round 1)
+void tall_svd(Ctx& c, cplx* A, int64_t p, int q, cplx* V) {
+  if (q > 384 && p >= q)
+    svd_hqr(c, A, p, q, V, true);
+  else
+    precond_jacobi(c, A, p, q, V);
 }
 
 // Rank-revealing factorisation of M (rows x cols, ld rows).
@@ -444,30 +415,43 @@ int factorize(Ctx& c, const cplx* M, int64_t rows, int64_t cols, bool left, int 
   }
   int kk = (int)std::min<int64_t>(std::max(r_prev, 1) + os, mn);
   const int64_t p1 = left ? rows : cols, p2 = left ? cols : rows;
+  int kk_done = 0;   // columns of the raw sketch already formed (a grown sketch keeps them)
   for (;;) {
-    // Y = M Omega (L->R) or M^H Omega (R->L)
-    w.omega.ensure(p2 * kk);
-    launch_gaussian(w.omega.p, p2 * kk, c.seed ^ (0xABCDEF12345ull + 977 * (++c.sketch_counter)), c.st);
-    w.Y.ensure(p1 * kk);
-    if (left)
-      zgemm1(c, kN, kN, rows, kk, cols, M, rows, w.omega.p, cols, w.Y.p, rows);
-    else
-      zgemm1(c, kC, kN, cols, kk, rows, M, rows, w.omega.p, rows, w.Y.p, cols);
-    // Orthonormal basis Q of the sketch's numerical range (svd_cholqr: directions below
-    // floor of the largest are dropped; precond_jacobi when the cholqr floor would reach
-    // into the truncation level or a factorisation fails)
-    const double floor_rel = 2e-8;
-    const bool cq = floor_rel <= 0.05 * c.delta && svd_cholqr(c, w.Y.p, p1, kk, nullptr, floor_rel, false);
-    if (!cq) {
-      launch_gaussian(w.omega.p, p2 * kk, c.seed ^ (0xABCDEF12345ull + 977 * c.sketch_counter), c.st);
-      if (left)
-        zgemm1(c, kN, kN, rows, kk, cols, M, rows, w.omega.p, cols, w.Y.p, rows);
-      else
-        zgemm1(c, kC, kN, cols, kk, rows, M, rows, w.omega.p, rows, w.Y.p, cols);
-      precond_jacobi(c, w.Y.p, p1, kk, nullptr);
+    // Y = M Omega (L->R) or M^H Omega (R->L) for the new columns [kk_done, kk): a Gaussian Omega
+    // per column block; R->L as conj(M^T Omega) = M^H conj(Omega), an equally Gaussian sketch
+    {
+      const int nn = kk - kk_done;
+      w.omega.ensure(p2 * nn);
+      launch_gaussian(w.omega.p, p2 * nn, c.seed ^ (0xABCDEF12345ull + 977 * (++c.sketch_counter)), c.st);
+      if (kk_done == 0) {
+        w.Yraw.ensure(p1 * (int64_t)std::min<int64_t>(mn, 2 * (int64_t)kk + 4 * os));
+      } else if ((int64_t)w.Yraw.n < p1 * kk) {
+        DevBuf<cplx> grown(p1 * (int64_t)std::min<int64_t>(mn, 2 * (int64_t)kk + 4 * os));
+        VSIE_CHECK_CUDA(cudaMemcpyAsync(grown.p, w.Yraw.p, p1 * kk_done * sizeof(cplx), cudaMemcpyDeviceToDevice, c.st));
+        sync(c);
+        w.Yraw = std::move(grown);
+      }
+      cplx* dst = w.Yraw.p + p1 * kk_done;
+      if (left) {
+        zgemm_tc(c, kN, rows, nn, cols, M, rows, w.omega.p, cols, dst, rows);
+      } else {
+        zgemm_tc(c, kT, cols, nn, rows, M, rows, w.omega.p, rows, dst, cols);
+        launch_conj(dst, p1 * nn, c.st);
+      }
+      kk_done = kk;
     }
+    w.Y.ensure(p1 * kk);
+    VSIE_CHECK_CUDA(cudaMemcpyAsync(w.Y.p, w.Yraw.p, p1 * kk * sizeof(cplx), cudaMemcpyDeviceToDevice, c.st));
+    // Orthonormal basis Q of the sketch's range: Householder QR (unit columns; for a rank-
+    // deficient sketch the extra columns are orthonormal directions with ~zero weight in B
+    // below).  The preconditioned tall Jacobi -- which leaves directions below 1e-3 delta
+    // ||Y||_F unrotated -- measured slower even on the narrow 576k-row sketches of the cfg 3
+    // R->L k = 2 supercore (157 vs 125 s for the cfg 3 build).
+    const bool hq = true;
+    svd_hqr(c, w.Y.p, p1, kk, nullptr, false);   // kk <= mn <= p1
     auto sy = sorted_norms(c, w.Y.p, p1, kk);
-    const double cut = (cq ? 0.5 : 1e-13) * sy[0].first;
+    const double cut = 0.5 * sy[0].first;   // unit columns
+    (void)hq;
     std::vector<int> keep;
     std::vector<double> inv;
     for (auto& e : sy)
@@ -484,18 +468,13 @@ int factorize(Ctx& c, const cplx* M, int64_t rows, int64_t cols, bool left, int 
     // Bh = M^H Q (L->R) or M Q (R->L): p2 x kq
     w.Bh.ensure(p2 * kq);
     if (left)
-      zgemm1(c, kC, kN, cols, kq, rows, M, rows, w.Q.p, rows, w.Bh.p, cols);
+      zgemm_tc(c, kC, cols, kq, rows, M, rows, w.Q.p, rows, w.Bh.p, cols);
     else
-      zgemm1(c, kN, kN, rows, kq, cols, M, rows, w.Q.p, cols, w.Bh.p, rows);
+      zgemm_tc(c, kN, rows, kq, cols, M, rows, w.Q.p, cols, w.Bh.p, rows);
     w.V.ensure((int64_t)kq * kq);
-    w.J.ensure(p2 * kq);
-    VSIE_CHECK_CUDA(cudaMemcpyAsync(w.J.p, w.Bh.p, p2 * kq * sizeof(cplx), cudaMemcpyDeviceToDevice, c.st));
-    if (!(floor_rel <= 0.05 * c.delta && svd_cholqr(c, w.Bh.p, p2, kq, w.V.p, floor_rel, true))) {
-      VSIE_CHECK_CUDA(cudaMemcpyAsync(w.Bh.p, w.J.p, p2 * kq * sizeof(cplx), cudaMemcpyDeviceToDevice, c.st));
-      precond_jacobi(c, w.Bh.p, p2, kq, w.V.p);
-    }
+    tall_svd(c, w.Bh.p, p2, kq, w.V.p);
     auto s = sorted_norms(c, w.Bh.p, p2, kq);
-    int nnz = 0;   // directions svd_cholqr dropped are exact zeros: never part of a basis
+    int nnz = 0;   // exactly zero singular values are never part of a basis
     for (auto& e : s) nnz += e.first > 0 ? 1 : 0;
     const int r = choose_rank(s, total2, true, c.delta, std::max(1, std::min({cap, kq, nnz})));
     // grow the sketch while the rank leaves less than `os` oversampling inside it (a sketch
@@ -892,7 +871,7 @@ void round_chi(Ctx& c, const int n[4], int r[3], DevBuf<cplx> core[4]) {
     w.J.ensure(nb * a);
     launch_transpose(core[k].p, a, nb, w.J.p, false, c.st);  // X = core_k^T: (n_k r_k) x r_{k-1}
     w.V.ensure((int64_t)q * q);
-    precond_jacobi(c, w.J.p, nb, q, w.V.p);
+    tall_svd(c, w.J.p, nb, q, w.V.p);
     auto s = select(w.J.p, nb, q, false, 0);
     const int rp = (int)s.size();
     if (c.o.verbose)
@@ -936,7 +915,7 @@ void round_chi(Ctx& c, const int n[4], int r[3], DevBuf<cplx> core[4]) {
     w.J.ensure(rows * q);
     VSIE_CHECK_CUDA(cudaMemcpyAsync(w.J.p, core[k].p, rows * q * sizeof(cplx), cudaMemcpyDeviceToDevice, c.st));
     w.V.ensure((int64_t)q * q);
-    precond_jacobi(c, w.J.p, rows, q, w.V.p);
+    tall_svd(c, w.J.p, rows, q, w.V.p);
     auto s = nrm2 > 0 ? select(w.J.p, rows, q, true, abs2) : select(w.J.p, rows, q, false, 0);
     const int rp = (int)s.size();
     if (c.o.verbose)

@@ -507,6 +507,20 @@ __global__ void __launch_bounds__(128) k_upper_inverse(const cplx* Rt, int q, cp
   for (int k = threadIdx.x; k < q; k += blockDim.x) X[k + (int64_t)q * c] = xcol[k];
 }
 
+__global__ void k_copy_conj(const cplx* src, int64_t lds, int64_t rows, int64_t cols, cplx* dst) {
+  for (int64_t e = blockIdx.x * (int64_t)NT + threadIdx.x; e < rows * cols; e += (int64_t)gridDim.x * NT) {
+    const int64_t r = e % rows, c = e / rows;
+    dst[e] = cconj(src[r + lds * c]);
+  }
+}
+
+__global__ void k_conj_2d(cplx* C, int64_t ldc, int64_t rows, int64_t cols) {
+  for (int64_t e = blockIdx.x * (int64_t)NT + threadIdx.x; e < rows * cols; e += (int64_t)gridDim.x * NT) {
+    const int64_t r = e % rows, c = e / rows;
+    C[r + ldc * c].y = -C[r + ldc * c].y;
+  }
+}
+
 unsigned grid1(int64_t work) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, NT), 148 * 16)); }
 
 }  // namespace
@@ -582,6 +596,18 @@ void launch_add_diag(cplx* G, int q, double s, cudaStream_t st) {
 
 void launch_trace_real(const cplx* G, int q, double* out, cudaStream_t st) {
   k_trace_real<<<1, NT, 0, st>>>(G, q, out);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_copy_conj(const cplx* src, int64_t lds, int64_t rows, int64_t cols, cplx* dst, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return;
+  k_copy_conj<<<grid1(rows * cols), NT, 0, st>>>(src, lds, rows, cols, dst);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_conj_2d(cplx* C, int64_t ldc, int64_t rows, int64_t cols, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return;
+  k_conj_2d<<<grid1(rows * cols), NT, 0, st>>>(C, ldc, rows, cols);
   VSIE_CHECK_LAUNCH();
 }
 

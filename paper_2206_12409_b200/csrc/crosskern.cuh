@@ -31,6 +31,9 @@ void launch_gather_cols(const cplx* src, int64_t rows, int64_t lds, const int* i
 // dst[i, :] = src[idx[i], :]   (dst nr x cols, ld nr)
 void launch_gather_rows(const cplx* src, int64_t lds, const int* idx, int nr, int64_t cols, cplx* dst,
                         cudaStream_t st);
+// dst (rows x cols, ld rows) = conj(src (ld lds)); conj of C (rows x cols, ld ldc) in place
+void launch_copy_conj(const cplx* src, int64_t lds, int64_t rows, int64_t cols, cplx* dst, cudaStream_t st);
+void launch_conj_2d(cplx* C, int64_t ldc, int64_t rows, int64_t cols, cudaStream_t st);
 // dst (C x R) = op(src (R x C)), op = transpose or conj-transpose
 void launch_transpose(const cplx* src, int64_t R, int64_t C, cplx* dst, bool conj, cudaStream_t st);
 
@@ -45,6 +48,31 @@ void launch_cholesky_upper(cplx* G, int q, int* bad, cudaStream_t st);
 void launch_upper_inverse(const cplx* R, int q, cplx* Rt, cplx* X, cudaStream_t st);
 // sum of the real diagonal of G -> *out (device)
 void launch_trace_real(const cplx* G, int q, double* out, cudaStream_t st);
+
+// ---- blocked Householder QR (hqr.cu) ---------------------------------------------------
+struct HqrWs {
+  cplx* V;          // >= p x panel width
+  cplx* W;          // >= panel width x n (trailing / applied columns)
+  cplx* W2;         // same
+  cplx* Gv;         // >= panel width^2
+  double* part;     // >= hqr_part_doubles()
+  cplx* zws;        // ZGEMM split-K workspace
+  int64_t zws_elems;
+};
+int hqr_panels(int q);
+int hqr_panel_width();
+size_t hqr_part_doubles();
+// A (p x q, ld lda, p >= q) = Q R in place (R upper, reflectors below the diagonal); tau[q];
+// T: hqr_panels(q) panel factors of panel width^2 complex each
+void hqr_factor(cplx* A, int64_t lda, int64_t p, int q, cplx* tau, cplx* T, const HqrWs& w, cudaStream_t st);
+// C (p x n, ld ldc) <- Q C with Q from hqr_factor
+void hqr_apply_q(const cplx* A, int64_t lda, int64_t p, int q, const cplx* T, cplx* C, int64_t ldc, int n,
+                 const HqrWs& w, cudaStream_t st);
+// R (q x q, ld q) <- upper triangle of A (zero below)
+void hqr_copy_r(const cplx* A, int64_t lda, int q, cplx* R, cudaStream_t st);
+// C (p x n) <- [B; 0] (B q x n, ld ldb) or the first n columns of the identity
+void hqr_fill(const cplx* B, int64_t ldb, int q, int64_t p, int n, cplx* C, int64_t ldc, bool identity,
+              cudaStream_t st);
 
 // ---- maxvol -------------------------------------------------------------
 struct ArgMax {
