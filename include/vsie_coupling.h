@@ -260,6 +260,18 @@ int32_t vsie_coupling_apply_pair_pwl(const vsie_coupling_t h[4], const void* x, 
 int32_t vsie_coupling_entries(vsie_coupling_t h, const int64_t* idx, int64_t count, void* out,
                               void* stream);
 
+/* Structured supercore block of the TT-cross (the cross evaluates the
+ * entry function on index sets, not on arbitrary lists): the matrix
+ *   M_k[(a, i_k), (i_{k+1}, b)] = Z_chi(I[a], i_k, i_{k+1}, J[b]),  rows a + n_left i_k, columns
+ *   i_{k+1} + n_{k+1} b,  k = 1, 2, 3, evaluated by the same entry kernel as the build.
+ * left: device int32 [n_left][2] -- k = 1: ignored (n_left = 1), k = 2: (i1, -), k = 3: (i1, i2);
+ * right: device int32 [n_right][2] -- k = 1: (i3, n), k = 2: (n, -), k = 3: ignored (n_right = 1).
+ * out: device complex128, column-major (n_left n_k) x (n_{k+1} n_right).  Entries are the exact
+ * quadrature values (same definition as vsie_coupling_entries).  Errors: VSIE_ERR_ARG for
+ * chi / k out of range, n_left / n_right < 1, NULL pointers. */
+int32_t vsie_coupling_supercore(vsie_coupling_t h, int32_t chi, int32_t k, const int32_t* left, int32_t n_left,
+                                const int32_t* right, int32_t n_right, void* out, void* stream);
+
 /* TT value at (row, col) pairs (Eq. 9 chain product), same
  * layout as vsie_coupling_entries.  world == 1 handles only. */
 int32_t vsie_coupling_tt_eval(vsie_coupling_t h, const int64_t* idx, int64_t count, void* out,

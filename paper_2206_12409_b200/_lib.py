@@ -77,6 +77,8 @@ _SIGS = {
     "vsie_coupling_apply_host": (C.c_int32, [HANDLE, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32]),
     "vsie_coupling_entries": (C.c_int32, [HANDLE, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "vsie_coupling_tt_eval": (C.c_int32, [HANDLE, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "vsie_coupling_supercore": (C.c_int32, [HANDLE, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
+                                            C.c_int32, C.c_void_p, C.c_void_p]),
     "vsie_coupling_info": (C.c_int32, [HANDLE, C.POINTER(vsie_info)]),
     "vsie_coupling_set_timing": (C.c_int32, [HANDLE, C.c_int32]),
     "vsie_coupling_timers": (C.c_int32, [HANDLE, C.POINTER(vsie_timer), C.c_int32, C.POINTER(C.c_int32)]),

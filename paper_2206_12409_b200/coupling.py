@@ -284,6 +284,28 @@ class Coupling:
         """TT values at (rows, cols) (vsie_coupling_tt_eval)."""
         return self._idx_call(lib().vsie_coupling_tt_eval, rows, cols, stream)
 
+    def supercore(self, chi: int, k: int, left=None, right=None, stream=None):
+        """vsie_coupling_supercore: the cross's structured block M_k (column-major
+        (n_left n_k) x (n_{k+1} n_right)) on the device.  left / right: int32 arrays of shape
+        (n, 2) (see the header; None for k = 1 / k = 3)."""
+        torch = _torch()
+        inf = self.info()
+        dims = list(inf["n"]) + [inf["m"]]
+        dev = torch.device("cuda")
+        def prep(a):
+            if a is None:
+                return torch.zeros((1, 2), dtype=torch.int32, device=dev)
+            t = torch.as_tensor(a, dtype=torch.int32).reshape(-1, 2)
+            return t.to(dev).contiguous()
+        L, R = prep(left), prep(right)
+        nl, nr = L.shape[0], R.shape[0]
+        rows, cols = nl * dims[k - 1], dims[k] * nr
+        out = torch.empty((cols, rows), dtype=torch.complex128, device=dev)   # column-major rows x cols
+        check(lib().vsie_coupling_supercore(self._h, int(chi), int(k), C.c_void_p(L.data_ptr()), nl,
+                                            C.c_void_p(R.data_ptr()), nr, C.c_void_p(out.data_ptr()),
+                                            _stream_ptr(stream)))
+        return out.t()
+
     # ------------------------------------------------------------------ timing
     def set_timing(self, enable):
         """0/False off, 1/True serialised per-kernel timing, 2 concurrent timeline (trace())."""

@@ -307,6 +307,34 @@ int32_t vsie_coupling_entries(vsie_coupling_t h, const int64_t* idx, int64_t cou
   });
 }
 
+int32_t vsie_coupling_supercore(vsie_coupling_t h, int32_t chi, int32_t k, const int32_t* left, int32_t n_left,
+                                const int32_t* right, int32_t n_right, void* out, void* stream) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr && out != nullptr, VSIE_ERR_ARG, "handle / out is NULL");
+    VSIE_REQUIRE(chi >= 0 && chi < 3 && k >= 1 && k <= 3, VSIE_ERR_ARG, "chi / k out of range");
+    VSIE_REQUIRE(n_left >= 1 && n_right >= 1, VSIE_ERR_ARG, "n_left / n_right < 1");
+    VSIE_REQUIRE(k == 1 || left != nullptr, VSIE_ERR_ARG, "left is NULL");
+    VSIE_REQUIRE(k == 3 || right != nullptr, VSIE_ERR_ARG, "right is NULL");
+    VSIE_REQUIRE(k != 1 || n_left == 1, VSIE_ERR_ARG, "k = 1 has n_left = 1");
+    VSIE_REQUIRE(k != 3 || n_right == 1, VSIE_ERR_ARG, "k = 3 has n_right = 1");
+    const int64_t dims[4] = {h->grid.n[0], h->grid.n[1], h->grid.n[2], h->m};
+    BlockDesc b{};
+    b.chi = chi;
+    b.k = k;
+    b.rl = n_left;
+    b.nk = dims[k - 1];
+    b.nk1 = dims[k];
+    b.rr = n_right;
+    b.left = left;
+    b.right = right;
+    b.col0 = 0;
+    b.col1 = b.nk1 * b.rr;
+    b.ld = b.rl * b.nk;
+    launch_entries_block(h->eg, b, static_cast<cplx*>(out), static_cast<cudaStream_t>(stream));
+    return VSIE_OK;
+  });
+}
+
 int32_t vsie_coupling_tt_eval(vsie_coupling_t h, const int64_t* idx, int64_t count, void* out, void* stream) {
   return guarded([&] {
     VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "handle is NULL");

@@ -239,3 +239,42 @@ def test_apply_pair_loopback(dense1, cfg1, world):
             assert validate.rel_l2(zb.cpu().numpy(), za.cpu().numpy()) <= 1e-13, (sched, adj)
             assert validate.rel_l2(ya.cpu().numpy(), ttmv.apply(tts, x.cpu().numpy(), "N")) <= TOL
             assert validate.rel_l2(za.cpu().numpy(), ttmv.apply(tts, u.cpu().numpy(), adj)) <= TOL
+
+
+def test_cfg5_block_rhs_64_full_size():
+    """The block workload at its own shape (BASELINE cfg 5: cfg 3 geometry, m = 30000, random
+    cores at the cfg 3 build ranks (17, 137, 1541), nrhs = 64): P31 -- every one of the 64
+    columns of the block N / T / C results equals the single-RHS apply of that column (1e-13,
+    compared on the device) -- and T2 against the oracle's TT matvec for three columns per op
+    (1e-12)."""
+    import torch
+    from paper_2206_12409_b200 import Coupling
+    cfg = synth.get_config(5)
+    k = 64
+    ranks = [(17, 137, 1541), (16, 128, 1482), (18, 131, 1509)]
+    tts = rand_tts(cfg, ranks, 505)
+    h = Coupling.from_cores(grid_of(cfg), cfg.meshes(), cfg.freq, tts, nrhs_max=k)
+    X = synth.complex_gaussian(cfg.m, synth.SEEDS["X"], ncols=k)               # host, m x 64
+    Xt = torch.from_numpy(np.ascontiguousarray(X.T)).cuda()                    # (64, m): column j = Xt[j]
+    g = torch.Generator(device="cuda")
+    g.manual_seed(synth.SEEDS["U"])
+    Ut = torch.view_as_complex(torch.randn((k, 3 * cfg.n_v, 2), generator=g, device="cuda",
+                                           dtype=torch.float64) / np.sqrt(2.0))  # (64, 3 n_v)
+
+    def rel(a, b):
+        return float(torch.linalg.norm(a - b) / torch.linalg.norm(b))
+
+    Y = h.apply(Xt.t(), "N")                      # (3 n_v, 64) view of a (64, 3 n_v) block
+    for j in range(k):                            # P31, forward
+        assert rel(Y[:, j], h.apply(Xt[j], "N")) <= 1e-13, j
+    for j in (0, 37, 63):                         # T2 vs the oracle
+        yj = Y[:, j].cpu().numpy()
+        assert validate.rel_l2(yj, ttmv.apply(tts, X[:, j], "N")) <= TOL, j
+    del Y
+    for op in ("T", "C"):
+        Z = h.apply(Ut.t(), op)                   # (m, 64)
+        for j in range(k):
+            assert rel(Z[:, j], h.apply(Ut[j], op)) <= 1e-13, (op, j)
+        for j in (0, 37, 63):
+            uj = Ut[j].cpu().numpy()
+            assert validate.rel_l2(Z[:, j].cpu().numpy(), ttmv.apply(tts, uj, op)) <= TOL, (op, j)

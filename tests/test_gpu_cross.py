@@ -76,17 +76,27 @@ def test_rank_cap_returns_warning(cfg1):
     assert min(inf["heldout_err"]) > 10 * cfg1.tol
 
 
-@pytest.mark.parametrize("ci", [2])
+@pytest.mark.parametrize("ci", [2, 4, 3])
 def test_heldout_full_size(ci):
-    """P27 / T4: 1000 seeded held-out indices per chi, oracle entries vs TT values."""
+    """P27 / T4 on the full-size configs: 1000 seeded held-out indices per chi (PCG64 seed
+    12409005, independent of the build's own held-out sample), oracle entries vs TT values.
+    cfg 2: values from the exported cores by the oracle's chain product; cfgs 3 / 4 (cores of
+    1-6 GB): the device chain product (vsie_coupling_tt_eval), itself checked against the
+    oracle's on random cores in test_gpu_apply.py.  cfg 3 is the two-surface body config (the
+    r3 ~ 1500 supercores of the Householder-based factorisation)."""
+    import torch
     from paper_2206_12409_b200 import Coupling
     cfg = synth.get_config(ci)
     h = Coupling.build(grid_of(cfg), cfg.meshes(), cfg.freq, cfg.tol, nrhs_max=1)
     assert h.status == 0
-    tts = h.export_cores()
     prob = oent.problem_from_config(cfg)
     s = synth.uniform_indices(tuple(cfg.n) + (cfg.m,), 1000, synth.SEEDS["heldout"])
     v = s[:, 0] + cfg.n[0] * (s[:, 1] + cfg.n[1] * s[:, 2])
+    tts = h.export_cores() if ci == 2 else None
     for chi in range(3):
         ref = oent.entries(prob, chi * cfg.n_v + v, s[:, 3])
-        assert validate.rel_l2(ttmv.eval_at(tts[chi], s), ref) <= 10 * cfg.tol
+        if tts is not None:
+            got = ttmv.eval_at(tts[chi], s)
+        else:
+            got = h.tt_eval(torch.from_numpy(chi * cfg.n_v + v), torch.from_numpy(s[:, 3])).cpu().numpy()
+        assert validate.rel_l2(got, ref) <= 10 * cfg.tol, (ci, chi)

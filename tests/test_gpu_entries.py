@@ -59,3 +59,50 @@ def test_entries_edge_cases(cfg1, prob1):
     hs = Coupling.from_cores(grid_of(cfg1), cfg1.meshes(), cfg1.freq, cores, scale=2.0 - 1.0j)
     got2 = hs.entries([5], [7]).cpu().numpy()
     assert abs(got2[0] - (2 - 1j) * ref[0]) <= 1e-12 * abs(ref[0])
+
+
+def _block_rc(cfg, chi, k, left, right):
+    """Global (row, col) of every element of the column-major supercore M_k:
+    rows a + n_left i_k, columns i_{k+1} + n_{k+1} b."""
+    n1, n2, n3 = cfg.n
+    dims = (n1, n2, n3, cfg.m)
+    nl = 1 if left is None else len(left)
+    nr = 1 if right is None else len(right)
+    R = np.arange(nl * dims[k - 1])
+    Cc = np.arange(dims[k] * nr)
+    rr, cc = np.meshgrid(R, Cc, indexing="ij")          # element (row, col) of M_k
+    a, ik = rr % nl, rr // nl
+    ik1, b = cc % dims[k], cc // dims[k]
+    if k == 1:
+        i1, i2, i3, n = ik, ik1, right[b, 0], right[b, 1]
+    elif k == 2:
+        i1, i2, i3, n = left[a, 0], ik, ik1, right[b, 0]
+    else:
+        i1, i2, i3, n = left[a, 0], left[a, 1], ik, ik1
+    row = chi * cfg.n_v + i1 + n1 * (i2 + n2 * i3)
+    return row.ravel(order="F"), n.ravel(order="F")
+
+
+@pytest.mark.parametrize("ci,chi,k,nl,nr", [(2, 0, 1, 1, 12), (2, 1, 2, 3, 4), (2, 2, 3, 1, 1), (3, 1, 2, 2, 2),
+                                             (1, 2, 3, 8, 1)])
+def test_supercore_block_vs_oracle(ci, chi, k, nl, nr):
+    """Structured-block entry mode (the TT-cross's black box, vsie_coupling_supercore) vs the
+    oracle entries of the same (row, col) pairs, T1 at 1e-12, >= 1e5 entries per block."""
+    cfg = synth.get_config(ci)
+    h = _handle(cfg)
+    prob = oent.problem_from_config(cfg)
+    rng = np.random.default_rng(900 + 10 * ci + k)
+    n1, n2, n3 = cfg.n
+    left = right = None
+    if k == 1:
+        right = np.stack([rng.integers(0, n3, nr), rng.integers(0, cfg.m, nr)], axis=1).astype(np.int32)
+    elif k == 2:
+        left = np.stack([rng.integers(0, n1, nl), np.zeros(nl, int)], axis=1).astype(np.int32)
+        right = np.stack([rng.integers(0, cfg.m, nr), np.zeros(nr, int)], axis=1).astype(np.int32)
+    else:
+        left = np.stack([rng.integers(0, n1, nl), rng.integers(0, n2, nl)], axis=1).astype(np.int32)
+    got = h.supercore(chi, k, left, right).cpu().numpy().ravel(order="F")
+    assert got.size >= 100_000
+    rows, cols = _block_rc(cfg, chi, k, left, right)
+    ok, worst = validate.entry_parity(got, oent.entries(prob, rows, cols), tol=1e-12)
+    assert ok, worst

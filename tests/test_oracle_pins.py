@@ -668,3 +668,43 @@ def test_P41_pwl_moment_is_h_over_12_times_centre_gradient():
     assert by_d[ds[-1]] < 0.5 * (max(h) / ds[-1]) ** 2, errs   # O((h / D)^2)
     for a, b in zip(ds, ds[1:]):
         assert 2.5 < by_d[a] / by_d[b] < 6.0, by_d    # ~4 per doubling of D
+
+
+def test_P42_two_surface_column_order():
+    """SURVEY §8c-L10 (surfaces concatenated in input order, shield then bore) pinned by the
+    geometry itself, not by the GPU: every interior-rule source node of an RWG on a cylinder of
+    radius R with N_az azimuthal cells lies inside the chord polygon band
+    R cos(pi / N_az) <= r_xy <= R and |z| <= L / 2, and the shield (R 0.34, L 1.2) and bore
+    (R 0.40, L 2.0) bands are disjoint -- so the first 14960 columns of cfg 3 are exactly the
+    shield RWGs (N_az (3 N_ax - 1) = 88 x 170) and the last 15040 the bore RWGs (80 x 188).  The
+    combined table also equals the single-surface problems' tables, column for column."""
+    cfg = synth.get_config(3)
+    meshes = cfg.meshes()
+    rs, js = geometry.mesh_sources(meshes)
+    sh, bo = cfg.surfaces
+    ns, nb = sh.n_rwg, bo.n_rwg
+    assert (ns, nb) == (14960, 15040) and rs.shape[0] == ns + nb
+    rad = np.hypot(rs[..., 0], rs[..., 1])
+    for sl, s in ((slice(0, ns), sh), (slice(ns, ns + nb), bo)):
+        r = rad[sl]
+        assert r.max() <= s.radius * (1 + 1e-12)
+        assert r.min() >= s.radius * np.cos(np.pi / s.n_az) * (1 - 1e-12)
+        assert np.abs(rs[sl][..., 2]).max() <= s.length / 2 * (1 + 1e-12)
+    assert sh.radius < bo.radius * np.cos(np.pi / bo.n_az)       # the bands do not overlap
+    for sl, msh in ((slice(0, ns), meshes[0]), (slice(ns, ns + nb), meshes[1])):
+        r1, j1 = geometry.mesh_sources([msh])
+        assert np.array_equal(rs[sl], r1) and np.array_equal(js[sl], j1)
+
+
+def test_P35b_compression_factor_counts_arrays():
+    """The compression factor's numerator / denominator are the element counts of the dense
+    tensor (built by the oracle's dense expansion) and of the core arrays themselves, on a
+    small random TT -- not a retyped formula."""
+    from gpu_common import rand_cores
+    n, m = (3, 4, 5), 6
+    ranks = [(2, 3, 2), (1, 2, 3), (3, 1, 1)]
+    tts = [rand_cores(n + (m,), r, 11 + c) for c, r in enumerate(ranks)]
+    dense = ttmv.full_matrix(tts)
+    assert dense.shape == (3 * 3 * 4 * 5, m)
+    f = validate.compression_factor(n, m, ranks)
+    assert f == Fraction(dense.size, sum(g.size for t in tts for g in t))
