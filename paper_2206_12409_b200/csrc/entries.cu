@@ -20,15 +20,30 @@ namespace {
 // Accumulates sum_{p, s} pw_p [G(r_p - r_s) J_s]_chi (without w, scale); pw_p = 1/(4 pi)
 // times the PWL test function at node p (1 for PWC testing, +-1/(2 sqrt 3) for a linear one)
 // for one voxel centre (cx, cy, cz) and one RWG source record s36.
-template <int CHI>
-__device__ __forceinline__ void entry_acc(const EntryGeom& g, double cx, double cy, double cz,
+//
+// chi is a run-time value selected inside one instruction stream (a warp of list-mode
+// entries holds all three components: templated bodies would run all three).
+//
+// Phase: the 8 voxel nodes of a source node s sit within |d| = |h| / (2 sqrt 3) of the voxel
+// centre, so with R0 = |c - r_s|, k0 R_p = k0 R0 + delta_p, |delta_p| <= k0 |d| (<= 0.016 rad at
+// the 5 mm voxels of cfg 1).  One sincos(k0 R0) per source node and the order-7 Taylor
+// polynomials of cos / sin(delta_p) (truncation <= |delta|^8 / 8! < 1e-19) per pair give
+// exp(-i k0 R_p) by angle addition -- the same value as a sincos per pair to rounding, at
+// ~1/3 of its FP64 instructions (g.taylor; otherwise a sincos per pair).
+__device__ __forceinline__ void entry_acc(const EntryGeom& g, int chi, double cx, double cy, double cz,
                                           const double* __restrict__ s36, double& ar, double& ai) {
 #pragma unroll 1
   for (int q = 0; q < 6; ++q) {
     const double sx = __ldg(s36 + 6 * q + 0), sy = __ldg(s36 + 6 * q + 1), sz = __ldg(s36 + 6 * q + 2);
     const double jx = __ldg(s36 + 6 * q + 3), jy = __ldg(s36 + 6 * q + 4), jz = __ldg(s36 + 6 * q + 5);
-    const double jc = CHI == 0 ? jx : (CHI == 1 ? jy : jz);
+    const double jc = chi == 0 ? jx : (chi == 1 ? jy : jz);
     const double bx = cx - sx, by = cy - sy, bz = cz - sz;
+    double s0 = 0, c0 = 1, kr0 = 0;
+    if (g.taylor) {
+      const double b2 = fma(bx, bx, fma(by, by, bz * bz));
+      kr0 = g.k0 * (b2 * rsqrt(b2));
+      sincos(kr0, &s0, &c0);
+    }
 #pragma unroll
     for (int p = 0; p < 8; ++p) {
       const double rx = (p & 1) ? bx + g.dx : bx - g.dx;
@@ -38,10 +53,19 @@ __device__ __forceinline__ void entry_acc(const EntryGeom& g, double cx, double 
       const double ir = rsqrt(r2);
       const double R = r2 * ir;
       double sn, cs;
-      sincos(g.k0 * R, &sn, &cs);
+      if (g.taylor) {
+        const double dl = fma(g.k0, R, -kr0), d2 = dl * dl;
+        // cos dl = 1 - d2/2 + d2^2/24 - d2^3/720,  sin dl = dl (1 - d2/6 + d2^2/120 - d2^3/5040)
+        const double cd = fma(d2, fma(d2, fma(d2, -1.0 / 720.0, 1.0 / 24.0), -0.5), 1.0);
+        const double sd = dl * fma(d2, fma(d2, fma(d2, -1.0 / 5040.0, 1.0 / 120.0), -1.0 / 6.0), 1.0);
+        cs = fma(c0, cd, -s0 * sd);
+        sn = fma(s0, cd, c0 * sd);
+      } else {
+        sincos(g.k0 * R, &sn, &cs);
+      }
       const double u = g.inv_k0 * ir;
       const double u2 = u * u;
-      const double rc = CHI == 0 ? rx : (CHI == 1 ? ry : rz);
+      const double rc = chi == 0 ? rx : (chi == 1 ? ry : rz);
       const double rj = fma(rx, jx, fma(ry, jy, rz * jz));
       const double t = rj * rc * (ir * ir);                 // Rhat_chi (Rhat . J)
       const double A = fma(1.0 - u2, jc, (3.0 * u2 - 1.0) * t);  // Re(alpha J_chi + beta t)
@@ -59,12 +83,7 @@ __device__ __forceinline__ cplx entry_value(const EntryGeom& g, int chi, int i1,
   const double cx = g.ox + i1 * g.hx, cy = g.oy + i2 * g.hy, cz = g.oz + i3 * g.hz;
   const double* s36 = g.src + 36 * n;
   double ar = 0, ai = 0;
-  if (chi == 0)
-    entry_acc<0>(g, cx, cy, cz, s36, ar, ai);
-  else if (chi == 1)
-    entry_acc<1>(g, cx, cy, cz, s36, ar, ai);
-  else
-    entry_acc<2>(g, cx, cy, cz, s36, ar, ai);
+  entry_acc(g, chi, cx, cy, cz, s36, ar, ai);
   ar *= g.w;
   ai *= g.w;
   return cmk(g.scale_re * ar - g.scale_im * ai, g.scale_re * ai + g.scale_im * ar);

@@ -119,6 +119,8 @@ void handle_init_geometry(vsie_coupling_s* h, const vsie_grid* grid, const vsie_
   }
   g.k0 = h->k0;
   g.inv_k0 = 1.0 / h->k0;
+  // |delta| <= k0 |d|: the order-7 phase polynomial is exact to < 1e-19 while k0 |d| <= 0.03
+  g.taylor = h->k0 * std::sqrt(g.dx * g.dx + g.dy * g.dy + g.dz * g.dz) <= 0.03 ? 1 : 0;
   g.scale_re = h->scale_re;
   g.scale_im = h->scale_im;
   g.src = h->d_src.p;

@@ -14,6 +14,7 @@ struct EntryGeom {
   double w;               // h1 h2 h3 / 8
   double pw[8];           // per-node factor 1/(4 pi) x PWL test function at node p (1 for PWC)
   double k0, inv_k0;
+  int taylor;             // 1: one sincos per source node + order-7 Taylor phase per pair (entries.cu)
   double scale_re, scale_im;
   const double* src;     // [m][36] device
   int64_t m;
