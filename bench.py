@@ -449,12 +449,35 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     ent_s = ne * 5 / (e0.elapsed_time(e1) * 1e-3)
+    # block mode (the TT-cross's structured supercores): a k = 2 block of 16 x 64 index sets
+    brng = np.random.default_rng(5)
+    bl = np.stack([brng.integers(0, cfg.n[0], 16), np.zeros(16, int)], axis=1)
+    br = np.stack([brng.integers(0, cfg.m, 64), np.zeros(64, int)], axis=1)
+    Mb = h.supercore(1, 2, bl, br)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(3):
+        Mb = h.supercore(1, 2, bl, br)
+    e1.record()
+    torch.cuda.synchronize()
+    blk_s = 3 * Mb.numel() / (e0.elapsed_time(e1) * 1e-3)
+    del Mb
 
     if world > 1:
         dist.barrier()
     if rank != 0:
         dist.destroy_process_group()
         return 0
+
+    # ---- FP64 roofline of the entry kernel: measured FP64 instructions per entry x entries/s
+    # over the measured DFMA issue rate (one FP64-pipe thread instruction per FMA)
+    fp64_ops = None
+    ep = os.path.join(ROOT, "profiles", "r02", "ncu_entries.json")
+    if os.path.exists(ep):
+        with open(ep) as f:
+            fp64_ops = float(json.load(f)["captures"][0]["fp64_ops_per_entry"])
+    with open(os.path.join(ROOT, "profiles", "r01", "fp64_peaks.json")) as f:
+        fp64_peak_ops = float(json.load(f)["dfma_tflops"]) * 1e12 / 2.0
 
     # ---- roofline of the dominant kernel (largest share of the step)
     peak, peak_kind = load_peaks()
@@ -538,6 +561,14 @@ def main():
                    "compression": float(inf["compression"]) if inf["compression"] else None},
         "entries": {"value": ent_s, "unit": "entries/s", "pair_interactions_per_s": 48 * ent_s,
                     "sample": "1e6 uniform random (row, col), 5 reps",
+                    "block_entries_per_s": blk_s,
+                    "block_sample": "k = 2 supercore, 16 x 64 index sets (vsie_coupling_supercore), 3 reps",
+                    "fp64_ops_per_entry": fp64_ops,
+                    "fp64_ops_source": "ncu DFMA + DMUL + DADD thread instructions per entry (profiles/r02/ncu_entries.json)",
+                    "fp64_peak_ops_per_s": fp64_peak_ops,
+                    "fp64_peak_source": "measured DFMA rate / 2 (profiles/r01/fp64_peaks.json, tools/microbench/fp64_peaks.cu)",
+                    "fp64_frac": ent_s * fp64_ops / fp64_peak_ops if fp64_ops else None,
+                    "fp64_frac_block": blk_s * fp64_ops / fp64_peak_ops if fp64_ops else None,
                     "structured_blocks_per_s": (inf["entries_evaluated"] / inf["build_entry_s"])
                     if mode == "build" and inf["build_entry_s"] > 0 else None,
                     "structured_note": "supercore blocks evaluated by the TT-cross build (entries / entry-kernel time)"},

@@ -106,6 +106,12 @@ typedef struct {
                           * every voxel node p by (r_p - c)_l / h_l, the linear PWL test
                           * function along axis l.  The q = 12 coupling is the four handles
                           * l = 0..3 (vsie_coupling_apply_pwl).  Out of range: VSIE_ERR_ARG. */
+  const char* ipc_name;  /* world > 1 without loopback: NULL (default) = NCCL (one GPU per rank, the
+                          * nccl_unique_id above); else the ranks are processes sharing ONE GPU and
+                          * combine through CUDA-IPC buffers and a host barrier in the POSIX shared-
+                          * memory segment "/vsie_<ipc_name>" (unique per job, <= 200 chars; the
+                          * segment is unlinked once every rank attached).  A test transport: every
+                          * collective synchronises the stream, so applies run eagerly (no graphs). */
 } vsie_build_opts;
 
 typedef struct {

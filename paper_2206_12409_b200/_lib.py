@@ -32,7 +32,7 @@ class vsie_build_opts(C.Structure):
                 ("seed", C.c_uint64), ("scale_re", C.c_double), ("scale_im", C.c_double),
                 ("rank", C.c_int32), ("world", C.c_int32), ("loopback", C.c_int32),
                 ("nccl_unique_id", C.c_void_p), ("device", C.c_int32), ("verbose", C.c_int32),
-                ("test_moment", C.c_int32)]
+                ("test_moment", C.c_int32), ("ipc_name", C.c_char_p)]
 
 
 class vsie_info(C.Structure):

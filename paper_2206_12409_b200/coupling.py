@@ -57,6 +57,8 @@ def _opts(**kw):
         elif k == "nccl_unique_id":
             keep = C.create_string_buffer(bytes(v), 128)
             o.nccl_unique_id = C.cast(keep, C.c_void_p)
+        elif k == "ipc_name":
+            o.ipc_name = str(v).encode()
         else:
             setattr(o, k, v)
     return o, keep

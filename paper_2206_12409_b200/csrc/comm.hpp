@@ -21,6 +21,9 @@ class Comm {
   virtual void broadcast(void* buf, size_t n_bytes, int root, cudaStream_t st) = 0;
 };
 
+// Several processes on ONE GPU: CUDA-IPC exchange buffers + a host barrier in the POSIX
+// shared-memory segment "/vsie_<name>" (comm_ipc.cu; a test transport for 1-GPU boxes).
+Comm* make_ipc_comm(const char* name, int rank, int world);
 // NCCL communicator; throws Error(VSIE_ERR_NCCL) on failure.
 Comm* make_nccl_comm(const void* unique_id_128, int rank, int world);
 int nccl_unique_id(void* out128);

@@ -127,8 +127,13 @@ void handle_init_geometry(vsie_coupling_s* h, const vsie_grid* grid, const vsie_
   g.m = h->m;
   g.nv = h->grid.nv();
   if (h->world > 1 && !h->loopback) {
-    VSIE_REQUIRE(o->nccl_unique_id != nullptr, VSIE_ERR_ARG, "world > 1 needs nccl_unique_id");
-    h->comm.reset(make_nccl_comm(o->nccl_unique_id, h->rank, h->world));
+    if (o->ipc_name) {
+      VSIE_REQUIRE(std::strlen(o->ipc_name) > 0 && std::strlen(o->ipc_name) <= 200, VSIE_ERR_ARG, "bad ipc_name");
+      h->comm.reset(make_ipc_comm(o->ipc_name, h->rank, h->world));
+    } else {
+      VSIE_REQUIRE(o->nccl_unique_id != nullptr, VSIE_ERR_ARG, "world > 1 needs nccl_unique_id or ipc_name");
+      h->comm.reset(make_nccl_comm(o->nccl_unique_id, h->rank, h->world));
+    }
   }
   handle_partition(h);
 }
