@@ -956,8 +956,6 @@ int tt_round(vsie_coupling_s* h, double tol) {
                "round of a multi-process handle: round the full cores before sharding");
   VSIE_REQUIRE(tol >= 0 && tol < 1, VSIE_ERR_ARG, "tol must be in [0, 1)");
   vsie_build_opts o{};
-  const char* ev = std::getenv("VSIE_ROUND_VERBOSE");
-  o.verbose = ev ? std::atoi(ev) : 0;
   Ctx c{h, o, nullptr, {}, tol, tol / std::sqrt(3.0), 0};
   VSIE_CHECK_CUDA(cudaDeviceSynchronize());
   VSIE_CHECK_CUDA(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking));
@@ -966,9 +964,13 @@ int tt_round(vsie_coupling_s* h, double tol) {
     ~StreamGuard() { cudaStreamDestroy(s); }
   } guard{c.st};
   const int n[4] = {h->grid.n[0], h->grid.n[1], h->grid.n[2], (int)h->m};
+  // round all three chi into new buffers first: the handle keeps its cores (and captured
+  // graphs) untouched if any factorisation throws
+  DevBuf<cplx> rounded[3][4];
+  int rr[3][3];
   for (int chi = 0; chi < 3; ++chi) {
     int r[3] = {h->ranks[chi][0], h->ranks[chi][1], h->ranks[chi][2]};
-    DevBuf<cplx> core[4];
+    DevBuf<cplx>* core = rounded[chi];
     // assemble the full cores (G3 / G4 may be split over loopback shards) on c.st (a
     // non-blocking stream: plain cudaMemcpy D2D would not be ordered before its kernels)
     core[0].alloc((size_t)n[0] * r[0]);
@@ -988,12 +990,23 @@ int tt_round(vsie_coupling_s* h, double tol) {
                                         cudaMemcpyDeviceToDevice, c.st));
     }
     round_chi(c, n, r, core);
-    const cplx* dev[4] = {core[0].p, core[1].p, core[2].p, core[3].p};
     sync(c);
-    handle_set_cores_device(h, chi, r, dev);
-    VSIE_CHECK_CUDA(cudaDeviceSynchronize());
+    for (int k = 0; k < 3; ++k) rr[chi][k] = r[k];
   }
-  handle_alloc_workspace(h);
+  // commit: from here on the old cores are replaced; if an allocation fails the handle is
+  // marked core-less (every apply then fails with VSIE_ERR_STATE) instead of half-updated
+  apply_reset_graphs(h);
+  try {
+    for (int chi = 0; chi < 3; ++chi) {
+      const cplx* dev[4] = {rounded[chi][0].p, rounded[chi][1].p, rounded[chi][2].p, rounded[chi][3].p};
+      handle_set_cores_device(h, chi, rr[chi], dev);
+    }
+    VSIE_CHECK_CUDA(cudaDeviceSynchronize());
+    handle_alloc_workspace(h);
+  } catch (...) {
+    h->has_cores = false;
+    throw;
+  }
   VSIE_CHECK_CUDA(cudaDeviceSynchronize());
   return VSIE_OK;
 }
