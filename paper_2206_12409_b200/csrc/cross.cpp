@@ -11,8 +11,10 @@
 //     cores: L->R  core_k = L L[P]^{-1}, G4 = M_3[P, :]
 //            R->L  core_{k+1} = (R R[Q]^{-1})^T, G1 = M_1[:, Q]
 //   stop when the ranks are unchanged over a sweep and the held-out error <= 10 tol.
-// Multi-process (NCCL): supercore columns are split across ranks, evaluated
-// locally and allgathered; the factorisation is replicated (deterministic).
+// Multi-process (NCCL or the single-GPU IPC transport): supercore ROWS are split across the
+// ranks: each rank evaluates and keeps its row block; the randomized range
+// finder's products and sums run on the blocks (allgather of the sketch rows / allreduce of
+// Q^H M), small factorisations are replicated (deterministic).
 #include "cross.hpp"
 
 #include <algorithm>
@@ -46,6 +48,7 @@ struct Ws {
   DevBuf<cplx> G, Rinv, Rt, Rtmp, Ra, Rb, Atmp, zws, other;
   DevBuf<cplx> tau, Th, Vh, W, W2, Gv;   // blocked Householder QR (hqr.cu)
   DevBuf<cplx> Bc, Yraw;                 // conj(B) staging of zgemm_tc; raw sketch M Omega
+  DevBuf<cplx> gsend, grecv, Mfull, Yloc, Bloc;   // row-split build: allgather staging, assembled blocks
   DevBuf<double> hpart;
   DevBuf<double> norms, frob_partial, frob;
   DevBuf<int> perm, piv_pos, idx, bad;
@@ -68,6 +71,10 @@ struct Ctx {
   int64_t n_eval = 0;
   int64_t jacobi_sweeps = 0;
   double t_jsmall = 0, t_chol = 0, t_gemm = 0;
+  // multi-process build (SURVEY §8e cross step): the supercore's ROWS are split over the
+  // ranks; this rank holds rows [rp0, rp1) of the current M (ld rp1 - rp0)
+  bool dist = false;
+  int64_t rp0 = 0, rp1 = 0;
 };
 
 void sync(Ctx& c) { VSIE_CHECK_CUDA(cudaStreamSynchronize(c.st)); }
@@ -212,6 +219,42 @@ void zgemm_tc(Ctx& c, Trans ta, int64_t M, int64_t N, int64_t K, const cplx* A, 
   if (ta == kC) launch_conj_2d(C, ldc, M, N, c.st);
 }
 
+// ---- row-split helpers of the multi-process build
+void rank_rows(const Ctx& c, int64_t rows, int p, int64_t& r0, int64_t& r1) {
+  const int P = c.h->world;
+  r0 = rows * p / P;
+  r1 = rows * (p + 1) / P;
+}
+
+// every rank holds rows [r0_p, r1_p) of a rows x ncols matrix (local, ld r1_p - r0_p):
+// full (rows x ncols, ld rows) on every rank (allgather of equal padded blocks)
+void assemble_rows(Ctx& c, const cplx* local, int64_t rows, int64_t ncols, cplx* full) {
+  vsie_coupling_s* h = c.h;
+  const int P = h->world;
+  const int64_t rpmax = ceil_div(rows, P);
+  int64_t r0, r1;
+  rank_rows(c, rows, h->rank, r0, r1);
+  c.ws.gsend.ensure(std::max<int64_t>(1, rpmax * ncols));
+  c.ws.grecv.ensure(std::max<int64_t>(1, P * rpmax * ncols));
+  if (r1 > r0)
+    VSIE_CHECK_CUDA(cudaMemcpy2DAsync(c.ws.gsend.p, rpmax * sizeof(cplx), local, (r1 - r0) * sizeof(cplx),
+                                      (r1 - r0) * sizeof(cplx), ncols, cudaMemcpyDeviceToDevice, c.st));
+  h->comm->allgather(reinterpret_cast<const double*>(c.ws.gsend.p), reinterpret_cast<double*>(c.ws.grecv.p),
+                     2 * (size_t)(rpmax * ncols), c.st);
+  for (int p = 0; p < P; ++p) {
+    int64_t a, b;
+    rank_rows(c, rows, p, a, b);
+    if (b > a)
+      VSIE_CHECK_CUDA(cudaMemcpy2DAsync(full + a, rows * sizeof(cplx), c.ws.grecv.p + (int64_t)p * rpmax * ncols,
+                                        rpmax * sizeof(cplx), (b - a) * sizeof(cplx), ncols,
+                                        cudaMemcpyDeviceToDevice, c.st));
+  }
+}
+
+void allreduce_c(Ctx& c, cplx* buf, int64_t n) {
+  c.h->comm->allreduce_sum(reinterpret_cast<double*>(buf), 2 * (size_t)n, c.st);
+}
+
 void set_identity(Ctx& c, DevBuf<cplx>& V, int q) {
   V.ensure((int64_t)q * q);
   std::vector<cplx> I((size_t)q * q, cmk(0, 0));
@@ -343,10 +386,22 @@ void tall_svd(Ctx& c, cplx* A, int64_t p, int q, cplx* V) {
 // other != null also receives the basis of the opposite side (right basis R for
 // left = true, left basis L for left = false) of the same truncated SVD, so that
 // the half-sweep turnaround on the same supercore needs no second factorisation.
+// Multi-process (c.dist): M holds this rank's rows [c.rp0, c.rp1) (ld rp1 - rp0) of the
+// rows x cols supercore; small supercores are assembled and factorised on every rank, the
+// randomized path keeps M row-split: the sketch M Omega is formed locally and allgathered
+// (L->R) or its sum M^H Omega = sum_p M_p^H Omega_p allreduced (R->L), B = Q^H M likewise --
+// no rank ever holds the whole large supercore; the small factorisations are replicated
+// (bitwise identical inputs on every rank, so every rank picks the same ranks and pivots).
 int factorize(Ctx& c, const cplx* M, int64_t rows, int64_t cols, bool left, int r_prev, DevBuf<cplx>* other) {
   Ws& w = c.ws;
   const int64_t mn = std::min(rows, cols);
   const int cap = (int)std::min<int64_t>(c.o.max_rank, mn);
+  const int64_t rl = c.dist ? c.rp1 - c.rp0 : rows;   // local rows of M
+  if (c.dist && mn <= c.o.direct_svd_max) {
+    w.Mfull.ensure(rows * cols);
+    assemble_rows(c, M, rows, cols, w.Mfull.p);
+    M = w.Mfull.p;
+  }
   if (mn <= c.o.direct_svd_max) {
     const bool tall = rows >= cols;
     const int64_t p = tall ? rows : cols;
@@ -399,7 +454,8 @@ int factorize(Ctx& c, const cplx* M, int64_t rows, int64_t cols, bool left, int 
   const int os = c.o.oversample;
   w.frob_partial.ensure(1024);
   w.frob.ensure(1);
-  launch_frob2(M, rows * cols, w.frob_partial.p, w.frob.p, c.st);
+  launch_frob2(M, rl * cols, w.frob_partial.p, w.frob.p, c.st);
+  if (c.dist) c.h->comm->allreduce_sum(w.frob.p, 1, c.st);
   double total2 = 0;
   VSIE_CHECK_CUDA(cudaMemcpyAsync(&total2, w.frob.p, sizeof(double), cudaMemcpyDeviceToHost, c.st));
   sync(c);
@@ -433,9 +489,17 @@ int factorize(Ctx& c, const cplx* M, int64_t rows, int64_t cols, bool left, int 
       }
       cplx* dst = w.Yraw.p + p1 * kk_done;
       if (left) {
-        zgemm_tc(c, kN, rows, nn, cols, M, rows, w.omega.p, cols, dst, rows);
+        if (c.dist) {   // local rows of M Omega, allgathered into the full sketch
+          w.Yloc.ensure(std::max<int64_t>(1, rl * nn));
+          zgemm_tc(c, kN, rl, nn, cols, M, rl, w.omega.p, cols, w.Yloc.p, rl);
+          assemble_rows(c, w.Yloc.p, rows, nn, dst);
+        } else {
+          zgemm_tc(c, kN, rows, nn, cols, M, rows, w.omega.p, cols, dst, rows);
+        }
       } else {
-        zgemm_tc(c, kT, cols, nn, rows, M, rows, w.omega.p, rows, dst, cols);
+        // conj(M^T Omega) = M^H conj(Omega); row-split: sum over the ranks' row blocks
+        zgemm_tc(c, kT, cols, nn, rl, M, rl, w.omega.p + (c.dist ? c.rp0 : 0), rows, dst, cols);
+        if (c.dist) allreduce_c(c, dst, cols * nn);
         launch_conj(dst, p1 * nn, c.st);
       }
       kk_done = kk;
@@ -467,10 +531,16 @@ int factorize(Ctx& c, const cplx* M, int64_t rows, int64_t cols, bool left, int 
     launch_gather_cols(w.Y.p, p1, p1, c.ws.idx.p, w.norms.p, kq, w.Q.p, p1, false, c.st);
     // Bh = M^H Q (L->R) or M Q (R->L): p2 x kq
     w.Bh.ensure(p2 * kq);
-    if (left)
-      zgemm_tc(c, kC, cols, kq, rows, M, rows, w.Q.p, rows, w.Bh.p, cols);
-    else
+    if (left) {   // M^H Q = sum over the row blocks M_p^H Q_p
+      zgemm_tc(c, kC, cols, kq, rl, M, rl, w.Q.p + (c.dist ? c.rp0 : 0), rows, w.Bh.p, cols);
+      if (c.dist) allreduce_c(c, w.Bh.p, cols * kq);
+    } else if (c.dist) {   // M Q: local rows, allgathered
+      w.Bloc.ensure(std::max<int64_t>(1, rl * kq));
+      zgemm_tc(c, kN, rl, kq, cols, M, rl, w.Q.p, cols, w.Bloc.p, rl);
+      assemble_rows(c, w.Bloc.p, rows, kq, w.Bh.p);
+    } else {
       zgemm_tc(c, kN, rows, kq, cols, M, rows, w.Q.p, cols, w.Bh.p, rows);
+    }
     w.V.ensure((int64_t)kq * kq);
     tall_svd(c, w.Bh.p, p2, kq, w.V.p);
     auto s = sorted_norms(c, w.Bh.p, p2, kq);
@@ -605,25 +675,24 @@ void eval_supercore(Ctx& c, ChiState& s, int k, int64_t& rows, int64_t& cols) {
   c.ws.right.ensure(right.size());
   VSIE_CHECK_CUDA(cudaMemcpyAsync(c.ws.left.p, left.data(), left.size() * 4, cudaMemcpyHostToDevice, c.st));
   VSIE_CHECK_CUDA(cudaMemcpyAsync(c.ws.right.p, right.data(), right.size() * 4, cudaMemcpyHostToDevice, c.st));
-  const int P = h->comm ? h->world : 1;
-  const int64_t cp = ceil_div(cols, P);
-  c.ws.M.ensure(rows * cp * P);
+  c.dist = h->comm != nullptr;
+  c.rp0 = 0;
+  c.rp1 = rows;
+  if (c.dist) rank_rows(c, rows, h->rank, c.rp0, c.rp1);   // this rank's rows
+  c.ws.M.ensure(std::max<int64_t>(1, (c.rp1 - c.rp0) * cols));
   BlockDesc b{};
   b.chi = s.chi;
   b.k = k;
   b.rl = rl; b.nk = nk; b.nk1 = nk1; b.rr = rr;
   b.left = c.ws.left.p;
   b.right = c.ws.right.p;
-  b.ld = rows;
-  const int me = h->comm ? h->rank : 0;
-  b.col0 = std::min(cols, cp * me);
-  b.col1 = std::min(cols, cp * (me + 1));
+  b.ld = c.rp1 - c.rp0;
+  b.col0 = 0;
+  b.col1 = cols;
+  b.row0 = c.rp0;
+  b.row1 = c.rp1;
   auto t0 = Clock::now();
-  launch_entries_block(h->eg, b, c.ws.M.p + rows * b.col0, c.st);
-  if (h->comm) {
-    h->comm->allgather(reinterpret_cast<const double*>(c.ws.M.p + rows * cp * me),
-                       reinterpret_cast<double*>(c.ws.M.p), 2 * (size_t)(rows * cp), c.st);
-  }
+  if (c.rp1 > c.rp0) launch_entries_block(h->eg, b, c.ws.M.p, c.st);
   sync(c);
   c.t_entry += secs(t0);
   c.n_eval += rows * cols;
@@ -745,7 +814,12 @@ int cross_chi(Ctx& c, int chi, Heldout& ho) {
         for (int p : P) s.I3.push_back({s.I2[p % rl][0], s.I2[p % rl][1], p / rl});
         upload_idx(c, P);
         s.core[3].ensure((int64_t)r * cols);
-        launch_gather_rows(c.ws.M.p, rows, c.ws.idx.p, r, cols, s.core[3].p, c.st);
+        if (c.dist) {   // rows P of the row-split M_3: owned rows copied, the rest zero, summed
+          launch_gather_rows_owned(c.ws.M.p, c.rp1 - c.rp0, c.ws.idx.p, r, cols, c.rp0, c.rp1, s.core[3].p, c.st);
+          allreduce_c(c, s.core[3].p, (int64_t)r * cols);
+        } else {
+          launch_gather_rows(c.ws.M.p, rows, c.ws.idx.p, r, cols, s.core[3].p, c.st);
+        }
         reuse = true;  // R->L starts with the same M_3 (right basis in ws.other)
         reuse_r = r;
       }
@@ -786,7 +860,14 @@ int cross_chi(Ctx& c, int chi, Heldout& ho) {
         for (int q : Q) s.J1.push_back({(int)(q % nk1), s.J2[q / nk1][0], s.J2[q / nk1][1]});
         upload_idx(c, Q);
         s.core[0].ensure(rows * r);
-        launch_gather_cols(c.ws.M.p, rows, rows, c.ws.idx.p, nullptr, r, s.core[0].p, rows, false, c.st);
+        if (c.dist) {   // columns Q of the row-split M_1, rows assembled from the ranks
+          const int64_t rloc = c.rp1 - c.rp0;
+          c.ws.Bloc.ensure(std::max<int64_t>(1, rloc * r));
+          launch_gather_cols(c.ws.M.p, rloc, rloc, c.ws.idx.p, nullptr, r, c.ws.Bloc.p, rloc, false, c.st);
+          assemble_rows(c, c.ws.Bloc.p, rows, r, s.core[0].p);
+        } else {
+          launch_gather_cols(c.ws.M.p, rows, rows, c.ws.idx.p, nullptr, r, s.core[0].p, rows, false, c.st);
+        }
         reuse = true;  // the next L->R starts with the same M_1 (left basis in ws.other)
         reuse_r = r;
       }

@@ -507,6 +507,16 @@ __global__ void __launch_bounds__(128) k_upper_inverse(const cplx* Rt, int q, cp
   for (int k = threadIdx.x; k < q; k += blockDim.x) X[k + (int64_t)q * c] = xcol[k];
 }
 
+__global__ void k_gather_rows_owned(const cplx* src, int64_t lds, const int* idx, int nr, int64_t cols, int64_t r0,
+                                    int64_t r1, cplx* dst) {
+  for (int64_t e = blockIdx.x * (int64_t)NT + threadIdx.x; e < (int64_t)nr * cols; e += (int64_t)gridDim.x * NT) {
+    const int i = (int)(e % nr);
+    const int64_t c = e / nr;
+    const int64_t row = idx[i];
+    dst[e] = (row >= r0 && row < r1) ? src[(row - r0) + lds * c] : cmk(0, 0);
+  }
+}
+
 __global__ void k_copy_conj(const cplx* src, int64_t lds, int64_t rows, int64_t cols, cplx* dst) {
   for (int64_t e = blockIdx.x * (int64_t)NT + threadIdx.x; e < rows * cols; e += (int64_t)gridDim.x * NT) {
     const int64_t r = e % rows, c = e / rows;
@@ -596,6 +606,13 @@ void launch_add_diag(cplx* G, int q, double s, cudaStream_t st) {
 
 void launch_trace_real(const cplx* G, int q, double* out, cudaStream_t st) {
   k_trace_real<<<1, NT, 0, st>>>(G, q, out);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_gather_rows_owned(const cplx* src, int64_t lds, const int* idx, int nr, int64_t cols, int64_t r0,
+                              int64_t r1, cplx* dst, cudaStream_t st) {
+  if (nr <= 0 || cols <= 0) return;
+  k_gather_rows_owned<<<grid1((int64_t)nr * cols), NT, 0, st>>>(src, lds, idx, nr, cols, r0, r1, dst);
   VSIE_CHECK_LAUNCH();
 }
 

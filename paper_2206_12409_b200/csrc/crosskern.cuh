@@ -34,6 +34,9 @@ void launch_gather_rows(const cplx* src, int64_t lds, const int* idx, int nr, in
 // dst (rows x cols, ld rows) = conj(src (ld lds)); conj of C (rows x cols, ld ldc) in place
 void launch_copy_conj(const cplx* src, int64_t lds, int64_t rows, int64_t cols, cplx* dst, cudaStream_t st);
 void launch_conj_2d(cplx* C, int64_t ldc, int64_t rows, int64_t cols, cudaStream_t st);
+// dst[i, :] = src[idx[i] - r0, :] for idx[i] in [r0, r1), else 0 (row-split matrices)
+void launch_gather_rows_owned(const cplx* src, int64_t lds, const int* idx, int nr, int64_t cols, int64_t r0,
+                              int64_t r1, cplx* dst, cudaStream_t st);
 // dst (C x R) = op(src (R x C)), op = transpose or conj-transpose
 void launch_transpose(const cplx* src, int64_t R, int64_t C, cplx* dst, bool conj, cudaStream_t st);
 

@@ -104,11 +104,12 @@ __global__ void __launch_bounds__(256) k_entries_list(EntryGeom g, const int64_t
 }
 
 __global__ void __launch_bounds__(256) k_entries_block(EntryGeom g, BlockDesc b, cplx* __restrict__ out) {
-  const int64_t rows = b.rl * b.nk;
+  const int64_t r0 = b.row1 > b.row0 ? b.row0 : 0;
+  const int64_t rows = b.row1 > b.row0 ? b.row1 - b.row0 : b.rl * b.nk;   // rows evaluated
   const int64_t total = rows * (b.col1 - b.col0);
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = t % rows;
+    const int64_t rr = t % rows, r = r0 + rr;
     const int64_t cl = t / rows;
     const int64_t c = b.col0 + cl;
     const int64_t alpha = r % b.rl, ik = r / b.rl;
@@ -131,7 +132,7 @@ __global__ void __launch_bounds__(256) k_entries_block(EntryGeom g, BlockDesc b,
       i3 = (int)ik;
       n = ik1;
     }
-    out[r + b.ld * cl] = entry_value(g, b.chi, i1, i2, i3, n);
+    out[rr + b.ld * cl] = entry_value(g, b.chi, i1, i2, i3, n);
   }
 }
 
@@ -151,7 +152,8 @@ void launch_entries_list(const EntryGeom& g, const int64_t* idx, int64_t count, 
 }
 
 void launch_entries_block(const EntryGeom& g, const BlockDesc& b, cplx* out, cudaStream_t st) {
-  const int64_t total = b.rl * b.nk * (b.col1 - b.col0);
+  const int64_t rows = b.row1 > b.row0 ? b.row1 - b.row0 : b.rl * b.nk;
+  const int64_t total = rows * (b.col1 - b.col0);
   if (total <= 0) return;
   k_entries_block<<<grid_for(total, 256), 256, 0, st>>>(g, b, out);
   VSIE_CHECK_LAUNCH();

@@ -38,6 +38,7 @@ struct BlockDesc {
   const int32_t* right;
   int64_t col0, col1;
   int64_t ld;
+  int64_t row0 = 0, row1 = 0;   // rows [row0, row1) only when row1 > row0 (written at out + (r - row0))
 };
 void launch_entries_block(const EntryGeom& g, const BlockDesc& b, cplx* out, cudaStream_t st);
 

@@ -88,6 +88,21 @@ def main():
                     "N": rel(bp.apply(torch.from_numpy(x).cuda(), "N").cpu().numpy(), y1),
                     "T": rel(bp.apply(torch.from_numpy(us).cuda(), "T").cpu().numpy(),
                              b1.apply(torch.from_numpy(u).cuda(), "T").cpu().numpy())}
+    # cfg 2: the randomized range finder on row-split supercores (k = 2, 3: min dim > 384);
+    # the sums over the ranks' row blocks round differently, so the TT is an equally valid
+    # approximation, compared through its applies (both within ~1e-6 of Z)
+    cfg = synth.get_config(2)
+    b1 = Coupling.build(grid_of(cfg), cfg.meshes(), cfg.freq, cfg.tol, nrhs_max=1)
+    bp = Coupling.build(grid_of(cfg), cfg.meshes(), cfg.freq, cfg.tol, nrhs_max=1, world=world, rank=rank,
+                        ipc_name=f"{name}_c")
+    x = synth.complex_gaussian(cfg.m, 43)
+    s0, s1 = bp.info()["slab"]
+    n12 = cfg.n[0] * cfg.n[1]
+    y1 = b1.apply(torch.from_numpy(x).cuda(), "N").cpu().numpy().reshape(3, -1)[:, n12 * s0:n12 * s1].reshape(-1)
+    i1, ip = b1.info(), bp.info()
+    res["build_rowsplit"] = {"status": bp.status, "heldout": list(ip["heldout_err"]),
+                             "ranks1": i1["ranks"], "ranksp": ip["ranks"],
+                             "N": rel(bp.apply(torch.from_numpy(x).cuda(), "N").cpu().numpy(), y1)}
     with open(out, "w") as f:
         json.dump(res, f)
     print("worker ok", rank)
