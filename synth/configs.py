@@ -133,3 +133,26 @@ CONFIGS = {
 
 def get_config(i: int) -> Config:
     return CONFIGS[int(i)]
+
+
+# Near-domain conductor of the 3 x 3 hybrid system ("the receive array is usually in the
+# near domain"; Fig. 1): no coil meshes are available, so an open cylinder coaxial
+# with the far surfaces, just outside the voxel box, stands in for the receive-array former
+# (reading R-CC3).  #RWG = n_az (3 n_ax - 1).
+NEAR_COILS = {
+    1: Surface("near", radius=0.15, length=0.20, n_az=16, n_ax=8),     # 368 RWG
+    2: Surface("near", radius=0.17, length=0.26, n_az=48, n_ax=30),    # 4272 RWG
+    3: Surface("near", radius=0.26, length=0.60, n_az=64, n_ax=40),    # 7616 RWG
+    4: Surface("near", radius=0.17, length=0.26, n_az=64, n_ax=40),    # 7616 RWG
+    5: Surface("near", radius=0.26, length=0.60, n_az=64, n_ax=40),
+}
+
+
+def near_coil(i: int) -> Surface:
+    return NEAR_COILS[int(i)]
+
+
+def near_mesh(i: int):
+    """(xyz, tri) of the near conductor of config i."""
+    s = near_coil(i)
+    return cylinder_mesh(s.radius, s.length, s.n_az, s.n_ax)

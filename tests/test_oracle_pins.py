@@ -708,3 +708,124 @@ def test_P35b_compression_factor_counts_arrays():
     assert dense.shape == (3 * 3 * 4 * 5, m)
     f = validate.compression_factor(n, m, ranks)
     assert f == Fraction(dense.size, sum(g.size for t in tts for g in t))
+
+
+# ---------------------------------------------------------------- far-near block (NEXT-3)
+
+def _farnear_tables(ci):
+    from oracle import farnear  # noqa: F401
+    cfg = synth.get_config(ci)
+    rs_n, js_n = geometry.mesh_sources([synth.near_mesh(ci)])
+    rs_f, js_f = geometry.mesh_sources(cfg.meshes())
+    return cfg, rs_n, js_n, rs_f, js_f
+
+
+def _mp_cc_entry(near, far, m, n):
+    """One Z_cc^fn entry at 40 digits from f = +-(l / 2A) (r - p) on each triangle, area weights
+    A / 3 on both sides, and the dyad (I + grad grad / k0^2) g by mpmath derivatives of g (no
+    closed-form dyad)."""
+    mp.mp.dps = 40
+    k0 = 2 * mp.pi * mp.mpf(synth.configs.FREQ_7T) / mp.mpf(synth.configs.C0)
+
+    def rwg_nodes(mesh, idx):
+        xyz, tri = mesh
+        rwg = geometry.rwg_edges(xyz, tri)
+        tp, tm = int(rwg["tp"][idx]), int(rwg["tm"][idx])
+        a, b = int(rwg["a"][idx]), int(rwg["b"][idx])
+        P = lambda v: [mp.mpf(float(x)) for x in v]
+        l = mp.sqrt(sum((P(xyz[a])[i] - P(xyz[b])[i]) ** 2 for i in range(3)))
+        out = []
+        for sgn, T in ((1, tp), (-1, tm)):
+            V = [P(xyz[v]) for v in tri[T]]
+            p = [P(xyz[v]) for v in tri[T] if v not in (a, b)][0]
+            e1 = [V[1][i] - V[0][i] for i in range(3)]
+            e2 = [V[2][i] - V[0][i] for i in range(3)]
+            cr = [e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]]
+            A = mp.sqrt(sum(x * x for x in cr)) / 2
+            for q in range(3):
+                bary = [mp.mpf(1) / 6] * 3
+                bary[q] = mp.mpf(2) / 3
+                rq = [sum(bary[j] * V[j][i] for j in range(3)) for i in range(3)]
+                f = [sgn * l / (2 * A) * (rq[i] - p[i]) for i in range(3)]
+                out.append((rq, [A / 3 * fi for fi in f]))
+        return out
+
+    def g(x, y, z):
+        rr = mp.sqrt(x * x + y * y + z * z)
+        return mp.exp(-1j * k0 * rr) / (4 * mp.pi * rr)
+
+    total = mp.mpc(0)
+    for rp, jp in rwg_nodes(near, m):
+        for rs, js in rwg_nodes(far, n):
+            R = [rp[i] - rs[i] for i in range(3)]
+            g0 = g(*R)
+            for a in range(3):
+                for b in range(3):
+                    order = [0, 0, 0]
+                    order[a] += 1
+                    order[b] += 1
+                    Gab = (g0 if a == b else 0) + mp.diff(g, R, tuple(order)) / k0 ** 2
+                    total += jp[a] * Gab * js[b]
+    return complex(total)
+
+
+def test_P44_farnear_entry_extended_precision():
+    from oracle import farnear
+    cfg, rs_n, js_n, rs_f, js_f = _farnear_tables(1)
+    k0 = 2 * np.pi * cfg.freq / synth.configs.C0
+    for m, n in ((3, 17), (200, 1000)):
+        ref = _mp_cc_entry(synth.near_mesh(1), cfg.meshes()[0], m, n)
+        got = farnear.entries_cc(rs_n, js_n, rs_f, js_f, k0, [m], [n])[0]
+        assert abs(got - ref) <= 1e-13 * abs(ref), (m, n, got, ref)
+
+
+def test_P43_farnear_reciprocity_and_disjointness():
+    """Z^nf = (Z^fn)^T (the dyad is symmetric and even: the transposed block of Eq. 11 / 15),
+    and the near and far conductors are disjoint (non-singular rule)."""
+    from oracle import farnear
+    cfg, rs_n, js_n, rs_f, js_f = _farnear_tables(1)
+    k0 = 2 * np.pi * cfg.freq / synth.configs.C0
+    rng = np.random.default_rng(43)
+    rows = rng.integers(0, rs_n.shape[0], 50)
+    cols = rng.integers(0, rs_f.shape[0], 50)
+    a = farnear.entries_cc(rs_n, js_n, rs_f, js_f, k0, rows, cols)
+    b = farnear.entries_cc(rs_f, js_f, rs_n, js_n, k0, cols, rows)
+    assert np.max(np.abs(a - b)) <= 1e-14 * np.max(np.abs(a))
+    d = np.min(np.linalg.norm(rs_n.reshape(-1, 1, 3) - rs_f.reshape(1, -1, 3)[:, ::7], axis=-1))
+    assert d > 0.15
+
+
+def test_P45_aca_exact_on_low_rank_and_interpolates_pivots():
+    """A seeded random rank-5 complex 60 x 80 matrix is recovered to 1e-12 with rank <= 6; the
+    ACA residual vanishes on the pivot rows and columns (cross interpolation)."""
+    from oracle import farnear
+    rng = np.random.default_rng(45)
+    A = (rng.standard_normal((60, 5)) + 1j * rng.standard_normal((60, 5))) @ \
+        (rng.standard_normal((5, 80)) + 1j * rng.standard_normal((5, 80)))
+    U, W = farnear.aca(lambda i: A[i], lambda j: A[:, j], 60, 80, 1e-14)
+    assert U.shape[1] <= 6
+    assert np.linalg.norm(A - U @ W.T) <= 1e-12 * np.linalg.norm(A)
+    B = rng.standard_normal((40, 30)) + 1j * rng.standard_normal((40, 30))   # full rank
+    U, W = farnear.aca(lambda i: B[i], lambda j: B[:, j], 40, 30, 1e-3, max_rank=7)
+    Rz = B - U @ W.T
+    piv_cols = [int(np.argmax(np.abs(W[:, k]))) for k in range(W.shape[1])]
+    assert np.max(np.abs(Rz[:, piv_cols])) <= 1e-12 * np.max(np.abs(B))
+
+
+def test_P46_aca_far_near_block_vs_dense():
+    """The ACA of the cfg 1 far-near block (368 near x 1128 far RWG) meets its tolerance
+    against the dense block, and is near the SVD-optimal rank."""
+    from oracle import farnear
+    cfg, rs_n, js_n, rs_f, js_f = _farnear_tables(1)
+    k0 = 2 * np.pi * cfg.freq / synth.configs.C0
+    Z = farnear.dense_cc(rs_n, js_n, rs_f, js_f, k0)
+    tol = 1e-6
+    U, W = farnear.aca(lambda i: Z[i], lambda j: Z[:, j], Z.shape[0], Z.shape[1], tol)
+    err = np.linalg.norm(Z - U @ W.T) / np.linalg.norm(Z)
+    assert err <= 10 * tol, err
+    s = np.linalg.svd(Z, compute_uv=False)
+    tail = np.sqrt(np.cumsum((s ** 2)[::-1])[::-1])
+    r_opt = int(np.argmax(tail <= tol * np.linalg.norm(Z)))
+    assert r_opt <= U.shape[1] <= 2 * r_opt + 10, (r_opt, U.shape[1])
+    x = synth.complex_gaussian(Z.shape[1], 46)
+    assert np.linalg.norm(farnear.apply_lowrank(U, W, x, "N") - Z @ x) <= 10 * tol * np.linalg.norm(Z) * np.linalg.norm(x)
