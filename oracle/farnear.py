@@ -47,9 +47,15 @@ def dense_cc(rs_a, js_a, rs_b, js_b, k0, scale=1.0 + 0.0j):
     return entries_cc(rs_a, js_a, rs_b, js_b, k0, r.ravel(), c.ravel(), scale).reshape(ma, mb)
 
 
-def aca(row_fn, col_fn, m, n, tol, max_rank=None):
+def aca(row_fn, col_fn, m, n, tol, max_rank=None, pivots=None, trace=None):
     """Partially pivoted ACA of an m x n matrix given by row_fn(i) -> A[i, :] and
     col_fn(j) -> A[:, j].  Returns (U [m, k], W [n, k]) with A ~= U W^T.
+
+    pivots: optional [(i_k, j_k)] to replay another run's pivot sequence (near-ties of |.| on a
+    rotationally symmetric geometry make the argmax order-dependent); the steps below are
+    unchanged, only the two argmax choices are replaced, and when trace is a list it receives
+    per step (|rrow[j_k]| / max_j |rrow|, |u_{k-1}[i_k]| / max_unused |u_{k-1}|) -- both 1 for
+    a valid ACA pivot.
 
     Step k (rows I, columns J used so far; S_{k-1} = sum_{l<k} u_l w_l^T):
       1. residual row  rrow = A[i_k, :] - sum_l U[i_k, l] w_l
@@ -68,10 +74,24 @@ def aca(row_fn, col_fn, m, n, tol, max_rank=None):
     used = np.zeros(m, dtype=bool)
     norm2 = 0.0
     i = 0
+    row_ratio = 1.0
     while U.shape[1] < max_rank and not used.all():
+        if pivots is not None:
+            if U.shape[1] >= len(pivots):
+                break
+            i = int(pivots[U.shape[1]][0])
+            if U.shape[1] > 0:
+                au = np.abs(U[:, -1]).copy()
+                au[used] = -1.0
+                row_ratio = abs(U[i, -1]) / au.max() if au.max() > 0 else 1.0
         rrow = np.asarray(row_fn(i), dtype=np.complex128) - U[i, :] @ W.T
         used[i] = True
         j = int(np.argmax(np.abs(rrow)))
+        if pivots is not None:
+            jf = int(pivots[U.shape[1]][1])
+            if trace is not None:
+                trace.append((abs(rrow[jf]) / abs(rrow[j]) if abs(rrow[j]) > 0 else 1.0, row_ratio))
+            j = jf
         if abs(rrow[j]) == 0.0:
             cand = np.flatnonzero(~used)
             if cand.size == 0:
@@ -85,7 +105,7 @@ def aca(row_fn, col_fn, m, n, tol, max_rank=None):
         norm2 += cross + (nu * nw) ** 2
         U = np.concatenate([U, u[:, None]], axis=1)
         W = np.concatenate([W, w[:, None]], axis=1)
-        if nu * nw <= tol * np.sqrt(max(norm2, 0.0)):
+        if nu * nw <= tol * np.sqrt(max(norm2, 0.0)) and pivots is None:
             break
         au = np.abs(u)
         au[used] = -1.0

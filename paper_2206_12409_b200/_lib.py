@@ -11,7 +11,8 @@ import re
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libvsie_coupling.so")
-HEADER = os.path.join(os.path.dirname(PKG), "include", "vsie_coupling.h")
+INCLUDE = os.path.join(os.path.dirname(PKG), "include")
+HEADER = os.path.join(INCLUDE, "vsie_coupling.h")
 
 VSIE_OK = 0
 VSIE_WARN_NOT_CONVERGED = 1
@@ -56,6 +57,18 @@ class vsie_trace(C.Structure):
                 ("t1_ms", C.c_double)]
 
 
+class vsie_farnear_opts(C.Structure):
+    _fields_ = [("max_rank", C.c_int32), ("scale_re", C.c_double), ("scale_im", C.c_double), ("device", C.c_int32),
+                ("verbose", C.c_int32)]
+
+
+class vsie_farnear_info(C.Structure):
+    _fields_ = [("m_near", C.c_int64), ("m_far", C.c_int64), ("rank", C.c_int32), ("stop", C.c_int32),
+                ("est_err", C.c_double), ("frob", C.c_double), ("min_distance", C.c_double),
+                ("max_edge", C.c_double), ("k0", C.c_double), ("build_s", C.c_double),
+                ("entries_evaluated", C.c_int64), ("factor_bytes", C.c_int64), ("apply_calls", C.c_int64)]
+
+
 HANDLE = C.c_void_p
 
 _SIGS = {
@@ -92,13 +105,25 @@ _SIGS = {
     "vsie_coupling_configure": (C.c_int32, [HANDLE, C.c_int32, C.c_int32]),
     "vsie_coupling_trace": (C.c_int32, [HANDLE, C.POINTER(vsie_trace), C.c_int32, C.POINTER(C.c_int32)]),
     "vsie_coupling_destroy": (None, [HANDLE]),
+    # include/vsie_farnear.h
+    "vsie_farnear_opts_default": (None, [C.POINTER(vsie_farnear_opts)]),
+    "vsie_farnear_build": (C.c_int32, [C.POINTER(vsie_mesh), C.c_int32, C.POINTER(vsie_mesh), C.c_int32, C.c_double,
+                                       C.c_double, C.POINTER(vsie_farnear_opts), C.POINTER(HANDLE)]),
+    "vsie_farnear_entries": (C.c_int32, [HANDLE, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "vsie_farnear_apply": (C.c_int32, [HANDLE, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    "vsie_farnear_apply_pair": (C.c_int32, [HANDLE, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vsie_farnear_export": (C.c_int32, [HANDLE, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vsie_farnear_get_info": (C.c_int32, [HANDLE, C.POINTER(vsie_farnear_info)]),
+    "vsie_farnear_destroy": (None, [HANDLE]),
 }
 
 
-def header_symbols(path: str = HEADER):
-    """Function names declared in include/vsie_coupling.h."""
-    txt = open(path).read()
-    return sorted(set(re.findall(r"\b(vsie_[a-z_]+)\s*\(", txt)) - {"vsie_coupling_t"})
+def header_symbols(paths=None):
+    """Function names declared in include/*.h."""
+    if paths is None:
+        paths = sorted(os.path.join(INCLUDE, f) for f in os.listdir(INCLUDE) if f.endswith(".h"))
+    txt = "".join(open(p).read() for p in paths)
+    return sorted(set(re.findall(r"\b(vsie_[a-z_]+)\s*\(", txt)) - {"vsie_coupling_t", "vsie_farnear_t"})
 
 
 class VsieError(RuntimeError):

@@ -1,13 +1,16 @@
 // C ABI of the Z_bc coupling library (include/vsie_coupling.h).  Every entry
 // point converts exceptions into status codes and records a thread-local
 // message; no C++ exception crosses the boundary.
+#include <algorithm>
 #include <chrono>
+#include <memory>
 #include <cmath>
 #include <cstring>
 #include <numeric>
 #include <string>
 
 #include "cross.hpp"
+#include "farnear.hpp"
 #include "handle.hpp"
 
 using namespace vsie;
@@ -490,6 +493,97 @@ int32_t vsie_coupling_trace(vsie_coupling_t h, vsie_trace* out, int32_t max, int
 }
 
 void vsie_coupling_destroy(vsie_coupling_t h) {
+  if (!h) return;
+  cudaDeviceSynchronize();
+  delete h;
+}
+
+// ----------------------------------------------------------------- far-near block (vsie_farnear.h)
+void vsie_farnear_opts_default(vsie_farnear_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->max_rank = 2048;
+  o->scale_re = 1.0;
+  o->scale_im = 0.0;
+  o->device = -1;
+  o->verbose = 0;
+}
+
+int32_t vsie_farnear_build(const vsie_mesh* near_meshes, int32_t n_near, const vsie_mesh* far_meshes, int32_t n_far,
+                           double freq_hz, double tol, const vsie_farnear_opts* opts, vsie_farnear_t* out) {
+  if (out) *out = nullptr;
+  return guarded([&] {
+    VSIE_REQUIRE(out != nullptr && near_meshes != nullptr && far_meshes != nullptr && n_near >= 1 && n_far >= 1,
+                 VSIE_ERR_ARG, "farnear_build: NULL argument or no meshes");
+    vsie_farnear_opts o;
+    vsie_farnear_opts_default(&o);
+    if (opts) o = *opts;
+    std::unique_ptr<vsie_farnear_s> h(new vsie_farnear_s());
+    const int st = farnear_build(near_meshes, n_near, far_meshes, n_far, freq_hz, tol, o, h.get());
+    *out = h.release();
+    return st;
+  });
+}
+
+int32_t vsie_farnear_entries(vsie_farnear_t h, const int64_t* idx, int64_t count, void* out, void* stream) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "NULL handle");
+    farnear_entries(h, idx, count, out, static_cast<cudaStream_t>(stream));
+    return VSIE_OK;
+  });
+}
+
+int32_t vsie_farnear_apply(vsie_farnear_t h, const void* x, void* y, int32_t op, int32_t nrhs, void* stream) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "NULL handle");
+    farnear_apply(h, x, y, op, nrhs, static_cast<cudaStream_t>(stream));
+    return VSIE_OK;
+  });
+}
+
+int32_t vsie_farnear_apply_pair(vsie_farnear_t h, const void* x_far, void* y_near, const void* x_near, void* y_far,
+                                void* stream) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "NULL handle");
+    farnear_apply_pair(h, x_far, y_near, x_near, y_far, static_cast<cudaStream_t>(stream));
+    return VSIE_OK;
+  });
+}
+
+int32_t vsie_farnear_export(vsie_farnear_t h, void* U_host, void* W_host, int32_t* rows, int32_t* cols) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "NULL handle");
+    VSIE_CHECK_CUDA(cudaDeviceSynchronize());
+    if (U_host && h->rank > 0) VSIE_CHECK_CUDA(cudaMemcpy(U_host, h->U.p, h->U.bytes(), cudaMemcpyDeviceToHost));
+    if (W_host && h->rank > 0) VSIE_CHECK_CUDA(cudaMemcpy(W_host, h->W.p, h->W.bytes(), cudaMemcpyDeviceToHost));
+    if (rows) std::copy(h->piv_i.begin(), h->piv_i.end(), rows);
+    if (cols) std::copy(h->piv_j.begin(), h->piv_j.end(), cols);
+    return VSIE_OK;
+  });
+}
+
+int32_t vsie_farnear_get_info(vsie_farnear_t h, vsie_farnear_info* out) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr && out != nullptr, VSIE_ERR_ARG, "NULL argument");
+    std::memset(out, 0, sizeof(*out));
+    out->m_near = h->mn;
+    out->m_far = h->mf;
+    out->rank = h->rank;
+    out->stop = h->stop;
+    out->est_err = h->est_err;
+    out->frob = h->frob;
+    out->min_distance = h->min_dist;
+    out->max_edge = h->max_edge;
+    out->k0 = h->k0;
+    out->build_s = h->build_s;
+    out->entries_evaluated = h->entries;
+    out->factor_bytes = (int64_t)16 * h->rank * (h->mn + h->mf);
+    out->apply_calls = h->apply_calls;
+    return VSIE_OK;
+  });
+}
+
+void vsie_farnear_destroy(vsie_farnear_t h) {
   if (!h) return;
   cudaDeviceSynchronize();
   delete h;

@@ -109,12 +109,33 @@ void append_mesh(const vsie_mesh& mesh, std::vector<double>& table) {
 
 }  // namespace
 
-Sources build_sources(const vsie_mesh* meshes, int n_meshes, const GridDesc& grid) {
+Sources build_rwg_sources(const vsie_mesh* meshes, int n_meshes) {
   VSIE_REQUIRE(meshes != nullptr && n_meshes >= 1, VSIE_ERR_ARG, "no meshes");
   Sources s;
   for (int k = 0; k < n_meshes; ++k) append_mesh(meshes[k], s.table);
   s.m = (int64_t)(s.table.size() / kSrcStride);
   VSIE_REQUIRE(s.m >= 1, VSIE_ERR_GEOMETRY, "meshes have no interior edge (no RWG function)");
+  return s;
+}
+
+double max_edge_length(const vsie_mesh* meshes, int n_meshes) {
+  double best = 0;
+  for (int k = 0; k < n_meshes; ++k) {
+    const double* X = meshes[k].xyz;
+    const int32_t* T = meshes[k].tri;
+    for (int64_t t = 0; t < meshes[k].n_triangles; ++t)
+      for (int e = 0; e < 3; ++e) {
+        const int64_t a = T[3 * t + e], b = T[3 * t + (e + 1) % 3];
+        double d2 = 0;
+        for (int c = 0; c < 3; ++c) d2 += (X[3 * a + c] - X[3 * b + c]) * (X[3 * a + c] - X[3 * b + c]);
+        best = std::max(best, std::sqrt(d2));
+      }
+  }
+  return best;
+}
+
+Sources build_sources(const vsie_mesh* meshes, int n_meshes, const GridDesc& grid) {
+  Sources s = build_rwg_sources(meshes, n_meshes);
   // Non-singular rule (reading R-L18): every source node must be at
   // least 10 max(h) away from the bounding box of the voxel quadrature nodes.
   double lo[3], hi[3], hmax = 0;

@@ -31,5 +31,9 @@ struct GridDesc {
 // Validates and converts the public structs; throws Error(VSIE_ERR_ARG / VSIE_ERR_GEOMETRY).
 GridDesc make_grid(const vsie_grid* g);
 Sources build_sources(const vsie_mesh* meshes, int n_meshes, const GridDesc& grid);
+// The RWG table alone (no voxel-grid check): the surface-surface blocks (farnear.cu).
+Sources build_rwg_sources(const vsie_mesh* meshes, int n_meshes);
+// Longest triangle edge of the meshes (validated by build_rwg_sources first).
+double max_edge_length(const vsie_mesh* meshes, int n_meshes);
 
 }  // namespace vsie

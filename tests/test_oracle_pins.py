@@ -810,6 +810,17 @@ def test_P45_aca_exact_on_low_rank_and_interpolates_pivots():
     Rz = B - U @ W.T
     piv_cols = [int(np.argmax(np.abs(W[:, k]))) for k in range(W.shape[1])]
     assert np.max(np.abs(Rz[:, piv_cols])) <= 1e-12 * np.max(np.abs(B))
+    # replaying the run's own (row, column) pivots reproduces it with unit pivot ratios, and the
+    # residual vanishes on the pivot rows too
+    rows, cols = [], []
+    U0, W0 = farnear.aca(lambda i: (rows.append(i), B[i])[1], lambda j: (cols.append(j), B[:, j])[1], 40, 30, 1e-3,
+                         max_rank=7)
+    assert np.max(np.abs(Rz[rows])) <= 1e-12 * np.max(np.abs(B))
+    tr = []
+    U1, W1 = farnear.aca(lambda i: B[i], lambda j: B[:, j], 40, 30, 1e-3, max_rank=7, pivots=list(zip(rows, cols)),
+                         trace=tr)
+    assert np.array_equal(U0, U1) and np.array_equal(W0, W1)
+    assert len(tr) == 7 and all(abs(a - 1) <= 1e-12 and abs(b - 1) <= 1e-12 for a, b in tr), tr
 
 
 def test_P46_aca_far_near_block_vs_dense():
