@@ -261,6 +261,7 @@ def main():
                     help="TT-round the cores (vsie_coupling_round, SURVEY 8f NEXT-1) at TOL before timing "
                          "(single process only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-farnear", action="store_true", help="skip the far-near ACA block sub-measurement")
     ap.add_argument("--separate", action="store_true",
                     help="time the step as two vsie_coupling_apply calls instead of vsie_coupling_apply_pair")
     args = ap.parse_args()
@@ -471,6 +472,38 @@ def main():
         dist.destroy_process_group()
         return 0
 
+    # ---- far-near block: device ACA of Z_cc^fn against the synthetic near
+    # coil, then the Eq. 15 pair y_n = U W^T j_f, y_f = W U^T j_n (two launches), L2 flushed
+    farnear = None
+    if not args.no_farnear:
+        from paper_2206_12409_b200 import FarNear
+        tol_fn = max(cfg.tol, 1e-6)
+        fn = FarNear.build([synth.near_mesh(cfg.idx)], cfg.meshes(), cfg.freq, tol_fn)
+        fi = fn.info()
+        xf = device_gaussian(fi["m_far"], 1, 7101, dev)
+        xn = device_gaussian(fi["m_near"], 1, 7102, dev)
+        yn = torch.empty_like(xn)
+        yf = torch.empty_like(xf)
+        for _ in range(3):
+            fn.apply_pair_raw(xf.data_ptr(), yn.data_ptr(), xn.data_ptr(), yf.data_ptr())
+        ts = []
+        for i in range(20):
+            flush.fill_(i & 255)
+            e0.record()
+            fn.apply_pair_raw(xf.data_ptr(), yn.data_ptr(), xn.data_ptr(), yf.data_ptr())
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        fms = float(np.median(ts))
+        fbytes = 2 * fi["factor_bytes"] + 32 * (fi["m_far"] + fi["m_near"])
+        farnear = {"m_near": fi["m_near"], "m_far": fi["m_far"], "aca_tol": tol_fn, "rank": fi["rank"],
+                   "stop": fi["stop"], "aca_est_err": fi["est_err"], "build_s": fi["build_s"],
+                   "aca_entries": fi["entries_evaluated"], "pair_ms": fms, "pair_bytes": fbytes,
+                   "pair_gbs": fbytes / (fms * 1e-3) / 1e9,
+                   "note": ("near surface = synthetic open cylinder (synth.NEAR_COILS); pair = both Eq. 15 "
+                            "products, each factor read twice (dot + expand), median of 20, L2 flushed")}
+        fn.close()
+
     # ---- FP64 roofline of the entry kernel: measured FP64 instructions per entry x entries/s
     # over the measured DFMA issue rate (one FP64-pipe thread instruction per FMA)
     fp64_ops = None
@@ -575,6 +608,7 @@ def main():
                     if mode == "build" and inf["build_entry_s"] > 0 else None,
                     "structured_note": "supercore blocks evaluated by the TT-cross build (entries / entry-kernel time)"},
         "roofline": roof,
+        "farnear": farnear,
         "kernels": kern_table,
         "cpu_baseline": cpu,
         "e2e": e2e,
