@@ -840,3 +840,146 @@ def test_P46_aca_far_near_block_vs_dense():
     assert r_opt <= U.shape[1] <= 2 * r_opt + 10, (r_opt, U.shape[1])
     x = synth.complex_gaussian(Z.shape[1], 46)
     assert np.linalg.norm(farnear.apply_lowrank(U, W, x, "N") - Z @ x) <= 10 * tol * np.linalg.norm(Z) * np.linalg.norm(x)
+
+
+# ---------------------------------------------------------------- far-far block (NEXT-3)
+
+def _duffy(V, r, fn, order=48):
+    """int_T fn(r') dS' by splitting T into the signed sub-triangles (rho, V_i, V_i+1) about the
+    in-plane projection rho of r and a Duffy map r' = rho + u (d_i + v e_i), dS' = 2 A_i u du dv
+    (the 1/R singularity at rho is cancelled by the Jacobian), Gauss-Legendre order x order."""
+    V = np.asarray(V, dtype=np.float64)
+    n = np.cross(V[1] - V[0], V[2] - V[0])
+    n /= np.linalg.norm(n)
+    h = (r - V[0]) @ n
+    rho = r - h * n
+    x, w = np.polynomial.legendre.leggauss(order)
+    x = 0.5 * (x + 1)
+    w = 0.5 * w
+    U, Vv = np.meshgrid(x, x, indexing="ij")
+    WW = np.outer(w, w)
+    tot = 0
+    for i in range(3):
+        a, b = V[i], V[(i + 1) % 3]
+        d, e = a - rho, b - a
+        A2 = np.cross(d, e) @ n                     # 2 x signed area
+        P = rho + U[..., None] * (d + Vv[..., None] * e)
+        tot = tot + np.tensordot(WW * U * A2, fn(P), axes=([0, 1], [0, 1]))
+    return tot
+
+
+def test_P47_triangle_potentials_vs_duffy_quadrature():
+    """Closed-form I0 = int 1/R and I1 = int (r' - r)/R over a flat triangle against Duffy-mapped
+    Gauss quadrature: points in the plane (inside, at a quadrature node, outside, on a vertex, on
+    an edge) and off the plane."""
+    from oracle import farfar
+    rng = np.random.default_rng(47)
+    for trial in range(4):
+        V = rng.standard_normal((3, 3)) * 0.03
+        L = farfar.longest_edge(V)
+        n = np.cross(V[1] - V[0], V[2] - V[0])
+        n /= np.linalg.norm(n)
+        c = V.mean(axis=0)
+        pts = [c, V.T @ np.array([2 / 3, 1 / 6, 1 / 6]), c + 1.5 * (V[0] - c), V[1], 0.5 * (V[1] + V[2]),
+               c + 0.3 * L * n, V[2] + 0.05 * L * n, c + 2 * (V[1] - c) - 0.7 * L * n]
+        for r in pts:
+            I0, I1 = farfar.tri_potentials(V, r[None])
+            q0 = _duffy(V, r, lambda P: 1.0 / np.linalg.norm(P - r, axis=-1), order=160)
+            q1 = _duffy(V, r, lambda P: (P - r) / np.linalg.norm(P - r, axis=-1)[..., None], order=160)
+            assert abs(I0[0] - q0) <= 1e-12 * abs(q0), (trial, r, I0, q0)
+            assert np.max(np.abs(I1[0] - q1)) <= 1e-12 * np.max(np.abs(q1)), (trial, I1, q1)
+
+
+def _ff_tables(ci):
+    from oracle import farfar
+    cfg = synth.get_config(ci)
+    return cfg, farfar.rwg_triangle_tables(cfg.meshes()), 2 * np.pi * cfg.freq / synth.configs.C0
+
+
+def test_P48_near_pair_integral_within_rule_error():
+    """The near-pair K (analytic 1/R part + 3-point g_s remainder) against the same integral
+    with the inner integral done by Duffy-mapped Gauss quadrature of the full integrand: they
+    differ only by the 3-point rule's error on the bounded remainder g_s, which is
+    O((k0 L)^2) smaller than the 1/R part -- bound 0.01 (k0 L)^2 of |K| (measured 1.3e-4 self,
+    1.7e-5 adjacent at k0 L = 0.24), checked on the self pair and an edge-adjacent pair of cfg 2's
+    shield; the plain 3 x 3 rule misses the adjacent pair by > 1 % (the subtraction matters)."""
+    from oracle import farfar
+    cfg, T, k0 = _ff_tables(2)
+    for (m, sm), (n, sn) in (((0, "p"), (0, "p")), ((5, "p"), (5, "m")), ((7, "m"), (40, "p"))):
+        Va, pa = T["V" + sm][m], T["p" + sm][m]
+        Vb, pb = T["V" + sn][n], T["p" + sn][n]
+        if not farfar.is_near(Va, Vb):
+            continue
+        K = farfar.k_near_oneway(Va, pa, Vb, pb, k0)
+        ra = np.einsum("qj,jc->qc", geometry.TRI_BARY, Va)
+        ref = 0
+        for q in range(3):
+            f = lambda P, q=q: ((P - pb) @ (ra[q] - pa) - 4 / k0 ** 2) * np.exp(
+                -1j * k0 * np.linalg.norm(P - ra[q], axis=-1)) / (4 * np.pi * np.linalg.norm(P - ra[q], axis=-1))
+            ref += farfar.tri_area(Va) / 3 * _duffy(Vb, ra[q], f, order=48)
+        kL = k0 * max(farfar.longest_edge(Va), farfar.longest_edge(Vb))
+        assert abs(K - ref) <= 0.01 * kL ** 2 * abs(ref), (m, n, K, ref, kL)
+        if m != n or sm != sn:
+            assert abs(farfar.k_regular(Va, pa, Vb, pb, k0) - ref) > 0.01 * abs(ref)
+
+
+def test_P49_farfar_regular_entry_extended_precision():
+    """A regular (well separated) Z^ff entry against a 40-digit evaluation of the typed-out
+    mixed-potential formula with f = s (l/2A)(r - p), div f = s l / A and the 3 x 3 rule."""
+    from oracle import farfar
+    cfg, T, k0 = _ff_tables(1)
+    mp.mp.dps = 40
+    K0 = 2 * mp.pi * mp.mpf(synth.configs.FREQ_7T) / mp.mpf(synth.configs.C0)
+    m, n = 600, 3
+    Va0, Vb0 = T["Vp"][m], T["Vp"][n]
+    assert not farfar.is_near(Va0, Vb0)
+    tot = mp.mpc(0)
+    P = lambda v: [mp.mpf(float(x)) for x in v]
+    for sa, Va, pa in ((1, T["Vp"][m], T["pp"][m]), (-1, T["Vm"][m], T["pm"][m])):
+        for sb, Vb, pb in ((1, T["Vp"][n], T["pp"][n]), (-1, T["Vm"][n], T["pm"][n])):
+            A = [P(v) for v in Va]
+            B = [P(v) for v in Vb]
+            area = lambda X: mp.sqrt(sum(c * c for c in [
+                (X[1][1] - X[0][1]) * (X[2][2] - X[0][2]) - (X[1][2] - X[0][2]) * (X[2][1] - X[0][1]),
+                (X[1][2] - X[0][2]) * (X[2][0] - X[0][0]) - (X[1][0] - X[0][0]) * (X[2][2] - X[0][2]),
+                (X[1][0] - X[0][0]) * (X[2][1] - X[0][1]) - (X[1][1] - X[0][1]) * (X[2][0] - X[0][0])])) / 2
+            Aa, Ab = area(A), area(B)
+            lm, ln_ = mp.mpf(float(T["l"][m])), mp.mpf(float(T["l"][n]))
+            PA, PB = P(pa), P(pb)
+            for q in range(3):
+                wq = [mp.mpf(1) / 6] * 3
+                wq[q] = mp.mpf(2) / 3
+                rq = [sum(wq[j] * A[j][c] for j in range(3)) for c in range(3)]
+                for s in range(3):
+                    ws = [mp.mpf(1) / 6] * 3
+                    ws[s] = mp.mpf(2) / 3
+                    rs = [sum(ws[j] * B[j][c] for j in range(3)) for c in range(3)]
+                    fm = [sa * lm / (2 * Aa) * (rq[c] - PA[c]) for c in range(3)]
+                    fn = [sb * ln_ / (2 * Ab) * (rs[c] - PB[c]) for c in range(3)]
+                    div = (sa * lm / Aa) * (sb * ln_ / Ab)
+                    R = mp.sqrt(sum((rq[c] - rs[c]) ** 2 for c in range(3)))
+                    g = mp.exp(-1j * K0 * R) / (4 * mp.pi * R)
+                    tot += (Aa / 3) * (Ab / 3) * (sum(fm[c] * fn[c] for c in range(3)) - div / K0 ** 2) * g
+    got = farfar.entries_ff(T, k0, [m], [n])[0]
+    assert abs(got - complex(tot)) <= 1e-13 * abs(complex(tot)), (got, tot)
+
+
+def test_P50_farfar_symmetry_and_near_rule():
+    """Z^ff is symmetric by construction, the diagonal carries the near (singular) rule, and
+    the near rule changes a regular pair's K only by the 3-point rule error."""
+    from oracle import farfar
+    cfg, T, k0 = _ff_tables(1)
+    rng = np.random.default_rng(50)
+    r = rng.integers(0, len(T["l"]), 40)
+    c = rng.integers(0, len(T["l"]), 40)
+    assert np.array_equal(farfar.entries_ff(T, k0, r, c), farfar.entries_ff(T, k0, c, r))
+    assert farfar.is_near(T["Vp"][3], T["Vp"][3])
+    # a pair just outside the near radius: both rules agree to ~ the 3-point error
+    Va, pa = T["Vp"][0], T["pp"][0]
+    d = np.linalg.norm(T["Vp"].mean(axis=1) - Va.mean(axis=0), axis=1)
+    far = np.flatnonzero(~farfar.is_near(np.broadcast_to(Va, T["Vp"].shape), T["Vp"]))
+    j = far[np.argmin(d[far])]
+    Kr = farfar.k_regular(Va, pa, T["Vp"][j], T["pp"][j], k0)
+    Kn = 0.5 * (farfar.k_near_oneway(Va, pa, T["Vp"][j], T["pp"][j], k0)
+                + farfar.k_near_oneway(T["Vp"][j], T["pp"][j], Va, pa, k0))
+    assert abs(Kr - Kn) <= 2e-3 * abs(Kn), (Kr, Kn)
