@@ -69,6 +69,11 @@ class vsie_farnear_info(C.Structure):
                 ("entries_evaluated", C.c_int64), ("factor_bytes", C.c_int64), ("apply_calls", C.c_int64)]
 
 
+class vsie_farfar_info(C.Structure):
+    _fields_ = [("m", C.c_int64), ("tile", C.c_int32), ("tiles", C.c_int64), ("matrix_bytes", C.c_int64),
+                ("near_pairs", C.c_int64), ("build_s", C.c_double), ("k0", C.c_double), ("apply_calls", C.c_int64)]
+
+
 HANDLE = C.c_void_p
 
 _SIGS = {
@@ -115,6 +120,14 @@ _SIGS = {
     "vsie_farnear_export": (C.c_int32, [HANDLE, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "vsie_farnear_get_info": (C.c_int32, [HANDLE, C.POINTER(vsie_farnear_info)]),
     "vsie_farnear_destroy": (None, [HANDLE]),
+    # include/vsie_farfar.h
+    "vsie_farfar_build": (C.c_int32, [C.POINTER(vsie_mesh), C.c_int32, C.c_double, C.c_double, C.c_double, C.c_int32,
+                                      C.POINTER(HANDLE)]),
+    "vsie_farfar_entries": (C.c_int32, [HANDLE, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "vsie_farfar_apply": (C.c_int32, [HANDLE, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
+    "vsie_farfar_export": (C.c_int32, [HANDLE, C.c_void_p]),
+    "vsie_farfar_get_info": (C.c_int32, [HANDLE, C.POINTER(vsie_farfar_info)]),
+    "vsie_farfar_destroy": (None, [HANDLE]),
 }
 
 
@@ -123,7 +136,7 @@ def header_symbols(paths=None):
     if paths is None:
         paths = sorted(os.path.join(INCLUDE, f) for f in os.listdir(INCLUDE) if f.endswith(".h"))
     txt = "".join(open(p).read() for p in paths)
-    return sorted(set(re.findall(r"\b(vsie_[a-z_]+)\s*\(", txt)) - {"vsie_coupling_t", "vsie_farnear_t"})
+    return sorted(set(re.findall(r"\b(vsie_[a-z_]+)\s*\(", txt)) - {"vsie_coupling_t", "vsie_farnear_t", "vsie_farfar_t"})
 
 
 class VsieError(RuntimeError):

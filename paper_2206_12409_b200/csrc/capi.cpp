@@ -10,6 +10,7 @@
 #include <string>
 
 #include "cross.hpp"
+#include "farfar.hpp"
 #include "farnear.hpp"
 #include "handle.hpp"
 
@@ -584,6 +585,66 @@ int32_t vsie_farnear_get_info(vsie_farnear_t h, vsie_farnear_info* out) {
 }
 
 void vsie_farnear_destroy(vsie_farnear_t h) {
+  if (!h) return;
+  cudaDeviceSynchronize();
+  delete h;
+}
+
+// ----------------------------------------------------------------- far-far block (vsie_farfar.h)
+int32_t vsie_farfar_build(const vsie_mesh* meshes, int32_t n_meshes, double freq_hz, double scale_re, double scale_im,
+                          int32_t device, vsie_farfar_t* out) {
+  if (out) *out = nullptr;
+  return guarded([&] {
+    VSIE_REQUIRE(out != nullptr, VSIE_ERR_ARG, "farfar_build: NULL out");
+    std::unique_ptr<vsie_farfar_s> h(new vsie_farfar_s());
+    farfar_build(meshes, n_meshes, freq_hz, scale_re, scale_im, device, h.get());
+    *out = h.release();
+    return VSIE_OK;
+  });
+}
+
+int32_t vsie_farfar_entries(vsie_farfar_t h, const int64_t* idx, int64_t count, void* out, void* stream) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "NULL handle");
+    farfar_entries(h, idx, count, out, static_cast<cudaStream_t>(stream));
+    return VSIE_OK;
+  });
+}
+
+int32_t vsie_farfar_apply(vsie_farfar_t h, const void* x, void* y, int32_t op, int32_t nrhs, int32_t accumulate,
+                          void* stream) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "NULL handle");
+    farfar_apply(h, x, y, op, nrhs, accumulate != 0, static_cast<cudaStream_t>(stream));
+    return VSIE_OK;
+  });
+}
+
+int32_t vsie_farfar_export(vsie_farfar_t h, void* host_dense) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "NULL handle");
+    farfar_export(h, host_dense);
+    return VSIE_OK;
+  });
+}
+
+int32_t vsie_farfar_get_info(vsie_farfar_t h, vsie_farfar_info* out) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr && out != nullptr, VSIE_ERR_ARG, "NULL argument");
+    std::memset(out, 0, sizeof(*out));
+    out->m = h->m;
+    out->tile = 128;
+    out->tiles = h->tiles;
+    out->matrix_bytes = (int64_t)h->Z.bytes();
+    out->near_pairs = h->near_pairs;
+    out->build_s = h->build_s;
+    out->k0 = h->k0;
+    out->apply_calls = h->apply_calls;
+    return VSIE_OK;
+  });
+}
+
+void vsie_farfar_destroy(vsie_farfar_t h) {
   if (!h) return;
   cudaDeviceSynchronize();
   delete h;

@@ -31,7 +31,9 @@ struct EdgeRec {
   int64_t opp;   // vertex opposite the edge in `tri`
 };
 
-void append_mesh(const vsie_mesh& mesh, std::vector<double>& table) {
+}  // namespace
+
+std::vector<RwgRec> extract_rwgs(const vsie_mesh& mesh) {
   VSIE_REQUIRE(mesh.xyz != nullptr && mesh.tri != nullptr, VSIE_ERR_ARG, "mesh arrays are NULL");
   VSIE_REQUIRE(mesh.n_vertices >= 3 && mesh.n_triangles >= 1, VSIE_ERR_ARG, "mesh too small");
   VSIE_REQUIRE(mesh.n_vertices < (int64_t(1) << 31), VSIE_ERR_ARG, "too many vertices");
@@ -67,43 +69,53 @@ void append_mesh(const vsie_mesh& mesh, std::vector<double>& table) {
   std::sort(recs.begin(), recs.end(), [](const EdgeRec& p, const EdgeRec& q) {
     return p.key != q.key ? p.key < q.key : p.tri < q.tri;
   });
-  // barycentric interior rule (2/3, 1/6, 1/6) and permutations
-  const double b_hi = 2.0 / 3.0, b_lo = 1.0 / 6.0;
+  std::vector<RwgRec> out;
   size_t i = 0;
   while (i < recs.size()) {
     size_t j = i + 1;
     while (j < recs.size() && recs[j].key == recs[i].key) ++j;
-    const size_t cnt = j - i;
-    VSIE_REQUIRE(cnt <= 2, VSIE_ERR_GEOMETRY, "edge shared by more than two triangles");
-    if (cnt == 2) {
+    VSIE_REQUIRE(j - i <= 2, VSIE_ERR_GEOMETRY, "edge shared by more than two triangles");
+    if (j - i == 2) {
       const EdgeRec& P = recs[i];      // T+ : smaller triangle id
       const EdgeRec& M = recs[i + 1];  // T-
-      const int64_t a = (int64_t)(P.key >> 32), b = (int64_t)(P.key & 0xffffffffu);
-      double l = 0;
-      for (int c = 0; c < 3; ++c) {
-        double d = X[3 * a + c] - X[3 * b + c];
-        l += d * d;
-      }
-      l = std::sqrt(l);
-      const double coef = l / 6.0;
-      double rec[kSrcStride];
-      for (int side = 0; side < 2; ++side) {
-        const EdgeRec& E = side == 0 ? P : M;
-        const int64_t v0 = T[3 * E.tri], v1 = T[3 * E.tri + 1], v2 = T[3 * E.tri + 2];
-        for (int q = 0; q < 3; ++q) {
-          const double w0 = q == 0 ? b_hi : b_lo, w1 = q == 1 ? b_hi : b_lo, w2 = q == 2 ? b_hi : b_lo;
-          double* o = rec + 6 * (3 * side + q);
-          for (int c = 0; c < 3; ++c) {
-            const double r = w0 * X[3 * v0 + c] + w1 * X[3 * v1 + c] + w2 * X[3 * v2 + c];
-            const double p = X[3 * E.opp + c];
-            o[c] = r;
-            o[3 + c] = side == 0 ? coef * (r - p) : coef * (p - r);  // J+ = l/6 (r - p+), J- = l/6 (p- - r)
-          }
-        }
-      }
-      table.insert(table.end(), rec, rec + kSrcStride);
+      out.push_back({P.tri, M.tri, P.opp, M.opp, (int64_t)(P.key >> 32), (int64_t)(P.key & 0xffffffffu)});
     }
     i = j;
+  }
+  return out;
+}
+
+namespace {
+
+void append_mesh(const vsie_mesh& mesh, std::vector<double>& table) {
+  const double* X = mesh.xyz;
+  const int32_t* T = mesh.tri;
+  // barycentric interior rule (2/3, 1/6, 1/6) and permutations
+  const double b_hi = 2.0 / 3.0, b_lo = 1.0 / 6.0;
+  for (const RwgRec& r : extract_rwgs(mesh)) {
+    double l = 0;
+    for (int c = 0; c < 3; ++c) {
+      double d = X[3 * r.a + c] - X[3 * r.b + c];
+      l += d * d;
+    }
+    l = std::sqrt(l);
+    const double coef = l / 6.0;
+    double rec[kSrcStride];
+    for (int side = 0; side < 2; ++side) {
+      const int64_t tri = side == 0 ? r.tp : r.tm, opp = side == 0 ? r.pp : r.pm;
+      const int64_t v0 = T[3 * tri], v1 = T[3 * tri + 1], v2 = T[3 * tri + 2];
+      for (int q = 0; q < 3; ++q) {
+        const double w0 = q == 0 ? b_hi : b_lo, w1 = q == 1 ? b_hi : b_lo, w2 = q == 2 ? b_hi : b_lo;
+        double* o = rec + 6 * (3 * side + q);
+        for (int c = 0; c < 3; ++c) {
+          const double rr = w0 * X[3 * v0 + c] + w1 * X[3 * v1 + c] + w2 * X[3 * v2 + c];
+          const double p = X[3 * opp + c];
+          o[c] = rr;
+          o[3 + c] = side == 0 ? coef * (rr - p) : coef * (p - rr);  // J+ = l/6 (r - p+), J- = l/6 (p- - r)
+        }
+      }
+    }
+    table.insert(table.end(), rec, rec + kSrcStride);
   }
 }
 

@@ -31,6 +31,13 @@ struct GridDesc {
 // Validates and converts the public structs; throws Error(VSIE_ERR_ARG / VSIE_ERR_GEOMETRY).
 GridDesc make_grid(const vsie_grid* g);
 Sources build_sources(const vsie_mesh* meshes, int n_meshes, const GridDesc& grid);
+// One RWG function of a mesh (canonical order): T+ / T- triangle ids, the
+// vertices opposite the shared edge (p+, p-) and the shared edge's vertices (a < b).
+struct RwgRec {
+  int64_t tp, tm, pp, pm, a, b;
+};
+// Validates one mesh (degenerate / non-manifold -> VSIE_ERR_GEOMETRY) and lists its RWGs.
+std::vector<RwgRec> extract_rwgs(const vsie_mesh& mesh);
 // The RWG table alone (no voxel-grid check): the surface-surface blocks (farnear.cu).
 Sources build_rwg_sources(const vsie_mesh* meshes, int n_meshes);
 // Longest triangle edge of the meshes (validated by build_rwg_sources first).

@@ -118,3 +118,69 @@ class FarNear:
     def apply_pair_raw(self, xf_ptr: int, yn_ptr: int, xn_ptr: int, yf_ptr: int, stream=None):
         check(lib().vsie_farnear_apply_pair(self._h, C.c_void_p(xf_ptr), C.c_void_p(yn_ptr), C.c_void_p(xn_ptr),
                                             C.c_void_p(yf_ptr), _stream_ptr(stream)))
+
+
+class FarFar:
+    """Dense far-far block Z_cc^ff (include/vsie_farfar.h): symmetric, lower-triangle tiles."""
+
+    def __init__(self, handle):
+        self._h = _lib.HANDLE(handle)
+
+    @classmethod
+    def build(cls, far_meshes, freq: float, scale=1.0, device=-1):
+        arr, keep = _meshes_c(far_meshes)
+        h = _lib.HANDLE()
+        check(lib().vsie_farfar_build(arr, len(far_meshes), float(freq), float(np.real(scale)), float(np.imag(scale)),
+                                      int(device), C.byref(h)))
+        del keep
+        return cls(h.value)
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            lib().vsie_farfar_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> dict:
+        i = _lib.vsie_farfar_info()
+        check(lib().vsie_farfar_get_info(self._h, C.byref(i)))
+        return dict(m=i.m, tile=i.tile, tiles=i.tiles, matrix_bytes=i.matrix_bytes, near_pairs=i.near_pairs,
+                    build_s=i.build_s, k0=i.k0, apply_calls=i.apply_calls)
+
+    def export(self):
+        m = self.info()["m"]
+        Z = np.empty((m, m), dtype=np.complex128, order="F")
+        check(lib().vsie_farfar_export(self._h, Z.ctypes.data))
+        return Z
+
+    def entries(self, rows, cols, stream=None):
+        torch = _torch()
+        idx = torch.stack([torch.as_tensor(rows, dtype=torch.int64), torch.as_tensor(cols, dtype=torch.int64)],
+                          dim=1).contiguous().cuda()
+        out = torch.empty(idx.shape[0], dtype=torch.complex128, device=idx.device)
+        check(lib().vsie_farfar_entries(self._h, C.c_void_p(idx.data_ptr()), idx.shape[0], C.c_void_p(out.data_ptr()),
+                                        _stream_ptr(stream)))
+        return out
+
+    def apply(self, x, op: str = "N", out=None, accumulate=False, stream=None):
+        torch = _torch()
+        vec = x.dim() == 1
+        X = x.reshape(-1, 1) if vec else x
+        nrhs = X.shape[1]
+        Xc = X.t().contiguous()
+        if out is None:
+            Y = torch.empty_like(Xc)
+        else:
+            Y = out.reshape(-1, 1).t() if vec else out.t()
+        check(lib().vsie_farfar_apply(self._h, C.c_void_p(Xc.data_ptr()), C.c_void_p(Y.data_ptr()), _lib.OPS[op], nrhs,
+                                      1 if accumulate else 0, _stream_ptr(stream)))
+        return Y[0] if vec else Y.t()
+
+    def apply_raw(self, x_ptr: int, y_ptr: int, op: str = "N", accumulate=False, stream=None):
+        check(lib().vsie_farfar_apply(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr), _lib.OPS[op], 1,
+                                      1 if accumulate else 0, _stream_ptr(stream)))
