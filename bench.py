@@ -476,8 +476,8 @@ def main():
     # coil, then the Eq. 15 pair y_n = U W^T j_f, y_f = W U^T j_n (two launches), L2 flushed
     farnear = None
     if not args.no_farnear:
-        from paper_2206_12409_b200 import FarNear
-        tol_fn = max(cfg.tol, 1e-6)
+        from paper_2206_12409_b200 import FarFar, FarNear
+        tol_fn = 1e-3   # the hybrid method's ACA tolerance
         fn = FarNear.build([synth.near_mesh(cfg.idx)], cfg.meshes(), cfg.freq, tol_fn)
         fi = fn.info()
         xf = device_gaussian(fi["m_far"], 1, 7101, dev)
@@ -496,12 +496,34 @@ def main():
             ts.append(e0.elapsed_time(e1))
         fms = float(np.median(ts))
         fbytes = 2 * fi["factor_bytes"] + 32 * (fi["m_far"] + fi["m_near"])
+        # dense far-far block Z_cc^ff: symmetric lower-triangle tiles, one read per apply
+        ff = FarFar.build(cfg.meshes(), cfg.freq)
+        ffi = ff.info()
+        for _ in range(3):
+            ff.apply_raw(xf.data_ptr(), yf.data_ptr())
+        ts2 = []
+        for i in range(20):
+            flush.fill_(i & 255)
+            e0.record()
+            ff.apply_raw(xf.data_ptr(), yf.data_ptr())
+            e1.record()
+            torch.cuda.synchronize()
+            ts2.append(e0.elapsed_time(e1))
+        ffms = float(np.median(ts2))
+        ff.close()
         farnear = {"m_near": fi["m_near"], "m_far": fi["m_far"], "aca_tol": tol_fn, "rank": fi["rank"],
                    "stop": fi["stop"], "aca_est_err": fi["est_err"], "build_s": fi["build_s"],
                    "aca_entries": fi["entries_evaluated"], "pair_ms": fms, "pair_bytes": fbytes,
                    "pair_gbs": fbytes / (fms * 1e-3) / 1e9,
+                   "pair_frac": fbytes / (fms * 1e-3) / 1e9 / load_peaks()[0],
                    "note": ("near surface = synthetic open cylinder (synth.NEAR_COILS); pair = both Eq. 15 "
-                            "products, each factor read twice (dot + expand), median of 20, L2 flushed")}
+                            "products, each factor read twice (dot + expand), median of 20, L2 flushed"),
+                   "farfar": {"m": ffi["m"], "build_s": ffi["build_s"], "matrix_bytes": ffi["matrix_bytes"],
+                              "near_pairs": ffi["near_pairs"], "apply_ms": ffms,
+                              "apply_gbs": ffi["matrix_bytes"] / (ffms * 1e-3) / 1e9,
+                              "apply_frac": ffi["matrix_bytes"] / (ffms * 1e-3) / 1e9 / load_peaks()[0],
+                              "dense_equivalent_gbs": 16 * ffi["m"] ** 2 / (ffms * 1e-3) / 1e9,
+                              "note": "Z_cc^ff y = Z x from the symmetric half (128 x 128 lower tiles, read once)"}}
         fn.close()
 
     # ---- FP64 roofline of the entry kernel: measured FP64 instructions per entry x entries/s

@@ -10,10 +10,11 @@
 //  * k_ff_fill: one thread per stored element of the 128 x 128 lower-triangle tiles (the
 //    symmetric half of the matrix: 8 x 10^8 entries at cfg 4, 12.8 GB).
 //  * k_ff_tiles + k_ff_sum: the symmetric GEMV.  Z is HBM-bound (AI 0.5 flop/B), so each stored
-//    tile is read ONCE for both of its products, Z_IJ x_J (rows) and Z_IJ^T x_I (columns):
-//    warp w takes columns j = w + 8 c, lane the rows lane + 32 q (4 coalesced 512-B segments per
-//    column), the column sums reduce across the warp by shuffles.  Per-tile partials ([tile][2
-//    x 128]) are summed per output block in a fixed order by k_ff_sum (bitwise reproducible).
+//    tile is read ONCE for both of its products, Z_IJ x_J (rows) and Z_IJ^T x_I (columns): one
+//    warp per tile, lane the rows lane + 32 q (4 coalesced 512-B segments per column), 4 columns
+//    in flight, the column sums reduced across the warp by shuffles, no block barrier.  Per-tile
+//    partials ([tile][2 x 128]) are summed per output block in a fixed order by k_ff_sum
+//    (bitwise reproducible).
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -205,64 +206,57 @@ __global__ void __launch_bounds__(256) k_ff_list(FfGeom g, const int64_t* __rest
 
 __device__ __forceinline__ cplx opz(cplx v, int conj) { return conj ? cconj(v) : v; }
 
-// per stored tile (I, J): part[t][0..128) = Z_IJ x_J, part[t][128..256) = Z_IJ^T x_I (I > J)
+// per stored tile (I, J): part[t][0..128) = Z_IJ x_J, part[t][128..256) = Z_IJ^T x_I (I > J).
+// One WARP per tile (no block barriers): lane holds rows lane + 32 q (q < 4) of the row sums;
+// for each column j the 4 elements are coalesced 512-B segments, the column sum is a warp
+// shuffle reduction.  Columns are unrolled by 4 (16 independent 16-B loads per lane in flight).
 __global__ void __launch_bounds__(256) k_ff_tiles(const cplx* __restrict__ Z, int64_t tiles, int64_t m,
                                                   const cplx* __restrict__ x, int conj, cplx* __restrict__ part) {
-  __shared__ cplx xJ[kTile], xI[kTile];
-  __shared__ cplx red[8][kTile];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   pdl_wait();
-  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+  for (int64_t t = warp; t < tiles; t += nwarps) {
     int I, J;
     tile_ij(t, I, J);
-    __syncthreads();
-    if (threadIdx.x < kTile) {
-      const int64_t r = (int64_t)J * kTile + threadIdx.x;
-      xJ[threadIdx.x] = r < m ? x[r] : cmk(0, 0);
-    } else {
-      const int64_t r = (int64_t)I * kTile + threadIdx.x - kTile;
-      xI[threadIdx.x - kTile] = r < m ? x[r] : cmk(0, 0);
-    }
-    __syncthreads();
-    const cplx* Zt = Z + t * kTile * kTile;
-    cplx acc[4];
-    cplx xi[4];
+    const int64_t i0 = (int64_t)I * kTile, j0 = (int64_t)J * kTile;
+    cplx xi[4], acc[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
+      const int64_t r = i0 + lane + 32 * q;
+      xi[q] = r < m ? x[r] : cmk(0, 0);
       acc[q] = cmk(0, 0);
-      xi[q] = xI[lane + 32 * q];
     }
     const bool offdiag = I != J;
-#pragma unroll 2
-    for (int j = w; j < kTile; j += 8) {
-      const cplx* col = Zt + (int64_t)kTile * j;
-      cplx z[4];
+    const cplx* Zt = Z + t * kTile * kTile + lane;
+    cplx* pt = part + t * 2 * kTile;
+    for (int j = 0; j < kTile; j += 4) {
+      cplx z[4][4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) z[q] = opz(__ldcs(col + lane + 32 * q), conj);
-      const cplx xj = xJ[j];
-      cplx cs = cmk(0, 0);
+      for (int c = 0; c < 4; ++c)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        cfma(acc[q], z[q], xj);
-        cfma(cs, z[q], xi[q]);
-      }
-      if (offdiag) {
-        for (int o = 16; o > 0; o >>= 1) {
-          cs.x += __shfl_xor_sync(0xffffffffu, cs.x, o);
-          cs.y += __shfl_xor_sync(0xffffffffu, cs.y, o);
+        for (int q = 0; q < 4; ++q) z[c][q] = opz(__ldcs(Zt + (int64_t)kTile * (j + c) + 32 * q), conj);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int64_t cj = j0 + j + c;
+        const cplx xj = cj < m ? x[cj] : cmk(0, 0);
+        cplx cs = cmk(0, 0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          cfma(acc[q], z[c][q], xj);
+          cfma(cs, z[c][q], xi[q]);
         }
-        if (lane == 0) part[t * 2 * kTile + kTile + j] = cs;
+        if (offdiag) {
+          for (int o = 16; o > 0; o >>= 1) {
+            cs.x += __shfl_xor_sync(0xffffffffu, cs.x, o);
+            cs.y += __shfl_xor_sync(0xffffffffu, cs.y, o);
+          }
+          if (lane == 0) pt[kTile + j + c] = cs;
+        }
       }
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) red[w][lane + 32 * q] = acc[q];
-    __syncthreads();
-    if (threadIdx.x < kTile) {
-      cplx s = red[0][threadIdx.x];
-#pragma unroll
-      for (int q = 1; q < 8; ++q) s = cadd(s, red[q][threadIdx.x]);
-      part[t * 2 * kTile + threadIdx.x] = s;
-    }
+    for (int q = 0; q < 4; ++q) pt[lane + 32 * q] = acc[q];
   }
   pdl_trigger();
 }

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("cfgs", nargs="*", type=int, default=[1, 2, 4])
     ap.add_argument("--tol", type=float, default=None)
     ap.add_argument("--iters", type=int, default=200)
+    ap.add_argument("--ff", action="store_true", help="also build Z_cc^ff and time its apply")
     a = ap.parse_args()
     for ci in a.cfgs:
         cfg = synth.get_config(ci)
@@ -57,6 +58,25 @@ def main():
             factor = 16 * k * (mn + mf)
             moved = 2 * factor if mode == "pair" else factor
             res[mode] = dict(ms=ms, factor_bytes=factor, moved_bytes=moved, gbs=moved / ms / 1e6)
+        if a.ff:
+            from paper_2206_12409_b200 import FarFar
+            ff = FarFar.build(cfg.meshes(), cfg.freq)
+            fi = ff.info()
+            for _ in range(3):
+                ff.apply_raw(xf.data_ptr(), yf.data_ptr())
+            ts = []
+            for it in range(min(a.iters, 50)):
+                flush.fill_(it & 255)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                ff.apply_raw(xf.data_ptr(), yf.data_ptr())
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            ms = float(np.median(ts))
+            res["ff"] = dict(build_s=fi["build_s"], matrix_bytes=fi["matrix_bytes"], near_pairs=fi["near_pairs"],
+                             ms=ms, gbs=fi["matrix_bytes"] / ms / 1e6)
+            ff.close()
         print(json.dumps(dict(cfg=ci, tol=tol, m_near=mn, m_far=mf, rank=k, stop=inf["stop"],
                               est_err=inf["est_err"], build_s=inf["build_s"], min_distance=inf["min_distance"],
                               max_edge=inf["max_edge"], **res)), flush=True)
