@@ -67,7 +67,8 @@ struct Ctx {
   double tol, delta;
   uint64_t seed;
   uint64_t sketch_counter = 0;
-  double t_entry = 0, t_factor = 0, t_maxvol = 0;
+  double t_entry = 0, t_factor = 0, t_maxvol = 0, t_maxvol_lu = 0;
+  int64_t maxvol_swaps = 0;
   int64_t n_eval = 0;
   int64_t jacobi_sweeps = 0;
   double t_jsmall = 0, t_chol = 0, t_gemm = 0;
@@ -588,14 +589,43 @@ std::vector<int> maxvol(Ctx& c, cplx* A, int64_t n, int r, cplx* Bout) {
     VSIE_CHECK_CUDA(cudaMemsetAsync(w.bad.p, 0, sizeof(int), c.st));
   }
   // 1. initial pivots: LU with partial pivoting (rows physically swapped)
-  launch_lu_update(A, n, r, -1, w.partials.p, nparts, c.st);
-  for (int j = 0; j < r; ++j) {
-    launch_lu_pivot(A, n, r, j, w.perm.p, w.partials.p, nparts, w.bad.p, c.st);
-    launch_lu_update(A, n, r, j, w.partials.p, nparts, c.st);
+  const auto t_lu = Clock::now();
+  // blocked right-looking: per panel of kLuPanel columns the unblocked steps restricted to the
+  // panel, then U12 = L11^{-1} A12 and A22 -= L21 U12 (one ZGEMM) -- the same pivots as the
+  // column-by-column LU up to the rounding order of the trailing updates, at n r^2 / kLuPanel
+  // instead of n r^2 bytes of rank-1 update traffic
+  launch_lu_update(A, n, r, -1, r, false, true, w.partials.p, nparts, c.st);
+  for (int j0 = 0; j0 < r; j0 += kLuPanel) {
+    const int jb = std::min(kLuPanel, r - j0);
+    for (int j = j0; j < j0 + jb; ++j) {
+      launch_lu_pivot(A, n, r, j, w.perm.p, w.partials.p, nparts, w.bad.p, c.st);
+      launch_lu_update(A, n, r, j, j0 + jb, true, j + 1 < j0 + jb, w.partials.p, nparts, c.st);
+    }
+    if (j0 + jb < r) {
+      launch_lu_trsm(A, n, r, j0, jb, c.st);
+      Zgemm z{};
+      z.nbatch = 1;
+      z.ta = kN;
+      z.tb = kN;
+      z.M[0] = n - j0 - jb;
+      z.N[0] = r - j0 - jb;
+      z.K[0] = jb;
+      z.A[0] = A + (j0 + jb) + n * j0;
+      z.lda[0] = n;
+      z.B[0] = A + j0 + n * (j0 + jb);
+      z.ldb[0] = n;
+      z.C[0] = A + (j0 + jb) + n * (j0 + jb);
+      z.ldc[0] = n;
+      z.alpha = cmk(-1, 0);
+      z.beta = cmk(1, 0);
+      if (z.M[0] > 0) launch_zgemm(z, nullptr, 0, c.st);
+      launch_lu_update(A, n, r, j0 + jb - 1, r, false, true, w.partials.p, nparts, c.st);   // next pivot column
+    }
   }
   int bad = 0;
   VSIE_CHECK_CUDA(cudaMemcpyAsync(&bad, w.bad.p, sizeof(int), cudaMemcpyDeviceToHost, c.st));
   sync(c);
+  c.t_maxvol_lu += secs(t_lu);
   VSIE_REQUIRE(!bad, VSIE_ERR_CUDA, "maxvol: rank-deficient factor (zero pivot in LU)");
   // 2. B_perm = [I_r ; L2 L1^{-1}]
   w.Lr.ensure((int64_t)r * r);
@@ -631,6 +661,7 @@ std::vector<int> maxvol(Ctx& c, cplx* A, int64_t n, int r, cplx* Bout) {
     sync(c);
     if (hs.done) break;
   }
+  c.maxvol_swaps += hs.swaps;
   // 4. outputs in the original row order
   std::vector<int> perm(n), pos(r), piv(r);
   VSIE_CHECK_CUDA(cudaMemcpyAsync(perm.data(), w.perm.p, n * sizeof(int), cudaMemcpyDeviceToHost, c.st));
@@ -876,9 +907,9 @@ int cross_chi(Ctx& c, int chi, Heldout& ho) {
     sync(c);
     const double e = heldout_error(c, s, ho);
     if (c.o.verbose)
-      fprintf(stderr, "[vsie cross] chi %d sweep %d ranks (%d, %d, %d) heldout %.3e  (entry %.2fs factor %.2fs [cholqr %.2f jacobi(R) %.2f gemm %.2f] maxvol %.2fs, jacobi sweeps %ld)\n",
+      fprintf(stderr, "[vsie cross] chi %d sweep %d ranks (%d, %d, %d) heldout %.3e  (entry %.2fs factor %.2fs [cholqr %.2f jacobi(R) %.2f gemm %.2f] maxvol %.2fs [LU %.2f, %lld swaps], jacobi sweeps %ld)\n",
               chi, sweep, s.r[1], s.r[2], s.r[3], e, c.t_entry, c.t_factor, c.t_chol, c.t_jsmall, c.t_gemm,
-              c.t_maxvol, (long)c.jacobi_sweeps);
+              c.t_maxvol, c.t_maxvol_lu, (long long)c.maxvol_swaps, (long)c.jacobi_sweeps);
     if (e < best_e) {
       best_e = e;
       for (int k = 0; k < 5; ++k) best_r[k] = s.r[k];

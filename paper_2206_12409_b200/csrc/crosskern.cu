@@ -226,12 +226,17 @@ __device__ void block_argmax(ArgMax& m, ArgMax* sh /* >= 8 */) {
   m = sh[0];
 }
 
-__global__ void __launch_bounds__(NT) k_lu_update(cplx* W, int64_t n, int r, int j, ArgMax* partials) {
+// Step j of the LU: scale column j below the diagonal (when scale), rank-1 update of columns
+// (j, c1), then argmax partials of column j + 1 over rows > j (when j + 1 < r and argmax).
+// The blocked LU (panel width kLuPanel) passes c1 = the panel end; the trailing columns are
+// updated by a TRSM + ZGEMM per panel.
+__global__ void __launch_bounds__(NT) k_lu_update(cplx* W, int64_t n, int r, int j, int c1, int scale, int argmax,
+                                                  ArgMax* partials) {
   extern __shared__ cplx urow[];
   __shared__ cplx inv;
   __shared__ ArgMax sh[8];
-  if (j >= 0) {
-    for (int c = j + 1 + threadIdx.x; c < r; c += NT) urow[c] = W[j + n * c];
+  if (j >= 0 && scale) {
+    for (int c = j + 1 + threadIdx.x; c < c1; c += NT) urow[c] = W[j + n * c];
     if (threadIdx.x == 0) {
       const cplx pv = W[j + n * j];
       const double d = cabs2(pv);
@@ -241,10 +246,10 @@ __global__ void __launch_bounds__(NT) k_lu_update(cplx* W, int64_t n, int r, int
   }
   ArgMax best{-1.0, INT64_MAX, -1, j + 1};
   for (int64_t i = j + 1 + blockIdx.x * (int64_t)NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NT) {
-    if (j >= 0) {
+    if (j >= 0 && scale) {
       const cplx l = cmul(W[i + n * j], inv);
       W[i + n * j] = l;
-      for (int c = j + 1; c < r; ++c) {
+      for (int c = j + 1; c < c1; ++c) {
         const cplx u = urow[c];
         cplx w = W[i + n * c];
         w.x -= l.x * u.x - l.y * u.y;
@@ -252,13 +257,37 @@ __global__ void __launch_bounds__(NT) k_lu_update(cplx* W, int64_t n, int r, int
         W[i + n * c] = w;
       }
     }
-    if (j + 1 < r) {
+    if (argmax && j + 1 < r) {
       const double v = cabs2(W[i + n * (j + 1)]);
       if (better(v, i, best.v, best.key)) { best.v = v; best.key = i; best.i = i; }
     }
   }
   block_argmax(best, sh);
   if (threadIdx.x == 0) partials[blockIdx.x] = best;
+}
+
+// U12 = L11^{-1} A12 in place: L11 the unit lower jb x jb block at (j0, j0), A12 rows
+// [j0, j0 + jb), columns [j0 + jb, r); one thread per column, L11 in smem
+__global__ void __launch_bounds__(NT) k_lu_trsm(cplx* W, int64_t n, int r, int j0, int jb) {
+  __shared__ cplx L[kLuPanel * kLuPanel];
+  for (int e = threadIdx.x; e < jb * jb; e += NT) {
+    const int i = e % jb, k = e / jb;
+    L[e] = W[(j0 + i) + n * (j0 + k)];
+  }
+  __syncthreads();
+  const int64_t c = (int64_t)j0 + jb + blockIdx.x * (int64_t)NT + threadIdx.x;
+  if (c >= r) return;
+  cplx x[kLuPanel];
+  for (int i = 0; i < jb; ++i) {
+    cplx v = W[(j0 + i) + n * c];
+    for (int k = 0; k < i; ++k) {
+      const cplx l = L[i + jb * k];
+      v.x -= l.x * x[k].x - l.y * x[k].y;
+      v.y -= l.x * x[k].y + l.y * x[k].x;
+    }
+    x[i] = v;
+    W[(j0 + i) + n * c] = v;
+  }
 }
 
 __global__ void __launch_bounds__(NT) k_lu_pivot(cplx* W, int64_t n, int r, int j, int* perm, const ArgMax* partials,
@@ -651,7 +680,8 @@ void launch_upper_inverse(const cplx* R, int q, cplx* Rt, cplx* X, cudaStream_t 
 
 int lu_nparts(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, NT), 592)); }
 
-void launch_lu_update(cplx* W, int64_t n, int r, int j, ArgMax* partials, int nparts, cudaStream_t st) {
+void launch_lu_update(cplx* W, int64_t n, int r, int j, int c1, bool scale, bool argmax, ArgMax* partials, int nparts,
+                      cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
     VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_lu_update, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
@@ -659,7 +689,13 @@ void launch_lu_update(cplx* W, int64_t n, int r, int j, ArgMax* partials, int np
     VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_unit_lower_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     configured = true;
   }
-  k_lu_update<<<nparts, NT, (size_t)r * sizeof(cplx), st>>>(W, n, r, j, partials);
+  k_lu_update<<<nparts, NT, (size_t)r * sizeof(cplx), st>>>(W, n, r, j, c1, scale ? 1 : 0, argmax ? 1 : 0, partials);
+  VSIE_CHECK_LAUNCH();
+}
+
+void launch_lu_trsm(cplx* W, int64_t n, int r, int j0, int jb, cudaStream_t st) {
+  if (j0 + jb >= r) return;
+  k_lu_trsm<<<(unsigned)ceil_div(r - j0 - jb, NT), NT, 0, st>>>(W, n, r, j0, jb);
   VSIE_CHECK_LAUNCH();
 }
 

@@ -86,8 +86,14 @@ struct ArgMax {
 };
 
 // LU with partial pivoting of W (n x r, ld n), in place, rows physically swapped;
-// perm[i] = original row of permuted row i.  j = -1: argmax of column 0 only.
-void launch_lu_update(cplx* W, int64_t n, int r, int j, ArgMax* partials, int nparts, cudaStream_t st);
+// perm[i] = original row of permuted row i.  Step j: scale column j and update columns
+// (j, c1) on rows > j (scale), then argmax partials of column j + 1 (argmax); j = -1: argmax
+// of column 0 only.  Blocked: panels of kLuPanel columns, the trailing matrix updated per
+// panel by launch_lu_trsm (U12 = L11^{-1} A12) and a ZGEMM A22 -= L21 U12.
+constexpr int kLuPanel = 32;
+void launch_lu_update(cplx* W, int64_t n, int r, int j, int c1, bool scale, bool argmax, ArgMax* partials, int nparts,
+                      cudaStream_t st);
+void launch_lu_trsm(cplx* W, int64_t n, int r, int j0, int jb, cudaStream_t st);
 void launch_lu_pivot(cplx* W, int64_t n, int r, int j, int* perm, const ArgMax* partials, int nparts,
                      int* bad, cudaStream_t st);
 int lu_nparts(int64_t n);
