@@ -93,3 +93,38 @@ def test_pwl_per_moment_nccl_ids():
     assert all("nccl_unique_id" not in p for p in PWLCoupling._per_moment({"world": 1}, None))
     with pytest.raises(ValueError):
         PWLCoupling._per_moment({"nccl_unique_id": b"x"}, None)
+
+
+def test_farnear_farfar_host_validation():
+    """The surface-surface blocks (include/vsie_farnear.h, vsie_farfar.h) reject bad arguments and
+    bad meshes on the host, before any CUDA call (runs without a GPU)."""
+    L = _lib.lib()
+    cfg = synth.get_config(1)
+    xyz, tri = cfg.meshes()[0]
+    near = synth.near_mesh(1)
+    bad = tri.copy()
+    bad[3] = (bad[3][1], bad[3][1], bad[3][2])
+    o = _lib.vsie_farnear_opts()
+    L.vsie_farnear_opts_default(C.byref(o))
+    assert (o.max_rank, o.scale_re, o.scale_im, o.device) == (2048, 1.0, 0.0, -1)
+    h = _lib.HANDLE()
+    an, k1 = _meshes_c([near])
+    af, k2 = _meshes_c([(xyz, bad)])
+    assert L.vsie_farnear_build(an, 1, af, 1, cfg.freq, 1e-3, C.byref(o), C.byref(h)) == -2 and not h.value
+    af, k3 = _meshes_c([(xyz, tri)])
+    assert L.vsie_farnear_build(an, 1, af, 1, cfg.freq, 0.0, C.byref(o), C.byref(h)) == -1
+    assert L.vsie_farnear_build(an, 1, af, 1, -5.0, 1e-3, C.byref(o), C.byref(h)) == -1
+    o.max_rank = 0
+    assert L.vsie_farnear_build(an, 1, af, 1, cfg.freq, 1e-3, C.byref(o), C.byref(h)) == -1
+    assert L.vsie_farnear_build(None, 0, af, 1, cfg.freq, 1e-3, None, C.byref(h)) == -1
+    ab, k4 = _meshes_c([(xyz, bad)])
+    assert L.vsie_farfar_build(ab, 1, cfg.freq, 1.0, 0.0, -1, C.byref(h)) == -2
+    assert "degenerate" in L.vsie_last_error_message().decode()
+    assert L.vsie_farfar_build(af, 1, 0.0, 1.0, 0.0, -1, C.byref(h)) == -1
+    assert L.vsie_farfar_build(af, 1, cfg.freq, float("nan"), 0.0, -1, C.byref(h)) == -1
+    assert L.vsie_farnear_apply(None, None, None, 0, 1, None) == -1
+    assert L.vsie_farfar_apply(None, None, None, 0, 1, 0, None) == -1
+    assert L.vsie_farfar_get_info(None, None) == -1
+    L.vsie_farnear_destroy(None)
+    L.vsie_farfar_destroy(None)
+    del k1, k2, k3, k4
