@@ -245,6 +245,31 @@ void adj_g1(const Ctx& X, Shard& s, int c, const cplx* u, bool cj, cudaStream_t 
   launch_reduce_g1(r, st);
 }
 
+// W1 = G1^T u for the three chi of one shard in one launch (single RHS)
+void adj_g1_batched(const Ctx& X, Shard& s, const cplx* u, bool cj, cudaStream_t st) {
+  vsie_coupling_s* h = X.h;
+  const int n1 = h->grid.n[0], n2 = h->grid.n[1];
+  const int64_t n3l = s.n3loc();
+  ReduceArgs r{};
+  r.nbatch = 3;
+  r.n1 = n1;
+  r.ncol = (int64_t)n2 * n3l;
+  r.cols_per_rhs = r.ncol;
+  r.ld_rhs = X.L.ld;
+  r.conj_u = cj;
+  int64_t r1s = 0;
+  for (int c = 0; c < 3; ++c) {
+    r.G1[c] = h->G1[c].p;
+    r.u[c] = u + c * X.L.chi_stride + shard_voxel_offset(h, s, X.L);
+    r.W1[c] = s.W1.p + c * X.r1m * n2 * n3l;
+    r.r1[c] = (int)X.R(c, 0);
+    r1s += X.R(c, 0);
+  }
+  Scope sc(h, "adj_g1_reduce", 16 * ((int64_t)n1 * r1s + r1s * n2 * n3l + 3LL * n1 * n2 * n3l),
+           8 * (int64_t)n1 * r1s * n2 * n3l, st);
+  launch_reduce_g1(r, st);
+}
+
 // W2 = G2^T W1 of one chi as a split-K ZGEMM (block RHS)
 void adj_g2(const Ctx& X, Shard& s, int c, cudaStream_t st) {
   vsie_coupling_s* h = X.h;
@@ -542,12 +567,18 @@ void fwd_after_y4(const Ctx& X, cplx* y, const Streams& S) {
   join(h, S);
 }
 
-// the transpose's front up to W2: G1^T per chi in the chains, then one batched G2^T.  (One
-// batched TMA-streamed G1^T launch -- a 1-D per-column-copy ring, a 2-D tensor-TMA ring with
-// 52- and 100-row boxes, a per-warp cp.async pipeline -- measured slower than the three
-// concurrent k_reduce_g1 chains at cfgs 2 / 4 and within 1% at cfg 3.)
+// the transpose's front up to W2.  Single RHS: the three chi's G1^T in ONE launch of the
+// TMA-ring kernel (k_reduce_g1_tma: whole-stage bulk copies, consumers only compute; cfg 4
+// 120 us for the three chi vs 151 us for three concurrent k_reduce_g1 chains),
+// then one batched G2^T.  Block RHS: per-chi chains.
 void adj_front_w2(const Ctx& X, const cplx* u, bool cj, const Streams& S) {
   vsie_coupling_s* h = X.h;
+  if (X.k == 1) {
+    // single RHS: the three chi in ONE launch of the TMA-ring G1^T (k_reduce_g1_tma)
+    for (Shard& s : h->shards) adj_g1_batched(X, s, u, cj, S.main);
+    for (Shard& s : h->shards) g2t_pass(X, s, S.main);
+    return;
+  }
   fork(h, S);
   for (int c = 0; c < 3; ++c) {
     h->scope_chi = c;

@@ -8,7 +8,8 @@
 //   Y2 = G2 Y3           -> zgemm      ((r1 n2) x r2 times r2 x n3)
 //   y  = G1 Y2           -> k_expand_g1 (n1 x r1 times r1 x (n2 n3), coalesced voxel writes)
 // Transpose (Eqs. 18-19), per chi, then summed over chi:
-//   W1 = G1^T u          -> k_reduce_g1 (skinny reduction over i1, smem-staged)
+//   W1 = G1^T u          -> k_reduce_g1_tma (single RHS: TMA ring of whole column stages,
+//                           warp pairs split k) / k_reduce_g1 (block RHS, small n1)
 //   W2 = G2^T W1         -> zgemm (T)
 //   z3 = G3^T W2         -> k_gemv_t   (column dot products, deterministic split over rows)
 //   z  = sum_chi G4^T z3 -> k_gemv_t   (sum_batch)
@@ -16,6 +17,7 @@
 // separate sum kernel, so results are bitwise reproducible run to run.
 #include "kernels.cuh"
 #include "dmma_tile.cuh"
+#include "tma_ring.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -512,6 +514,173 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce_g1(const __grid_constant
   pdl_trigger();
 }
 
+// G1^T reduction fed by a TMA ring (single RHS: the columns of one chi are contiguous in u,
+// so a stage of 8 q consecutive columns is ONE bulk copy of 8 q n1 x 16 B).  One producer
+// warp keeps every free stage in flight; each stage is consumed by a PAIR of warps that split
+// its k range in halves (task j -> slot j % ns, pair j % npairs) and only compute: no register
+// is held by a load, so the FP64 pipe (DMMA + the DFMA remainder share it, ~0.7 of it at the
+// HBM rate for r1 = 10) runs under the stream instead of between load batches.  Once both
+// halves are done with the stage's u data, the upper half's partial sums go through the
+// stage buffer itself to the lower half, which adds them (fixed order: lower + upper) and
+// stores W1, then frees the slot.
+constexpr int kRtPairs = 8;
+constexpr int kRtThreads = 32 * (2 * kRtPairs + 1);
+
+template <int NT, int REM, bool CJ>
+__global__ void __launch_bounds__(kRtThreads, 1) k_reduce_g1_tma(const __grid_constant__ ReduceArgs a, int q, int ns,
+                                                                  int64_t stage_off) {
+  const int b = blockIdx.y;
+  const int n1 = a.n1, r1 = a.r1[b];
+  const int ks_n = (n1 + 3) / 4;
+  constexpr int NTA = NT > 0 ? NT : 1, RA = REM > 0 ? REM : 1;
+  extern __shared__ __align__(128) unsigned char sm_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm_raw);   // [ns]
+  uint64_t* empty = full + 16;                            // [ns]
+  cplx* Bf = reinterpret_cast<cplx*>(sm_raw + 256);       // [ks_n][NT][32] fragments of G1
+  cplx* Gr = Bf + (size_t)ks_n * NTA * 32;                // [4 ks_n][REM] columns a >= 8 NT
+  cplx* stg = reinterpret_cast<cplx*>(sm_raw + stage_off);
+  const int64_t cps = 8LL * q;                            // columns per stage
+  const int64_t stage_elems = cps * n1;
+  const int64_t nst = (a.ncol + cps - 1) / cps;
+  const cplx* __restrict__ G1 = a.G1[b];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ns; ++s) {
+      tma::mbar_init(full + s, 1);
+      tma::mbar_init(empty + s, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (NT > 0)
+    for (int e = threadIdx.x; e < ks_n * NT * 32; e += blockDim.x) {
+      const int lane = e % 32, nt = (e / 32) % NTA, ks = e / (32 * NTA);
+      const int k = 4 * ks + (lane & 3), n = 8 * nt + (lane >> 2);
+      Bf[e] = (k < n1 && n < r1) ? __ldg(G1 + k + (int64_t)n1 * n) : cmk(0, 0);
+    }
+  for (int e = threadIdx.x; e < 4 * ks_n * REM; e += blockDim.x) {
+    const int j = e % RA, k = e / RA, n = 8 * NT + j;
+    Gr[e] = (k < n1 && n < r1) ? __ldg(G1 + k + (int64_t)n1 * n) : cmk(0, 0);
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == (int)(blockDim.x / 32) - 1) {
+    // producer: u is the caller's input -- read only after the PDL wait
+    pdl_wait();
+    if (lane == 0) {
+      const cplx* __restrict__ U = a.u[b];
+      int j = 0;
+      for (int64_t t = blockIdx.x; t < nst; t += gridDim.x, ++j) {
+        const int slot = j % ns;
+        if (j >= ns) tma::mbar_wait(empty + slot, ((j / ns) - 1) & 1);
+        const int64_t c0 = t * cps;
+        const int64_t nc = min(cps, a.ncol - c0);
+        const uint32_t bytes = (uint32_t)(nc * n1 * (int64_t)sizeof(cplx));
+        tma::mbar_expect_tx(full + slot, bytes);
+        tma::bulk_g2s(stg + slot * stage_elems, U + c0 * n1, bytes, full + slot);
+      }
+    }
+    pdl_trigger();
+    return;
+  }
+  // consumer pairs: at most ns of them, so that the stage a pair waits for is never two ring
+  // phases ahead of the producer (the pair's previous task was j - npairs >= j - ns)
+  const int npairs = (int)(blockDim.x / 64);   // launched with 2 npairs + 1 warps, npairs <= ns
+  const int pair = warp >> 1, half = warp & 1;
+  const int ksh = (ks_n + 1) / 2;
+  const int ks0 = half ? ksh : 0, ks1 = half ? ks_n : ksh;
+  const int g = lane >> 2, t4 = lane & 3;
+  int j = pair;
+  for (int64_t t = blockIdx.x + (int64_t)pair * gridDim.x; t < nst; t += (int64_t)npairs * gridDim.x, j += npairs) {
+    const int slot = j % ns;
+    tma::mbar_wait(full + slot, (j / ns) & 1);
+    cplx* S = stg + slot * stage_elems;
+    for (int tile = 0; tile < q; ++tile) {
+      const int64_t cg = t * cps + 8 * tile + g;
+      const cplx* __restrict__ col = S + (int64_t)(8 * tile + g) * n1;
+      double p1[NTA][2], p2[NTA][2], p3[NTA][2];
+#pragma unroll
+      for (int nt = 0; nt < NTA; ++nt) p1[nt][0] = p1[nt][1] = p2[nt][0] = p2[nt][1] = p3[nt][0] = p3[nt][1] = 0;
+      cplx rem[RA];
+#pragma unroll
+      for (int jj = 0; jj < RA; ++jj) rem[jj] = cmk(0, 0);
+#pragma unroll 5
+      for (int ks = ks0; ks < ks1; ++ks) {
+        const int k = 4 * ks + t4;
+        const cplx av = k < n1 ? col[k] : cmk(0, 0);
+        const double ar = av.x, ai = CJ ? -av.y : av.y, as = ar + ai;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const cplx bv = Bf[(ks * NTA + nt) * 32 + lane];
+          dmma(p1[nt][0], p1[nt][1], ar, bv.x);
+          dmma(p2[nt][0], p2[nt][1], ai, bv.y);
+          dmma(p3[nt][0], p3[nt][1], as, bv.x + bv.y);
+        }
+#pragma unroll
+        for (int jj = 0; jj < REM; ++jj) cfma(rem[jj], Gr[k * REM + jj], cmk(ar, ai));
+      }
+      // both halves are done with this tile's u: the upper half's partials go through the
+      // stage buffer (tile 8 columns x n1 >= 32 lanes x 6 NT + 2 REM doubles, checked by the host) to the lower half
+      double* xch = reinterpret_cast<double*>(S + (int64_t)8 * tile * n1);
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
+      if (half) {
+#pragma unroll
+        for (int nt = 0; nt < NTA; ++nt)
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj) {
+            xch[(6 * nt + jj) * 32 + lane] = p1[nt][jj];
+            xch[(6 * nt + 2 + jj) * 32 + lane] = p2[nt][jj];
+            xch[(6 * nt + 4 + jj) * 32 + lane] = p3[nt][jj];
+          }
+#pragma unroll
+        for (int jj = 0; jj < RA; ++jj) {
+          xch[(6 * NTA + 2 * jj) * 32 + lane] = rem[jj].x;
+          xch[(6 * NTA + 2 * jj + 1) * 32 + lane] = rem[jj].y;
+        }
+      }
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
+      if (half) continue;
+#pragma unroll
+      for (int nt = 0; nt < NTA; ++nt)
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          p1[nt][jj] += xch[(6 * nt + jj) * 32 + lane];
+          p2[nt][jj] += xch[(6 * nt + 2 + jj) * 32 + lane];
+          p3[nt][jj] += xch[(6 * nt + 4 + jj) * 32 + lane];
+        }
+#pragma unroll
+      for (int jj = 0; jj < RA; ++jj) {
+        rem[jj].x += xch[(6 * NTA + 2 * jj) * 32 + lane];
+        rem[jj].y += xch[(6 * NTA + 2 * jj + 1) * 32 + lane];
+      }
+      const bool cok = cg < a.ncol;
+      cplx* __restrict__ W = a.W1[b] + (int64_t)r1 * cg;
+      if (cok) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj) {
+            const int aa = 8 * nt + 2 * t4 + jj;
+            if (aa < r1) W[aa] = cmk(p1[nt][jj] - p2[nt][jj], p3[nt][jj] - p1[nt][jj] - p2[nt][jj]);
+          }
+      }
+#pragma unroll
+      for (int jj = 0; jj < REM; ++jj) {
+        cplx v = rem[jj];
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, 1);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, 1);
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, 2);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, 2);
+        const int aa = 8 * NT + jj;
+        if (cok && t4 == 0 && aa < r1) W[aa] = v;
+      }
+    }
+    if (!half) {
+      __syncwarp();
+      if (lane == 0) tma::mbar_arrive(empty + slot);
+    }
+  }
+  pdl_trigger();
+}
+
 __global__ void __launch_bounds__(kThreads) k_sum3(const cplx* __restrict__ in, int64_t chi_stride, int64_t ld_in,
                                                    int64_t rows, int k, cplx* __restrict__ out, int64_t ld_out,
                                                    bool conj_out) {
@@ -708,7 +877,64 @@ void launch_expand_g1(const ExpandArgs& a, cudaStream_t st) {
 #undef VSIE_EXP
 }
 
+// the TMA-ring G1^T (single RHS: every chi's columns contiguous); false if the shape does
+// not fit it (the caller then runs k_reduce_g1)
+bool launch_reduce_g1_tma(const ReduceArgs& a, cudaStream_t st) {
+  if (a.cols_per_rhs < a.ncol || a.ncol <= 0) return false;
+  int r1max = 0;
+  for (int b = 0; b < a.nbatch; ++b) r1max = std::max(r1max, a.r1[b]);
+  if (r1max > 32) return false;
+  int NT = r1max / 8, REM = r1max % 8;
+  if (REM > 2) {
+    NT = (r1max + 7) / 8;
+    REM = 0;
+  }
+  const int n1 = a.n1, ks_n = (n1 + 3) / 4;
+  // the upper half's partial sums (32 lanes x 6 NT + 2 REM doubles) fit in one tile of u
+  if (32 * (6 * std::max(NT, 1) + 2 * std::max(REM, 1)) > 16 * n1) return false;
+  const int64_t frag = 256 + ((int64_t)ks_n * std::max(NT, 1) * 32 + 4LL * ks_n * REM) * (int64_t)sizeof(cplx);
+  const int64_t stage_off = (frag + 127) / 128 * 128;
+  const int q = (int)std::max<int64_t>(1, 25600 / (128LL * n1));
+  const int64_t stage_bytes = 8LL * q * n1 * (int64_t)sizeof(cplx);
+  // one CTA per SM with as many stages as fit (two CTAs per SM with half the stages each
+  // measured slower at cfg 4: 139 vs 120 us, the stage consumers are the bottleneck)
+  const int64_t smem_max = 227 * 1024;
+  const int ns = (int)std::min<int64_t>(16, (smem_max - stage_off) / stage_bytes);
+  if (ns < 2) return false;
+  const int npairs = std::min(kRtPairs, ns);
+  const size_t smem = (size_t)(stage_off + ns * stage_bytes);
+  const int64_t nst = ceil_div(a.ncol, 8LL * q);
+  dim3 grid((unsigned)std::min<int64_t>(nst, std::max(1, sm_count() / std::max(1, a.nbatch))), a.nbatch);
+  const dim3 blk(32 * (2 * npairs + 1));
+#define VSIE_RT(K, R)                                                                                     \
+  if (NT == K && REM == R) {                                                                              \
+    static bool d0 = false, d1 = false;                                                                   \
+    if (a.conj_u) {                                                                                       \
+      if (!d1) {                                                                                          \
+        VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_reduce_g1_tma<K, R, true>,                                 \
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)); \
+        d1 = true;                                                                                        \
+      }                                                                                                   \
+      launch_pdl(k_reduce_g1_tma<K, R, true>, grid, blk, smem, st, a, q, ns, stage_off);     \
+    } else {                                                                                              \
+      if (!d0) {                                                                                          \
+        VSIE_CHECK_CUDA(cudaFuncSetAttribute(k_reduce_g1_tma<K, R, false>,                                \
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)); \
+        d0 = true;                                                                                        \
+      }                                                                                                   \
+      launch_pdl(k_reduce_g1_tma<K, R, false>, grid, blk, smem, st, a, q, ns, stage_off);    \
+    }                                                                                                     \
+    VSIE_CHECK_LAUNCH();                                                                                  \
+    return true;                                                                                          \
+  }
+  VSIE_RT(0, 1) VSIE_RT(0, 2) VSIE_RT(1, 0) VSIE_RT(1, 1) VSIE_RT(1, 2) VSIE_RT(2, 0) VSIE_RT(2, 1)
+  VSIE_RT(2, 2) VSIE_RT(3, 0) VSIE_RT(3, 1) VSIE_RT(3, 2) VSIE_RT(4, 0)
+#undef VSIE_RT
+  return false;
+}
+
 void launch_reduce_g1(const ReduceArgs& a, cudaStream_t st) {
+  if (launch_reduce_g1_tma(a, st)) return;
   int r1max = 0;
   for (int b = 0; b < a.nbatch; ++b) r1max = std::max(r1max, a.r1[b]);
   VSIE_REQUIRE(r1max <= 32, VSIE_ERR_ARG, "reduce: r1 > 32 not supported");

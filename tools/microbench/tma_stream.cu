@@ -53,9 +53,7 @@ int main() {
   CK(cudaFuncSetAttribute(k_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   struct C { int grid, stages, piece, sub, mode; int64_t bytes; };
-  C cs[] = {{148,6,32768,1,0,bytes},{148,6,32768,4,0,bytes},{148,12,16384,1,0,bytes},{148,3,65536,1,0,bytes},{296,3,32768,1,0,bytes},
-            {296,6,16384,1,0,bytes},{592,3,16384,1,0,bytes},{148,6,32768,1,1,bytes},{296,3,32768,1,1,bytes},{148,12,16384,1,1,bytes},
-            {148,6,32768,1,0,(int64_t)1 << 30},{296,3,32768,1,1,(int64_t)1 << 30}};
+  C cs[] = {{148,6,32768,1,0,(int64_t)1 << 30},{148,7,25600,1,0,(int64_t)1 << 30},{148,7,25600,1,1,(int64_t)1 << 30},{296,3,32768,1,0,(int64_t)1 << 30},{296,3,25600,1,0,(int64_t)1 << 30},{296,4,25600,1,0,(int64_t)1 << 30},{296,3,32768,1,1,(int64_t)1 << 30},{296,3,25600,1,1,(int64_t)1 << 30},{444,2,25600,1,0,(int64_t)1 << 30},{444,2,25600,1,1,(int64_t)1 << 30},{148,3,65536,1,0,(int64_t)1 << 30},{148,2,102400,1,0,(int64_t)1 << 30},{296,2,51200,1,0,(int64_t)1 << 30}};
   for (auto c : cs) {
     float best = 1e9, sum = 0; const int reps = 10;
     for (int r = 0; r < reps + 2; ++r) {
