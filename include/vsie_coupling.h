@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define VSIE_ABI_VERSION 3
+#define VSIE_ABI_VERSION 4
 
 /* status codes */
 #define VSIE_OK 0
@@ -112,6 +112,12 @@ typedef struct {
                           * memory segment "/vsie_<ipc_name>" (unique per job, <= 200 chars; the
                           * segment is unlinked once every rank attached).  A test transport: every
                           * collective synchronises the stream, so applies run eagerly (no graphs). */
+  int32_t quad_rule;     /* entry quadrature: 0 = 2 x 2 x 2 Gauss voxel nodes x the 3-point triangle rule
+                          * (48 pairs per entry; default); 1 = the paper's rule for the far
+                          * coupling block Z_bc^f, "1 volume and 1 surface integration point":
+                          * the voxel centre with weight h1 h2 h3 x each triangle's centroid with the
+                          * whole triangle's weight (2 pairs per entry; linear PWL moments vanish).
+                          * Other values: VSIE_ERR_ARG. */
 } vsie_build_opts;
 
 typedef struct {
@@ -136,6 +142,7 @@ typedef struct {
                                  * front, one G4 pass for both products, forward tail), 2 = G3 read
                                  * once (forward G4 pass, one G3 pass for both products, transpose
                                  * G4 pass); chosen to move fewer bytes unless configured       */
+  int32_t quad_rule;            /* vsie_build_opts.quad_rule of the build / import            */
 } vsie_info;
 
 /* Per-kernel device timing of apply calls (opt-in, see vsie_coupling_set_timing). */
@@ -148,6 +155,20 @@ typedef struct {
 } vsie_timer;
 
 int32_t vsie_abi_version(void);
+
+/* Device-memory hook (SURVEY §8(b) "torch caching allocator hook"), process-wide: every
+ * device buffer the library allocates after this call (cores, workspaces, build scratch,
+ * the surface-surface blocks) comes from dev_alloc(bytes, ctx), which must return memory of
+ * the current CUDA device, 256-B aligned, or NULL (the calling API returns VSIE_ERR_NOMEM).
+ * Each buffer is returned through the dev_free of the hook that allocated it, after a
+ * cudaDeviceSynchronize (cudaFree's ordering: a caching allocator reuses memory at once).
+ * The hook functions must stay callable until every buffer they allocated is freed (the
+ * handles holding them destroyed), also after another hook was installed.
+ * Both NULL restores cudaMalloc / cudaFree; exactly one NULL is VSIE_ERR_ARG.  Not
+ * thread-safe against concurrent library calls.  The CUDA-IPC test transport's exchange
+ * buffer stays on cudaMalloc (IPC handles need it). */
+int32_t vsie_set_allocator(void* (*dev_alloc)(size_t bytes, void* ctx), void (*dev_free)(void* ptr, void* ctx),
+                           void* ctx);
 void vsie_build_opts_default(vsie_build_opts* opts);
 const char* vsie_status_string(int32_t status);
 const char* vsie_last_error_message(void);

@@ -55,12 +55,19 @@ class Problem:
         return (3 * self.n_v, self.m)
 
 
-def make_problem(n, h, origin, meshes, freq, scale=1.0 + 0.0j, ng=2, bary=None, moment=0):
+def make_problem(n, h, origin, meshes, freq, scale=1.0 + 0.0j, ng=2, bary=None, moment=0, quad_rule=0):
     """k0 = 2 pi f / c0 (§8c-L19); sources from geometry.mesh_sources.
 
-    moment l in 1..3: node weights w_p (r_p - c)_l / h_l (PWL test function, module header)."""
+    moment l in 1..3: node weights w_p (r_p - c)_l / h_l (PWL test function, module header).
+    quad_rule 1: the paper's far-block rule, "1 volume and 1 surface integration point" for
+    Z_bc^f: ng = 1 (voxel centre, weight h1 h2 h3) and the triangle centroid
+    (geometry.TRI_CENTROID, weight A); 0 keeps ng / bary (default 2 x 2 x 2 x 3-point)."""
     if moment not in (0, 1, 2, 3):
         raise ValueError("moment must be 0 (PWC) or 1..3 (linear in x, y, z)")
+    if quad_rule not in (0, 1):
+        raise ValueError("quad_rule must be 0 (2x2x2 x 3-point) or 1 (1 x 1, P:287)")
+    if quad_rule == 1:
+        ng, bary = 1, geometry.TRI_CENTROID
     rs, js = geometry.mesh_sources(meshes, geometry.TRI_BARY if bary is None else bary)
     offs, wts = geometry.gauss_legendre_offsets(h, ng)
     if moment:

@@ -19,6 +19,11 @@ TRI_BARY = np.array([[2.0 / 3.0, 1.0 / 6.0, 1.0 / 6.0],
                      [1.0 / 6.0, 1.0 / 6.0, 2.0 / 3.0]])
 
 
+# one point per triangle, the centroid with the whole triangle's weight: the paper's surface
+# rule for the far coupling block Z_bc^f ("1 volume and 1 surface integration point")
+TRI_CENTROID = np.array([[1.0 / 3.0, 1.0 / 3.0, 1.0 / 3.0]])
+
+
 class GeometryError(ValueError):
     pass
 

@@ -33,7 +33,7 @@ class vsie_build_opts(C.Structure):
                 ("seed", C.c_uint64), ("scale_re", C.c_double), ("scale_im", C.c_double),
                 ("rank", C.c_int32), ("world", C.c_int32), ("loopback", C.c_int32),
                 ("nccl_unique_id", C.c_void_p), ("device", C.c_int32), ("verbose", C.c_int32),
-                ("test_moment", C.c_int32), ("ipc_name", C.c_char_p)]
+                ("test_moment", C.c_int32), ("ipc_name", C.c_char_p), ("quad_rule", C.c_int32)]
 
 
 class vsie_info(C.Structure):
@@ -44,7 +44,7 @@ class vsie_info(C.Structure):
                 ("build_maxvol_s", C.c_double), ("slab", C.c_int32 * 2), ("cols", C.c_int64 * 2),
                 ("world", C.c_int32), ("rank", C.c_int32), ("loopback", C.c_int32), ("k0", C.c_double),
                 ("apply_launches", C.c_int64), ("apply_calls", C.c_int64), ("test_moment", C.c_int32),
-                ("pair_schedule", C.c_int32)]
+                ("pair_schedule", C.c_int32), ("quad_rule", C.c_int32)]
 
 
 class vsie_timer(C.Structure):
@@ -75,9 +75,12 @@ class vsie_farfar_info(C.Structure):
 
 
 HANDLE = C.c_void_p
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
 
 _SIGS = {
     "vsie_abi_version": (C.c_int32, []),
+    "vsie_set_allocator": (C.c_int32, [ALLOC_FN, FREE_FN, C.c_void_p]),
     "vsie_build_opts_default": (None, [C.POINTER(vsie_build_opts)]),
     "vsie_status_string": (C.c_char_p, [C.c_int32]),
     "vsie_last_error_message": (C.c_char_p, []),

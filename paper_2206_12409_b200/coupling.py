@@ -160,7 +160,7 @@ class Coupling:
             build_s=i.build_s, build_entry_s=i.build_entry_s, build_factor_s=i.build_factor_s,
             build_maxvol_s=i.build_maxvol_s, slab=tuple(i.slab), cols=tuple(i.cols), world=i.world,
             rank=i.rank, loopback=i.loopback, k0=i.k0, apply_launches=i.apply_launches,
-            apply_calls=i.apply_calls, test_moment=i.test_moment,
+            apply_calls=i.apply_calls, test_moment=i.test_moment, quad_rule=i.quad_rule,
             pair_schedule={1: "g4_shared", 2: "g3_shared"}.get(i.pair_schedule))
 
     @property
@@ -423,3 +423,41 @@ class PWLCoupling:
         hs = (_lib.HANDLE * 4)(*[h._h for h in self.handles])
         check(lib().vsie_coupling_apply_pair_pwl(hs, C.c_void_p(x_ptr), C.c_void_p(y_ptr), C.c_void_p(u_ptr),
                                                  C.c_void_p(z_ptr), _lib.OPS[adj], _stream_ptr(stream)))
+
+
+_alloc_keep = []   # every hook ever installed stays callable: buffers are freed through the hook
+                   # that allocated them, possibly after the hook was replaced
+
+
+def use_torch_allocator(enable: bool = True):
+    """Route the library's device allocations through PyTorch's caching allocator
+    (vsie_set_allocator; SURVEY §8(b) allocator hook), or back to cudaMalloc / cudaFree.
+    Marshalling only: the callbacks call torch.cuda.caching_allocator_alloc / _delete on the
+    current device and stream."""
+    if not enable:
+        check(lib().vsie_set_allocator(_lib.ALLOC_FN(), _lib.FREE_FN(), None))
+        return
+    torch = _torch()
+
+    def _alloc(nbytes):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes))
+        except RuntimeError:
+            return None
+
+    def _free(ptr):
+        torch.cuda.caching_allocator_delete(ptr)
+
+    set_allocator(_alloc, _free)
+
+
+def set_allocator(alloc, free):
+    """vsie_set_allocator with Python callables alloc(nbytes) -> device pointer (int) or None
+    and free(pointer); both None restores cudaMalloc / cudaFree.  The callables are kept
+    alive for the rest of the process."""
+    if alloc is None and free is None:
+        check(lib().vsie_set_allocator(_lib.ALLOC_FN(), _lib.FREE_FN(), None))
+        return
+    keep = (_lib.ALLOC_FN(lambda n, _c: alloc(n)), _lib.FREE_FN(lambda p, _c: free(p)))
+    _alloc_keep.append(keep)
+    check(lib().vsie_set_allocator(keep[0], keep[1], None))

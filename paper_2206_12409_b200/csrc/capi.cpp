@@ -16,6 +16,40 @@
 
 using namespace vsie;
 
+namespace vsie {
+
+AllocHook& alloc_hook() {
+  static AllocHook h;
+  return h;
+}
+
+void* dev_alloc_bytes(size_t bytes, AllocHook& used) {
+  used = alloc_hook();
+  void* p = nullptr;
+  if (!used.alloc) {
+    VSIE_CHECK_CUDA(cudaMalloc(&p, bytes));
+    return p;
+  }
+  p = used.alloc(bytes, used.ctx);
+  VSIE_REQUIRE(p != nullptr, VSIE_ERR_NOMEM,
+               "device allocation hook returned NULL for " + std::to_string(bytes) + " bytes");
+  VSIE_REQUIRE(reinterpret_cast<uintptr_t>(p) % 256 == 0, VSIE_ERR_ARG, "device allocation hook: pointer not 256-B aligned");
+  return p;
+}
+
+void dev_free_bytes(void* p, const AllocHook& used) {
+  if (!used.free) {
+    cudaFree(p);
+    return;
+  }
+  // cudaFree's ordering: work already queued on any stream may still use p, and a caching
+  // allocator hands p out again at once
+  cudaDeviceSynchronize();
+  used.free(p, used.ctx);
+}
+
+}  // namespace vsie
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -61,6 +95,18 @@ extern "C" {
 
 int32_t vsie_abi_version(void) { return VSIE_ABI_VERSION; }
 
+int32_t vsie_set_allocator(void* (*dev_alloc)(size_t, void*), void (*dev_free)(void*, void*), void* ctx) {
+  return guarded([&] {
+    VSIE_REQUIRE((dev_alloc == nullptr) == (dev_free == nullptr), VSIE_ERR_ARG,
+                 "dev_alloc and dev_free must both be set or both be NULL");
+    AllocHook& h = alloc_hook();
+    h.alloc = dev_alloc;
+    h.free = dev_free;
+    h.ctx = dev_alloc ? ctx : nullptr;
+    return VSIE_OK;
+  });
+}
+
 void vsie_build_opts_default(vsie_build_opts* o) {
   if (!o) return;
   std::memset(o, 0, sizeof(*o));
@@ -80,6 +126,7 @@ void vsie_build_opts_default(vsie_build_opts* o) {
   o->device = -1;
   o->verbose = 0;
   o->test_moment = 0;
+  o->quad_rule = 0;
 }
 
 const char* vsie_status_string(int32_t s) {
@@ -390,6 +437,7 @@ int32_t vsie_coupling_info(vsie_coupling_t h, vsie_info* out) {
     out->apply_calls = h->apply_calls;
     out->test_moment = h->test_moment;
     out->pair_schedule = h->has_cores ? pair_schedule(h) : 0;
+    out->quad_rule = h->quad_rule;
     return VSIE_OK;
   });
 }

@@ -59,31 +59,44 @@ __device__ __forceinline__ void cfma(cplx& acc, cplx a, cplx b) {
 __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // ----------------------------------------------------------------- device memory
-// Simple owning device buffer (cudaMalloc / cudaFree).
+// Device allocations go through a process-wide hook (vsie_set_allocator; default cudaMalloc /
+// cudaFree), e.g. the caller's caching allocator (torch.cuda.caching_allocator_alloc).  Each
+// buffer remembers the hook that allocated it and is returned through that hook.
+struct AllocHook {
+  void* (*alloc)(size_t bytes, void* ctx) = nullptr;   // nullptr: cudaMalloc / cudaFree
+  void (*free)(void* p, void* ctx) = nullptr;
+  void* ctx = nullptr;
+};
+AllocHook& alloc_hook();                 // the current hook (capi.cpp)
+void* dev_alloc_bytes(size_t bytes, AllocHook& used);
+void dev_free_bytes(void* p, const AllocHook& used);
+
+// Simple owning device buffer.
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  AllocHook hook;   // the hook that allocated p
   DevBuf() = default;
   explicit DevBuf(size_t count) { alloc(count); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), hook(o.hook) { o.p = nullptr; o.n = 0; }
   DevBuf& operator=(DevBuf&& o) noexcept {
-    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    if (this != &o) { release(); p = o.p; n = o.n; hook = o.hook; o.p = nullptr; o.n = 0; }
     return *this;
   }
   ~DevBuf() { release(); }
   void alloc(size_t count) {
     release();
     if (count == 0) return;
-    VSIE_CHECK_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    p = static_cast<T*>(dev_alloc_bytes(count * sizeof(T), hook));
     n = count;
   }
   // grow-only reallocation (contents not preserved)
   void ensure(size_t count) { if (count > n) alloc(count); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) dev_free_bytes(p, hook);
     p = nullptr;
     n = 0;
   }

@@ -479,7 +479,9 @@ __global__ void k_chol_step(cplx* G, int q, int j) {
   }
 }
 
-// final scaling: R[j, c] = G[j, c] / sqrt(G[j, j]) (c >= j), zero below the diagonal
+// final scaling: R[j, c] = G[j, c] / sqrt(G[j, j]) (c > j), zero below the diagonal; the
+// diagonal itself is written by k_chol_diag afterwards (scaling and overwriting it in one
+// pass let some threads read an already replaced G[j, j]: a race that changed R run to run)
 __global__ void k_chol_finish(cplx* G, int q, int* bad) {
   const int64_t total = (int64_t)q * q;
   for (int64_t e = blockIdx.x * (int64_t)NT + threadIdx.x; e < total; e += (int64_t)gridDim.x * NT) {
@@ -488,18 +490,26 @@ __global__ void k_chol_finish(cplx* G, int q, int* bad) {
       G[e] = cmk(0, 0);
       continue;
     }
+    if (j == c) continue;
     const double d = G[j + (int64_t)q * j].x;
     if (!(d > 0)) {
       if (bad) *bad = 1;
       continue;
     }
     const double s = 1.0 / sqrt(d);
-    if (j == c) {
-      G[e] = cmk(sqrt(d), 0.0);
-    } else {
-      const cplx v = G[e];
-      G[e] = cmk(v.x * s, v.y * s);
+    const cplx v = G[e];
+    G[e] = cmk(v.x * s, v.y * s);
+  }
+}
+
+__global__ void k_chol_diag(cplx* G, int q, int* bad) {
+  for (int j = blockIdx.x * NT + threadIdx.x; j < q; j += gridDim.x * NT) {
+    const double d = G[j + (int64_t)q * j].x;
+    if (!(d > 0)) {
+      if (bad) *bad = 1;
+      continue;
     }
+    G[j + (int64_t)q * j] = cmk(sqrt(d), 0.0);
   }
 }
 
@@ -664,6 +674,8 @@ void launch_cholesky_upper(cplx* G, int q, int* bad, cudaStream_t st) {
     VSIE_CHECK_LAUNCH();
   }
   k_chol_finish<<<grid1((int64_t)q * q), NT, 0, st>>>(G, q, bad);
+  VSIE_CHECK_LAUNCH();
+  k_chol_diag<<<grid1(q), NT, 0, st>>>(G, q, bad);
   VSIE_CHECK_LAUNCH();
 }
 

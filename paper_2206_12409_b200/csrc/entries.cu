@@ -3,7 +3,8 @@
 // the dyadic Green's function (Eq. 3) between a PWC voxel testing
 // function and an RWG basis function, by the fixed non-singular
 // quadrature of SURVEY §8c-E (2x2x2 Gauss per voxel x 3-point rule per
-// triangle, 48 pair interactions per entry).
+// triangle, 48 pair interactions per entry; or the paper's far-block rule of P:287, one
+// voxel point x one point per triangle, 2 pairs per entry, build option quad_rule = 1).
 //
 // Per pair, with R = r_p - r_s, u = 1/(k0 |R|), g = exp(-i k0 |R|)/(4 pi |R|):
 //   [G(R) J]_chi = g [ alpha J_chi + beta Rhat_chi (Rhat . J) ],
@@ -30,10 +31,11 @@ namespace {
 // polynomials of cos / sin(delta_p) (truncation <= |delta|^8 / 8! < 1e-19) per pair give
 // exp(-i k0 R_p) by angle addition -- the same value as a sincos per pair to rounding, at
 // ~1/3 of its FP64 instructions (g.taylor; otherwise a sincos per pair).
+template <int NP>
 __device__ __forceinline__ void entry_acc(const EntryGeom& g, int chi, double cx, double cy, double cz,
                                           const double* __restrict__ s36, double& ar, double& ai) {
 #pragma unroll 1
-  for (int q = 0; q < 6; ++q) {
+  for (int q = 0; q < g.nsrc; ++q) {
     const double sx = __ldg(s36 + 6 * q + 0), sy = __ldg(s36 + 6 * q + 1), sz = __ldg(s36 + 6 * q + 2);
     const double jx = __ldg(s36 + 6 * q + 3), jy = __ldg(s36 + 6 * q + 4), jz = __ldg(s36 + 6 * q + 5);
     const double jc = chi == 0 ? jx : (chi == 1 ? jy : jz);
@@ -45,10 +47,11 @@ __device__ __forceinline__ void entry_acc(const EntryGeom& g, int chi, double cx
       sincos(kr0, &s0, &c0);
     }
 #pragma unroll
-    for (int p = 0; p < 8; ++p) {
-      const double rx = (p & 1) ? bx + g.dx : bx - g.dx;
-      const double ry = (p & 2) ? by + g.dy : by - g.dy;
-      const double rz = (p & 4) ? bz + g.dz : bz - g.dz;
+    for (int p = 0; p < NP; ++p) {
+      // NP = 8: the 2 x 2 x 2 Gauss nodes c +- h / (2 sqrt 3); NP = 1: the centre
+      const double rx = NP == 1 ? bx : ((p & 1) ? bx + g.dx : bx - g.dx);
+      const double ry = NP == 1 ? by : ((p & 2) ? by + g.dy : by - g.dy);
+      const double rz = NP == 1 ? bz : ((p & 4) ? bz + g.dz : bz - g.dz);
       const double r2 = fma(rx, rx, fma(ry, ry, rz * rz));
       const double ir = rsqrt(r2);
       const double R = r2 * ir;
@@ -83,7 +86,10 @@ __device__ __forceinline__ cplx entry_value(const EntryGeom& g, int chi, int i1,
   const double cx = g.ox + i1 * g.hx, cy = g.oy + i2 * g.hy, cz = g.oz + i3 * g.hz;
   const double* s36 = g.src + 36 * n;
   double ar = 0, ai = 0;
-  entry_acc(g, chi, cx, cy, cz, s36, ar, ai);
+  if (g.nodes == 1)
+    entry_acc<1>(g, chi, cx, cy, cz, s36, ar, ai);
+  else
+    entry_acc<8>(g, chi, cx, cy, cz, s36, ar, ai);
   ar *= g.w;
   ai *= g.w;
   return cmk(g.scale_re * ar - g.scale_im * ai, g.scale_re * ai + g.scale_im * ar);

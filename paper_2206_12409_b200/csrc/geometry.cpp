@@ -87,7 +87,7 @@ std::vector<RwgRec> extract_rwgs(const vsie_mesh& mesh) {
 
 namespace {
 
-void append_mesh(const vsie_mesh& mesh, std::vector<double>& table) {
+void append_mesh(const vsie_mesh& mesh, std::vector<double>& table, int tri_points) {
   const double* X = mesh.xyz;
   const int32_t* T = mesh.tri;
   // barycentric interior rule (2/3, 1/6, 1/6) and permutations
@@ -101,6 +101,25 @@ void append_mesh(const vsie_mesh& mesh, std::vector<double>& table) {
     l = std::sqrt(l);
     const double coef = l / 6.0;
     double rec[kSrcStride];
+    if (tri_points == 1) {
+      // one point per triangle (the paper's far-block rule): the centroid with the
+      // whole triangle's weight, J = +-(l/2)(r_c - p); records 0 (T+) and 1 (T-), the other
+      // four records carry J = 0 (the kernel reads only the first two, EntryGeom::nsrc)
+      for (int side = 0; side < 2; ++side) {
+        const int64_t tri = side == 0 ? r.tp : r.tm, opp = side == 0 ? r.pp : r.pm;
+        double* o = rec + 6 * side;
+        for (int c = 0; c < 3; ++c) {
+          const double rr = (X[3 * T[3 * tri] + c] + X[3 * T[3 * tri + 1] + c] + X[3 * T[3 * tri + 2] + c]) / 3.0;
+          const double p = X[3 * opp + c];
+          o[c] = rr;
+          o[3 + c] = side == 0 ? 0.5 * l * (rr - p) : 0.5 * l * (p - rr);
+        }
+      }
+      for (int q = 2; q < kSrcPerRwg; ++q)
+        for (int c = 0; c < 6; ++c) rec[6 * q + c] = c < 3 ? rec[c] : 0.0;
+      table.insert(table.end(), rec, rec + kSrcStride);
+      continue;
+    }
     for (int side = 0; side < 2; ++side) {
       const int64_t tri = side == 0 ? r.tp : r.tm, opp = side == 0 ? r.pp : r.pm;
       const int64_t v0 = T[3 * tri], v1 = T[3 * tri + 1], v2 = T[3 * tri + 2];
@@ -121,10 +140,11 @@ void append_mesh(const vsie_mesh& mesh, std::vector<double>& table) {
 
 }  // namespace
 
-Sources build_rwg_sources(const vsie_mesh* meshes, int n_meshes) {
+Sources build_rwg_sources(const vsie_mesh* meshes, int n_meshes, int tri_points) {
   VSIE_REQUIRE(meshes != nullptr && n_meshes >= 1, VSIE_ERR_ARG, "no meshes");
+  VSIE_REQUIRE(tri_points == 3 || tri_points == 1, VSIE_ERR_ARG, "triangle rule must have 3 or 1 points");
   Sources s;
-  for (int k = 0; k < n_meshes; ++k) append_mesh(meshes[k], s.table);
+  for (int k = 0; k < n_meshes; ++k) append_mesh(meshes[k], s.table, tri_points);
   s.m = (int64_t)(s.table.size() / kSrcStride);
   VSIE_REQUIRE(s.m >= 1, VSIE_ERR_GEOMETRY, "meshes have no interior edge (no RWG function)");
   return s;
@@ -146,8 +166,8 @@ double max_edge_length(const vsie_mesh* meshes, int n_meshes) {
   return best;
 }
 
-Sources build_sources(const vsie_mesh* meshes, int n_meshes, const GridDesc& grid) {
-  Sources s = build_rwg_sources(meshes, n_meshes);
+Sources build_sources(const vsie_mesh* meshes, int n_meshes, const GridDesc& grid, int tri_points) {
+  Sources s = build_rwg_sources(meshes, n_meshes, tri_points);
   // Non-singular rule (reading R-L18): every source node must be at
   // least 10 max(h) away from the bounding box of the voxel quadrature nodes.
   double lo[3], hi[3], hmax = 0;

@@ -30,7 +30,8 @@ struct GridDesc {
 
 // Validates and converts the public structs; throws Error(VSIE_ERR_ARG / VSIE_ERR_GEOMETRY).
 GridDesc make_grid(const vsie_grid* g);
-Sources build_sources(const vsie_mesh* meshes, int n_meshes, const GridDesc& grid);
+// tri_points: 3 (interior rule, default) or 1 (centroid; the paper's far-block rule)
+Sources build_sources(const vsie_mesh* meshes, int n_meshes, const GridDesc& grid, int tri_points = 3);
 // One RWG function of a mesh (canonical order): T+ / T- triangle ids, the
 // vertices opposite the shared edge (p+, p-) and the shared edge's vertices (a < b).
 struct RwgRec {
@@ -39,7 +40,7 @@ struct RwgRec {
 // Validates one mesh (degenerate / non-manifold -> VSIE_ERR_GEOMETRY) and lists its RWGs.
 std::vector<RwgRec> extract_rwgs(const vsie_mesh& mesh);
 // The RWG table alone (no voxel-grid check): the surface-surface blocks (farnear.cu).
-Sources build_rwg_sources(const vsie_mesh* meshes, int n_meshes);
+Sources build_rwg_sources(const vsie_mesh* meshes, int n_meshes, int tri_points = 3);
 // Longest triangle edge of the meshes (validated by build_rwg_sources first).
 double max_edge_length(const vsie_mesh* meshes, int n_meshes);
 

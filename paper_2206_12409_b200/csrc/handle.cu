@@ -69,7 +69,9 @@ void handle_init_geometry(vsie_coupling_s* h, const vsie_grid* grid, const vsie_
                           double freq, const vsie_build_opts* o) {
   VSIE_REQUIRE(freq > 0 && std::isfinite(freq), VSIE_ERR_ARG, "freq must be > 0");
   h->grid = make_grid(grid);
-  h->sources = build_sources(meshes, n_meshes, h->grid);
+  VSIE_REQUIRE(o->quad_rule == 0 || o->quad_rule == 1, VSIE_ERR_ARG, "quad_rule must be 0 or 1");
+  h->quad_rule = o->quad_rule;
+  h->sources = build_sources(meshes, n_meshes, h->grid, h->quad_rule == 1 ? 1 : 3);
   h->m = h->sources.m;
   {
     uint64_t f = 1469598103934665603ull;
@@ -107,7 +109,11 @@ void handle_init_geometry(vsie_coupling_s* h, const vsie_grid* grid, const vsie_
   g.dx = g.hx / s3;
   g.dy = g.hy / s3;
   g.dz = g.hz / s3;
-  g.w = g.hx * g.hy * g.hz / 8.0;
+  // quad_rule 1 (P:287 far block): one node at the voxel centre with the whole voxel weight,
+  // one centroid per triangle; otherwise 2 x 2 x 2 Gauss nodes x the 3-point triangle rule
+  g.nodes = h->quad_rule == 1 ? 1 : 8;
+  g.nsrc = h->quad_rule == 1 ? 2 : 6;
+  g.w = g.hx * g.hy * g.hz / (g.nodes == 1 ? 1.0 : 8.0);
   // node p = (sigma1, sigma2, sigma3) with bit l-1 of p set for +h_l / (2 sqrt 3): the linear
   // PWL test function (r_p - c)_l / h_l is +-1 / (2 sqrt 3) there (DESIGN.md R-PWL)
   h->test_moment = o->test_moment;
@@ -116,6 +122,7 @@ void handle_init_geometry(vsie_coupling_s* h, const vsie_grid* grid, const vsie_
   for (int p = 0; p < 8; ++p) {
     const int l = h->test_moment;
     g.pw[p] = l == 0 ? inv4pi : (((p >> (l - 1)) & 1) ? inv4pi / s3 : -inv4pi / s3);
+    if (g.nodes == 1 && l != 0) g.pw[p] = 0.0;   // the linear test function vanishes at the centre
   }
   g.k0 = h->k0;
   g.inv_k0 = 1.0 / h->k0;

@@ -73,6 +73,7 @@ struct vsie_coupling_s {
   std::vector<vsie::Shard> shards;         // 1 shard (own rank) or `world` (loopback)
   int rank = 0, world = 1, loopback = 0, device = 0;
   int nrhs_max = 64;
+  int quad_rule = 0;                       // vsie_build_opts.quad_rule
   int test_moment = 0;                     // PWL test moment (vsie_build_opts.test_moment)
   std::unique_ptr<vsie::Comm> comm;
   vsie::DevBuf<vsie::cplx> partials;       // [3][partials_per_chi]

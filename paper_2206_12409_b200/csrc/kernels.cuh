@@ -15,6 +15,8 @@ struct EntryGeom {
   double pw[8];           // per-node factor 1/(4 pi) x PWL test function at node p (1 for PWC)
   double k0, inv_k0;
   int taylor;             // 1: one sincos per source node + order-7 Taylor phase per pair (entries.cu)
+  int nodes;              // voxel nodes: 8 (2 x 2 x 2 Gauss) or 1 (centre, quad_rule 1)
+  int nsrc;               // source records per RWG read: 6 (3-point rule x 2 triangles) or 2
   double scale_re, scale_im;
   const double* src;     // [m][36] device
   int64_t m;

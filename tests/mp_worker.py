@@ -83,6 +83,18 @@ def main():
     n12 = cfg.n[0] * cfg.n[1]
     us = np.ascontiguousarray(u.reshape(3, -1)[:, n12 * s0:n12 * s1].reshape(-1))
     y1 = b1.apply(torch.from_numpy(x).cuda(), "N").cpu().numpy().reshape(3, -1)[:, n12 * s0:n12 * s1].reshape(-1)
+    # diagnostics: the replicated cores G1 / G2 of both builds, and a digest of b1's cores
+    c1 = b1.export_cores()
+    try:
+        cp = bp.export_cores()
+        g12 = max(float(np.max(np.abs(c1[c][k] - cp[c][k]))) for c in range(3) for k in (0, 1))
+    except Exception as ex:  # noqa: BLE001 (diagnostic only)
+        g12 = str(ex)
+    digest = float(sum(np.sum(np.abs(c1[c][k]) * (1 + np.arange(c1[c][k].size).reshape(c1[c][k].shape) % 7))
+                       for c in range(3) for k in range(4)))
+    res["build_diag"] = {"g12_diff": g12, "b1_digest": digest, "sweeps1": b1.info()["sweeps"],
+                         "sweepsp": bp.info()["sweeps"], "held1": list(b1.info()["heldout_err"]),
+                         "heldp": list(bp.info()["heldout_err"])}
     res["build"] = {"ranks_equal": bp.info()["ranks"] == b1.info()["ranks"],
                     "status": bp.status,
                     "N": rel(bp.apply(torch.from_numpy(x).cuda(), "N").cpu().numpy(), y1),

@@ -18,7 +18,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(L, s), s
     assert set(syms) <= set(_lib._SIGS), set(syms) - set(_lib._SIGS)
-    assert L.vsie_abi_version() == 3
+    assert L.vsie_abi_version() == 4
 
 
 def test_status_strings_and_defaults():
@@ -30,6 +30,7 @@ def test_status_strings_and_defaults():
     L.vsie_build_opts_default(C.byref(o))
     assert (o.max_rank, o.max_sweeps, o.oversample, o.heldout, o.world, o.seed) == (2048, 8, 16, 1000, 1, 12409010)
     assert (o.scale_re, o.scale_im) == (1.0, 0.0)
+    assert o.quad_rule == 0 and o.test_moment == 0
 
 
 def _import(grid, meshes, freq=298.2e6, **kw):
@@ -52,6 +53,8 @@ def test_argument_errors():
     assert st == -1 and not h.value and "n must be" in msg
     st, h, msg = _import(Grid(cfg.n, (5e-3, -1.0, 5e-3), cfg.origin), meshes)
     assert st == -1 and not h.value
+    st, _, msg = _import(Grid(cfg.n, cfg.h, cfg.origin), meshes, quad_rule=2)
+    assert st == -1 and "quad_rule" in msg
     st, h, msg = _import(Grid(cfg.n, cfg.h, cfg.origin), meshes, freq=-1.0)
     assert st == -1 and "freq" in msg
     L = _lib.lib()
@@ -128,3 +131,12 @@ def test_farnear_farfar_host_validation():
     L.vsie_farnear_destroy(None)
     L.vsie_farfar_destroy(None)
     del k1, k2, k3, k4
+
+
+def test_set_allocator_arguments():
+    """vsie_set_allocator: both hooks or neither (no CUDA call)."""
+    L = _lib.lib()
+    hook = _lib.ALLOC_FN(lambda n, c: None)
+    assert L.vsie_set_allocator(hook, _lib.FREE_FN(), None) == -1
+    assert "both" in L.vsie_last_error_message().decode()
+    assert L.vsie_set_allocator(_lib.ALLOC_FN(), _lib.FREE_FN(), None) == 0

@@ -106,3 +106,47 @@ def test_supercore_block_vs_oracle(ci, chi, k, nl, nr):
     rows, cols = _block_rc(cfg, chi, k, left, right)
     ok, worst = validate.entry_parity(got, oent.entries(prob, rows, cols), tol=1e-12)
     assert ok, worst
+
+
+# ---------------------------------------------------------------- the paper's 1 x 1 far rule
+def _handle_rule1(cfg):
+    from paper_2206_12409_b200 import Coupling
+    dims = tuple(cfg.n) + (cfg.m,)
+    cores = [rand_cores(dims, (1, 1, 1), 5 + c) for c in range(3)]
+    return Coupling.from_cores(grid_of(cfg), cfg.meshes(), cfg.freq, cores, nrhs_max=1, quad_rule=1)
+
+
+@pytest.mark.parametrize("ci", [1, 2, 4])
+def test_entries_paper_far_rule(ci):
+    """quad_rule = 1 (1 volume x 1 surface point for Z_bc^f) vs the oracle's
+    make_problem(quad_rule=1) (pinned by P51) at T1 1e-12: cfg 1 every entry, cfgs 2 / 4
+    1e5 uniform random entries + the corners."""
+    import torch
+    cfg = synth.get_config(ci)
+    h = _handle_rule1(cfg)
+    assert h.info()["quad_rule"] == 1
+    prob = oent.problem_from_config(cfg, quad_rule=1)
+    if ci == 1:
+        rows, cols = np.meshgrid(np.arange(3 * cfg.n_v), np.arange(cfg.m), indexing="ij")
+        rows, cols = rows.ravel(), cols.ravel()
+    else:
+        idx = synth.uniform_indices((3 * cfg.n_v, cfg.m), 100_000, 7100 + ci)
+        idx[:4] = [[0, 0], [3 * cfg.n_v - 1, cfg.m - 1], [0, cfg.m - 1], [3 * cfg.n_v - 1, 0]]
+        rows, cols = idx[:, 0], idx[:, 1]
+    got = h.entries(torch.from_numpy(rows), torch.from_numpy(cols)).cpu().numpy()
+    ref = oent.entries(prob, rows, cols)
+    ok, worst = validate.entry_parity(got, ref, tol=1e-12)
+    assert ok, worst
+
+
+def test_entries_paper_far_rule_pwl_moments_vanish(cfg1):
+    """P40 on the device: with one volume point the linear PWL test moments are zero."""
+    import torch
+    from paper_2206_12409_b200 import Coupling
+    dims = tuple(cfg1.n) + (cfg1.m,)
+    cores = [rand_cores(dims, (1, 1, 1), 5 + c) for c in range(3)]
+    h = Coupling.from_cores(grid_of(cfg1), cfg1.meshes(), cfg1.freq, cores, quad_rule=1, test_moment=2)
+    rows = np.arange(0, 3 * cfg1.n_v, 37)
+    cols = (rows * 11) % cfg1.m
+    got = h.entries(torch.from_numpy(rows), torch.from_numpy(cols)).cpu().numpy()
+    assert np.all(got == 0)

@@ -184,9 +184,11 @@ def test_P9_P10_rwg_moments(prob1, cfg1):
 
 # ---------------------------------------------------------------- entries
 
-def _mp_entry(cfg, rwg_idx, chi, vox):
+def _mp_entry(cfg, rwg_idx, chi, vox, one_point=False):
     """P12: one entry at 40 digits, from the definitions (f_n = l/(2A)(r - p) with the
-    area-weighted 3-point rule; dyad by mpmath differentiation of g)."""
+    area-weighted 3-point rule; dyad by mpmath differentiation of g).  one_point (P51): the
+    paper's far-block rule of P:287, the triangle centroid with weight A and the voxel centre
+    with weight h1 h2 h3."""
     xyz, tri = cfg.meshes()[0]
     rwg = geometry.rwg_edges(xyz, tri)
     a, b = rwg["a"][rwg_idx], rwg["b"][rwg_idx]
@@ -211,14 +213,16 @@ def _mp_entry(cfg, rwg_idx, chi, vox):
         e2 = [V[2][i] - V[0][i] for i in range(3)]
         cr = [e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]]
         A = mp.sqrt(sum(x * x for x in cr)) / 2
-        for q in range(3):
+        for q in range(1 if one_point else 3):
             bary = [mp.mpf(1) / 6] * 3
             bary[q] = mp.mpf(2) / 3
+            if one_point:
+                bary = [mp.mpf(1) / 3] * 3
             rq = [sum(bary[j] * V[j][i] for j in range(3)) for i in range(3)]
             f = [sgn * l / (2 * A) * (rq[i] - p[i]) for i in range(3)]
-            for sig in itertools.product((-1, 1), repeat=3):
+            for sig in ([(0, 0, 0)] if one_point else itertools.product((-1, 1), repeat=3)):
                 rp = [c[i] + sig[i] * hh[i] / (2 * mp.sqrt(3)) for i in range(3)]
-                w = hh[0] * hh[1] * hh[2] / 8
+                w = hh[0] * hh[1] * hh[2] / (1 if one_point else 8)
                 R = [rp[i] - rq[i] for i in range(3)]
                 def g(x, y, z):
                     rr = mp.sqrt(x * x + y * y + z * z)
@@ -229,7 +233,7 @@ def _mp_entry(cfg, rwg_idx, chi, vox):
                     order[chi] += 1
                     order[j] += 1
                     row.append((g(*R) if j == chi else 0) + mp.diff(g, R, tuple(order)) / k0 ** 2)
-                total += w * (A / 3) * sum(row[j] * f[j] for j in range(3))
+                total += w * (A if one_point else A / 3) * sum(row[j] * f[j] for j in range(3))
     return complex(total)
 
 
@@ -618,10 +622,14 @@ def test_P39_round_special_cases_and_idempotence():
 
 # ---------------------------------------------------------------- PWL test moments (NEXT-2)
 
-def _one_rwg_problem(D, moment, ng=2, h=(3e-3, 4e-3, 5e-3), origin=(0.0, 0.0, 0.0)):
+def _one_rwg_mesh(D):
     xyz = np.array([[0, -0.01, 0], [0, 0.01, 0], [0.015, 0, 0.002], [-0.012, 0.001, 0]], dtype=float)
     tri = np.array([[0, 1, 2], [1, 0, 3]], dtype=np.int32)
-    shifted = xyz + D * np.array([0.8, 0.5, -0.33])
+    return xyz + D * np.array([0.8, 0.5, -0.33]), tri
+
+
+def _one_rwg_problem(D, moment, ng=2, h=(3e-3, 4e-3, 5e-3), origin=(0.0, 0.0, 0.0)):
+    shifted, tri = _one_rwg_mesh(D)
     return entries.make_problem((1, 1, 1), h, origin, [(shifted, tri)], 298e6, ng=ng, moment=moment)
 
 
@@ -983,3 +991,49 @@ def test_P50_farfar_symmetry_and_near_rule():
     Kn = 0.5 * (farfar.k_near_oneway(Va, pa, T["Vp"][j], T["pp"][j], k0)
                 + farfar.k_near_oneway(T["Vp"][j], T["pp"][j], Va, pa, k0))
     assert abs(Kr - Kn) <= 2e-3 * abs(Kn), (Kr, Kn)
+
+
+def test_P51_paper_far_rule_one_by_one():
+    """The paper's far-block quadrature ("1 volume and 1 surface integration point"
+    for Z_bc^f; oracle quad_rule = 1).  (a) Exactness: the RWG function is linear on each
+    triangle, so the centroid rule and the 3-point interior rule integrate it exactly and
+    their moment vectors agree: J(centroid) = sum_q J_q(3-point), and the centroid is the
+    mean of the 3 interior nodes.  (b) 40 digits: two entries of cfg 1 from the definitions
+    (mpmath dyad, centroid weight A, voxel-centre weight h1 h2 h3).  (c) Consistency: shrinking the
+    RWG and the voxel by s at a fixed distance, the 1 x 1 rule approaches the 8 x 3 rule at
+    first order in s (the RWG function varies by O(1) over its triangles), ~2x per halving;
+    a wrong weight would leave an O(1) difference."""
+    cfg = synth.get_config(1)
+    xyz, tri = cfg.meshes()[0]
+    rwg = geometry.rwg_edges(xyz, tri)
+    r3, j3 = geometry.source_table(xyz, tri, rwg)
+    r1, j1 = geometry.source_table(xyz, tri, rwg, geometry.TRI_CENTROID)
+    assert r1.shape[1] == 2 and r3.shape[1] == 6
+    assert np.allclose(j1[:, 0], j3[:, :3].sum(axis=1), rtol=0, atol=1e-14 * np.abs(j1).max())
+    assert np.allclose(j1[:, 1], j3[:, 3:].sum(axis=1), rtol=0, atol=1e-14 * np.abs(j1).max())
+    assert np.allclose(r1[:, 0], r3[:, :3].mean(axis=1), rtol=0, atol=1e-15)
+    prob = entries.problem_from_config(cfg, quad_rule=1)
+    assert prob.wts.shape == (1,) and np.all(prob.offs == 0)
+    for (n, chi, vox) in ((5, 0, (0, 3, 11)), (700, 2, (6, 6, 6))):
+        ref = _mp_entry(cfg, n, chi, vox, one_point=True)
+        v = vox[0] + cfg.n[0] * (vox[1] + cfg.n[1] * vox[2])
+        got = entries.entries(prob, [chi * cfg.n_v + v], [n])[0]
+        assert abs(got - ref) <= 1e-14 * abs(ref), (got, ref)
+    errs = {}
+    for sc in (1.0, 0.5, 0.25, 0.125):
+        xyz1, tri1 = _one_rwg_mesh(0.0)
+        xyz1 = xyz1 * sc + 0.1 * np.array([0.8, 0.5, -0.33])
+        h = tuple(np.array((3e-3, 4e-3, 5e-3)) * sc)
+        Z8 = entries.field_vectors(entries.make_problem((1, 1, 1), h, (0.0, 0.0, 0.0), [(xyz1, tri1)], 298e6),
+                                   [0], [0])[0]
+        Z1 = entries.field_vectors(entries.make_problem((1, 1, 1), h, (0.0, 0.0, 0.0), [(xyz1, tri1)], 298e6,
+                                                        quad_rule=1), [0], [0])[0]
+        errs[sc] = np.max(np.abs(Z1 - Z8)) / np.max(np.abs(Z8))
+    # both rules converge to the same integral; the RWG function varies by O(1) across its
+    # triangles, so the 1 x 1 rule's error is first order in the element size (a wrong
+    # weight would not converge at all)
+    assert errs[1.0] < 0.01, errs
+    for a, b in ((1.0, 0.5), (0.5, 0.25), (0.25, 0.125)):
+        assert 1.6 < errs[a] / errs[b] < 2.6, errs
+    with pytest.raises(ValueError):
+        entries.make_problem(cfg.n, cfg.h, cfg.origin, cfg.meshes(), cfg.freq, quad_rule=2)
