@@ -12,4 +12,4 @@ Both ``oracle/`` and ``paper_2206_12409_b200`` may import it; it imports
 neither.
 """
 from .configs import CONFIGS, Config, Surface, cylinder_mesh, get_config, near_coil, near_mesh  # noqa: F401
-from .vectors import complex_gaussian, uniform_indices, SEEDS  # noqa: F401
+from .vectors import complex_gaussian, phantom_eps, uniform_indices, SEEDS  # noqa: F401

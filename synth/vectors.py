@@ -25,3 +25,20 @@ def uniform_indices(dims, count: int, seed: int) -> np.ndarray:
     rng = np.random.Generator(np.random.PCG64(seed))
     cols = [rng.integers(0, d, size=count, dtype=np.int64) for d in dims]
     return np.stack(cols, axis=1)
+
+
+def phantom_eps(n, h, origin, freq: float, eps_tissue: float = 52.0, sigma: float = 0.55) -> np.ndarray:
+    """Synthetic body phantom (the paper's head / body models are not available): complex
+    relative permittivity per voxel, i1 fastest (v = i1 + n1 (i2 + n2 i3)).  An ellipsoid
+    filling 80% of the box along each axis holds tissue eps_r - i sigma / (omega eps0)
+    (exp(+i omega t), matching g = exp(-i k0 R) / (4 pi R)); outside it is air (eps_r = 1).
+    Defaults: muscle-like 52, 0.55 S/m (the 7 T range of the paper's tissue values)."""
+    eps0 = 8.8541878128e-12
+    c = [origin[a] + (n[a] - 1) * h[a] / 2.0 for a in range(3)]
+    ax = [0.4 * n[a] * h[a] for a in range(3)]
+    i1, i2, i3 = np.meshgrid(np.arange(n[0]), np.arange(n[1]), np.arange(n[2]), indexing="ij")
+    r2 = sum(((origin[a] + idx * h[a] - c[a]) / ax[a]) ** 2 for a, idx in enumerate((i1, i2, i3)))
+    inside = (r2 <= 1.0).transpose(2, 1, 0).reshape(-1)   # i1 fastest
+    eps = np.ones(n[0] * n[1] * n[2], dtype=np.complex128)
+    eps[inside] = eps_tissue - 1j * sigma / (2 * np.pi * freq * eps0)
+    return eps

@@ -1037,3 +1037,67 @@ def test_P51_paper_far_rule_one_by_one():
         assert 1.6 < errs[a] / errs[b] < 2.6, errs
     with pytest.raises(ValueError):
         entries.make_problem(cfg.n, cfg.h, cfg.origin, cfg.meshes(), cfg.freq, quad_rule=2)
+
+
+# ---------------------------------------------------------------- GMRES consumer (NEXT-4)
+def test_P52_gmres_textbook_properties():
+    """oracle/gmres.py against what the mathematics fixes (Saad & Schultz GMRES; P:287
+    tol 1e-5, restart 50): (a) an n x n system is solved in <= n iterations (Krylov space
+    exhausts C^n) to the accuracy of numpy.linalg.solve; (b) the Arnoldi relation
+    A V_k = V_{k+1} H_k and V_{k+1}^H V_{k+1} = I; (c) the recurrence residual |g_{j+1}| equals
+    the true residual ||b - A x_j|| (checked at a cycle end); (d) identity and scaled identity
+    converge in one iteration; (e) residuals never increase within a cycle (least squares over
+    nested spaces); (f) a restart (m < n) still converges on a well-conditioned system, and
+    the zero right-hand side returns x = 0 after 0 iterations."""
+    from oracle import gmres
+    rng = np.random.default_rng(52)
+    n = 40
+    A = np.eye(n) * 4 + (rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))) / np.sqrt(n)
+    b = rng.normal(size=n) + 1j * rng.normal(size=n)
+    hist = []
+    x, its, rel = gmres.gmres(lambda v: A @ v, b, tol=1e-13, restart=n, max_iter=n, history=hist)
+    xs = np.linalg.solve(A, b)
+    assert its <= n and np.linalg.norm(x - xs) <= 1e-11 * np.linalg.norm(xs)
+    assert all(h1 <= h0 * (1 + 1e-12) for h0, h1 in zip(hist, hist[1:]))
+    V, H = gmres.arnoldi(lambda v: A @ v, b, 12)
+    assert np.linalg.norm(A @ V[:, :12] - V @ H) <= 1e-13 * np.linalg.norm(A) * np.sqrt(12)
+    assert np.linalg.norm(V.conj().T @ V - np.eye(13)) <= 1e-14 * 13
+    assert np.allclose(np.triu(H, -1), H)   # upper Hessenberg
+    x7, its7, rel7 = gmres.gmres(lambda v: A @ v, b, tol=1e-30, restart=7, max_iter=7)
+    assert its7 == 7 and abs(rel7 - np.linalg.norm(b - A @ x7) / np.linalg.norm(b)) <= 1e-12
+    for s in (1.0, 2.5 - 1j):
+        x1, its1, _ = gmres.gmres(lambda v: s * v, b, tol=1e-12)
+        assert its1 == 1 and np.allclose(x1, b / s, rtol=1e-14, atol=0)
+    xr, itsr, relr = gmres.gmres(lambda v: A @ v, b, tol=1e-10, restart=5, max_iter=400)
+    assert relr <= 1e-10 and np.linalg.norm(b - A @ xr) <= 2e-10 * np.linalg.norm(b)
+    x0, its0, rel0 = gmres.gmres(lambda v: A @ v, np.zeros(n), tol=1e-5)
+    assert its0 == 0 and not x0.any()
+
+
+def test_P53_hybrid_operator_blocks():
+    """oracle/hybrid.py: the block structure of Eq. 15 -- unit vectors of each unknown group
+    pick out the block columns (Z_cc^ff / Z_cc^fn / Z_cb^f for e_f; (Z_cc^fn)^T / Z_cc^nn /
+    Z_cb^n for e_n; (Z_cb^f)^T / (Z_cb^n)^T / d_b for e_b), checked against dense copies of
+    the TT blocks (ttmv.full_matrix); and the PWC body diagonal is h1 h2 h3 eps_r (Eq. 2)."""
+    from oracle import hybrid
+    rng = np.random.default_rng(53)
+    n, mf, mn = (3, 2, 2), 5, 4
+    dims_f, dims_n = n + (mf,), n + (mn,)
+    def tt(dims, seed):
+        r = np.random.default_rng(seed)
+        ranks = (1, 2, 2, 2, 1)
+        return [r.normal(size=(ranks[k], dims[k], ranks[k + 1])) + 1j * r.normal(size=(ranks[k], dims[k], ranks[k + 1]))
+                for k in range(4)]
+    ttf = [tt(dims_f, 10 + c) for c in range(3)]
+    ttn = [tt(dims_n, 20 + c) for c in range(3)]
+    c = lambda *s: rng.normal(size=s) + 1j * rng.normal(size=s)   # noqa: E731
+    blocks = dict(Zff=c(mf, mf), Zfn=c(mn, mf), Znn=c(mn, mn), tt_far=ttf, tt_near=ttn,
+                  d_body=hybrid.body_diagonal(n, (1e-3, 2e-3, 3e-3), c(12)))
+    assert np.allclose(blocks["d_body"][:12] / 6e-9, blocks["d_body"][12:24] / 6e-9)
+    Ff, Fn = ttmv.full_matrix(ttf), ttmv.full_matrix(ttn)      # [3 n_v x m]
+    N = mf + mn + 3 * 12
+    A = np.column_stack([hybrid.matvec(blocks, e) for e in np.eye(N)])
+    ref = np.block([[blocks["Zff"], blocks["Zfn"].T, Ff.T],
+                    [blocks["Zfn"], blocks["Znn"], Fn.T],
+                    [Ff, Fn, np.diag(blocks["d_body"])]])
+    assert np.allclose(A, ref, rtol=1e-13, atol=1e-13 * np.abs(ref).max())
