@@ -267,7 +267,7 @@ void adj_g1_batched(const Ctx& X, Shard& s, const cplx* u, bool cj, cudaStream_t
   }
   Scope sc(h, "adj_g1_reduce", 16 * ((int64_t)n1 * r1s + r1s * n2 * n3l + 3LL * n1 * n2 * n3l),
            8 * (int64_t)n1 * r1s * n2 * n3l, st);
-  launch_reduce_g1(r, st);
+  launch_reduce_g1(r, st, true);
 }
 
 // W2 = G2^T W1 of one chi as a split-K ZGEMM (block RHS)

@@ -166,7 +166,9 @@ struct ReduceArgs {
   int nbatch;
   bool conj_u;
 };
-void launch_reduce_g1(const ReduceArgs& a, cudaStream_t st);
+// tma: the TMA-ring kernel (one launch for a batch that owns the GPU, single RHS); false keeps
+// the small-footprint k_reduce_g1 (a chain kernel that shares the SMs with a concurrent stream)
+void launch_reduce_g1(const ReduceArgs& a, cudaStream_t st, bool tma = false);
 
 // out[i + ld_out j] = sum_{c<3} in[c * chi_stride + i + ld_in j] (fixed order), conj if asked;
 // i < rows, j < k  (the Eq. 18 sum over chi of the per-chi transposes)

@@ -896,15 +896,23 @@ bool launch_reduce_g1_tma(const ReduceArgs& a, cudaStream_t st) {
   const int64_t stage_off = (frag + 127) / 128 * 128;
   const int q = (int)std::max<int64_t>(1, 25600 / (128LL * n1));
   const int64_t stage_bytes = 8LL * q * n1 * (int64_t)sizeof(cplx);
-  // one CTA per SM with as many stages as fit (two CTAs per SM with half the stages each
-  // measured slower at cfg 4: 139 vs 120 us, the stage consumers are the bottleneck)
-  const int64_t smem_max = 227 * 1024;
-  const int ns = (int)std::min<int64_t>(16, (smem_max - stage_off) / stage_bytes);
+  // CTAs per SM: one with as many stages as fit for long streams (cfg 4: 120 us vs 139 us for
+  // two per SM with half the stages each), two when each CTA would get few stages (cfg 2:
+  // ~17 stages per CTA, pair step 0.158 vs 0.170 ms: pipeline fill and drain dominate)
+  const int64_t nst_all = ceil_div(a.ncol, 8LL * q);
+  int cps_sm = nst_all / std::max(1, sm_count() / std::max(1, a.nbatch)) < 64 ? 2 : 1;
+  int64_t smem_max = cps_sm == 1 ? 227 * 1024 : 233472 / 2 - 1024;
+  int ns = (int)std::min<int64_t>(16, (smem_max - stage_off) / stage_bytes);
+  if (ns < 3 && cps_sm == 2) {
+    cps_sm = 1;
+    smem_max = 227 * 1024;
+    ns = (int)std::min<int64_t>(16, (smem_max - stage_off) / stage_bytes);
+  }
   if (ns < 2) return false;
   const int npairs = std::min(kRtPairs, ns);
   const size_t smem = (size_t)(stage_off + ns * stage_bytes);
   const int64_t nst = ceil_div(a.ncol, 8LL * q);
-  dim3 grid((unsigned)std::min<int64_t>(nst, std::max(1, sm_count() / std::max(1, a.nbatch))), a.nbatch);
+  dim3 grid((unsigned)std::min<int64_t>(nst, std::max(1, cps_sm * sm_count() / std::max(1, a.nbatch))), a.nbatch);
   const dim3 blk(32 * (2 * npairs + 1));
 #define VSIE_RT(K, R)                                                                                     \
   if (NT == K && REM == R) {                                                                              \
@@ -933,8 +941,8 @@ bool launch_reduce_g1_tma(const ReduceArgs& a, cudaStream_t st) {
   return false;
 }
 
-void launch_reduce_g1(const ReduceArgs& a, cudaStream_t st) {
-  if (launch_reduce_g1_tma(a, st)) return;
+void launch_reduce_g1(const ReduceArgs& a, cudaStream_t st, bool tma) {
+  if (tma && launch_reduce_g1_tma(a, st)) return;
   int r1max = 0;
   for (int b = 0; b < a.nbatch; ++b) r1max = std::max(r1max, a.r1[b]);
   VSIE_REQUIRE(r1max <= 32, VSIE_ERR_ARG, "reduce: r1 > 32 not supported");
