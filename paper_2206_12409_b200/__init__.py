@@ -6,6 +6,7 @@ The compute path is the sm_100a C-ABI library ``libvsie_coupling.so``
 from ._lib import VsieError, lib  # noqa: F401
 from .coupling import Coupling, Grid, PWLCoupling, nccl_unique_id, slab_partition, set_allocator, use_torch_allocator  # noqa: F401
 from .farnear import FarFar, FarNear  # noqa: F401
+from .hybrid import Hybrid  # noqa: F401
 
 
 def grid_of(cfg) -> Grid:

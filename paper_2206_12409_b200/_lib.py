@@ -69,6 +69,16 @@ class vsie_farnear_info(C.Structure):
                 ("entries_evaluated", C.c_int64), ("factor_bytes", C.c_int64), ("apply_calls", C.c_int64)]
 
 
+class vsie_hybrid_info(C.Structure):
+    _fields_ = [("m_far", C.c_int64), ("m_near", C.c_int64), ("n_body", C.c_int64), ("n", C.c_int64),
+                ("matvecs", C.c_int64)]
+
+
+class vsie_gmres_info(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("restarts", C.c_int32), ("converged", C.c_int32),
+                ("rel_residual", C.c_double), ("seconds", C.c_double), ("matvec_seconds", C.c_double)]
+
+
 class vsie_farfar_info(C.Structure):
     _fields_ = [("m", C.c_int64), ("tile", C.c_int32), ("tiles", C.c_int64), ("matrix_bytes", C.c_int64),
                 ("near_pairs", C.c_int64), ("build_s", C.c_double), ("k0", C.c_double), ("apply_calls", C.c_int64)]
@@ -130,6 +140,12 @@ _SIGS = {
     "vsie_farfar_apply": (C.c_int32, [HANDLE, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
     "vsie_farfar_export": (C.c_int32, [HANDLE, C.c_void_p]),
     "vsie_farfar_get_info": (C.c_int32, [HANDLE, C.POINTER(vsie_farfar_info)]),
+    "vsie_hybrid_create": (C.c_int32, [HANDLE, HANDLE, HANDLE, HANDLE, HANDLE, C.c_void_p, C.POINTER(HANDLE)]),
+    "vsie_hybrid_matvec": (C.c_int32, [HANDLE, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vsie_hybrid_gmres": (C.c_int32, [HANDLE, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_double,
+                                      C.c_void_p, C.POINTER(vsie_gmres_info), C.c_void_p]),
+    "vsie_hybrid_get_info": (C.c_int32, [HANDLE, C.POINTER(vsie_hybrid_info)]),
+    "vsie_hybrid_destroy": (None, [HANDLE]),
     "vsie_farfar_destroy": (None, [HANDLE]),
 }
 
@@ -139,7 +155,8 @@ def header_symbols(paths=None):
     if paths is None:
         paths = sorted(os.path.join(INCLUDE, f) for f in os.listdir(INCLUDE) if f.endswith(".h"))
     txt = "".join(open(p).read() for p in paths)
-    return sorted(set(re.findall(r"\b(vsie_[a-z_]+)\s*\(", txt)) - {"vsie_coupling_t", "vsie_farnear_t", "vsie_farfar_t"})
+    return sorted(set(re.findall(r"\b(vsie_[a-z_]+)\s*\(", txt))
+                  - {"vsie_coupling_t", "vsie_farnear_t", "vsie_farfar_t", "vsie_hybrid_t"})
 
 
 class VsieError(RuntimeError):

@@ -13,6 +13,7 @@
 #include "farfar.hpp"
 #include "farnear.hpp"
 #include "handle.hpp"
+#include "hybrid.hpp"
 
 using namespace vsie;
 
@@ -696,6 +697,51 @@ void vsie_farfar_destroy(vsie_farfar_t h) {
   if (!h) return;
   cudaDeviceSynchronize();
   delete h;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ hybrid system + GMRES (vsie_hybrid.h)
+extern "C" {
+
+int32_t vsie_hybrid_create(vsie_farfar_t ff, vsie_farnear_t fn, vsie_farfar_t nn, vsie_coupling_t cb_far,
+                           vsie_coupling_t cb_near, const void* d_body, vsie_hybrid_t* out) {
+  return guarded([&] {
+    VSIE_REQUIRE(out != nullptr, VSIE_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    std::unique_ptr<vsie_hybrid_s, void (*)(vsie_hybrid_s*)> h(hybrid_new(), hybrid_delete);
+    hybrid_create(ff, fn, nn, cb_far, cb_near, d_body, h.get());
+    *out = h.release();
+    return VSIE_OK;
+  });
+}
+
+int32_t vsie_hybrid_matvec(vsie_hybrid_t h, const void* x, void* y, void* stream) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "NULL handle");
+    hybrid_matvec(h, x, y, static_cast<cudaStream_t>(stream));
+    return VSIE_OK;
+  });
+}
+
+int32_t vsie_hybrid_gmres(vsie_hybrid_t h, const void* b, void* x, int32_t restart, int32_t max_iter, double tol,
+                          double* history, vsie_gmres_info* info, void* stream) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr, VSIE_ERR_ARG, "NULL handle");
+    return hybrid_gmres(h, b, x, restart, max_iter, tol, history, info, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int32_t vsie_hybrid_get_info(vsie_hybrid_t h, vsie_hybrid_info* out) {
+  return guarded([&] {
+    VSIE_REQUIRE(h != nullptr && out != nullptr, VSIE_ERR_ARG, "NULL argument");
+    hybrid_info(h, out);
+    return VSIE_OK;
+  });
+}
+
+void vsie_hybrid_destroy(vsie_hybrid_t h) {
+  if (h) hybrid_delete(h);
 }
 
 }  // extern "C"
