@@ -217,12 +217,12 @@ def run_reference(args):
     return 0
 
 
-def device_cores(cfg, ranks, seed, dev):
+def device_cores(cfg, ranks, seed, dev, m=None):
     """Seeded random complex TT cores at the given ranks, drawn on the device (the core
     values do not change the matvec cost) and returned as host arrays."""
     import torch
     g = torch.Generator(device=dev)
-    dims = tuple(cfg.n) + (cfg.m,)
+    dims = tuple(cfg.n) + (cfg.m if m is None else m,)
     out = []
     for c in range(3):
         rr = (1,) + tuple(ranks[c]) + (1,)
@@ -262,6 +262,9 @@ def main():
                          "(single process only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-farnear", action="store_true", help="skip the far-near ACA block sub-measurement")
+    ap.add_argument("--no-gmres", action="store_true", help="skip the GMRES consumer sub-measurement")
+    ap.add_argument("--no-paper-setting", action="store_true",
+                    help="skip the paper-setting build (tol 1e-3, 1 x 1 quadrature) sub-measurement")
     ap.add_argument("--separate", action="store_true",
                     help="time the step as two vsie_coupling_apply calls instead of vsie_coupling_apply_pair")
     args = ap.parse_args()
@@ -475,6 +478,7 @@ def main():
     # ---- far-near block: device ACA of Z_cc^fn against the synthetic near
     # coil, then the Eq. 15 pair y_n = U W^T j_f, y_f = W U^T j_n (two launches), L2 flushed
     farnear = None
+    gm = None
     if not args.no_farnear:
         from paper_2206_12409_b200 import FarFar, FarNear
         tol_fn = 1e-3   # the hybrid method's ACA tolerance
@@ -510,6 +514,49 @@ def main():
             torch.cuda.synchronize()
             ts2.append(e0.elapsed_time(e1))
         ffms = float(np.median(ts2))
+        # ---- GMRES consumer (include/vsie_hybrid.h): the Eq. 15 system with
+        # this handle as Z_cb^f, the two blocks above, Z_cc^nn on the near coil, a near coupling
+        # TT (seeded cores at this handle's ranks) and the PWC body diagonal h1 h2 h3 eps_r of the
+        # synthetic phantom; restarted GMRES(50) for a fixed 60 iterations (tol out of reach)
+        gm = None
+        if world == 1 and k == 1 and not args.no_gmres:
+            from paper_2206_12409_b200 import Hybrid
+            near = [synth.near_mesh(cfg.idx)]
+            nn = FarFar.build(near, cfg.freq)
+            cbn = Coupling.from_cores(grid_of(cfg), near, cfg.freq,
+                                      device_cores(cfg, ranks, 8, dev, m=fi["m_near"]), nrhs_max=1)
+            eps = synth.phantom_eps(cfg.n, cfg.h, cfg.origin, cfg.freq)
+            d_b = torch.from_numpy(np.tile(cfg.h[0] * cfg.h[1] * cfg.h[2] * eps, 3)).to(dev)
+            hy = Hybrid(ff, h, d_b, fn=fn, nn=nn, cb_near=cbn)
+            hn = hy.info()["n"]
+            bvec = torch.zeros(hn, dtype=torch.complex128, device=dev)
+            bvec[: fi["m_far"]] = device_gaussian(fi["m_far"], 1, 7103, dev)
+            hy.gmres(bvec, restart=50, max_iter=3, tol=1e-30)            # warm-up (graph captures)
+            xg, gi, ghist = hy.gmres(bvec, restart=50, max_iter=60, tol=1e-30)
+            mv0 = hy.info()["matvecs"]
+            t_mv = []
+            for i in range(5):
+                flush.fill_(i & 255)
+                e0.record()
+                hy.matvec(bvec, out=xg)
+                e1.record()
+                torch.cuda.synchronize()
+                t_mv.append(e0.elapsed_time(e1))
+            gm = {"n": hn, "m_far": fi["m_far"], "m_near": fi["m_near"], "n_body": 3 * cfg.n_v,
+                  "restart": 50, "iterations": gi["iterations"], "restarts": gi["restarts"],
+                  "rel_residual_after": gi["rel_residual"], "solve_s": gi["seconds"],
+                  "ms_per_iteration": 1e3 * gi["seconds"] / gi["iterations"],
+                  "matvec_share": gi["matvec_seconds"] / gi["seconds"],
+                  "matvec_ms": float(np.median(t_mv)), "matvecs_counted": mv0,
+                  "krylov_basis_gb": 16 * hn * 51 / 1e9,
+                  "note": ("Eq. 15 operator: Z_cc^ff + ACA (tol 1e-3) + Z_cc^nn + the TT coupling pair of "
+                           "this handle + a near TT pair (seeded cores) + body diagonal; Z_bb's nonlocal "
+                           "FFT part and pFFT are out of scope (DESIGN.md R-G1); 60 iterations of "
+                           "GMRES(50) incl. one restart, host wall time; matvec_ms: staged matvec, "
+                           "median of 5, L2 flushed")}
+            hy.close()
+            nn.close()
+            cbn.close()
         ff.close()
         farnear = {"m_near": fi["m_near"], "m_far": fi["m_far"], "aca_tol": tol_fn, "rank": fi["rank"],
                    "stop": fi["stop"], "aca_est_err": fi["est_err"], "build_s": fi["build_s"],
@@ -525,6 +572,31 @@ def main():
                               "dense_equivalent_gbs": 16 * ffi["m"] ** 2 / (ffms * 1e-3) / 1e9,
                               "note": "Z_cc^ff y = Z x from the symmetric half (128 x 128 lower tiles, read once)"}}
         fn.close()
+
+    # ---- the paper's own setting: TT-cross tol 1e-3 on the 1 x 1 far rule (quad_rule 1):
+    # build time, ranks, held-out error, and the GMRES coupling pair on those cores (L2 flushed)
+    paper = None
+    if world == 1 and k == 1 and not args.no_paper_setting:
+        t1 = time.perf_counter()
+        hp = Coupling.build(grid_of(cfg), cfg.meshes(), cfg.freq, 1e-3, nrhs_max=1, quad_rule=1)
+        pb = time.perf_counter() - t1
+        pi = hp.info()
+        for _ in range(3):
+            hp.apply_pair(x, u, "T", out_y=y, out_z=z)
+        tp = []
+        for i in range(20):
+            flush.fill_(i & 255)
+            e0.record()
+            hp.apply_pair(x, u, "T", out_y=y, out_z=z)
+            e1.record()
+            torch.cuda.synchronize()
+            tp.append(e0.elapsed_time(e1))
+        pms = float(np.median(tp))
+        pbytes = moved_bytes(cfg.n, cfg.m, pi["ranks"], pi["pair_schedule"])
+        paper = {"tol": 1e-3, "quad_rule": 1, "ranks": pi["ranks"], "build_s": pb, "heldout_err": pi["heldout_err"],
+                 "pair_ms": pms, "pair_moved_gbs": pbytes / (pms * 1e-3) / 1e9,
+                 "note": "P:287: TT-cross tolerance 1e-3, 1 volume x 1 surface integration point for Z_bc^f"}
+        hp.close()
 
     # ---- FP64 roofline of the entry kernel: measured FP64 instructions per entry x entries/s
     # over the measured DFMA issue rate (one FP64-pipe thread instruction per FMA)
@@ -631,6 +703,8 @@ def main():
                     "structured_note": "supercore blocks evaluated by the TT-cross build (entries / entry-kernel time)"},
         "roofline": roof,
         "farnear": farnear,
+        "gmres": gm if not args.no_farnear else None,
+        "paper_setting": paper,
         "kernels": kern_table,
         "cpu_baseline": cpu,
         "e2e": e2e,
