@@ -519,12 +519,17 @@ def main():
         # TT (seeded cores at this handle's ranks) and the PWC body diagonal h1 h2 h3 eps_r of the
         # synthetic phantom; restarted GMRES(50) for a fixed 60 iterations (tol out of reach)
         gm = None
+        cbn = None
         if world == 1 and k == 1 and not args.no_gmres:
-            from paper_2206_12409_b200 import Hybrid
+            from paper_2206_12409_b200 import Hybrid, VsieError
             near = [synth.near_mesh(cfg.idx)]
+            try:
+                cbn = Coupling.from_cores(grid_of(cfg), near, cfg.freq,
+                                          device_cores(cfg, ranks, 8, dev, m=fi["m_near"]), nrhs_max=1)
+            except VsieError as ex:   # the near coil too close to this grid for the coupling's rule
+                gm = {"skipped": f"near coupling not buildable on this grid: {ex}"}
+        if cbn is not None:
             nn = FarFar.build(near, cfg.freq)
-            cbn = Coupling.from_cores(grid_of(cfg), near, cfg.freq,
-                                      device_cores(cfg, ranks, 8, dev, m=fi["m_near"]), nrhs_max=1)
             eps = synth.phantom_eps(cfg.n, cfg.h, cfg.origin, cfg.freq)
             d_b = torch.from_numpy(np.tile(cfg.h[0] * cfg.h[1] * cfg.h[2] * eps, 3)).to(dev)
             hy = Hybrid(ff, h, d_b, fn=fn, nn=nn, cb_near=cbn)
