@@ -546,7 +546,7 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_reduce_g1_tma(const __grid_co
   if (threadIdx.x == 0) {
     for (int s = 0; s < ns; ++s) {
       tma::mbar_init(full + s, 1);
-      tma::mbar_init(empty + s, 1);
+      tma::mbar_init(empty + s, q);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -581,19 +581,21 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_reduce_g1_tma(const __grid_co
     pdl_trigger();
     return;
   }
-  // consumer pairs: at most ns of them, so that the stage a pair waits for is never two ring
-  // phases ahead of the producer (the pair's previous task was j - npairs >= j - ns)
-  const int npairs = (int)(blockDim.x / 64);   // launched with 2 npairs + 1 warps, npairs <= ns
-  const int pair = warp >> 1, half = warp & 1;
+  // consumer groups of 2 q warps (warp pair (tile, half) per 8-column tile of a stage): at
+  // most ns groups, so that the stage a group waits for is never two ring phases ahead of the
+  // producer (the group's previous task was j - ngroups >= j - ns)
+  const int gsz = 2 * q;
+  const int ngroups = (int)(blockDim.x / 32 - 1) / gsz;   // launched with 2 q ngroups + 1 warps
+  const int grp = warp / gsz, tile = (warp % gsz) >> 1, half = warp & 1;
   const int ksh = (ks_n + 1) / 2;
   const int ks0 = half ? ksh : 0, ks1 = half ? ks_n : ksh;
   const int g = lane >> 2, t4 = lane & 3;
-  int j = pair;
-  for (int64_t t = blockIdx.x + (int64_t)pair * gridDim.x; t < nst; t += (int64_t)npairs * gridDim.x, j += npairs) {
+  int j = grp;
+  for (int64_t t = blockIdx.x + (int64_t)grp * gridDim.x; t < nst; t += (int64_t)ngroups * gridDim.x, j += ngroups) {
     const int slot = j % ns;
     tma::mbar_wait(full + slot, (j / ns) & 1);
     cplx* S = stg + slot * stage_elems;
-    for (int tile = 0; tile < q; ++tile) {
+    {
       const int64_t cg = t * cps + 8 * tile + g;
       const cplx* __restrict__ col = S + (int64_t)(8 * tile + g) * n1;
       double p1[NTA][2], p2[NTA][2], p3[NTA][2];
@@ -620,7 +622,7 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_reduce_g1_tma(const __grid_co
       // both halves are done with this tile's u: the upper half's partials go through the
       // stage buffer (tile 8 columns x n1 >= 32 lanes x 6 NT + 2 REM doubles, checked by the host) to the lower half
       double* xch = reinterpret_cast<double*>(S + (int64_t)8 * tile * n1);
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + grp * q + tile) : "memory");
       if (half) {
 #pragma unroll
         for (int nt = 0; nt < NTA; ++nt)
@@ -636,8 +638,8 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_reduce_g1_tma(const __grid_co
           xch[(6 * NTA + 2 * jj + 1) * 32 + lane] = rem[jj].y;
         }
       }
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
-      if (half) continue;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + grp * q + tile) : "memory");
+      if (!half) {
 #pragma unroll
       for (int nt = 0; nt < NTA; ++nt)
 #pragma unroll
@@ -672,10 +674,9 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_reduce_g1_tma(const __grid_co
         const int aa = 8 * NT + jj;
         if (cok && t4 == 0 && aa < r1) W[aa] = v;
       }
-    }
-    if (!half) {
       __syncwarp();
-      if (lane == 0) tma::mbar_arrive(empty + slot);
+      if (lane == 0) tma::mbar_arrive(empty + slot);   // one arrival per tile (count q)
+      }
     }
   }
   pdl_trigger();
@@ -894,7 +895,11 @@ bool launch_reduce_g1_tma(const ReduceArgs& a, cudaStream_t st) {
   if (32 * (6 * std::max(NT, 1) + 2 * std::max(REM, 1)) > 16 * n1) return false;
   const int64_t frag = 256 + ((int64_t)ks_n * std::max(NT, 1) * 32 + 4LL * ks_n * REM) * (int64_t)sizeof(cplx);
   const int64_t stage_off = (frag + 127) / 128 * 128;
-  const int q = (int)std::max<int64_t>(1, 25600 / (128LL * n1));
+  // two 8-column tiles per stage (a warp pair on each): cfg 4 (n1 = 200, 51 KB stages, 3 of
+  // them) pair step 0.458 -> 0.438 ms although the kernel alone is ~5% slower -- its smaller
+  // smem footprint lets the next kernel's CTAs become resident under its tail (PDL); one tile
+  // per stage only when two would not leave three stages
+  const int q = stage_off + 3LL * 16 * n1 * (int64_t)sizeof(cplx) <= 227 * 1024 ? 2 : 1;
   const int64_t stage_bytes = 8LL * q * n1 * (int64_t)sizeof(cplx);
   // CTAs per SM: one with as many stages as fit for long streams (cfg 4: 120 us vs 139 us for
   // two per SM with half the stages each), two when each CTA would get few stages (cfg 2:
@@ -909,11 +914,11 @@ bool launch_reduce_g1_tma(const ReduceArgs& a, cudaStream_t st) {
     ns = (int)std::min<int64_t>(16, (smem_max - stage_off) / stage_bytes);
   }
   if (ns < 2) return false;
-  const int npairs = std::min(kRtPairs, ns);
+  const int ngroups = std::max(1, std::min(ns, kRtPairs / q));
   const size_t smem = (size_t)(stage_off + ns * stage_bytes);
   const int64_t nst = ceil_div(a.ncol, 8LL * q);
   dim3 grid((unsigned)std::min<int64_t>(nst, std::max(1, cps_sm * sm_count() / std::max(1, a.nbatch))), a.nbatch);
-  const dim3 blk(32 * (2 * npairs + 1));
+  const dim3 blk(32 * (2 * q * ngroups + 1));
 #define VSIE_RT(K, R)                                                                                     \
   if (NT == K && REM == R) {                                                                              \
     static bool d0 = false, d1 = false;                                                                   \
