@@ -31,13 +31,15 @@ namespace {
 // polynomials of cos / sin(delta_p) (truncation <= |delta|^8 / 8! < 1e-19) per pair give
 // exp(-i k0 R_p) by angle addition -- the same value as a sincos per pair to rounding, at
 // ~1/3 of its FP64 instructions (g.taylor; otherwise a sincos per pair).
-template <int NP>
+template <int NP, bool SM>
 __device__ __forceinline__ void entry_acc(const EntryGeom& g, int chi, double cx, double cy, double cz,
                                           const double* __restrict__ s36, double& ar, double& ai) {
+  // SM: the source record is staged in shared memory (block mode); else read through L1
+  auto ld = [&](int i) { return SM ? s36[i] : __ldg(s36 + i); };
 #pragma unroll 1
   for (int q = 0; q < g.nsrc; ++q) {
-    const double sx = __ldg(s36 + 6 * q + 0), sy = __ldg(s36 + 6 * q + 1), sz = __ldg(s36 + 6 * q + 2);
-    const double jx = __ldg(s36 + 6 * q + 3), jy = __ldg(s36 + 6 * q + 4), jz = __ldg(s36 + 6 * q + 5);
+    const double sx = ld(6 * q + 0), sy = ld(6 * q + 1), sz = ld(6 * q + 2);
+    const double jx = ld(6 * q + 3), jy = ld(6 * q + 4), jz = ld(6 * q + 5);
     const double jc = chi == 0 ? jx : (chi == 1 ? jy : jz);
     const double bx = cx - sx, by = cy - sy, bz = cz - sz;
     double s0 = 0, c0 = 1, kr0 = 0;
@@ -81,15 +83,15 @@ __device__ __forceinline__ void entry_acc(const EntryGeom& g, int chi, double cx
   }
 }
 
+template <bool SM>
 __device__ __forceinline__ cplx entry_value(const EntryGeom& g, int chi, int i1, int i2, int i3,
-                                            int64_t n) {
+                                            const double* __restrict__ s36) {
   const double cx = g.ox + i1 * g.hx, cy = g.oy + i2 * g.hy, cz = g.oz + i3 * g.hz;
-  const double* s36 = g.src + 36 * n;
   double ar = 0, ai = 0;
   if (g.nodes == 1)
-    entry_acc<1>(g, chi, cx, cy, cz, s36, ar, ai);
+    entry_acc<1, SM>(g, chi, cx, cy, cz, s36, ar, ai);
   else
-    entry_acc<8>(g, chi, cx, cy, cz, s36, ar, ai);
+    entry_acc<8, SM>(g, chi, cx, cy, cz, s36, ar, ai);
   ar *= g.w;
   ai *= g.w;
   return cmk(g.scale_re * ar - g.scale_im * ai, g.scale_re * ai + g.scale_im * ar);
@@ -105,40 +107,85 @@ __global__ void __launch_bounds__(256) k_entries_list(EntryGeom g, const int64_t
     const int i1 = (int)(v % g.n1);
     const int i2 = (int)((v / g.n1) % g.n2);
     const int i3 = (int)(v / ((int64_t)g.n1 * g.n2));
-    out[t] = entry_value(g, chi, i1, i2, i3, col);
+    out[t] = entry_value<false>(g, chi, i1, i2, i3, g.src + 36 * col);
   }
 }
 
-__global__ void __launch_bounds__(256) k_entries_block(EntryGeom g, BlockDesc b, cplx* __restrict__ out) {
+// Block mode: tiles of 256 consecutive entries (rows fastest), so a tile touches only
+// ceil(256 / rows) + 1 columns of the supercore: their RWG source records (the quadrature
+// nodes and moments, 36 doubles each) are staged in shared memory once per tile.
+constexpr int kEntThreads = 256;
+constexpr int kEntPer = 4;                           // entries per thread and tile
+constexpr int kEntTile = kEntThreads * kEntPer;
+constexpr int kEntMaxCols = 96;   // rows >= 12 (every k_n of the configs); wider tiles fall back
+
+__device__ __forceinline__ void block_coords(const BlockDesc& b, int64_t r, int64_t c, int& i1, int& i2, int& i3,
+                                             int64_t& n) {
+  const int64_t alpha = r % b.rl, ik = r / b.rl;
+  const int64_t ik1 = c % b.nk1, beta = c / b.nk1;
+  if (b.k == 1) {
+    i1 = (int)ik;
+    i2 = (int)ik1;
+    i3 = b.right[2 * beta];
+    n = b.right[2 * beta + 1];
+  } else if (b.k == 2) {
+    i1 = b.left[2 * alpha];
+    i2 = (int)ik;
+    i3 = (int)ik1;
+    n = b.right[2 * beta];
+  } else {
+    i1 = b.left[2 * alpha];
+    i2 = b.left[2 * alpha + 1];
+    i3 = (int)ik;
+    n = ik1;
+  }
+}
+
+__global__ void __launch_bounds__(kEntThreads) k_entries_block(EntryGeom g, BlockDesc b, cplx* __restrict__ out) {
+  __shared__ double rec[kEntMaxCols][36];
   const int64_t r0 = b.row1 > b.row0 ? b.row0 : 0;
   const int64_t rows = b.row1 > b.row0 ? b.row1 - b.row0 : b.rl * b.nk;   // rows evaluated
   const int64_t total = rows * (b.col1 - b.col0);
+  const int64_t ntile = (total + kEntTile - 1) / kEntTile;
+  for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+    const int64_t t0 = tile * kEntTile;
+    const int64_t cl0 = t0 / rows, cl1 = min(total - 1, t0 + kEntTile - 1) / rows;
+    const int ncl = (int)(cl1 - cl0 + 1);
+    __syncthreads();   // the previous tile's records are no longer read
+    for (int e = threadIdx.x; e < ncl * 36; e += kEntThreads) {
+      const int q = e / 36, w = e - 36 * q;
+      int i1, i2, i3;
+      int64_t n;
+      block_coords(b, r0, b.col0 + cl0 + q, i1, i2, i3, n);
+      rec[q][w] = __ldg(g.src + 36 * n + w);
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int u = 0; u < kEntPer; ++u) {
+      const int64_t t = t0 + u * kEntThreads + threadIdx.x;
+      if (t < total) {
+        const int64_t rr = t % rows, cl = t / rows;
+        int i1, i2, i3;
+        int64_t n;
+        block_coords(b, r0 + rr, b.col0 + cl, i1, i2, i3, n);
+        out[rr + b.ld * cl] = entry_value<true>(g, b.chi, i1, i2, i3, rec[cl - cl0]);
+      }
+    }
+  }
+}
+
+// the same without staging (tiles wider than kEntMaxCols columns: rows < 12)
+__global__ void __launch_bounds__(256) k_entries_block_direct(EntryGeom g, BlockDesc b, cplx* __restrict__ out) {
+  const int64_t r0 = b.row1 > b.row0 ? b.row0 : 0;
+  const int64_t rows = b.row1 > b.row0 ? b.row1 - b.row0 : b.rl * b.nk;
+  const int64_t total = rows * (b.col1 - b.col0);
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t rr = t % rows, r = r0 + rr;
-    const int64_t cl = t / rows;
-    const int64_t c = b.col0 + cl;
-    const int64_t alpha = r % b.rl, ik = r / b.rl;
-    const int64_t ik1 = c % b.nk1, beta = c / b.nk1;
+    const int64_t rr = t % rows, cl = t / rows;
     int i1, i2, i3;
     int64_t n;
-    if (b.k == 1) {
-      i1 = (int)ik;
-      i2 = (int)ik1;
-      i3 = b.right[2 * beta];
-      n = b.right[2 * beta + 1];
-    } else if (b.k == 2) {
-      i1 = b.left[2 * alpha];
-      i2 = (int)ik;
-      i3 = (int)ik1;
-      n = b.right[2 * beta];
-    } else {
-      i1 = b.left[2 * alpha];
-      i2 = b.left[2 * alpha + 1];
-      i3 = (int)ik;
-      n = ik1;
-    }
-    out[rr + b.ld * cl] = entry_value(g, b.chi, i1, i2, i3, n);
+    block_coords(b, r0 + rr, b.col0 + cl, i1, i2, i3, n);
+    out[rr + b.ld * cl] = entry_value<false>(g, b.chi, i1, i2, i3, g.src + 36 * n);
   }
 }
 
@@ -161,7 +208,10 @@ void launch_entries_block(const EntryGeom& g, const BlockDesc& b, cplx* out, cud
   const int64_t rows = b.row1 > b.row0 ? b.row1 - b.row0 : b.rl * b.nk;
   const int64_t total = rows * (b.col1 - b.col0);
   if (total <= 0) return;
-  k_entries_block<<<grid_for(total, 256), 256, 0, st>>>(g, b, out);
+  if (kEntTile / rows + 2 <= kEntMaxCols)
+    k_entries_block<<<grid_for(ceil_div(total, kEntPer), kEntThreads), kEntThreads, 0, st>>>(g, b, out);
+  else
+    k_entries_block_direct<<<grid_for(total, 256), 256, 0, st>>>(g, b, out);
   VSIE_CHECK_LAUNCH();
 }
 
