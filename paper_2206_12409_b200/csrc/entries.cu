@@ -34,12 +34,24 @@ namespace {
 template <int NP, bool SM>
 __device__ __forceinline__ void entry_acc(const EntryGeom& g, int chi, double cx, double cy, double cz,
                                           const double* __restrict__ s36, double& ar, double& ai) {
-  // SM: the source record is staged in shared memory (block mode); else read through L1
-  auto ld = [&](int i) { return SM ? s36[i] : __ldg(s36 + i); };
+  // SM: the source record is staged in shared memory (block mode); else read through L1 as
+  // three 16-B loads per source node (list mode: 32 different records per warp, so the load
+  // instruction count, not the bytes, is what the LSU pays for)
 #pragma unroll 1
   for (int q = 0; q < g.nsrc; ++q) {
-    const double sx = ld(6 * q + 0), sy = ld(6 * q + 1), sz = ld(6 * q + 2);
-    const double jx = ld(6 * q + 3), jy = ld(6 * q + 4), jz = ld(6 * q + 5);
+    double2 a, b, c;
+    if (SM) {
+      a = make_double2(s36[6 * q], s36[6 * q + 1]);
+      b = make_double2(s36[6 * q + 2], s36[6 * q + 3]);
+      c = make_double2(s36[6 * q + 4], s36[6 * q + 5]);
+    } else {
+      const double2* p2 = reinterpret_cast<const double2*>(s36 + 6 * q);
+      a = __ldg(p2);
+      b = __ldg(p2 + 1);
+      c = __ldg(p2 + 2);
+    }
+    const double sx = a.x, sy = a.y, sz = b.x;
+    const double jx = b.y, jy = c.x, jz = c.y;
     const double jc = chi == 0 ? jx : (chi == 1 ? jy : jz);
     const double bx = cx - sx, by = cy - sy, bz = cz - sz;
     double s0 = 0, c0 = 1, kr0 = 0;
