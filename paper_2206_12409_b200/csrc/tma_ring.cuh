@@ -30,6 +30,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// L2 prefetch of a global range (no shared memory, no completion tracking)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 // d0 (column j, all lanes) and d1 (column j + 1): after the call lane l holds the full
 // column sum of column j + (l >= 16) -- one exchange of the other half's column, then a
 // 16-lane butterfly (10 shuffles of 64 bits for two columns instead of 20)

@@ -526,6 +526,9 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce_g1(const __grid_constant
 constexpr int kRtPairs = 8;
 constexpr int kRtThreads = 32 * (2 * kRtPairs + 1);
 
+// stages L2-prefetched beyond the ring (cfg 4 pair 0.438 -> 0.422 ms with 1-3, slower with 8)
+constexpr int kG1tPrefetch = 2;
+
 template <int NT, int REM, bool CJ>
 __global__ void __launch_bounds__(kRtThreads, 1) k_reduce_g1_tma(const __grid_constant__ ReduceArgs a, int q, int ns,
                                                                   int64_t stage_off) {
@@ -568,6 +571,13 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_reduce_g1_tma(const __grid_co
     if (lane == 0) {
       const cplx* __restrict__ U = a.u[b];
       int j = 0;
+      // L2 prefetch pf stages beyond the ring: more bytes in flight than the shared memory
+      // holds (the stage a slot is refilled with is then an L2 hit)
+      constexpr int pf = kG1tPrefetch;
+      for (int64_t tp = blockIdx.x; tp < nst && tp < blockIdx.x + (int64_t)pf * gridDim.x; tp += gridDim.x) {
+        const int64_t c0 = tp * cps;
+        tma::bulk_prefetch_l2(U + c0 * n1, (uint32_t)(min(cps, a.ncol - c0) * n1 * (int64_t)sizeof(cplx)));
+      }
       for (int64_t t = blockIdx.x; t < nst; t += gridDim.x, ++j) {
         const int slot = j % ns;
         if (j >= ns) tma::mbar_wait(empty + slot, ((j / ns) - 1) & 1);
@@ -576,6 +586,11 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_reduce_g1_tma(const __grid_co
         const uint32_t bytes = (uint32_t)(nc * n1 * (int64_t)sizeof(cplx));
         tma::mbar_expect_tx(full + slot, bytes);
         tma::bulk_g2s(stg + slot * stage_elems, U + c0 * n1, bytes, full + slot);
+        const int64_t tn = t + (int64_t)pf * gridDim.x;
+        if (tn < nst) {
+          const int64_t cn = tn * cps;
+          tma::bulk_prefetch_l2(U + cn * n1, (uint32_t)(min(cps, a.ncol - cn) * n1 * (int64_t)sizeof(cplx)));
+        }
       }
     }
     pdl_trigger();
@@ -882,6 +897,7 @@ void launch_expand_g1(const ExpandArgs& a, cudaStream_t st) {
 // not fit it (the caller then runs k_reduce_g1)
 bool launch_reduce_g1_tma(const ReduceArgs& a, cudaStream_t st) {
   if (a.cols_per_rhs < a.ncol || a.ncol <= 0) return false;
+
   int r1max = 0;
   for (int b = 0; b < a.nbatch; ++b) r1max = std::max(r1max, a.r1[b]);
   if (r1max > 32) return false;
