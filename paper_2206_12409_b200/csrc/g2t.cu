@@ -11,6 +11,8 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <cstdlib>
+
 namespace vsie {
 namespace {
 
@@ -117,11 +119,21 @@ __global__ void __launch_bounds__(32 * NW) k_g2t(const __grid_constant__ G2tArgs
 
 }  // namespace
 
-// one CTA per 8 x 8 output tile, K split over its 8 warps (16 x 16 / 8 x 16 tiles measured slower)
+// one CTA per 8 x 8 output tile, K split over its 8 warps (16 x 16 / 8 x 16 tiles measured slower at
+// cfgs 2 / 4), or per 16 x 16 tile for large r2 n3
 void launch_g2t(const G2tArgs& a, cudaStream_t st) {
   int mmax = 0;
   for (int b = 0; b < a.nbatch; ++b) mmax = std::max(mmax, a.M[b]);
   if (mmax == 0 || a.N == 0) return;
+  // 16 x 16 tiles (a quarter of the L2 operand traffic) when a chi has many 8 x 8 tiles: cfg 3
+  // (r2 = 137, n3 = 400: 900 tiles) pair 1.895 -> 1.831 ms; at cfg 4 (252 tiles) the 8 x 8
+  // grid's parallelism wins (0.423 vs 0.432 ms)
+  if (ceil_div(mmax, 8) * ceil_div(a.N, 8) >= 512) {
+    dim3 grid((unsigned)ceil_div(mmax, 16), (unsigned)ceil_div(a.N, 16), a.nbatch);
+    launch_pdl(k_g2t<2, 2, 8>, grid, dim3(32 * 8), 0, st, a);
+    VSIE_CHECK_LAUNCH();
+    return;
+  }
   dim3 grid((unsigned)ceil_div(mmax, 8), (unsigned)ceil_div(a.N, 8), a.nbatch);
   launch_pdl(k_g2t<1, 1, 8>, grid, dim3(32 * 8), 0, st, a);
   VSIE_CHECK_LAUNCH();
