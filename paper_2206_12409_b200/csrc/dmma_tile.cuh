@@ -99,13 +99,18 @@ __device__ __noinline__ void gemm_tile(const cplx* __restrict__ A, int64_t lda, 
         for (int i = 0; i < 2; ++i) av[i] = Ab[(4 * ks + t) * SA + wm + 8 * i + gq];
 #pragma unroll
         for (int j = 0; j < 2; ++j) bv[j] = Bb[(wn + 8 * j + gq) * SB + 4 * ks + t];
+        double as[2], bs[2];   // the 3M operand sums, once per fragment
+#pragma unroll
+        for (int i = 0; i < 2; ++i) as[i] = av[i].x + av[i].y;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) bs[j] = bv[j].x + bv[j].y;
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             dmma(p1[i][j][0], p1[i][j][1], av[i].x, bv[j].x);
             dmma(p2[i][j][0], p2[i][j][1], av[i].y, bv[j].y);
-            dmma(p3[i][j][0], p3[i][j][1], av[i].x + av[i].y, bv[j].x + bv[j].y);
+            dmma(p3[i][j][0], p3[i][j][1], as[i], bs[j]);
           }
       }
     }
