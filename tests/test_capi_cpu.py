@@ -140,3 +140,18 @@ def test_set_allocator_arguments():
     assert L.vsie_set_allocator(hook, _lib.FREE_FN(), None) == -1
     assert "both" in L.vsie_last_error_message().decode()
     assert L.vsie_set_allocator(_lib.ALLOC_FN(), _lib.FREE_FN(), None) == 0
+
+
+def test_hybrid_host_validation():
+    """vsie_hybrid_*: NULL handles / blocks are rejected on the host (no CUDA call)."""
+    L = _lib.lib()
+    h = _lib.HANDLE()
+    assert L.vsie_hybrid_create(None, None, None, None, None, None, C.byref(h)) == -1
+    assert "required" in L.vsie_last_error_message().decode() and not h.value
+    assert L.vsie_hybrid_create(None, None, None, None, None, None, None) == -1
+    inf = _lib.vsie_gmres_info()
+    assert L.vsie_hybrid_gmres(None, None, None, 50, 10, 1e-5, None, C.byref(inf), None) == -1
+    assert L.vsie_hybrid_matvec(None, None, None, None) == -1
+    hi = _lib.vsie_hybrid_info()
+    assert L.vsie_hybrid_get_info(None, C.byref(hi)) == -1
+    L.vsie_hybrid_destroy(None)
