@@ -191,36 +191,51 @@ void fwd_g3(const Ctx& X, Shard& s, int c, cudaStream_t st) {
   launch_zgemm_dmma(z, X.zws(c), h->zgemm_ws_per_chi, st);
 }
 
-// Y2 = G2 Y3, then y = G1 Y2: the forward's compute-bound tail of one chi
-void fwd_tail(const Ctx& X, Shard& s, int c, cplx* y, cudaStream_t st) {
+// Y2 = G2 Y3 of one chi
+void fwd_g2(const Ctx& X, Shard& s, int c, cudaStream_t st) {
+  vsie_coupling_s* h = X.h;
+  const int k = X.k;
+  const int n2 = h->grid.n[1];
+  const int64_t n3l = s.n3loc(), r1 = X.R(c, 0), r2 = X.R(c, 1);
+  Zgemm z{};
+  z.M[0] = r1 * n2; z.N[0] = n3l * k; z.K[0] = r2;
+  z.A[0] = h->G2[c].p; z.lda[0] = r1 * n2;
+  z.B[0] = s.Y3.p + c * X.r2m * n3l * k; z.ldb[0] = r2;
+  z.C[0] = s.Y2.p + c * X.r1m * n2 * n3l * k; z.ldc[0] = r1 * n2;
+  Scope sc(h, "fwd_g2_zgemm", 16 * (r1 * n2 * r2 + r2 * n3l * k + r1 * n2 * n3l * k), 8 * r1 * n2 * r2 * n3l * k, st);
+  launch_zgemm_dmma(z, X.zws(c), h->zgemm_ws_per_chi, st);
+}
+
+// y = G1 Y2 of the chi [c0, c0 + nb) in one launch
+void fwd_g1(const Ctx& X, Shard& s, int c0, int nb, cplx* y, cudaStream_t st) {
   vsie_coupling_s* h = X.h;
   const int k = X.k;
   const int n1 = h->grid.n[0], n2 = h->grid.n[1];
-  const int64_t n3l = s.n3loc(), r1 = X.R(c, 0), r2 = X.R(c, 1);
-  cplx* Y3 = s.Y3.p + c * X.r2m * n3l * k;
-  cplx* Y2 = s.Y2.p + c * X.r1m * n2 * n3l * k;
-  {
-    Zgemm z{};
-    z.M[0] = r1 * n2; z.N[0] = n3l * k; z.K[0] = r2;
-    z.A[0] = h->G2[c].p; z.lda[0] = r1 * n2;
-    z.B[0] = Y3; z.ldb[0] = r2;
-    z.C[0] = Y2; z.ldc[0] = r1 * n2;
-    Scope sc(h, "fwd_g2_zgemm", 16 * (r1 * n2 * r2 + r2 * n3l * k + r1 * n2 * n3l * k), 8 * r1 * n2 * r2 * n3l * k, st);
-    launch_zgemm_dmma(z, X.zws(c), h->zgemm_ws_per_chi, st);
-  }
+  const int64_t n3l = s.n3loc();
   ExpandArgs e{};
-  e.nbatch = 1;
+  e.nbatch = nb;
   e.n1 = n1;
   e.ncol = (int64_t)n2 * n3l * k;
   e.cols_per_rhs = (int64_t)n2 * n3l;
   e.ld_rhs = X.L.ld;
-  e.G1[0] = h->G1[c].p;
-  e.Y2[0] = Y2;
-  e.y[0] = y + c * X.L.chi_stride + shard_voxel_offset(h, s, X.L);
-  e.r1[0] = (int)r1;
-  Scope sc(h, "fwd_g1_expand", 16 * ((int64_t)n1 * r1 + r1 * n2 * n3l * k + (int64_t)n1 * n2 * n3l * k),
-           8 * (int64_t)n1 * r1 * n2 * n3l * k, st);
+  int64_t r1s = 0;
+  for (int i = 0; i < nb; ++i) {
+    const int c = c0 + i;
+    e.G1[i] = h->G1[c].p;
+    e.Y2[i] = s.Y2.p + c * X.r1m * n2 * n3l * k;
+    e.y[i] = y + c * X.L.chi_stride + shard_voxel_offset(h, s, X.L);
+    e.r1[i] = (int)X.R(c, 0);
+    r1s += X.R(c, 0);
+  }
+  Scope sc(h, "fwd_g1_expand", 16 * ((int64_t)n1 * r1s + r1s * n2 * n3l * k + (int64_t)nb * n1 * n2 * n3l * k),
+           8 * (int64_t)n1 * r1s * n2 * n3l * k, st);
   launch_expand_g1(e, st);
+}
+
+// the forward's compute-bound tail of one chi: Y2 = G2 Y3, y = G1 Y2
+void fwd_tail(const Ctx& X, Shard& s, int c, cplx* y, cudaStream_t st) {
+  fwd_g2(X, s, c, st);
+  fwd_g1(X, s, c, 1, y, st);
 }
 
 // W1 = G1^T u, conj(u) for op C
@@ -703,7 +718,12 @@ void pair_dag(vsie_coupling_s* h, const cplx* x, cplx* y, const cplx* u, cplx* z
     return;
   }
   // G3-shared: the forward's G4 pass streams while the transpose's G1^T / G2^T chains
-  // compute (per chi: chi c's G2^T runs beside chi c + 1's G1^T and the G4 stream)
+  // compute (per chi: chi c's G2^T runs beside chi c + 1's G1^T and the G4 stream).  Measured
+  // against the alternatives at cfg 3 (profiles/r02c/g3s_schedules.json):
+  // one batched TMA G1^T first and the G2^T beside the G4 stream 1.748 ms, fully serial
+  // 1.737, the forward's G2 products first and the expansions beside the transpose's G4
+  // stream 1.710-1.757, vs 1.683 ms for this one (a persistent G4 stream starves the
+  // kernels beside it of SMs, so overlap only pays for short compute kernels)
   fork(h, S);
   for (Shard& s : h->shards) g4_pass(X, s, x, nullptr, false, S.main);
   for (int c = 0; c < 3; ++c) {
