@@ -291,15 +291,21 @@ __device__ __forceinline__ void zmma(double (&cr)[2], double (&ci)[2], cplx a, c
 // y[i1 + n1 c] = sum_a G1[i1 + n1 a] Y2[a + r1 c]: warp task = 8 columns x all i1;
 // Y2 fragments in registers (KT k-steps), G1 fragments from shared memory; each
 // 8 x 8 output tile is stored as 4 whole 128-B lines per warp instruction.
-// KT DMMA k-steps cover k < 4 KT; the REMK <= 2 remaining k = 4 KT .. (r1 = 10, 17, 18 at
-// the measured ranks) run as exact DFMA (shared FP64 pipe: no padding of K to 4 KT + 4)
+// KT DMMA k-steps cover k < 4 KT.  REMK = 1 (r1 = 9, 17): the remaining k = 4 KT runs as exact
+// DFMA.  REMK = 2 (r1 = 10, 18): the two remaining k run as ONE extra k-step per output product
+// pair with real and imaginary parts concatenated along k -- A = [Gr(k0) Gr(k1) Gi(k0) Gi(k1)],
+// Re += A [Yr; Yr; -Yi; -Yi], Im += A [Yi; Yi; Yr; Yr] -- 2 DMMAs instead of the 3 of a padded
+// 3M k-step (8 instead of 9 DMMAs per 8 x 8 tile at r1 = 10; the DMMA sub-pipe is this
+// kernel's limiter, ncu 66% active with math-pipe throttle the top stall)
 template <int KT, int REMK>
 __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant__ ExpandArgs a) {
   const int b = blockIdx.y;
   const int n1 = a.n1, r1 = a.r1[b];
   const int mt = (n1 + 7) / 8;
-  constexpr int KTA = KT > 0 ? KT : 1, RA = REMK > 0 ? REMK : 1;
-  extern __shared__ cplx Af[];   // [mt][KT][32] fragments of G1, then [8 mt][REMK] columns
+  constexpr int KTA = KT > 0 ? KT : 1;
+  // [mt][KT][32] fragments of G1, then (REMK 1) [8 mt] column 4 KT or (REMK 2) [mt][32] the
+  // concatenated k-step's fragments
+  extern __shared__ cplx Af[];
   cplx* Gk = Af + (size_t)mt * KTA * 32;
   const cplx* __restrict__ G1 = a.G1[b];
   // G1 is a constant core: staged before waiting on the producer of Y2 (PDL overlap), all
@@ -321,9 +327,18 @@ __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant_
         if (e0 + q * kG1Threads < tot) Af[e0 + q * kG1Threads] = v[q];
     }
   }
-  for (int e = threadIdx.x; e < 8 * mt * REMK; e += kG1Threads) {
-    const int j = e % RA, i1 = e / RA, k = 4 * KT + j;
-    Gk[e] = (i1 < n1 && k < r1) ? __ldg(G1 + i1 + (int64_t)n1 * k) : cmk(0, 0);
+  if (REMK == 1)
+    for (int e = threadIdx.x; e < 8 * mt; e += kG1Threads) {
+      const int i1 = e, k = 4 * KT;
+      Gk[e] = (i1 < n1 && k < r1) ? __ldg(G1 + i1 + (int64_t)n1 * k) : cmk(0, 0);
+    }
+  if (REMK == 2) {   // concatenated k-step fragments: Gc[m][lane] = (t < 2 ? Gr : Gi)[8 m + g][4 KT + (t & 1)]
+    double* Gc = reinterpret_cast<double*>(Gk);
+    for (int e = threadIdx.x; e < 32 * mt; e += kG1Threads) {
+      const int ln = e % 32, i1 = 8 * (e / 32) + (ln >> 2), k = 4 * KT + (ln & 1);
+      const cplx v = (i1 < n1 && k < r1) ? __ldg(G1 + i1 + (int64_t)n1 * k) : cmk(0, 0);
+      Gc[e] = (ln & 2) ? v.y : v.x;
+    }
   }
   __syncthreads();
   pdl_wait();
@@ -335,8 +350,9 @@ __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant_
   const int64_t ntask = (a.ncol + kColsPerWarp - 1) / kColsPerWarp;
   const int64_t stride = (int64_t)gridDim.x * kWarpsG1;
   int64_t task = (int64_t)blockIdx.x * kWarpsG1 + warp;
-  // DMMA fragments bf[ks] = Y2[4 ks + t][col g]; DFMA values yr[j][jj] = Y2[4 KT + j][col 2 t + jj]
-  auto load_bf = [&](int64_t tk, cplx (&bf)[KTA], cplx (&yr)[RA][2]) {
+  // DMMA fragments bf[ks] = Y2[4 ks + t][col g]; REMK 1: DFMA values yr[jj] = Y2[4 KT][col 2 t + jj];
+  // REMK 2: yr[0] = Y2[4 KT + (t & 1)][col g] (the concatenated k-step's B values)
+  auto load_bf = [&](int64_t tk, cplx (&bf)[KTA], cplx (&yr)[2]) {
     const int64_t c = tk * kColsPerWarp + g;
     const cplx* __restrict__ Y2 = a.Y2[b] + (int64_t)r1 * c;
 #pragma unroll
@@ -344,19 +360,23 @@ __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant_
       const int k = 4 * ks + t;
       bf[ks] = (tk < ntask && c < a.ncol && k < r1) ? __ldg(Y2 + k) : cmk(0, 0);
     }
-#pragma unroll
-    for (int j = 0; j < REMK; ++j)
+    if (REMK == 1) {
 #pragma unroll
       for (int jj = 0; jj < 2; ++jj) {
         const int64_t cc = tk * kColsPerWarp + 2 * t + jj;
-        const int k = 4 * KT + j;
-        yr[j][jj] = (tk < ntask && cc < a.ncol && k < r1) ? __ldg(a.Y2[b] + (int64_t)r1 * cc + k) : cmk(0, 0);
+        const int k = 4 * KT;
+        yr[jj] = (tk < ntask && cc < a.ncol && k < r1) ? __ldg(a.Y2[b] + (int64_t)r1 * cc + k) : cmk(0, 0);
       }
+    }
+    if (REMK == 2) {
+      const int k = 4 * KT + (t & 1);
+      yr[0] = (tk < ntask && c < a.ncol && k < r1) ? __ldg(Y2 + k) : cmk(0, 0);
+    }
   };
-  cplx bf[KTA], yr[RA][2];
+  cplx bf[KTA], yr[2];
   load_bf(task, bf, yr);
   for (; task < ntask; task += stride) {
-    cplx bn[KTA], yn[RA][2];
+    cplx bn[KTA], yn[2];
     load_bf(task + stride, bn, yn);
     const int64_t c0 = task * kColsPerWarp;
     int64_t oaddr[2];
@@ -370,6 +390,8 @@ __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant_
     double bsum[KTA];
 #pragma unroll
     for (int ks = 0; ks < KT; ++ks) bsum[ks] = bf[ks].x + bf[ks].y;
+    // the concatenated k-step's B fragments (REMK 2)
+    const double bre = (t & 2) ? -yr[0].y : yr[0].x, bim = (t & 2) ? yr[0].x : yr[0].y;
     for (int m = 0; m < mt; ++m) {
       // 3 real DMMAs per complex product: P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi)
       double p1[2] = {0, 0}, p2[2] = {0, 0}, p3[2] = {0, 0};
@@ -384,11 +406,21 @@ __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant_
       cplx o[2];
 #pragma unroll
       for (int jj = 0; jj < 2; ++jj) o[jj] = cmk(p1[jj] - p2[jj], p3[jj] - p1[jj] - p2[jj]);
+      if (REMK == 1) {
+        const cplx gv = Gk[i1];
 #pragma unroll
-      for (int j = 0; j < REMK; ++j) {
-        const cplx gv = Gk[i1 * RA + j];
+        for (int jj = 0; jj < 2; ++jj) cfma(o[jj], gv, yr[jj]);
+      }
+      if (REMK == 2) {
+        const double ac = reinterpret_cast<const double*>(Gk)[m * 32 + lane];
+        double er[2] = {0, 0}, ei[2] = {0, 0};
+        dmma(er[0], er[1], ac, bre);
+        dmma(ei[0], ei[1], ac, bim);
 #pragma unroll
-        for (int jj = 0; jj < 2; ++jj) cfma(o[jj], gv, yr[j][jj]);
+        for (int jj = 0; jj < 2; ++jj) {
+          o[jj].x += er[jj];
+          o[jj].y += ei[jj];
+        }
       }
       if (i1 < n1) {
 #pragma unroll
@@ -398,11 +430,8 @@ __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant_
     }
 #pragma unroll
     for (int ks = 0; ks < KT; ++ks) bf[ks] = bn[ks];
-#pragma unroll
-    for (int j = 0; j < REMK; ++j) {
-      yr[j][0] = yn[j][0];
-      yr[j][1] = yn[j][1];
-    }
+    yr[0] = yn[0];
+    yr[1] = yn[1];
   }
   pdl_trigger();
 }
@@ -867,8 +896,9 @@ void launch_expand_g1(const ExpandArgs& a, cudaStream_t st) {
   // instead of 5 padded k-steps, cfg 5 expansion 2.62 -> 2.53 ms per chi); with r1 % 4 == 2
   // (r1 = 10) the padded DMMA step measured faster than two DFMA columns (14.6 vs 15.4 us at
   // cfg 2), so only the remainder 1 takes the DFMA path
+  // r1 % 4 == 2 (r1 = 10, 18): the concatenated real / imaginary k-step (2 DMMAs instead of 3)
   int KT = r1max / 4, REMK = r1max % 4;
-  if (REMK > 1) {
+  if (REMK > 2) {
     KT = (r1max + 3) / 4;
     REMK = 0;
   }
