@@ -334,11 +334,7 @@ __global__ void __launch_bounds__(tc::kThreads) k_zgemm_tc(const __grid_constant
   pdl_trigger();
 }
 
-// Split-K inside a thread-block cluster: the S CTAs of a cluster share one output tile and
-// take K ranges [chunks sp / S, chunks (sp + 1) / S); each leaves its partial tile in its
-// own shared memory, and after a cluster barrier rank sp sums a 1/S slice of the tile over
-// the S peers' shared memory (distributed shared memory, fixed rank order: deterministic)
-// and writes C = alpha sum + beta C.  One launch, no global partials, no reduce kernel.
+// the scalar (DFMA) ZGEMM for the operand combinations the DMMA kernel does not take
 template <int TA, int TB>
 void zgemm_t(const Zgemm& g, int splits, dim3 grid, cplx* ws, int64_t stride, cudaStream_t st) {
   k_zgemm<TA, TB><<<grid, NT, 0, st>>>(g, splits, ws, stride);
