@@ -26,7 +26,6 @@
 #include <cstdlib>
 
 #include "handle.hpp"
-#include "tma_ring.cuh"
 
 namespace vsie {
 
@@ -240,7 +239,7 @@ void fwd_tail(const Ctx& X, Shard& s, int c, cplx* y, cudaStream_t st) {
 }
 
 // W1 = G1^T u, conj(u) for op C
-void adj_g1(const Ctx& X, Shard& s, int c, const cplx* u, bool cj, cudaStream_t st, bool tma = false) {
+void adj_g1(const Ctx& X, Shard& s, int c, const cplx* u, bool cj, cudaStream_t st) {
   vsie_coupling_s* h = X.h;
   const int k = X.k;
   const int n1 = h->grid.n[0], n2 = h->grid.n[1];
@@ -258,7 +257,7 @@ void adj_g1(const Ctx& X, Shard& s, int c, const cplx* u, bool cj, cudaStream_t 
   r.r1[0] = (int)r1;
   Scope sc(h, "adj_g1_reduce", 16 * ((int64_t)n1 * r1 + r1 * n2 * n3l * k + (int64_t)n1 * n2 * n3l * k),
            8 * (int64_t)n1 * r1 * n2 * n3l * k, st);
-  launch_reduce_g1(r, st, tma);
+  launch_reduce_g1(r, st);
 }
 
 // W1 = G1^T u for the three chi of one shard in one launch (single RHS)
@@ -544,28 +543,6 @@ void g2t_pass(const Ctx& X, Shard& s, cudaStream_t st, int chi_only = -1) {
   launch_g2t(g, st);
 }
 
-// L2 prefetch of a core's head while an FP64-bound step leaves the HBM idle (fire and forget)
-__global__ void k_prefetch_l2(const char* p, int64_t bytes, int chunk) {
-  const int64_t o = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * chunk;
-  if (o < bytes) tma::bulk_prefetch_l2(p + o, (uint32_t)std::min<int64_t>(chunk, bytes - o));
-}
-
-// the head of the row-blocked G3 (chi 0 first: every CTA of the G3 pass starts with its chi 0
-// block) up to `budget` bytes, on stream st
-void prefetch_g3_head(const Ctx& X, Shard& s, int64_t budget, cudaStream_t st) {
-  vsie_coupling_s* h = X.h;
-  for (int c = 0; c < 3 && budget > 0; ++c) {
-    const int64_t bytes = std::min<int64_t>(budget, 16LL * X.R(c, 1) * s.n3loc() * X.R(c, 2)) / 16 * 16;
-    if (bytes <= 0) break;
-    const int chunk = 16384;
-    const int64_t nth = (bytes + chunk - 1) / chunk;
-    Scope sc(h, "g3_l2_prefetch", 0, 0, st);
-    k_prefetch_l2<<<(unsigned)((nth + 63) / 64), 64, 0, st>>>(reinterpret_cast<const char*>(s.G3b[c].p), bytes, chunk);
-    VSIE_CHECK_LAUNCH();
-    budget -= bytes;
-  }
-}
-
 bool tma_ok(vsie_coupling_s* h, const Ctx& X) {
   if (X.k != 1 || X.r3m > pair_g4_max_rank()) return false;
   for (Shard& s : h->shards) {
@@ -608,37 +585,15 @@ void fwd_after_y4(const Ctx& X, cplx* y, const Streams& S) {
 // the transpose's front up to W2.  Single RHS: the three chi's G1^T in ONE launch of the
 // TMA-ring kernel (k_reduce_g1_tma: whole-stage bulk copies, consumers only compute; cfg 4
 // 120 us for the three chi vs 151 us for three concurrent k_reduce_g1 chains),
-// then one batched G2^T.  Block RHS: per-chi chains.
+// then one batched G2^T.  Block RHS: per-chi chains.  Measured and rejected
+// (profiles/r02d/ab_last_session.json): per-chi TMA G1^T launches with chi c's G2^T beside
+// chi c + 1's G1^T (cfg 4 0.439 vs 0.433 ms, cfg 2 0.165 vs 0.150), and an L2 prefetch of the
+// head of G3 on a side stream under the FP64-bound G2^T (cfg 4 0.443, cfg 2 0.164-0.168).
 void adj_front_w2(const Ctx& X, const cplx* u, bool cj, const Streams& S) {
   vsie_coupling_s* h = X.h;
-  static const int xchi = getenv("VSIE_X_ADJCHI") ? atoi(getenv("VSIE_X_ADJCHI")) : 0;
-  if (X.k == 1 && xchi) {
-    // experiment: per-chi TMA G1^T launches on the chi streams, chi c's G2^T beside chi c + 1's G1^T
-    fork(h, S);
-    for (int c = 0; c < 3; ++c) {
-      h->scope_chi = c;
-      for (Shard& s : h->shards) {
-        adj_g1(X, s, c, u, cj, S.chi[c], true);
-        if (xchi == 1) g2t_pass(X, s, S.chi[c], c);
-      }
-    }
-    h->scope_chi = -1;
-    join(h, S);
-    if (xchi == 2)
-      for (Shard& s : h->shards) g2t_pass(X, s, S.main);
-    return;
-  }
   if (X.k == 1) {
     // single RHS: the three chi in ONE launch of the TMA-ring G1^T (k_reduce_g1_tma)
     for (Shard& s : h->shards) adj_g1_batched(X, s, u, cj, S.main);
-    static const int pfmb = getenv("VSIE_X_PFG3") ? atoi(getenv("VSIE_X_PFG3")) : 0;
-    if (pfmb > 0 && S.parallel) {
-      fork(h, S);
-      for (Shard& s : h->shards) prefetch_g3_head(X, s, (int64_t)pfmb << 20, S.chi[0]);
-      for (Shard& s : h->shards) g2t_pass(X, s, S.main);
-      join(h, S);
-      return;
-    }
     for (Shard& s : h->shards) g2t_pass(X, s, S.main);
     return;
   }

@@ -296,7 +296,11 @@ __device__ __forceinline__ void zmma(double (&cr)[2], double (&ci)[2], cplx a, c
 // pair with real and imaginary parts concatenated along k -- A = [Gr(k0) Gr(k1) Gi(k0) Gi(k1)],
 // Re += A [Yr; Yr; -Yi; -Yi], Im += A [Yi; Yi; Yr; Yr] -- 2 DMMAs instead of the 3 of a padded
 // 3M k-step (8 instead of 9 DMMAs per 8 x 8 tile at r1 = 10; the DMMA sub-pipe is this
-// kernel's limiter, ncu 66% active with math-pipe throttle the top stall)
+// kernel's limiter, ncu 66% active with math-pipe throttle the top stall).  The ~12 FP64 adds
+// per tile (operand sum, recombination) are NOT the limiter: a chained form with none --
+// k1 = (Ar + Ai) Br, re = k1 - Ai (Br + Bi), im = k1 + Ar (Bi - Br) continuing the k1
+// accumulator, operand sums staged in shared memory -- measured equal (39.3-39.6 us at cfg 4,
+// four variants, profiles/r02d/ab_last_session.json), so the DMMA issue rate itself bounds it
 template <int KT, int REMK>
 __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant__ ExpandArgs a) {
   const int b = blockIdx.y;
