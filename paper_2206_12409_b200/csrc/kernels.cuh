@@ -150,6 +150,7 @@ struct ExpandArgs {
   int r1[3];
   int64_t ncol, cols_per_rhs, ld_rhs;
   int nbatch;
+  int balanced;   // set by the launcher: contiguous (task, i1 tile) unit ranges per warp
 };
 void launch_expand_g1(const ExpandArgs& a, cudaStream_t st);
 

@@ -20,6 +20,7 @@
 #include "tma_ring.cuh"
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <utility>
 #include <vector>
@@ -349,11 +350,18 @@ __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant_
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   cplx* __restrict__ Y = a.y[b];
-  // persistent: warp tasks of 8 columns, the next task's Y2 values loaded before the
-  // current task's DMMAs and stores
+  // persistent: whole 8-column tasks strided over the warps (adjacent warps write adjacent
+  // 25-KB blocks), or -- a.balanced, when the strided rounds would leave > 10% of the kernel
+  // idle (cfg 3: 6000 tasks on 2368 warps = 2.53 rounds, expansion 61 -> 50 us) -- the (task, i1
+  // tile) units split into one contiguous range per warp, equal to within one unit.  The next
+  // task's Y2 values are loaded before the current task's DMMAs and stores
   const int64_t ntask = (a.ncol + kColsPerWarp - 1) / kColsPerWarp;
-  const int64_t stride = (int64_t)gridDim.x * kWarpsG1;
-  int64_t task = (int64_t)blockIdx.x * kWarpsG1 + warp;
+  const int64_t nwarp = (int64_t)gridDim.x * kWarpsG1, wi = (int64_t)blockIdx.x * kWarpsG1 + warp;
+  const bool bal = a.balanced != 0;
+  int64_t u0 = bal ? ntask * mt * wi / nwarp : 0;
+  const int64_t u1 = bal ? ntask * mt * (wi + 1) / nwarp : 0;
+  int64_t task = bal ? u0 / mt : wi;
+  int m0 = bal ? (int)(u0 - task * mt) : 0;
   // DMMA fragments bf[ks] = Y2[4 ks + t][col g]; REMK 1: DFMA values yr[jj] = Y2[4 KT][col 2 t + jj];
   // REMK 2: yr[0] = Y2[4 KT + (t & 1)][col g] (the concatenated k-step's B values)
   auto load_bf = [&](int64_t tk, cplx (&bf)[KTA], cplx (&yr)[2]) {
@@ -378,10 +386,14 @@ __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant_
     }
   };
   cplx bf[KTA], yr[2];
+  if (bal && u0 >= u1) task = ntask;
   load_bf(task, bf, yr);
-  for (; task < ntask; task += stride) {
+  while (task < ntask) {
+    const int m1 = bal ? (int)min((int64_t)mt, m0 + (u1 - u0)) : mt;
+    u0 += m1 - m0;
+    const int64_t next = bal ? (u0 < u1 ? task + 1 : ntask) : task + nwarp;
     cplx bn[KTA], yn[2];
-    load_bf(task + stride, bn, yn);
+    load_bf(next, bn, yn);
     const int64_t c0 = task * kColsPerWarp;
     int64_t oaddr[2];
     bool ok[2];
@@ -396,7 +408,7 @@ __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant_
     for (int ks = 0; ks < KT; ++ks) bsum[ks] = bf[ks].x + bf[ks].y;
     // the concatenated k-step's B fragments (REMK 2)
     const double bre = (t & 2) ? -yr[0].y : yr[0].x, bim = (t & 2) ? yr[0].x : yr[0].y;
-    for (int m = 0; m < mt; ++m) {
+    for (int m = m0; m < m1; ++m) {
       // 3 real DMMAs per complex product: P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi)
       double p1[2] = {0, 0}, p2[2] = {0, 0}, p3[2] = {0, 0};
 #pragma unroll
@@ -436,6 +448,8 @@ __global__ void __launch_bounds__(kG1Threads) k_expand_g1(const __grid_constant_
     for (int ks = 0; ks < KT; ++ks) bf[ks] = bn[ks];
     yr[0] = yn[0];
     yr[1] = yn[1];
+    task = next;
+    m0 = 0;
   }
   pdl_trigger();
 }
@@ -915,7 +929,10 @@ void launch_expand_g1(const ExpandArgs& a, cudaStream_t st) {
     set_smem_attr_once(k_expand_g1<K, R>, d);                                                              \
     dim3 grid((unsigned)std::min<int64_t>(ceil_div(a.ncol, kColsPerCtaG1),                                 \
                                           g1_ctas_per_chi(a.nbatch, (const void*)k_expand_g1<K, R>, smem, kG1Threads)), a.nbatch); \
-    launch_pdl(k_expand_g1<K, R>, grid, dim3(kG1Threads), smem, st, a);                                    \
+    ExpandArgs ab = a;                                                                                     \
+    const double rounds = (double)ceil_div(a.ncol, kColsPerWarp) / ((double)grid.x * kWarpsG1);            \
+    ab.balanced = rounds >= 1.0 && rounds < 0.9 * std::ceil(rounds);                                       \
+    launch_pdl(k_expand_g1<K, R>, grid, dim3(kG1Threads), smem, st, ab);                                   \
     VSIE_CHECK_LAUNCH();                                                                                   \
     return;                                                                                                \
   }
