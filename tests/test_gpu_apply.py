@@ -93,6 +93,24 @@ def test_full_size_probe_ranks(ci):
     _check_all_ops(h, tts, cfg)
 
 
+def test_expansion_balanced_partition_ragged():
+    """The G1 expansion's balanced warp partition (contiguous (task, i1 tile) unit ranges, used
+    when whole-task rounds would leave > 10% of the kernel idle: here 5344 column tasks on at most
+    3552 warps = 1.5 rounds) on a grid with a ragged column tail (42750 = 8 * 5343 + 6) and a
+    ragged i1 tile (n1 = 13), for r1 % 4 = 2, 1 and 0, vs the oracle (T2, 1e-12)."""
+    import dataclasses
+    from paper_2206_12409_b200 import Coupling
+    c1 = synth.get_config(1)
+    n = (13, 150, 285)
+    ext = [c1.n[a] * c1.h[a] for a in range(3)]
+    cfg = dataclasses.replace(c1, n=n, h=tuple(ext[a] / n[a] for a in range(3)))
+    ranks = [(10, 12, 9), (9, 11, 10), (8, 13, 8)]
+    tts = rand_tts(cfg, ranks, 77)
+    h = Coupling.from_cores(grid_of(cfg), cfg.meshes(), cfg.freq, tts, nrhs_max=2)
+    _check_all_ops(h, tts, cfg)
+    _check_all_ops(h, tts, cfg, nrhs=2, seed=3)
+
+
 @pytest.mark.parametrize("world", [2, 3, 5])
 def test_loopback_slabs_equal_single(dense1, cfg1, world):
     """P33 (emulated on one GPU): the i3-slab / G4-column partition with P ranks
