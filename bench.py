@@ -636,6 +636,14 @@ def main():
                 "step_frac_basis": "bytes the step's schedule moves (moved_bytes_per_step) / time / peak",
                 "step_frac_formula": value / peak}
         ai = dom.get("flops_per_launch", 0) / max(1, dom["bytes_per_launch"])
+        if dom.get("flops_per_launch"):
+            # the G1 / G2 steps stream HBM and issue FP64 tensor work from the same warps: report the
+            # FP64 side too (nominal 8 flop per complex multiply-add against the measured DMMA rate;
+            # the 3M form issues 6 of them, plus K padding -- DESIGN.md §7)
+            tf0 = dom["flops_per_launch"] / (avg_ms * 1e-3) / 1e12
+            roof["co_bound"] = {"fp64_tflops": tf0, "fp64_peak_tflops": dmma_peak, "fp64_frac": tf0 / dmma_peak,
+                                "hbm_frac": ach / peak, "flop_per_byte": ai,
+                                "ridge_flop_per_byte": dmma_peak * 1e12 / (peak * 1e9)}
         if k > 1 or ai > dmma_peak * 1e12 / (peak * 1e9):
             # above the FP64 ridge (block RHS, SURVEY §8d AI ~ 15; the G2 contractions, AI ~ 20):
             # a tensor-core bound kernel, against the DMMA rate measured on this pool

@@ -320,18 +320,33 @@ __global__ void __launch_bounds__(kPairThreads, 1) k_pair_g4_band(const __grid_c
         const cplx* col1 = two ? col + R : col;
         const cplx xv0 = FW ? xs[cb + j] : cmk(0, 0), xv1 = FW && two ? xs[cb + j + 1] : cmk(0, 0);
         cplx d0 = cmk(0, 0), d1 = cmk(0, 0);
+        if (two) {
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-          const int r = min(32 * q, last) + lane;   // rows past the band re-read its last row
-          const cplx v0 = col[r], v1 = col1[r];
-          if (TR) {
-            cfma(d0, v0, zv[q]);
-            cfma(d1, v1, zv[q]);
+          for (int q = 0; q < NQ; ++q) {
+            const int r = min(32 * q, last) + lane;   // rows past the band re-read its last row
+            const cplx v0 = col[r], v1 = col1[r];
+            if (TR) {
+              cfma(d0, v0, zv[q]);
+              cfma(d1, v1, zv[q]);
+            }
+            if (FW) {
+              cfma(acc[q], v0, xv0);
+              cfma(acc[q], v1, xv1);
+            }
           }
-          if (FW) {
-            cfma(acc[q], v0, xv0);
-            cfma(acc[q], v1, xv1);
+        } else {   // a lone column (one column per stage at r3 ~ 1500): no duplicate reads
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            const cplx v0 = col[min(32 * q, last) + lane];
+            if (TR) cfma(d0, v0, zv[q]);
+            if (FW) cfma(acc[q], v0, xv0);
           }
+        }
+        // the stage's last column pair is in registers: free the slot before the shuffle
+        // reduction, so the refill does not wait on it (one column per stage at r3 ~ 1500)
+        if (j + 2 >= ncol) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[slot]);
         }
         if (TR) {
           const cplx d = pair_reduce(d0, d1, lane);
@@ -340,8 +355,6 @@ __global__ void __launch_bounds__(kPairThreads, 1) k_pair_g4_band(const __grid_c
           if ((lane & 15) == 0 && (lane == 0 || two)) *zp = b == 0 ? d : cadd(*zp, d);
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
     }
     if (FW) {
 #pragma unroll
