@@ -192,7 +192,9 @@ void launch_g2t_t(const G2tArgs& a, int mmax, cudaStream_t st) {
 // (profiles/r02c/ab_g2t_cluster.json, same box): cfg 2 (378 tiles) G2^T 22.9 -> 18.9 us, pair
 // 0.1536 -> 0.1475-0.149 ms; cfg 4 (756 tiles) S = 2 45.8 vs 43.7 us, 16 x 16 tiles with S = 2
 // / 4 (half the L2 operand traffic at >= as many CTAs) 54 / 48 us -- so the kernel is not bound
-// by its L2 operand traffic; cfg 3 per-chi launches 16 x 16 S = 1 44.5 us vs 50-52 for S = 2 / 4
+// by its L2 operand traffic; cfg 3 per-chi launches 16 x 16 S = 1 44.5 us vs 50-52 for S = 2 / 4;
+// cfg 4 8 x 16 and 16 x 8 tiles without split-K (378 / 420 CTAs, 3/4 of the operand traffic)
+// 46.1-46.4 / 45.8-46.1 vs 44.8 us (profiles/r02f/ab_g2t_tiles.json)
 void launch_g2t(const G2tArgs& a, cudaStream_t st) {
   int mmax = 0;
   for (int b = 0; b < a.nbatch; ++b) mmax = std::max(mmax, a.M[b]);
